@@ -1,0 +1,524 @@
+"""Pins for the CPU oracle: each check compares the oracle with something the paper or
+the mathematics fixes — never with the CUDA path and never by retyping the oracle's own
+formula.  (Runs on CPU: ``-m "not gpu"``.)
+"""
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from workloads import bf16_bits_to_f32, f32_to_bf16_bits
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+LOG2E = 1.4426950408889634
+
+
+def bf16_row(vals):
+    return f32_to_bf16_bits(np.asarray(vals, dtype=np.float32))
+
+
+# ------------------------------------------------------------------ Philox (R6)
+def test_philox_known_answer_vectors(orc):
+    """Random123 KAT vectors (tests/golden/philox4x32_10_kat.txt)."""
+    n = 0
+    for line in open(os.path.join(GOLDEN, "philox4x32_10_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        w = [int(x, 16) for x in line.split()]
+        assert orc.philox4x32_10(w[0:4], w[4:6]) == w[6:10]
+        n += 1
+    assert n == 3
+
+
+def test_uniform_floor_special_cases(orc):
+    """U = floor(r Z / 2^128): SPEC S:88 (u = 0.25 -> first half, 0.75 -> second half)."""
+    assert orc.uniform_floor([0x40000000, 0, 0, 0], 2) == 0          # u = 1/4
+    assert orc.uniform_floor([0xC0000000, 0, 0, 0], 2) == 1          # u = 3/4
+    assert orc.uniform_floor([0xFFFFFFFF] * 4, 1) == 0               # U < Z always
+    assert orc.uniform_floor([0xFFFFFFFF] * 4, 2**64 - 1) == 2**64 - 2
+    assert orc.uniform_floor([0, 0, 0, 0], 2**64 - 1) == 0
+
+
+def test_uniform_floor_is_exact_floor(orc):
+    """The 64-bit-halves evaluation equals the plain bigint definition floor(r*Z/2^128)."""
+    rng = np.random.default_rng(5)
+    for _ in range(2000):
+        r = [int(x) for x in rng.integers(0, 2**32, size=4, dtype=np.uint64)]
+        Z = int(rng.integers(1, 2**63, dtype=np.uint64)) * int(rng.integers(1, 3))
+        Z = min(Z, 2**64 - 1)
+        r128 = (r[0] << 96) | (r[1] << 64) | (r[2] << 32) | r[3]
+        assert orc.uniform_floor(r, Z) == (r128 * Z) >> 128
+
+
+def test_draw_counter_layout(orc):
+    """ctr = (position, purpose, uid_lo, uid_hi), key = (seed_lo, seed_hi) (reading R6)."""
+    seed, uid = 0x1122334455667788, 0x99AABBCCDDEEFF00
+    got = orc.draw_r128(seed, uid, 7, 1)
+    want = orc.philox4x32_10([7, 1, uid & 0xFFFFFFFF, uid >> 32],
+                             [seed & 0xFFFFFFFF, seed >> 32])
+    assert got == want
+
+
+# ------------------------------------------------------------------ exp2_R (R3/R4)
+def test_exp2_poly_relative_error_closed_form(orc):
+    """|p(f)/2^f - 1| <= 2.5e-7 on a dense fp32 grid of [-1/2, 1/2] (closed form 2^f)."""
+    fs = np.float32(np.linspace(-0.5, 0.5, 20001))
+    worst = max(abs(orc.exp2_poly(float(f)) / 2.0 ** float(f) - 1.0) for f in fs)
+    assert worst <= 2.5e-7, worst
+
+
+def test_mass_shift_values(orc):
+    """R4: S = 62 - ceil(log2 V)."""
+    assert orc.mass_shift(151936) == 44
+    assert orc.mass_shift(1024) == 52
+    assert orc.mass_shift(1025) == 51
+    assert orc.mass_shift(4) == 60
+    assert orc.mass_shift(2) == 61
+
+
+def test_mass_of_y_against_exp2(orc):
+    """mass(y)/2^S = 2^y within the polynomial bound plus one fixed-point ulp; special cases."""
+    S = 44
+    rng = np.random.default_rng(1)
+    ys = np.concatenate([np.float32(rng.uniform(-47, 0.5, 3000)),
+                         np.float32([0.0, -0.5, 0.5, -1.5, -2.5, -44.0, -45.9])])
+    for y in ys:
+        m = orc.mass_of_y(float(y), S)
+        exact = 2.0 ** float(y) * 2.0 ** S
+        assert abs(m - exact) <= 2.6e-7 * exact + 1.0, (y, m, exact)
+    # p(0) = C0 = 1 + 2^-23 exactly, so mass(0) = 2^S + 2^(S-23)
+    assert orc.mass_of_y(0.0, S) == 2**S + 2**(S - 23)
+    assert orc.mass_of_y(-1.0, S) == 2**(S - 1) + 2**(S - 24)
+    assert orc.mass_of_y(float("-inf"), S) == 0
+    assert orc.mass_of_y(-(S + 2.5), S) == 0
+    assert orc.mass_of_y(-(S + 1.0), S) == 0  # 2^-(S+1) * 2^S = 1/2 -> floor 0
+
+
+def test_temp_scale(orc):
+    """R2: c = fl32(log2 e / T); T = 1 -> 0x3FB8AA3B."""
+    assert np.float32(orc.temp_scale(1.0)).view(np.uint32) == 0x3FB8AA3B
+    assert orc.temp_scale(float(np.float32(LOG2E))) == 1.0
+
+
+# ------------------------------------------------------------------ row distribution
+def test_row_masses_exact_powers_of_two(orc):
+    """With c = 1 (T = fl32(log2 e)), logits {0,-1,-2,-3} give masses C0 * 2^(S-j)."""
+    T = float(np.float32(LOG2E))
+    V = 4
+    d = orc.row_dist(bf16_row([0.0, -1.0, -2.0, -3.0]), T)
+    S = orc.mass_shift(V)
+    c0 = 2**S + 2**(S - 23)
+    assert [int(x) for x in d.mass] == [c0 >> j for j in range(4)]
+    assert d.z == sum(c0 >> j for j in range(4))
+
+
+def test_row_normaliser_vs_fp64(orc):
+    """Z * 2^-S equals sum_i exp((l_i - m)/T) (libm, fp64) within 1e-6 relative — the
+    north_star's 1e-5 normaliser bar with margin."""
+    rng = np.random.default_rng(2)
+    for V, T in [(1024, 1.0), (1000, 0.7), (4096, 1.3), (151936, 1.0)]:
+        row = bf16_row(rng.normal(0, 2.5, V))
+        d = orc.row_dist(row, T)
+        l = bf16_bits_to_f32(row).astype(np.float64)
+        ref = float(np.sum(np.exp((l - l.max()) / float(np.float32(T)))))
+        S = orc.mass_shift(V)
+        assert abs(d.z_full / 2.0**S / ref - 1) < 1e-6
+        assert abs(d.norm_r / ref - 1) < 1e-6
+        assert abs(d.norm_fp64 / ref - 1) < 1e-12
+
+
+def test_uniform_row_masses_equal(orc):
+    for v in [0.0, 3.5, -17.25]:
+        d = orc.row_dist(bf16_row([v] * 37), 0.9)
+        assert len(set(int(x) for x in d.mass)) == 1
+        assert d.z == 37 * int(d.mass[0])
+
+
+def test_greedy_is_argmax_lowest_id(orc):
+    """R1 / S:74: T = 0 is the degenerate distribution on the argmax, ties -> lowest id."""
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        row = bf16_row(np.round(rng.normal(0, 2, 300)))  # many ties
+        d = orc.row_dist(row, 0.0)
+        g = int(np.argmax(bf16_bits_to_f32(row)))  # numpy: first occurrence
+        assert d.greedy == g and d.z == 1 and int(d.mass[g]) == 1 and int(d.mass.sum()) == 1
+
+
+def test_invalid_rows(orc):
+    """R0: NaN or +inf -> error; all -inf -> error; -inf entries get mass 0."""
+    with pytest.raises(orc.OracleError):
+        orc.row_dist(np.array([0x3F80, 0x7FC0], dtype=np.uint16), 1.0)
+    with pytest.raises(orc.OracleError):
+        orc.row_dist(np.array([0x3F80, 0x7F80], dtype=np.uint16), 1.0)
+    with pytest.raises(orc.OracleError):
+        orc.row_dist(np.array([0xFF80, 0xFF80], dtype=np.uint16), 1.0)
+    d = orc.row_dist(np.array([0x3F80, 0xFF80], dtype=np.uint16), 1.0)
+    assert int(d.mass[1]) == 0 and int(d.mass[0]) > 0
+
+
+# ------------------------------------------------------------------ top-p (R5)
+def test_top_p_spec_example(orc):
+    """(0.5,0.3,0.2), top_p 0.7 -> kept {0,1}, renormalised (0.625, 0.375, 0)."""
+    for k in [0, 10, 40]:
+        m, z = orc.top_p_filter([5 << k, 3 << k, 2 << k], 0.7)
+        assert [Fraction(int(x), z) for x in m] == [Fraction(5, 8), Fraction(3, 8), 0]
+    m, z = orc.top_p_filter([5, 3, 2], 0.5)      # cumulative 0.5 >= 0.5 after {0}
+    assert list(m) == [5, 0, 0] and z == 5
+    m, z = orc.top_p_filter([2, 3, 5], 0.75)     # order is by mass, not by id
+    assert list(m) == [0, 3, 5] and z == 8
+    m, z = orc.top_p_filter([3, 3, 3, 1], 0.5)   # ties broken by lowest id
+    assert list(m) == [3, 3, 0, 0]
+    m, z = orc.top_p_filter([1, 7], 1.0)         # identity
+    assert list(m) == [1, 7] and z == 8
+    m, z = orc.top_p_filter([1, 7], 1e-9)        # never empties the support
+    assert list(m) == [0, 7]
+
+
+def test_top_p_nucleus_properties(orc):
+    """The kept set is the smallest (mass desc, id asc) prefix whose mass reaches
+    top_p * Z (checked with exact fractions), and it grows monotonically with top_p.
+    (SPEC S:97 also claims idempotence; with renormalisation that is false in general,
+    e.g. (0.6, 0.3, 0.1) at top_p 0.65 -> {0.6, 0.3} -> {0.6} — DESIGN.md reading R5.)"""
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        m0 = rng.integers(0, 1000, 20).astype(np.uint64)
+        m0[0] += 1
+        Z = int(m0.sum())
+        order = sorted(range(20), key=lambda i: (-int(m0[i]), i))
+        prev_kept = set()
+        for p in sorted(float(np.float32(x)) for x in rng.uniform(0.01, 1.0, 4)):
+            m1, z1 = orc.top_p_filter(m0, p)
+            kept = [i for i in order if int(m1[i]) > 0 or (int(m0[i]) == 0 and False)]
+            n = len(kept)
+            assert kept == order[:n]                       # a prefix of the order
+            pth = Fraction(p) * Z
+            assert sum(int(m0[i]) for i in order[:n]) >= pth          # reaches top_p
+            assert n == 1 or sum(int(m0[i]) for i in order[:n - 1]) < pth  # smallest
+            assert prev_kept <= set(kept)                  # monotone in top_p
+            prev_kept = set(kept)
+
+
+# ------------------------------------------------------------------ sampling (R8), Eq. 3
+def test_inverse_cdf_spec_example(orc):
+    """(0.5,0.5): u = 0.25 -> 0, u = 0.75 -> 1; S:85 degenerate (0,1,0) -> 1."""
+    mass = [1, 1]
+    assert orc.sample_index(mass, -1, orc.uniform_floor([0x40000000, 0, 0, 0], 2)) == 0
+    assert orc.sample_index(mass, -1, orc.uniform_floor([0xC0000000, 0, 0, 0], 2)) == 1
+    for U in range(1):
+        assert orc.sample_index([0, 1, 0], -1, U) == 1
+
+
+def test_residual_spec_example_exhaustive(orc):
+    """S:232-233 (Eq. 3): (0.5,0.3,0.2) reject 0 -> (0, 0.6, 0.4); (0.5,0.5) reject 1 -> (1,0).
+    Exact: enumerate every U in [0, Z - mass(excl))."""
+    def dist(mass, excl):
+        zx = sum(mass) - mass[excl]
+        cnt = [0] * len(mass)
+        for U in range(zx):
+            cnt[orc.sample_index(mass, excl, U)] += 1
+        return [Fraction(c, zx) for c in cnt]
+
+    assert dist([5, 3, 2], 0) == [0, Fraction(3, 5), Fraction(2, 5)]
+    assert dist([1, 1], 1) == [1, 0]
+
+
+def test_per_token_marginal_identity(orc):
+    """S:267 / P:211: p(d) 1[x=d] + (1 - p(d)) r(x) = p(x), exactly, by enumerating the
+    accept draw and the residual draw on random small integer masses."""
+    rng = np.random.default_rng(6)
+    for _ in range(60):
+        V = int(rng.integers(2, 6))
+        mass = [int(x) for x in rng.integers(0, 7, V)]
+        if sum(mass) == 0:
+            mass[0] = 1
+        Z = sum(mass)
+        for d in range(V):
+            P = [Fraction(0)] * V
+            P[d] += Fraction(mass[d], Z)            # accept region U < mass(d)
+            zx = Z - mass[d]
+            if zx:
+                for U in range(zx):                 # residual draw
+                    P[orc.sample_index(mass, d, U)] += Fraction(Z - mass[d], Z) / zx
+            assert P == [Fraction(m, Z) for m in mass]
+
+
+# ------------------------------------------------------------------ Alg. 1 step
+def onehot_row(V, tok):
+    v = np.full(V, -np.inf, dtype=np.float32)
+    v[tok] = 0.0
+    return bf16_row(v)
+
+
+def test_degenerate_rows_all_accepted(orc):
+    """p_t(d_t) = 1 on every row -> all accepted, q + 1 emitted (bonus)."""
+    V, k = 16, 4
+    draft = [3, 5, 7, 9]
+    rows = [onehot_row(V, t) for t in draft] + [onehot_row(V, 11)]
+    for uid in range(20):
+        out = orc.verify_one(rows, 1.0, 1.0, 9, uid, 0, 100, -1, False, draft, k)
+        assert out.tokens == draft + [11] and out.accepted == 4 and out.rows_used == 5
+
+
+def test_zero_mass_draft_rejected_first(orc):
+    """p(d_1) = 0 -> rejected at 1, emitted token drawn from p_1 itself."""
+    V = 8
+    rng = np.random.default_rng(7)
+    base = rng.normal(0, 1, V).astype(np.float32)
+    base[2] = -np.inf
+    row0 = bf16_row(base)
+    rows = [row0] + [bf16_row(rng.normal(0, 1, V)) for _ in range(3)]
+    for uid in range(50):
+        out = orc.verify_one(rows, 1.0, 1.0, 1, uid, 5, 100, -1, False, [2, 1, 1], 3)
+        assert out.accepted == 0 and len(out.tokens) == 1 and out.tokens[0] != 2
+        assert out.rows_used == 1  # lazy: rows after the first rejection untouched
+
+
+def test_step_token_distribution_chi_square(orc):
+    """First emitted token of a step is distributed as p_0 (P:211 losslessness):
+    chi-square over 20000 uids with a draft token of moderate probability."""
+    from scipy.stats import chisquare
+
+    V = 6
+    rng = np.random.default_rng(8)
+    rows = [bf16_row(rng.normal(0, 1, V)) for _ in range(3)]
+    d0 = orc.row_dist(rows[0], 1.0)
+    p = d0.mass.astype(np.float64) / d0.z
+    n = 20000
+    cnt = np.zeros(V)
+    for uid in range(n):
+        out = orc.verify_one(rows, 1.0, 1.0, 123, uid, 0, 100, -1, False, [1, 2], 2)
+        cnt[out.tokens[0]] += 1
+    assert chisquare(cnt, p * n).pvalue > 1e-3
+
+
+def test_closed_form_acceptance_length(orc):
+    """S:244 / S:594: i.i.d. per-row acceptance probability rho -> E[emitted] =
+    sum_{i=0}^{q} rho^i (geometric truncation), and the accepted-count histogram matches."""
+    V, q = 32, 4
+    vals = np.zeros(V, dtype=np.float32)
+    vals[0] = 2.0
+    row = bf16_row(vals)
+    d = orc.row_dist(row, 1.0)
+    rho = int(d.mass[0]) / d.z
+    rows = [row] * (q + 1)
+    n = 20000
+    emitted = np.zeros(n)
+    acc_hist = np.zeros(q + 1)
+    for uid in range(n):
+        out = orc.verify_one(rows, 1.0, 1.0, 77, uid, 0, 1000, -1, False, [0] * q, q)
+        emitted[uid] = len(out.tokens)
+        acc_hist[out.accepted] += 1
+    expect = sum(rho**i for i in range(q + 1))
+    assert abs(emitted.mean() - expect) / expect < 0.01
+    probs = np.array([rho**a * (1 - rho) for a in range(q)] + [rho**q])
+    sd = np.sqrt(n * probs * (1 - probs))
+    assert np.all(np.abs(acc_hist - n * probs) < 4 * sd + 1)
+
+
+def test_accepted_eos_stops_block(orc):
+    """an accepted EOS ends the block; no bonus token."""
+    V, eos = 8, 7
+    rows = [onehot_row(V, 1), onehot_row(V, eos), onehot_row(V, 2), onehot_row(V, 3)]
+    out = orc.verify_one(rows, 1.0, 1.0, 1, 0, 0, 100, eos, False, [1, eos, 2], 3)
+    assert out.tokens == [1, eos] and out.accepted == 2 and out.rows_used == 2
+
+
+def test_max_len_clamp_and_finished(orc):
+    """Reading L6: q <= max_len - pos - 1; finished or pos >= max_len emits nothing."""
+    V = 8
+    rows = [onehot_row(V, t) for t in [1, 2, 3, 4, 5]]
+    out = orc.verify_one(rows, 1.0, 1.0, 1, 0, 8, 10, -1, False, [1, 2, 3, 4], 4)
+    assert out.tokens == [1, 2] and out.accepted == 1   # q clamped to 1, bonus from row 1
+    out = orc.verify_one(rows, 1.0, 1.0, 1, 0, 10, 10, -1, False, [1, 2], 4)
+    assert out.tokens == []
+    out = orc.verify_one(rows, 1.0, 1.0, 1, 0, 0, 10, -1, True, [1, 2], 4)
+    assert out.tokens == []
+
+
+def test_greedy_accepted_length_is_lcp(orc):
+    """north_star (2): under greedy decoding the accepted length equals the brute-force
+    longest common prefix of the draft and the greedy (argmax) continuation."""
+    rng = np.random.default_rng(9)
+    V, k = 12, 6
+    for trial in range(200):
+        rows = [bf16_row(rng.normal(0, 2, V)) for _ in range(k + 1)]
+        greedy = [int(np.argmax(bf16_bits_to_f32(r))) for r in rows]
+        draft = [g if rng.random() < 0.7 else int(rng.integers(0, V)) for g in greedy[:k]]
+        lcp = 0
+        while lcp < k and draft[lcp] == greedy[lcp]:
+            lcp += 1
+        out = orc.verify_one(rows, 0.0, 1.0, 5, trial, 0, 1000, -1, False, draft, k)
+        assert out.accepted == lcp
+        assert out.tokens == greedy[: lcp + 1]
+
+
+# ------------------------------------------------------------------ full rollouts
+def _markov_setup(V, seed):
+    """Order-1 Markov target over V tokens: row for prev token x is rows[x]."""
+    rng = np.random.default_rng(seed)
+    return [bf16_row(rng.normal(0, 1.0, V)) for _ in range(V)]
+
+
+def _run_spec_rollouts(orc, rows_by_prev, pools, n, L, k, T, eos, prompt_last=0, seed=11):
+    from oracle.rollout import OracleRollout, run_rollouts
+
+    def row_fn(P, positions, prevs):
+        return [rows_by_prev[p] for p in prevs]
+
+    ros = [OracleRollout(prompt=0, uid=u, context=[prompt_last], max_len=L) for u in range(n)]
+    run_rollouts(ros, pools, row_fn, k=k, M=8, Lmin=1, T=T, top_p=1.0, seed=seed, eos=eos)
+    return ros
+
+
+def test_lossless_sequence_distribution_chi_square(orc):
+    """S:591-592 / P:211 'exactly preserves the target rollout distribution': V=4 order-1
+    Markov target, L=5, K=2, a 6-sequence pool.  The empirical distribution of whole
+    speculative rollouts matches the autoregressive product distribution (exact masses)."""
+    from scipy.stats import chisquare
+
+    V, L, k, eos = 4, 5, 2, 3
+    rows = _markov_setup(V, 12)
+    pools = {0: [[0, 1, 2, 1, 0], [1, 2, 1, 2], [2, 2, 0, 1], [0, 0, 1, 2, 3], [1, 1, 1], [2, 0]]}
+    n = 30000
+    ros = _run_spec_rollouts(orc, rows, pools, n, L, k, 1.0, eos)
+    assert sum(len(s[2]) > 0 for r in ros for s in r.steps) > n  # drafts were used
+    probs = {}
+    dists = [orc.row_dist(r, 1.0) for r in rows]
+
+    def expand(prefix, prev, pr):
+        if len(prefix) == L or (prefix and prefix[-1] == eos):
+            probs[tuple(prefix)] = pr
+            return
+        d = dists[prev]
+        for x in range(V):
+            if int(d.mass[x]):
+                expand(prefix + [x], x, pr * Fraction(int(d.mass[x]), d.z))
+
+    expand([], 0, Fraction(1))
+    keys = sorted(probs)
+    idx = {kk: i for i, kk in enumerate(keys)}
+    cnt = np.zeros(len(keys))
+    for r in ros:
+        cnt[idx[tuple(r.generated)]] += 1
+    exp = np.array([float(probs[kk]) for kk in keys]) * n
+    big = exp >= 5
+    obs = np.append(cnt[big], cnt[~big].sum())
+    ex = np.append(exp[big], exp[~big].sum())
+    assert chisquare(obs, ex).pvalue > 1e-3
+
+
+def test_empty_pool_is_plain_decoding(orc):
+    """north_star (3) / S:252: with an empty pool every step is one plain sample drawn
+    with counter (t, SAMPLE); under T = 0 this is the argmax chain (numpy argmax)."""
+    V, L = 6, 12
+    rows = _markov_setup(V, 13)
+    ros = _run_spec_rollouts(orc, rows, {}, 5, L, 3, 0.0, -1)
+    for r in ros:
+        chain, prev = [], 0
+        for _ in range(L):
+            prev = int(np.argmax(bf16_bits_to_f32(rows[prev])))
+            chain.append(prev)
+        assert r.generated == chain and len(r.steps) == L
+    ros = _run_spec_rollouts(orc, rows, {}, 3, L, 3, 1.0, -1, seed=99)
+    for r in ros:
+        prev = 0
+        for t, x in enumerate(r.generated):
+            d = orc.row_dist(rows[prev], 1.0)
+            U = orc.uniform_floor(orc.draw_r128(99, r.uid, t, 1), d.z)
+            c = np.cumsum(d.mass.astype(object))
+            assert x == int(np.argmax(c > U))
+            prev = x
+
+
+# ------------------------------------------------------------------ lookup
+def _trie_lookup(pool, ctx, M, Lmin, K):
+    """Independent route to the lookup definition: count every window of the pool with
+    a Python Counter (a depth-bounded suffix trie), then anchor + greedy descent."""
+    from collections import Counter
+
+    D = M + K + 1
+    cnt, cont = Counter(), Counter()
+    for s in pool:
+        for i in range(len(s)):
+            for l in range(1, min(D, len(s) - i) + 1):
+                w = tuple(s[i:i + l])
+                cnt[w] += 1
+                if i + l < len(s):
+                    cont[w] += 1
+    mstar = 0
+    for m in range(min(M, len(ctx)), Lmin - 1, -1):
+        if cont[tuple(ctx[len(ctx) - m:])] >= 1:
+            mstar = m
+            break
+    if mstar == 0:
+        return [], 0
+    w = list(ctx[len(ctx) - mstar:])
+    out = []
+    for _ in range(K):
+        kids = {w2[-1]: c for w2, c in cnt.items() if len(w2) == len(w) + 1 and list(w2[:-1]) == w}
+        if not kids:
+            break
+        best = min(kids, key=lambda t: (-kids[t], t))
+        out.append(best)
+        w.append(best)
+    return out, mstar
+
+
+def test_lookup_spec_examples(orc):
+    """S:154."""
+    pool = [[1, 2, 3], [1, 2, 3], [1, 2, 5]]
+    d, m = orc.lookup(pool, [9, 1, 2], 8, 1, 4)
+    assert d[0] == 3 and m == 2 and d == [3]
+    d, m = orc.lookup([[7, 8]], [4, 4, 7], 8, 1, 4)
+    assert d == [8] and m == 1
+    d, m = orc.lookup(pool, [9, 9, 9], 8, 1, 4)
+    assert d == [] and m == 0
+    d, m = orc.lookup([], [1, 2], 8, 1, 4)
+    assert d == [] and m == 0
+
+
+def test_lookup_anchor_needs_continuation(orc):
+    """Reading L2: a suffix that occurs only at sequence ends does not anchor; the
+    longest suffix WITH a continuation does."""
+    pool = [[5, 6, 7], [6, 1]]
+    d, m = orc.lookup(pool, [5, 6], 8, 1, 3)
+    assert m == 2 and d == [7]
+    d, m = orc.lookup(pool, [9, 6, 7], 8, 1, 3)   # "6 7" and "7" only at ends
+    assert m == 0 and d == []
+    d, m = orc.lookup([[1, 2], [3, 1, 4]], [3, 9, 3, 1], 8, 1, 3)  # "3 1" has cont via seq 2
+    assert m == 2 and d == [4]
+
+
+def test_lookup_vs_trie_random(orc):
+    """200 random pools x several prefixes, oracle == independent trie lookup."""
+    rng = np.random.default_rng(10)
+    for t in range(200):
+        V = int(rng.integers(2, 6))
+        pool = [list(rng.integers(0, V, int(rng.integers(0, 12)))) for _ in range(int(rng.integers(0, 5)))]
+        pool = [[int(x) for x in s] for s in pool]
+        for _ in range(5):
+            ctx = [int(x) for x in rng.integers(0, V, int(rng.integers(1, 10)))]
+            M = int(rng.integers(1, 6))
+            Lmin = int(rng.integers(1, 3))
+            K = int(rng.integers(0, 5))
+            assert orc.lookup(pool, ctx, M, Lmin, K) == _trie_lookup(pool, ctx, M, Lmin, K)
+
+
+def test_lookup_invariants(orc):
+    """The draft is the continuation of some occurrence of anchor+draft in one sequence;
+    the anchor is maximal (m*+1 has no continuation)."""
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        pool = [[int(x) for x in rng.integers(0, 4, 15)] for _ in range(4)]
+        ctx = [int(x) for x in rng.integers(0, 4, 10)]
+        d, m = orc.lookup(pool, ctx, 6, 1, 5)
+        if m == 0:
+            continue
+        s = ctx[-m:] + d
+        assert any(seq[i:i + len(s)] == s for seq in pool for i in range(len(seq)))
+        if m < 6:
+            w = ctx[-(m + 1):]
+            assert not any(seq[i:i + len(w)] == w and i + len(w) < len(seq)
+                           for seq in pool for i in range(len(seq)))
