@@ -102,11 +102,14 @@ float orc_exp2_poly(float f) {
     return p;
 }
 
-/* R4: S = 62 - ceil(log2 V): every mass < 2^(S+2), so Z = sum < 2^64.          */
+/* R4: S = 62 - ceil(log2 V), rounded down to an even number: every mass is
+ * < 2^(S+2), so Z = sum < 2^64.  (Evenness is part of the definition: it lets a
+ * fast implementation fold S into the round-half-even constant of R3.)          */
 int orc_mass_shift(int V) {
     int lg = 0;
     while (((int64_t)1 << lg) < (int64_t)V) ++lg;
-    return 62 - lg;
+    int S = 62 - lg;
+    return S - (S & 1);
 }
 
 /* R3+R4: mass(y) = floor(2^S * p(f) * 2^n), n = round-half-even(y), f = y - n.

@@ -70,12 +70,13 @@ def test_exp2_poly_relative_error_closed_form(orc):
 
 
 def test_mass_shift_values(orc):
-    """R4: S = 62 - ceil(log2 V)."""
+    """R4: S = 62 - ceil(log2 V), rounded down to even; Z < 2^64 for any row."""
     assert orc.mass_shift(151936) == 44
     assert orc.mass_shift(1024) == 52
-    assert orc.mass_shift(1025) == 51
+    assert orc.mass_shift(1025) == 50
     assert orc.mass_shift(4) == 60
-    assert orc.mass_shift(2) == 61
+    assert orc.mass_shift(2) == 60
+    assert orc.mass_shift(1) == 62
 
 
 def test_mass_of_y_against_exp2(orc):
@@ -127,6 +128,13 @@ def test_row_normaliser_vs_fp64(orc):
         assert abs(d.z_full / 2.0**S / ref - 1) < 1e-6
         assert abs(d.norm_r / ref - 1) < 1e-6
         assert abs(d.norm_fp64 / ref - 1) < 1e-12
+
+
+def test_z_fits_64_bits_worst_case(orc):
+    """R4 bound: a row of V equal maximal logits has Z = V * mass(y~0) < 2^64."""
+    for V in [1, 2, 3, 1000, 1024, 1025, 4096]:
+        d = orc.row_dist(bf16_row([7.0] * V), 1.0)
+        assert 0 < d.z < 2**64 and d.z == V * int(d.mass[0])
 
 
 def test_uniform_row_masses_equal(orc):
