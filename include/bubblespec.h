@@ -1,0 +1,228 @@
+/*
+ * bubblespec.h — C-ABI of the B200-native BubbleSpec hot path (arXiv 2605.08862).
+ *
+ * The calls follow the paper's problem statement, Alg. 1:
+ * inputs are the prompt, the target policy's logits, the suffix index built from
+ * the pre-generated token pools and the maximum length L.  One decoding
+ * step of a batch of rollouts is
+ *
+ *     bs_draft_lookup  ->  [engine forward produces logits rows]  ->  bs_verify_step  ->  bs_commit
+ *
+ * and once per RL step the pools pre-generated in the inter-GPU bubbles
+ * are put, optionally exchanged across DP ranks by prompt id (P:199,
+ * P:346), and sealed (index build).
+ *
+ * Conventions (all functions):
+ *  - Every array argument is a DEVICE pointer owned by the caller, unless stated.
+ *    The library owns pools, the index, per-slot rollout state and scratch.
+ *  - Every call is stream-ordered and asynchronous on `stream` (a cudaStream_t
+ *    passed as void*; NULL = legacy default stream).  One bs_ctx must be driven
+ *    from one stream at a time; a bs_ctx is not thread-safe (one per GPU / rank).
+ *  - Host-side argument validation returns a bs_status synchronously and never
+ *    throws; bs_last_error() gives the text.  Device-side anomalies (NaN / +inf
+ *    logits, an all -inf row, |max logit / T| too large, draft id outside [0, V),
+ *    index key collision) set a sticky device error word that bs_sync_status()
+ *    reports and clears.
+ *  - Randomness: the only random numbers are Philox4x32-10 draws with
+ *    key = config.seed and counter = (position, purpose, uid_lo, uid_hi), where
+ *    position = generated-token index, purpose 0 = ACCEPT, 1 = SAMPLE, and uid
+ *    is the rollout's global id (reading R6).  Results are therefore
+ *    independent of batching, slot assignment and DP sharding.
+ *  - Arithmetic: decisions are made in the reference arithmetic R of DESIGN.md §3
+ *    (integer masses, exact sums), so outputs are bit-identical to the CPU oracle.
+ */
+#ifndef BUBBLESPEC_H_
+#define BUBBLESPEC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bs_ctx bs_ctx;
+
+typedef enum {
+    BS_OK = 0,
+    BS_ERR_INVALID = 1,   /* bad argument (host-side check)                       */
+    BS_ERR_OOM = 2,       /* device allocation failed                             */
+    BS_ERR_CUDA = 3,      /* a CUDA runtime call failed (no GPU, launch error ...) */
+    BS_ERR_STALE = 4,     /* lookup against a pool sealed for another rl_step     */
+    BS_ERR_CAPACITY = 5,  /* pool / slot capacity exceeded                        */
+    BS_ERR_NCCL = 6,      /* NCCL unavailable or a collective failed              */
+    BS_ERR_DEVICE = 7     /* device error word set (see bs_sync_status)           */
+} bs_status;
+
+/* Device error word bits (bs_sync_status). */
+#define BS_DEV_BAD_LOGIT   0x1u  /* NaN or +inf logit in a verified row (reading R0)   */
+#define BS_DEV_ALL_NEGINF  0x2u  /* a verified row is all -inf (reading R0)            */
+#define BS_DEV_RANGE       0x4u  /* |fl(m * log2e/T)| >= 2^24 (reading R0)              */
+#define BS_DEV_BAD_DRAFT   0x8u  /* draft token outside [0, V)                          */
+#define BS_DEV_INDEX_KEY   0x10u /* 64-bit key collision between two index windows      */
+
+typedef struct {
+    int32_t vocab;                /* V >= 1: logits row length                          */
+    int32_t eos_id;               /* EOS token id, or -1 for none (Alg. 1) */
+    int32_t k_max;                /* max draft block length K, 1..31 (P:299 uses 4)    */
+    int32_t match_max;            /* M, max anchor length, 1..32 (reading L1)          */
+    int32_t match_min;            /* L_min >= 1, min anchor length              */
+    int32_t max_rollouts;         /* number of rollout slots                            */
+    int64_t pool_capacity_tokens; /* pool token capacity per RL step                    */
+    int32_t pool_capacity_seqs;   /* pool sequence capacity per RL step                 */
+    int32_t device;               /* CUDA device ordinal                                */
+    uint64_t seed;                /* Philox key (reading R6)                            */
+} bs_config;
+
+typedef struct {
+    float temperature; /* T >= 0; T == 0 is greedy (argmax, lowest id)          */
+    float top_p;       /* (0, 1]; nucleus over integer masses (reading R5)     */
+} bs_sampling;
+
+/* ---------------------------------------------------------------- lifetime */
+/* Allocate a context on config->device.  Returns BS_ERR_INVALID for an invalid
+ * config, BS_ERR_CUDA if no device, BS_ERR_OOM on allocation failure. */
+bs_status bs_create(const bs_config* config, bs_ctx** out);
+void bs_destroy(bs_ctx* ctx);
+/* Text of the last host-side error of this ctx (or of the last bs_create if ctx is NULL). */
+const char* bs_last_error(const bs_ctx* ctx);
+/* Synchronise `stream`, read and clear the device error word.  Writes the word to
+ * *word (may be NULL); returns BS_ERR_DEVICE if it was non-zero. */
+bs_status bs_sync_status(bs_ctx* ctx, void* stream, uint32_t* word);
+/* Library version string. */
+const char* bs_version(void);
+
+/* ---------------------------------------------------------------- rollouts */
+/* Start n rollouts (Alg. 1 line 1: y <- x_{1:m}).
+ *   slots[n]        slot index in [0, max_rollouts)
+ *   uids[n]         globally unique rollout id (Philox counter words 2-3)
+ *   prompt_ids[n]   prompt id; selects the pool used by lookup
+ *   prompt_tail[n*M] the last M prompt tokens, right-aligned, -1 = padding on the left;
+ *                   at least one valid token per rollout
+ *   max_len[n]      L: maximum number of generated tokens (Alg. 1 "while |y| < L")
+ * Resets pos = 0, finished = 0. */
+bs_status bs_rollout_begin(bs_ctx* ctx, int32_t n, const int32_t* slots, const uint64_t* uids,
+                           const int32_t* prompt_ids, const int32_t* prompt_tail,
+                           const int32_t* max_len, void* stream);
+
+/* Read per-slot state (device outputs, any may be NULL): pos[n], finished[n]. */
+bs_status bs_rollout_state(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* pos,
+                           int32_t* finished, void* stream);
+
+/* Bind (or unbind with NULL) a caller-owned device buffer [max_rollouts, stride]:
+ * bs_commit then also writes every emitted token of slot s at responses[s*stride + t]
+ * (t = generated-token index, t < stride), i.e. the rollout y of Alg. 1. */
+bs_status bs_rollout_bind_output(bs_ctx* ctx, int32_t* responses, int64_t stride);
+
+/* Copy the first n (<= 41) device statistics counters to HOST memory out[n] and
+ * optionally reset them.  Counters (SPEC S:478-484 accounting): 0 verification steps
+ * (q >= 1), 1 plain steps (q = 0), 2 tokens emitted by verification steps, 3 tokens
+ * emitted by plain steps, 4 accepted drafts, 5 proposed drafts, 6 logits rows read by
+ * the verify kernel, 7 rows Alg. 1 needs (up to the first rejection / EOS),
+ * 8 + e (e = 0..32) verification steps that emitted e tokens.  Synchronises `stream`. */
+bs_status bs_stats_read(bs_ctx* ctx, uint64_t* out, int32_t n, int32_t reset, void* stream);
+
+/* ---------------------------------------------------------------- pools (per RL step) */
+/* Append n_seqs pre-generated sequences to the pool being assembled for rl_step
+ * ("prompt-associated token pools").  If rl_step differs from
+ * the step being assembled, the staging pool is cleared first.
+ *   prompt_ids[n_seqs]      owning prompt of each sequence
+ *   seq_offsets[n_seqs+1]   offsets into tokens (offsets[0] may be non-zero)
+ *   tokens[...]             token ids in [0, V)
+ *   n_tokens                host copy of seq_offsets[n_seqs] - seq_offsets[0]
+ * Returns BS_ERR_CAPACITY if the pool capacity would be exceeded. */
+bs_status bs_draft_pool_put(bs_ctx* ctx, uint64_t rl_step, int32_t n_seqs,
+                            const int32_t* prompt_ids, const int64_t* seq_offsets,
+                            const int32_t* tokens, int64_t n_tokens, void* stream);
+
+/* Build the draft index over the assembled pool for rl_step (the
+ * suffix index of §3.2 bounded to depth M+K).  Synchronises
+ * `stream` internally (per RL step, off the decode path).  Lookups against
+ * another rl_step then return BS_ERR_STALE. */
+bs_status bs_draft_pool_seal(bs_ctx* ctx, uint64_t rl_step, void* stream);
+
+/* Cross-rank draft exchange: all-gather the staging pools of all
+ * ranks of `nccl_comm` (an ncclComm_t of world size R, this rank = rank) and keep
+ * only sequences whose prompt_id % R == rank.  Replaces the staging pool with the
+ * routed one; call bs_draft_pool_seal afterwards.  Returns BS_ERR_NCCL if NCCL
+ * cannot be loaded.  Synchronises `stream`. */
+bs_status bs_draft_exchange(bs_ctx* ctx, void* nccl_comm, int32_t rank, int32_t world,
+                            uint64_t rl_step, void* stream);
+/* Host-only routing plan used by bs_draft_exchange (no GPU needed).  Given the
+ * all-gathered per-rank metadata — counts[2*world] = (n_seqs_r, n_tokens_r),
+ * offs_all[world*(max_seqs+1)] (rank r's offsets, relative to its token segment, at
+ * r*(max_seqs+1)) and prompts_all[world*max_seqs] — list, in (rank, seq) order, the
+ * sequences this rank owns (prompt % world == rank): source position in the gathered
+ * token buffer (r*max_tokens + offset), destination offset, length, prompt id.
+ * Output arrays hold >= sum_r n_seqs_r entries (host memory).  Returns 0, or 1 on
+ * inconsistent input. */
+int bs_route_plan(int32_t world, int32_t rank, const int64_t* counts, const int64_t* offs_all,
+                  const int32_t* prompts_all, int64_t max_seqs, int64_t max_tokens,
+                  int64_t* plan_src, int64_t* plan_dst, int64_t* plan_len, int32_t* plan_prompt,
+                  int32_t* nkeep, int64_t* ntok);
+/* Helper: ncclGetUniqueId into a 128-byte host buffer (for bootstrapping a comm). */
+bs_status bs_nccl_unique_id(void* id128);
+/* Helper: ncclCommInitRank from a 128-byte unique id; *comm_out receives the ncclComm_t. */
+bs_status bs_nccl_comm_init(void** comm_out, const void* id128, int32_t world, int32_t rank);
+bs_status bs_nccl_comm_destroy(void* comm);
+
+/* ---------------------------------------------------------------- per decoding step */
+/* Draft lookup (Alg. 1 line 3: "Retrieve a draft block from T using prefix y"):
+ * anchor on the longest suffix (<= M) of each rollout's context that occurs in
+ * its prompt's pool with a continuation, then descend greedily by occurrence
+ * count (ties -> lowest id) for up to k tokens (readings L1-L6).
+ *   slots[n]; outputs draft_tokens[n*k] (row b holds draft_len[b] tokens, rest -1),
+ *   draft_len[n] (clamped to max_len - pos - 1, 0 if finished),
+ *   match_len[n] (anchor length m*, 0 if none; may be NULL).
+ * BS_ERR_STALE if the index is not sealed for rl_step; k in [0, k_max]. */
+bs_status bs_draft_lookup(bs_ctx* ctx, uint64_t rl_step, int32_t n, const int32_t* slots,
+                          int32_t k, int32_t* draft_tokens, int32_t* draft_len,
+                          int32_t* match_len, void* stream);
+
+/* Lossless verification of one draft block per rollout (Eq. 2 P:203-205,
+ * Eq. 3, Alg. 1, bonus P:308).  Pure: reads rollout state,
+ * writes only its outputs.
+ *   logits_bf16  bf16 logits rows of length V, row stride row_stride_elems (>= V)
+ *   row_index    [n*(k+1)] int64 row numbers into logits_bf16, or NULL for the dense
+ *                layout [n, k+1, V] (row b*(k+1)+j).  Row j of rollout b is the
+ *                target distribution for generated-token index pos_b + j, i.e.
+ *                after prefix y_b + d_1..d_j.  Rows j > draft_len[b] are not read.
+ *   draft_tokens [n*k], draft_len[n] (values are clamped to [0, min(k, max_len-pos-1)])
+ *   sampling     temperature / top-p of p_t
+ * Outputs: out_tokens[n*(k+1)] emitted tokens (accepted drafts, then the recovered
+ *   or bonus token unless an accepted EOS ended the block), out_len[n],
+ *   out_accepted[n] accepted draft count, and (may be NULL) out_norm[n*(k+1)] the
+ *   softmax normaliser sum_i exp((l_i - max)/T) of each verified row (fp32 from the
+ *   exact integer sum) and out_z[n*(k+1)] the exact integer normaliser Z' of R.
+ *   Entries of rows that were not needed are 0. */
+bs_status bs_verify_step(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits_bf16,
+                         const int64_t* row_index, int64_t row_stride_elems,
+                         const int32_t* draft_tokens, const int32_t* draft_len, int32_t k,
+                         bs_sampling sampling, int32_t* out_tokens, int32_t* out_len,
+                         int32_t* out_accepted, float* out_norm, uint64_t* out_z,
+                         void* stream);
+
+/* Commit (Alg. 1 lines 15/22 "y <- y o a"): append out_len[b] tokens of row b of
+ * out_tokens [n*(k+1)] to each rollout, advance its position, and mark it
+ * finished on an emitted EOS or when pos reaches max_len (Alg. 1 line 2).
+ * finished[n] (may be NULL) receives the finished flags. */
+bs_status bs_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* out_tokens,
+                    const int32_t* out_len, int32_t k, int32_t* finished, void* stream);
+
+/* ---------------------------------------------------------------- synthetic workload */
+/* Not part of the method: device twins of workloads/synth.py so a
+ * multi-GB logit bank need not be generated on the host.  Bit-identical to numpy. */
+/* bank[rows, V] bf16: Irwin-Hall(4 hashed bytes) * 2^-6, + beta at the peak column. */
+bs_status bsx_synth_bank(void* bank_bf16, int64_t rows, int32_t V, uint32_t bank_seed,
+                         float beta, void* stream);
+/* Synthetic target "forward": row_index[b*(k+1)+j] = target_row(prompt, pos+j, prev_j)
+ * for j <= draft_len[b] (prev_0 = last context token, prev_j = draft[j-1]).
+ * mode: 0 position, 1 markov, 2 mixed (workloads.TargetSpec). */
+bs_status bsx_target_rows(bs_ctx* ctx, int32_t n, const int32_t* slots,
+                          const int32_t* draft_tokens, const int32_t* draft_len, int32_t k,
+                          uint32_t target_seed, int32_t mode, int64_t nbank,
+                          int64_t* row_index, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BUBBLESPEC_H_ */

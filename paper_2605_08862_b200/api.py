@@ -1,0 +1,188 @@
+"""Thin Python binding of the C-ABI (include/bubblespec.h): argument marshalling only.
+
+Every function has the name of the C call it wraps and passes torch CUDA tensors as raw
+device pointers; every step of the hot path runs in libbubblespec.so's kernels.  PyTorch
+provides device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import BubbleSpecError, bs_config, bs_sampling, load
+
+_V = C.c_void_p
+
+
+def _p(t):
+    """Device pointer of a tensor (or None)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return _V(t.data_ptr())
+
+
+def _stream(stream, device):
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return _V(s.cuda_stream)
+
+
+def _chk(ctx, st, where):
+    if st != 0:
+        msg = load().bs_last_error(ctx.handle if ctx is not None else None)
+        raise BubbleSpecError(st, where, msg.decode() if msg else "")
+
+
+class Context:
+    """Owns a bs_ctx (pools, index, rollout slots, scratch) on one GPU."""
+
+    def __init__(self, vocab: int, eos_id: int = -1, k_max: int = 8, match_max: int = 32,
+                 match_min: int = 1, max_rollouts: int = 256, pool_capacity_tokens: int = 1 << 20,
+                 pool_capacity_seqs: int = 1 << 14, device: int | None = None, seed: int = 0):
+        lib = load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device
+        self.vocab, self.eos_id, self.k_max, self.M = vocab, eos_id, k_max, match_max
+        self.match_min, self.max_rollouts, self.seed = match_min, max_rollouts, seed
+        cfg = bs_config(vocab, eos_id, k_max, match_max, match_min, max_rollouts,
+                        pool_capacity_tokens, pool_capacity_seqs, device, seed)
+        h = _V()
+        st = lib.bs_create(C.byref(cfg), C.byref(h))
+        if st != 0:
+            raise BubbleSpecError(st, "bs_create", (lib.bs_last_error(None) or b"").decode())
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            load().bs_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ C calls
+    def bs_sync_status(self, stream=None) -> int:
+        w = C.c_uint32(0)
+        st = load().bs_sync_status(self.handle, _stream(stream, self.device), C.byref(w))
+        if st not in (0, 7):
+            _chk(self, st, "bs_sync_status")
+        return int(w.value)
+
+    def bs_rollout_begin(self, slots, uids, prompt_ids, prompt_tail, max_len, stream=None):
+        n = slots.numel()
+        _chk(self, load().bs_rollout_begin(self.handle, n, _p(slots), _p(uids), _p(prompt_ids),
+                                           _p(prompt_tail), _p(max_len),
+                                           _stream(stream, self.device)), "bs_rollout_begin")
+
+    def bs_rollout_state(self, slots, pos=None, finished=None, stream=None):
+        _chk(self, load().bs_rollout_state(self.handle, slots.numel(), _p(slots), _p(pos),
+                                           _p(finished), _stream(stream, self.device)),
+             "bs_rollout_state")
+
+    def bs_draft_pool_put(self, rl_step, prompt_ids, seq_offsets, tokens, n_tokens: int,
+                          stream=None):
+        _chk(self, load().bs_draft_pool_put(self.handle, rl_step, prompt_ids.numel(),
+                                            _p(prompt_ids), _p(seq_offsets), _p(tokens),
+                                            n_tokens, _stream(stream, self.device)),
+             "bs_draft_pool_put")
+
+    def bs_draft_pool_seal(self, rl_step, stream=None):
+        _chk(self, load().bs_draft_pool_seal(self.handle, rl_step, _stream(stream, self.device)),
+             "bs_draft_pool_seal")
+
+    def bs_draft_exchange(self, comm, rank: int, world: int, rl_step, stream=None):
+        _chk(self, load().bs_draft_exchange(self.handle, comm, rank, world, rl_step,
+                                            _stream(stream, self.device)), "bs_draft_exchange")
+
+    def bs_draft_lookup(self, rl_step, slots, k, draft_tokens, draft_len, match_len=None,
+                        stream=None):
+        _chk(self, load().bs_draft_lookup(self.handle, rl_step, slots.numel(), _p(slots), k,
+                                          _p(draft_tokens), _p(draft_len), _p(match_len),
+                                          _stream(stream, self.device)), "bs_draft_lookup")
+
+    def bs_verify_step(self, slots, logits, row_index, row_stride, draft_tokens, draft_len, k,
+                       temperature, top_p, out_tokens, out_len, out_accepted, out_norm=None,
+                       out_z=None, stream=None):
+        sp = bs_sampling(temperature, top_p)
+        _chk(self, load().bs_verify_step(self.handle, slots.numel(), _p(slots), _p(logits),
+                                         _p(row_index), row_stride, _p(draft_tokens),
+                                         _p(draft_len), k, sp, _p(out_tokens), _p(out_len),
+                                         _p(out_accepted), _p(out_norm), _p(out_z),
+                                         _stream(stream, self.device)), "bs_verify_step")
+
+    def bs_commit(self, slots, out_tokens, out_len, k, finished=None, stream=None):
+        _chk(self, load().bs_commit(self.handle, slots.numel(), _p(slots), _p(out_tokens),
+                                    _p(out_len), k, _p(finished), _stream(stream, self.device)),
+             "bs_commit")
+
+    def bs_stats_read(self, reset: bool = False, stream=None):
+        import numpy as np
+
+        out = np.zeros(41, dtype=np.uint64)
+        _chk(self, load().bs_stats_read(self.handle, _V(out.ctypes.data), 41, int(reset),
+                                        _stream(stream, self.device)), "bs_stats_read")
+        return out
+
+    def bs_rollout_bind_output(self, responses=None, stride: int = 0):
+        _chk(self, load().bs_rollout_bind_output(self.handle, _p(responses),
+                                                 stride if responses is not None else 0),
+             "bs_rollout_bind_output")
+
+    def bsx_target_rows(self, slots, draft_tokens, draft_len, k, target_seed, mode, nbank,
+                        row_index, stream=None):
+        _chk(self, load().bsx_target_rows(self.handle, slots.numel(), _p(slots), _p(draft_tokens),
+                                          _p(draft_len), k, target_seed, mode, nbank,
+                                          _p(row_index), _stream(stream, self.device)),
+             "bsx_target_rows")
+
+
+def bsx_synth_bank(bank, rows: int, V: int, bank_seed: int, beta: float, stream=None):
+    st = load().bsx_synth_bank(_p(bank), rows, V, bank_seed & 0xFFFFFFFF, beta,
+                               _stream(stream, bank.device))
+    _chk(None, st, "bsx_synth_bank")
+
+
+def bs_route_plan(world, rank, counts, offs_all, prompts_all, max_seqs, max_tokens):
+    """Host routing plan (numpy in/out); see include/bubblespec.h."""
+    import numpy as np
+
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    offs_all = np.ascontiguousarray(offs_all, dtype=np.int64)
+    prompts_all = np.ascontiguousarray(prompts_all, dtype=np.int32)
+    tot = int(counts[0::2].sum()) + 1
+    src, dst, ln = (np.zeros(tot, np.int64) for _ in range(3))
+    pr = np.zeros(tot, np.int32)
+    nk, nt = C.c_int32(), C.c_int64()
+    pp = lambda a: _V(a.ctypes.data)  # noqa: E731
+    rc = load().bs_route_plan(world, rank, pp(counts), pp(offs_all), pp(prompts_all), max_seqs,
+                              max_tokens, pp(src), pp(dst), pp(ln), pp(pr), C.byref(nk),
+                              C.byref(nt))
+    if rc != 0:
+        raise ValueError("inconsistent routing metadata")
+    k = nk.value
+    return src[:k], dst[:k], ln[:k], pr[:k], int(nt.value)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _chk(None, load().bs_nccl_unique_id(buf), "bs_nccl_unique_id")
+    return buf.raw
+
+
+def nccl_comm_init(uid: bytes, world: int, rank: int):
+    comm = _V()
+    buf = C.create_string_buffer(uid, 128)
+    _chk(None, load().bs_nccl_comm_init(C.byref(comm), buf, world, rank), "bs_nccl_comm_init")
+    return comm
+
+
+def nccl_comm_destroy(comm):
+    _chk(None, load().bs_nccl_comm_destroy(comm), "bs_nccl_comm_destroy")

@@ -1,0 +1,314 @@
+// api.cu — the C-ABI of include/bubblespec.h: argument validation, context lifetime,
+// and dispatch to the kernels.  No torch types anywhere in this library.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "ctx.h"
+
+using namespace bs;
+
+static thread_local std::string g_create_err;
+
+static bs_status fail(bs_ctx* ctx, bs_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    else g_create_err = buf;
+    return s;
+}
+
+static bs_status cuda_fail(bs_ctx* ctx, cudaError_t e, const char* where) {
+    cudaGetLastError();  // clear sticky-less errors
+    return fail(ctx, e == cudaErrorMemoryAllocation ? BS_ERR_OOM : BS_ERR_CUDA, "%s: %s", where,
+                cudaGetErrorString(e));
+}
+
+#define CK(ctx, x, where)                                  \
+    do {                                                   \
+        cudaError_t e_ = (x);                              \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, where); \
+    } while (0)
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char* bs_version(void) { return "bubblespec-b200 0.1 (sm_100a)"; }
+
+const char* bs_last_error(const bs_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
+    if (!cfg || !out) return fail(nullptr, BS_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (cfg->vocab < 1) return fail(nullptr, BS_ERR_INVALID, "vocab must be >= 1");
+    if (cfg->k_max < 1 || cfg->k_max > 31) return fail(nullptr, BS_ERR_INVALID, "k_max must be in [1, 31]");
+    if (cfg->match_max < 1 || cfg->match_max > 32)
+        return fail(nullptr, BS_ERR_INVALID, "match_max must be in [1, 32]");
+    if (cfg->match_min < 1) return fail(nullptr, BS_ERR_INVALID, "match_min must be >= 1");
+    if (cfg->max_rollouts < 1) return fail(nullptr, BS_ERR_INVALID, "max_rollouts must be >= 1");
+    if (cfg->pool_capacity_tokens < 0 || cfg->pool_capacity_seqs < 0)
+        return fail(nullptr, BS_ERR_INVALID, "negative pool capacity");
+    if (cfg->eos_id >= cfg->vocab) return fail(nullptr, BS_ERR_INVALID, "eos_id >= vocab");
+    if ((int64_t)((cfg->vocab + 7) / 8) * 2 * 8 > (int64_t)8 * 76 * 1024 * 2)
+        return fail(nullptr, BS_ERR_INVALID, "vocab too large for an 8-CTA cluster row");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, BS_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, BS_ERR_INVALID, "bad device ordinal");
+    e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+    bs_ctx* c = new bs_ctx();
+    c->cfg = *cfg;
+    c->S = mass_shift(cfg->vocab);
+    c->M = cfg->match_max;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    const size_t R = (size_t)cfg->max_rollouts;
+    const size_t rows = R * (size_t)(cfg->k_max + 1);
+    bool okk = c->tail.ensure(R * c->M) == cudaSuccess && c->ctx_len.ensure(R) == cudaSuccess &&
+               c->pos.ensure(R) == cudaSuccess && c->max_len.ensure(R) == cudaSuccess &&
+               c->prompt.ensure(R) == cudaSuccess && c->finished.ensure(R) == cudaSuccess &&
+               c->uid.ensure(R) == cudaSuccess && c->dev_err.ensure(1) == cudaSuccess &&
+               c->rowres.ensure(rows) == cudaSuccess && c->row_b.ensure(rows) == cudaSuccess &&
+               c->row_j.ensure(rows) == cudaSuccess && c->rb_base.ensure(R) == cudaSuccess &&
+               c->rb_q.ensure(R) == cudaSuccess && c->done_ctr.ensure(R) == cudaSuccess &&
+               c->total_rows.ensure(1) == cudaSuccess &&
+               c->staging.tokens.ensure((size_t)cfg->pool_capacity_tokens) == cudaSuccess &&
+               c->staging.seq_off.ensure((size_t)cfg->pool_capacity_seqs + 1) == cudaSuccess &&
+               c->staging.seq_prompt.ensure((size_t)cfg->pool_capacity_seqs) == cudaSuccess &&
+               c->sealed.tokens.ensure((size_t)cfg->pool_capacity_tokens) == cudaSuccess &&
+               c->sealed.seq_off.ensure((size_t)cfg->pool_capacity_seqs + 1) == cudaSuccess &&
+               c->sealed.seq_prompt.ensure((size_t)cfg->pool_capacity_seqs) == cudaSuccess &&
+               c->table.ensure(2) == cudaSuccess && c->stats.ensure(STAT_COUNT) == cudaSuccess;
+    if (!okk) {
+        bs_destroy(c);
+        cudaGetLastError();
+        return fail(nullptr, BS_ERR_OOM, "device allocation failed");
+    }
+    cudaMemset(c->tail.p, 0xFF, R * c->M * sizeof(int32_t));
+    cudaMemset(c->ctx_len.p, 0, R * sizeof(int32_t));
+    cudaMemset(c->pos.p, 0, R * sizeof(int32_t));
+    cudaMemset(c->max_len.p, 0, R * sizeof(int32_t));
+    cudaMemset(c->prompt.p, 0, R * sizeof(int32_t));
+    cudaMemset(c->uid.p, 0, R * sizeof(unsigned long long));
+    // unused slots are finished (no rows, no drafts)
+    cudaMemset(c->finished.p, 0, R * sizeof(int32_t));
+    cudaMemset(c->dev_err.p, 0, sizeof(uint32_t));
+    cudaMemset(c->done_ctr.p, 0, R * sizeof(int32_t));
+    cudaMemset(c->stats.p, 0, STAT_COUNT * sizeof(unsigned long long));
+    cudaMemset(c->table.p, 0, 2 * sizeof(IndexEntry));
+    cudaMemset(c->staging.seq_off.p, 0, sizeof(int64_t));
+    cudaMemset(c->sealed.seq_off.p, 0, sizeof(int64_t));
+    c->table_mask = 1;
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        bs_destroy(c);
+        return cuda_fail(nullptr, e, "bs_create");
+    }
+    *out = c;
+    return BS_OK;
+}
+
+void bs_destroy(bs_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->cfg.device);
+    c->tail.release(); c->ctx_len.release(); c->pos.release(); c->max_len.release();
+    c->prompt.release(); c->finished.release(); c->uid.release(); c->dev_err.release();
+    c->staging.tokens.release(); c->staging.seq_off.release(); c->staging.seq_prompt.release();
+    c->sealed.tokens.release(); c->sealed.seq_off.release(); c->sealed.seq_prompt.release();
+    c->seq_start_of.release(); c->seq_end_of.release(); c->prompt_of.release();
+    c->table.release(); c->rowres.release(); c->row_b.release(); c->row_j.release();
+    c->rb_base.release(); c->rb_q.release(); c->done_ctr.release(); c->total_rows.release();
+    c->stats.release();
+    delete c;
+}
+
+bs_status bs_sync_status(bs_ctx* c, void* stream, uint32_t* word) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    uint32_t w = 0;
+    CK(c, cudaMemcpyAsync(&w, c->dev_err.p, sizeof w, cudaMemcpyDeviceToHost, S(stream)), "read error word");
+    CK(c, cudaMemsetAsync(c->dev_err.p, 0, sizeof(uint32_t), S(stream)), "clear error word");
+    CK(c, cudaStreamSynchronize(S(stream)), "bs_sync_status");
+    if (word) *word = w;
+    if (w) return fail(c, BS_ERR_DEVICE, "device error word 0x%x", w);
+    return BS_OK;
+}
+
+bs_status bs_rollout_begin(bs_ctx* c, int32_t n, const int32_t* slots, const uint64_t* uids,
+                           const int32_t* prompt_ids, const int32_t* prompt_tail,
+                           const int32_t* max_len, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
+    if (n && (!slots || !uids || !prompt_ids || !prompt_tail || !max_len))
+        return fail(c, BS_ERR_INVALID, "null array");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_begin(c, n, slots, reinterpret_cast<const unsigned long long*>(uids), prompt_ids,
+                       prompt_tail, max_len, S(stream)),
+       "bs_rollout_begin");
+    return BS_OK;
+}
+
+bs_status bs_rollout_state(bs_ctx* c, int32_t n, const int32_t* slots, int32_t* pos,
+                           int32_t* finished, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_state(c, n, slots, pos, finished, S(stream)), "bs_rollout_state");
+    return BS_OK;
+}
+
+bs_status bs_draft_pool_put(bs_ctx* c, uint64_t rl_step, int32_t n_seqs, const int32_t* prompt_ids,
+                            const int64_t* seq_offsets, const int32_t* tokens, int64_t n_tokens,
+                            void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (n_seqs < 0 || n_tokens < 0) return fail(c, BS_ERR_INVALID, "negative size");
+    if (n_seqs && (!prompt_ids || !seq_offsets)) return fail(c, BS_ERR_INVALID, "null array");
+    if (n_tokens && !tokens) return fail(c, BS_ERR_INVALID, "null tokens");
+    Pool& P = c->staging;
+    if (!P.valid || P.step != rl_step) {
+        P.valid = true;
+        P.step = rl_step;
+        P.n_tokens = 0;
+        P.n_seqs = 0;
+    }
+    if (P.n_tokens + n_tokens > c->cfg.pool_capacity_tokens ||
+        (int64_t)P.n_seqs + n_seqs > c->cfg.pool_capacity_seqs)
+        return fail(c, BS_ERR_CAPACITY, "pool capacity exceeded (%lld tokens, %d seqs)",
+                    (long long)(P.n_tokens + n_tokens), P.n_seqs + n_seqs);
+    if (n_seqs == 0) return BS_OK;
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_pool_append(c, n_seqs, prompt_ids, seq_offsets, tokens, n_tokens, S(stream)),
+       "bs_draft_pool_put");
+    P.n_tokens += n_tokens;
+    P.n_seqs += n_seqs;
+    return BS_OK;
+}
+
+bs_status bs_draft_pool_seal(bs_ctx* c, uint64_t rl_step, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    Pool& P = c->staging;
+    if (!P.valid || P.step != rl_step) {  // nothing put for this step: an empty pool
+        P.valid = true;
+        P.step = rl_step;
+        P.n_tokens = 0;
+        P.n_seqs = 0;
+        CK(c, cudaMemsetAsync(P.seq_off.p, 0, sizeof(int64_t), S(stream)), "seal");
+    }
+    std::swap(c->staging, c->sealed);
+    c->staging.valid = false;
+    c->sealed.valid = false;
+    std::string why;
+    cudaError_t e = seal_index(c, S(stream), why);
+    if (e != cudaSuccess) {
+        if (!why.empty()) return fail(c, BS_ERR_CAPACITY, "seal: %s", why.c_str());
+        return cuda_fail(c, e, "bs_draft_pool_seal");
+    }
+    c->sealed.valid = true;
+    c->sealed.step = rl_step;
+    return BS_OK;
+}
+
+bs_status bs_draft_lookup(bs_ctx* c, uint64_t rl_step, int32_t n, const int32_t* slots, int32_t k,
+                          int32_t* draft_tokens, int32_t* draft_len, int32_t* match_len,
+                          void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (!c->sealed.valid || c->sealed.step != rl_step)
+        return fail(c, BS_ERR_STALE, "index not sealed for rl_step %llu", (unsigned long long)rl_step);
+    if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
+    if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
+    if (n && (!slots || !draft_len || (k && !draft_tokens))) return fail(c, BS_ERR_INVALID, "null array");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_lookup(c, n, slots, k, draft_tokens, draft_len, match_len, S(stream)),
+       "bs_draft_lookup");
+    return BS_OK;
+}
+
+bs_status bs_verify_step(bs_ctx* c, int32_t n, const int32_t* slots, const void* logits,
+                         const int64_t* row_index, int64_t stride, const int32_t* draft_tokens,
+                         const int32_t* draft_len, int32_t k, bs_sampling sp,
+                         int32_t* out_tokens, int32_t* out_len, int32_t* out_accepted,
+                         float* out_norm, uint64_t* out_z, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
+    if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
+    if (stride < c->cfg.vocab) return fail(c, BS_ERR_INVALID, "row stride < vocab");
+    if (!(sp.temperature >= 0.f) || sp.temperature == INFINITY)
+        return fail(c, BS_ERR_INVALID, "temperature must be finite and >= 0");
+    if (!(sp.top_p > 0.f && sp.top_p <= 1.f)) return fail(c, BS_ERR_INVALID, "top_p must be in (0, 1]");
+    if (sp.temperature > 0.f && !((float)(1.4426950408889634 / (double)sp.temperature) < INFINITY))
+        return fail(c, BS_ERR_INVALID, "temperature too small");
+    if (sp.top_p < 1.f && sp.temperature > 0.f)
+        return fail(c, BS_ERR_INVALID, "top_p < 1 is not implemented yet");
+    if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
+              (k && !draft_tokens)))
+        return fail(c, BS_ERR_INVALID, "null array");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
+                        sp.temperature, sp.top_p, out_tokens, out_len, out_accepted, out_norm,
+                        reinterpret_cast<unsigned long long*>(out_z), S(stream)),
+       "bs_verify_step");
+    return BS_OK;
+}
+
+bs_status bs_commit(bs_ctx* c, int32_t n, const int32_t* slots, const int32_t* out_tokens,
+                    const int32_t* out_len, int32_t k, int32_t* finished, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
+    if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
+    if (n && (!slots || !out_tokens || !out_len)) return fail(c, BS_ERR_INVALID, "null array");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_commit(c, n, slots, out_tokens, out_len, k, finished, S(stream)), "bs_commit");
+    return BS_OK;
+}
+
+bs_status bs_stats_read(bs_ctx* c, uint64_t* out, int32_t n, int32_t reset, void* stream) {
+    if (!c || (n && !out) || n < 0) return fail(c, BS_ERR_INVALID, "bad arguments");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const int m = n < (int)STAT_COUNT ? n : (int)STAT_COUNT;
+    if (m) CK(c, cudaMemcpyAsync(out, c->stats.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, S(stream)), "stats");
+    if (reset) CK(c, cudaMemsetAsync(c->stats.p, 0, STAT_COUNT * sizeof(uint64_t), S(stream)), "stats");
+    CK(c, cudaStreamSynchronize(S(stream)), "stats");
+    return BS_OK;
+}
+
+bs_status bs_rollout_bind_output(bs_ctx* c, int32_t* responses, int64_t stride) {
+    if (!c || stride < 0 || (responses && stride == 0)) return fail(c, BS_ERR_INVALID, "bad arguments");
+    c->responses = responses;
+    c->resp_stride = responses ? stride : 0;
+    return BS_OK;
+}
+
+bs_status bsx_synth_bank(void* bank, int64_t rows, int32_t V, uint32_t seed, float beta,
+                         void* stream) {
+    if (!bank || rows < 0 || V < 1) return fail(nullptr, BS_ERR_INVALID, "bad bank arguments");
+    cudaError_t e = launch_synth_bank(bank, rows, V, seed, beta, S(stream));
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "bsx_synth_bank");
+    return BS_OK;
+}
+
+bs_status bsx_target_rows(bs_ctx* c, int32_t n, const int32_t* slots, const int32_t* draft,
+                          const int32_t* draft_len, int32_t k, uint32_t tseed, int32_t mode,
+                          int64_t nbank, int64_t* row_index, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (n < 0 || n > c->cfg.max_rollouts || k < 0 || k > c->cfg.k_max || nbank < 1 || mode < 0 ||
+        mode > 2)
+        return fail(c, BS_ERR_INVALID, "bad target arguments");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_target_rows(c, n, slots, draft, draft_len, k, tseed, mode, nbank, row_index,
+                             S(stream)),
+       "bsx_target_rows");
+    return BS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// ctx.h — internal context of libbubblespec (host side).  Not part of the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/bubblespec.h"
+#include "common.cuh"
+
+namespace bs {
+
+// Device statistics counters (bs_stats_read): decoding-step accounting of SPEC S:478-484.
+enum : int {
+    STAT_STEPS_SPEC = 0,     // verification steps (q >= 1)
+    STAT_STEPS_PLAIN = 1,    // plain decoding steps (empty draft, Alg. 1 lines 4-7)
+    STAT_EMIT_SPEC = 2,      // tokens emitted by verification steps
+    STAT_EMIT_PLAIN = 3,     // tokens emitted by plain steps
+    STAT_ACCEPTED = 4,       // accepted draft tokens
+    STAT_PROPOSED = 5,       // proposed draft tokens
+    STAT_ROWS_VERIFIED = 6,  // logits rows streamed by the verify kernel
+    STAT_ROWS_NEEDED = 7,    // rows Alg. 1 needs (up to the first rejection / EOS)
+    STAT_HIST = 8,           // emitted-per-verification-step histogram, bins 0..32
+    STAT_HIST_BINS = 33,
+    STAT_COUNT = STAT_HIST + STAT_HIST_BINS
+};
+
+// Per-row verification result (one per verified logits row).
+struct RowRes {
+    unsigned long long z;  // Z' (exact integer normaliser after top-p)
+    float norm;            // Z_full * 2^-S as fp32
+    int32_t accept;        // row j < q: d_{j+1} accepted
+    int32_t cand;          // residual (j < q) or bonus (j == q) candidate token
+    int32_t pad;
+};
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= n && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        size_t alloc = want ? want : 1;
+        cudaError_t e = cudaMalloc(&p, alloc * sizeof(T));
+        if (e == cudaSuccess) n = alloc;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct Pool {
+    DevBuf<int32_t> tokens;
+    DevBuf<int64_t> seq_off;  // absolute offsets into tokens, n_seqs + 1
+    DevBuf<int32_t> seq_prompt;
+    int64_t n_tokens = 0;
+    int32_t n_seqs = 0;
+    uint64_t step = 0;
+    bool valid = false;
+};
+
+}  // namespace bs
+
+struct bs_ctx {
+    bs_config cfg;
+    int S = 0;  // mass shift (reading R4)
+    int M = 0;  // match_max
+    std::string err;
+    int num_sms = 148;
+    // rollout slots
+    bs::DevBuf<int32_t> tail;  // [R, M] right-aligned context tail
+    bs::DevBuf<int32_t> ctx_len, pos, max_len, prompt, finished;
+    bs::DevBuf<unsigned long long> uid;
+    bs::DevBuf<uint32_t> dev_err;
+    // pools: staging (being assembled) and sealed (indexed)
+    bs::Pool staging, sealed;
+    bs::DevBuf<int32_t> seq_start_of, seq_end_of, prompt_of;  // per sealed pool token
+    bs::DevBuf<bs::IndexEntry> table;
+    uint64_t table_mask = 0;
+    // verify scratch
+    bs::DevBuf<bs::RowRes> rowres;
+    bs::DevBuf<int32_t> row_b, row_j, rb_base, rb_q, done_ctr, total_rows;
+    bs::DevBuf<unsigned long long> stats;  // STAT_COUNT counters
+    int32_t* responses = nullptr;           // optional [max_rollouts, resp_stride] output
+    int64_t resp_stride = 0;
+};
+
+namespace bs {
+// launchers implemented in the .cu files
+cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits,
+                          const int64_t* row_index, int64_t stride, const int32_t* draft,
+                          const int32_t* draft_len, int32_t k, float T, float top_p,
+                          int32_t* out_tokens, int32_t* out_len, int32_t* out_acc,
+                          float* out_norm, unsigned long long* out_z, cudaStream_t st);
+cudaError_t launch_lookup(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k,
+                          int32_t* draft, int32_t* draft_len, int32_t* match_len,
+                          cudaStream_t st);
+cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why);
+cudaError_t launch_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* out_tokens,
+                          const int32_t* out_len, int32_t k, int32_t* finished, cudaStream_t st);
+cudaError_t launch_begin(bs_ctx* ctx, int32_t n, const int32_t* slots,
+                         const unsigned long long* uids, const int32_t* prompt_ids,
+                         const int32_t* tail, const int32_t* max_len, cudaStream_t st);
+cudaError_t launch_state(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* pos,
+                         int32_t* finished, cudaStream_t st);
+cudaError_t launch_pool_append(bs_ctx* ctx, int32_t n_seqs, const int32_t* prompt_ids,
+                               const int64_t* seq_offsets, const int32_t* tokens,
+                               int64_t n_tokens, cudaStream_t st);
+cudaError_t launch_synth_bank(void* bank, int64_t rows, int32_t V, uint32_t seed, float beta,
+                              cudaStream_t st);
+cudaError_t launch_target_rows(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* draft,
+                               const int32_t* draft_len, int32_t k, uint32_t tseed, int32_t mode,
+                               int64_t nbank, int64_t* row_index, cudaStream_t st);
+}  // namespace bs

@@ -1,0 +1,501 @@
+// index.cu — draft pool index build (K2, per RL step) and batched lookup (K1, per step).
+//
+// Lookup semantics (readings L1-L6):
+//   anchor m* = longest suffix (<= M) of the rollout context that occurs in the prompt's
+//   pool followed by a token; draft = greedy descent by occurrence count (ties -> lowest
+//   id) for up to K tokens.
+//
+// Build (exact, no hashing): level l = 1..M+K sorts the active window occurrences by
+// (run id of the length-(l-1) prefix, last token) with a device radix sort, so runs at
+// level l are exactly the distinct windows of length l.  Unique windows drop out (their
+// extensions are unique).  A descending pass computes, per distinct non-unique window,
+// the end point of its greedy path (best child = largest child run, lowest token on ties;
+// a unique child continues as plain text).  Windows of length <= M are inserted into a
+// hashed table keyed (prompt, length, polynomial hash): every non-unique window, plus the
+// FIRST unique window at each end position (its left extensions share its one occurrence
+// and thus its draft).  The set of stored suffix lengths of any context is then contiguous,
+// so lookup is one round of parallel probes (one lane per length) + one pool read.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.h"
+
+namespace bs {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint64_t hash_window(const int32_t* T, int64_t start, int len) {
+    uint64_t H = 0;
+    for (int t = 0; t < len; ++t) H = H * HASH_B + (uint64_t)(uint32_t)(T[start + t] + 1);
+    return H;
+}
+
+__device__ void table_insert(IndexEntry* table, uint64_t mask, uint64_t key, uint32_t occ,
+                             uint32_t meta, uint32_t* dev_err) {
+    uint64_t s = key & mask;
+    for (;;) {
+        unsigned long long prev = atomicCAS(&table[s].key, 0ull, (unsigned long long)key);
+        if (prev == 0ull) {
+            table[s].occ = occ;
+            table[s].meta = meta;
+            return;
+        }
+        if (prev == key) {  // two distinct windows with one 64-bit key
+            atomicOr(dev_err, DEV_INDEX_KEY);
+            return;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+__global__ void seq_meta_kernel(const int64_t* seq_off, const int32_t* seq_prompt, int n_seqs,
+                                int32_t* seq_start_of, int32_t* seq_end_of, int32_t* prompt_of) {
+    for (int s = blockIdx.x; s < n_seqs; s += gridDim.x) {
+        const int64_t a = seq_off[s], b = seq_off[s + 1];
+        const int32_t P = seq_prompt[s];
+        for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+            seq_start_of[i] = (int32_t)a;
+            seq_end_of[i] = (int32_t)b;
+            prompt_of[i] = P;
+        }
+    }
+}
+
+__global__ void iota_kernel(int32_t* a, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+__global__ void fill_kernel(int32_t* a, int n, int32_t v) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = v;
+}
+
+__global__ void level_keys_kernel(int l, int A, int VB, const int32_t* act, const int32_t* T,
+                                  const int32_t* prompt_of, const int32_t* runid_pos,
+                                  unsigned long long* keys) {
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < A; a += gridDim.x * blockDim.x) {
+        const int i = act[a];
+        const uint64_t hi = (l == 1) ? (uint64_t)(uint32_t)prompt_of[i] : (uint64_t)(uint32_t)runid_pos[i];
+        keys[a] = (hi << VB) | (uint64_t)(uint32_t)T[i + l - 1];
+    }
+}
+
+__global__ void run_flags_kernel(int A, const unsigned long long* keys, int32_t* flag) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < A; r += gridDim.x * blockDim.x)
+        flag[r] = (r == 0 || keys[r] != keys[r - 1]) ? 1 : 0;
+}
+
+__global__ void run_starts_kernel(int l, int A, int VB, const unsigned long long* keys,
+                                  const int32_t* flag, const int32_t* runid_incl, int32_t* runstart,
+                                  int32_t* parent) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < A; r += gridDim.x * blockDim.x) {
+        if (flag[r]) {
+            const int R = runid_incl[r] - 1;
+            runstart[R] = r;
+            parent[R] = (l == 1) ? -1 : (int32_t)(keys[r] >> VB);
+        }
+        if (r == A - 1) runstart[runid_incl[r]] = A;
+    }
+}
+
+// per sorted element: record run id per position, first-unique level, next-level activity
+__global__ void run_members_kernel(int l, int A, const int32_t* pos_sorted, const int32_t* runid_incl,
+                                   const int32_t* runstart, const int32_t* seq_end_of,
+                                   int32_t* runid_pos, int32_t* fu, int32_t* next_flag) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < A; r += gridDim.x * blockDim.x) {
+        const int R = runid_incl[r] - 1;
+        const int size = runstart[R + 1] - runstart[R];
+        const int i = pos_sorted[r];
+        runid_pos[i] = R;
+        if (size == 1) {
+            fu[i] = l;
+            next_flag[r] = 0;
+        } else {
+            next_flag[r] = (i + l < seq_end_of[i]) ? 1 : 0;
+        }
+    }
+}
+
+struct Level {
+    int A = 0, nruns = 0;
+    int32_t* pos_sorted = nullptr;  // [A]
+    int32_t* runstart = nullptr;    // [nruns + 1]
+    int32_t* parent = nullptr;      // [nruns]
+};
+
+__global__ void child_ranges_kernel(int nruns_child, const int32_t* parent, int32_t* cbeg,
+                                    int32_t* cend) {
+    for (int C = blockIdx.x * blockDim.x + threadIdx.x; C < nruns_child; C += gridDim.x * blockDim.x) {
+        const int p = parent[C];
+        if (C == 0 || parent[C - 1] != p) cbeg[p] = C;
+        if (C == nruns_child - 1 || parent[C + 1] != p) cend[p] = C + 1;
+    }
+}
+
+// Descending pass at level l: greedy path end points for non-unique runs, table inserts
+// for l <= M (non-unique windows, and first-unique windows).
+__global__ void level_paths_kernel(int l, int M, int K, int top, Level lv, Level ch,
+                                   const int32_t* cbeg, const int32_t* cend, const int32_t* pq_child,
+                                   const int32_t* po_child, int32_t* pq, int32_t* po,
+                                   const int32_t* T, const int32_t* seq_end_of,
+                                   const int32_t* prompt_of, const int32_t* fu, IndexEntry* table,
+                                   uint64_t mask, uint32_t* dev_err) {
+    for (int R = blockIdx.x * blockDim.x + threadIdx.x; R < lv.nruns; R += gridDim.x * blockDim.x) {
+        const int rs = lv.runstart[R];
+        const int size = lv.runstart[R + 1] - rs;
+        const int i0 = lv.pos_sorted[rs];
+        if (size == 1) {
+            // first unique window at its end position?  (l == 1, or (i0+1, l-1) non-unique)
+            if (l <= M && (l == 1 || fu[i0 + 1] >= l)) {
+                const int q = min(K, seq_end_of[i0] - (i0 + l));
+                const uint32_t meta = (uint32_t)q | META_UNIQUE | (q > 0 ? META_CONT : 0u);
+                table_insert(table, mask, window_key(hash_window(T, i0, l), prompt_of[i0], l),
+                             (uint32_t)i0, meta, dev_err);
+            }
+            continue;
+        }
+        int q = 0, occ = i0;
+        if (!top) {
+            const int c0 = cbeg[R], c1 = cend[R];
+            int best = -1, bsz = 0;
+            for (int C = c0; C < c1; ++C) {  // children ordered by next token ascending
+                const int sz = ch.runstart[C + 1] - ch.runstart[C];
+                if (sz > bsz) {
+                    bsz = sz;
+                    best = C;
+                }
+            }
+            if (best >= 0) {
+                const int cpos = ch.pos_sorted[ch.runstart[best]];
+                if (bsz == 1) {
+                    occ = cpos;
+                    q = min(K, seq_end_of[cpos] - cpos - l);
+                } else {
+                    q = min(K, 1 + pq_child[best]);
+                    occ = po_child[best];
+                }
+            }
+        }
+        pq[R] = q;
+        po[R] = occ;
+        if (l <= M) {
+            const uint32_t meta = (uint32_t)q | (q > 0 ? META_CONT : 0u);
+            table_insert(table, mask, window_key(hash_window(T, occ, l), prompt_of[occ], l),
+                         (uint32_t)occ, meta, dev_err);
+        }
+    }
+}
+
+static int bits_for(uint64_t v) {
+    int b = 0;
+    while (b < 64 && (v >> b) != 0) ++b;
+    return b;
+}
+
+#define BS_TRY(x)                       \
+    do {                                \
+        cudaError_t e__ = (x);          \
+        if (e__ != cudaSuccess) return e__; \
+    } while (0)
+
+cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
+    const int64_t N = ctx->sealed.n_tokens;
+    const int M = ctx->M, K = ctx->cfg.k_max, D = M + K;
+    const int V = ctx->cfg.vocab;
+    const int VB = std::max(1, bits_for((uint64_t)V));
+    if (N >= (int64_t)0x7FFFFFFF) {
+        why = "pool too large for 32-bit positions";
+        return cudaErrorInvalidValue;
+    }
+    const int n = (int)N;
+    BS_TRY(ctx->seq_start_of.ensure(n));
+    BS_TRY(ctx->seq_end_of.ensure(n));
+    BS_TRY(ctx->prompt_of.ensure(n));
+    if (ctx->sealed.n_seqs > 0 && n > 0)
+        seq_meta_kernel<<<std::min(ctx->sealed.n_seqs, 4096), 256, 0, st>>>(
+            ctx->sealed.seq_off.p, ctx->sealed.seq_prompt.p, ctx->sealed.n_seqs, ctx->seq_start_of.p,
+            ctx->seq_end_of.p, ctx->prompt_of.p);
+    if (n == 0) {
+        BS_TRY(ctx->table.ensure(2));
+        BS_TRY(cudaMemsetAsync(ctx->table.p, 0, 2 * sizeof(IndexEntry), st));
+        ctx->table_mask = 1;
+        return cudaStreamSynchronize(st);
+    }
+    const int* T = ctx->sealed.tokens.p;
+    // scratch
+    DevBuf<int32_t> act, act_next, flag, runid, runid_pos, fu, nflag;
+    DevBuf<unsigned long long> keys, keys_sorted;
+    DevBuf<int> d_count;
+    BS_TRY(act.ensure(n));
+    BS_TRY(act_next.ensure(n));
+    BS_TRY(flag.ensure(n));
+    BS_TRY(runid.ensure(n));
+    BS_TRY(runid_pos.ensure(n));
+    BS_TRY(fu.ensure(n));
+    BS_TRY(nflag.ensure(n));
+    BS_TRY(keys.ensure(n));
+    BS_TRY(keys_sorted.ensure(n));
+    BS_TRY(d_count.ensure(1));
+    size_t tmp_bytes = 0, t1 = 0, t2 = 0, t3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, keys.p, keys_sorted.p, act.p, act_next.p, n, 0, 64, st);
+    cub::DeviceScan::InclusiveSum(nullptr, t2, flag.p, runid.p, n, st);
+    cub::DeviceSelect::Flagged(nullptr, t3, act.p, nflag.p, act_next.p, d_count.p, n, st);
+    tmp_bytes = std::max(t1, std::max(t2, t3));
+    DevBuf<uint8_t> tmp;
+    BS_TRY(tmp.ensure(tmp_bytes));
+    const int G = std::max(1, std::min(ctx->num_sms * 8, (n + 255) / 256));
+    iota_kernel<<<G, 256, 0, st>>>(act.p, n);
+    fill_kernel<<<G, 256, 0, st>>>(fu.p, n, 0x7FFFFFFF);
+
+    std::vector<Level> levels;
+    int A = n;
+    uint64_t hi_max = 0;  // max of the high key part (prompt id or previous run count)
+    {
+        // prompt ids are int32: use the full 32 bits at level 1
+        hi_max = 0xFFFFFFFFull;
+    }
+    for (int l = 1; l <= D && A > 0; ++l) {
+        Level lv;
+        lv.A = A;
+        BS_TRY(cudaMalloc(&lv.pos_sorted, sizeof(int32_t) * (size_t)A));
+        const int g = std::max(1, std::min(ctx->num_sms * 8, (A + 255) / 256));
+        level_keys_kernel<<<g, 256, 0, st>>>(l, A, VB, act.p, T, ctx->prompt_of.p, runid_pos.p, keys.p);
+        const int end_bit = std::min(64, VB + bits_for(hi_max));
+        size_t tb = tmp_bytes;
+        BS_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys_sorted.p, act.p, lv.pos_sorted, A, 0,
+                                               end_bit, st));
+        run_flags_kernel<<<g, 256, 0, st>>>(A, keys_sorted.p, flag.p);
+        tb = tmp_bytes;
+        BS_TRY(cub::DeviceScan::InclusiveSum(tmp.p, tb, flag.p, runid.p, A, st));
+        int nr = 0;
+        BS_TRY(cudaMemcpyAsync(&nr, runid.p + (A - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+        BS_TRY(cudaStreamSynchronize(st));
+        lv.nruns = nr;
+        BS_TRY(cudaMalloc(&lv.runstart, sizeof(int32_t) * (size_t)(nr + 1)));
+        BS_TRY(cudaMalloc(&lv.parent, sizeof(int32_t) * (size_t)std::max(nr, 1)));
+        run_starts_kernel<<<g, 256, 0, st>>>(l, A, VB, keys_sorted.p, flag.p, runid.p, lv.runstart, lv.parent);
+        run_members_kernel<<<g, 256, 0, st>>>(l, A, lv.pos_sorted, runid.p, lv.runstart, ctx->seq_end_of.p,
+                                              runid_pos.p, fu.p, nflag.p);
+        tb = tmp_bytes;
+        BS_TRY(cub::DeviceSelect::Flagged(tmp.p, tb, lv.pos_sorted, nflag.p, act.p, d_count.p, A, st));
+        int an = 0;
+        BS_TRY(cudaMemcpyAsync(&an, d_count.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        BS_TRY(cudaStreamSynchronize(st));
+        levels.push_back(lv);
+        A = an;
+        hi_max = (uint64_t)nr;
+    }
+    // table capacity: <= one entry per run at levels <= M
+    int64_t cap_need = 0;
+    for (size_t li = 0; li < levels.size() && (int)li < M; ++li) cap_need += levels[li].nruns;
+    uint64_t cap = 2;
+    while (cap < (uint64_t)(2 * cap_need + 2)) cap <<= 1;
+    BS_TRY(ctx->table.ensure(cap));
+    BS_TRY(cudaMemsetAsync(ctx->table.p, 0, cap * sizeof(IndexEntry), st));
+    ctx->table_mask = cap - 1;
+    // descending pass
+    int maxr = 1;
+    for (auto& lv : levels) maxr = std::max(maxr, lv.nruns);
+    DevBuf<int32_t> pqa, poa, pqb, pob, cbeg, cend;
+    BS_TRY(pqa.ensure(maxr));
+    BS_TRY(poa.ensure(maxr));
+    BS_TRY(pqb.ensure(maxr));
+    BS_TRY(pob.ensure(maxr));
+    BS_TRY(cbeg.ensure(maxr));
+    BS_TRY(cend.ensure(maxr));
+    int32_t *pq_child = pqb.p, *po_child = pob.p, *pq = pqa.p, *po = poa.p;
+    const int L = (int)levels.size();
+    for (int li = L - 1; li >= 0; --li) {
+        const int l = li + 1;
+        Level lv = levels[li];
+        Level ch;
+        const int top = (li == L - 1) ? 1 : 0;
+        if (!top) {
+            ch = levels[li + 1];
+            BS_TRY(cudaMemsetAsync(cbeg.p, 0, sizeof(int32_t) * (size_t)lv.nruns, st));
+            BS_TRY(cudaMemsetAsync(cend.p, 0, sizeof(int32_t) * (size_t)lv.nruns, st));
+            const int gc = std::max(1, std::min(ctx->num_sms * 8, (ch.nruns + 255) / 256));
+            if (ch.nruns > 0) child_ranges_kernel<<<gc, 256, 0, st>>>(ch.nruns, ch.parent, cbeg.p, cend.p);
+        }
+        const int gr = std::max(1, std::min(ctx->num_sms * 8, (lv.nruns + 255) / 256));
+        level_paths_kernel<<<gr, 256, 0, st>>>(l, M, K, top, lv, ch, cbeg.p, cend.p, pq_child, po_child, pq, po,
+                                               T, ctx->seq_end_of.p, ctx->prompt_of.p, fu.p, ctx->table.p,
+                                               ctx->table_mask, ctx->dev_err.p);
+        BS_TRY(cudaGetLastError());
+        std::swap(pq, pq_child);
+        std::swap(po, po_child);
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    for (auto& lv : levels) {
+        cudaFree(lv.pos_sorted);
+        cudaFree(lv.runstart);
+        cudaFree(lv.parent);
+    }
+    act.release(); act_next.release(); flag.release(); runid.release(); runid_pos.release();
+    fu.release(); nflag.release(); keys.release(); keys_sorted.release(); d_count.release();
+    tmp.release(); pqa.release(); poa.release(); pqb.release(); pob.release(); cbeg.release();
+    cend.release();
+    return e;
+}
+
+// ------------------------------------------------------------------ lookup (K1)
+struct LookupArgs {
+    const int32_t* slots;
+    int n, k, M, Lmin;
+    const int32_t* tail;
+    const int32_t* ctx_len;
+    const int32_t* prompt;
+    const int32_t* pos;
+    const int32_t* max_len;
+    const int32_t* finished;
+    const IndexEntry* table;
+    uint64_t mask;
+    const int32_t* T;
+    const int32_t* seq_start_of;
+    int32_t* draft;
+    int32_t* draft_len;
+    int32_t* match_len;
+};
+
+__device__ __forceinline__ bool probe(const IndexEntry* table, uint64_t mask, uint64_t key,
+                                      uint32_t& occ, uint32_t& meta) {
+    uint64_t s = key & mask;
+    for (;;) {
+        const uint4 e = __ldg(reinterpret_cast<const uint4*>(table + s));
+        const uint64_t k = ((uint64_t)e.y << 32) | e.x;
+        if (k == key) {
+            occ = e.z;
+            meta = e.w;
+            return true;
+        }
+        if (k == 0) return false;
+        s = (s + 1) & mask;
+    }
+}
+
+__global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= a.n) return;
+    const int slot = a.slots[b];
+    const int M = a.M;
+    const int L = a.ctx_len[slot];
+    const int P = a.prompt[slot];
+    const int p = a.pos[slot], ml = a.max_len[slot];
+    const bool fin = a.finished[slot] || p >= ml;
+    const int mmax = min(M, L);
+    // y[-1-lane]
+    const int tok = (lane < mmax) ? a.tail[(int64_t)slot * M + (M - 1 - lane)] : -1;
+    // B^lane
+    uint64_t bp = 1;
+    for (int t = 0; t < lane; ++t) bp *= HASH_B;
+    uint64_t H = (lane < mmax) ? (uint64_t)(uint32_t)(tok + 1) * bp : 0ull;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t lo = __shfl_up_sync(0xFFFFFFFFu, (uint32_t)H, dd);
+        const uint32_t hi = __shfl_up_sync(0xFFFFFFFFu, (uint32_t)(H >> 32), dd);
+        if (lane >= dd) H += ((uint64_t)hi << 32) | lo;
+    }
+    uint32_t occ = 0, meta = 0;
+    bool found = false;
+    if (!fin && lane < mmax) found = probe(a.table, a.mask, window_key(H, P, lane + 1), occ, meta);
+    unsigned hit = __ballot_sync(0xFFFFFFFFu, found);
+    int mstar = 0, q = 0, dstart = 0;
+    for (;;) {
+        if (hit == 0) break;
+        const int m0 = 32 - __clz(hit);  // largest stored suffix length
+        const uint32_t occ0 = __shfl_sync(0xFFFFFFFFu, occ, m0 - 1);
+        const uint32_t meta0 = __shfl_sync(0xFFFFFFFFu, meta, m0 - 1);
+        // verify y[-m0:] == T[occ0 .. occ0+m0) (guards a 64-bit key false positive)
+        bool okc = true;
+        if (lane < m0) okc = (a.T[(int64_t)occ0 + m0 - 1 - lane] == tok);
+        if (!__all_sync(0xFFFFFFFFu, okc)) {
+            hit &= ~(1u << (m0 - 1));
+            continue;
+        }
+        if ((meta0 & META_UNIQUE) && (meta0 & META_CONT)) {
+            // unique occurrence: extend the anchor to the left within its sequence
+            const int sstart = a.seq_start_of[occ0];
+            const int jj = lane;  // compare y[-m0-1-jj] with T[occ0-1-jj]
+            bool eq = false;
+            if (m0 + jj < mmax) {
+                const int64_t pp = (int64_t)occ0 - 1 - jj;
+                if (pp >= sstart) {
+                    const int yt = a.tail[(int64_t)slot * M + (M - 1 - (m0 + jj))];
+                    eq = (a.T[pp] == yt);
+                }
+            }
+            const unsigned eqm = __ballot_sync(0xFFFFFFFFu, eq);
+            const int ext = (~eqm == 0u) ? 32 : (__ffs(~eqm) - 1);
+            mstar = m0 + ext;
+            q = (int)(meta0 & 0xFFu);
+            dstart = (int)occ0 + m0;
+            break;
+        }
+        // longest stored suffix with a continuation (non-unique entries, <= m0)
+        const unsigned lim = (meta0 & META_UNIQUE) ? ((1u << (m0 - 1)) - 1u)
+                                                   : (m0 == 32 ? 0xFFFFFFFFu : ((1u << m0) - 1u));
+        const unsigned contm = __ballot_sync(0xFFFFFFFFu, found && (meta & META_CONT)) & hit & lim;
+        if (contm == 0) break;
+        const int ms = 32 - __clz(contm);
+        const uint32_t occs = __shfl_sync(0xFFFFFFFFu, occ, ms - 1);
+        const uint32_t metas = __shfl_sync(0xFFFFFFFFu, meta, ms - 1);
+        bool oks = true;
+        if (lane < ms) oks = (a.T[(int64_t)occs + ms - 1 - lane] == tok);
+        if (!__all_sync(0xFFFFFFFFu, oks)) {
+            hit &= ~(1u << (ms - 1));
+            continue;
+        }
+        mstar = ms;
+        q = (int)(metas & 0xFFu);
+        dstart = (int)occs + ms;
+        break;
+    }
+    if (mstar < a.Lmin) {
+        mstar = 0;
+        q = 0;
+    }
+    if (fin) {
+        mstar = 0;
+        q = 0;
+    }
+    q = min(q, a.k);
+    q = min(q, max(0, ml - p - 1));
+    if (lane < a.k) a.draft[(int64_t)b * a.k + lane] = (lane < q) ? a.T[(int64_t)dstart + lane] : -1;
+    if (lane == 0) {
+        a.draft_len[b] = q;
+        if (a.match_len) a.match_len[b] = mstar;
+    }
+}
+
+cudaError_t launch_lookup(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k, int32_t* draft,
+                          int32_t* draft_len, int32_t* match_len, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    LookupArgs a;
+    a.slots = slots;
+    a.n = n;
+    a.k = k;
+    a.M = ctx->M;
+    a.Lmin = ctx->cfg.match_min;
+    a.tail = ctx->tail.p;
+    a.ctx_len = ctx->ctx_len.p;
+    a.prompt = ctx->prompt.p;
+    a.pos = ctx->pos.p;
+    a.max_len = ctx->max_len.p;
+    a.finished = ctx->finished.p;
+    a.table = ctx->table.p;
+    a.mask = ctx->table_mask;
+    a.T = ctx->sealed.tokens.p;
+    a.seq_start_of = ctx->seq_start_of.p;
+    a.draft = draft;
+    a.draft_len = draft_len;
+    a.match_len = match_len;
+    const int blocks = (n * 32 + 255) / 256;
+    lookup_kernel<<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace bs

@@ -1,0 +1,139 @@
+"""RolloutEngine — drives Alg. 1's decoding loop on one GPU through the C-ABI.
+
+One decoding step is four library calls and no host synchronisation:
+
+    bs_draft_lookup -> bsx_target_rows (the synthetic target's "forward": which logits row
+    is p_t for each position; a real engine runs its model here) -> bs_verify_step ->
+    bs_commit
+
+so a chunk of steps can be captured once into a CUDA graph and replayed.  The engine
+owns the per-step device buffers; PyTorch only allocates them and provides the stream.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .api import Context
+
+
+@dataclass
+class Target:
+    """Synthetic target policy: logits rows live in `bank` [nbank, V] (bf16, on device) and
+    the row for a position is workloads.target_row(spec, prompt, t, prev)."""
+    bank: torch.Tensor
+    nbank: int
+    target_seed: int
+    mode: int  # 0 position, 1 markov, 2 mixed
+
+
+class RolloutEngine:
+    def __init__(self, ctx: Context, n: int, k: int, temperature: float, top_p: float,
+                 target: Target, stream: torch.cuda.Stream | None = None):
+        self.ctx, self.n, self.k = ctx, n, k
+        self.T, self.top_p, self.target = temperature, top_p, target
+        dev = torch.device("cuda", ctx.device)
+        self.stream = stream or torch.cuda.current_stream(dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.slots = torch.arange(n, **i32)
+        self.draft = torch.full((n, max(k, 1)), -1, **i32)
+        self.draft_len = torch.zeros(n, **i32)
+        self.match_len = torch.zeros(n, **i32)
+        self.row_index = torch.zeros((n, k + 1), dtype=torch.int64, device=dev)
+        self.out_tokens = torch.full((n, k + 1), -1, **i32)
+        self.out_len = torch.zeros(n, **i32)
+        self.out_acc = torch.zeros(n, **i32)
+        self.finished = torch.zeros(n, **i32)
+        self.rl_step = 0
+        self.graph = None
+        self.graph_steps = 0
+
+    # ------------------------------------------------------------------ RL-step setup
+    def put_pools(self, rl_step, seq_prompt, seq_off, tokens):
+        """bs_draft_pool_put of device tensors (int32 prompt ids, int64 offsets, int32 tokens)."""
+        n_tok = int(tokens.numel())
+        self.ctx.bs_draft_pool_put(rl_step, seq_prompt, seq_off, tokens, n_tok, stream=self.stream)
+
+    def seal(self, rl_step):
+        self.ctx.bs_draft_pool_seal(rl_step, stream=self.stream)
+        self.rl_step = rl_step
+
+    def begin(self, uids, prompt_ids, prompt_tail, max_len):
+        self.ctx.bs_rollout_begin(self.slots, uids, prompt_ids, prompt_tail, max_len,
+                                  stream=self.stream)
+
+    # ------------------------------------------------------------------ decoding
+    def step(self):
+        c, k, s = self.ctx, self.k, self.stream
+        c.bs_draft_lookup(self.rl_step, self.slots, k, self.draft, self.draft_len, self.match_len,
+                          stream=s)
+        t = self.target
+        c.bsx_target_rows(self.slots, self.draft, self.draft_len, k, t.target_seed, t.mode,
+                          t.nbank, self.row_index, stream=s)
+        c.bs_verify_step(self.slots, t.bank, self.row_index, t.bank.shape[1], self.draft,
+                         self.draft_len, k, self.T, self.top_p, self.out_tokens, self.out_len,
+                         self.out_acc, stream=s)
+        c.bs_commit(self.slots, self.out_tokens, self.out_len, k, self.finished, stream=s)
+
+    LAUNCHES_PER_STEP = 5  # lookup, target rows, verify plan, verify rows, commit
+
+    def capture(self, steps: int):
+        """Capture `steps` decoding steps into one CUDA graph (replayed by run_graph)."""
+        with torch.cuda.stream(self.stream):
+            self.step()  # warm (first-call attribute setup happens outside the capture)
+        self.stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            for _ in range(steps):
+                self.step()
+        self.graph, self.graph_steps = g, steps
+        return g
+
+    def run_graph(self):
+        self.graph.replay()
+
+    def all_finished(self) -> bool:
+        return bool(self.finished.all().item())
+
+    def run_until_done(self, max_steps: int = 1 << 20, chunk: int = 64, use_graph: bool = True):
+        """Decode until every rollout finished (EOS or max_len); host checks once per chunk."""
+        steps = 0
+        if use_graph and (self.graph is None or self.graph_steps != chunk):
+            self.capture(chunk)
+            steps = 1  # capture() ran one real (eager) warm-up step
+        while steps < max_steps:
+            if use_graph:
+                self.run_graph()
+                steps += chunk
+            else:
+                for _ in range(chunk):
+                    self.step()
+                steps += chunk
+            if self.all_finished():
+                break
+        return steps
+
+    def stats(self, reset: bool = False):
+        st = self.ctx.bs_stats_read(reset=reset, stream=self.stream)
+        return summarize_stats(st)
+
+
+def summarize_stats(st: np.ndarray) -> dict:
+    """AL / DL / AR and streak histogram from the device counters (
+    identity AR = (AL - 1) / DL pinned by P:269)."""
+    st = st.astype(np.int64)
+    spec, plain = int(st[0]), int(st[1])
+    emit_spec, emit_plain = int(st[2]), int(st[3])
+    acc, prop = int(st[4]), int(st[5])
+    out = {
+        "verify_steps": spec, "plain_steps": plain, "decode_steps": spec + plain,
+        "tokens": emit_spec + emit_plain, "accepted": acc, "proposed": prop,
+        "rows_verified": int(st[6]), "rows_needed": int(st[7]),
+        "acceptance_length": emit_spec / spec if spec else None,
+        "draft_length": prop / spec if spec else None,
+        "acceptance_rate": acc / prop if prop else None,
+        "streak_hist": [int(x) for x in st[8:41]],
+    }
+    return out

@@ -1,0 +1,97 @@
+"""CPU checks of the boundary: the C-ABI library builds, loads without a GPU and exports
+every function include/bubblespec.h declares; host-only entry points work on CPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "bubblespec.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_08862_b200 import build
+
+    path = build.build()
+    return ctypes.CDLL(path)
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bsx?_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ["bs_draft_pool_put", "bs_draft_lookup", "bs_verify_step", "bs_commit",
+              "bs_draft_pool_seal", "bs_draft_exchange", "bs_create", "bs_destroy"]:
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_signatures_cover_header(lib):
+    from paper_2605_08862_b200._lib import SIGNATURES
+
+    assert set(declared_functions()) == set(SIGNATURES)
+
+
+def test_create_without_gpu_fails_cleanly(lib):
+    """No GPU here: bs_create must return BS_ERR_CUDA (3), never crash."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2605_08862_b200 import BubbleSpecError, Context
+
+    with pytest.raises(BubbleSpecError) as e:
+        Context(vocab=1024, device=0)
+    assert e.value.status == 3
+
+
+def test_invalid_config_rejected_before_device(lib):
+    from paper_2605_08862_b200._lib import bs_config, load
+
+    L = load()
+    h = ctypes.c_void_p()
+    cfg = bs_config(0, -1, 4, 32, 1, 4, 16, 4, 0, 0)
+    assert L.bs_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    assert b"vocab" in L.bs_last_error(None)
+    cfg = bs_config(1024, -1, 40, 32, 1, 4, 16, 4, 0, 0)
+    assert L.bs_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+
+
+def test_version_string(lib):
+    from paper_2605_08862_b200._lib import load
+
+    assert b"sm_100a" in load().bs_version()
+
+
+def test_route_plan_host_logic():
+    """bs_route_plan (the host half of bs_draft_exchange): owner = prompt mod world."""
+    from paper_2605_08862_b200 import bs_route_plan
+
+    world, max_seqs, max_tok = 3, 4, 20
+    counts = np.array([2, 5, 3, 9, 0, 0], np.int64)
+    offs = np.zeros((world, max_seqs + 1), np.int64)
+    offs[0, :3] = [0, 2, 5]
+    offs[1, :4] = [0, 4, 4, 9]
+    prm = np.zeros((world, max_seqs), np.int32)
+    prm[0, :2] = [3, 4]
+    prm[1, :3] = [6, 1, 9]
+    for rank in range(world):
+        src, dst, ln, pr, nt = bs_route_plan(world, rank, counts, offs.ravel(), prm.ravel(),
+                                             max_seqs, max_tok)
+        assert all(p % world == rank for p in pr)
+        assert nt == int(ln.sum())
+        assert list(dst) == list(np.cumsum(ln) - ln)
+    src, dst, ln, pr, nt = bs_route_plan(world, 0, counts, offs.ravel(), prm.ravel(), max_seqs,
+                                         max_tok)
+    assert list(pr) == [3, 6, 9] and list(ln) == [2, 4, 5] and list(src) == [0, 20, 24]

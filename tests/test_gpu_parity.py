@@ -1,0 +1,264 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by element on
+the same seeded inputs.  Bit-exact on drafts, accepted lengths, emitted tokens and the
+integer normaliser Z; softmax normalisers within 1e-5 relative of the oracle's fp64 sum.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from workloads import TargetSpec, bank_rows, bf16_bits_to_f32, f32_to_bf16_bits  # noqa: E402
+
+from tests.gpu_util import bank_numpy, pools_for, setup_rollouts, to_dev  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def bs():
+    import paper_2605_08862_b200 as bs
+
+    assert torch.cuda.is_available()
+    return bs
+
+
+def _verify_gpu(bs, ctx, rows_dense, drafts, dlen, k, T, top_p, stride=None):
+    """Run bs_verify_step on dense rows [n, k+1, V] (uint16) with rollouts already begun."""
+    n = drafts.shape[0]
+    V = rows_dense.shape[2]
+    stride = stride or V
+    if stride != V:
+        buf = np.zeros((n, k + 1, stride), dtype=np.uint16)
+        buf[:, :, :V] = rows_dense
+    else:
+        buf = rows_dense
+    lg = to_dev(buf.view(np.int16).reshape(-1))
+    slots = to_dev(np.arange(n, dtype=np.int32))
+    out_t = torch.full((n, k + 1), -7, dtype=torch.int32, device="cuda")
+    out_l = torch.zeros(n, dtype=torch.int32, device="cuda")
+    out_a = torch.zeros(n, dtype=torch.int32, device="cuda")
+    out_n = torch.zeros((n, k + 1), dtype=torch.float32, device="cuda")
+    out_z = torch.zeros((n, k + 1), dtype=torch.int64, device="cuda")
+    ctx.bs_verify_step(slots, lg, None, stride, to_dev(drafts.astype(np.int32)),
+                       to_dev(dlen.astype(np.int32)), k, T, top_p, out_t, out_l, out_a, out_n, out_z)
+    torch.cuda.synchronize()
+    return (out_t.cpu().numpy(), out_l.cpu().numpy(), out_a.cpu().numpy(), out_n.cpu().numpy(),
+            out_z.cpu().numpy().view(np.uint64))
+
+
+def _begin(bs, ctx, n, pos_max_len, uids, M):
+    slots = to_dev(np.arange(n, dtype=np.int32))
+    tail = np.full((n, M), -1, dtype=np.int32)
+    tail[:, -1] = 0
+    ctx.bs_rollout_begin(slots, to_dev(np.asarray(uids, dtype=np.uint64).view(np.int64)),
+                         to_dev(np.zeros(n, dtype=np.int32)), to_dev(tail),
+                         to_dev(np.asarray(pos_max_len, dtype=np.int32)))
+
+
+def _compare_step(orc, rows, drafts, dlen, k, T, top_p, seed, uids, max_len, eos, got,
+                  pos=0):
+    ot, ol, oa, on, oz = got
+    for b in range(drafts.shape[0]):
+        q = int(dlen[b])
+        o = orc.verify_one([rows[b, j] for j in range(k + 1)], T, top_p, seed, int(uids[b]), pos,
+                           int(max_len[b]), eos, False, [int(x) for x in drafts[b, :q]], k)
+        assert int(ol[b]) == len(o.tokens), (b, ol[b], o.tokens)
+        assert [int(x) for x in ot[b, : ol[b]]] == o.tokens, (b, ot[b], o.tokens)
+        assert int(oa[b]) == o.accepted
+        for j in range(o.rows_used):
+            assert int(oz[b, j]) == o.z[j], (b, j)
+            if T > 0:
+                assert abs(float(on[b, j]) / o.norm_fp64[j] - 1) < 1e-5, (b, j)
+        for j in range(o.rows_used, k + 1):
+            assert int(oz[b, j]) == 0 and float(on[b, j]) == 0.0
+
+
+@pytest.mark.parametrize("V,T,stride", [(1024, 1.0, None), (1000, 0.7, None), (4096, 1.3, None),
+                                        (1001, 1.0, 1003), (1024, 0.0, None), (33, 1.0, None),
+                                        (151936, 1.0, None)])
+def test_verify_step_parity(bs, orc, V, T, stride):
+    """Random logits rows (several tiles + ragged tail, odd strides), random drafts mixing
+    the argmax (often accepted) with random tokens."""
+    rng = np.random.default_rng(V + int(T * 10))
+    k = 4 if V < 100000 else 8
+    n = 48 if V < 100000 else 12
+    rows = f32_to_bf16_bits(rng.normal(0, 2.0, size=(n, k + 1, V)).astype(np.float32))
+    # make some rows peaked so acceptance happens
+    for b in range(n):
+        for j in range(k + 1):
+            if rng.random() < 0.6:
+                rows[b, j, rng.integers(0, V)] = f32_to_bf16_bits(np.float32(9.0))
+    argm = bf16_bits_to_f32(rows).argmax(axis=2)
+    drafts = np.where(rng.random((n, k)) < 0.7, argm[:, :k], rng.integers(0, V, (n, k)))
+    dlen = rng.integers(0, k + 1, n)
+    max_len = np.where(rng.random(n) < 0.2, rng.integers(1, 4, n), 1000)
+    seed = 0xABCDEF
+    ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=8, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    uids = np.arange(n, dtype=np.uint64) * np.uint64(7919) + np.uint64(3)
+    _begin(bs, ctx, n, max_len, uids, 8)
+    got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, T, 1.0, stride)
+    assert ctx.bs_sync_status() == 0
+    _compare_step(orc, rows, drafts, dlen, k, T, 1.0, seed, uids, max_len, -1, got)
+
+
+def test_verify_eos_and_edge_cases(bs, orc):
+    """Accepted EOS ends the block; q=0 is a plain sample; -inf logits; max_len clamp."""
+    V, k, n, eos = 64, 4, 32, 5
+    rng = np.random.default_rng(1)
+    vals = rng.normal(0, 1, (n, k + 1, V)).astype(np.float32)
+    vals[:, :, 7] = -np.inf
+    vals[::2, 1, eos] = 12.0  # EOS very likely at row 1
+    rows = f32_to_bf16_bits(vals)
+    drafts = rng.integers(0, V, (n, k))
+    drafts[:, 1] = eos
+    drafts[::3, 0] = 7  # zero-mass draft token: rejected at row 0
+    dlen = np.full(n, k)
+    dlen[::5] = 0
+    max_len = np.full(n, 100)
+    max_len[::7] = 2
+    seed = 99
+    ctx = bs.Context(vocab=V, eos_id=eos, k_max=k, match_max=8, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    uids = np.arange(n, dtype=np.uint64) + np.uint64(11)
+    _begin(bs, ctx, n, max_len, uids, 8)
+    got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, 1.0, 1.0)
+    assert ctx.bs_sync_status() == 0
+    _compare_step(orc, rows, drafts, dlen, k, 1.0, 1.0, seed, uids, max_len, eos, got)
+
+
+def test_verify_device_errors(bs):
+    V, k, n = 64, 2, 4
+    rows = np.zeros((n, k + 1, V), dtype=np.uint16)
+    rows[1, 0, 3] = 0x7FC0  # NaN
+    ctx = bs.Context(vocab=V, k_max=k, match_max=8, max_rollouts=n, pool_capacity_tokens=16,
+                     pool_capacity_seqs=4)
+    _begin(bs, ctx, n, [10] * n, np.arange(n, dtype=np.uint64), 8)
+    _verify_gpu(bs, ctx, rows, np.zeros((n, k), np.int64), np.full(n, 2), k, 1.0, 1.0)
+    assert ctx.bs_sync_status() & 0x1
+    _verify_gpu(bs, ctx, np.zeros((n, k + 1, V), np.uint16), np.full((n, k), V + 3),
+                np.full(n, 2), k, 1.0, 1.0)
+    assert ctx.bs_sync_status() & 0x8
+    allneg = np.full((n, k + 1, V), 0xFF80, dtype=np.uint16)
+    _verify_gpu(bs, ctx, allneg, np.zeros((n, k), np.int64), np.full(n, 1), k, 1.0, 1.0)
+    assert ctx.bs_sync_status() & 0x2
+
+
+# ------------------------------------------------------------------ lookup
+def _gpu_lookup(bs, ctx, seq_prompt, seq_off, tokens, ctxs, prompt_of, k, M, max_len=1 << 20,
+                rl_step=1):
+    n = len(ctxs)
+    ctx.bs_draft_pool_put(rl_step, to_dev(seq_prompt.astype(np.int32)), to_dev(seq_off),
+                          to_dev(tokens.astype(np.int32)) if len(tokens) else
+                          to_dev(np.zeros(1, np.int32)), int(len(tokens)))
+    ctx.bs_draft_pool_seal(rl_step)
+    tail = np.full((n, M), -1, dtype=np.int32)
+    for b, c in enumerate(ctxs):
+        c = list(c)[-M:]
+        tail[b, M - len(c):] = c
+    slots = to_dev(np.arange(n, dtype=np.int32))
+    ctx.bs_rollout_begin(slots, to_dev(np.arange(n, dtype=np.int64)),
+                         to_dev(np.asarray(prompt_of, dtype=np.int32)), to_dev(tail),
+                         to_dev(np.full(n, max_len, dtype=np.int32)))
+    d = torch.zeros((n, k), dtype=torch.int32, device="cuda")
+    dl = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ml = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ctx.bs_draft_lookup(rl_step, slots, k, d, dl, ml)
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() == 0
+    return d.cpu().numpy(), dl.cpu().numpy(), ml.cpu().numpy()
+
+
+@pytest.mark.parametrize("vocab,Lmin,M,k", [(3, 1, 8, 4), (5, 1, 6, 3), (4, 2, 8, 5),
+                                            (50, 1, 32, 8), (2, 1, 32, 16)])
+def test_lookup_parity_random_pools(bs, orc, vocab, Lmin, M, k):
+    """random pools x prefixes, GPU index lookup == brute-force oracle (drafts and
+    anchor length), several prompts per pool."""
+    rng = np.random.default_rng(vocab * 100 + M)
+    n_prompts = 6
+    seqs, sp = [], []
+    for P in range(n_prompts):
+        for _ in range(int(rng.integers(0, 6))):
+            L = int(rng.integers(0, 40))
+            seqs.append(rng.integers(0, vocab, L).astype(np.int32))
+            sp.append(P)
+    off = np.zeros(len(seqs) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(s) for s in seqs])
+    tokens = np.concatenate(seqs) if seqs and off[-1] else np.zeros(0, np.int32)
+    ctxs, pof = [], []
+    for _ in range(200):
+        P = int(rng.integers(0, n_prompts))
+        # contexts: either random or copied from a pool sequence (long matches)
+        own = [s for s, p in zip(seqs, sp) if p == P and len(s) > 3]
+        if own and rng.random() < 0.6:
+            s = own[int(rng.integers(0, len(own)))]
+            e = int(rng.integers(1, len(s) + 1))
+            c = list(rng.integers(0, vocab, int(rng.integers(0, 5)))) + list(s[:e])
+        else:
+            c = list(rng.integers(0, vocab, int(rng.integers(1, 40))))
+        ctxs.append([int(x) for x in c] or [0])
+        pof.append(P)
+    ctx = bs.Context(vocab=vocab, k_max=k, match_max=M, match_min=Lmin, max_rollouts=len(ctxs),
+                     pool_capacity_tokens=max(1, len(tokens)), pool_capacity_seqs=max(1, len(seqs)))
+    d, dl, ml = _gpu_lookup(bs, ctx, np.asarray(sp, np.int32), off, tokens, ctxs, pof, k, M)
+    pools = {}
+    for s, P in zip(seqs, sp):
+        pools.setdefault(P, []).append([int(x) for x in s])
+    for b, c in enumerate(ctxs):
+        want_d, want_m = orc.lookup(pools.get(pof[b], []), c[-M:], M, Lmin, k)
+        assert list(d[b, : dl[b]]) == want_d, (b, c, want_d, d[b], dl[b])
+        assert int(ml[b]) == want_m, (b, c, ml[b], want_m)
+
+
+def test_lookup_stale_and_clamp(bs, orc):
+    V, k, M = 10, 4, 8
+    seqs = [np.array([1, 2, 3, 4, 5, 6], np.int32)]
+    off = np.array([0, 6], np.int64)
+    ctx = bs.Context(vocab=V, k_max=k, match_max=M, max_rollouts=2, pool_capacity_tokens=16,
+                     pool_capacity_seqs=2)
+    d, dl, ml = _gpu_lookup(bs, ctx, np.array([0], np.int32), off, seqs[0], [[1, 2], [1, 2]],
+                            [0, 0], k, M, max_len=3)
+    assert list(dl) == [2, 2] and list(d[0, :2]) == [3, 4]  # clamp: max_len - pos - 1 = 2
+    with pytest.raises(bs.BubbleSpecError):
+        slots = to_dev(np.arange(2, dtype=np.int32))
+        z = torch.zeros((2, k), dtype=torch.int32, device="cuda")
+        ctx.bs_draft_lookup(2, slots, k, z, z[:, 0].contiguous())
+
+
+def test_lookup_index_on_perturbed_pools(bs, orc):
+    """Qwen-shaped vocab, pools = 16 perturbed copies of a reference text (the bench's
+    recipe): GPU == oracle on contexts sampled along the reference."""
+    spec = TargetSpec(V=151936, nbank=64, mode="position")
+    M, k = 32, 8
+    prompts, tails, *_ = setup_rollouts(spec, 3, 1, M, 100)
+    rng = np.random.default_rng(3)
+    lens = rng.integers(50, 400, (3, 16))
+    sp, off, tok = pools_for(spec, prompts, tails, 16, lens, 0.8, prefix=M)
+    ctxs, pof = [], []
+    for i, P in enumerate(prompts):
+        s = tok[off[16 * i]: off[16 * i + 1]]
+        for _ in range(40):
+            e = int(rng.integers(1, len(s)))
+            c = [int(x) for x in s[max(0, e - 40): e]]
+            if rng.random() < 0.3:
+                c[-1] = int(rng.integers(0, spec.V))
+            ctxs.append(c)
+            pof.append(int(P))
+    ctx = bs.Context(vocab=spec.V, k_max=k, match_max=M, max_rollouts=len(ctxs),
+                     pool_capacity_tokens=len(tok), pool_capacity_seqs=len(sp))
+    d, dl, ml = _gpu_lookup(bs, ctx, sp, off, tok, ctxs, pof, k, M)
+    pools = {}
+    for s_i, P in enumerate(sp):
+        pools.setdefault(int(P), []).append([int(x) for x in tok[off[s_i]:off[s_i + 1]]])
+    for b, c in enumerate(ctxs):
+        want_d, want_m = orc.lookup(pools[pof[b]], c[-M:], M, 1, k)
+        assert list(d[b, : dl[b]]) == want_d and int(ml[b]) == want_m, b
+
+
+# ------------------------------------------------------------------ synthetic twins
+def test_synth_bank_matches_numpy(bs):
+    V, rows = 151936, 6
+    bank = torch.empty((rows, V), dtype=torch.int16, device="cuda")
+    bs.bsx_synth_bank(bank, rows, V, 1234, 11.5)
+    torch.cuda.synchronize()
+    want = bank_rows(1234, np.arange(rows), V, 11.5)
+    assert np.array_equal(bank.cpu().numpy().view(np.uint16), want)
