@@ -147,16 +147,7 @@ __global__ void level_paths_kernel(int l, int M, int K, int top, Level lv, Level
         const int rs = lv.runstart[R];
         const int size = lv.runstart[R + 1] - rs;
         const int i0 = lv.pos_sorted[rs];
-        if (size == 1) {
-            // first unique window at its end position?  (l == 1, or (i0+1, l-1) non-unique)
-            if (l <= M && (l == 1 || fu[i0 + 1] >= l)) {
-                const int q = min(K, seq_end_of[i0] - (i0 + l));
-                const uint32_t meta = (uint32_t)q | META_UNIQUE | (q > 0 ? META_CONT : 0u);
-                table_insert(table, mask, window_key(hash_window(T, i0, l), prompt_of[i0], l),
-                             (uint32_t)i0, meta, dev_err);
-            }
-            continue;
-        }
+        if (size == 1) continue;  // unique windows: first_unique_kernel
         int q = 0, occ = i0;
         if (!top) {
             const int c0 = cbeg[R], c1 = cend[R];
@@ -185,6 +176,33 @@ __global__ void level_paths_kernel(int l, int M, int K, int top, Level lv, Level
             const uint32_t meta = (uint32_t)q | (q > 0 ? META_CONT : 0u);
             table_insert(table, mask, window_key(hash_window(T, occ, l), prompt_of[occ], l),
                          (uint32_t)occ, meta, dev_err);
+        }
+    }
+}
+
+// First-unique windows.  fu[i] = the length at which the window starting at i became
+// unique (its extensions stay unique and share its single occurrence).  The window (i, l)
+// is the FIRST unique window at its end position e = i+l-1 iff it is unique (l >= fu[i])
+// and (i+1, l-1) is not (l <= fu[i+1]); so position i contributes the lengths
+// [fu[i], min(fu[i+1], M, seq_end - i)].  At most one entry per end position.
+__global__ void first_unique_kernel(int n, int M, int K, const int32_t* T, const int32_t* fu,
+                                    const int32_t* seq_end_of, const int32_t* prompt_of,
+                                    IndexEntry* table, uint64_t mask, uint32_t* dev_err) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int lo = fu[i];
+        if (lo > M) continue;
+        const int se = seq_end_of[i];
+        int hi = min(M, se - i);
+        if (i + 1 < se) hi = min(hi, fu[i + 1]);
+        if (lo > hi) continue;
+        const int32_t P = prompt_of[i];
+        uint64_t H = 0;
+        for (int t = 0; t < lo - 1; ++t) H = H * HASH_B + (uint64_t)(uint32_t)(T[i + t] + 1);
+        for (int l = lo; l <= hi; ++l) {
+            H = H * HASH_B + (uint64_t)(uint32_t)(T[i + l - 1] + 1);
+            const int q = min(K, se - (i + l));
+            const uint32_t meta = (uint32_t)q | META_UNIQUE | (q > 0 ? META_CONT : 0u);
+            table_insert(table, mask, window_key(H, P, l), (uint32_t)i, meta, dev_err);
         }
     }
 }
@@ -288,14 +306,16 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         A = an;
         hi_max = (uint64_t)nr;
     }
-    // table capacity: <= one entry per run at levels <= M
-    int64_t cap_need = 0;
+    // table capacity: one entry per run at levels <= M, plus one first-unique per end position
+    int64_t cap_need = n;
     for (size_t li = 0; li < levels.size() && (int)li < M; ++li) cap_need += levels[li].nruns;
     uint64_t cap = 2;
     while (cap < (uint64_t)(2 * cap_need + 2)) cap <<= 1;
     BS_TRY(ctx->table.ensure(cap));
     BS_TRY(cudaMemsetAsync(ctx->table.p, 0, cap * sizeof(IndexEntry), st));
     ctx->table_mask = cap - 1;
+    first_unique_kernel<<<G, 256, 0, st>>>(n, M, K, T, fu.p, ctx->seq_end_of.p, ctx->prompt_of.p,
+                                           ctx->table.p, ctx->table_mask, ctx->dev_err.p);
     // descending pass
     int maxr = 1;
     for (auto& lv : levels) maxr = std::max(maxr, lv.nruns);

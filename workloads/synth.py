@@ -101,6 +101,9 @@ def target_row(spec: TargetSpec, P, t, prev):
 
 def reference_text(spec: TargetSpec, P: int, length: int, prompt_last: int) -> np.ndarray:
     """R_P[t] = peak column of the target row at t when following the reference."""
+    if spec.mode == "position":  # rows do not depend on the previous token: vectorise
+        r = target_row(spec, P, np.arange(length, dtype=np.int64), 0)
+        return bank_peak(spec.bank_seed, r, spec.V).astype(np.int32)
     out = np.empty(length, dtype=np.int32)
     prev = prompt_last
     for t in range(length):
