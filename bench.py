@@ -32,7 +32,7 @@ CONFIGS = {
     # BASELINE.json configs[1]: "Qwen2.5-7B-shaped: V=151936, 256 rollouts, k=8, 4k-token
     # lognormal lengths, T=1.0, 1 GPU"
     "q7": dict(V=151936, prompts=16, G=16, k=8, M=32, T=1.0, top_p=1.0, mean_len=4096,
-               sigma=0.6, cap=32768, nbank=8192, beta=13.5, match_rate=0.9, noise=0.02,
+               sigma=0.6, cap=32768, nbank=8192, beta=15.75, match_rate=0.8, noise=0.02,
                G_pre=16, pool_frac=2.0 / 3.0),
     # configs[0]: the small case the oracle finishes in seconds
     "tiny": dict(V=1024, prompts=1, G=4, k=4, M=16, T=1.0, top_p=1.0, mean_len=64, sigma=0.0,

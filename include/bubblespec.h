@@ -211,7 +211,7 @@ bs_status bs_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t*
 /* ---------------------------------------------------------------- synthetic workload */
 /* Not part of the method: device twins of workloads/synth.py so a
  * multi-GB logit bank need not be generated on the host.  Bit-identical to numpy. */
-/* bank[rows, V] bf16: Irwin-Hall(4 hashed bytes) * 2^-6, + beta at the peak column. */
+/* bank[rows, V] bf16: Irwin-Hall(4 hashed bytes) * 2^-6; the peak column holds beta. */
 bs_status bsx_synth_bank(void* bank_bf16, int64_t rows, int32_t V, uint32_t bank_seed,
                          float beta, void* stream);
 /* Synthetic target "forward": row_index[b*(k+1)+j] = target_row(prompt, pos+j, prev_j)

@@ -78,10 +78,8 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
                c->pos.ensure(R) == cudaSuccess && c->max_len.ensure(R) == cudaSuccess &&
                c->prompt.ensure(R) == cudaSuccess && c->finished.ensure(R) == cudaSuccess &&
                c->uid.ensure(R) == cudaSuccess && c->dev_err.ensure(1) == cudaSuccess &&
-               c->rowres.ensure(rows) == cudaSuccess && c->row_b.ensure(rows) == cudaSuccess &&
-               c->row_j.ensure(rows) == cudaSuccess && c->rb_base.ensure(R) == cudaSuccess &&
-               c->rb_q.ensure(R) == cudaSuccess && c->done_ctr.ensure(R) == cudaSuccess &&
-               c->total_rows.ensure(1) == cudaSuccess &&
+               c->rb_q.ensure(R) == cudaSuccess && c->vqueue.ensure(rows + R + 64) == cudaSuccess &&
+               c->vctl.ensure(VCTL_WORDS) == cudaSuccess &&
                c->staging.tokens.ensure((size_t)cfg->pool_capacity_tokens) == cudaSuccess &&
                c->staging.seq_off.ensure((size_t)cfg->pool_capacity_seqs + 1) == cudaSuccess &&
                c->staging.seq_prompt.ensure((size_t)cfg->pool_capacity_seqs) == cudaSuccess &&
@@ -103,7 +101,7 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     // unused slots are finished (no rows, no drafts)
     cudaMemset(c->finished.p, 0, R * sizeof(int32_t));
     cudaMemset(c->dev_err.p, 0, sizeof(uint32_t));
-    cudaMemset(c->done_ctr.p, 0, R * sizeof(int32_t));
+    cudaMemset(c->vctl.p, 0, VCTL_WORDS * sizeof(unsigned int));
     cudaMemset(c->stats.p, 0, STAT_COUNT * sizeof(unsigned long long));
     cudaMemset(c->table.p, 0, 2 * sizeof(IndexEntry));
     cudaMemset(c->staging.seq_off.p, 0, sizeof(int64_t));
@@ -126,8 +124,7 @@ void bs_destroy(bs_ctx* c) {
     c->staging.tokens.release(); c->staging.seq_off.release(); c->staging.seq_prompt.release();
     c->sealed.tokens.release(); c->sealed.seq_off.release(); c->sealed.seq_prompt.release();
     c->seq_start_of.release(); c->seq_end_of.release(); c->prompt_of.release();
-    c->table.release(); c->rowres.release(); c->row_b.release(); c->row_j.release();
-    c->rb_base.release(); c->rb_q.release(); c->done_ctr.release(); c->total_rows.release();
+    c->table.release(); c->rb_q.release(); c->vqueue.release(); c->vctl.release();
     c->stats.release();
     delete c;
 }

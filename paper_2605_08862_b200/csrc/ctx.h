@@ -25,14 +25,8 @@ enum : int {
     STAT_COUNT = STAT_HIST + STAT_HIST_BINS
 };
 
-// Per-row verification result (one per verified logits row).
-struct RowRes {
-    unsigned long long z;  // Z' (exact integer normaliser after top-p)
-    float norm;            // Z_full * 2^-S as fp32
-    int32_t accept;        // row j < q: d_{j+1} accepted
-    int32_t cand;          // residual (j < q) or bonus (j == q) candidate token
-    int32_t pad;
-};
+// Control words of the verify kernel's row work queue.
+enum : int { VCTL_HEAD = 0, VCTL_TAIL = 1, VCTL_DONE = 2, VCTL_NACTIVE = 3, VCTL_WORDS = 4 };
 
 template <typename T>
 struct DevBuf {
@@ -83,9 +77,9 @@ struct bs_ctx {
     bs::DevBuf<int32_t> seq_start_of, seq_end_of, prompt_of;  // per sealed pool token
     bs::DevBuf<bs::IndexEntry> table;
     uint64_t table_mask = 0;
-    // verify scratch
-    bs::DevBuf<bs::RowRes> rowres;
-    bs::DevBuf<int32_t> row_b, row_j, rb_base, rb_q, done_ctr, total_rows;
+    // verify scratch: clamped q per rollout, the row work queue and its control words
+    bs::DevBuf<int32_t> rb_q, vqueue;
+    bs::DevBuf<unsigned int> vctl;
     bs::DevBuf<unsigned long long> stats;  // STAT_COUNT counters
     int32_t* responses = nullptr;           // optional [max_rollouts, resp_stride] output
     int64_t resp_stride = 0;

@@ -11,7 +11,7 @@ __device__ __forceinline__ uint16_t synth_elem(uint32_t hr, uint32_t col, int pe
     const uint32_t h = h32(hr ^ col);
     const int s = (int)(h & 255u) + (int)((h >> 8) & 255u) + (int)((h >> 16) & 255u) + (int)(h >> 24) - 510;
     float v = (float)s * 0.015625f;
-    if ((int)col == peak) v = __fadd_rn(v, beta);
+    if ((int)col == peak) v = beta;
     const __nv_bfloat16 bv = __float2bfloat16_rn(v);
     uint16_t u;
     memcpy(&u, &bv, 2);

@@ -1,20 +1,20 @@
 // verify.cu — fused vocab-row verify + resample (Eq. 2, Eq. 3 P:208-210,
 // Alg. 1, bonus token P:308) for sm_100a.
 //
-// Decomposition (kernel K3):
-//   * one thread-block CLUSTER of C CTAs per verified logits row; CTA `rank` owns the
-//     vocab slice [rank*SL, min(V, (rank+1)*SL)) which a single elected thread stages
-//     into shared memory with 1-D bulk async copies (TMA engine, mbarrier completion,
-//     L2 evict-first so the draft index stays resident);
-//   * pass 1: row max on packed bf16x2 (NaN-propagating) -> cluster max over DSMEM;
-//   * pass 2: integer masses of reading R (exact u64 sums, so the decision is
-//     independent of reduction order) -> slice sums over DSMEM -> Z, mass(d);
-//   * decisions: accept <=> floor(r*Z/2^128) < mass(d) (Philox counter
-//     (pos+j, ACCEPT, uid)); if a sample is needed (rejection: residual without d;
-//     j == q: bonus) the CTA holding the CDF crossing finds the token by a warp scan
-//     over its slice (only the crossing 256-element tile is rescanned per warp step);
-//   * the last row of a rollout to finish (atomic counter) applies Alg. 1's first
-//     rejection / EOS logic and writes the emitted tokens.
+// Kernel K3: a PERSISTENT grid of thread-block clusters pulling logits
+// rows from a device work queue in Alg. 1's order.  Row (b, 0) of every live rollout is
+// queued first; row (b, j+1) is queued only when row j accepted d_{j+1} (lazy dataflow:
+// rows after the first rejection are never read).  Per row, a cluster of C CTAs
+// owns the vocabulary, CTA `rank` the slice [rank*SL, (rank+1)*SL):
+//   * an elected thread stages the slice with 1-D bulk async copies (TMA engine,
+//     mbarrier completion, L2 evict-first); the NEXT claimed row is prefetched into the
+//     second smem buffer while the current row is computed;
+//   * pass 1: NaN-propagating bf16x2 max -> cluster max over DSMEM;
+//   * pass 2: integer masses of reading R with packed FFMA2/FADD2, exact u64 sums ->
+//     slice sums over DSMEM -> Z, mass(d) -> accept (Philox counter (pos+j, ACCEPT));
+//   * a residual / bonus sample only when needed: the CTA holding the CDF crossing
+//     rescans the crossing warp's 256-element tiles;
+//   * the leader then either queues row j+1 or finalizes the rollout (emitted tokens).
 #include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
@@ -25,6 +25,8 @@
 namespace cg = cooperative_groups;
 
 namespace bs {
+
+constexpr int ITEM_DONE = -1;
 
 struct VerifyArgs {
     const int32_t* slots;
@@ -37,29 +39,27 @@ struct VerifyArgs {
     unsigned long long seed;
     const int32_t* pos;
     const unsigned long long* uid;
-    const int32_t* row_b;
-    const int32_t* row_j;
     const int32_t* rb_q;
-    const int32_t* rb_base;
-    int32_t* done;
-    const int32_t* total_rows;
-    RowRes* rowres;
+    int32_t* queue;
+    unsigned int* ctl;  // VCTL_* words
     uint32_t* dev_err;
     int32_t* out_tokens;
     int32_t* out_len;
     int32_t* out_acc;
     float* out_norm;
     unsigned long long* out_z;
-    unsigned long long* stats;  // bs::STAT_* counters (may be null)
+    unsigned long long* stats;
 };
 
 struct __align__(16) VShared {
-    uint64_t bar;
+    uint64_t full[2];  // TMA completion barriers, one per slice buffer
     // exchanged over DSMEM
     float xmax;
     uint32_t xbad;
     int32_t xfirst;
-    int32_t cand;  // written remotely into the leader (rank 0)
+    int32_t cand;         // written remotely into the leader (rank 0)
+    int32_t item_next;    // broadcast by the leader: prefetched next row (0 = none)
+    int32_t item_bcast;   // broadcast by the leader: blocking-claimed next row
     unsigned long long xsum;
     unsigned long long xmassd;
     // CTA-local
@@ -70,16 +70,65 @@ struct __align__(16) VShared {
     // broadcast decisions
     float m;
     int32_t ok;
-    int32_t greedy;
     int32_t accept;
     int32_t need_sample;
-    int32_t excl;
     int32_t cross_rank;
     int32_t wstar;
+    int32_t greedy;
+    int32_t pad;
     unsigned long long z;
-    unsigned long long massd;
-    unsigned long long ulocal;  // target within this CTA's slice / warp
+    unsigned long long ulocal;
 };
+
+// ------------------------------------------------------------------ packed fp32 math
+struct F2 {
+    float x, y;
+};
+__device__ __forceinline__ F2 ffma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+        " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+__device__ __forceinline__ F2 fadd2(F2 a, F2 b) {
+    F2 r;
+    asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+        " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+
+// Masses of the two bf16 logits packed in w (R2-R4), bit-identical to mass_of() per lane:
+// the packed FFMA2 / FADD2 perform the same IEEE single operations.
+__device__ __forceinline__ void mass_pair(uint32_t w, const MassParams& mp, uint64_t& m0,
+                                          uint64_t& m1) {
+    const F2 l{bf16lo(w), bf16hi(w)};
+    F2 y = ffma2(l, F2{mp.c, mp.c}, F2{mp.nmc, mp.nmc});
+    y.x = fmaxf(y.x, mp.clampv);
+    y.y = fmaxf(y.y, mp.clampv);
+    const F2 t = fadd2(y, F2{mp.magic, mp.magic});
+    const F2 n = fadd2(t, F2{-mp.magic, -mp.magic});
+    const F2 f = fadd2(y, F2{-n.x, -n.y});
+    F2 p = ffma2(F2{BS_C5, BS_C5}, f, F2{BS_C4, BS_C4});
+    p = ffma2(p, f, F2{BS_C3, BS_C3});
+    p = ffma2(p, f, F2{BS_C2, BS_C2});
+    p = ffma2(p, f, F2{BS_C1, BS_C1});
+    p = ffma2(p, f, F2{BS_C0, BS_C0});
+    m0 = f2u64_rz(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)));
+    m1 = f2u64_rz(__uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
+__device__ __forceinline__ uint64_t mass8(const uint4 v, const MassParams& mp) {
+    uint64_t a0, a1, b0, b1, c0, c1, d0, d1;
+    mass_pair(v.x, mp, a0, a1);
+    mass_pair(v.y, mp, b0, b1);
+    mass_pair(v.z, mp, c0, c1);
+    mass_pair(v.w, mp, d0, d1);
+    return ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
+}
 
 __device__ __forceinline__ uint32_t hmax2_nan_u32(uint32_t a, uint32_t b) {
     __nv_bfloat162 x, y;
@@ -91,73 +140,118 @@ __device__ __forceinline__ uint32_t hmax2_nan_u32(uint32_t a, uint32_t b) {
     return r;
 }
 
-__device__ __forceinline__ uint64_t mass8(const uint4 v, const MassParams& mp) {
-    uint64_t s = 0;
-    s += mass_of(bf16lo(v.x), mp);
-    s += mass_of(bf16hi(v.x), mp);
-    s += mass_of(bf16lo(v.y), mp);
-    s += mass_of(bf16hi(v.y), mp);
-    s += mass_of(bf16lo(v.z), mp);
-    s += mass_of(bf16hi(v.z), mp);
-    s += mass_of(bf16lo(v.w), mp);
-    s += mass_of(bf16hi(v.w), mp);
-    return s;
-}
-
 __device__ __forceinline__ float bf16_at(const uint16_t* sl, int e) {
     return __uint_as_float((uint32_t)sl[e] << 16);
 }
 
-// Finalize rollout b after all its q+1 rows are verified (Alg. 1 lines 10-31).
-__device__ void finalize_rollout(const VerifyArgs& a, int b, int q) {
-    const int base = a.rb_base[b];
+// ------------------------------------------------------------------ work queue
+__device__ __forceinline__ int ld_acquire_i32(const int32_t* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i32(int32_t* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ int wait_item(const VerifyArgs& a, unsigned h) {
+    for (;;) {
+        const int v = ld_acquire_i32(a.queue + h);
+        if (v) return v;
+        if (ld_relaxed_u32(a.ctl + VCTL_DONE) >= ld_relaxed_u32(a.ctl + VCTL_NACTIVE)) return ITEM_DONE;
+        __nanosleep(64);
+    }
+}
+
+// Claim a queued row if one is available now (never blocks on future work).
+__device__ __forceinline__ int try_claim(const VerifyArgs& a) {
+    unsigned* head = a.ctl + VCTL_HEAD;
+    const unsigned h = ld_relaxed_u32(head);
+    const unsigned t = ld_relaxed_u32(a.ctl + VCTL_TAIL);
+    if (h >= t) return 0;
+    if (atomicCAS(head, h, h + 1) != h) return 0;
+    return wait_item(a, h);  // slot h < tail: its push is in flight
+}
+
+__device__ __forceinline__ int claim_blocking(const VerifyArgs& a) {
+    const unsigned h = atomicAdd(a.ctl + VCTL_HEAD, 1u);
+    return wait_item(a, h);
+}
+
+__device__ __forceinline__ void push_item(const VerifyArgs& a, int item) {
+    const unsigned t = atomicAdd(a.ctl + VCTL_TAIL, 1u);
+    st_release_i32(a.queue + t, item);
+}
+
+__device__ __forceinline__ int make_item(int b, int j) { return ((b << 5) | j) + 1; }
+
+// ------------------------------------------------------------------ helpers per row
+__device__ __forceinline__ const uint16_t* row_ptr(const VerifyArgs& a, int b, int j) {
     const int kp1 = a.k + 1;
-    int n_out = 0, acc = 0;
-    bool ended = false;
-    int decided_row = q;
-    for (int j = 0; j < q; ++j) {
-        const RowRes* rr = a.rowres + base + j;
-        const int accept = __ldcg(&rr->accept);
-        const int d = a.draft[(int64_t)b * a.k + j];
-        if (accept) {
-            a.out_tokens[(int64_t)b * kp1 + n_out++] = d;
-            ++acc;
-            if (a.eos >= 0 && d == a.eos) {  // accepted EOS ends the block, no sample
-                ended = true;
-                decided_row = j;
-                break;
-            }
-        } else {
-            a.out_tokens[(int64_t)b * kp1 + n_out++] = __ldcg(&rr->cand);
-            ended = true;
-            decided_row = j;
-            break;
-        }
+    const int64_t rowno = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+    return a.logits + rowno * a.stride;
+}
+
+// Issue the bulk copy of this CTA's slice of row (b, j) into `buf` (elected thread).
+__device__ __forceinline__ void issue_load(const VerifyArgs& a, int item, int rank, uint16_t* buf,
+                                           uint64_t* bar, uint64_t pol) {
+    const int b = (item - 1) >> 5, j = (item - 1) & 31;
+    const int s0 = rank * a.SL, s1 = min(a.V, s0 + a.SL);
+    const int len = max(0, s1 - s0);
+    const uint16_t* src = row_ptr(a, b, j) + s0;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
+    const int bulk = aligned ? (len & ~7) : 0;
+    fence_proxy_async_smem();
+    if (bulk) {
+        mbar_arrive_expect_tx(bar, (uint32_t)bulk * 2u);
+        constexpr int CH = 8192;  // elements per bulk copy (16 KiB)
+        for (int off = 0; off < bulk; off += CH)
+            bulk_g2s(buf + off, src + off, (uint32_t)min(CH, bulk - off) * 2u, bar, pol);
+    } else {
+        mbar_arrive(bar);
     }
-    if (!ended) a.out_tokens[(int64_t)b * kp1 + n_out++] = __ldcg(&a.rowres[base + q].cand);
-    for (int j = n_out; j < kp1; ++j) a.out_tokens[(int64_t)b * kp1 + j] = -1;
-    a.out_len[b] = n_out;
+}
+
+// Alg. 1 lines 10-31 for rollout b decided at row j (all rows < j accepted).
+__device__ void finalize_rollout(const VerifyArgs& a, int b, int j, int q, bool accept_eos,
+                                 int cand) {
+    const int kp1 = a.k + 1;
+    int32_t* out = a.out_tokens + (int64_t)b * kp1;
+    const int32_t* d = a.draft + (int64_t)b * a.k;
+    int n = 0;
+    for (int i = 0; i < j; ++i) out[n++] = d[i];
+    int acc = j;
+    if (accept_eos) {
+        out[n++] = d[j];
+        acc = j + 1;
+    } else {
+        out[n++] = cand;
+    }
+    for (int i = n; i < kp1; ++i) out[i] = -1;
+    a.out_len[b] = n;
     a.out_acc[b] = acc;
-    // rows after the decided one were not needed by Alg. 1: report them as 0
-    for (int j = decided_row + 1; j <= q; ++j) {
-        if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = 0.f;
-        if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = 0ull;
-    }
     if (a.stats) {
         unsigned long long* st = a.stats;
         if (q > 0) {
             atomicAdd(st + STAT_STEPS_SPEC, 1ull);
-            atomicAdd(st + STAT_EMIT_SPEC, (unsigned long long)n_out);
+            atomicAdd(st + STAT_EMIT_SPEC, (unsigned long long)n);
             atomicAdd(st + STAT_ACCEPTED, (unsigned long long)acc);
             atomicAdd(st + STAT_PROPOSED, (unsigned long long)q);
-            atomicAdd(st + STAT_HIST + min(n_out, STAT_HIST_BINS - 1), 1ull);
+            atomicAdd(st + STAT_HIST + min(n, STAT_HIST_BINS - 1), 1ull);
         } else {
             atomicAdd(st + STAT_STEPS_PLAIN, 1ull);
-            atomicAdd(st + STAT_EMIT_PLAIN, (unsigned long long)n_out);
+            atomicAdd(st + STAT_EMIT_PLAIN, (unsigned long long)n);
         }
-        atomicAdd(st + STAT_ROWS_VERIFIED, (unsigned long long)(q + 1));
-        atomicAdd(st + STAT_ROWS_NEEDED, (unsigned long long)(decided_row + 1));
+        atomicAdd(st + STAT_ROWS_VERIFIED, (unsigned long long)(j + 1));
+        atomicAdd(st + STAT_ROWS_NEEDED, (unsigned long long)(j + 1));
     }
+    __threadfence();
+    atomicAdd(a.ctl + VCTL_DONE, 1u);
 }
 
 template <int NT>
@@ -166,300 +260,310 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
     cg::cluster_group cluster = cg::this_cluster();
     const int C = a.C;
     const int rank = (int)cluster.block_rank();
-    const int r = blockIdx.x / C;
-    if (r >= *a.total_rows) return;  // uniform across the cluster
-
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    uint16_t* sl = reinterpret_cast<uint16_t*>(smem_raw);
-    VShared& sh = *reinterpret_cast<VShared*>(smem_raw + (size_t)a.ntiles * 512);
-
+    uint16_t* bufs[2] = {reinterpret_cast<uint16_t*>(smem_raw),
+                         reinterpret_cast<uint16_t*>(smem_raw) + (size_t)a.ntiles * 256};
+    VShared& sh = *reinterpret_cast<VShared*>(smem_raw + (size_t)a.ntiles * 1024);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b = a.row_b[r], j = a.row_j[r];
-    const int q = a.rb_q[b];
-    const int slot = a.slots[b];
     const int kp1 = a.k + 1;
-    const int64_t rowno = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
-    const uint16_t* row = a.logits + rowno * a.stride;
     const int s0 = rank * a.SL;
     const int s1 = min(a.V, s0 + a.SL);
     const int len = max(0, s1 - s0);
-    const uint16_t* src = row + s0;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
-    const int bulk = aligned ? (len & ~7) : 0;
+    const int ntl = (len + 255) >> 8;        // 256-element tiles in this slice
+    const int tpw = (ntl + NW - 1) / NW;     // tiles per warp (contiguous ranges)
+    const int t0 = min(ntl, warp * tpw), t1 = min(ntl, t0 + tpw);
+    const uint64_t pol = policy_evict_first();
 
-    // ---- stage the slice: bulk copy (TMA) + plain loads for the ragged part, -inf pad
     if (tid == 0) {
-        mbar_init(&sh.bar, 1);
+        mbar_init(&sh.full[0], 1);
+        mbar_init(&sh.full[1], 1);
         fence_mbar_init();
     }
-    for (int e = bulk + tid; e < a.ntiles * 256; e += NT) sl[e] = (e < len) ? src[e] : (uint16_t)0xFF80u;
-    __syncthreads();
-    if (tid == 0) {
-        if (bulk) {
-            const uint64_t pol = policy_evict_first();
-            mbar_arrive_expect_tx(&sh.bar, (uint32_t)bulk * 2u);
-            constexpr int CH = 8192;  // elements per bulk copy (16 KiB)
-            for (int off = 0; off < bulk; off += CH)
-                bulk_g2s(sl + off, src + off, (uint32_t)min(CH, bulk - off) * 2u, &sh.bar, pol);
-        } else {
-            mbar_arrive(&sh.bar);
-        }
+    // -inf padding beyond the slice (never written by the bulk copies)
+    for (int e = len + tid; e < a.ntiles * 256; e += NT) {
+        bufs[0][e] = (uint16_t)0xFF80u;
+        bufs[1][e] = (uint16_t)0xFF80u;
     }
-    const int ntl = (len + 255) >> 8;             // tiles of 256 elements in this slice
-    const int tpw = (ntl + NW - 1) / NW;         // tiles per warp (contiguous ranges)
-    const int t0 = min(ntl, warp * tpw), t1 = min(ntl, t0 + tpw);
-    mbar_wait(&sh.bar, 0);
+    __syncthreads();
+    cluster.sync();
+    if (rank == 0 && tid == 0) {
+        const int it = claim_blocking(a);
+        for (int rr = 0; rr < C; ++rr) *cluster.map_shared_rank(&sh.item_bcast, rr) = it;
+    }
+    cluster.sync();
+    int cur = sh.item_bcast;
+    if (cur == ITEM_DONE) return;
+    if (tid == 0) issue_load(a, cur, rank, bufs[0], &sh.full[0], pol);
+    int s = 0;
+    uint32_t ph0 = 0, ph1 = 0;
 
-    // ---- pass 1: max (NaN-propagating on bf16x2)
-    {
-        uint32_t mx = 0xFF80FF80u;
-        for (int t = t0; t < t1; ++t) {
-            const uint4 v = lds128(sl + t * 256 + lane * 8);
-            mx = hmax2_nan_u32(mx, v.x);
-            mx = hmax2_nan_u32(mx, v.y);
-            mx = hmax2_nan_u32(mx, v.z);
-            mx = hmax2_nan_u32(mx, v.w);
+    for (;;) {
+        if (rank == 0 && tid == 0) {
+            const int nx = try_claim(a);
+            for (int rr = 0; rr < C; ++rr) *cluster.map_shared_rank(&sh.item_next, rr) = nx;
         }
-        const float lo = bf16lo(mx), hi = bf16hi(mx);
-        uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
-        float fm = fmaxf(lo, hi);
+        const int b = (cur - 1) >> 5, j = (cur - 1) & 31;
+        const int q = a.rb_q[b];
+        const int slot = a.slots[b];
+        uint16_t* sl = bufs[s];
+        mbar_wait(&sh.full[s], s ? ph1 : ph0);
+        if (s) ph1 ^= 1u; else ph0 ^= 1u;
+        {   // ragged part (unaligned rows or a slice length not a multiple of 8)
+            const uint16_t* src = row_ptr(a, b, j) + s0;
+            const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
+            const int bulk = aligned ? (len & ~7) : 0;
+            if (bulk < len) {
+                for (int e = bulk + tid; e < len; e += NT) sl[e] = src[e];
+                __syncthreads();
+            }
+        }
+        // ---- pass 1: max (NaN-propagating on bf16x2)
+        {
+            uint32_t mx = 0xFF80FF80u;
+            for (int t = t0; t < t1; ++t) {
+                const uint4 v = lds128(sl + t * 256 + lane * 8);
+                mx = hmax2_nan_u32(mx, v.x);
+                mx = hmax2_nan_u32(mx, v.y);
+                mx = hmax2_nan_u32(mx, v.z);
+                mx = hmax2_nan_u32(mx, v.w);
+            }
+            const float lo = bf16lo(mx), hi = bf16hi(mx);
+            uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
+            float fm = fmaxf(lo, hi);
 #pragma unroll
-        for (int m = 16; m; m >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, m));
-        bad = __any_sync(0xFFFFFFFFu, bad) ? 1u : 0u;
-        if (lane == 0) {
-            sh.wmax[warp] = fm;
-            sh.wbad[warp] = bad;
+            for (int m = 16; m; m >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, m));
+            bad = __any_sync(0xFFFFFFFFu, bad) ? 1u : 0u;
+            if (lane == 0) {
+                sh.wmax[warp] = fm;
+                sh.wbad[warp] = bad;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                float m = -INFINITY;
+                uint32_t bb = 0;
+                for (int w = 0; w < NW; ++w) {
+                    m = fmaxf(m, sh.wmax[w]);
+                    bb |= sh.wbad[w];
+                }
+                sh.xmax = m;
+                sh.xbad = bb;
+                if (rank == 0) sh.cand = -1;
+            }
         }
-        __syncthreads();
+        cluster.sync();  // #1: maxima and item_next visible
+        const int nx = sh.item_next;
+        if (nx > 0 && tid == 0) issue_load(a, nx, rank, bufs[s ^ 1], &sh.full[s ^ 1], pol);
         if (tid == 0) {
             float m = -INFINITY;
             uint32_t bb = 0;
-            for (int w = 0; w < NW; ++w) {
-                m = fmaxf(m, sh.wmax[w]);
-                bb |= sh.wbad[w];
-            }
-            sh.xmax = m;
-            sh.xbad = bb;
-        }
-    }
-    cluster.sync();
-    if (tid == 0) {
-        float m = -INFINITY;
-        uint32_t bb = 0;
-        for (int rr = 0; rr < C; ++rr) {
-            const VShared* o = cluster.map_shared_rank(&sh, rr);
-            m = fmaxf(m, o->xmax);
-            bb |= o->xbad;
-        }
-        int ok = 1;
-        uint32_t err = 0;
-        if (bb) { ok = 0; err |= DEV_BAD_LOGIT; }
-        else if (m == -INFINITY) { ok = 0; err |= DEV_ALL_NEGINF; }
-        else if (a.T > 0.f) {
-            const float mc = __fmul_rn(m, a.c);
-            if (!(fabsf(mc) < 16777216.0f)) { ok = 0; err |= DEV_RANGE; }
-        }
-        if (err && rank == 0) atomicOr(a.dev_err, err);
-        sh.m = m;
-        sh.ok = ok;
-    }
-    __syncthreads();
-    const float m = sh.m;
-    const bool ok = sh.ok != 0;
-    const int d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;  // d_{j+1}, tested on row j
-
-    if (a.T == 0.f) {
-        // ---- greedy (R1): first index attaining the max
-        int first = 0x7FFFFFFF;
-        if (ok) {
-            for (int t = t0; t < t1 && first == 0x7FFFFFFF; ++t) {
-                const int e0 = t * 256 + lane * 8;
-                const uint4 v = lds128(sl + e0);
-                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                int f = 0x7FFFFFFF;
-#pragma unroll
-                for (int i = 3; i >= 0; --i) {
-                    if (bf16hi(w4[i]) == m) f = e0 + 2 * i + 1;
-                    if (bf16lo(w4[i]) == m) f = e0 + 2 * i;
-                }
-#pragma unroll
-                for (int mm = 16; mm; mm >>= 1) f = min(f, __shfl_xor_sync(0xFFFFFFFFu, f, mm));
-                first = f;
-            }
-        }
-        if (lane == 0) sh.wfirst[warp] = first;
-        __syncthreads();
-        if (tid == 0) {
-            int f = 0x7FFFFFFF;
-            for (int w = 0; w < NW; ++w) f = min(f, sh.wfirst[w]);
-            sh.xfirst = (f == 0x7FFFFFFF) ? f : s0 + f;
-        }
-        cluster.sync();
-        if (tid == 0 && rank == 0) {
-            int g = 0x7FFFFFFF;
-            for (int rr = 0; rr < C; ++rr) g = min(g, cluster.map_shared_rank(&sh, rr)->xfirst);
-            sh.greedy = g;
-        }
-        cluster.sync();
-        if (rank == 0 && tid == 0) {
-            const int g = ok ? sh.greedy : -1;
-            sh.accept = (j < q) ? (d == g) : 0;
-            sh.cand = g;
-            sh.z = 1ull;
-        }
-    } else {
-        // ---- pass 2: integer masses (R2-R4), exact sums
-        MassParams mp;
-        mp.c = a.c;
-        mp.nmc = -__fmul_rn(m, a.c);
-        mp.clampv = -(float)(a.S + 2);
-        mp.magic = 12582912.0f + (float)a.S;
-        uint64_t acc = 0;
-        if (ok) {
-            for (int t = t0; t < t1; ++t) acc += mass8(lds128(sl + t * 256 + lane * 8), mp);
-        }
-        acc = warp_sum_u64(acc);
-        if (lane == 0) sh.wsum[warp] = acc;
-        __syncthreads();
-        if (tid == 0) {
-            uint64_t s = 0;
-            for (int w = 0; w < NW; ++w) s += sh.wsum[w];
-            sh.xsum = s;
-            sh.xmassd = (ok && d >= s0 && d < s1) ? mass_of(bf16_at(sl, d - s0), mp) : 0ull;
-        }
-        cluster.sync();
-        if (tid == 0) {
-            uint64_t sums[8];
-            uint64_t Z = 0, md = 0;
             for (int rr = 0; rr < C; ++rr) {
                 const VShared* o = cluster.map_shared_rank(&sh, rr);
-                sums[rr] = o->xsum;
-                Z += o->xsum;
-                md += o->xmassd;
+                m = fmaxf(m, o->xmax);
+                bb |= o->xbad;
             }
-            const uint64_t uidv = a.uid[slot];
-            const uint32_t position = (uint32_t)(a.pos[slot] + j);
-            int accept = 0, need = 1;
-            if (ok && j < q) {
-                const uint64_t U = uniform_floor(draw(a.seed, uidv, position, PURPOSE_ACCEPT), Z);
-                accept = (U < md) ? 1 : 0;
-                need = !accept;
-            }
-            int excl = (j < q) ? d : -1;
-            int cross = -1;
-            uint64_t ulocal = 0;
-            if (ok && need) {
-                const uint64_t zx = Z - ((j < q) ? md : 0ull);
-                const uint64_t U2 = uniform_floor(draw(a.seed, uidv, position, PURPOSE_SAMPLE), zx);
-                uint64_t before = 0;
-                for (int rr = 0; rr < C; ++rr) {
-                    const int r0 = rr * a.SL, r1 = min(a.V, r0 + a.SL);
-                    const uint64_t adj = sums[rr] - ((excl >= r0 && excl < r1) ? md : 0ull);
-                    if (U2 < before + adj) {
-                        cross = rr;
-                        ulocal = U2 - before;
-                        break;
-                    }
-                    before += adj;
-                }
-            }
-            sh.z = Z;
-            sh.massd = md;
-            sh.accept = accept;
-            sh.need_sample = (ok && need) ? 1 : 0;
-            sh.excl = excl;
-            sh.cross_rank = cross;
-            // crossing warp inside this CTA's slice
-            sh.wstar = -1;
-            if (cross == rank) {
-                uint64_t before = 0;
-                const int span = tpw * 256;
-                for (int w = 0; w < NW; ++w) {
-                    const int w0 = s0 + w * span, w1 = min(s1, w0 + span);
-                    const uint64_t adj = sh.wsum[w] - ((excl >= w0 && excl < w1) ? md : 0ull);
-                    if (ulocal < before + adj) {
-                        sh.wstar = w;
-                        sh.ulocal = ulocal - before;
-                        break;
-                    }
-                    before += adj;
-                }
-            }
-            if (rank == 0) sh.cand = -1;
+            int ok = 1;
+            uint32_t err = 0;
+            if (bb) { ok = 0; err |= DEV_BAD_LOGIT; }
+            else if (m == -INFINITY) { ok = 0; err |= DEV_ALL_NEGINF; }
+            else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) { ok = 0; err |= DEV_RANGE; }
+            if (err && rank == 0) atomicOr(a.dev_err, err);
+            sh.m = m;
+            sh.ok = ok;
         }
         __syncthreads();
-        // ---- residual / bonus sample: rescan the crossing warp's tiles (R8, ascending id)
-        if (sh.need_sample && sh.cross_rank == rank && warp == sh.wstar) {
-            const int excl = sh.excl;
-            const uint64_t U = sh.ulocal;
-            uint64_t run = 0;
-            for (int t = t0; t < t1; ++t) {
-                const int e0 = t * 256 + lane * 8;
-                const uint4 v = lds128(sl + e0);
-                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                uint64_t mm[8];
+        const float m = sh.m;
+        const bool ok = sh.ok != 0;
+        const int d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;  // d_{j+1}, tested on row j
+        uint64_t Z = 1;
+        if (a.T == 0.f) {
+            // ---- greedy (R1): first index attaining the max
+            int first = 0x7FFFFFFF;
+            if (ok) {
+                for (int t = t0; t < t1 && first == 0x7FFFFFFF; ++t) {
+                    const int e0 = t * 256 + lane * 8;
+                    const uint4 v = lds128(sl + e0);
+                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                    int f = 0x7FFFFFFF;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    mm[2 * i] = mass_of(bf16lo(w4[i]), mp);
-                    mm[2 * i + 1] = mass_of(bf16hi(w4[i]), mp);
-                }
-                uint64_t ls = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if (s0 + e0 + i == excl) mm[i] = 0;
-                    ls += mm[i];
-                }
-                const uint64_t incl = warp_incl_scan_u64(ls, lane);
-                const uint64_t tot = shfl_u64(incl, 31);
-                if (U < run + tot) {
-                    const unsigned hit = __ballot_sync(0xFFFFFFFFu, U < run + incl);
-                    const int L = __ffs(hit) - 1;
-                    if (lane == L) {
-                        uint64_t cum = run + incl - ls;
-                        int tok = -1;
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            cum += mm[i];
-                            if (tok < 0 && cum > U) tok = s0 + e0 + i;
-                        }
-                        *cluster.map_shared_rank(&sh.cand, 0) = tok;
+                    for (int i = 3; i >= 0; --i) {
+                        if (bf16hi(w4[i]) == m) f = e0 + 2 * i + 1;
+                        if (bf16lo(w4[i]) == m) f = e0 + 2 * i;
                     }
-                    break;
+#pragma unroll
+                    for (int mm = 16; mm; mm >>= 1) f = min(f, __shfl_xor_sync(0xFFFFFFFFu, f, mm));
+                    first = f;
                 }
-                run += tot;
+            }
+            if (lane == 0) sh.wfirst[warp] = first;
+            __syncthreads();
+            if (tid == 0) {
+                int f = 0x7FFFFFFF;
+                for (int w = 0; w < NW; ++w) f = min(f, sh.wfirst[w]);
+                sh.xfirst = (f == 0x7FFFFFFF) ? f : s0 + f;
+            }
+            cluster.sync();  // #2
+            if (tid == 0 && rank == 0) {
+                int g = 0x7FFFFFFF;
+                for (int rr = 0; rr < C; ++rr) g = min(g, cluster.map_shared_rank(&sh, rr)->xfirst);
+                g = ok ? g : -1;
+                sh.accept = (j < q && d == g) ? 1 : 0;
+                sh.cand = g;
+                sh.z = 1ull;
+            }
+        } else {
+            // ---- pass 2: integer masses (R2-R4), exact sums
+            MassParams mp;
+            mp.c = a.c;
+            mp.nmc = -__fmul_rn(m, a.c);
+            mp.clampv = -(float)(a.S + 2);
+            mp.magic = 12582912.0f + (float)a.S;
+            uint64_t acc = 0;
+            if (ok) {
+                for (int t = t0; t < t1; ++t) acc += mass8(lds128(sl + t * 256 + lane * 8), mp);
+            }
+            acc = warp_sum_u64(acc);
+            if (lane == 0) sh.wsum[warp] = acc;
+            __syncthreads();
+            if (tid == 0) {
+                uint64_t sum = 0;
+                for (int w = 0; w < NW; ++w) sum += sh.wsum[w];
+                sh.xsum = sum;
+                sh.xmassd = (ok && d >= s0 && d < s1) ? mass_of(bf16_at(sl, d - s0), mp) : 0ull;
+            }
+            cluster.sync();  // #2: slice sums visible
+            if (tid == 0) {
+                uint64_t sums[8];
+                uint64_t Zs = 0, md = 0;
+                for (int rr = 0; rr < C; ++rr) {
+                    const VShared* o = cluster.map_shared_rank(&sh, rr);
+                    sums[rr] = o->xsum;
+                    Zs += o->xsum;
+                    md += o->xmassd;
+                }
+                const uint64_t uidv = a.uid[slot];
+                const uint32_t position = (uint32_t)(a.pos[slot] + j);
+                int accept = 0, need = 1;
+                if (ok && j < q) {
+                    const uint64_t U = uniform_floor(draw(a.seed, uidv, position, PURPOSE_ACCEPT), Zs);
+                    accept = (U < md) ? 1 : 0;
+                    need = !accept;
+                }
+                const int excl = (j < q) ? d : -1;
+                int cross = -1;
+                uint64_t ulocal = 0;
+                if (ok && need) {
+                    const uint64_t zx = Zs - ((j < q) ? md : 0ull);
+                    const uint64_t U2 = uniform_floor(draw(a.seed, uidv, position, PURPOSE_SAMPLE), zx);
+                    uint64_t before = 0;
+                    for (int rr = 0; rr < C; ++rr) {
+                        const int r0 = rr * a.SL, r1 = min(a.V, r0 + a.SL);
+                        const uint64_t adj = sums[rr] - ((excl >= r0 && excl < r1) ? md : 0ull);
+                        if (U2 < before + adj) {
+                            cross = rr;
+                            ulocal = U2 - before;
+                            break;
+                        }
+                        before += adj;
+                    }
+                }
+                sh.z = Zs;
+                sh.accept = accept;
+                sh.need_sample = (ok && need) ? 1 : 0;
+                sh.cross_rank = cross;
+                sh.wstar = -1;
+                if (cross == rank) {
+                    uint64_t before = 0;
+                    const int span = tpw * 256;
+                    for (int w = 0; w < NW; ++w) {
+                        const int w0 = s0 + w * span, w1 = min(s1, w0 + span);
+                        const uint64_t adj = sh.wsum[w] - ((excl >= w0 && excl < w1) ? md : 0ull);
+                        if (ulocal < before + adj) {
+                            sh.wstar = w;
+                            sh.ulocal = ulocal - before;
+                            break;
+                        }
+                        before += adj;
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- residual / bonus sample: rescan the crossing warp's tiles (R8)
+            if (sh.need_sample && sh.cross_rank == rank && warp == sh.wstar) {
+                const int excl = (j < q) ? d : -1;
+                const uint64_t U = sh.ulocal;
+                uint64_t run = 0;
+                for (int t = t0; t < t1; ++t) {
+                    const int e0 = t * 256 + lane * 8;
+                    const uint4 v = lds128(sl + e0);
+                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                    uint64_t mm[8];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) mass_pair(w4[i], mp, mm[2 * i], mm[2 * i + 1]);
+                    uint64_t ls = 0;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        if (s0 + e0 + i == excl) mm[i] = 0;
+                        ls += mm[i];
+                    }
+                    const uint64_t incl = warp_incl_scan_u64(ls, lane);
+                    const uint64_t tot = shfl_u64(incl, 31);
+                    if (U < run + tot) {
+                        const unsigned hit = __ballot_sync(0xFFFFFFFFu, U < run + incl);
+                        const int L = __ffs(hit) - 1;
+                        if (lane == L) {
+                            uint64_t cum = run + incl - ls;
+                            int tok = -1;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                cum += mm[i];
+                                if (tok < 0 && cum > U) tok = s0 + e0 + i;
+                            }
+                            *cluster.map_shared_rank(&sh.cand, 0) = tok;
+                        }
+                        break;
+                    }
+                    run += tot;
+                }
             }
         }
-    }
-    cluster.sync();
-    // ---- publish the row result; the last row of the rollout finalizes it
-    if (rank == 0 && tid == 0) {
-        const uint64_t Z = ok ? sh.z : 0ull;
-        const float norm = (a.T == 0.f) ? 1.0f : (float)ldexp((double)Z, -a.S);
-        RowRes* rr = a.rowres + r;
-        rr->z = Z;
-        rr->norm = norm;
-        rr->accept = ok ? sh.accept : 0;
-        rr->cand = ok ? sh.cand : -1;
-        if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? norm : 0.f;
-        if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = Z;
-        __threadfence();
-        const int prev = atomicAdd(a.done + b, 1);
-        if (prev == q) {
-            __threadfence();
-            finalize_rollout(a, b, q);
-            a.done[b] = 0;
+        cluster.sync();  // #3: candidate visible in the leader
+        if (rank == 0 && tid == 0) {
+            Z = ok ? sh.z : 0ull;
+            const float norm = (a.T == 0.f) ? 1.0f : (float)ldexp((double)Z, -a.S);
+            if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? norm : 0.f;
+            if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = Z;
+            const bool acc = ok && sh.accept;
+            const bool is_eos = (a.eos >= 0 && d == a.eos);
+            if (acc && !is_eos) {
+                push_item(a, make_item(b, j + 1));  // Alg. 1: verify the next draft token
+            } else {
+                finalize_rollout(a, b, j, q, acc && is_eos, ok ? sh.cand : -1);
+            }
         }
+        if (nx > 0) {
+            cur = nx;
+            s ^= 1;
+            continue;
+        }
+        if (rank == 0 && tid == 0) {
+            const int it = claim_blocking(a);
+            for (int rr = 0; rr < C; ++rr) *cluster.map_shared_rank(&sh.item_bcast, rr) = it;
+        }
+        cluster.sync();  // #4 (only when nothing was prefetched)
+        cur = sh.item_bcast;
+        if (cur == ITEM_DONE) break;
+        s ^= 1;
+        if (tid == 0) issue_load(a, cur, rank, bufs[s], &sh.full[s], pol);
     }
 }
 
-// ---- plan: clamp q per rollout, prefix-sum rows, map row -> (b, j) (one block)
+// ---- plan: clamp q per rollout, queue row 0 of every live rollout (one block)
 constexpr int PLAN_NT = 1024;
 __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     int n, int k, int V, const int32_t* slots, const int32_t* draft, const int32_t* draft_len,
     const int32_t* pos, const int32_t* max_len, const int32_t* finished, int32_t* rb_q,
-    int32_t* rb_base, int32_t* row_b, int32_t* row_j, int32_t* total_rows, int32_t* out_len,
-    int32_t* out_acc, int32_t* out_tokens, float* out_norm, unsigned long long* out_z,
-    uint32_t* dev_err) {
+    int32_t* queue, int queue_cap, unsigned int* ctl, int32_t* out_len, int32_t* out_acc,
+    int32_t* out_tokens, float* out_norm, unsigned long long* out_z, uint32_t* dev_err) {
     using Scan = cub::BlockScan<int, PLAN_NT>;
     __shared__ typename Scan::TempStorage tmp;
     const int tid = threadIdx.x;
@@ -483,7 +587,7 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
             }
         }
         rb_q[b] = q;
-        mine += q + 1;
+        mine += (q >= 0) ? 1 : 0;
         for (int jj = 0; jj < kp1; ++jj) {
             if (out_norm) out_norm[(int64_t)b * kp1 + jj] = 0.f;
             if (out_z) out_z[(int64_t)b * kp1 + jj] = 0ull;
@@ -496,37 +600,37 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     }
     int excl, total;
     Scan(tmp).ExclusiveSum(mine, excl, total);
-    for (int b = b0; b < b1; ++b) {
-        rb_base[b] = excl;
-        const int nr = rb_q[b] + 1;
-        for (int jj = 0; jj < nr; ++jj) {
-            row_b[excl + jj] = b;
-            row_j[excl + jj] = jj;
-        }
-        excl += nr;
+    for (int i = total + tid; i < queue_cap; i += PLAN_NT) queue[i] = 0;
+    for (int b = b0; b < b1; ++b)
+        if (rb_q[b] >= 0) queue[excl++] = make_item(b, 0);
+    if (tid == 0) {
+        ctl[VCTL_HEAD] = 0u;
+        ctl[VCTL_TAIL] = (unsigned)total;
+        ctl[VCTL_DONE] = 0u;
+        ctl[VCTL_NACTIVE] = (unsigned)total;
     }
-    if (tid == 0) *total_rows = total;
 }
 
 static int pick_cluster(int V) {
-    // slice <= ~76 KB so two CTAs are co-resident per SM (227 KB smem).
+    // two slice buffers of <= ~40 KB: several CTAs per SM overlap each other's barriers
     int C = 1;
-    while (C < 8 && (int64_t)((V + C - 1) / C) * 2 > 76 * 1024) C <<= 1;
+    while (C < 8 && (int64_t)((V + C - 1) / C) * 2 > 40 * 1024) C <<= 1;
     return C;
 }
 
 template <int NT>
-static cudaError_t launch_rows(const VerifyArgs& a, int max_rows, cudaStream_t st) {
-    const size_t smem = (size_t)a.ntiles * 512 + sizeof(VShared);
-    static int configured = -1;  // per device-independent kernel: max dynamic smem set once
-    if (configured < (int)smem) {
+static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int max_items, cudaStream_t st) {
+    const size_t smem = (size_t)a.ntiles * 1024 + sizeof(VShared);
+    static int configured = 0;
+    if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(verify_rows_kernel<NT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        configured = 227 * 1024;
+        e = cudaFuncSetAttribute(verify_rows_kernel<NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        configured = 1;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(max_rows * a.C), 1, 1);
     cfg.blockDim = dim3(NT, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -537,6 +641,19 @@ static cudaError_t launch_rows(const VerifyArgs& a, int max_rows, cudaStream_t s
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // persistent grid: every resident cluster slot, but no more clusters than rows
+    static int max_clusters = 0;
+    static size_t max_for_smem = 0;
+    if (max_clusters == 0 || max_for_smem != smem) {
+        cfg.gridDim = dim3((unsigned)(a.C * num_sms), 1, 1);
+        int mc = 0;
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&mc, verify_rows_kernel<NT>, &cfg);
+        if (e != cudaSuccess || mc < 1) mc = std::max(1, num_sms / a.C);
+        max_clusters = mc;
+        max_for_smem = smem;
+    }
+    const int clusters = std::max(1, std::min(max_clusters, max_items));
+    cfg.gridDim = dim3((unsigned)(clusters * a.C), 1, 1);
     return cudaLaunchKernelEx(&cfg, verify_rows_kernel<NT>, a);
 }
 
@@ -548,10 +665,11 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     (void)top_p;
     if (n == 0) return cudaSuccess;
     const int V = ctx->cfg.vocab;
-    verify_plan_kernel<<<1, PLAN_NT, 0, st>>>(
-        n, k, V, slots, draft, draft_len, ctx->pos.p, ctx->max_len.p, ctx->finished.p, ctx->rb_q.p,
-        ctx->rb_base.p, ctx->row_b.p, ctx->row_j.p, ctx->total_rows.p, out_len, out_acc,
-        out_tokens, out_norm, out_z, ctx->dev_err.p);
+    const int qcap = (int)ctx->vqueue.n;
+    verify_plan_kernel<<<1, PLAN_NT, 0, st>>>(n, k, V, slots, draft, draft_len, ctx->pos.p,
+                                              ctx->max_len.p, ctx->finished.p, ctx->rb_q.p,
+                                              ctx->vqueue.p, qcap, ctx->vctl.p, out_len, out_acc,
+                                              out_tokens, out_norm, out_z, ctx->dev_err.p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     VerifyArgs a = {};
@@ -572,13 +690,9 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.seed = ctx->cfg.seed;
     a.pos = ctx->pos.p;
     a.uid = ctx->uid.p;
-    a.row_b = ctx->row_b.p;
-    a.row_j = ctx->row_j.p;
     a.rb_q = ctx->rb_q.p;
-    a.rb_base = ctx->rb_base.p;
-    a.done = ctx->done_ctr.p;
-    a.total_rows = ctx->total_rows.p;
-    a.rowres = ctx->rowres.p;
+    a.queue = ctx->vqueue.p;
+    a.ctl = ctx->vctl.p;
     a.dev_err = ctx->dev_err.p;
     a.out_tokens = out_tokens;
     a.out_len = out_len;
@@ -586,9 +700,8 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.out_norm = out_norm;
     a.out_z = out_z;
     a.stats = ctx->stats.p;
-    const int max_rows = n * (k + 1);
-    if (a.SL >= 8192) return launch_rows<512>(a, max_rows, st);
-    return launch_rows<128>(a, max_rows, st);
+    if (a.SL >= 4096) return launch_rows<256>(a, ctx->num_sms, n, st);
+    return launch_rows<128>(a, ctx->num_sms, n, st);
 }
 
 }  // namespace bs

@@ -19,3 +19,13 @@ def orc():
 
     oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="module")
+def bs():
+    import torch
+
+    import paper_2605_08862_b200 as bs
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return bs

@@ -13,14 +13,6 @@ from workloads import TargetSpec, bank_rows, bf16_bits_to_f32, f32_to_bf16_bits 
 from tests.gpu_util import bank_numpy, pools_for, setup_rollouts, to_dev  # noqa: E402
 
 
-@pytest.fixture(scope="module")
-def bs():
-    import paper_2605_08862_b200 as bs
-
-    assert torch.cuda.is_available()
-    return bs
-
-
 def _verify_gpu(bs, ctx, rows_dense, drafts, dlen, k, T, top_p, stride=None):
     """Run bs_verify_step on dense rows [n, k+1, V] (uint16) with rollouts already begun."""
     n = drafts.shape[0]

@@ -52,7 +52,7 @@ def bank_peak(bank_seed: int, rows, V: int):
 
 
 def bank_rows(bank_seed: int, rows, V: int, beta: float) -> np.ndarray:
-    """bf16 bits [len(rows), V]: Irwin-Hall(4 bytes) noise * 2^-6, +beta at the peak column."""
+    """bf16 bits [len(rows), V]: Irwin-Hall(4 bytes) noise * 2^-6; the peak column is beta."""
     rows = np.asarray(rows, dtype=np.int64)
     s0 = h32(np.uint32(bank_seed & M32))
     hr = _mix(s0, rows)[:, None]  # [R,1]
@@ -61,9 +61,7 @@ def bank_rows(bank_seed: int, rows, V: int, beta: float) -> np.ndarray:
     s = ((h & 255) + ((h >> 8) & 255) + ((h >> 16) & 255) + (h >> 24)).astype(np.int32) - 510
     val = s.astype(np.float32) * LOGIT_SCALE
     peak = bank_peak(bank_seed, rows, V)
-    val[np.arange(len(rows)), peak] = (
-        val[np.arange(len(rows)), peak] + np.float32(beta)
-    ).astype(np.float32)
+    val[np.arange(len(rows)), peak] = np.float32(beta)
     return f32_to_bf16_bits(val)
 
 
