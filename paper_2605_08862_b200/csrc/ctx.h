@@ -25,8 +25,8 @@ enum : int {
     STAT_COUNT = STAT_HIST + STAT_HIST_BINS
 };
 
-// Control words of the verify kernel's row work queue.
-enum : int { VCTL_HEAD = 0, VCTL_TAIL = 1, VCTL_DONE = 2, VCTL_NACTIVE = 3, VCTL_WORDS = 4 };
+// Control words of the verify kernel: next rollout to claim, number of live rollouts.
+enum : int { VCTL_NEXT = 0, VCTL_NACTIVE = 1, VCTL_WORDS = 4 };
 
 template <typename T>
 struct DevBuf {

@@ -1,20 +1,22 @@
 // verify.cu — fused vocab-row verify + resample (Eq. 2, Eq. 3 P:208-210,
 // Alg. 1, bonus token P:308) for sm_100a.
 //
-// Kernel K3: a PERSISTENT grid of thread-block clusters pulling logits
-// rows from a device work queue in Alg. 1's order.  Row (b, 0) of every live rollout is
-// queued first; row (b, j+1) is queued only when row j accepted d_{j+1} (lazy dataflow:
-// rows after the first rejection are never read).  Per row, a cluster of C CTAs
-// owns the vocabulary, CTA `rank` the slice [rank*SL, (rank+1)*SL):
-//   * an elected thread stages the slice with 1-D bulk async copies (TMA engine,
-//     mbarrier completion, L2 evict-first); the NEXT claimed row is prefetched into the
-//     second smem buffer while the current row is computed;
-//   * pass 1: NaN-propagating bf16x2 max -> cluster max over DSMEM;
-//   * pass 2: integer masses of reading R with packed FFMA2/FADD2, exact u64 sums ->
-//     slice sums over DSMEM -> Z, mass(d) -> accept (Philox counter (pos+j, ACCEPT));
+// Kernel K3.  A PERSISTENT grid of thread-block clusters; a cluster of C
+// CTAs owns one logits row at a time, CTA `rank` the vocabulary slice
+// [rank*SL, (rank+1)*SL).  Work is claimed per ROLLOUT (one atomic each) and a rollout's
+// rows are verified in Alg. 1's order, lazily: row j+1 is read only if row j accepted
+// d_{j+1} (rows after the first rejection are never read).  Each cluster keeps two
+// rollouts in flight and alternates between them, so while one row is computed the next
+// row of the other rollout streams in (1-D bulk async copies on the TMA engine, mbarrier
+// completion, L2 evict-first) — the dependency chain of one rollout never stalls the SM.
+// Per row:
+//   * pass 1: NaN-propagating bf16x2 max; every CTA pushes its slice max into all CTAs'
+//     shared memory (DSMEM stores) -> cluster barrier -> row max;
+//   * pass 2: integer masses of reading R with packed FFMA2/FADD2, exact u64 sums; slice
+//     sums and mass(d) pushed over DSMEM -> cluster barrier -> Z, accept (Philox counter
+//     (pos+j, ACCEPT), drawn while the row streams in);
 //   * a residual / bonus sample only when needed: the CTA holding the CDF crossing
-//     rescans the crossing warp's 256-element tiles;
-//   * the leader then either queues row j+1 or finalizes the rollout (emitted tokens).
+//     rescans the crossing warp's 256-element tiles and finalizes the rollout itself.
 #include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
@@ -26,7 +28,7 @@ namespace cg = cooperative_groups;
 
 namespace bs {
 
-constexpr int ITEM_DONE = -1;
+constexpr int MAXC = 8;  // max cluster size
 
 struct VerifyArgs {
     const int32_t* slots;
@@ -40,8 +42,8 @@ struct VerifyArgs {
     const int32_t* pos;
     const unsigned long long* uid;
     const int32_t* rb_q;
-    int32_t* queue;
-    unsigned int* ctl;  // VCTL_* words
+    const int32_t* active;  // compacted live rollouts (plan kernel)
+    unsigned int* ctl;      // VCTL_* words
     uint32_t* dev_err;
     int32_t* out_tokens;
     int32_t* out_len;
@@ -52,22 +54,20 @@ struct VerifyArgs {
 };
 
 struct __align__(16) VShared {
-    uint64_t full[2];  // TMA completion barriers, one per slice buffer
-    // exchanged over DSMEM
-    float xmax;
-    uint32_t xbad;
-    int32_t xfirst;
-    int32_t cand;         // written remotely into the leader (rank 0)
-    int32_t item_next;    // broadcast by the leader: prefetched next row (0 = none)
-    int32_t item_bcast;   // broadcast by the leader: blocking-claimed next row
-    unsigned long long xsum;
-    unsigned long long xmassd;
+    uint64_t full[2];  // TMA completion barrier per slot buffer
+    // written remotely by every CTA of the cluster (index = source rank)
+    float xmax[MAXC];
+    uint32_t xbad[MAXC];
+    int32_t xfirst[MAXC];
+    unsigned long long xsum[MAXC];
+    unsigned long long xmassd[MAXC];
+    int32_t spare;  // claimed-ahead rollout index (written by the leader into all CTAs)
     // CTA-local
     float wmax[32];
     uint32_t wbad[32];
     int32_t wfirst[32];
     unsigned long long wsum[32];
-    // broadcast decisions
+    uint32_t racc[4], rsmp[4];  // Philox draws of the current row
     float m;
     int32_t ok;
     int32_t accept;
@@ -78,6 +78,7 @@ struct __align__(16) VShared {
     int32_t pad;
     unsigned long long z;
     unsigned long long ulocal;
+    unsigned long long stat[STAT_COUNT];
 };
 
 // ------------------------------------------------------------------ packed fp32 math
@@ -144,52 +145,6 @@ __device__ __forceinline__ float bf16_at(const uint16_t* sl, int e) {
     return __uint_as_float((uint32_t)sl[e] << 16);
 }
 
-// ------------------------------------------------------------------ work queue
-__device__ __forceinline__ int ld_acquire_i32(const int32_t* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_i32(int32_t* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ int wait_item(const VerifyArgs& a, unsigned h) {
-    for (;;) {
-        const int v = ld_acquire_i32(a.queue + h);
-        if (v) return v;
-        if (ld_relaxed_u32(a.ctl + VCTL_DONE) >= ld_relaxed_u32(a.ctl + VCTL_NACTIVE)) return ITEM_DONE;
-        __nanosleep(64);
-    }
-}
-
-// Claim a queued row if one is available now (never blocks on future work).
-__device__ __forceinline__ int try_claim(const VerifyArgs& a) {
-    unsigned* head = a.ctl + VCTL_HEAD;
-    const unsigned h = ld_relaxed_u32(head);
-    const unsigned t = ld_relaxed_u32(a.ctl + VCTL_TAIL);
-    if (h >= t) return 0;
-    if (atomicCAS(head, h, h + 1) != h) return 0;
-    return wait_item(a, h);  // slot h < tail: its push is in flight
-}
-
-__device__ __forceinline__ int claim_blocking(const VerifyArgs& a) {
-    const unsigned h = atomicAdd(a.ctl + VCTL_HEAD, 1u);
-    return wait_item(a, h);
-}
-
-__device__ __forceinline__ void push_item(const VerifyArgs& a, int item) {
-    const unsigned t = atomicAdd(a.ctl + VCTL_TAIL, 1u);
-    st_release_i32(a.queue + t, item);
-}
-
-__device__ __forceinline__ int make_item(int b, int j) { return ((b << 5) | j) + 1; }
-
 // ------------------------------------------------------------------ helpers per row
 __device__ __forceinline__ const uint16_t* row_ptr(const VerifyArgs& a, int b, int j) {
     const int kp1 = a.k + 1;
@@ -198,9 +153,8 @@ __device__ __forceinline__ const uint16_t* row_ptr(const VerifyArgs& a, int b, i
 }
 
 // Issue the bulk copy of this CTA's slice of row (b, j) into `buf` (elected thread).
-__device__ __forceinline__ void issue_load(const VerifyArgs& a, int item, int rank, uint16_t* buf,
-                                           uint64_t* bar, uint64_t pol) {
-    const int b = (item - 1) >> 5, j = (item - 1) & 31;
+__device__ __forceinline__ void issue_load(const VerifyArgs& a, int b, int j, int rank,
+                                           uint16_t* buf, uint64_t* bar, uint64_t pol) {
     const int s0 = rank * a.SL, s1 = min(a.V, s0 + a.SL);
     const int len = max(0, s1 - s0);
     const uint16_t* src = row_ptr(a, b, j) + s0;
@@ -218,8 +172,8 @@ __device__ __forceinline__ void issue_load(const VerifyArgs& a, int item, int ra
 }
 
 // Alg. 1 lines 10-31 for rollout b decided at row j (all rows < j accepted).
-__device__ void finalize_rollout(const VerifyArgs& a, int b, int j, int q, bool accept_eos,
-                                 int cand) {
+__device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int j, int q,
+                                 bool accept_eos, int cand) {
     const int kp1 = a.k + 1;
     int32_t* out = a.out_tokens + (int64_t)b * kp1;
     const int32_t* d = a.draft + (int64_t)b * a.k;
@@ -235,8 +189,8 @@ __device__ void finalize_rollout(const VerifyArgs& a, int b, int j, int q, bool 
     for (int i = n; i < kp1; ++i) out[i] = -1;
     a.out_len[b] = n;
     a.out_acc[b] = acc;
-    if (a.stats) {
-        unsigned long long* st = a.stats;
+    if (a.stats) {  // CTA-local counters, flushed once at kernel exit
+        unsigned long long* st = sh.stat;
         if (q > 0) {
             atomicAdd(st + STAT_STEPS_SPEC, 1ull);
             atomicAdd(st + STAT_EMIT_SPEC, (unsigned long long)n);
@@ -250,8 +204,6 @@ __device__ void finalize_rollout(const VerifyArgs& a, int b, int j, int q, bool 
         atomicAdd(st + STAT_ROWS_VERIFIED, (unsigned long long)(j + 1));
         atomicAdd(st + STAT_ROWS_NEEDED, (unsigned long long)(j + 1));
     }
-    __threadfence();
-    atomicAdd(a.ctl + VCTL_DONE, 1u);
 }
 
 template <int NT>
@@ -273,41 +225,66 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
     const int tpw = (ntl + NW - 1) / NW;     // tiles per warp (contiguous ranges)
     const int t0 = min(ntl, warp * tpw), t1 = min(ntl, t0 + tpw);
     const uint64_t pol = policy_evict_first();
+    const int nact = (int)a.ctl[VCTL_NACTIVE];
 
     if (tid == 0) {
         mbar_init(&sh.full[0], 1);
         mbar_init(&sh.full[1], 1);
         fence_mbar_init();
     }
+    for (int i = tid; i < STAT_COUNT; i += NT) sh.stat[i] = 0ull;
     // -inf padding beyond the slice (never written by the bulk copies)
     for (int e = len + tid; e < a.ntiles * 256; e += NT) {
         bufs[0][e] = (uint16_t)0xFF80u;
         bufs[1][e] = (uint16_t)0xFF80u;
     }
+    if (rank == 0 && tid == 0) {  // claim two rollouts + one spare
+        const int base = (int)atomicAdd(a.ctl + VCTL_NEXT, 3u);
+        for (int rr = 0; rr < C; ++rr) {
+            VShared* o = cluster.map_shared_rank(&sh, rr);
+            o->xfirst[0] = base;  // scratch for the broadcast below
+        }
+    }
     __syncthreads();
     cluster.sync();
-    if (rank == 0 && tid == 0) {
-        const int it = claim_blocking(a);
-        for (int rr = 0; rr < C; ++rr) *cluster.map_shared_rank(&sh.item_bcast, rr) = it;
+    const int base0 = sh.xfirst[0];
+    int rb[2], rj[2];  // rollout (index into active[], -1 = empty) and row of each slot
+    rb[0] = (base0 < nact) ? base0 : -1;
+    rb[1] = (base0 + 1 < nact) ? base0 + 1 : -1;
+    int spare = (base0 + 2 < nact) ? base0 + 2 : -1;
+    bool exhausted = (base0 + 2 >= nact - 1);
+    rj[0] = rj[1] = 0;
+    if (tid == 0) {
+        for (int sl = 0; sl < 2; ++sl)
+            if (rb[sl] >= 0) issue_load(a, a.active[rb[sl]], 0, rank, bufs[sl], &sh.full[sl], pol);
     }
-    cluster.sync();
-    int cur = sh.item_bcast;
-    if (cur == ITEM_DONE) return;
-    if (tid == 0) issue_load(a, cur, rank, bufs[0], &sh.full[0], pol);
-    int s = 0;
-    uint32_t ph0 = 0, ph1 = 0;
+    uint32_t ph[2] = {0u, 0u};
+    int cur = 0;
+    if (rb[0] < 0) cur = 1;
 
-    for (;;) {
-        if (rank == 0 && tid == 0) {
-            const int nx = try_claim(a);
-            for (int rr = 0; rr < C; ++rr) *cluster.map_shared_rank(&sh.item_next, rr) = nx;
-        }
-        const int b = (cur - 1) >> 5, j = (cur - 1) & 31;
+    while (rb[0] >= 0 || rb[1] >= 0) {
+        if (rb[cur] < 0) cur ^= 1;
+        const int b = a.active[rb[cur]];
+        const int j = rj[cur];
         const int q = a.rb_q[b];
         const int slot = a.slots[b];
-        uint16_t* sl = bufs[s];
-        mbar_wait(&sh.full[s], s ? ph1 : ph0);
-        if (s) ph1 ^= 1u; else ph0 ^= 1u;
+        uint16_t* sl = bufs[cur];
+        const int d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;  // d_{j+1}, tested on row j
+        // leader claims the next spare early; the atomic's latency overlaps pass 1
+        int claimed = -1;
+        const bool want_spare = (rank == 0 && tid == 0 && spare < 0 && !exhausted);
+        if (want_spare) claimed = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
+        // the row's two Philox draws, while the slice streams in
+        if (tid == 32) {
+            const uint64_t uidv = a.uid[slot];
+            const uint32_t position = (uint32_t)(a.pos[slot] + j);
+            const U128 r1 = draw(a.seed, uidv, position, PURPOSE_ACCEPT);
+            const U128 r2 = draw(a.seed, uidv, position, PURPOSE_SAMPLE);
+            sh.racc[0] = r1.x0; sh.racc[1] = r1.x1; sh.racc[2] = r1.x2; sh.racc[3] = r1.x3;
+            sh.rsmp[0] = r2.x0; sh.rsmp[1] = r2.x1; sh.rsmp[2] = r2.x2; sh.rsmp[3] = r2.x3;
+        }
+        mbar_wait(&sh.full[cur], ph[cur]);
+        ph[cur] ^= 1u;
         {   // ragged part (unaligned rows or a slice length not a multiple of 8)
             const uint16_t* src = row_ptr(a, b, j) + s0;
             const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
@@ -331,35 +308,35 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
             uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
             float fm = fmaxf(lo, hi);
 #pragma unroll
-            for (int m = 16; m; m >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, m));
+            for (int mm = 16; mm; mm >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, mm));
             bad = __any_sync(0xFFFFFFFFu, bad) ? 1u : 0u;
             if (lane == 0) {
                 sh.wmax[warp] = fm;
                 sh.wbad[warp] = bad;
             }
             __syncthreads();
-            if (tid == 0) {
-                float m = -INFINITY;
+            if (tid < C) {  // push this slice's max into CTA `tid`
+                float mloc = -INFINITY;
                 uint32_t bb = 0;
                 for (int w = 0; w < NW; ++w) {
-                    m = fmaxf(m, sh.wmax[w]);
+                    mloc = fmaxf(mloc, sh.wmax[w]);
                     bb |= sh.wbad[w];
                 }
-                sh.xmax = m;
-                sh.xbad = bb;
-                if (rank == 0) sh.cand = -1;
+                VShared* o = cluster.map_shared_rank(&sh, tid);
+                o->xmax[rank] = mloc;
+                o->xbad[rank] = bb;
+            }
+            if (want_spare) {
+                for (int rr = 0; rr < C; ++rr) cluster.map_shared_rank(&sh, rr)->spare = claimed;
             }
         }
-        cluster.sync();  // #1: maxima and item_next visible
-        const int nx = sh.item_next;
-        if (nx > 0 && tid == 0) issue_load(a, nx, rank, bufs[s ^ 1], &sh.full[s ^ 1], pol);
+        cluster.sync();  // #1: slice maxima (and a claimed spare) visible everywhere
         if (tid == 0) {
             float m = -INFINITY;
             uint32_t bb = 0;
             for (int rr = 0; rr < C; ++rr) {
-                const VShared* o = cluster.map_shared_rank(&sh, rr);
-                m = fmaxf(m, o->xmax);
-                bb |= o->xbad;
+                m = fmaxf(m, sh.xmax[rr]);
+                bb |= sh.xbad[rr];
             }
             int ok = 1;
             uint32_t err = 0;
@@ -370,11 +347,17 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
             sh.m = m;
             sh.ok = ok;
         }
+        if (spare < 0 && !exhausted) {  // uniform: everyone read the broadcast spare
+            const int cl = sh.spare;
+            if (cl < nact) spare = cl;
+            if (cl >= nact - 1) exhausted = true;
+        }
         __syncthreads();
         const float m = sh.m;
         const bool ok = sh.ok != 0;
-        const int d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;  // d_{j+1}, tested on row j
-        uint64_t Z = 1;
+        bool finished_here = false;  // this rollout's step is decided at row j
+        bool accepted = false;
+        MassParams mp;
         if (a.T == 0.f) {
             // ---- greedy (R1): first index attaining the max
             int first = 0x7FFFFFFF;
@@ -396,23 +379,32 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
             }
             if (lane == 0) sh.wfirst[warp] = first;
             __syncthreads();
-            if (tid == 0) {
+            if (tid < C) {
                 int f = 0x7FFFFFFF;
                 for (int w = 0; w < NW; ++w) f = min(f, sh.wfirst[w]);
-                sh.xfirst = (f == 0x7FFFFFFF) ? f : s0 + f;
+                cluster.map_shared_rank(&sh, tid)->xfirst[rank] = (f == 0x7FFFFFFF) ? f : s0 + f;
             }
             cluster.sync();  // #2
-            if (tid == 0 && rank == 0) {
+            if (tid == 0) {
                 int g = 0x7FFFFFFF;
-                for (int rr = 0; rr < C; ++rr) g = min(g, cluster.map_shared_rank(&sh, rr)->xfirst);
-                g = ok ? g : -1;
-                sh.accept = (j < q && d == g) ? 1 : 0;
-                sh.cand = g;
+                for (int rr = 0; rr < C; ++rr) g = min(g, sh.xfirst[rr]);
+                sh.greedy = ok ? g : -1;
+                sh.accept = (ok && j < q && d == g) ? 1 : 0;
                 sh.z = 1ull;
+                sh.need_sample = 0;
             }
+            __syncthreads();
+            accepted = sh.accept != 0;
+            if (rank == 0 && tid == 0) {
+                if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? 1.0f : 0.f;
+                if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = ok ? 1ull : 0ull;
+            }
+            const bool eos_acc = accepted && a.eos >= 0 && d == a.eos;
+            finished_here = !accepted || eos_acc;
+            if (finished_here && rank == 0 && tid == 0)
+                finalize_rollout(a, sh, b, j, q, eos_acc, sh.greedy);
         } else {
             // ---- pass 2: integer masses (R2-R4), exact sums
-            MassParams mp;
             mp.c = a.c;
             mp.nmc = -__fmul_rn(m, a.c);
             mp.clampv = -(float)(a.S + 2);
@@ -424,40 +416,37 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
             acc = warp_sum_u64(acc);
             if (lane == 0) sh.wsum[warp] = acc;
             __syncthreads();
-            if (tid == 0) {
+            if (tid < C) {
                 uint64_t sum = 0;
                 for (int w = 0; w < NW; ++w) sum += sh.wsum[w];
-                sh.xsum = sum;
-                sh.xmassd = (ok && d >= s0 && d < s1) ? mass_of(bf16_at(sl, d - s0), mp) : 0ull;
+                const uint64_t md = (ok && d >= s0 && d < s1) ? mass_of(bf16_at(sl, d - s0), mp) : 0ull;
+                VShared* o = cluster.map_shared_rank(&sh, tid);
+                o->xsum[rank] = sum;
+                o->xmassd[rank] = md;
             }
-            cluster.sync();  // #2: slice sums visible
+            cluster.sync();  // #2: slice sums visible everywhere
             if (tid == 0) {
-                uint64_t sums[8];
                 uint64_t Zs = 0, md = 0;
                 for (int rr = 0; rr < C; ++rr) {
-                    const VShared* o = cluster.map_shared_rank(&sh, rr);
-                    sums[rr] = o->xsum;
-                    Zs += o->xsum;
-                    md += o->xmassd;
+                    Zs += sh.xsum[rr];
+                    md += sh.xmassd[rr];
                 }
-                const uint64_t uidv = a.uid[slot];
-                const uint32_t position = (uint32_t)(a.pos[slot] + j);
                 int accept = 0, need = 1;
                 if (ok && j < q) {
-                    const uint64_t U = uniform_floor(draw(a.seed, uidv, position, PURPOSE_ACCEPT), Zs);
-                    accept = (U < md) ? 1 : 0;
+                    const U128 r1{sh.racc[0], sh.racc[1], sh.racc[2], sh.racc[3]};
+                    accept = (uniform_floor(r1, Zs) < md) ? 1 : 0;
                     need = !accept;
                 }
                 const int excl = (j < q) ? d : -1;
                 int cross = -1;
                 uint64_t ulocal = 0;
                 if (ok && need) {
-                    const uint64_t zx = Zs - ((j < q) ? md : 0ull);
-                    const uint64_t U2 = uniform_floor(draw(a.seed, uidv, position, PURPOSE_SAMPLE), zx);
+                    const U128 r2{sh.rsmp[0], sh.rsmp[1], sh.rsmp[2], sh.rsmp[3]};
+                    const uint64_t U2 = uniform_floor(r2, Zs - ((j < q) ? md : 0ull));
                     uint64_t before = 0;
                     for (int rr = 0; rr < C; ++rr) {
-                        const int r0 = rr * a.SL, r1 = min(a.V, r0 + a.SL);
-                        const uint64_t adj = sums[rr] - ((excl >= r0 && excl < r1) ? md : 0ull);
+                        const int r0 = rr * a.SL, r1e = min(a.V, r0 + a.SL);
+                        const uint64_t adj = sh.xsum[rr] - ((excl >= r0 && excl < r1e) ? md : 0ull);
                         if (U2 < before + adj) {
                             cross = rr;
                             ulocal = U2 - before;
@@ -485,84 +474,89 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
                         before += adj;
                     }
                 }
+                if (rank == 0) {
+                    const uint64_t Zo = ok ? Zs : 0ull;
+                    if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? (float)ldexp((double)Zo, -a.S) : 0.f;
+                    if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = Zo;
+                }
             }
             __syncthreads();
-            // ---- residual / bonus sample: rescan the crossing warp's tiles (R8)
-            if (sh.need_sample && sh.cross_rank == rank && warp == sh.wstar) {
-                const int excl = (j < q) ? d : -1;
-                const uint64_t U = sh.ulocal;
-                uint64_t run = 0;
-                for (int t = t0; t < t1; ++t) {
-                    const int e0 = t * 256 + lane * 8;
-                    const uint4 v = lds128(sl + e0);
-                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                    uint64_t mm[8];
+            accepted = ok && sh.accept;
+            const bool eos_acc = accepted && a.eos >= 0 && d == a.eos;
+            finished_here = !accepted || eos_acc;
+            if (finished_here) {
+                if (!ok) {
+                    if (rank == 0 && tid == 0) finalize_rollout(a, sh, b, j, q, false, -1);
+                } else if (eos_acc) {
+                    if (rank == 0 && tid == 0) finalize_rollout(a, sh, b, j, q, true, -1);
+                } else if (sh.cross_rank == rank && warp == sh.wstar) {
+                    // ---- residual / bonus sample: rescan the crossing warp's tiles (R8)
+                    const int excl = (j < q) ? d : -1;
+                    const uint64_t U = sh.ulocal;
+                    uint64_t run = 0;
+                    for (int t = t0; t < t1; ++t) {
+                        const int e0 = t * 256 + lane * 8;
+                        const uint4 v = lds128(sl + e0);
+                        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                        uint64_t mm[8];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) mass_pair(w4[i], mp, mm[2 * i], mm[2 * i + 1]);
-                    uint64_t ls = 0;
+                        for (int i = 0; i < 4; ++i) mass_pair(w4[i], mp, mm[2 * i], mm[2 * i + 1]);
+                        uint64_t ls = 0;
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        if (s0 + e0 + i == excl) mm[i] = 0;
-                        ls += mm[i];
-                    }
-                    const uint64_t incl = warp_incl_scan_u64(ls, lane);
-                    const uint64_t tot = shfl_u64(incl, 31);
-                    if (U < run + tot) {
-                        const unsigned hit = __ballot_sync(0xFFFFFFFFu, U < run + incl);
-                        const int L = __ffs(hit) - 1;
-                        if (lane == L) {
-                            uint64_t cum = run + incl - ls;
-                            int tok = -1;
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                cum += mm[i];
-                                if (tok < 0 && cum > U) tok = s0 + e0 + i;
-                            }
-                            *cluster.map_shared_rank(&sh.cand, 0) = tok;
+                        for (int i = 0; i < 8; ++i) {
+                            if (s0 + e0 + i == excl) mm[i] = 0;
+                            ls += mm[i];
                         }
-                        break;
+                        const uint64_t incl = warp_incl_scan_u64(ls, lane);
+                        const uint64_t tot = shfl_u64(incl, 31);
+                        if (U < run + tot) {
+                            const unsigned hit = __ballot_sync(0xFFFFFFFFu, U < run + incl);
+                            const int L = __ffs(hit) - 1;
+                            if (lane == L) {
+                                uint64_t cum = run + incl - ls;
+                                int tok = -1;
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    cum += mm[i];
+                                    if (tok < 0 && cum > U) tok = s0 + e0 + i;
+                                }
+                                finalize_rollout(a, sh, b, j, q, false, tok);
+                            }
+                            break;
+                        }
+                        run += tot;
                     }
-                    run += tot;
                 }
             }
         }
-        cluster.sync();  // #3: candidate visible in the leader
-        if (rank == 0 && tid == 0) {
-            Z = ok ? sh.z : 0ull;
-            const float norm = (a.T == 0.f) ? 1.0f : (float)ldexp((double)Z, -a.S);
-            if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? norm : 0.f;
-            if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = Z;
-            const bool acc = ok && sh.accept;
-            const bool is_eos = (a.eos >= 0 && d == a.eos);
-            if (acc && !is_eos) {
-                push_item(a, make_item(b, j + 1));  // Alg. 1: verify the next draft token
-            } else {
-                finalize_rollout(a, b, j, q, acc && is_eos, ok ? sh.cand : -1);
-            }
+        // ---- advance this slot: next row of the same rollout, or a new rollout
+        __syncthreads();  // the sampling warp is done reading bufs[cur]
+        if (!finished_here) {
+            rj[cur] = j + 1;
+            if (tid == 0) issue_load(a, b, j + 1, rank, bufs[cur], &sh.full[cur], pol);
+        } else {
+            rb[cur] = spare;
+            rj[cur] = 0;
+            spare = -1;
+            if (rb[cur] >= 0 && tid == 0)
+                issue_load(a, a.active[rb[cur]], 0, rank, bufs[cur], &sh.full[cur], pol);
         }
-        if (nx > 0) {
-            cur = nx;
-            s ^= 1;
-            continue;
-        }
-        if (rank == 0 && tid == 0) {
-            const int it = claim_blocking(a);
-            for (int rr = 0; rr < C; ++rr) *cluster.map_shared_rank(&sh.item_bcast, rr) = it;
-        }
-        cluster.sync();  // #4 (only when nothing was prefetched)
-        cur = sh.item_bcast;
-        if (cur == ITEM_DONE) break;
-        s ^= 1;
-        if (tid == 0) issue_load(a, cur, rank, bufs[s], &sh.full[s], pol);
+        cur ^= 1;
     }
+    // flush the CTA's statistics counters
+    __syncthreads();
+    if (a.stats)
+        for (int i = tid; i < STAT_COUNT; i += NT)
+            if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
+    cluster.sync();  // no CTA exits while a peer may still write into its shared memory
 }
 
-// ---- plan: clamp q per rollout, queue row 0 of every live rollout (one block)
+// ---- plan: clamp q per rollout, compact the live rollouts (one block)
 constexpr int PLAN_NT = 1024;
 __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     int n, int k, int V, const int32_t* slots, const int32_t* draft, const int32_t* draft_len,
     const int32_t* pos, const int32_t* max_len, const int32_t* finished, int32_t* rb_q,
-    int32_t* queue, int queue_cap, unsigned int* ctl, int32_t* out_len, int32_t* out_acc,
+    int32_t* active, unsigned int* ctl, int32_t* out_len, int32_t* out_acc,
     int32_t* out_tokens, float* out_norm, unsigned long long* out_z, uint32_t* dev_err) {
     using Scan = cub::BlockScan<int, PLAN_NT>;
     __shared__ typename Scan::TempStorage tmp;
@@ -600,33 +594,28 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     }
     int excl, total;
     Scan(tmp).ExclusiveSum(mine, excl, total);
-    for (int i = total + tid; i < queue_cap; i += PLAN_NT) queue[i] = 0;
     for (int b = b0; b < b1; ++b)
-        if (rb_q[b] >= 0) queue[excl++] = make_item(b, 0);
+        if (rb_q[b] >= 0) active[excl++] = b;
     if (tid == 0) {
-        ctl[VCTL_HEAD] = 0u;
-        ctl[VCTL_TAIL] = (unsigned)total;
-        ctl[VCTL_DONE] = 0u;
+        ctl[VCTL_NEXT] = 0u;
         ctl[VCTL_NACTIVE] = (unsigned)total;
     }
 }
 
 static int pick_cluster(int V) {
-    // two slice buffers of <= ~40 KB: several CTAs per SM overlap each other's barriers
+    // two slice buffers of <= ~40 KB: two CTAs per SM overlap each other's barriers
     int C = 1;
-    while (C < 8 && (int64_t)((V + C - 1) / C) * 2 > 40 * 1024) C <<= 1;
+    while (C < MAXC && (int64_t)((V + C - 1) / C) * 2 > 40 * 1024) C <<= 1;
     return C;
 }
 
 template <int NT>
-static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int max_items, cudaStream_t st) {
+static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int n, cudaStream_t st) {
     const size_t smem = (size_t)a.ntiles * 1024 + sizeof(VShared);
     static int configured = 0;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(verify_rows_kernel<NT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(verify_rows_kernel<NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         configured = 1;
     }
@@ -641,18 +630,21 @@ static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int max_items, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    // persistent grid: every resident cluster slot, but no more clusters than rows
+    // persistent grid: every resident cluster slot, but no more clusters than rollouts / 2
     static int max_clusters = 0;
     static size_t max_for_smem = 0;
     if (max_clusters == 0 || max_for_smem != smem) {
         cfg.gridDim = dim3((unsigned)(a.C * num_sms), 1, 1);
         int mc = 0;
         cudaError_t e = cudaOccupancyMaxActiveClusters(&mc, verify_rows_kernel<NT>, &cfg);
-        if (e != cudaSuccess || mc < 1) mc = std::max(1, num_sms / a.C);
+        if (e != cudaSuccess || mc < 1) {
+            cudaGetLastError();
+            mc = std::max(1, num_sms / a.C);
+        }
         max_clusters = mc;
         max_for_smem = smem;
     }
-    const int clusters = std::max(1, std::min(max_clusters, max_items));
+    const int clusters = std::max(1, std::min(max_clusters, (n + 1) / 2));
     cfg.gridDim = dim3((unsigned)(clusters * a.C), 1, 1);
     return cudaLaunchKernelEx(&cfg, verify_rows_kernel<NT>, a);
 }
@@ -665,10 +657,9 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     (void)top_p;
     if (n == 0) return cudaSuccess;
     const int V = ctx->cfg.vocab;
-    const int qcap = (int)ctx->vqueue.n;
     verify_plan_kernel<<<1, PLAN_NT, 0, st>>>(n, k, V, slots, draft, draft_len, ctx->pos.p,
                                               ctx->max_len.p, ctx->finished.p, ctx->rb_q.p,
-                                              ctx->vqueue.p, qcap, ctx->vctl.p, out_len, out_acc,
+                                              ctx->vqueue.p, ctx->vctl.p, out_len, out_acc,
                                               out_tokens, out_norm, out_z, ctx->dev_err.p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -691,7 +682,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.pos = ctx->pos.p;
     a.uid = ctx->uid.p;
     a.rb_q = ctx->rb_q.p;
-    a.queue = ctx->vqueue.p;
+    a.active = ctx->vqueue.p;
     a.ctl = ctx->vctl.p;
     a.dev_err = ctx->dev_err.p;
     a.out_tokens = out_tokens;

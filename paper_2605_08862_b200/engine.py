@@ -35,7 +35,8 @@ class RolloutEngine:
         self.ctx, self.n, self.k = ctx, n, k
         self.T, self.top_p, self.target = temperature, top_p, target
         dev = torch.device("cuda", ctx.device)
-        self.stream = stream or torch.cuda.current_stream(dev)
+        # a dedicated stream: CUDA graphs cannot be captured on the legacy default stream
+        self.stream = stream or torch.cuda.Stream(dev)
         i32 = dict(dtype=torch.int32, device=dev)
         self.slots = torch.arange(n, **i32)
         self.draft = torch.full((n, max(k, 1)), -1, **i32)
@@ -54,13 +55,21 @@ class RolloutEngine:
     def put_pools(self, rl_step, seq_prompt, seq_off, tokens):
         """bs_draft_pool_put of device tensors (int32 prompt ids, int64 offsets, int32 tokens)."""
         n_tok = int(tokens.numel())
+        self._sync_inputs()
         self.ctx.bs_draft_pool_put(rl_step, seq_prompt, seq_off, tokens, n_tok, stream=self.stream)
 
     def seal(self, rl_step):
         self.ctx.bs_draft_pool_seal(rl_step, stream=self.stream)
         self.rl_step = rl_step
 
+    def _sync_inputs(self):
+        """Order the engine stream after work the caller queued on its current stream."""
+        cur = torch.cuda.current_stream(self.stream.device)
+        if cur != self.stream:
+            self.stream.wait_stream(cur)
+
     def begin(self, uids, prompt_ids, prompt_tail, max_len):
+        self._sync_inputs()
         self.ctx.bs_rollout_begin(self.slots, uids, prompt_ids, prompt_tail, max_len,
                                   stream=self.stream)
 
