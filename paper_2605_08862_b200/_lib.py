@@ -9,6 +9,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbubblespec.so")
+# profiling builds (e.g. libbubblespec_timing.so, -DBS_PHASE_TIMING) are selected explicitly
+if os.environ.get("BS_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_HERE, f"libbubblespec_{os.environ['BS_LIB_VARIANT']}.so")
 
 BS_OK, BS_ERR_INVALID, BS_ERR_OOM, BS_ERR_CUDA, BS_ERR_STALE, BS_ERR_CAPACITY, BS_ERR_NCCL, \
     BS_ERR_DEVICE = range(8)
@@ -68,6 +71,9 @@ def load():
                 f"libbubblespec.so not found at {LIB_PATH}: the CUDA extension is required "
                 "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
         lib = C.CDLL(LIB_PATH)
+        if hasattr(lib, "bsx_phase_times"):  # diagnostics (not part of the C-ABI header)
+            lib.bsx_phase_times.restype = C.c_int
+            lib.bsx_phase_times.argtypes = [C.c_void_p, C.c_int]
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -17,20 +17,23 @@ FLAGS = [
 ]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(HERE, "..", "include", "bubblespec.h"))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-shared", "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Compile libbubblespec.so (or libbubblespec_<variant>.so with extra -D defines)."""
+    lib = LIB if not variant else os.path.join(HERE, f"libbubblespec_{variant}.so")
+    if not force and not _stale(lib):
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", tmp,
+           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
@@ -40,9 +43,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--timing" in sys.argv:
+        print(build(force=True, variant="timing", defines=["BS_PHASE_TIMING"]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

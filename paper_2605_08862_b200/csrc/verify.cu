@@ -5,18 +5,23 @@
 // CTAs owns one logits row at a time, CTA `rank` the vocabulary slice
 // [rank*SL, (rank+1)*SL).  Work is claimed per ROLLOUT (one atomic each) and a rollout's
 // rows are verified in Alg. 1's order, lazily: row j+1 is read only if row j accepted
-// d_{j+1} (rows after the first rejection are never read).  Each cluster keeps two
-// rollouts in flight and alternates between them, so while one row is computed the next
-// row of the other rollout streams in (1-D bulk async copies on the TMA engine, mbarrier
-// completion, L2 evict-first) — the dependency chain of one rollout never stalls the SM.
-// Per row:
-//   * pass 1: NaN-propagating bf16x2 max; every CTA pushes its slice max into all CTAs'
-//     shared memory (DSMEM stores) -> cluster barrier -> row max;
-//   * pass 2: integer masses of reading R with packed FFMA2/FADD2, exact u64 sums; slice
-//     sums and mass(d) pushed over DSMEM -> cluster barrier -> Z, accept (Philox counter
-//     (pos+j, ACCEPT), drawn while the row streams in);
-//   * a residual / bonus sample only when needed: the CTA holding the CDF crossing
-//     rescans the crossing warp's 256-element tiles and finalizes the rollout itself.
+// d_{j+1} (rows after the first rejection are never read).
+//
+// Each cluster keeps two rollouts in flight ("slots" A and B) and runs the three stages
+// of a row — P1 (row max), P2 (integer masses, exact sums), DEC (accept / sample) — on
+// the fixed software-pipelined schedule  P1(A) DEC(B) P2(A) P1(B) DEC(A) P2(B), so the
+// TMA load of a slot's next row streams in under the other slot's mass pass.  The
+// cross-CTA reductions are point-to-point: every CTA pushes its slice record into all
+// peers' shared memory (DSMEM stores) and arrives remotely on their mbarrier
+// (release.cluster); a consumer waits only for that record (acquire.cluster) — there is
+// no cluster-wide barrier in the loop, so CTAs that share an SM with other clusters
+// drift freely.
+//   * P1: NaN-propagating bf16x2 max over the slice (1-D bulk async copies on the TMA
+//     engine, mbarrier completion, L2 evict-first);
+//   * P2: masses of reading R with packed FFMA2/FADD2, exact u64 per-warp sums;
+//   * DEC: Z, mass(d) -> accept (Philox counter (pos+j, ACCEPT), drawn under P1); a
+//     residual / bonus sample is found by the CTA holding the CDF crossing, which
+//     rescans the crossing warp's 256-element tiles and finalizes the rollout.
 #include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
@@ -29,6 +34,24 @@ namespace cg = cooperative_groups;
 namespace bs {
 
 constexpr int MAXC = 8;  // max cluster size
+
+// Optional per-stage cycle accounting (build with -DBS_PHASE_TIMING; read with
+// bsx_phase_times): thread 0 of every CTA adds the clock64() delta of each stage.
+#ifdef BS_PHASE_TIMING
+__device__ unsigned long long g_phase[16];
+#define PH_MARK(i)                                                     \
+    do {                                                               \
+        if (tid == 0) {                                                \
+            const long long now_ = clock64();                          \
+            atomicAdd(&g_phase[i], (unsigned long long)(now_ - ph_t)); \
+            ph_t = now_;                                               \
+        }                                                              \
+    } while (0)
+#else
+#define PH_MARK(i) \
+    do {           \
+    } while (0)
+#endif
 
 struct VerifyArgs {
     const int32_t* slots;
@@ -53,31 +76,31 @@ struct VerifyArgs {
     unsigned long long* stats;
 };
 
+// Records pushed to every CTA of the cluster (index = source rank), double-buffered by
+// row parity so a producer one row ahead never overwrites an unread record.
+struct MaxRec {
+    float max;
+    uint32_t bad;
+    int32_t spare;  // rank 0 only: the slot's claimed-ahead next rollout (-1: none left)
+    int32_t pad;
+};
+struct SumRec {
+    unsigned long long sum;    // slice mass sum (greedy: first argmax index)
+    unsigned long long massd;  // mass of the draft token if it lies in the slice
+};
+
 struct __align__(16) VShared {
-    uint64_t full[2];  // TMA completion barrier per slot buffer
-    // written remotely by every CTA of the cluster (index = source rank)
-    float xmax[MAXC];
-    uint32_t xbad[MAXC];
-    int32_t xfirst[MAXC];
-    unsigned long long xsum[MAXC];
-    unsigned long long xmassd[MAXC];
-    int32_t spare;  // claimed-ahead rollout index (written by the leader into all CTAs)
+    uint64_t full[2];     // TMA completion, one per slot buffer
+    uint64_t bar_max[2];  // C arrivals per row: slice maxima of the slot's row
+    uint64_t bar_sum[2];  // C arrivals per row: slice sums of the slot's row
+    MaxRec rmax[2][2][MAXC];
+    SumRec rsum[2][2][MAXC];
+    int32_t init_rollouts[4];
     // CTA-local
     float wmax[32];
     uint32_t wbad[32];
-    int32_t wfirst[32];
-    unsigned long long wsum[32];
-    uint32_t racc[4], rsmp[4];  // Philox draws of the current row
-    float m;
-    int32_t ok;
-    int32_t accept;
-    int32_t need_sample;
-    int32_t cross_rank;
-    int32_t wstar;
-    int32_t greedy;
-    int32_t pad;
-    unsigned long long z;
-    unsigned long long ulocal;
+    unsigned long long wsum[2][32];  // per slot: exact per-warp sums (sample search)
+    uint32_t rng[2][8];              // per slot: Philox ACCEPT (0-3) and SAMPLE (4-7) draws
     unsigned long long stat[STAT_COUNT];
 };
 
@@ -152,12 +175,12 @@ __device__ __forceinline__ const uint16_t* row_ptr(const VerifyArgs& a, int b, i
     return a.logits + rowno * a.stride;
 }
 
-// Issue the bulk copy of this CTA's slice of row (b, j) into `buf` (elected thread).
-__device__ __forceinline__ void issue_load(const VerifyArgs& a, int b, int j, int rank,
+// Issue the bulk copy of this CTA's slice of `row` into `buf` (elected thread).
+__device__ __forceinline__ void issue_load(const VerifyArgs& a, const uint16_t* row, int rank,
                                            uint16_t* buf, uint64_t* bar, uint64_t pol) {
     const int s0 = rank * a.SL, s1 = min(a.V, s0 + a.SL);
     const int len = max(0, s1 - s0);
-    const uint16_t* src = row_ptr(a, b, j) + s0;
+    const uint16_t* src = row + s0;
     const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
     const int bulk = aligned ? (len & ~7) : 0;
     fence_proxy_async_smem();
@@ -206,6 +229,17 @@ __device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int j,
     }
 }
 
+// Per-slot state kept (uniformly) in registers of every thread.
+struct Slot {
+    int stage;  // 0 = P1, 1 = P2, 2 = DEC, 3 = empty
+    int ri;     // index into active[]
+    int b, j, q, d;
+    int par;    // row parity of the exchange records / barriers
+    float m;    // row max (after P1 exchange)
+    bool ok;
+};
+enum { ST_P1 = 0, ST_P2 = 1, ST_DEC = 2, ST_EMPTY = 3 };
+
 template <int NT>
 __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
     constexpr int NW = NT / 32;
@@ -226,67 +260,76 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
     const int t0 = min(ntl, warp * tpw), t1 = min(ntl, t0 + tpw);
     const uint64_t pol = policy_evict_first();
     const int nact = (int)a.ctl[VCTL_NACTIVE];
+    MassParams mp;
+    mp.c = a.c;
+    mp.clampv = -(float)(a.S + 2);
+    mp.magic = 12582912.0f + (float)a.S;
 
     if (tid == 0) {
-        mbar_init(&sh.full[0], 1);
-        mbar_init(&sh.full[1], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sh.full[i], 1);
+            mbar_init(&sh.bar_max[i], (uint32_t)C);
+            mbar_init(&sh.bar_sum[i], (uint32_t)C);
+        }
         fence_mbar_init();
     }
     for (int i = tid; i < STAT_COUNT; i += NT) sh.stat[i] = 0ull;
-    // -inf padding beyond the slice (never written by the bulk copies)
-    for (int e = len + tid; e < a.ntiles * 256; e += NT) {
+    for (int e = len + tid; e < a.ntiles * 256; e += NT) {  // -inf padding past the slice
         bufs[0][e] = (uint16_t)0xFF80u;
         bufs[1][e] = (uint16_t)0xFF80u;
     }
-    if (rank == 0 && tid == 0) {  // claim two rollouts + one spare
-        const int base = (int)atomicAdd(a.ctl + VCTL_NEXT, 3u);
+    // leader claims two rollouts + one spare per slot
+    int spare_reg[2] = {-1, -1};  // meaningful in the leader thread only
+    if (rank == 0 && tid == 0) {
+        const int base = (int)atomicAdd(a.ctl + VCTL_NEXT, 4u);
         for (int rr = 0; rr < C; ++rr) {
             VShared* o = cluster.map_shared_rank(&sh, rr);
-            o->xfirst[0] = base;  // scratch for the broadcast below
+            o->init_rollouts[0] = base;
+            o->init_rollouts[1] = base + 1;
         }
+        spare_reg[0] = (base + 2 < nact) ? base + 2 : -1;
+        spare_reg[1] = (base + 3 < nact) ? base + 3 : -1;
     }
     __syncthreads();
     cluster.sync();
-    const int base0 = sh.xfirst[0];
-    int rb[2], rj[2];  // rollout (index into active[], -1 = empty) and row of each slot
-    rb[0] = (base0 < nact) ? base0 : -1;
-    rb[1] = (base0 + 1 < nact) ? base0 + 1 : -1;
-    int spare = (base0 + 2 < nact) ? base0 + 2 : -1;
-    bool exhausted = (base0 + 2 >= nact - 1);
-    rj[0] = rj[1] = 0;
-    if (tid == 0) {
-        for (int sl = 0; sl < 2; ++sl)
-            if (rb[sl] >= 0) issue_load(a, a.active[rb[sl]], 0, rank, bufs[sl], &sh.full[sl], pol);
+    Slot S[2];
+    for (int x = 0; x < 2; ++x) {
+        const int ri = sh.init_rollouts[x];
+        S[x].ri = ri;
+        S[x].stage = (ri < nact) ? ST_P1 : ST_EMPTY;
+        S[x].j = 0;
+        S[x].par = 0;
+        S[x].b = (ri < nact) ? a.active[ri] : 0;
+        S[x].q = (ri < nact) ? a.rb_q[S[x].b] : 0;
+        S[x].d = -1;
+        S[x].m = 0.f;
+        S[x].ok = true;
+        if (tid == 0 && ri < nact) issue_load(a, row_ptr(a, S[x].b, 0), rank, bufs[x], &sh.full[x], pol);
     }
-    uint32_t ph[2] = {0u, 0u};
-    int cur = 0;
-    if (rb[0] < 0) cur = 1;
+    uint32_t fph[2] = {0u, 0u}, mph[2] = {0u, 0u}, sph[2] = {0u, 0u};  // barrier phases
+#ifdef BS_PHASE_TIMING
+    long long ph_t = clock64();
+#endif
 
-    while (rb[0] >= 0 || rb[1] >= 0) {
-        if (rb[cur] < 0) cur ^= 1;
-        const int b = a.active[rb[cur]];
-        const int j = rj[cur];
-        const int q = a.rb_q[b];
-        const int slot = a.slots[b];
-        uint16_t* sl = bufs[cur];
-        const int d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;  // d_{j+1}, tested on row j
-        // leader claims the next spare early; the atomic's latency overlaps pass 1
-        int claimed = -1;
-        const bool want_spare = (rank == 0 && tid == 0 && spare < 0 && !exhausted);
-        if (want_spare) claimed = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
-        // the row's two Philox draws, while the slice streams in
-        if (tid == 32) {
+    // ------------------------------------------------------------ stage bodies
+    auto stage_p1 = [&](int x) {
+        Slot& s = S[x];
+        uint16_t* sl = bufs[x];
+        s.d = (s.j < s.q) ? a.draft[(int64_t)s.b * a.k + s.j] : -1;  // d_{j+1}, tested on row j
+        if (tid == 32) {  // the row's two Philox draws, under the max pass
+            const int slot = a.slots[s.b];
             const uint64_t uidv = a.uid[slot];
-            const uint32_t position = (uint32_t)(a.pos[slot] + j);
+            const uint32_t position = (uint32_t)(a.pos[slot] + s.j);
             const U128 r1 = draw(a.seed, uidv, position, PURPOSE_ACCEPT);
             const U128 r2 = draw(a.seed, uidv, position, PURPOSE_SAMPLE);
-            sh.racc[0] = r1.x0; sh.racc[1] = r1.x1; sh.racc[2] = r1.x2; sh.racc[3] = r1.x3;
-            sh.rsmp[0] = r2.x0; sh.rsmp[1] = r2.x1; sh.rsmp[2] = r2.x2; sh.rsmp[3] = r2.x3;
+            sh.rng[x][0] = r1.x0; sh.rng[x][1] = r1.x1; sh.rng[x][2] = r1.x2; sh.rng[x][3] = r1.x3;
+            sh.rng[x][4] = r2.x0; sh.rng[x][5] = r2.x1; sh.rng[x][6] = r2.x2; sh.rng[x][7] = r2.x3;
         }
-        mbar_wait(&sh.full[cur], ph[cur]);
-        ph[cur] ^= 1u;
+        mbar_wait(&sh.full[x], fph[x]);
+        fph[x] ^= 1u;
+        PH_MARK(1);
         {   // ragged part (unaligned rows or a slice length not a multiple of 8)
-            const uint16_t* src = row_ptr(a, b, j) + s0;
+            const uint16_t* src = row_ptr(a, s.b, s.j) + s0;
             const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
             const int bulk = aligned ? (len & ~7) : 0;
             if (bulk < len) {
@@ -294,72 +337,66 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
                 __syncthreads();
             }
         }
-        // ---- pass 1: max (NaN-propagating on bf16x2)
-        {
-            uint32_t mx = 0xFF80FF80u;
-            for (int t = t0; t < t1; ++t) {
-                const uint4 v = lds128(sl + t * 256 + lane * 8);
-                mx = hmax2_nan_u32(mx, v.x);
-                mx = hmax2_nan_u32(mx, v.y);
-                mx = hmax2_nan_u32(mx, v.z);
-                mx = hmax2_nan_u32(mx, v.w);
-            }
-            const float lo = bf16lo(mx), hi = bf16hi(mx);
-            uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
-            float fm = fmaxf(lo, hi);
+        uint32_t mx = 0xFF80FF80u;
+        for (int t = t0; t < t1; ++t) {
+            const uint4 v = lds128(sl + t * 256 + lane * 8);
+            mx = hmax2_nan_u32(mx, v.x);
+            mx = hmax2_nan_u32(mx, v.y);
+            mx = hmax2_nan_u32(mx, v.z);
+            mx = hmax2_nan_u32(mx, v.w);
+        }
+        const float lo = bf16lo(mx), hi = bf16hi(mx);
+        uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
+        float fm = fmaxf(lo, hi);
 #pragma unroll
-            for (int mm = 16; mm; mm >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, mm));
-            bad = __any_sync(0xFFFFFFFFu, bad) ? 1u : 0u;
-            if (lane == 0) {
-                sh.wmax[warp] = fm;
-                sh.wbad[warp] = bad;
-            }
-            __syncthreads();
-            if (tid < C) {  // push this slice's max into CTA `tid`
-                float mloc = -INFINITY;
-                uint32_t bb = 0;
-                for (int w = 0; w < NW; ++w) {
-                    mloc = fmaxf(mloc, sh.wmax[w]);
-                    bb |= sh.wbad[w];
-                }
-                VShared* o = cluster.map_shared_rank(&sh, tid);
-                o->xmax[rank] = mloc;
-                o->xbad[rank] = bb;
-            }
-            if (want_spare) {
-                for (int rr = 0; rr < C; ++rr) cluster.map_shared_rank(&sh, rr)->spare = claimed;
-            }
-        }
-        cluster.sync();  // #1: slice maxima (and a claimed spare) visible everywhere
-        if (tid == 0) {
-            float m = -INFINITY;
-            uint32_t bb = 0;
-            for (int rr = 0; rr < C; ++rr) {
-                m = fmaxf(m, sh.xmax[rr]);
-                bb |= sh.xbad[rr];
-            }
-            int ok = 1;
-            uint32_t err = 0;
-            if (bb) { ok = 0; err |= DEV_BAD_LOGIT; }
-            else if (m == -INFINITY) { ok = 0; err |= DEV_ALL_NEGINF; }
-            else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) { ok = 0; err |= DEV_RANGE; }
-            if (err && rank == 0) atomicOr(a.dev_err, err);
-            sh.m = m;
-            sh.ok = ok;
-        }
-        if (spare < 0 && !exhausted) {  // uniform: everyone read the broadcast spare
-            const int cl = sh.spare;
-            if (cl < nact) spare = cl;
-            if (cl >= nact - 1) exhausted = true;
+        for (int mm = 16; mm; mm >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, mm));
+        bad = __any_sync(0xFFFFFFFFu, bad) ? 1u : 0u;
+        if (lane == 0) {
+            sh.wmax[warp] = fm;
+            sh.wbad[warp] = bad;
         }
         __syncthreads();
-        const float m = sh.m;
-        const bool ok = sh.ok != 0;
-        bool finished_here = false;  // this rollout's step is decided at row j
-        bool accepted = false;
-        MassParams mp;
-        if (a.T == 0.f) {
-            // ---- greedy (R1): first index attaining the max
+        const int spv = __shfl_sync(0xFFFFFFFFu, spare_reg[x], 0);  // the leader's, in warp 0
+        if (tid < C) {  // push this slice's record into CTA `tid`, then arrive there
+            MaxRec r;
+            r.max = -INFINITY;
+            r.bad = 0;
+            for (int w = 0; w < NW; ++w) {
+                r.max = fmaxf(r.max, sh.wmax[w]);
+                r.bad |= sh.wbad[w];
+            }
+            r.spare = (rank == 0) ? spv : -1;
+            r.pad = 0;
+            cluster.map_shared_rank(&sh, tid)->rmax[x][s.par][rank] = r;
+            mbar_arrive_remote(&sh.bar_max[x], (uint32_t)tid);
+        }
+        s.stage = ST_P2;
+        PH_MARK(2);
+    };
+
+    auto stage_p2 = [&](int x) {
+        Slot& s = S[x];
+        uint16_t* sl = bufs[x];
+        mbar_wait_cluster(&sh.bar_max[x], mph[x]);
+        mph[x] ^= 1u;
+        PH_MARK(3);
+        float m = -INFINITY;
+        uint32_t bb = 0;
+        for (int rr = 0; rr < C; ++rr) {
+            m = fmaxf(m, sh.rmax[x][s.par][rr].max);
+            bb |= sh.rmax[x][s.par][rr].bad;
+        }
+        bool ok = true;
+        uint32_t err = 0;
+        if (bb) { ok = false; err |= DEV_BAD_LOGIT; }
+        else if (m == -INFINITY) { ok = false; err |= DEV_ALL_NEGINF; }
+        else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) { ok = false; err |= DEV_RANGE; }
+        if (err && rank == 0 && tid == 0) atomicOr(a.dev_err, err);
+        s.m = m;
+        s.ok = ok;
+        SumRec rec;
+        rec.massd = 0ull;
+        if (a.T == 0.f) {  // greedy (R1): first index attaining the max
             int first = 0x7FFFFFFF;
             if (ok) {
                 for (int t = t0; t < t1 && first == 0x7FFFFFFF; ++t) {
@@ -377,178 +414,194 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
                     first = f;
                 }
             }
-            if (lane == 0) sh.wfirst[warp] = first;
+            if (lane == 0) sh.wsum[x][warp] = (unsigned long long)(uint32_t)first;
             __syncthreads();
-            if (tid < C) {
-                int f = 0x7FFFFFFF;
-                for (int w = 0; w < NW; ++w) f = min(f, sh.wfirst[w]);
-                cluster.map_shared_rank(&sh, tid)->xfirst[rank] = (f == 0x7FFFFFFF) ? f : s0 + f;
-            }
-            cluster.sync();  // #2
-            if (tid == 0) {
-                int g = 0x7FFFFFFF;
-                for (int rr = 0; rr < C; ++rr) g = min(g, sh.xfirst[rr]);
-                sh.greedy = ok ? g : -1;
-                sh.accept = (ok && j < q && d == g) ? 1 : 0;
-                sh.z = 1ull;
-                sh.need_sample = 0;
-            }
-            __syncthreads();
-            accepted = sh.accept != 0;
-            if (rank == 0 && tid == 0) {
-                if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? 1.0f : 0.f;
-                if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = ok ? 1ull : 0ull;
-            }
-            const bool eos_acc = accepted && a.eos >= 0 && d == a.eos;
-            finished_here = !accepted || eos_acc;
-            if (finished_here && rank == 0 && tid == 0)
-                finalize_rollout(a, sh, b, j, q, eos_acc, sh.greedy);
-        } else {
-            // ---- pass 2: integer masses (R2-R4), exact sums
-            mp.c = a.c;
+            int f = 0x7FFFFFFF;
+            for (int w = 0; w < NW; ++w) f = min(f, (int)sh.wsum[x][w]);
+            rec.sum = (unsigned long long)(uint32_t)((f == 0x7FFFFFFF) ? f : s0 + f);
+        } else {  // integer masses (R2-R4), exact sums
             mp.nmc = -__fmul_rn(m, a.c);
-            mp.clampv = -(float)(a.S + 2);
-            mp.magic = 12582912.0f + (float)a.S;
             uint64_t acc = 0;
             if (ok) {
                 for (int t = t0; t < t1; ++t) acc += mass8(lds128(sl + t * 256 + lane * 8), mp);
             }
             acc = warp_sum_u64(acc);
-            if (lane == 0) sh.wsum[warp] = acc;
+            if (lane == 0) sh.wsum[x][warp] = acc;
             __syncthreads();
-            if (tid < C) {
-                uint64_t sum = 0;
-                for (int w = 0; w < NW; ++w) sum += sh.wsum[w];
-                const uint64_t md = (ok && d >= s0 && d < s1) ? mass_of(bf16_at(sl, d - s0), mp) : 0ull;
-                VShared* o = cluster.map_shared_rank(&sh, tid);
-                o->xsum[rank] = sum;
-                o->xmassd[rank] = md;
+            uint64_t sum = 0;
+            for (int w = 0; w < NW; ++w) sum += sh.wsum[x][w];
+            rec.sum = sum;
+            if (ok && s.d >= s0 && s.d < s1) rec.massd = mass_of(bf16_at(sl, s.d - s0), mp);
+        }
+        if (tid < C) {
+            cluster.map_shared_rank(&sh, tid)->rsum[x][s.par][rank] = rec;
+            mbar_arrive_remote(&sh.bar_sum[x], (uint32_t)tid);
+        }
+        s.stage = ST_DEC;
+        PH_MARK(4);
+    };
+
+    auto stage_dec = [&](int x) {
+        Slot& s = S[x];
+        uint16_t* sl = bufs[x];
+        mbar_wait_cluster(&sh.bar_sum[x], sph[x]);
+        sph[x] ^= 1u;
+        PH_MARK(5);
+        const int j = s.j, q = s.q, d = s.d, b = s.b;
+        const bool ok = s.ok;
+        bool accepted = false, finished = false, eos_acc = false;
+        if (a.T == 0.f) {
+            int g = 0x7FFFFFFF;
+            for (int rr = 0; rr < C; ++rr) g = min(g, (int)(uint32_t)sh.rsum[x][s.par][rr].sum);
+            g = ok ? g : -1;
+            accepted = ok && j < q && d == g;
+            eos_acc = accepted && a.eos >= 0 && d == a.eos;
+            finished = !accepted || eos_acc;
+            if (rank == 0 && tid == 0) {
+                if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? 1.0f : 0.f;
+                if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = ok ? 1ull : 0ull;
+                if (finished) finalize_rollout(a, sh, b, j, q, eos_acc, g);
             }
-            cluster.sync();  // #2: slice sums visible everywhere
-            if (tid == 0) {
-                uint64_t Zs = 0, md = 0;
-                for (int rr = 0; rr < C; ++rr) {
-                    Zs += sh.xsum[rr];
-                    md += sh.xmassd[rr];
-                }
-                int accept = 0, need = 1;
-                if (ok && j < q) {
-                    const U128 r1{sh.racc[0], sh.racc[1], sh.racc[2], sh.racc[3]};
-                    accept = (uniform_floor(r1, Zs) < md) ? 1 : 0;
-                    need = !accept;
-                }
+        } else {
+            uint64_t Zs = 0, md = 0;
+            for (int rr = 0; rr < C; ++rr) {
+                Zs += sh.rsum[x][s.par][rr].sum;
+                md += sh.rsum[x][s.par][rr].massd;
+            }
+            if (ok && j < q) {
+                const U128 r1{sh.rng[x][0], sh.rng[x][1], sh.rng[x][2], sh.rng[x][3]};
+                accepted = uniform_floor(r1, Zs) < md;
+            }
+            eos_acc = accepted && a.eos >= 0 && d == a.eos;
+            finished = !accepted || eos_acc;
+            if (rank == 0 && tid == 0) {
+                const uint64_t Zo = ok ? Zs : 0ull;
+                if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? (float)ldexp((double)Zo, -a.S) : 0.f;
+                if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = Zo;
+                if (!ok) finalize_rollout(a, sh, b, j, q, false, -1);
+                else if (eos_acc) finalize_rollout(a, sh, b, j, q, true, -1);
+            }
+            if (ok && finished && !eos_acc) {
+                // residual (rejection: d excluded) or bonus sample (R8): which CTA / warp
+                // holds the CDF crossing?  (computed redundantly, no synchronisation)
                 const int excl = (j < q) ? d : -1;
+                const U128 r2{sh.rng[x][4], sh.rng[x][5], sh.rng[x][6], sh.rng[x][7]};
+                const uint64_t U2 = uniform_floor(r2, Zs - ((j < q) ? md : 0ull));
+                uint64_t before = 0;
                 int cross = -1;
-                uint64_t ulocal = 0;
-                if (ok && need) {
-                    const U128 r2{sh.rsmp[0], sh.rsmp[1], sh.rsmp[2], sh.rsmp[3]};
-                    const uint64_t U2 = uniform_floor(r2, Zs - ((j < q) ? md : 0ull));
-                    uint64_t before = 0;
-                    for (int rr = 0; rr < C; ++rr) {
-                        const int r0 = rr * a.SL, r1e = min(a.V, r0 + a.SL);
-                        const uint64_t adj = sh.xsum[rr] - ((excl >= r0 && excl < r1e) ? md : 0ull);
-                        if (U2 < before + adj) {
-                            cross = rr;
-                            ulocal = U2 - before;
-                            break;
-                        }
-                        before += adj;
+                uint64_t ul = 0;
+                for (int rr = 0; rr < C; ++rr) {
+                    const int r0 = rr * a.SL, r1e = min(a.V, r0 + a.SL);
+                    const uint64_t adj = sh.rsum[x][s.par][rr].sum - ((excl >= r0 && excl < r1e) ? md : 0ull);
+                    if (U2 < before + adj) {
+                        cross = rr;
+                        ul = U2 - before;
+                        break;
                     }
+                    before += adj;
                 }
-                sh.z = Zs;
-                sh.accept = accept;
-                sh.need_sample = (ok && need) ? 1 : 0;
-                sh.cross_rank = cross;
-                sh.wstar = -1;
                 if (cross == rank) {
-                    uint64_t before = 0;
+                    int wstar = -1;
+                    uint64_t uw = 0;
+                    before = 0;
                     const int span = tpw * 256;
                     for (int w = 0; w < NW; ++w) {
                         const int w0 = s0 + w * span, w1 = min(s1, w0 + span);
-                        const uint64_t adj = sh.wsum[w] - ((excl >= w0 && excl < w1) ? md : 0ull);
-                        if (ulocal < before + adj) {
-                            sh.wstar = w;
-                            sh.ulocal = ulocal - before;
+                        const uint64_t adj = sh.wsum[x][w] - ((excl >= w0 && excl < w1) ? md : 0ull);
+                        if (ul < before + adj) {
+                            wstar = w;
+                            uw = ul - before;
                             break;
                         }
                         before += adj;
                     }
-                }
-                if (rank == 0) {
-                    const uint64_t Zo = ok ? Zs : 0ull;
-                    if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? (float)ldexp((double)Zo, -a.S) : 0.f;
-                    if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = Zo;
-                }
-            }
-            __syncthreads();
-            accepted = ok && sh.accept;
-            const bool eos_acc = accepted && a.eos >= 0 && d == a.eos;
-            finished_here = !accepted || eos_acc;
-            if (finished_here) {
-                if (!ok) {
-                    if (rank == 0 && tid == 0) finalize_rollout(a, sh, b, j, q, false, -1);
-                } else if (eos_acc) {
-                    if (rank == 0 && tid == 0) finalize_rollout(a, sh, b, j, q, true, -1);
-                } else if (sh.cross_rank == rank && warp == sh.wstar) {
-                    // ---- residual / bonus sample: rescan the crossing warp's tiles (R8)
-                    const int excl = (j < q) ? d : -1;
-                    const uint64_t U = sh.ulocal;
-                    uint64_t run = 0;
-                    for (int t = t0; t < t1; ++t) {
-                        const int e0 = t * 256 + lane * 8;
-                        const uint4 v = lds128(sl + e0);
-                        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                        uint64_t mm[8];
+                    if (warp == wstar) {
+                        mp.nmc = -__fmul_rn(s.m, a.c);
+                        uint64_t run = 0;
+                        for (int t = t0; t < t1; ++t) {
+                            const int e0 = t * 256 + lane * 8;
+                            const uint4 v = lds128(sl + e0);
+                            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                            uint64_t mm[8];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) mass_pair(w4[i], mp, mm[2 * i], mm[2 * i + 1]);
-                        uint64_t ls = 0;
+                            for (int i = 0; i < 4; ++i) mass_pair(w4[i], mp, mm[2 * i], mm[2 * i + 1]);
+                            uint64_t ls = 0;
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            if (s0 + e0 + i == excl) mm[i] = 0;
-                            ls += mm[i];
-                        }
-                        const uint64_t incl = warp_incl_scan_u64(ls, lane);
-                        const uint64_t tot = shfl_u64(incl, 31);
-                        if (U < run + tot) {
-                            const unsigned hit = __ballot_sync(0xFFFFFFFFu, U < run + incl);
-                            const int L = __ffs(hit) - 1;
-                            if (lane == L) {
-                                uint64_t cum = run + incl - ls;
-                                int tok = -1;
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) {
-                                    cum += mm[i];
-                                    if (tok < 0 && cum > U) tok = s0 + e0 + i;
-                                }
-                                finalize_rollout(a, sh, b, j, q, false, tok);
+                            for (int i = 0; i < 8; ++i) {
+                                if (s0 + e0 + i == excl) mm[i] = 0;
+                                ls += mm[i];
                             }
-                            break;
+                            const uint64_t incl = warp_incl_scan_u64(ls, lane);
+                            const uint64_t tot = shfl_u64(incl, 31);
+                            if (uw < run + tot) {
+                                const unsigned hit = __ballot_sync(0xFFFFFFFFu, uw < run + incl);
+                                const int L = __ffs(hit) - 1;
+                                if (lane == L) {
+                                    uint64_t cum = run + incl - ls;
+                                    int tok = -1;
+#pragma unroll
+                                    for (int i = 0; i < 8; ++i) {
+                                        cum += mm[i];
+                                        if (tok < 0 && cum > uw) tok = s0 + e0 + i;
+                                    }
+                                    finalize_rollout(a, sh, b, j, q, false, tok);
+                                }
+                                break;
+                            }
+                            run += tot;
                         }
-                        run += tot;
                     }
                 }
             }
         }
-        // ---- advance this slot: next row of the same rollout, or a new rollout
-        __syncthreads();  // the sampling warp is done reading bufs[cur]
-        if (!finished_here) {
-            rj[cur] = j + 1;
-            if (tid == 0) issue_load(a, b, j + 1, rank, bufs[cur], &sh.full[cur], pol);
+        PH_MARK(6);
+        // ---- advance the slot: the next row of this rollout, or the slot's spare rollout
+        s.par ^= 1;
+        if (!finished) {
+            s.j = j + 1;
+            s.stage = ST_P1;
+            if (tid == 0) issue_load(a, row_ptr(a, b, j + 1), rank, bufs[x], &sh.full[x], pol);
         } else {
-            rb[cur] = spare;
-            rj[cur] = 0;
-            spare = -1;
-            if (rb[cur] >= 0 && tid == 0)
-                issue_load(a, a.active[rb[cur]], 0, rank, bufs[cur], &sh.full[cur], pol);
+            const int nri = sh.rmax[x][s.par ^ 1][0].spare;  // broadcast with this row's P1
+            __syncthreads();  // the sampling warp is done with bufs[x]
+            if (nri >= 0) {
+                s.ri = nri;
+                s.b = a.active[nri];
+                s.q = a.rb_q[s.b];
+                s.j = 0;
+                s.stage = ST_P1;
+                if (tid == 0) issue_load(a, row_ptr(a, s.b, 0), rank, bufs[x], &sh.full[x], pol);
+                if (rank == 0 && tid == 0) {  // claim the next spare for this slot
+                    const int c2 = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
+                    spare_reg[x] = (c2 < nact) ? c2 : -1;
+                }
+            } else {
+                s.stage = ST_EMPTY;
+            }
         }
-        cur ^= 1;
+        PH_MARK(7);
+#ifdef BS_PHASE_TIMING
+        if (tid == 0) atomicAdd(&g_phase[15], 1ull);
+#endif
+    };
+
+    // ------------------------------------------------------------ the pipelined schedule
+    for (;;) {
+        PH_MARK(0);
+        if (S[0].stage == ST_P1) stage_p1(0);
+        if (S[1].stage == ST_DEC) stage_dec(1);
+        if (S[0].stage == ST_P2) stage_p2(0);
+        if (S[1].stage == ST_P1) stage_p1(1);
+        if (S[0].stage == ST_DEC) stage_dec(0);
+        if (S[1].stage == ST_P2) stage_p2(1);
+        if (S[0].stage == ST_EMPTY && S[1].stage == ST_EMPTY) break;
     }
     // flush the CTA's statistics counters
     __syncthreads();
     if (a.stats)
         for (int i = tid; i < STAT_COUNT; i += NT)
             if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
-    cluster.sync();  // no CTA exits while a peer may still write into its shared memory
+    cluster.sync();  // no CTA exits while a peer may still access its shared memory
 }
 
 // ---- plan: clamp q per rollout, compact the live rollouts (one block)
@@ -603,7 +656,7 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
 }
 
 static int pick_cluster(int V) {
-    // two slice buffers of <= ~40 KB: two CTAs per SM overlap each other's barriers
+    // two slice buffers of <= ~40 KB: two CTAs per SM overlap each other's waits
     int C = 1;
     while (C < MAXC && (int64_t)((V + C - 1) / C) * 2 > 40 * 1024) C <<= 1;
     return C;
@@ -633,7 +686,8 @@ static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int n, cudaStre
     // persistent grid: every resident cluster slot, but no more clusters than rollouts / 2
     static int max_clusters = 0;
     static size_t max_for_smem = 0;
-    if (max_clusters == 0 || max_for_smem != smem) {
+    static int max_for_c = 0;
+    if (max_clusters == 0 || max_for_smem != smem || max_for_c != a.C) {
         cfg.gridDim = dim3((unsigned)(a.C * num_sms), 1, 1);
         int mc = 0;
         cudaError_t e = cudaOccupancyMaxActiveClusters(&mc, verify_rows_kernel<NT>, &cfg);
@@ -643,6 +697,7 @@ static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int n, cudaStre
         }
         max_clusters = mc;
         max_for_smem = smem;
+        max_for_c = a.C;
     }
     const int clusters = std::max(1, std::min(max_clusters, (n + 1) / 2));
     cfg.gridDim = dim3((unsigned)(clusters * a.C), 1, 1);
@@ -696,3 +751,18 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
 }
 
 }  // namespace bs
+
+extern "C" int bsx_phase_times(unsigned long long* out16, int reset) {
+#ifdef BS_PHASE_TIMING
+    cudaMemcpyFromSymbol(out16, bs::g_phase, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(bs::g_phase, z, sizeof z);
+    }
+    return 1;
+#else
+    (void)out16;
+    (void)reset;
+    return 0;
+#endif
+}

@@ -50,6 +50,18 @@ for i in range(a.iters):
     torch.cuda.synchronize()
     ts.append(s.elapsed_time(e))
 st = ctx.bs_stats_read()
+if os.environ.get("BS_LIB_VARIANT") == "timing":
+    import ctypes
+    lib = bs.load()
+    ph = (ctypes.c_ulonglong * 16)()
+    if lib.bsx_phase_times(ph, 1):
+        names = ["loop top", "wait slice", "P1 max+push", "wait maxima", "P2 masses+push",
+                 "wait sums", "DEC decide+sample", "advance/load"]
+        tot = sum(ph[i] for i in range(len(names)))
+        it = max(1, ph[15])
+        print(f"phase cycles per row-iteration per CTA (n={ph[15]}):")
+        for i, nm in enumerate(names):
+            print(f"  {nm:18s} {ph[i] / it:10.0f} cyc  {100 * ph[i] / max(1, tot):5.1f}%")
 moved = int(st[6]) * 2 * V
 need = int(st[7]) * 2 * V
 tot = sum(ts[2:]) / 1e3
