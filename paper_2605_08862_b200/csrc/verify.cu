@@ -13,15 +13,16 @@
 // TMA load of a slot's next row streams in under the other slot's mass pass.  The
 // cross-CTA reductions are point-to-point: every CTA pushes its slice record into all
 // peers' shared memory (DSMEM stores) and arrives remotely on their mbarrier
-// (release.cluster); a consumer waits only for that record (acquire.cluster) — there is
-// no cluster-wide barrier in the loop, so CTAs that share an SM with other clusters
-// drift freely.
+// (release.cluster); one thread per consumer CTA waits (acquire.cluster) and a CTA
+// barrier orders the rest — there is no cluster-wide barrier in the loop.  All
+// control-path global loads (row numbers, draft tokens, the next rollout) are issued by
+// thread 0 one stage early and published through shared memory.
 //   * P1: NaN-propagating bf16x2 max over the slice (1-D bulk async copies on the TMA
 //     engine, mbarrier completion, L2 evict-first);
 //   * P2: masses of reading R with packed FFMA2/FADD2, exact u64 per-warp sums;
 //   * DEC: Z, mass(d) -> accept (Philox counter (pos+j, ACCEPT), drawn under P1); a
-//     residual / bonus sample is found by the CTA holding the CDF crossing, which
-//     rescans the crossing warp's 256-element tiles and finalizes the rollout.
+//     residual / bonus sample is found by the CTA holding the CDF crossing: all its
+//     warps sum the crossing warp's tiles in parallel, one warp scans the crossing tile.
 #include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
@@ -89,17 +90,26 @@ struct SumRec {
     unsigned long long massd;  // mass of the draft token if it lies in the slice
 };
 
+// Slot metadata, written by thread 0 (issuer), read by every thread after a barrier.
+struct SlotMeta {
+    int32_t b, j, q, d;  // rollout, row, clamped draft length, d_{j+1} (-1 if j == q)
+    int32_t bulk;        // elements of this CTA's slice staged by the bulk copy
+    int32_t pad[3];
+};
+
 struct __align__(16) VShared {
     uint64_t full[2];     // TMA completion, one per slot buffer
     uint64_t bar_max[2];  // C arrivals per row: slice maxima of the slot's row
     uint64_t bar_sum[2];  // C arrivals per row: slice sums of the slot's row
     MaxRec rmax[2][2][MAXC];
     SumRec rsum[2][2][MAXC];
+    SlotMeta meta[2];
     int32_t init_rollouts[4];
     // CTA-local
     float wmax[32];
     uint32_t wbad[32];
     unsigned long long wsum[2][32];  // per slot: exact per-warp sums (sample search)
+    unsigned long long tsum[32];     // sample search: sums of the crossing warp's tiles
     uint32_t rng[2][8];              // per slot: Philox ACCEPT (0-3) and SAMPLE (4-7) draws
     unsigned long long stat[STAT_COUNT];
 };
@@ -154,6 +164,18 @@ __device__ __forceinline__ uint64_t mass8(const uint4 v, const MassParams& mp) {
     return ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
 }
 
+// Masses of one lane's 8 elements of a tile with element `excl` (slice-local) zeroed.
+__device__ __forceinline__ void mass8_excl(const uint4 v, const MassParams& mp, int e0, int excl,
+                                           uint64_t mm[8]) {
+    mass_pair(v.x, mp, mm[0], mm[1]);
+    mass_pair(v.y, mp, mm[2], mm[3]);
+    mass_pair(v.z, mp, mm[4], mm[5]);
+    mass_pair(v.w, mp, mm[6], mm[7]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (e0 + i == excl) mm[i] = 0;
+}
+
 __device__ __forceinline__ uint32_t hmax2_nan_u32(uint32_t a, uint32_t b) {
     __nv_bfloat162 x, y;
     memcpy(&x, &a, 4);
@@ -169,18 +191,18 @@ __device__ __forceinline__ float bf16_at(const uint16_t* sl, int e) {
 }
 
 // ------------------------------------------------------------------ helpers per row
-__device__ __forceinline__ const uint16_t* row_ptr(const VerifyArgs& a, int b, int j) {
+__device__ __forceinline__ int64_t row_no(const VerifyArgs& a, int b, int j) {
     const int kp1 = a.k + 1;
-    const int64_t rowno = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
-    return a.logits + rowno * a.stride;
+    return a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
 }
 
-// Issue the bulk copy of this CTA's slice of `row` into `buf` (elected thread).
-__device__ __forceinline__ void issue_load(const VerifyArgs& a, const uint16_t* row, int rank,
-                                           uint16_t* buf, uint64_t* bar, uint64_t pol) {
+// Issue the bulk copy of this CTA's slice of logits row `rowno` into `buf` (thread 0);
+// returns the number of elements the bulk copy stages (the rest is loaded by the CTA).
+__device__ __forceinline__ int issue_load(const VerifyArgs& a, int64_t rowno, int rank,
+                                          uint16_t* buf, uint64_t* bar, uint64_t pol) {
     const int s0 = rank * a.SL, s1 = min(a.V, s0 + a.SL);
     const int len = max(0, s1 - s0);
-    const uint16_t* src = row + s0;
+    const uint16_t* src = a.logits + rowno * a.stride + s0;
     const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
     const int bulk = aligned ? (len & ~7) : 0;
     fence_proxy_async_smem();
@@ -192,6 +214,7 @@ __device__ __forceinline__ void issue_load(const VerifyArgs& a, const uint16_t* 
     } else {
         mbar_arrive(bar);
     }
+    return bulk;
 }
 
 // Alg. 1 lines 10-31 for rollout b decided at row j (all rows < j accepted).
@@ -229,16 +252,15 @@ __device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int j,
     }
 }
 
-// Per-slot state kept (uniformly) in registers of every thread.
-struct Slot {
-    int stage;  // 0 = P1, 1 = P2, 2 = DEC, 3 = empty
-    int ri;     // index into active[]
-    int b, j, q, d;
-    int par;    // row parity of the exchange records / barriers
-    float m;    // row max (after P1 exchange)
-    bool ok;
-};
 enum { ST_P1 = 0, ST_P2 = 1, ST_DEC = 2, ST_EMPTY = 3 };
+
+// Thread 0's prefetched successors of a slot (registers of thread 0 only).
+struct Prefetch {
+    int64_t next_row;  // row (b, j+1)
+    int next_d;        // d_{j+2} (-1 when j+1 == q)
+    int nb, nq, nd;    // the spare rollout: b, q, d_1
+    int64_t nrow0;     // its row 0
+};
 
 template <int NT>
 __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
@@ -292,50 +314,51 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
     }
     __syncthreads();
     cluster.sync();
-    Slot S[2];
+    int stage[2], par[2];
+    Prefetch pf[2];
     for (int x = 0; x < 2; ++x) {
         const int ri = sh.init_rollouts[x];
-        S[x].ri = ri;
-        S[x].stage = (ri < nact) ? ST_P1 : ST_EMPTY;
-        S[x].j = 0;
-        S[x].par = 0;
-        S[x].b = (ri < nact) ? a.active[ri] : 0;
-        S[x].q = (ri < nact) ? a.rb_q[S[x].b] : 0;
-        S[x].d = -1;
-        S[x].m = 0.f;
-        S[x].ok = true;
-        if (tid == 0 && ri < nact) issue_load(a, row_ptr(a, S[x].b, 0), rank, bufs[x], &sh.full[x], pol);
+        stage[x] = (ri < nact) ? ST_P1 : ST_EMPTY;
+        par[x] = 0;
+        if (tid == 0 && ri < nact) {
+            const int b = a.active[ri];
+            const int q = a.rb_q[b];
+            SlotMeta& mt = sh.meta[x];
+            mt.b = b;
+            mt.j = 0;
+            mt.q = q;
+            mt.d = (q > 0) ? a.draft[(int64_t)b * a.k] : -1;
+            mt.bulk = issue_load(a, row_no(a, b, 0), rank, bufs[x], &sh.full[x], pol);
+        }
     }
+    __syncthreads();
     uint32_t fph[2] = {0u, 0u}, mph[2] = {0u, 0u}, sph[2] = {0u, 0u};  // barrier phases
+    float mrow[2] = {0.f, 0.f};
+    bool okrow[2] = {true, true};
 #ifdef BS_PHASE_TIMING
     long long ph_t = clock64();
 #endif
 
     // ------------------------------------------------------------ stage bodies
     auto stage_p1 = [&](int x) {
-        Slot& s = S[x];
         uint16_t* sl = bufs[x];
-        s.d = (s.j < s.q) ? a.draft[(int64_t)s.b * a.k + s.j] : -1;  // d_{j+1}, tested on row j
-        if (tid == 32) {  // the row's two Philox draws, under the max pass
-            const int slot = a.slots[s.b];
+        __syncthreads();  // meta[x] was rewritten by thread 0 when the slot advanced
+        const SlotMeta mt = sh.meta[x];
+        if (warp == NW - 1 && lane < 2) {  // the row's two Philox draws (one per lane), in
+            const int slot = a.slots[mt.b];  // the warp with the fewest max/mass tiles
             const uint64_t uidv = a.uid[slot];
-            const uint32_t position = (uint32_t)(a.pos[slot] + s.j);
-            const U128 r1 = draw(a.seed, uidv, position, PURPOSE_ACCEPT);
-            const U128 r2 = draw(a.seed, uidv, position, PURPOSE_SAMPLE);
-            sh.rng[x][0] = r1.x0; sh.rng[x][1] = r1.x1; sh.rng[x][2] = r1.x2; sh.rng[x][3] = r1.x3;
-            sh.rng[x][4] = r2.x0; sh.rng[x][5] = r2.x1; sh.rng[x][6] = r2.x2; sh.rng[x][7] = r2.x3;
+            const uint32_t position = (uint32_t)(a.pos[slot] + mt.j);
+            const U128 r = draw(a.seed, uidv, position, lane ? PURPOSE_SAMPLE : PURPOSE_ACCEPT);
+            uint32_t* o = sh.rng[x] + 4 * lane;
+            o[0] = r.x0; o[1] = r.x1; o[2] = r.x2; o[3] = r.x3;
         }
         mbar_wait(&sh.full[x], fph[x]);
         fph[x] ^= 1u;
         PH_MARK(1);
-        {   // ragged part (unaligned rows or a slice length not a multiple of 8)
-            const uint16_t* src = row_ptr(a, s.b, s.j) + s0;
-            const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
-            const int bulk = aligned ? (len & ~7) : 0;
-            if (bulk < len) {
-                for (int e = bulk + tid; e < len; e += NT) sl[e] = src[e];
-                __syncthreads();
-            }
+        if (mt.bulk < len) {  // ragged part (unaligned rows / slice length not a multiple of 8)
+            const uint16_t* src = a.logits + row_no(a, mt.b, mt.j) * a.stride + s0;
+            for (int e = mt.bulk + tid; e < len; e += NT) sl[e] = src[e];
+            __syncthreads();
         }
         uint32_t mx = 0xFF80FF80u;
         for (int t = t0; t < t1; ++t) {
@@ -367,24 +390,42 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
             }
             r.spare = (rank == 0) ? spv : -1;
             r.pad = 0;
-            cluster.map_shared_rank(&sh, tid)->rmax[x][s.par][rank] = r;
+            cluster.map_shared_rank(&sh, tid)->rmax[x][par[x]][rank] = r;
             mbar_arrive_remote(&sh.bar_max[x], (uint32_t)tid);
         }
-        s.stage = ST_P2;
+        stage[x] = ST_P2;
         PH_MARK(2);
     };
 
     auto stage_p2 = [&](int x) {
-        Slot& s = S[x];
         uint16_t* sl = bufs[x];
-        mbar_wait_cluster(&sh.bar_max[x], mph[x]);
+        // one thread acquires at cluster scope (its L1 invalidation is paid once), the CTA
+        // barrier then orders every thread after it
+        if (tid == 0) mbar_wait_cluster(&sh.bar_max[x], mph[x]);
         mph[x] ^= 1u;
+        __syncthreads();
         PH_MARK(3);
+        const SlotMeta mt = sh.meta[x];
+        const MaxRec* rec = sh.rmax[x][par[x]];
+        if (tid == 0) {  // prefetch the slot's successors (consumed at DEC)
+            Prefetch& p = pf[x];
+            if (mt.j < mt.q) {
+                p.next_row = row_no(a, mt.b, mt.j + 1);
+                p.next_d = (mt.j + 1 < mt.q) ? a.draft[(int64_t)mt.b * a.k + mt.j + 1] : -1;
+            }
+            const int nri = rec[0].spare;
+            if (nri >= 0) {
+                p.nb = a.active[nri];
+                p.nq = a.rb_q[p.nb];
+                p.nd = (p.nq > 0) ? a.draft[(int64_t)p.nb * a.k] : -1;
+                p.nrow0 = row_no(a, p.nb, 0);
+            }
+        }
         float m = -INFINITY;
         uint32_t bb = 0;
         for (int rr = 0; rr < C; ++rr) {
-            m = fmaxf(m, sh.rmax[x][s.par][rr].max);
-            bb |= sh.rmax[x][s.par][rr].bad;
+            m = fmaxf(m, rec[rr].max);
+            bb |= rec[rr].bad;
         }
         bool ok = true;
         uint32_t err = 0;
@@ -392,10 +433,10 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
         else if (m == -INFINITY) { ok = false; err |= DEV_ALL_NEGINF; }
         else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) { ok = false; err |= DEV_RANGE; }
         if (err && rank == 0 && tid == 0) atomicOr(a.dev_err, err);
-        s.m = m;
-        s.ok = ok;
-        SumRec rec;
-        rec.massd = 0ull;
+        mrow[x] = m;
+        okrow[x] = ok;
+        SumRec out;
+        out.massd = 0ull;
         if (a.T == 0.f) {  // greedy (R1): first index attaining the max
             int first = 0x7FFFFFFF;
             if (ok) {
@@ -418,44 +459,53 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
             __syncthreads();
             int f = 0x7FFFFFFF;
             for (int w = 0; w < NW; ++w) f = min(f, (int)sh.wsum[x][w]);
-            rec.sum = (unsigned long long)(uint32_t)((f == 0x7FFFFFFF) ? f : s0 + f);
+            out.sum = (unsigned long long)(uint32_t)((f == 0x7FFFFFFF) ? f : s0 + f);
         } else {  // integer masses (R2-R4), exact sums
             mp.nmc = -__fmul_rn(m, a.c);
-            uint64_t acc = 0;
+            uint64_t acc0 = 0, acc1 = 0;
             if (ok) {
-                for (int t = t0; t < t1; ++t) acc += mass8(lds128(sl + t * 256 + lane * 8), mp);
+                int t = t0;
+                for (; t + 1 < t1; t += 2) {  // two tiles per step: 8 independent pair chains
+                    const uint4 v0 = lds128(sl + t * 256 + lane * 8);
+                    const uint4 v1 = lds128(sl + (t + 1) * 256 + lane * 8);
+                    acc0 += mass8(v0, mp);
+                    acc1 += mass8(v1, mp);
+                }
+                if (t < t1) acc0 += mass8(lds128(sl + t * 256 + lane * 8), mp);
             }
-            acc = warp_sum_u64(acc);
+            const uint64_t acc = warp_sum_u64(acc0 + acc1);
             if (lane == 0) sh.wsum[x][warp] = acc;
             __syncthreads();
             uint64_t sum = 0;
             for (int w = 0; w < NW; ++w) sum += sh.wsum[x][w];
-            rec.sum = sum;
-            if (ok && s.d >= s0 && s.d < s1) rec.massd = mass_of(bf16_at(sl, s.d - s0), mp);
+            out.sum = sum;
+            if (ok && mt.d >= s0 && mt.d < s1) out.massd = mass_of(bf16_at(sl, mt.d - s0), mp);
         }
         if (tid < C) {
-            cluster.map_shared_rank(&sh, tid)->rsum[x][s.par][rank] = rec;
+            cluster.map_shared_rank(&sh, tid)->rsum[x][par[x]][rank] = out;
             mbar_arrive_remote(&sh.bar_sum[x], (uint32_t)tid);
         }
-        s.stage = ST_DEC;
+        stage[x] = ST_DEC;
         PH_MARK(4);
     };
 
     auto stage_dec = [&](int x) {
-        Slot& s = S[x];
         uint16_t* sl = bufs[x];
-        mbar_wait_cluster(&sh.bar_sum[x], sph[x]);
+        if (tid == 0) mbar_wait_cluster(&sh.bar_sum[x], sph[x]);
         sph[x] ^= 1u;
+        __syncthreads();
         PH_MARK(5);
-        const int j = s.j, q = s.q, d = s.d, b = s.b;
-        const bool ok = s.ok;
-        bool accepted = false, finished = false, eos_acc = false;
+        const SlotMeta mt = sh.meta[x];
+        const int j = mt.j, q = mt.q, d = mt.d, b = mt.b;
+        const bool ok = okrow[x];
+        const SumRec* rs = sh.rsum[x][par[x]];
+        bool finished;
         if (a.T == 0.f) {
             int g = 0x7FFFFFFF;
-            for (int rr = 0; rr < C; ++rr) g = min(g, (int)(uint32_t)sh.rsum[x][s.par][rr].sum);
+            for (int rr = 0; rr < C; ++rr) g = min(g, (int)(uint32_t)rs[rr].sum);
             g = ok ? g : -1;
-            accepted = ok && j < q && d == g;
-            eos_acc = accepted && a.eos >= 0 && d == a.eos;
+            const bool accepted = ok && j < q && d == g;
+            const bool eos_acc = accepted && a.eos >= 0 && d == a.eos;
             finished = !accepted || eos_acc;
             if (rank == 0 && tid == 0) {
                 if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? 1.0f : 0.f;
@@ -465,14 +515,15 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
         } else {
             uint64_t Zs = 0, md = 0;
             for (int rr = 0; rr < C; ++rr) {
-                Zs += sh.rsum[x][s.par][rr].sum;
-                md += sh.rsum[x][s.par][rr].massd;
+                Zs += rs[rr].sum;
+                md += rs[rr].massd;
             }
+            bool accepted = false;
             if (ok && j < q) {
                 const U128 r1{sh.rng[x][0], sh.rng[x][1], sh.rng[x][2], sh.rng[x][3]};
                 accepted = uniform_floor(r1, Zs) < md;
             }
-            eos_acc = accepted && a.eos >= 0 && d == a.eos;
+            const bool eos_acc = accepted && a.eos >= 0 && d == a.eos;
             finished = !accepted || eos_acc;
             if (rank == 0 && tid == 0) {
                 const uint64_t Zo = ok ? Zs : 0ull;
@@ -482,8 +533,8 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
                 else if (eos_acc) finalize_rollout(a, sh, b, j, q, true, -1);
             }
             if (ok && finished && !eos_acc) {
-                // residual (rejection: d excluded) or bonus sample (R8): which CTA / warp
-                // holds the CDF crossing?  (computed redundantly, no synchronisation)
+                // residual (rejection: d excluded) or bonus sample (R8): which CTA holds the
+                // CDF crossing?  (computed redundantly, no synchronisation)
                 const int excl = (j < q) ? d : -1;
                 const U128 r2{sh.rng[x][4], sh.rng[x][5], sh.rng[x][6], sh.rng[x][7]};
                 const uint64_t U2 = uniform_floor(r2, Zs - ((j < q) ? md : 0ull));
@@ -492,7 +543,7 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
                 uint64_t ul = 0;
                 for (int rr = 0; rr < C; ++rr) {
                     const int r0 = rr * a.SL, r1e = min(a.V, r0 + a.SL);
-                    const uint64_t adj = sh.rsum[x][s.par][rr].sum - ((excl >= r0 && excl < r1e) ? md : 0ull);
+                    const uint64_t adj = rs[rr].sum - ((excl >= r0 && excl < r1e) ? md : 0ull);
                     if (U2 < before + adj) {
                         cross = rr;
                         ul = U2 - before;
@@ -500,55 +551,62 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
                     }
                     before += adj;
                 }
-                if (cross == rank) {
-                    int wstar = -1;
-                    uint64_t uw = 0;
+                if (cross == rank) {  // this CTA samples (uniform inside the CTA)
+                    const int lex = excl - s0;  // slice-local excluded index
+                    int wstar = 0;
                     before = 0;
-                    const int span = tpw * 256;
                     for (int w = 0; w < NW; ++w) {
-                        const int w0 = s0 + w * span, w1 = min(s1, w0 + span);
-                        const uint64_t adj = sh.wsum[x][w] - ((excl >= w0 && excl < w1) ? md : 0ull);
+                        const int w0 = w * tpw * 256, w1 = min(len, w0 + tpw * 256);
+                        const uint64_t adj = sh.wsum[x][w] - ((lex >= w0 && lex < w1) ? md : 0ull);
                         if (ul < before + adj) {
                             wstar = w;
-                            uw = ul - before;
+                            ul -= before;
                             break;
                         }
                         before += adj;
                     }
-                    if (warp == wstar) {
-                        mp.nmc = -__fmul_rn(s.m, a.c);
-                        uint64_t run = 0;
-                        for (int t = t0; t < t1; ++t) {
-                            const int e0 = t * 256 + lane * 8;
-                            const uint4 v = lds128(sl + e0);
-                            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                            uint64_t mm[8];
+                    mp.nmc = -__fmul_rn(mrow[x], a.c);
+                    // tile sums of the crossing warp's tiles, all warps in parallel
+                    const int c0 = min(ntl, wstar * tpw), c1 = min(ntl, c0 + tpw);
+                    for (int t = c0 + warp; t < c1; t += NW) {
+                        uint64_t mm[8];
+                        mass8_excl(lds128(sl + t * 256 + lane * 8), mp, t * 256 + lane * 8, lex, mm);
+                        uint64_t ls = 0;
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) mass_pair(w4[i], mp, mm[2 * i], mm[2 * i + 1]);
-                            uint64_t ls = 0;
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                if (s0 + e0 + i == excl) mm[i] = 0;
-                                ls += mm[i];
-                            }
-                            const uint64_t incl = warp_incl_scan_u64(ls, lane);
-                            const uint64_t tot = shfl_u64(incl, 31);
-                            if (uw < run + tot) {
-                                const unsigned hit = __ballot_sync(0xFFFFFFFFu, uw < run + incl);
-                                const int L = __ffs(hit) - 1;
-                                if (lane == L) {
-                                    uint64_t cum = run + incl - ls;
-                                    int tok = -1;
-#pragma unroll
-                                    for (int i = 0; i < 8; ++i) {
-                                        cum += mm[i];
-                                        if (tok < 0 && cum > uw) tok = s0 + e0 + i;
-                                    }
-                                    finalize_rollout(a, sh, b, j, q, false, tok);
-                                }
+                        for (int i = 0; i < 8; ++i) ls += mm[i];
+                        ls = warp_sum_u64(ls);
+                        if (lane == 0) sh.tsum[t - c0] = ls;
+                    }
+                    __syncthreads();
+                    if (warp == 0) {  // crossing tile, then the crossing lane and element
+                        int tstar = c0;
+                        uint64_t ut = ul;
+                        for (int t = c0; t < c1; ++t) {
+                            const uint64_t ts = sh.tsum[t - c0];
+                            if (ut < ts) {
+                                tstar = t;
                                 break;
                             }
-                            run += tot;
+                            ut -= ts;
+                        }
+                        uint64_t mm[8];
+                        const int e0 = tstar * 256 + lane * 8;
+                        mass8_excl(lds128(sl + e0), mp, e0, lex, mm);
+                        uint64_t ls = 0;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) ls += mm[i];
+                        const uint64_t incl = warp_incl_scan_u64(ls, lane);
+                        const unsigned hit = __ballot_sync(0xFFFFFFFFu, ut < incl);
+                        const int L = hit ? (__ffs(hit) - 1) : 31;
+                        if (lane == L) {
+                            uint64_t cum = incl - ls;
+                            int tok = -1;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                cum += mm[i];
+                                if (tok < 0 && cum > ut) tok = s0 + e0 + i;
+                            }
+                            finalize_rollout(a, sh, b, j, q, false, tok);
                         }
                     }
                 }
@@ -556,27 +614,34 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
         }
         PH_MARK(6);
         // ---- advance the slot: the next row of this rollout, or the slot's spare rollout
-        s.par ^= 1;
+        const int nri = sh.rmax[x][par[x]][0].spare;  // broadcast with this row's P1
+        par[x] ^= 1;
         if (!finished) {
-            s.j = j + 1;
-            s.stage = ST_P1;
-            if (tid == 0) issue_load(a, row_ptr(a, b, j + 1), rank, bufs[x], &sh.full[x], pol);
+            stage[x] = ST_P1;
+            if (tid == 0) {
+                SlotMeta& m2 = sh.meta[x];
+                m2.j = j + 1;
+                m2.d = pf[x].next_d;
+                m2.bulk = issue_load(a, pf[x].next_row, rank, bufs[x], &sh.full[x], pol);
+            }
         } else {
-            const int nri = sh.rmax[x][s.par ^ 1][0].spare;  // broadcast with this row's P1
-            __syncthreads();  // the sampling warp is done with bufs[x]
+            __syncthreads();  // the sampling warps are done with bufs[x] and meta[x]
             if (nri >= 0) {
-                s.ri = nri;
-                s.b = a.active[nri];
-                s.q = a.rb_q[s.b];
-                s.j = 0;
-                s.stage = ST_P1;
-                if (tid == 0) issue_load(a, row_ptr(a, s.b, 0), rank, bufs[x], &sh.full[x], pol);
+                stage[x] = ST_P1;
+                if (tid == 0) {
+                    SlotMeta& m2 = sh.meta[x];
+                    m2.b = pf[x].nb;
+                    m2.j = 0;
+                    m2.q = pf[x].nq;
+                    m2.d = pf[x].nd;
+                    m2.bulk = issue_load(a, pf[x].nrow0, rank, bufs[x], &sh.full[x], pol);
+                }
                 if (rank == 0 && tid == 0) {  // claim the next spare for this slot
                     const int c2 = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
                     spare_reg[x] = (c2 < nact) ? c2 : -1;
                 }
             } else {
-                s.stage = ST_EMPTY;
+                stage[x] = ST_EMPTY;
             }
         }
         PH_MARK(7);
@@ -588,13 +653,13 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
     // ------------------------------------------------------------ the pipelined schedule
     for (;;) {
         PH_MARK(0);
-        if (S[0].stage == ST_P1) stage_p1(0);
-        if (S[1].stage == ST_DEC) stage_dec(1);
-        if (S[0].stage == ST_P2) stage_p2(0);
-        if (S[1].stage == ST_P1) stage_p1(1);
-        if (S[0].stage == ST_DEC) stage_dec(0);
-        if (S[1].stage == ST_P2) stage_p2(1);
-        if (S[0].stage == ST_EMPTY && S[1].stage == ST_EMPTY) break;
+        if (stage[0] == ST_P1) stage_p1(0);
+        if (stage[1] == ST_DEC) stage_dec(1);
+        if (stage[0] == ST_P2) stage_p2(0);
+        if (stage[1] == ST_P1) stage_p1(1);
+        if (stage[0] == ST_DEC) stage_dec(0);
+        if (stage[1] == ST_P2) stage_p2(1);
+        if (stage[0] == ST_EMPTY && stage[1] == ST_EMPTY) break;
     }
     // flush the CTA's statistics counters
     __syncthreads();
