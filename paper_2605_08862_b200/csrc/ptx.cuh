@@ -68,6 +68,21 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
         : "memory");
 }
 
+// 16-byte asynchronous store into CTA `rank`'s shared memory at the offset of `dst`,
+// completing 16 transaction bytes on that CTA's mbarrier at the offset of `bar`
+// (st.async: no fence, the data and the completion signal travel together).
+__device__ __forceinline__ void st_async_v4(void* dst, uint4 v, uint64_t* bar, uint32_t rank) {
+    asm volatile(
+        "{\n"
+        ".reg .b32 ra, rb;\n"
+        "mapa.shared::cluster.u32 ra, %0, %6;\n"
+        "mapa.shared::cluster.u32 rb, %1, %6;\n"
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [ra], {%2, %3, %4, %5}, [rb];\n"
+        "}\n" ::"r"(smem_u32(dst)),
+        "r"(smem_u32(bar)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rank)
+        : "memory");
+}
+
 // L2 eviction-first policy for streamed logits (keeps the draft index resident in L2).
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t pol;

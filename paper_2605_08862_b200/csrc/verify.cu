@@ -263,7 +263,7 @@ struct Prefetch {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
+__global__ void __launch_bounds__(NT, 2) verify_rows_kernel(const VerifyArgs a) {
     constexpr int NW = NT / 32;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = a.C;
@@ -290,10 +290,14 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&sh.full[i], 1);
-            mbar_init(&sh.bar_max[i], (uint32_t)C);
-            mbar_init(&sh.bar_sum[i], (uint32_t)C);
+            mbar_init(&sh.bar_max[i], 1);  // one local arrive.expect_tx + C*16 async bytes
+            mbar_init(&sh.bar_sum[i], 1);
         }
         fence_mbar_init();
+        for (int i = 0; i < 2; ++i) {  // arm the first phase of every exchange barrier
+            mbar_arrive_expect_tx(&sh.bar_max[i], (uint32_t)C * 16u);
+            mbar_arrive_expect_tx(&sh.bar_sum[i], (uint32_t)C * 16u);
+        }
     }
     for (int i = tid; i < STAT_COUNT; i += NT) sh.stat[i] = 0ull;
     for (int e = len + tid; e < a.ntiles * 256; e += NT) {  // -inf padding past the slice
@@ -390,8 +394,9 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
             }
             r.spare = (rank == 0) ? spv : -1;
             r.pad = 0;
-            cluster.map_shared_rank(&sh, tid)->rmax[x][par[x]][rank] = r;
-            mbar_arrive_remote(&sh.bar_max[x], (uint32_t)tid);
+            uint4 v;
+            memcpy(&v, &r, 16);
+            st_async_v4(&sh.rmax[x][par[x]][rank], v, &sh.bar_max[x], (uint32_t)tid);
         }
         stage[x] = ST_P2;
         PH_MARK(2);
@@ -399,11 +404,11 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
 
     auto stage_p2 = [&](int x) {
         uint16_t* sl = bufs[x];
-        // one thread acquires at cluster scope (its L1 invalidation is paid once), the CTA
-        // barrier then orders every thread after it
-        if (tid == 0) mbar_wait_cluster(&sh.bar_max[x], mph[x]);
+        // the peers' records landed with their transaction bytes (st.async): a CTA-scope
+        // wait suffices; thread 0 then arms the barrier for the slot's next row
+        mbar_wait(&sh.bar_max[x], mph[x]);
         mph[x] ^= 1u;
-        __syncthreads();
+        if (tid == 0) mbar_arrive_expect_tx(&sh.bar_max[x], (uint32_t)C * 16u);
         PH_MARK(3);
         const SlotMeta mt = sh.meta[x];
         const MaxRec* rec = sh.rmax[x][par[x]];
@@ -482,8 +487,9 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
             if (ok && mt.d >= s0 && mt.d < s1) out.massd = mass_of(bf16_at(sl, mt.d - s0), mp);
         }
         if (tid < C) {
-            cluster.map_shared_rank(&sh, tid)->rsum[x][par[x]][rank] = out;
-            mbar_arrive_remote(&sh.bar_sum[x], (uint32_t)tid);
+            uint4 v;
+            memcpy(&v, &out, 16);
+            st_async_v4(&sh.rsum[x][par[x]][rank], v, &sh.bar_sum[x], (uint32_t)tid);
         }
         stage[x] = ST_DEC;
         PH_MARK(4);
@@ -491,9 +497,9 @@ __global__ void __launch_bounds__(NT) verify_rows_kernel(const VerifyArgs a) {
 
     auto stage_dec = [&](int x) {
         uint16_t* sl = bufs[x];
-        if (tid == 0) mbar_wait_cluster(&sh.bar_sum[x], sph[x]);
+        mbar_wait(&sh.bar_sum[x], sph[x]);
         sph[x] ^= 1u;
-        __syncthreads();
+        if (tid == 0) mbar_arrive_expect_tx(&sh.bar_sum[x], (uint32_t)C * 16u);
         PH_MARK(5);
         const SlotMeta mt = sh.meta[x];
         const int j = mt.j, q = mt.q, d = mt.d, b = mt.b;
