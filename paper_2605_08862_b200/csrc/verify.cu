@@ -24,6 +24,7 @@
 //     residual / bonus sample is found by the CTA holding the CDF crossing: all its
 //     warps sum the crossing warp's tiles in parallel, one warp scans the crossing tile.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -34,7 +35,7 @@ namespace cg = cooperative_groups;
 
 namespace bs {
 
-constexpr int MAXC = 8;  // max cluster size
+constexpr int MAXC = 16;  // max cluster size (16 is non-portable; B200 supports it)
 
 // Optional per-stage cycle accounting (build with -DBS_PHASE_TIMING; read with
 // bsx_phase_times): thread 0 of every CTA adds the clock64() delta of each stage.
@@ -262,8 +263,8 @@ struct Prefetch {
     int64_t nrow0;     // its row 0
 };
 
-template <int NT>
-__global__ void __launch_bounds__(NT, 2) verify_rows_kernel(const VerifyArgs a) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) verify_rows_kernel(const VerifyArgs a) {
     constexpr int NW = NT / 32;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = a.C;
@@ -726,20 +727,33 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     }
 }
 
+// Slice size limit (bytes per smem buffer; env BS_VERIFY_SLICE_KB overrides): small
+// slices -> bigger clusters -> more resident CTAs per SM to hide each other's latencies.
+static int slice_limit_bytes() {
+    static int lim = 0;
+    if (!lim) {
+        const char* e = getenv("BS_VERIFY_SLICE_KB");
+        lim = (e && atoi(e) > 0) ? atoi(e) * 1024 : 20 * 1024;
+    }
+    return lim;
+}
+
 static int pick_cluster(int V) {
-    // two slice buffers of <= ~40 KB: two CTAs per SM overlap each other's waits
     int C = 1;
-    while (C < MAXC && (int64_t)((V + C - 1) / C) * 2 > 40 * 1024) C <<= 1;
+    while (C < MAXC && (int64_t)((V + C - 1) / C) * 2 > slice_limit_bytes()) C <<= 1;
     return C;
 }
 
-template <int NT>
+template <int NT, int MINB>
 static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int n, cudaStream_t st) {
     const size_t smem = (size_t)a.ntiles * 1024 + sizeof(VShared);
     static int configured = 0;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(verify_rows_kernel<NT>,
+        cudaError_t e = cudaFuncSetAttribute(verify_rows_kernel<NT, MINB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(verify_rows_kernel<NT, MINB>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         configured = 1;
     }
@@ -761,7 +775,7 @@ static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int n, cudaStre
     if (max_clusters == 0 || max_for_smem != smem || max_for_c != a.C) {
         cfg.gridDim = dim3((unsigned)(a.C * num_sms), 1, 1);
         int mc = 0;
-        cudaError_t e = cudaOccupancyMaxActiveClusters(&mc, verify_rows_kernel<NT>, &cfg);
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&mc, verify_rows_kernel<NT, MINB>, &cfg);
         if (e != cudaSuccess || mc < 1) {
             cudaGetLastError();
             mc = std::max(1, num_sms / a.C);
@@ -772,7 +786,7 @@ static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int n, cudaStre
     }
     const int clusters = std::max(1, std::min(max_clusters, (n + 1) / 2));
     cfg.gridDim = dim3((unsigned)(clusters * a.C), 1, 1);
-    return cudaLaunchKernelEx(&cfg, verify_rows_kernel<NT>, a);
+    return cudaLaunchKernelEx(&cfg, verify_rows_kernel<NT, MINB>, a);
 }
 
 cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits,
@@ -817,8 +831,12 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.out_norm = out_norm;
     a.out_z = out_z;
     a.stats = ctx->stats.p;
-    if (a.SL >= 4096) return launch_rows<256>(a, ctx->num_sms, n, st);
-    return launch_rows<128>(a, ctx->num_sms, n, st);
+    if (a.SL >= 4096) {
+        if ((size_t)a.ntiles * 1024 + sizeof(VShared) <= 72 * 1024)
+            return launch_rows<256, 3>(a, ctx->num_sms, n, st);  // three CTAs per SM
+        return launch_rows<256, 2>(a, ctx->num_sms, n, st);
+    }
+    return launch_rows<128, 4>(a, ctx->num_sms, n, st);
 }
 
 }  // namespace bs
