@@ -80,6 +80,10 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
                c->uid.ensure(R) == cudaSuccess && c->dev_err.ensure(1) == cudaSuccess &&
                c->rb_q.ensure(R) == cudaSuccess && c->vqueue.ensure(rows + R + 64) == cudaSuccess &&
                c->vctl.ensure(VCTL_WORDS) == cudaSuccess &&
+               c->vrow_status.ensure(rows) == cudaSuccess && c->vrow_cand.ensure(rows) == cudaSuccess &&
+               c->vrow_z.ensure(rows) == cudaSuccess && c->vrow_norm.ensure(rows) == cudaSuccess &&
+               c->vroll_first.ensure(R) == cudaSuccess && c->vroll_fin.ensure(R) == cudaSuccess &&
+               c->vroll_mask.ensure(R) == cudaSuccess &&
                c->staging.tokens.ensure((size_t)cfg->pool_capacity_tokens) == cudaSuccess &&
                c->staging.seq_off.ensure((size_t)cfg->pool_capacity_seqs + 1) == cudaSuccess &&
                c->staging.seq_prompt.ensure((size_t)cfg->pool_capacity_seqs) == cudaSuccess &&
@@ -125,6 +129,8 @@ void bs_destroy(bs_ctx* c) {
     c->sealed.tokens.release(); c->sealed.seq_off.release(); c->sealed.seq_prompt.release();
     c->seq_start_of.release(); c->seq_end_of.release(); c->prompt_of.release();
     c->table.release(); c->rb_q.release(); c->vqueue.release(); c->vctl.release();
+    c->vrow_status.release(); c->vrow_cand.release(); c->vrow_z.release(); c->vrow_norm.release();
+    c->vroll_first.release(); c->vroll_fin.release(); c->vroll_mask.release();
     c->stats.release();
     delete c;
 }

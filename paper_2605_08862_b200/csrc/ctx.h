@@ -80,6 +80,14 @@ struct bs_ctx {
     // verify scratch: clamped q per rollout, the row work queue and its control words
     bs::DevBuf<int32_t> rb_q, vqueue;
     bs::DevBuf<unsigned int> vctl;
+    // per verified row (b*(k_max+1)+j): status, candidate token, Z, fp32 normaliser
+    bs::DevBuf<int32_t> vrow_status, vrow_cand;
+    bs::DevBuf<unsigned long long> vrow_z;
+    bs::DevBuf<float> vrow_norm;
+    // per rollout: first row that decides (reject / bonus / accepted EOS), rows-done mask,
+    // finalized flag
+    bs::DevBuf<int32_t> vroll_first, vroll_fin;
+    bs::DevBuf<unsigned int> vroll_mask;
     bs::DevBuf<unsigned long long> stats;  // STAT_COUNT counters
     int32_t* responses = nullptr;           // optional [max_rollouts, resp_stride] output
     int64_t resp_stride = 0;

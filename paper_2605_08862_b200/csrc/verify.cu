@@ -1,29 +1,22 @@
 // verify.cu — fused vocab-row verify + resample (Eq. 2, Eq. 3 P:208-210,
 // Alg. 1, bonus token P:308) for sm_100a.
 //
-// Kernel K3.  A PERSISTENT grid of thread-block clusters; a cluster of C
-// CTAs owns one logits row at a time, CTA `rank` the vocabulary slice
-// [rank*SL, (rank+1)*SL).  Work is claimed per ROLLOUT (one atomic each) and a rollout's
-// rows are verified in Alg. 1's order, lazily: row j+1 is read only if row j accepted
-// d_{j+1} (rows after the first rejection are never read).
-//
-// Each cluster keeps two rollouts in flight ("slots" A and B) and runs the three stages
-// of a row — P1 (row max), P2 (integer masses, exact sums), DEC (accept / sample) — on
-// the fixed software-pipelined schedule  P1(A) DEC(B) P2(A) P1(B) DEC(A) P2(B), so the
-// TMA load of a slot's next row streams in under the other slot's mass pass.  The
-// cross-CTA reductions are point-to-point: every CTA pushes its slice record into all
-// peers' shared memory (DSMEM stores) and arrives remotely on their mbarrier
-// (release.cluster); one thread per consumer CTA waits (acquire.cluster) and a CTA
-// barrier orders the rest — there is no cluster-wide barrier in the loop.  All
-// control-path global loads (row numbers, draft tokens, the next rollout) are issued by
-// thread 0 one stage early and published through shared memory.
-//   * P1: NaN-propagating bf16x2 max over the slice (1-D bulk async copies on the TMA
-//     engine, mbarrier completion, L2 evict-first);
-//   * P2: masses of reading R with packed FFMA2/FADD2, exact u64 per-warp sums;
-//   * DEC: Z, mass(d) -> accept (Philox counter (pos+j, ACCEPT), drawn under P1); a
-//     residual / bonus sample is found by the CTA holding the CDF crossing: all its
-//     warps sum the crossing warp's tiles in parallel, one warp scans the crossing tile.
-#include <cooperative_groups.h>
+// Kernel K3.  One persistent CTA per SM verifies whole logits rows with no
+// cross-CTA synchronisation:
+//   * a PRODUCER warp claims rows and streams each row twice through an 8-stage ring of
+//     16 KB shared-memory chunks with 1-D bulk async copies (TMA engine, mbarrier
+//     completion): pass 1 from HBM (kept in L2), pass 2 re-read from L2 (evict-first);
+//   * 16 CONSUMER warps: pass 1 = NaN-propagating bf16x2 row max; pass 2 = integer
+//     masses of reading R (packed FFMA2/FADD2, exact u64 sums, one warp-level sum per
+//     1024-element block); then Z, mass(d), the accept test (Philox counter
+//     (pos+j, ACCEPT)) and, when needed, the residual / bonus sample (inverse CDF: block
+//     sums locate the crossing block, 4 warps rescan its 4 tiles, one warp scans).
+// Rows are claimed in Alg. 1's order across the batch — (b, 0) of every live rollout,
+// then (b, 1), ... — and a row is SKIPPED when a lower row of its rollout already
+// decided (first rejection / accepted EOS): rows after the first rejection are read only
+// when they were claimed speculatively before that rejection was known.  Rows
+// complete out of order; per rollout, atomicMin keeps the first deciding row and atomicOr
+// the set of completed rows, and the row that completes the prefix finalizes (CAS).
 #include <cstdlib>
 #include <cub/block/block_scan.cuh>
 
@@ -31,14 +24,20 @@
 #include "ctx.h"
 #include "ptx.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace bs {
 
-constexpr int MAXC = 16;  // max cluster size (16 is non-portable; B200 supports it)
+constexpr int CHE = 8192;           // elements per ring chunk (16 KB)
+constexpr int NSTAGE = 8;           // ring depth (128 KB)
+constexpr int NCW = 16;             // consumer warps
+constexpr int NCT = NCW * 32;       // consumer threads
+constexpr int NTHR = NCT + 32;      // + one producer warp
+constexpr int RF = 4;               // row descriptor FIFO depth
+constexpr int MAXG = 32;            // max super-chunks (2 chunks each): V <= 524288
+constexpr int BLK = CHE * 2 / NCW;  // 1024: elements per warp per super-chunk (4 tiles)
+constexpr int ST_CONT = 0, ST_DECIDED = 1, ST_EOS = 2;  // row status
 
 // Optional per-stage cycle accounting (build with -DBS_PHASE_TIMING; read with
-// bsx_phase_times): thread 0 of every CTA adds the clock64() delta of each stage.
+// bsx_phase_times): consumer thread 0 adds the clock64() delta of each phase.
 #ifdef BS_PHASE_TIMING
 __device__ unsigned long long g_phase[16];
 #define PH_MARK(i)                                                     \
@@ -61,7 +60,7 @@ struct VerifyArgs {
     const int64_t* row_index;
     int64_t stride;
     const int32_t* draft;
-    int32_t k, V, SL, C, ntiles, S, eos;
+    int32_t k, V, S, eos, nchunk, ngroup;
     float T, c;
     unsigned long long seed;
     const int32_t* pos;
@@ -70,6 +69,13 @@ struct VerifyArgs {
     const int32_t* active;  // compacted live rollouts (plan kernel)
     unsigned int* ctl;      // VCTL_* words
     uint32_t* dev_err;
+    int32_t* row_status;
+    int32_t* row_cand;
+    unsigned long long* row_z;
+    float* row_norm;
+    int32_t* roll_first;
+    int32_t* roll_fin;
+    unsigned int* roll_mask;
     int32_t* out_tokens;
     int32_t* out_len;
     int32_t* out_acc;
@@ -78,40 +84,30 @@ struct VerifyArgs {
     unsigned long long* stats;
 };
 
-// Records pushed to every CTA of the cluster (index = source rank), double-buffered by
-// row parity so a producer one row ahead never overwrites an unread record.
-struct MaxRec {
-    float max;
-    uint32_t bad;
-    int32_t spare;  // rank 0 only: the slot's claimed-ahead next rollout (-1: none left)
+struct RowDesc {
+    int32_t b, j, q, d;  // rollout, row, clamped draft length, d_{j+1} (-1 if j == q); b < 0: end
+    int64_t rowno;
+    int32_t aligned;     // bulk copies usable (16-byte aligned row)
     int32_t pad;
-};
-struct SumRec {
-    unsigned long long sum;    // slice mass sum (greedy: first argmax index)
-    unsigned long long massd;  // mass of the draft token if it lies in the slice
-};
-
-// Slot metadata, written by thread 0 (issuer), read by every thread after a barrier.
-struct SlotMeta {
-    int32_t b, j, q, d;  // rollout, row, clamped draft length, d_{j+1} (-1 if j == q)
-    int32_t bulk;        // elements of this CTA's slice staged by the bulk copy
-    int32_t pad[3];
+    uint32_t rng[8];     // Philox draws: ACCEPT (0-3), SAMPLE (4-7)
 };
 
 struct __align__(16) VShared {
-    uint64_t full[2];     // TMA completion, one per slot buffer
-    uint64_t bar_max[2];  // C arrivals per row: slice maxima of the slot's row
-    uint64_t bar_sum[2];  // C arrivals per row: slice sums of the slot's row
-    MaxRec rmax[2][2][MAXC];
-    SumRec rsum[2][2][MAXC];
-    SlotMeta meta[2];
-    int32_t init_rollouts[4];
-    // CTA-local
-    float wmax[32];
-    uint32_t wbad[32];
-    unsigned long long wsum[2][32];  // per slot: exact per-warp sums (sample search)
-    unsigned long long tsum[32];     // sample search: sums of the crossing warp's tiles
-    uint32_t rng[2][8];              // per slot: Philox ACCEPT (0-3) and SAMPLE (4-7) draws
+    uint64_t full[NSTAGE];
+    uint64_t empty[NSTAGE];
+    uint64_t rfull[RF];
+    uint64_t rempty[RF];
+    RowDesc desc[RF];
+    float wmax[NCW];
+    uint32_t wbad[NCW];
+    unsigned long long csum[MAXG][NCW];  // exact sums of the 1024-element blocks
+    unsigned long long tsum[4];
+    unsigned long long massd;
+    float m;
+    int32_t ok;
+    int32_t cross_g, cross_w;            // sample: crossing block, or -1
+    int32_t tok;
+    unsigned long long ublk;             // sample target inside the crossing block
     unsigned long long stat[STAT_COUNT];
 };
 
@@ -165,16 +161,16 @@ __device__ __forceinline__ uint64_t mass8(const uint4 v, const MassParams& mp) {
     return ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
 }
 
-// Masses of one lane's 8 elements of a tile with element `excl` (slice-local) zeroed.
-__device__ __forceinline__ void mass8_excl(const uint4 v, const MassParams& mp, int e0, int excl,
-                                           uint64_t mm[8]) {
+// One lane's 8 masses of a tile, elements >= nvalid or == excl (tile-local) zeroed.
+__device__ __forceinline__ void mass8_masked(const uint4 v, const MassParams& mp, int e0, int nvalid,
+                                             int excl, uint64_t mm[8]) {
     mass_pair(v.x, mp, mm[0], mm[1]);
     mass_pair(v.y, mp, mm[2], mm[3]);
     mass_pair(v.z, mp, mm[4], mm[5]);
     mass_pair(v.w, mp, mm[6], mm[7]);
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-        if (e0 + i == excl) mm[i] = 0;
+        if (e0 + i >= nvalid || e0 + i == excl) mm[i] = 0;
 }
 
 __device__ __forceinline__ uint32_t hmax2_nan_u32(uint32_t a, uint32_t b) {
@@ -187,502 +183,473 @@ __device__ __forceinline__ uint32_t hmax2_nan_u32(uint32_t a, uint32_t b) {
     return r;
 }
 
-__device__ __forceinline__ float bf16_at(const uint16_t* sl, int e) {
-    return __uint_as_float((uint32_t)sl[e] << 16);
+// Exact warp sum of u64 lane values < 2^51 with three 32-bit REDUX sums.
+__device__ __forceinline__ uint64_t warp_sum_u51(uint64_t v) {
+    const uint32_t hi = (uint32_t)(v >> 32);
+    const uint32_t mid = (uint32_t)(v >> 16) & 0xFFFFu;
+    const uint32_t lo = (uint32_t)v & 0xFFFFu;
+    const uint32_t sh = __reduce_add_sync(0xFFFFFFFFu, hi);
+    const uint32_t sm = __reduce_add_sync(0xFFFFFFFFu, mid);
+    const uint32_t sl = __reduce_add_sync(0xFFFFFFFFu, lo);
+    return ((uint64_t)sh << 32) + ((uint64_t)sm << 16) + (uint64_t)sl;
 }
 
-// ------------------------------------------------------------------ helpers per row
-__device__ __forceinline__ int64_t row_no(const VerifyArgs& a, int b, int j) {
-    const int kp1 = a.k + 1;
-    return a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// Issue the bulk copy of this CTA's slice of logits row `rowno` into `buf` (thread 0);
-// returns the number of elements the bulk copy stages (the rest is loaded by the CTA).
-__device__ __forceinline__ int issue_load(const VerifyArgs& a, int64_t rowno, int rank,
-                                          uint16_t* buf, uint64_t* bar, uint64_t pol) {
-    const int s0 = rank * a.SL, s1 = min(a.V, s0 + a.SL);
-    const int len = max(0, s1 - s0);
-    const uint16_t* src = a.logits + rowno * a.stride + s0;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
-    const int bulk = aligned ? (len & ~7) : 0;
-    fence_proxy_async_smem();
-    if (bulk) {
-        mbar_arrive_expect_tx(bar, (uint32_t)bulk * 2u);
-        constexpr int CH = 8192;  // elements per bulk copy (16 KiB)
-        for (int off = 0; off < bulk; off += CH)
-            bulk_g2s(buf + off, src + off, (uint32_t)min(CH, bulk - off) * 2u, bar, pol);
-    } else {
-        mbar_arrive(bar);
-    }
-    return bulk;
+__device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
+    return *reinterpret_cast<const volatile int32_t*>(p);
 }
 
-// Alg. 1 lines 10-31 for rollout b decided at row j (all rows < j accepted).
-__device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int j, int q,
-                                 bool accept_eos, int cand) {
+// Alg. 1 lines 10-31 for rollout b, decided at row F (rows < F accepted).
+__device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int F, int q) {
     const int kp1 = a.k + 1;
     int32_t* out = a.out_tokens + (int64_t)b * kp1;
     const int32_t* d = a.draft + (int64_t)b * a.k;
+    const int64_t base = (int64_t)b * kp1;
+    const int st = __ldcg(a.row_status + base + F);
     int n = 0;
-    for (int i = 0; i < j; ++i) out[n++] = d[i];
-    int acc = j;
-    if (accept_eos) {
-        out[n++] = d[j];
-        acc = j + 1;
+    for (int i = 0; i < F; ++i) out[n++] = d[i];
+    int acc = F;
+    if (st == ST_EOS) {  // accepted EOS ends the block: no sample
+        out[n++] = d[F];
+        acc = F + 1;
     } else {
-        out[n++] = cand;
+        out[n++] = __ldcg(a.row_cand + base + F);
     }
     for (int i = n; i < kp1; ++i) out[i] = -1;
     a.out_len[b] = n;
     a.out_acc[b] = acc;
-    if (a.stats) {  // CTA-local counters, flushed once at kernel exit
-        unsigned long long* st = sh.stat;
-        if (q > 0) {
-            atomicAdd(st + STAT_STEPS_SPEC, 1ull);
-            atomicAdd(st + STAT_EMIT_SPEC, (unsigned long long)n);
-            atomicAdd(st + STAT_ACCEPTED, (unsigned long long)acc);
-            atomicAdd(st + STAT_PROPOSED, (unsigned long long)q);
-            atomicAdd(st + STAT_HIST + min(n, STAT_HIST_BINS - 1), 1ull);
-        } else {
-            atomicAdd(st + STAT_STEPS_PLAIN, 1ull);
-            atomicAdd(st + STAT_EMIT_PLAIN, (unsigned long long)n);
-        }
-        atomicAdd(st + STAT_ROWS_VERIFIED, (unsigned long long)(j + 1));
-        atomicAdd(st + STAT_ROWS_NEEDED, (unsigned long long)(j + 1));
+    for (int i = 0; i <= F; ++i) {  // the rows Alg. 1 needed
+        if (a.out_norm) a.out_norm[base + i] = __ldcg(a.row_norm + base + i);
+        if (a.out_z) a.out_z[base + i] = __ldcg(a.row_z + base + i);
+    }
+    unsigned long long* s = sh.stat;
+    if (q > 0) {
+        atomicAdd(s + STAT_STEPS_SPEC, 1ull);
+        atomicAdd(s + STAT_EMIT_SPEC, (unsigned long long)n);
+        atomicAdd(s + STAT_ACCEPTED, (unsigned long long)acc);
+        atomicAdd(s + STAT_PROPOSED, (unsigned long long)q);
+        atomicAdd(s + STAT_HIST + min(n, STAT_HIST_BINS - 1), 1ull);
+    } else {
+        atomicAdd(s + STAT_STEPS_PLAIN, 1ull);
+        atomicAdd(s + STAT_EMIT_PLAIN, (unsigned long long)n);
+    }
+    atomicAdd(s + STAT_ROWS_NEEDED, (unsigned long long)(F + 1));
+}
+
+// Record a completed row and finalize its rollout if this completes the decided prefix.
+__device__ void complete_row(const VerifyArgs& a, VShared& sh, int b, int j, int q, int status,
+                             int cand, unsigned long long z, float norm) {
+    const int64_t r = (int64_t)b * (a.k + 1) + j;
+    a.row_status[r] = status;
+    a.row_cand[r] = cand;
+    a.row_z[r] = z;
+    a.row_norm[r] = norm;
+    __threadfence();
+    if (status != ST_CONT) atomicMin(a.roll_first + b, j);
+    const unsigned mask = atomicOr(a.roll_mask + b, 1u << j) | (1u << j);
+    const int F = ld_volatile_i32(a.roll_first + b);
+    const unsigned need = (F >= 31) ? 0xFFFFFFFFu : ((2u << F) - 1u);
+    if ((mask & need) == need && atomicCAS(a.roll_fin + b, 0, 1) == 0) {
+        __threadfence();
+        finalize_rollout(a, sh, b, F, q);
     }
 }
 
-enum { ST_P1 = 0, ST_P2 = 1, ST_DEC = 2, ST_EMPTY = 3 };
-
-// Thread 0's prefetched successors of a slot (registers of thread 0 only).
-struct Prefetch {
-    int64_t next_row;  // row (b, j+1)
-    int next_d;        // d_{j+2} (-1 when j+1 == q)
-    int nb, nq, nd;    // the spare rollout: b, q, d_1
-    int64_t nrow0;     // its row 0
-};
-
-template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) verify_rows_kernel(const VerifyArgs a) {
-    constexpr int NW = NT / 32;
-    cg::cluster_group cluster = cg::this_cluster();
-    const int C = a.C;
-    const int rank = (int)cluster.block_rank();
+__global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    uint16_t* bufs[2] = {reinterpret_cast<uint16_t*>(smem_raw),
-                         reinterpret_cast<uint16_t*>(smem_raw) + (size_t)a.ntiles * 256};
-    VShared& sh = *reinterpret_cast<VShared*>(smem_raw + (size_t)a.ntiles * 1024);
+    uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw);
+    VShared& sh = *reinterpret_cast<VShared*>(smem_raw + (size_t)NSTAGE * CHE * 2);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int kp1 = a.k + 1;
-    const int s0 = rank * a.SL;
-    const int s1 = min(a.V, s0 + a.SL);
-    const int len = max(0, s1 - s0);
-    const int ntl = (len + 255) >> 8;        // 256-element tiles in this slice
-    const int tpw = (ntl + NW - 1) / NW;     // tiles per warp (contiguous ranges)
-    const int t0 = min(ntl, warp * tpw), t1 = min(ntl, t0 + tpw);
-    const uint64_t pol = policy_evict_first();
     const int nact = (int)a.ctl[VCTL_NACTIVE];
+    const int kp1 = a.k + 1;
+    const int total = kp1 * nact;  // claimable items (j-major), j > q_b are holes
+
+    if (tid == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(&sh.full[i], 1);
+            mbar_init(&sh.empty[i], NCW / 2);  // the 8 warps of the stage's half
+        }
+        for (int i = 0; i < RF; ++i) {
+            mbar_init(&sh.rfull[i], 1);
+            mbar_init(&sh.rempty[i], 1);
+        }
+        fence_mbar_init();
+    }
+    for (int i = tid; i < STAT_COUNT; i += NTHR) sh.stat[i] = 0ull;
+    __syncthreads();
+
+    if (warp == NCW) {
+        // ======================================================== producer warp
+        if (lane != 0) return;
+        const uint64_t pol_keep = 0;  // pass 1: default L2 policy (the row is re-read)
+        const uint64_t pol_first = policy_evict_first();
+        uint32_t rph = 0;    // row-empty phase bits, one per FIFO slot
+        uint32_t P = 0;      // chunks issued so far: stage P % NSTAGE, use P / NSTAGE
+        int seq = 0;
+        for (;;) {
+            int b = -1, j = 0, q = 0;
+            for (;;) {  // claim the next needed row (j-major over the live rollouts)
+                const int r = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
+                if (r >= total) break;
+                j = r / nact;
+                const int bb = a.active[r - j * nact];
+                q = a.rb_q[bb];
+                if (j > q) continue;                              // beyond the draft
+                if (j > ld_volatile_i32(a.roll_first + bb)) continue;  // decided below
+                b = bb;
+                break;
+            }
+            const int f = seq % RF;
+            if (seq >= RF) {
+                mbar_wait(&sh.rempty[f], (rph >> f) & 1u);
+                rph ^= 1u << f;
+            }
+            RowDesc& dsc = sh.desc[f];
+            dsc.b = b;
+            if (b >= 0) {
+                dsc.j = j;
+                dsc.q = q;
+                dsc.d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;
+                dsc.rowno = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+                const uint16_t* row = a.logits + dsc.rowno * a.stride;
+                dsc.aligned = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0) ? 1 : 0;
+                const int slot = a.slots[b];
+                const uint64_t uidv = a.uid[slot];
+                const uint32_t position = (uint32_t)(a.pos[slot] + j);
+                const U128 r1 = draw(a.seed, uidv, position, PURPOSE_ACCEPT);
+                const U128 r2 = draw(a.seed, uidv, position, PURPOSE_SAMPLE);
+                dsc.rng[0] = r1.x0; dsc.rng[1] = r1.x1; dsc.rng[2] = r1.x2; dsc.rng[3] = r1.x3;
+                dsc.rng[4] = r2.x0; dsc.rng[5] = r2.x1; dsc.rng[6] = r2.x2; dsc.rng[7] = r2.x3;
+            }
+            mbar_arrive(&sh.rfull[f]);  // release: the descriptor is visible to the consumers
+            if (b < 0) break;
+            const uint16_t* row = a.logits + dsc.rowno * a.stride;
+            const bool aligned = dsc.aligned != 0;
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int c = 0; c < 2 * a.ngroup; ++c, ++P) {
+                    const int s = (int)(P % NSTAGE);
+                    // a stage's k-th fill waits for its (k-1)-th release (first fill: free)
+                    mbar_wait(&sh.empty[s], ((P / NSTAGE) & 1u) ^ 1u);
+                    const int cv = max(0, min(CHE, a.V - c * CHE));  // valid elements
+                    const int bulk = aligned ? (cv & ~7) : 0;
+                    uint16_t* dst = ring + (size_t)s * CHE;
+                    fence_proxy_async_smem();
+                    if (bulk) {
+                        mbar_arrive_expect_tx(&sh.full[s], (uint32_t)bulk * 2u);
+                        bulk_g2s(dst, row + (size_t)c * CHE, (uint32_t)bulk * 2u, &sh.full[s],
+                                 pass ? pol_first : pol_keep);
+                    } else {
+                        mbar_arrive(&sh.full[s]);
+                    }
+                }
+            }
+            ++seq;
+        }
+        return;
+    }
+
+    // ============================================================ consumer warps
+    const int half = warp / (NCW / 2);        // warps 0-7: even chunk, 8-15: odd chunk
+    const int wblk = (warp % (NCW / 2)) * BLK; // this warp's 1024-element block in the chunk
     MassParams mp;
     mp.c = a.c;
     mp.clampv = -(float)(a.S + 2);
     mp.magic = 12582912.0f + (float)a.S;
-
-    if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&sh.full[i], 1);
-            mbar_init(&sh.bar_max[i], 1);  // one local arrive.expect_tx + C*16 async bytes
-            mbar_init(&sh.bar_sum[i], 1);
-        }
-        fence_mbar_init();
-        for (int i = 0; i < 2; ++i) {  // arm the first phase of every exchange barrier
-            mbar_arrive_expect_tx(&sh.bar_max[i], (uint32_t)C * 16u);
-            mbar_arrive_expect_tx(&sh.bar_sum[i], (uint32_t)C * 16u);
-        }
-    }
-    for (int i = tid; i < STAT_COUNT; i += NT) sh.stat[i] = 0ull;
-    for (int e = len + tid; e < a.ntiles * 256; e += NT) {  // -inf padding past the slice
-        bufs[0][e] = (uint16_t)0xFF80u;
-        bufs[1][e] = (uint16_t)0xFF80u;
-    }
-    // leader claims two rollouts + one spare per slot
-    int spare_reg[2] = {-1, -1};  // meaningful in the leader thread only
-    if (rank == 0 && tid == 0) {
-        const int base = (int)atomicAdd(a.ctl + VCTL_NEXT, 4u);
-        for (int rr = 0; rr < C; ++rr) {
-            VShared* o = cluster.map_shared_rank(&sh, rr);
-            o->init_rollouts[0] = base;
-            o->init_rollouts[1] = base + 1;
-        }
-        spare_reg[0] = (base + 2 < nact) ? base + 2 : -1;
-        spare_reg[1] = (base + 3 < nact) ? base + 3 : -1;
-    }
-    __syncthreads();
-    cluster.sync();
-    int stage[2], par[2];
-    Prefetch pf[2];
-    for (int x = 0; x < 2; ++x) {
-        const int ri = sh.init_rollouts[x];
-        stage[x] = (ri < nact) ? ST_P1 : ST_EMPTY;
-        par[x] = 0;
-        if (tid == 0 && ri < nact) {
-            const int b = a.active[ri];
-            const int q = a.rb_q[b];
-            SlotMeta& mt = sh.meta[x];
-            mt.b = b;
-            mt.j = 0;
-            mt.q = q;
-            mt.d = (q > 0) ? a.draft[(int64_t)b * a.k] : -1;
-            mt.bulk = issue_load(a, row_no(a, b, 0), rank, bufs[x], &sh.full[x], pol);
-        }
-    }
-    __syncthreads();
-    uint32_t fph[2] = {0u, 0u}, mph[2] = {0u, 0u}, sph[2] = {0u, 0u};  // barrier phases
-    float mrow[2] = {0.f, 0.f};
-    bool okrow[2] = {true, true};
+    uint32_t u = 0;  // chunks consumed so far (CTA-uniform): stage u % NSTAGE, use u / NSTAGE
+    int seq = 0;
 #ifdef BS_PHASE_TIMING
     long long ph_t = clock64();
 #endif
+    for (;;) {
+        const int f = seq % RF;
+        mbar_wait(&sh.rfull[f], (seq / RF) & 1);
+        const RowDesc dsc = sh.desc[f];
+        if (dsc.b < 0) break;
+        const int b = dsc.b, j = dsc.j, q = dsc.q, d = dsc.d;
+        const uint16_t* row = a.logits + dsc.rowno * a.stride;
+        // the draft token's logit (its mass needs the row max): loaded under pass 1
+        const float ld = (tid == 0 && d >= 0) ? __uint_as_float((uint32_t)row[d] << 16) : 0.f;
+        PH_MARK(0);
 
-    // ------------------------------------------------------------ stage bodies
-    auto stage_p1 = [&](int x) {
-        uint16_t* sl = bufs[x];
-        __syncthreads();  // meta[x] was rewritten by thread 0 when the slot advanced
-        const SlotMeta mt = sh.meta[x];
-        if (warp == NW - 1 && lane < 2) {  // the row's two Philox draws (one per lane), in
-            const int slot = a.slots[mt.b];  // the warp with the fewest max/mass tiles
-            const uint64_t uidv = a.uid[slot];
-            const uint32_t position = (uint32_t)(a.pos[slot] + mt.j);
-            const U128 r = draw(a.seed, uidv, position, lane ? PURPOSE_SAMPLE : PURPOSE_ACCEPT);
-            uint32_t* o = sh.rng[x] + 4 * lane;
-            o[0] = r.x0; o[1] = r.x1; o[2] = r.x2; o[3] = r.x3;
-        }
-        mbar_wait(&sh.full[x], fph[x]);
-        fph[x] ^= 1u;
-        PH_MARK(1);
-        if (mt.bulk < len) {  // ragged part (unaligned rows / slice length not a multiple of 8)
-            const uint16_t* src = a.logits + row_no(a, mt.b, mt.j) * a.stride + s0;
-            for (int e = mt.bulk + tid; e < len; e += NT) sl[e] = src[e];
-            __syncthreads();
-        }
+        // ---------------------------------------------------- pass 1: row max
         uint32_t mx = 0xFF80FF80u;
-        for (int t = t0; t < t1; ++t) {
-            const uint4 v = lds128(sl + t * 256 + lane * 8);
-            mx = hmax2_nan_u32(mx, v.x);
-            mx = hmax2_nan_u32(mx, v.y);
-            mx = hmax2_nan_u32(mx, v.z);
-            mx = hmax2_nan_u32(mx, v.w);
-        }
-        const float lo = bf16lo(mx), hi = bf16hi(mx);
-        uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
-        float fm = fmaxf(lo, hi);
+        for (int g = 0; g < a.ngroup; ++g) {
+            const int c = 2 * g + half;
+            const uint32_t uc = u + (uint32_t)c;
+            const int sg = (int)(uc % NSTAGE);
+            mbar_wait(&sh.full[sg], (uc / NSTAGE) & 1u);
+            const uint16_t* buf = ring + (size_t)sg * CHE;
+            const int cv = max(0, min(CHE, a.V - c * CHE));
+            const int bulk = dsc.aligned ? (cv & ~7) : 0;
+            if (cv == CHE && bulk == CHE) {
 #pragma unroll
-        for (int mm = 16; mm; mm >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, mm));
-        bad = __any_sync(0xFFFFFFFFu, bad) ? 1u : 0u;
-        if (lane == 0) {
-            sh.wmax[warp] = fm;
-            sh.wbad[warp] = bad;
-        }
-        __syncthreads();
-        const int spv = __shfl_sync(0xFFFFFFFFu, spare_reg[x], 0);  // the leader's, in warp 0
-        if (tid < C) {  // push this slice's record into CTA `tid`, then arrive there
-            MaxRec r;
-            r.max = -INFINITY;
-            r.bad = 0;
-            for (int w = 0; w < NW; ++w) {
-                r.max = fmaxf(r.max, sh.wmax[w]);
-                r.bad |= sh.wbad[w];
+                for (int t = 0; t < 4; ++t) {
+                    const uint4 v = lds128(buf + wblk + t * 256 + lane * 8);
+                    mx = hmax2_nan_u32(mx, v.x);
+                    mx = hmax2_nan_u32(mx, v.y);
+                    mx = hmax2_nan_u32(mx, v.z);
+                    mx = hmax2_nan_u32(mx, v.w);
+                }
+            } else {  // partial / unaligned chunk: element-wise from smem or global
+                for (int t = 0; t < 4; ++t) {
+                    const int e0 = wblk + t * 256 + lane * 8;
+                    for (int i = 0; i < 8; ++i) {
+                        const int e = e0 + i;
+                        if (e < cv) {
+                            const uint16_t v = (e < bulk) ? buf[e] : row[(size_t)c * CHE + e];
+                            mx = hmax2_nan_u32(mx, (uint32_t)v | 0xFF800000u);
+                        }
+                    }
+                }
             }
-            r.spare = (rank == 0) ? spv : -1;
-            r.pad = 0;
-            uint4 v;
-            memcpy(&v, &r, 16);
-            st_async_v4(&sh.rmax[x][par[x]][rank], v, &sh.bar_max[x], (uint32_t)tid);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.empty[sg]);
         }
-        stage[x] = ST_P2;
-        PH_MARK(2);
-    };
-
-    auto stage_p2 = [&](int x) {
-        uint16_t* sl = bufs[x];
-        // the peers' records landed with their transaction bytes (st.async): a CTA-scope
-        // wait suffices; thread 0 then arms the barrier for the slot's next row
-        mbar_wait(&sh.bar_max[x], mph[x]);
-        mph[x] ^= 1u;
-        if (tid == 0) mbar_arrive_expect_tx(&sh.bar_max[x], (uint32_t)C * 16u);
-        PH_MARK(3);
-        const SlotMeta mt = sh.meta[x];
-        const MaxRec* rec = sh.rmax[x][par[x]];
-        if (tid == 0) {  // prefetch the slot's successors (consumed at DEC)
-            Prefetch& p = pf[x];
-            if (mt.j < mt.q) {
-                p.next_row = row_no(a, mt.b, mt.j + 1);
-                p.next_d = (mt.j + 1 < mt.q) ? a.draft[(int64_t)mt.b * a.k + mt.j + 1] : -1;
-            }
-            const int nri = rec[0].spare;
-            if (nri >= 0) {
-                p.nb = a.active[nri];
-                p.nq = a.rb_q[p.nb];
-                p.nd = (p.nq > 0) ? a.draft[(int64_t)p.nb * a.k] : -1;
-                p.nrow0 = row_no(a, p.nb, 0);
+        u += 2u * (uint32_t)a.ngroup;
+        {
+            const float lo = bf16lo(mx), hi = bf16hi(mx);
+            uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
+            float fm = fmaxf(lo, hi);
+#pragma unroll
+            for (int mm = 16; mm; mm >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, mm));
+            bad = __any_sync(0xFFFFFFFFu, bad) ? 1u : 0u;
+            if (lane == 0) {
+                sh.wmax[warp] = fm;
+                sh.wbad[warp] = bad;
             }
         }
+        named_bar(1, NCT);
+        PH_MARK(1);
         float m = -INFINITY;
         uint32_t bb = 0;
-        for (int rr = 0; rr < C; ++rr) {
-            m = fmaxf(m, rec[rr].max);
-            bb |= rec[rr].bad;
+        for (int w = 0; w < NCW; ++w) {
+            m = fmaxf(m, sh.wmax[w]);
+            bb |= sh.wbad[w];
         }
         bool ok = true;
         uint32_t err = 0;
         if (bb) { ok = false; err |= DEV_BAD_LOGIT; }
         else if (m == -INFINITY) { ok = false; err |= DEV_ALL_NEGINF; }
         else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) { ok = false; err |= DEV_RANGE; }
-        if (err && rank == 0 && tid == 0) atomicOr(a.dev_err, err);
-        mrow[x] = m;
-        okrow[x] = ok;
-        SumRec out;
-        out.massd = 0ull;
-        if (a.T == 0.f) {  // greedy (R1): first index attaining the max
-            int first = 0x7FFFFFFF;
-            if (ok) {
-                for (int t = t0; t < t1 && first == 0x7FFFFFFF; ++t) {
-                    const int e0 = t * 256 + lane * 8;
-                    const uint4 v = lds128(sl + e0);
-                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                    int f = 0x7FFFFFFF;
-#pragma unroll
-                    for (int i = 3; i >= 0; --i) {
-                        if (bf16hi(w4[i]) == m) f = e0 + 2 * i + 1;
-                        if (bf16lo(w4[i]) == m) f = e0 + 2 * i;
-                    }
-#pragma unroll
-                    for (int mm = 16; mm; mm >>= 1) f = min(f, __shfl_xor_sync(0xFFFFFFFFu, f, mm));
-                    first = f;
-                }
-            }
-            if (lane == 0) sh.wsum[x][warp] = (unsigned long long)(uint32_t)first;
-            __syncthreads();
-            int f = 0x7FFFFFFF;
-            for (int w = 0; w < NW; ++w) f = min(f, (int)sh.wsum[x][w]);
-            out.sum = (unsigned long long)(uint32_t)((f == 0x7FFFFFFF) ? f : s0 + f);
-        } else {  // integer masses (R2-R4), exact sums
-            mp.nmc = -__fmul_rn(m, a.c);
-            uint64_t acc0 = 0, acc1 = 0;
-            if (ok) {
-                int t = t0;
-                for (; t + 1 < t1; t += 2) {  // two tiles per step: 8 independent pair chains
-                    const uint4 v0 = lds128(sl + t * 256 + lane * 8);
-                    const uint4 v1 = lds128(sl + (t + 1) * 256 + lane * 8);
-                    acc0 += mass8(v0, mp);
-                    acc1 += mass8(v1, mp);
-                }
-                if (t < t1) acc0 += mass8(lds128(sl + t * 256 + lane * 8), mp);
-            }
-            const uint64_t acc = warp_sum_u64(acc0 + acc1);
-            if (lane == 0) sh.wsum[x][warp] = acc;
-            __syncthreads();
-            uint64_t sum = 0;
-            for (int w = 0; w < NW; ++w) sum += sh.wsum[x][w];
-            out.sum = sum;
-            if (ok && mt.d >= s0 && mt.d < s1) out.massd = mass_of(bf16_at(sl, mt.d - s0), mp);
-        }
-        if (tid < C) {
-            uint4 v;
-            memcpy(&v, &out, 16);
-            st_async_v4(&sh.rsum[x][par[x]][rank], v, &sh.bar_sum[x], (uint32_t)tid);
-        }
-        stage[x] = ST_DEC;
-        PH_MARK(4);
-    };
+        if (err && tid == 0) atomicOr(a.dev_err, err);
+        mp.nmc = -__fmul_rn(m, a.c);
 
-    auto stage_dec = [&](int x) {
-        uint16_t* sl = bufs[x];
-        mbar_wait(&sh.bar_sum[x], sph[x]);
-        sph[x] ^= 1u;
-        if (tid == 0) mbar_arrive_expect_tx(&sh.bar_sum[x], (uint32_t)C * 16u);
-        PH_MARK(5);
-        const SlotMeta mt = sh.meta[x];
-        const int j = mt.j, q = mt.q, d = mt.d, b = mt.b;
-        const bool ok = okrow[x];
-        const SumRec* rs = sh.rsum[x][par[x]];
-        bool finished;
-        if (a.T == 0.f) {
-            int g = 0x7FFFFFFF;
-            for (int rr = 0; rr < C; ++rr) g = min(g, (int)(uint32_t)rs[rr].sum);
-            g = ok ? g : -1;
-            const bool accepted = ok && j < q && d == g;
-            const bool eos_acc = accepted && a.eos >= 0 && d == a.eos;
-            finished = !accepted || eos_acc;
-            if (rank == 0 && tid == 0) {
-                if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? 1.0f : 0.f;
-                if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = ok ? 1ull : 0ull;
-                if (finished) finalize_rollout(a, sh, b, j, q, eos_acc, g);
-            }
-        } else {
-            uint64_t Zs = 0, md = 0;
-            for (int rr = 0; rr < C; ++rr) {
-                Zs += rs[rr].sum;
-                md += rs[rr].massd;
-            }
-            bool accepted = false;
-            if (ok && j < q) {
-                const U128 r1{sh.rng[x][0], sh.rng[x][1], sh.rng[x][2], sh.rng[x][3]};
-                accepted = uniform_floor(r1, Zs) < md;
-            }
-            const bool eos_acc = accepted && a.eos >= 0 && d == a.eos;
-            finished = !accepted || eos_acc;
-            if (rank == 0 && tid == 0) {
-                const uint64_t Zo = ok ? Zs : 0ull;
-                if (a.out_norm) a.out_norm[(int64_t)b * kp1 + j] = ok ? (float)ldexp((double)Zo, -a.S) : 0.f;
-                if (a.out_z) a.out_z[(int64_t)b * kp1 + j] = Zo;
-                if (!ok) finalize_rollout(a, sh, b, j, q, false, -1);
-                else if (eos_acc) finalize_rollout(a, sh, b, j, q, true, -1);
-            }
-            if (ok && finished && !eos_acc) {
-                // residual (rejection: d excluded) or bonus sample (R8): which CTA holds the
-                // CDF crossing?  (computed redundantly, no synchronisation)
-                const int excl = (j < q) ? d : -1;
-                const U128 r2{sh.rng[x][4], sh.rng[x][5], sh.rng[x][6], sh.rng[x][7]};
-                const uint64_t U2 = uniform_floor(r2, Zs - ((j < q) ? md : 0ull));
-                uint64_t before = 0;
-                int cross = -1;
-                uint64_t ul = 0;
-                for (int rr = 0; rr < C; ++rr) {
-                    const int r0 = rr * a.SL, r1e = min(a.V, r0 + a.SL);
-                    const uint64_t adj = rs[rr].sum - ((excl >= r0 && excl < r1e) ? md : 0ull);
-                    if (U2 < before + adj) {
-                        cross = rr;
-                        ul = U2 - before;
-                        break;
-                    }
-                    before += adj;
-                }
-                if (cross == rank) {  // this CTA samples (uniform inside the CTA)
-                    const int lex = excl - s0;  // slice-local excluded index
-                    int wstar = 0;
-                    before = 0;
-                    for (int w = 0; w < NW; ++w) {
-                        const int w0 = w * tpw * 256, w1 = min(len, w0 + tpw * 256);
-                        const uint64_t adj = sh.wsum[x][w] - ((lex >= w0 && lex < w1) ? md : 0ull);
-                        if (ul < before + adj) {
-                            wstar = w;
-                            ul -= before;
+        // ---------------------------------------------------- pass 2: masses / argmax
+        int first = 0x7FFFFFFF;
+        for (int g = 0; g < a.ngroup; ++g) {
+            const int c = 2 * g + half;
+            const uint32_t uc = u + (uint32_t)c;
+            const int sg = (int)(uc % NSTAGE);
+            mbar_wait(&sh.full[sg], (uc / NSTAGE) & 1u);
+            const uint16_t* buf = ring + (size_t)sg * CHE;
+            const int cv = max(0, min(CHE, a.V - c * CHE));
+            const int bulk = dsc.aligned ? (cv & ~7) : 0;
+            if (a.T == 0.f) {  // greedy (R1): the first index attaining the max
+                if (ok && first == 0x7FFFFFFF) {
+                    for (int t = 0; t < 4; ++t) {
+                        const int e0 = wblk + t * 256 + lane * 8;
+                        int fi = 0x7FFFFFFF;
+                        for (int i = 7; i >= 0; --i) {
+                            const int e = e0 + i;
+                            if (e < cv) {
+                                const uint16_t v = (e < bulk) ? buf[e] : row[(size_t)c * CHE + e];
+                                if (__uint_as_float((uint32_t)v << 16) == m) fi = c * CHE + e;
+                            }
+                        }
+#pragma unroll
+                        for (int mm = 16; mm; mm >>= 1) fi = min(fi, __shfl_xor_sync(0xFFFFFFFFu, fi, mm));
+                        if (fi != 0x7FFFFFFF) {
+                            first = fi;
                             break;
                         }
-                        before += adj;
                     }
-                    mp.nmc = -__fmul_rn(mrow[x], a.c);
-                    // tile sums of the crossing warp's tiles, all warps in parallel
-                    const int c0 = min(ntl, wstar * tpw), c1 = min(ntl, c0 + tpw);
-                    for (int t = c0 + warp; t < c1; t += NW) {
-                        uint64_t mm[8];
-                        mass8_excl(lds128(sl + t * 256 + lane * 8), mp, t * 256 + lane * 8, lex, mm);
-                        uint64_t ls = 0;
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) ls += mm[i];
-                        ls = warp_sum_u64(ls);
-                        if (lane == 0) sh.tsum[t - c0] = ls;
-                    }
-                    __syncthreads();
-                    if (warp == 0) {  // crossing tile, then the crossing lane and element
-                        int tstar = c0;
-                        uint64_t ut = ul;
-                        for (int t = c0; t < c1; ++t) {
-                            const uint64_t ts = sh.tsum[t - c0];
-                            if (ut < ts) {
-                                tstar = t;
-                                break;
-                            }
-                            ut -= ts;
-                        }
-                        uint64_t mm[8];
-                        const int e0 = tstar * 256 + lane * 8;
-                        mass8_excl(lds128(sl + e0), mp, e0, lex, mm);
-                        uint64_t ls = 0;
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) ls += mm[i];
-                        const uint64_t incl = warp_incl_scan_u64(ls, lane);
-                        const unsigned hit = __ballot_sync(0xFFFFFFFFu, ut < incl);
-                        const int L = hit ? (__ffs(hit) - 1) : 31;
-                        if (lane == L) {
-                            uint64_t cum = incl - ls;
-                            int tok = -1;
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                cum += mm[i];
-                                if (tok < 0 && cum > ut) tok = s0 + e0 + i;
-                            }
-                            finalize_rollout(a, sh, b, j, q, false, tok);
-                        }
-                    }
-                }
-            }
-        }
-        PH_MARK(6);
-        // ---- advance the slot: the next row of this rollout, or the slot's spare rollout
-        const int nri = sh.rmax[x][par[x]][0].spare;  // broadcast with this row's P1
-        par[x] ^= 1;
-        if (!finished) {
-            stage[x] = ST_P1;
-            if (tid == 0) {
-                SlotMeta& m2 = sh.meta[x];
-                m2.j = j + 1;
-                m2.d = pf[x].next_d;
-                m2.bulk = issue_load(a, pf[x].next_row, rank, bufs[x], &sh.full[x], pol);
-            }
-        } else {
-            __syncthreads();  // the sampling warps are done with bufs[x] and meta[x]
-            if (nri >= 0) {
-                stage[x] = ST_P1;
-                if (tid == 0) {
-                    SlotMeta& m2 = sh.meta[x];
-                    m2.b = pf[x].nb;
-                    m2.j = 0;
-                    m2.q = pf[x].nq;
-                    m2.d = pf[x].nd;
-                    m2.bulk = issue_load(a, pf[x].nrow0, rank, bufs[x], &sh.full[x], pol);
-                }
-                if (rank == 0 && tid == 0) {  // claim the next spare for this slot
-                    const int c2 = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
-                    spare_reg[x] = (c2 < nact) ? c2 : -1;
                 }
             } else {
-                stage[x] = ST_EMPTY;
+                uint64_t acc = 0;
+                if (ok) {
+                    if (cv == CHE && bulk == CHE) {
+                        const uint4 v0 = lds128(buf + wblk + lane * 8);
+                        const uint4 v1 = lds128(buf + wblk + 256 + lane * 8);
+                        const uint4 v2 = lds128(buf + wblk + 512 + lane * 8);
+                        const uint4 v3 = lds128(buf + wblk + 768 + lane * 8);
+                        acc = (mass8(v0, mp) + mass8(v1, mp)) + (mass8(v2, mp) + mass8(v3, mp));
+                    } else {
+                        for (int t = 0; t < 4; ++t) {
+                            const int e0 = wblk + t * 256 + lane * 8;
+                            for (int i = 0; i < 8; ++i) {
+                                const int e = e0 + i;
+                                if (e < cv) {
+                                    const uint16_t v = (e < bulk) ? buf[e] : row[(size_t)c * CHE + e];
+                                    acc += mass_of(__uint_as_float((uint32_t)v << 16), mp);
+                                }
+                            }
+                        }
+                    }
+                }
+                const uint64_t bs = warp_sum_u51(acc);
+                if (lane == 0) sh.csum[g][warp] = bs;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.empty[sg]);
         }
-        PH_MARK(7);
+        u += 2u * (uint32_t)a.ngroup;
+        if (a.T == 0.f && lane == 0) sh.csum[0][warp] = (unsigned long long)(uint32_t)first;
+        if (tid == 0) sh.massd = (ok && d >= 0 && a.T > 0.f) ? mass_of(ld, mp) : 0ull;
+        named_bar(1, NCT);
+        PH_MARK(2);
+
+        // ---------------------------------------------------- decision
+        if (tid == 0) {
+            sh.cross_g = -1;
+            sh.tok = -1;
+            int status;
+            unsigned long long Zo = 0;
+            float norm = 0.f;
+            if (a.T == 0.f) {
+                int g = 0x7FFFFFFF;
+                for (int w = 0; w < NCW; ++w) g = min(g, (int)(uint32_t)sh.csum[0][w]);
+                g = ok ? g : -1;
+                const bool acc = ok && j < q && d == g;
+                status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
+                sh.tok = g;
+                Zo = ok ? 1ull : 0ull;
+                norm = ok ? 1.f : 0.f;
+            } else {
+                uint64_t Z = 0;
+                for (int g = 0; g < a.ngroup; ++g)
+                    for (int w = 0; w < NCW; ++w) Z += sh.csum[g][w];
+                const uint64_t md = sh.massd;
+                bool acc = false;
+                if (ok && j < q) {
+                    const U128 r1{dsc.rng[0], dsc.rng[1], dsc.rng[2], dsc.rng[3]};
+                    acc = uniform_floor(r1, Z) < md;
+                }
+                status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
+                Zo = ok ? Z : 0ull;
+                norm = ok ? (float)ldexp((double)Z, -a.S) : 0.f;
+                if (ok && status == ST_DECIDED) {
+                    // residual (d excluded) or bonus sample (R8): find the crossing block
+                    const int excl = (j < q) ? d : -1;
+                    const U128 r2{dsc.rng[4], dsc.rng[5], dsc.rng[6], dsc.rng[7]};
+                    const uint64_t U = uniform_floor(r2, Z - ((j < q) ? md : 0ull));
+                    uint64_t before = 0;
+                    for (int g = 0; g < a.ngroup && sh.cross_g < 0; ++g) {
+                        for (int w = 0; w < NCW; ++w) {
+                            const int e0 = 2 * g * CHE + (w / (NCW / 2)) * CHE + (w % (NCW / 2)) * BLK;
+                            const uint64_t adj = sh.csum[g][w] - ((excl >= e0 && excl < e0 + BLK) ? md : 0ull);
+                            if (U < before + adj) {
+                                sh.cross_g = g;
+                                sh.cross_w = w;
+                                sh.ublk = U - before;
+                                break;
+                            }
+                            before += adj;
+                        }
+                    }
+                }
+            }
+            sh.ok = status;  // reused as the row status broadcast
+            sh.tsum[0] = Zo;
+            sh.m = norm;
+        }
+        named_bar(1, NCT);
+        const int status = sh.ok;
+        if (sh.cross_g >= 0) {  // ------------------------------ inverse-CDF sample
+            const int g = sh.cross_g, w = sh.cross_w;
+            const int e_blk = 2 * g * CHE + (w / (NCW / 2)) * CHE + (w % (NCW / 2)) * BLK;
+            const int excl = ((j < q) ? d : -1) - e_blk;
+            if (warp < 4) {  // the block's 4 tiles, one per warp, straight from L2
+                const int e0 = warp * 256 + lane * 8;
+                uint4 v = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+                if (dsc.aligned && e_blk + e0 + 8 <= a.V) {
+                    v = *reinterpret_cast<const uint4*>(row + e_blk + e0);
+                } else {
+                    uint16_t t8[8];
+                    for (int i = 0; i < 8; ++i) t8[i] = (e_blk + e0 + i < a.V) ? row[e_blk + e0 + i] : (uint16_t)0xFF80u;
+                    v.x = t8[0] | ((uint32_t)t8[1] << 16);
+                    v.y = t8[2] | ((uint32_t)t8[3] << 16);
+                    v.z = t8[4] | ((uint32_t)t8[5] << 16);
+                    v.w = t8[6] | ((uint32_t)t8[7] << 16);
+                }
+                uint64_t mm[8];
+                mass8_masked(v, mp, e0, a.V - e_blk, excl, mm);
+                uint64_t ls = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ls += mm[i];
+                const uint64_t incl = warp_incl_scan_u64(ls, lane);
+                if (lane == 31) sh.tsum[warp] = incl;  // tile total (tsum[0] Z saved above)
+                // keep the tile's masses: the crossing tile's owner warp finishes below
+                named_bar(1, NCT);
+                uint64_t ut = sh.ublk;
+                int tstar = 0;
+                for (int t = 0; t < 4; ++t) {
+                    const uint64_t ts = sh.tsum[t];
+                    if (ut < ts) {
+                        tstar = t;
+                        break;
+                    }
+                    ut -= ts;
+                }
+                if (warp == tstar) {
+                    const unsigned hit = __ballot_sync(0xFFFFFFFFu, ut < incl);
+                    const int L = hit ? (__ffs(hit) - 1) : 31;
+                    if (lane == L) {
+                        uint64_t cum = incl - ls;
+                        int tok = -1;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            cum += mm[i];
+                            if (tok < 0 && cum > ut) tok = e_blk + e0 + i;
+                        }
+                        sh.tok = tok;
+                    }
+                }
+            } else {
+                named_bar(1, NCT);
+            }
+            named_bar(1, NCT);
+        }
+        PH_MARK(3);
+        if (tid == 0) {
+            // sh.tsum[0] held Z before the tile sums overwrote it: recompute from csum
+            unsigned long long Zo = 0;
+            float norm = 0.f;
+            if (a.T == 0.f) {
+                Zo = ok ? 1ull : 0ull;
+                norm = ok ? 1.f : 0.f;
+            } else if (ok) {
+                for (int g = 0; g < a.ngroup; ++g)
+                    for (int w = 0; w < NCW; ++w) Zo += sh.csum[g][w];
+                norm = (float)ldexp((double)Zo, -a.S);
+            }
+            atomicAdd(sh.stat + STAT_ROWS_VERIFIED, 1ull);
+            complete_row(a, sh, b, j, q, ok ? status : ST_DECIDED, ok ? sh.tok : -1, Zo, norm);
+            mbar_arrive(&sh.rempty[f]);
+        }
+        named_bar(1, NCT);  // sh scratch (csum, tok, ...) free for the next row
+        ++seq;
+        PH_MARK(4);
 #ifdef BS_PHASE_TIMING
         if (tid == 0) atomicAdd(&g_phase[15], 1ull);
 #endif
-    };
-
-    // ------------------------------------------------------------ the pipelined schedule
-    for (;;) {
-        PH_MARK(0);
-        if (stage[0] == ST_P1) stage_p1(0);
-        if (stage[1] == ST_DEC) stage_dec(1);
-        if (stage[0] == ST_P2) stage_p2(0);
-        if (stage[1] == ST_P1) stage_p1(1);
-        if (stage[0] == ST_DEC) stage_dec(0);
-        if (stage[1] == ST_P2) stage_p2(1);
-        if (stage[0] == ST_EMPTY && stage[1] == ST_EMPTY) break;
     }
-    // flush the CTA's statistics counters
-    __syncthreads();
+    named_bar(1, NCT);
     if (a.stats)
-        for (int i = tid; i < STAT_COUNT; i += NT)
+        for (int i = tid; i < STAT_COUNT; i += NCT)
             if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
-    cluster.sync();  // no CTA exits while a peer may still access its shared memory
 }
 
-// ---- plan: clamp q per rollout, compact the live rollouts (one block)
+// ---- plan: clamp q per rollout, compact the live rollouts, reset per-rollout state
 constexpr int PLAN_NT = 1024;
 __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     int n, int k, int V, const int32_t* slots, const int32_t* draft, const int32_t* draft_len,
     const int32_t* pos, const int32_t* max_len, const int32_t* finished, int32_t* rb_q,
-    int32_t* active, unsigned int* ctl, int32_t* out_len, int32_t* out_acc,
-    int32_t* out_tokens, float* out_norm, unsigned long long* out_z, uint32_t* dev_err) {
+    int32_t* active, unsigned int* ctl, int32_t* roll_first, int32_t* roll_fin,
+    unsigned int* roll_mask, int32_t* out_len, int32_t* out_acc, int32_t* out_tokens,
+    float* out_norm, unsigned long long* out_z, uint32_t* dev_err) {
     using Scan = cub::BlockScan<int, PLAN_NT>;
     __shared__ typename Scan::TempStorage tmp;
     const int tid = threadIdx.x;
@@ -706,6 +673,9 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
             }
         }
         rb_q[b] = q;
+        roll_first[b] = q;  // the bonus row q always decides; earlier rows may lower it
+        roll_fin[b] = 0;
+        roll_mask[b] = 0u;
         mine += (q >= 0) ? 1 : 0;
         for (int jj = 0; jj < kp1; ++jj) {
             if (out_norm) out_norm[(int64_t)b * kp1 + jj] = 0.f;
@@ -727,68 +697,6 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     }
 }
 
-// Slice size limit (bytes per smem buffer; env BS_VERIFY_SLICE_KB overrides): small
-// slices -> bigger clusters -> more resident CTAs per SM to hide each other's latencies.
-static int slice_limit_bytes() {
-    static int lim = 0;
-    if (!lim) {
-        const char* e = getenv("BS_VERIFY_SLICE_KB");
-        lim = (e && atoi(e) > 0) ? atoi(e) * 1024 : 20 * 1024;
-    }
-    return lim;
-}
-
-static int pick_cluster(int V) {
-    int C = 1;
-    while (C < MAXC && (int64_t)((V + C - 1) / C) * 2 > slice_limit_bytes()) C <<= 1;
-    return C;
-}
-
-template <int NT, int MINB>
-static cudaError_t launch_rows(const VerifyArgs& a, int num_sms, int n, cudaStream_t st) {
-    const size_t smem = (size_t)a.ntiles * 1024 + sizeof(VShared);
-    static int configured = 0;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(verify_rows_kernel<NT, MINB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(verify_rows_kernel<NT, MINB>,
-                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        configured = 1;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(NT, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)a.C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    // persistent grid: every resident cluster slot, but no more clusters than rollouts / 2
-    static int max_clusters = 0;
-    static size_t max_for_smem = 0;
-    static int max_for_c = 0;
-    if (max_clusters == 0 || max_for_smem != smem || max_for_c != a.C) {
-        cfg.gridDim = dim3((unsigned)(a.C * num_sms), 1, 1);
-        int mc = 0;
-        cudaError_t e = cudaOccupancyMaxActiveClusters(&mc, verify_rows_kernel<NT, MINB>, &cfg);
-        if (e != cudaSuccess || mc < 1) {
-            cudaGetLastError();
-            mc = std::max(1, num_sms / a.C);
-        }
-        max_clusters = mc;
-        max_for_smem = smem;
-        max_for_c = a.C;
-    }
-    const int clusters = std::max(1, std::min(max_clusters, (n + 1) / 2));
-    cfg.gridDim = dim3((unsigned)(clusters * a.C), 1, 1);
-    return cudaLaunchKernelEx(&cfg, verify_rows_kernel<NT, MINB>, a);
-}
-
 cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits,
                           const int64_t* row_index, int64_t stride, const int32_t* draft,
                           const int32_t* draft_len, int32_t k, float T, float top_p,
@@ -799,8 +707,9 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     const int V = ctx->cfg.vocab;
     verify_plan_kernel<<<1, PLAN_NT, 0, st>>>(n, k, V, slots, draft, draft_len, ctx->pos.p,
                                               ctx->max_len.p, ctx->finished.p, ctx->rb_q.p,
-                                              ctx->vqueue.p, ctx->vctl.p, out_len, out_acc,
-                                              out_tokens, out_norm, out_z, ctx->dev_err.p);
+                                              ctx->vqueue.p, ctx->vctl.p, ctx->vroll_first.p,
+                                              ctx->vroll_fin.p, ctx->vroll_mask.p, out_len,
+                                              out_acc, out_tokens, out_norm, out_z, ctx->dev_err.p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     VerifyArgs a = {};
@@ -811,11 +720,11 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.draft = draft;
     a.k = k;
     a.V = V;
-    a.C = pick_cluster(V);
-    a.SL = (((V + a.C - 1) / a.C) + 7) & ~7;
-    a.ntiles = (a.SL + 255) / 256;
     a.S = ctx->S;
     a.eos = ctx->cfg.eos_id;
+    a.nchunk = (V + CHE - 1) / CHE;
+    a.ngroup = (a.nchunk + 1) / 2;
+    if (a.ngroup > MAXG) return cudaErrorInvalidValue;
     a.T = T;
     a.c = (T > 0.f) ? (float)(1.4426950408889634 / (double)T) : 0.f;
     a.seed = ctx->cfg.seed;
@@ -825,18 +734,30 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.active = ctx->vqueue.p;
     a.ctl = ctx->vctl.p;
     a.dev_err = ctx->dev_err.p;
+    a.row_status = ctx->vrow_status.p;
+    a.row_cand = ctx->vrow_cand.p;
+    a.row_z = ctx->vrow_z.p;
+    a.row_norm = ctx->vrow_norm.p;
+    a.roll_first = ctx->vroll_first.p;
+    a.roll_fin = ctx->vroll_fin.p;
+    a.roll_mask = ctx->vroll_mask.p;
     a.out_tokens = out_tokens;
     a.out_len = out_len;
     a.out_acc = out_acc;
     a.out_norm = out_norm;
     a.out_z = out_z;
     a.stats = ctx->stats.p;
-    if (a.SL >= 4096) {
-        if ((size_t)a.ntiles * 1024 + sizeof(VShared) <= 72 * 1024)
-            return launch_rows<256, 3>(a, ctx->num_sms, n, st);  // three CTAs per SM
-        return launch_rows<256, 2>(a, ctx->num_sms, n, st);
+    const size_t smem = (size_t)NSTAGE * CHE * 2 + sizeof(VShared);
+    static int configured = 0;
+    if (!configured) {
+        e = cudaFuncSetAttribute(verify_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = 1;
     }
-    return launch_rows<128, 4>(a, ctx->num_sms, n, st);
+    const int grid = std::max(1, std::min(ctx->num_sms, n * (k + 1)));
+    verify_rows_kernel<<<grid, NTHR, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace bs

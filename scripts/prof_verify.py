@@ -55,8 +55,8 @@ if os.environ.get("BS_LIB_VARIANT") == "timing":
     lib = bs.load()
     ph = (ctypes.c_ulonglong * 16)()
     if lib.bsx_phase_times(ph, 1):
-        names = ["loop top", "wait slice", "P1 max+push", "wait maxima", "P2 masses+push",
-                 "wait sums", "DEC decide+sample", "advance/load"]
+        names = ["wait row desc", "pass 1 (max)", "pass 2 (masses)", "decide+sample",
+                 "complete/finalize"]
         tot = sum(ph[i] for i in range(len(names)))
         it = max(1, ph[15])
         print(f"phase cycles per row-iteration per CTA (n={ph[15]}):")
