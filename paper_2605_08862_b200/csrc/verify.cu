@@ -2,15 +2,18 @@
 // Alg. 1, bonus token P:308) for sm_100a.
 //
 // Kernel K3.  One persistent CTA per SM verifies whole logits rows with no
-// cross-CTA synchronisation:
-//   * a PRODUCER warp claims rows and streams each row twice through an 8-stage ring of
+// cross-CTA synchronisation, warp-specialized:
+//   * PRODUCER warp: claims rows and streams each row twice through an 8-stage ring of
 //     16 KB shared-memory chunks with 1-D bulk async copies (TMA engine, mbarrier
-//     completion): pass 1 from HBM (kept in L2), pass 2 re-read from L2 (evict-first);
-//   * 16 CONSUMER warps: pass 1 = NaN-propagating bf16x2 row max; pass 2 = integer
-//     masses of reading R (packed FFMA2/FADD2, exact u64 sums, one warp-level sum per
-//     1024-element block); then Z, mass(d), the accept test (Philox counter
-//     (pos+j, ACCEPT)) and, when needed, the residual / bonus sample (inverse CDF: block
-//     sums locate the crossing block, 4 warps rescan its 4 tiles, one warp scans).
+//     completion): pass 1 from HBM (left in L2), pass 2 re-read from L2 (evict-first);
+//   * 16 CONSUMER warps: pass 1 = NaN-propagating bf16x2 row max (the only CTA barrier
+//     of a row); pass 2 = integer masses of reading R (packed FFMA2/FADD2, exact u64
+//     sums, one warp-level sum per 1024-element block) handed to the epilogue through a
+//     double-buffered shared-memory record; then straight on to the next row;
+//   * EPILOGUE warp: Z, mass(d), the accept test (Philox counter (pos+j, ACCEPT)) and,
+//     when needed, the residual / bonus sample (inverse CDF: block sums locate the
+//     crossing 1024-element block, the warp rescans it from L2), then the rollout's
+//     bookkeeping — all off the consumers' critical path.
 // Rows are claimed in Alg. 1's order across the batch — (b, 0) of every live rollout,
 // then (b, 1), ... — and a row is SKIPPED when a lower row of its rollout already
 // decided (first rejection / accepted EOS): rows after the first rejection are read only
@@ -23,6 +26,7 @@
 #include "common.cuh"
 #include "ctx.h"
 #include "ptx.cuh"
+#include "verify_math.cuh"
 
 namespace bs {
 
@@ -30,7 +34,9 @@ constexpr int CHE = 8192;           // elements per ring chunk (16 KB)
 constexpr int NSTAGE = 8;           // ring depth (128 KB)
 constexpr int NCW = 16;             // consumer warps
 constexpr int NCT = NCW * 32;       // consumer threads
-constexpr int NTHR = NCT + 32;      // + one producer warp
+constexpr int PROD_WARP = NCW;      // producer warp
+constexpr int EPI_WARP = NCW + 1;   // epilogue warp
+constexpr int NTHR = NCT + 64;
 constexpr int RF = 4;               // row descriptor FIFO depth
 constexpr int MAXG = 32;            // max super-chunks (2 chunks each): V <= 524288
 constexpr int BLK = CHE * 2 / NCW;  // 1024: elements per warp per super-chunk (4 tiles)
@@ -92,115 +98,29 @@ struct RowDesc {
     uint32_t rng[8];     // Philox draws: ACCEPT (0-3), SAMPLE (4-7)
 };
 
+// Consumer -> epilogue handoff of one row (double-buffered).
+struct EpiBuf {
+    RowDesc dsc;
+    float m;
+    int32_t ok;
+    int32_t pad[2];
+    unsigned long long csum[MAXG][NCW];  // exact sums of the 1024-element blocks (greedy:
+                                         // csum[0][w] = first argmax index of warp w)
+};
+
 struct __align__(16) VShared {
     uint64_t full[NSTAGE];
     uint64_t empty[NSTAGE];
     uint64_t rfull[RF];
     uint64_t rempty[RF];
+    uint64_t efull[2];
+    uint64_t eempty[2];
     RowDesc desc[RF];
     float wmax[NCW];
     uint32_t wbad[NCW];
-    unsigned long long csum[MAXG][NCW];  // exact sums of the 1024-element blocks
-    unsigned long long tsum[4];
-    unsigned long long massd;
-    float m;
-    int32_t ok;
-    int32_t cross_g, cross_w;            // sample: crossing block, or -1
-    int32_t tok;
-    unsigned long long ublk;             // sample target inside the crossing block
+    EpiBuf epi[2];
     unsigned long long stat[STAT_COUNT];
 };
-
-// ------------------------------------------------------------------ packed fp32 math
-struct F2 {
-    float x, y;
-};
-__device__ __forceinline__ F2 ffma2(F2 a, F2 b, F2 c) {
-    F2 r;
-    asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-        " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
-        : "=f"(r.x), "=f"(r.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    return r;
-}
-__device__ __forceinline__ F2 fadd2(F2 a, F2 b) {
-    F2 r;
-    asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
-        " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
-        : "=f"(r.x), "=f"(r.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return r;
-}
-
-// Masses of the two bf16 logits packed in w (R2-R4), bit-identical to mass_of() per lane:
-// the packed FFMA2 / FADD2 perform the same IEEE single operations.
-__device__ __forceinline__ void mass_pair(uint32_t w, const MassParams& mp, uint64_t& m0,
-                                          uint64_t& m1) {
-    const F2 l{bf16lo(w), bf16hi(w)};
-    F2 y = ffma2(l, F2{mp.c, mp.c}, F2{mp.nmc, mp.nmc});
-    y.x = fmaxf(y.x, mp.clampv);
-    y.y = fmaxf(y.y, mp.clampv);
-    const F2 t = fadd2(y, F2{mp.magic, mp.magic});
-    const F2 n = fadd2(t, F2{-mp.magic, -mp.magic});
-    const F2 f = fadd2(y, F2{-n.x, -n.y});
-    F2 p = ffma2(F2{BS_C5, BS_C5}, f, F2{BS_C4, BS_C4});
-    p = ffma2(p, f, F2{BS_C3, BS_C3});
-    p = ffma2(p, f, F2{BS_C2, BS_C2});
-    p = ffma2(p, f, F2{BS_C1, BS_C1});
-    p = ffma2(p, f, F2{BS_C0, BS_C0});
-    m0 = f2u64_rz(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)));
-    m1 = f2u64_rz(__uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
-}
-
-__device__ __forceinline__ uint64_t mass8(const uint4 v, const MassParams& mp) {
-    uint64_t a0, a1, b0, b1, c0, c1, d0, d1;
-    mass_pair(v.x, mp, a0, a1);
-    mass_pair(v.y, mp, b0, b1);
-    mass_pair(v.z, mp, c0, c1);
-    mass_pair(v.w, mp, d0, d1);
-    return ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
-}
-
-// One lane's 8 masses of a tile, elements >= nvalid or == excl (tile-local) zeroed.
-__device__ __forceinline__ void mass8_masked(const uint4 v, const MassParams& mp, int e0, int nvalid,
-                                             int excl, uint64_t mm[8]) {
-    mass_pair(v.x, mp, mm[0], mm[1]);
-    mass_pair(v.y, mp, mm[2], mm[3]);
-    mass_pair(v.z, mp, mm[4], mm[5]);
-    mass_pair(v.w, mp, mm[6], mm[7]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        if (e0 + i >= nvalid || e0 + i == excl) mm[i] = 0;
-}
-
-__device__ __forceinline__ uint32_t hmax2_nan_u32(uint32_t a, uint32_t b) {
-    __nv_bfloat162 x, y;
-    memcpy(&x, &a, 4);
-    memcpy(&y, &b, 4);
-    __nv_bfloat162 z = __hmax2_nan(x, y);
-    uint32_t r;
-    memcpy(&r, &z, 4);
-    return r;
-}
-
-// Exact warp sum of u64 lane values < 2^51 with three 32-bit REDUX sums.
-__device__ __forceinline__ uint64_t warp_sum_u51(uint64_t v) {
-    const uint32_t hi = (uint32_t)(v >> 32);
-    const uint32_t mid = (uint32_t)(v >> 16) & 0xFFFFu;
-    const uint32_t lo = (uint32_t)v & 0xFFFFu;
-    const uint32_t sh = __reduce_add_sync(0xFFFFFFFFu, hi);
-    const uint32_t sm = __reduce_add_sync(0xFFFFFFFFu, mid);
-    const uint32_t sl = __reduce_add_sync(0xFFFFFFFFu, lo);
-    return ((uint64_t)sh << 32) + ((uint64_t)sm << 16) + (uint64_t)sl;
-}
-
-__device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-__device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
-    return *reinterpret_cast<const volatile int32_t*>(p);
-}
 
 // Alg. 1 lines 10-31 for rollout b, decided at row F (rows < F accepted).
 __device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int F, int q) {
@@ -227,16 +147,16 @@ __device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int F,
     }
     unsigned long long* s = sh.stat;
     if (q > 0) {
-        atomicAdd(s + STAT_STEPS_SPEC, 1ull);
-        atomicAdd(s + STAT_EMIT_SPEC, (unsigned long long)n);
-        atomicAdd(s + STAT_ACCEPTED, (unsigned long long)acc);
-        atomicAdd(s + STAT_PROPOSED, (unsigned long long)q);
-        atomicAdd(s + STAT_HIST + min(n, STAT_HIST_BINS - 1), 1ull);
+        s[STAT_STEPS_SPEC] += 1ull;
+        s[STAT_EMIT_SPEC] += (unsigned long long)n;
+        s[STAT_ACCEPTED] += (unsigned long long)acc;
+        s[STAT_PROPOSED] += (unsigned long long)q;
+        s[STAT_HIST + min(n, STAT_HIST_BINS - 1)] += 1ull;
     } else {
-        atomicAdd(s + STAT_STEPS_PLAIN, 1ull);
-        atomicAdd(s + STAT_EMIT_PLAIN, (unsigned long long)n);
+        s[STAT_STEPS_PLAIN] += 1ull;
+        s[STAT_EMIT_PLAIN] += (unsigned long long)n;
     }
-    atomicAdd(s + STAT_ROWS_NEEDED, (unsigned long long)(F + 1));
+    s[STAT_ROWS_NEEDED] += (unsigned long long)(F + 1);
 }
 
 // Record a completed row and finalize its rollout if this completes the decided prefix.
@@ -248,14 +168,145 @@ __device__ void complete_row(const VerifyArgs& a, VShared& sh, int b, int j, int
     a.row_z[r] = z;
     a.row_norm[r] = norm;
     __threadfence();
+    // Store-buffering pattern between rows of one rollout: (min first; OR mask) here vs
+    // (OR mask; read first) there.  The fences make at least one of any two finishing
+    // rows see both updates, so exactly one of them finalizes.
     if (status != ST_CONT) atomicMin(a.roll_first + b, j);
+    __threadfence();
     const unsigned mask = atomicOr(a.roll_mask + b, 1u << j) | (1u << j);
-    const int F = ld_volatile_i32(a.roll_first + b);
+    __threadfence();
+    const int F = atomicAdd(a.roll_first + b, 0);
     const unsigned need = (F >= 31) ? 0xFFFFFFFFu : ((2u << F) - 1u);
     if ((mask & need) == need && atomicCAS(a.roll_fin + b, 0, 1) == 0) {
         __threadfence();
         finalize_rollout(a, sh, b, F, q);
     }
+}
+
+// ================================================================ epilogue warp
+// Decision, sample and bookkeeping of one row (one warp).
+__device__ void epilogue_row(const VerifyArgs& a, VShared& sh, const EpiBuf& E, int lane) {
+    const RowDesc& dsc = E.dsc;
+    const int b = dsc.b, j = dsc.j, q = dsc.q, d = dsc.d;
+    const bool ok = E.ok != 0;
+    const uint16_t* row = a.logits + dsc.rowno * a.stride;
+    const int nb = a.ngroup * NCW;  // blocks in element order: i = g*NCW + w
+    int status = ST_DECIDED, cand = -1;
+    unsigned long long Zo = 0;
+    float norm = 0.f;
+    if (a.T == 0.f) {  // greedy (R1)
+        int g = (lane < NCW) ? (int)(uint32_t)E.csum[0][lane] : 0x7FFFFFFF;
+#pragma unroll
+        for (int mm = 16; mm; mm >>= 1) g = min(g, __shfl_xor_sync(0xFFFFFFFFu, g, mm));
+        g = ok ? g : -1;
+        const bool acc = ok && j < q && d == g;
+        status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
+        cand = g;
+        Zo = ok ? 1ull : 0ull;
+        norm = ok ? 1.f : 0.f;
+    } else if (ok) {
+        MassParams mp;
+        mp.c = a.c;
+        mp.nmc = -__fmul_rn(E.m, a.c);
+        mp.clampv = -(float)(a.S + 2);
+        mp.magic = 12582912.0f + (float)a.S;
+        // lane l owns the contiguous block range [l*per, (l+1)*per)
+        const int per = (nb + 31) / 32;
+        const int i0 = min(nb, lane * per), i1 = min(nb, i0 + per);
+        uint64_t ls = 0;
+        for (int i = i0; i < i1; ++i) ls += E.csum[i / NCW][i % NCW];
+        const uint64_t incl = warp_incl_scan_u64(ls, lane);
+        const uint64_t Z = shfl_u64(incl, 31);
+        const uint64_t md = (d >= 0) ? mass_of(__uint_as_float((uint32_t)row[d] << 16), mp) : 0ull;
+        bool acc = false;
+        if (j < q) {
+            const U128 r1{dsc.rng[0], dsc.rng[1], dsc.rng[2], dsc.rng[3]};
+            acc = uniform_floor(r1, Z) < md;
+        }
+        status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
+        Zo = Z;
+        norm = (float)ldexp((double)Z, -a.S);
+        if (status == ST_DECIDED) {
+            // residual (d excluded) or bonus sample (R8) by inverse CDF in ascending id
+            const int excl = (j < q) ? d : -1;
+            const U128 r2{dsc.rng[4], dsc.rng[5], dsc.rng[6], dsc.rng[7]};
+            const uint64_t U = uniform_floor(r2, Z - ((j < q) ? md : 0ull));
+            // the excluded token's mass comes off the block holding it
+            const int ex_blk = (excl >= 0) ? ((excl / (2 * CHE)) * NCW + ((excl % (2 * CHE)) / CHE) * (NCW / 2) +
+                                              ((excl % CHE) / BLK))
+                                           : -1;
+            const uint64_t ex_lane_adj = (ex_blk >= i0 && ex_blk < i1) ? md : 0ull;
+            const uint64_t incl2 = warp_incl_scan_u64(ls - ex_lane_adj, lane);
+            const unsigned hit = __ballot_sync(0xFFFFFFFFu, U < incl2);
+            const int L = hit ? (__ffs(hit) - 1) : 31;
+            int xb = 0;
+            uint64_t ub = 0;
+            if (lane == L) {  // the crossing block inside lane L's range
+                uint64_t cum = incl2 - (ls - ex_lane_adj);
+                for (int i = i0; i < i1; ++i) {
+                    const uint64_t bsum = E.csum[i / NCW][i % NCW] - ((i == ex_blk) ? md : 0ull);
+                    if (U < cum + bsum) {
+                        xb = i;
+                        ub = U - cum;
+                        break;
+                    }
+                    cum += bsum;
+                }
+            }
+            xb = __shfl_sync(0xFFFFFFFFu, xb, L);
+            ub = shfl_u64(ub, L);
+            const int g = xb / NCW, w = xb % NCW;
+            const int e_blk = 2 * g * CHE + (w / (NCW / 2)) * CHE + (w % (NCW / 2)) * BLK;
+            // rescan the block from L2: lane l owns 32 contiguous elements
+            const int e0 = lane * 32;
+            auto load8 = [&](int t) {
+                const int e = e_blk + e0 + t * 8;
+                uint4 v = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+                if (dsc.aligned && e + 8 <= a.V) {
+                    v = __ldg(reinterpret_cast<const uint4*>(row + e));
+                } else {
+                    uint16_t t8[8];
+                    for (int i = 0; i < 8; ++i) t8[i] = (e + i < a.V) ? row[e + i] : (uint16_t)0xFF80u;
+                    v.x = t8[0] | ((uint32_t)t8[1] << 16);
+                    v.y = t8[2] | ((uint32_t)t8[3] << 16);
+                    v.z = t8[4] | ((uint32_t)t8[5] << 16);
+                    v.w = t8[6] | ((uint32_t)t8[7] << 16);
+                }
+                return v;
+            };
+            uint4 vv[4];
+            uint64_t lsum = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                vv[t] = load8(t);
+                uint64_t mm[8];
+                mass8_masked(vv[t], mp, e0 + t * 8, a.V - e_blk, excl - e_blk, mm);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) lsum += mm[i];
+            }
+            const uint64_t inc3 = warp_incl_scan_u64(lsum, lane);
+            const unsigned hit3 = __ballot_sync(0xFFFFFFFFu, ub < inc3);
+            const int L3 = hit3 ? (__ffs(hit3) - 1) : 31;
+            int tok = -1;
+            if (lane == L3) {  // recompute this lane's 32 masses in order
+                uint64_t cum = inc3 - lsum;
+                for (int t = 0; t < 4 && tok < 0; ++t) {
+                    uint64_t mm[8];
+                    mass8_masked(vv[t], mp, e0 + t * 8, a.V - e_blk, excl - e_blk, mm);
+                    for (int i = 0; i < 8; ++i) {
+                        cum += mm[i];
+                        if (tok < 0 && cum > ub) tok = e_blk + e0 + t * 8 + i;
+                    }
+                }
+            }
+            cand = __shfl_sync(0xFFFFFFFFu, tok, L3);
+        }
+    }
+    if (lane == 0) {
+        sh.stat[STAT_ROWS_VERIFIED] += 1ull;
+        complete_row(a, sh, b, j, q, ok ? status : ST_DECIDED, ok ? cand : -1, Zo, norm);
+    }
+    __syncwarp();
 }
 
 __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a) {
@@ -276,12 +327,16 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
             mbar_init(&sh.rfull[i], 1);
             mbar_init(&sh.rempty[i], 1);
         }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sh.efull[i], NCW);  // every consumer warp hands its block sums over
+            mbar_init(&sh.eempty[i], 1);
+        }
         fence_mbar_init();
     }
     for (int i = tid; i < STAT_COUNT; i += NTHR) sh.stat[i] = 0ull;
     __syncthreads();
 
-    if (warp == NCW) {
+    if (warp == PROD_WARP) {
         // ======================================================== producer warp
         if (lane != 0) return;
         const uint64_t pol_keep = 0;  // pass 1: default L2 policy (the row is re-read)
@@ -297,7 +352,7 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
                 j = r / nact;
                 const int bb = a.active[r - j * nact];
                 q = a.rb_q[bb];
-                if (j > q) continue;                              // beyond the draft
+                if (j > q) continue;                                   // beyond the draft
                 if (j > ld_volatile_i32(a.roll_first + bb)) continue;  // decided below
                 b = bb;
                 break;
@@ -351,27 +406,48 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
         return;
     }
 
+    if (warp == EPI_WARP) {
+        // ======================================================== epilogue warp
+        for (int seq = 0;; ++seq) {
+            const int e = seq & 1;
+            mbar_wait(&sh.efull[e], (seq >> 1) & 1);
+            if (sh.epi[e].dsc.b < 0) break;
+            epilogue_row(a, sh, sh.epi[e], lane);
+            if (lane == 0) mbar_arrive(&sh.eempty[e]);
+        }
+        __syncwarp();
+        if (a.stats && lane == 0)
+            for (int i = 0; i < STAT_COUNT; ++i)
+                if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
+        return;
+    }
+
     // ============================================================ consumer warps
-    const int half = warp / (NCW / 2);        // warps 0-7: even chunk, 8-15: odd chunk
+    const int half = warp / (NCW / 2);         // warps 0-7: even chunk, 8-15: odd chunk
     const int wblk = (warp % (NCW / 2)) * BLK; // this warp's 1024-element block in the chunk
     MassParams mp;
     mp.c = a.c;
     mp.clampv = -(float)(a.S + 2);
     mp.magic = 12582912.0f + (float)a.S;
     uint32_t u = 0;  // chunks consumed so far (CTA-uniform): stage u % NSTAGE, use u / NSTAGE
-    int seq = 0;
 #ifdef BS_PHASE_TIMING
     long long ph_t = clock64();
 #endif
-    for (;;) {
+    for (int seq = 0;; ++seq) {
         const int f = seq % RF;
+        const int e = seq & 1;
         mbar_wait(&sh.rfull[f], (seq / RF) & 1);
         const RowDesc dsc = sh.desc[f];
-        if (dsc.b < 0) break;
-        const int b = dsc.b, j = dsc.j, q = dsc.q, d = dsc.d;
+        // the epilogue must be done with the record this row will fill (row seq - 2)
+        mbar_wait(&sh.eempty[e], ((seq >> 1) & 1) ^ 1);
+        EpiBuf& E = sh.epi[e];
+        if (dsc.b < 0) {  // end: pass the marker on to the epilogue warp
+            if (tid == 0) E.dsc.b = -1;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.efull[e]);
+            break;
+        }
         const uint16_t* row = a.logits + dsc.rowno * a.stride;
-        // the draft token's logit (its mass needs the row max): loaded under pass 1
-        const float ld = (tid == 0 && d >= 0) ? __uint_as_float((uint32_t)row[d] << 16) : 0.f;
         PH_MARK(0);
 
         // ---------------------------------------------------- pass 1: row max
@@ -397,9 +473,9 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
                 for (int t = 0; t < 4; ++t) {
                     const int e0 = wblk + t * 256 + lane * 8;
                     for (int i = 0; i < 8; ++i) {
-                        const int e = e0 + i;
-                        if (e < cv) {
-                            const uint16_t v = (e < bulk) ? buf[e] : row[(size_t)c * CHE + e];
+                        const int el = e0 + i;
+                        if (el < cv) {
+                            const uint16_t v = (el < bulk) ? buf[el] : row[(size_t)c * CHE + el];
                             mx = hmax2_nan_u32(mx, (uint32_t)v | 0xFF800000u);
                         }
                     }
@@ -434,7 +510,13 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
         if (bb) { ok = false; err |= DEV_BAD_LOGIT; }
         else if (m == -INFINITY) { ok = false; err |= DEV_ALL_NEGINF; }
         else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) { ok = false; err |= DEV_RANGE; }
-        if (err && tid == 0) atomicOr(a.dev_err, err);
+        if (tid == 0) {
+            if (err) atomicOr(a.dev_err, err);
+            mbar_arrive(&sh.rempty[f]);  // the descriptor slot is free (register copy kept)
+            E.dsc = dsc;
+            E.m = m;
+            E.ok = ok ? 1 : 0;
+        }
         mp.nmc = -__fmul_rn(m, a.c);
 
         // ---------------------------------------------------- pass 2: masses / argmax
@@ -453,10 +535,10 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
                         const int e0 = wblk + t * 256 + lane * 8;
                         int fi = 0x7FFFFFFF;
                         for (int i = 7; i >= 0; --i) {
-                            const int e = e0 + i;
-                            if (e < cv) {
-                                const uint16_t v = (e < bulk) ? buf[e] : row[(size_t)c * CHE + e];
-                                if (__uint_as_float((uint32_t)v << 16) == m) fi = c * CHE + e;
+                            const int el = e0 + i;
+                            if (el < cv) {
+                                const uint16_t v = (el < bulk) ? buf[el] : row[(size_t)c * CHE + el];
+                                if (__uint_as_float((uint32_t)v << 16) == m) fi = c * CHE + el;
                             }
                         }
 #pragma unroll
@@ -480,9 +562,9 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
                         for (int t = 0; t < 4; ++t) {
                             const int e0 = wblk + t * 256 + lane * 8;
                             for (int i = 0; i < 8; ++i) {
-                                const int e = e0 + i;
-                                if (e < cv) {
-                                    const uint16_t v = (e < bulk) ? buf[e] : row[(size_t)c * CHE + e];
+                                const int el = e0 + i;
+                                if (el < cv) {
+                                    const uint16_t v = (el < bulk) ? buf[el] : row[(size_t)c * CHE + el];
                                     acc += mass_of(__uint_as_float((uint32_t)v << 16), mp);
                                 }
                             }
@@ -490,156 +572,20 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
                     }
                 }
                 const uint64_t bs = warp_sum_u51(acc);
-                if (lane == 0) sh.csum[g][warp] = bs;
+                if (lane == 0) E.csum[g][warp] = bs;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sh.empty[sg]);
         }
         u += 2u * (uint32_t)a.ngroup;
-        if (a.T == 0.f && lane == 0) sh.csum[0][warp] = (unsigned long long)(uint32_t)first;
-        if (tid == 0) sh.massd = (ok && d >= 0 && a.T > 0.f) ? mass_of(ld, mp) : 0ull;
-        named_bar(1, NCT);
+        if (a.T == 0.f && lane == 0) E.csum[0][warp] = (unsigned long long)(uint32_t)first;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.efull[e]);  // release: block sums -> epilogue
         PH_MARK(2);
-
-        // ---------------------------------------------------- decision
-        if (tid == 0) {
-            sh.cross_g = -1;
-            sh.tok = -1;
-            int status;
-            unsigned long long Zo = 0;
-            float norm = 0.f;
-            if (a.T == 0.f) {
-                int g = 0x7FFFFFFF;
-                for (int w = 0; w < NCW; ++w) g = min(g, (int)(uint32_t)sh.csum[0][w]);
-                g = ok ? g : -1;
-                const bool acc = ok && j < q && d == g;
-                status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
-                sh.tok = g;
-                Zo = ok ? 1ull : 0ull;
-                norm = ok ? 1.f : 0.f;
-            } else {
-                uint64_t Z = 0;
-                for (int g = 0; g < a.ngroup; ++g)
-                    for (int w = 0; w < NCW; ++w) Z += sh.csum[g][w];
-                const uint64_t md = sh.massd;
-                bool acc = false;
-                if (ok && j < q) {
-                    const U128 r1{dsc.rng[0], dsc.rng[1], dsc.rng[2], dsc.rng[3]};
-                    acc = uniform_floor(r1, Z) < md;
-                }
-                status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
-                Zo = ok ? Z : 0ull;
-                norm = ok ? (float)ldexp((double)Z, -a.S) : 0.f;
-                if (ok && status == ST_DECIDED) {
-                    // residual (d excluded) or bonus sample (R8): find the crossing block
-                    const int excl = (j < q) ? d : -1;
-                    const U128 r2{dsc.rng[4], dsc.rng[5], dsc.rng[6], dsc.rng[7]};
-                    const uint64_t U = uniform_floor(r2, Z - ((j < q) ? md : 0ull));
-                    uint64_t before = 0;
-                    for (int g = 0; g < a.ngroup && sh.cross_g < 0; ++g) {
-                        for (int w = 0; w < NCW; ++w) {
-                            const int e0 = 2 * g * CHE + (w / (NCW / 2)) * CHE + (w % (NCW / 2)) * BLK;
-                            const uint64_t adj = sh.csum[g][w] - ((excl >= e0 && excl < e0 + BLK) ? md : 0ull);
-                            if (U < before + adj) {
-                                sh.cross_g = g;
-                                sh.cross_w = w;
-                                sh.ublk = U - before;
-                                break;
-                            }
-                            before += adj;
-                        }
-                    }
-                }
-            }
-            sh.ok = status;  // reused as the row status broadcast
-            sh.tsum[0] = Zo;
-            sh.m = norm;
-        }
-        named_bar(1, NCT);
-        const int status = sh.ok;
-        if (sh.cross_g >= 0) {  // ------------------------------ inverse-CDF sample
-            const int g = sh.cross_g, w = sh.cross_w;
-            const int e_blk = 2 * g * CHE + (w / (NCW / 2)) * CHE + (w % (NCW / 2)) * BLK;
-            const int excl = ((j < q) ? d : -1) - e_blk;
-            if (warp < 4) {  // the block's 4 tiles, one per warp, straight from L2
-                const int e0 = warp * 256 + lane * 8;
-                uint4 v = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
-                if (dsc.aligned && e_blk + e0 + 8 <= a.V) {
-                    v = *reinterpret_cast<const uint4*>(row + e_blk + e0);
-                } else {
-                    uint16_t t8[8];
-                    for (int i = 0; i < 8; ++i) t8[i] = (e_blk + e0 + i < a.V) ? row[e_blk + e0 + i] : (uint16_t)0xFF80u;
-                    v.x = t8[0] | ((uint32_t)t8[1] << 16);
-                    v.y = t8[2] | ((uint32_t)t8[3] << 16);
-                    v.z = t8[4] | ((uint32_t)t8[5] << 16);
-                    v.w = t8[6] | ((uint32_t)t8[7] << 16);
-                }
-                uint64_t mm[8];
-                mass8_masked(v, mp, e0, a.V - e_blk, excl, mm);
-                uint64_t ls = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) ls += mm[i];
-                const uint64_t incl = warp_incl_scan_u64(ls, lane);
-                if (lane == 31) sh.tsum[warp] = incl;  // tile total (tsum[0] Z saved above)
-                // keep the tile's masses: the crossing tile's owner warp finishes below
-                named_bar(1, NCT);
-                uint64_t ut = sh.ublk;
-                int tstar = 0;
-                for (int t = 0; t < 4; ++t) {
-                    const uint64_t ts = sh.tsum[t];
-                    if (ut < ts) {
-                        tstar = t;
-                        break;
-                    }
-                    ut -= ts;
-                }
-                if (warp == tstar) {
-                    const unsigned hit = __ballot_sync(0xFFFFFFFFu, ut < incl);
-                    const int L = hit ? (__ffs(hit) - 1) : 31;
-                    if (lane == L) {
-                        uint64_t cum = incl - ls;
-                        int tok = -1;
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            cum += mm[i];
-                            if (tok < 0 && cum > ut) tok = e_blk + e0 + i;
-                        }
-                        sh.tok = tok;
-                    }
-                }
-            } else {
-                named_bar(1, NCT);
-            }
-            named_bar(1, NCT);
-        }
-        PH_MARK(3);
-        if (tid == 0) {
-            // sh.tsum[0] held Z before the tile sums overwrote it: recompute from csum
-            unsigned long long Zo = 0;
-            float norm = 0.f;
-            if (a.T == 0.f) {
-                Zo = ok ? 1ull : 0ull;
-                norm = ok ? 1.f : 0.f;
-            } else if (ok) {
-                for (int g = 0; g < a.ngroup; ++g)
-                    for (int w = 0; w < NCW; ++w) Zo += sh.csum[g][w];
-                norm = (float)ldexp((double)Zo, -a.S);
-            }
-            atomicAdd(sh.stat + STAT_ROWS_VERIFIED, 1ull);
-            complete_row(a, sh, b, j, q, ok ? status : ST_DECIDED, ok ? sh.tok : -1, Zo, norm);
-            mbar_arrive(&sh.rempty[f]);
-        }
-        named_bar(1, NCT);  // sh scratch (csum, tok, ...) free for the next row
-        ++seq;
-        PH_MARK(4);
 #ifdef BS_PHASE_TIMING
         if (tid == 0) atomicAdd(&g_phase[15], 1ull);
 #endif
     }
-    named_bar(1, NCT);
-    if (a.stats)
-        for (int i = tid; i < STAT_COUNT; i += NCT)
-            if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
 }
 
 // ---- plan: clamp q per rollout, compact the live rollouts, reset per-rollout state

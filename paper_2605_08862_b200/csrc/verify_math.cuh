@@ -1,0 +1,101 @@
+// verify_math.cuh — per-element arithmetic of the verify kernel (reading R)
+// with packed sm_100a instructions, and small warp/CTA helpers.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace bs {
+
+struct F2 {
+    float x, y;
+};
+// fma.rn.f32x2 / add.rn.f32x2 (FFMA2 / FADD2): two IEEE single operations per instruction.
+__device__ __forceinline__ F2 ffma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+        " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+__device__ __forceinline__ F2 fadd2(F2 a, F2 b) {
+    F2 r;
+    asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+        " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+
+// Masses of the two bf16 logits packed in w (R2-R4), bit-identical to mass_of() per lane:
+// the packed FFMA2 / FADD2 perform the same IEEE single operations.
+__device__ __forceinline__ void mass_pair(uint32_t w, const MassParams& mp, uint64_t& m0,
+                                          uint64_t& m1) {
+    const F2 l{bf16lo(w), bf16hi(w)};
+    F2 y = ffma2(l, F2{mp.c, mp.c}, F2{mp.nmc, mp.nmc});
+    y.x = fmaxf(y.x, mp.clampv);
+    y.y = fmaxf(y.y, mp.clampv);
+    const F2 t = fadd2(y, F2{mp.magic, mp.magic});
+    const F2 n = fadd2(t, F2{-mp.magic, -mp.magic});
+    const F2 f = fadd2(y, F2{-n.x, -n.y});
+    F2 p = ffma2(F2{BS_C5, BS_C5}, f, F2{BS_C4, BS_C4});
+    p = ffma2(p, f, F2{BS_C3, BS_C3});
+    p = ffma2(p, f, F2{BS_C2, BS_C2});
+    p = ffma2(p, f, F2{BS_C1, BS_C1});
+    p = ffma2(p, f, F2{BS_C0, BS_C0});
+    m0 = f2u64_rz(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)));
+    m1 = f2u64_rz(__uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
+__device__ __forceinline__ uint64_t mass8(const uint4 v, const MassParams& mp) {
+    uint64_t a0, a1, b0, b1, c0, c1, d0, d1;
+    mass_pair(v.x, mp, a0, a1);
+    mass_pair(v.y, mp, b0, b1);
+    mass_pair(v.z, mp, c0, c1);
+    mass_pair(v.w, mp, d0, d1);
+    return ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
+}
+
+// One lane's 8 masses of a tile, elements >= nvalid or == excl (tile-relative) zeroed.
+__device__ __forceinline__ void mass8_masked(const uint4 v, const MassParams& mp, int e0, int nvalid,
+                                             int excl, uint64_t mm[8]) {
+    mass_pair(v.x, mp, mm[0], mm[1]);
+    mass_pair(v.y, mp, mm[2], mm[3]);
+    mass_pair(v.z, mp, mm[4], mm[5]);
+    mass_pair(v.w, mp, mm[6], mm[7]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (e0 + i >= nvalid || e0 + i == excl) mm[i] = 0;
+}
+
+__device__ __forceinline__ uint32_t hmax2_nan_u32(uint32_t a, uint32_t b) {
+    __nv_bfloat162 x, y;
+    memcpy(&x, &a, 4);
+    memcpy(&y, &b, 4);
+    __nv_bfloat162 z = __hmax2_nan(x, y);
+    uint32_t r;
+    memcpy(&r, &z, 4);
+    return r;
+}
+
+// Exact warp sum of u64 lane values < 2^51 with three 32-bit REDUX sums.
+__device__ __forceinline__ uint64_t warp_sum_u51(uint64_t v) {
+    const uint32_t hi = (uint32_t)(v >> 32);
+    const uint32_t mid = (uint32_t)(v >> 16) & 0xFFFFu;
+    const uint32_t lo = (uint32_t)v & 0xFFFFu;
+    const uint32_t sh = __reduce_add_sync(0xFFFFFFFFu, hi);
+    const uint32_t sm = __reduce_add_sync(0xFFFFFFFFu, mid);
+    const uint32_t sl = __reduce_add_sync(0xFFFFFFFFu, lo);
+    return ((uint64_t)sh << 32) + ((uint64_t)sm << 16) + (uint64_t)sl;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
+    return *reinterpret_cast<const volatile int32_t*>(p);
+}
+
+}  // namespace bs

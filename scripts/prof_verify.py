@@ -55,8 +55,7 @@ if os.environ.get("BS_LIB_VARIANT") == "timing":
     lib = bs.load()
     ph = (ctypes.c_ulonglong * 16)()
     if lib.bsx_phase_times(ph, 1):
-        names = ["wait row desc", "pass 1 (max)", "pass 2 (masses)", "decide+sample",
-                 "complete/finalize"]
+        names = ["row start (desc, epilogue slot)", "pass 1 (max) + barrier", "pass 2 (masses)"]
         tot = sum(ph[i] for i in range(len(names)))
         it = max(1, ph[15])
         print(f"phase cycles per row-iteration per CTA (n={ph[15]}):")
