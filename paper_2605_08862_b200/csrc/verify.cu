@@ -31,15 +31,18 @@
 namespace bs {
 
 constexpr int CHE = 8192;           // elements per ring chunk (16 KB)
-constexpr int NSTAGE = 8;           // ring depth (128 KB)
-constexpr int NCW = 16;             // consumer warps
+constexpr int NSTAGE = 4;           // ring depth (64 KB per CTA)
+constexpr int NCW = 8;              // consumer warps
+constexpr int CTAS_PER_SM = 2;      // one CTA's HBM pass overlaps the other's mass pass
 constexpr int NCT = NCW * 32;       // consumer threads
 constexpr int PROD_WARP = NCW;      // producer warp
 constexpr int EPI_WARP = NCW + 1;   // epilogue warp
 constexpr int NTHR = NCT + 64;
 constexpr int RF = 4;               // row descriptor FIFO depth
 constexpr int MAXG = 32;            // max super-chunks (2 chunks each): V <= 524288
-constexpr int BLK = CHE * 2 / NCW;  // 1024: elements per warp per super-chunk (4 tiles)
+constexpr int BLK = CHE * 2 / NCW;  // elements per warp per super-chunk (2048: 8 tiles)
+constexpr int TPW = BLK / 256;      // 256-element tiles per warp per chunk
+constexpr int EPL = BLK / 32;       // elements per lane when the epilogue rescans a block
 constexpr int ST_CONT = 0, ST_DECIDED = 1, ST_EOS = 2;  // row status
 
 // Optional per-stage cycle accounting (build with -DBS_PHASE_TIMING; read with
@@ -258,7 +261,7 @@ __device__ void epilogue_row(const VerifyArgs& a, VShared& sh, const EpiBuf& E, 
             const int g = xb / NCW, w = xb % NCW;
             const int e_blk = 2 * g * CHE + (w / (NCW / 2)) * CHE + (w % (NCW / 2)) * BLK;
             // rescan the block from L2: lane l owns 32 contiguous elements
-            const int e0 = lane * 32;
+            const int e0 = lane * EPL;
             auto load8 = [&](int t) {
                 const int e = e_blk + e0 + t * 8;
                 uint4 v = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
@@ -274,13 +277,11 @@ __device__ void epilogue_row(const VerifyArgs& a, VShared& sh, const EpiBuf& E, 
                 }
                 return v;
             };
-            uint4 vv[4];
             uint64_t lsum = 0;
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                vv[t] = load8(t);
+            for (int t = 0; t < EPL / 8; ++t) {
+                const uint4 v8 = load8(t);
                 uint64_t mm[8];
-                mass8_masked(vv[t], mp, e0 + t * 8, a.V - e_blk, excl - e_blk, mm);
+                mass8_masked(v8, mp, e0 + t * 8, a.V - e_blk, excl - e_blk, mm);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) lsum += mm[i];
             }
@@ -288,11 +289,11 @@ __device__ void epilogue_row(const VerifyArgs& a, VShared& sh, const EpiBuf& E, 
             const unsigned hit3 = __ballot_sync(0xFFFFFFFFu, ub < inc3);
             const int L3 = hit3 ? (__ffs(hit3) - 1) : 31;
             int tok = -1;
-            if (lane == L3) {  // recompute this lane's 32 masses in order
+            if (lane == L3) {  // reload and recompute this lane's masses in order
                 uint64_t cum = inc3 - lsum;
-                for (int t = 0; t < 4 && tok < 0; ++t) {
+                for (int t = 0; t < EPL / 8 && tok < 0; ++t) {
                     uint64_t mm[8];
-                    mass8_masked(vv[t], mp, e0 + t * 8, a.V - e_blk, excl - e_blk, mm);
+                    mass8_masked(load8(t), mp, e0 + t * 8, a.V - e_blk, excl - e_blk, mm);
                     for (int i = 0; i < 8; ++i) {
                         cum += mm[i];
                         if (tok < 0 && cum > ub) tok = e_blk + e0 + t * 8 + i;
@@ -309,7 +310,7 @@ __device__ void epilogue_row(const VerifyArgs& a, VShared& sh, const EpiBuf& E, 
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a) {
+__global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const VerifyArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw);
     VShared& sh = *reinterpret_cast<VShared*>(smem_raw + (size_t)NSTAGE * CHE * 2);
@@ -462,7 +463,7 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
             const int bulk = dsc.aligned ? (cv & ~7) : 0;
             if (cv == CHE && bulk == CHE) {
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
+                for (int t = 0; t < TPW; ++t) {
                     const uint4 v = lds128(buf + wblk + t * 256 + lane * 8);
                     mx = hmax2_nan_u32(mx, v.x);
                     mx = hmax2_nan_u32(mx, v.y);
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
                     mx = hmax2_nan_u32(mx, v.w);
                 }
             } else {  // partial / unaligned chunk: element-wise from smem or global
-                for (int t = 0; t < 4; ++t) {
+                for (int t = 0; t < TPW; ++t) {
                     const int e0 = wblk + t * 256 + lane * 8;
                     for (int i = 0; i < 8; ++i) {
                         const int el = e0 + i;
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
             const int bulk = dsc.aligned ? (cv & ~7) : 0;
             if (a.T == 0.f) {  // greedy (R1): the first index attaining the max
                 if (ok && first == 0x7FFFFFFF) {
-                    for (int t = 0; t < 4; ++t) {
+                    for (int t = 0; t < TPW; ++t) {
                         const int e0 = wblk + t * 256 + lane * 8;
                         int fi = 0x7FFFFFFF;
                         for (int i = 7; i >= 0; --i) {
@@ -553,13 +554,16 @@ __global__ void __launch_bounds__(NTHR, 1) verify_rows_kernel(const VerifyArgs a
                 uint64_t acc = 0;
                 if (ok) {
                     if (cv == CHE && bulk == CHE) {
-                        const uint4 v0 = lds128(buf + wblk + lane * 8);
-                        const uint4 v1 = lds128(buf + wblk + 256 + lane * 8);
-                        const uint4 v2 = lds128(buf + wblk + 512 + lane * 8);
-                        const uint4 v3 = lds128(buf + wblk + 768 + lane * 8);
-                        acc = (mass8(v0, mp) + mass8(v1, mp)) + (mass8(v2, mp) + mass8(v3, mp));
+#pragma unroll
+                        for (int t = 0; t < TPW; t += 4) {  // 4 tiles = 16 independent pair chains
+                            const uint4 v0 = lds128(buf + wblk + t * 256 + lane * 8);
+                            const uint4 v1 = lds128(buf + wblk + (t + 1) * 256 + lane * 8);
+                            const uint4 v2 = lds128(buf + wblk + (t + 2) * 256 + lane * 8);
+                            const uint4 v3 = lds128(buf + wblk + (t + 3) * 256 + lane * 8);
+                            acc += (mass8(v0, mp) + mass8(v1, mp)) + (mass8(v2, mp) + mass8(v3, mp));
+                        }
                     } else {
-                        for (int t = 0; t < 4; ++t) {
+                        for (int t = 0; t < TPW; ++t) {
                             const int e0 = wblk + t * 256 + lane * 8;
                             for (int i = 0; i < 8; ++i) {
                                 const int el = e0 + i;
@@ -701,7 +705,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
         if (e != cudaSuccess) return e;
         configured = 1;
     }
-    const int grid = std::max(1, std::min(ctx->num_sms, n * (k + 1)));
+    const int grid = std::max(1, std::min(ctx->num_sms * CTAS_PER_SM, n * (k + 1)));
     verify_rows_kernel<<<grid, NTHR, smem, st>>>(a);
     return cudaGetLastError();
 }
