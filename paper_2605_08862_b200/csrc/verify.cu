@@ -344,10 +344,12 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
         const uint64_t pol_first = policy_evict_first();
         uint32_t rph = 0;    // row-empty phase bits, one per FIFO slot
         uint32_t P = 0;      // chunks issued so far: stage P % NSTAGE, use P / NSTAGE
-        int seq = 0;
-        for (;;) {
+        // claim the next needed row (j-major over the live rollouts) and fill its descriptor
+        auto claim = [&]() {
+            RowDesc dsc;
+            dsc.b = -1;
             int b = -1, j = 0, q = 0;
-            for (;;) {  // claim the next needed row (j-major over the live rollouts)
+            for (;;) {
                 const int r = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
                 if (r >= total) break;
                 j = r / nact;
@@ -358,14 +360,8 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
                 b = bb;
                 break;
             }
-            const int f = seq % RF;
-            if (seq >= RF) {
-                mbar_wait(&sh.rempty[f], (rph >> f) & 1u);
-                rph ^= 1u << f;
-            }
-            RowDesc& dsc = sh.desc[f];
-            dsc.b = b;
             if (b >= 0) {
+                dsc.b = b;
                 dsc.j = j;
                 dsc.q = q;
                 dsc.d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;
@@ -380,11 +376,24 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
                 dsc.rng[0] = r1.x0; dsc.rng[1] = r1.x1; dsc.rng[2] = r1.x2; dsc.rng[3] = r1.x3;
                 dsc.rng[4] = r2.x0; dsc.rng[5] = r2.x1; dsc.rng[6] = r2.x2; dsc.rng[7] = r2.x3;
             }
+            return dsc;
+        };
+        RowDesc nxt = claim();
+        for (int seq = 0;; ++seq) {
+            const RowDesc cur = nxt;
+            const int f = seq % RF;
+            if (seq >= RF) {
+                mbar_wait(&sh.rempty[f], (rph >> f) & 1u);
+                rph ^= 1u << f;
+            }
+            sh.desc[f] = cur;
             mbar_arrive(&sh.rfull[f]);  // release: the descriptor is visible to the consumers
-            if (b < 0) break;
-            const uint16_t* row = a.logits + dsc.rowno * a.stride;
-            const bool aligned = dsc.aligned != 0;
+            if (cur.b < 0) break;
+            const uint16_t* row = a.logits + cur.rowno * a.stride;
+            const bool aligned = cur.aligned != 0;
             for (int pass = 0; pass < 2; ++pass) {
+                // the following row is claimed while this row's pass-1 chunks are consumed
+                if (pass == 1) nxt = claim();
                 for (int c = 0; c < 2 * a.ngroup; ++c, ++P) {
                     const int s = (int)(P % NSTAGE);
                     // a stage's k-th fill waits for its (k-1)-th release (first fill: free)
@@ -402,7 +411,6 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
                     }
                 }
             }
-            ++seq;
         }
         return;
     }
