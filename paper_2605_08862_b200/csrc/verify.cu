@@ -44,6 +44,7 @@ constexpr int BLK = CHE * 2 / NCW;  // elements per warp per super-chunk (2048: 
 constexpr int TPW = BLK / 256;      // 256-element tiles per warp per chunk
 constexpr int EPL = BLK / 32;       // elements per lane when the epilogue rescans a block
 constexpr int ST_CONT = 0, ST_DECIDED = 1, ST_EOS = 2;  // row status
+constexpr bool c_claim_early = false;  // producer claims row r+1 under row r's pass 1
 
 // Optional per-stage cycle accounting (build with -DBS_PHASE_TIMING; read with
 // bsx_phase_times): consumer thread 0 adds the clock64() delta of each phase.
@@ -392,8 +393,9 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
             const uint16_t* row = a.logits + cur.rowno * a.stride;
             const bool aligned = cur.aligned != 0;
             for (int pass = 0; pass < 2; ++pass) {
-                // the following row is claimed while this row's pass-1 chunks are consumed
-                if (pass == 1) nxt = claim();
+                // (claiming the following row earlier, under pass 1, raises speculative
+                // row reads more than it hides claim latency: measured slower)
+                if (pass == 1 && c_claim_early) nxt = claim();
                 for (int c = 0; c < 2 * a.ngroup; ++c, ++P) {
                     const int s = (int)(P % NSTAGE);
                     // a stage's k-th fill waits for its (k-1)-th release (first fill: free)
@@ -411,6 +413,7 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
                     }
                 }
             }
+            if (!c_claim_early) nxt = claim();
         }
         return;
     }
