@@ -150,19 +150,16 @@ typedef struct {
 /* (P:202).  Readings R0 (validity), R1 (max / greedy), R2 (scale), R3-R4       */
 /* (integer masses), R5 (top-p).  mass[] receives the kept masses mass'_i.    */
 /* ------------------------------------------------------------------------- */
-/* qsort comparator for reading R5's order (mass desc, id asc).  The test code is
- * single-threaded, so the masses being ordered are passed through a file static. */
-static const uint64_t* g_order_mass;
-static int cmp_mass_desc_id_asc(const void* a, const void* b) {
-    int32_t i = *(const int32_t*)a, j = *(const int32_t*)b;
-    uint64_t mi = g_order_mass[i], mj = g_order_mass[j];
-    if (mi != mj) return mi > mj ? -1 : 1;
-    return i < j ? -1 : (i > j ? 1 : 0);
+/* qsort comparator: masses in descending order (reading R5). */
+static int cmp_u64_desc(const void* a, const void* b) {
+    uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x > y ? -1 : (x < y ? 1 : 0);
 }
 
 /* R5 on given integer masses (exposed so the SPEC top-p example S:79 can pin it):
- * order by (mass desc, id asc); P = llround(top_p * 2^32); Theta = ceil(P*Z/2^32);
- * keep i  <=>  C_before(i) < Theta.  Zeroes the dropped masses, returns Z'.    */
+ * P = llround(top_p * 2^32); Theta = ceil(P*Z/2^32); G(t) = sum of the masses > t;
+ * keep i  <=>  G(mass_i) < Theta   (tie-closed nucleus: the tokens whose strictly
+ * heavier tokens have not yet reached top_p).  Zeroes the dropped masses, returns Z'. */
 uint64_t orc_top_p_filter(uint64_t* mass, int V, float top_p) {
     uint64_t Z = 0;
     for (int i = 0; i < V; ++i) Z += mass[i];
@@ -170,22 +167,26 @@ uint64_t orc_top_p_filter(uint64_t* mass, int V, float top_p) {
     uint64_t P = (uint64_t)llround((double)top_p * 4294967296.0);
     unsigned __int128 t = (unsigned __int128)P * Z + (((unsigned __int128)1 << 32) - 1);
     uint64_t theta = (uint64_t)(t >> 32);
-    int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)V);
-    for (int i = 0; i < V; ++i) order[i] = i;
-    g_order_mass = mass;
-    qsort(order, (size_t)V, sizeof(int32_t), cmp_mass_desc_id_asc);
-    uint64_t before = 0, zk = 0;
-    for (int r = 0; r < V; ++r) {
-        int32_t i = order[r];
-        uint64_t mi = mass[i];
-        if (before < theta) {
-            zk += mi;
-        } else {
-            mass[i] = 0;
-        }
-        before += mi;
+    /* sorted copy: G(mass_i) = sum of the sorted values strictly greater than mass_i */
+    uint64_t* sorted = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)V);
+    memcpy(sorted, mass, sizeof(uint64_t) * (size_t)V);
+    qsort(sorted, (size_t)V, sizeof(uint64_t), cmp_u64_desc);
+    /* tau = smallest mass value with G(tau) < Theta; keep i <=> mass_i >= tau */
+    uint64_t tau = sorted[0], greater = 0;
+    for (int r = 0; r < V;) {
+        int e = r;
+        uint64_t group = 0;
+        while (e < V && sorted[e] == sorted[r]) group += sorted[e++];
+        if (greater < theta) tau = sorted[r];
+        greater += group;
+        r = e;
     }
-    free(order);
+    free(sorted);
+    uint64_t zk = 0;
+    for (int i = 0; i < V; ++i) {
+        if (mass[i] >= tau) zk += mass[i];
+        else mass[i] = 0;
+    }
     return zk;
 }
 

@@ -176,8 +176,12 @@ def test_top_p_spec_example(orc):
     assert list(m) == [5, 0, 0] and z == 5
     m, z = orc.top_p_filter([2, 3, 5], 0.75)     # order is by mass, not by id
     assert list(m) == [0, 3, 5] and z == 8
-    m, z = orc.top_p_filter([3, 3, 3, 1], 0.5)   # ties broken by lowest id
-    assert list(m) == [3, 3, 0, 0]
+    m, z = orc.top_p_filter([3, 3, 3, 1], 0.5)   # a tie straddling top_p is kept whole
+    assert list(m) == [3, 3, 3, 0] and z == 9
+    m, z = orc.top_p_filter([3, 1, 1, 1, 1, 1], 0.375)  # {3} reaches 3/8 exactly: tie dropped
+    assert list(m) == [3, 0, 0, 0, 0, 0] and z == 3
+    m, z = orc.top_p_filter([3, 1, 1, 1, 1, 1], 0.376)  # ... just above: the whole tie joins
+    assert list(m) == [3, 1, 1, 1, 1, 1] and z == 8
     m, z = orc.top_p_filter([1, 7], 1.0)         # identity
     assert list(m) == [1, 7] and z == 8
     m, z = orc.top_p_filter([1, 7], 1e-9)        # never empties the support
@@ -185,27 +189,33 @@ def test_top_p_spec_example(orc):
 
 
 def test_top_p_nucleus_properties(orc):
-    """The kept set is the smallest (mass desc, id asc) prefix whose mass reaches
-    top_p * Z (checked with exact fractions), and it grows monotonically with top_p.
-    (SPEC S:97 also claims idempotence; with renormalisation that is false in general,
-    e.g. (0.6, 0.3, 0.1) at top_p 0.65 -> {0.6, 0.3} -> {0.6} — DESIGN.md reading R5.)"""
+    """The kept set is the smallest tie-closed set of heaviest tokens whose mass reaches
+    top_p * Z (checked with exact fractions, by brute force over the distinct mass levels),
+    and it grows monotonically with top_p.  (SPEC S:97 also claims idempotence; with
+    renormalisation that is false in general, e.g. (0.6, 0.3, 0.1) at top_p 0.65 ->
+    {0.6, 0.3} -> {0.6} — DESIGN.md reading R5.)"""
     rng = np.random.default_rng(4)
-    for _ in range(200):
-        m0 = rng.integers(0, 1000, 20).astype(np.uint64)
+    for trial in range(300):
+        hi = 1000 if trial % 2 else 6          # small value range -> many ties
+        m0 = rng.integers(0, hi, 20).astype(np.uint64)
         m0[0] += 1
         Z = int(m0.sum())
-        order = sorted(range(20), key=lambda i: (-int(m0[i]), i))
         prev_kept = set()
         for p in sorted(float(np.float32(x)) for x in rng.uniform(0.01, 1.0, 4)):
             m1, z1 = orc.top_p_filter(m0, p)
-            kept = [i for i in order if int(m1[i]) > 0 or (int(m0[i]) == 0 and False)]
-            n = len(kept)
-            assert kept == order[:n]                       # a prefix of the order
-            pth = Fraction(p) * Z
-            assert sum(int(m0[i]) for i in order[:n]) >= pth          # reaches top_p
-            assert n == 1 or sum(int(m0[i]) for i in order[:n - 1]) < pth  # smallest
-            assert prev_kept <= set(kept)                  # monotone in top_p
-            prev_kept = set(kept)
+            kept = {i for i in range(20) if int(m1[i]) > 0}
+            assert all(int(m1[i]) in (0, int(m0[i])) for i in range(20))
+            assert z1 == sum(int(m0[i]) for i in kept)
+            pth = Fraction(round(p * 2**32), 2**32) * Z            # Theta's real value
+            # brute force: try the levels t from the top; the answer is {mass >= t}
+            # for the first level whose set reaches top_p.
+            for t in sorted({int(x) for x in m0 if x > 0}, reverse=True):
+                cand = {i for i in range(20) if int(m0[i]) >= t}
+                if sum(int(m0[i]) for i in cand) >= pth:
+                    break
+            assert kept == cand
+            assert prev_kept <= kept                       # monotone in top_p
+            prev_kept = kept
 
 
 # ------------------------------------------------------------------ sampling (R8), Eq. 3
