@@ -177,7 +177,10 @@ def run_ours(args, cfg, rank, world, dist):
     ev_s = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(chunk)]
     ev_e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(chunk)]
 
-    def capture():
+    def capture(instrument=False):
+        """One graph of `chunk` decode iterations.  Event-record nodes cost several us each
+        inside a graph, so the timed graph has none; the instrumented twin (events around
+        every bs_verify_step) is replayed separately on the same deterministic work."""
         with torch.cuda.stream(stream):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
@@ -187,16 +190,18 @@ def run_ours(args, cfg, rank, world, dist):
                                       eng.match_len, stream=stream)
                     c.bsx_target_rows(eng.slots, eng.draft, eng.draft_len, k, t.target_seed,
                                       t.mode, t.nbank, eng.row_index, stream=stream)
-                    ev_s[i].record(stream)
+                    if instrument:
+                        ev_s[i].record(stream)
                     c.bs_verify_step(eng.slots, t.bank, eng.row_index, V, eng.draft,
                                      eng.draft_len, k, eng.T, eng.top_p, eng.out_tokens,
                                      eng.out_len, eng.out_acc, stream=stream)
-                    ev_e[i].record(stream)
+                    if instrument:
+                        ev_e[i].record(stream)
                     c.bs_commit(eng.slots, eng.out_tokens, eng.out_len, k, eng.finished,
                                 stream=stream)
         return g
 
-    def rl_step(s, rec):
+    def rl_step(s, rec, instrument=False):
         d = dins[s]
         with torch.cuda.stream(stream):
             ctx.bs_draft_pool_put(s + 1, d["sp"], d["off"], d["tok"], d["ntok"], stream=stream)
@@ -204,18 +209,20 @@ def run_ours(args, cfg, rank, world, dist):
                 ctx.bs_draft_exchange(comm, rank, world, s + 1, stream=stream)
             eng.seal(s + 1)  # synchronises the stream (index build is per RL step)
             eng.begin(d["uids"], d["pid"], d["tails"], d["ml"])
-        g = capture()  # sealed pool / index pointers change per RL step
+        g = capture(instrument)  # sealed pool / index pointers change per RL step
         rec["launches"] += 2 + rec["seal_launches"]
         steps, chunks = 0, 0
         while True:
-            g.replay()
+            with torch.cuda.stream(stream):
+                g.replay()
+                done = bool(eng.finished.all().item())  # one host sync per chunk
             steps += chunk
-            done = bool(eng.finished.all().item())  # one host sync per chunk
-            vt = sum(ev_s[i].elapsed_time(ev_e[i]) for i in range(chunk))
-            rec["verify_ms"] += vt
-            if chunks == 0:
-                rec["verify_ms_steady"] += vt
-                rec["steady_steps"] += chunk
+            if instrument:
+                vt = sum(ev_s[i].elapsed_time(ev_e[i]) for i in range(chunk))
+                rec["verify_ms"] += vt
+                if chunks == 0:
+                    rec["verify_ms_steady"] += vt
+                    rec["steady_steps"] += chunk
             chunks += 1
             if done:
                 break
@@ -251,6 +258,19 @@ def run_ours(args, cfg, rank, world, dist):
     clk = clocks.stop()
     elapsed_ms = start.elapsed_time(end)
     st = eng.stats(reset=True)
+    # ---- the verify op's device time on the same work: instrumented replay of the timed
+    # RL steps (deterministic: same pools, uids and Philox stream -> identical rows)
+    reci = dict(rec0)
+    for s in range(args.warmup, total_steps):
+        rl_step(s, reci, instrument=True)
+    torch.cuda.synchronize(dev)
+    sti = eng.stats(reset=True)
+    if sti["tokens"] != st["tokens"] or sti["rows_verified"] != st["rows_verified"]:
+        log(f"note: instrumented replay differs ({sti['tokens']} vs {st['tokens']} tokens, "
+            f"{sti['rows_verified']} vs {st['rows_verified']} rows)")
+    rec["verify_ms"] = reci["verify_ms"]
+    rec["verify_rows_verified"] = sti["rows_verified"]
+    rec["verify_rows_needed"] = sti["rows_needed"]
     # ---- steady-state kernel phase: full live batch, first chunk of a fresh RL step
     s_last = total_steps - 1
     d = dins[s_last]
@@ -260,8 +280,9 @@ def run_ours(args, cfg, rank, world, dist):
             ctx.bs_draft_exchange(comm, rank, world, 10_000, stream=stream)
         eng.seal(10_000)
         eng.begin(d["uids"], d["pid"], d["tails"], d["ml"])
-    g = capture()
-    g.replay()
+    g = capture(instrument=True)
+    with torch.cuda.stream(stream):
+        g.replay()
     torch.cuda.synchronize(dev)
     steady_ms = sum(ev_s[i].elapsed_time(ev_e[i]) for i in range(chunk))
     sst = eng.stats(reset=True)
@@ -325,9 +346,10 @@ def run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, 
             eng.begin(d["uids"], d["pid"], d["tails"], d["max_len"])
         g = capture()
         while True:
-            g.replay()
-            if bool(eng.finished.all().item()):
-                break
+            with torch.cuda.stream(stream):
+                g.replay()
+                if bool(eng.finished.all().item()):
+                    break
         with torch.cuda.stream(stream):
             resp_host.copy_(resp, non_blocking=True)
     end.record(stream)
@@ -443,8 +465,8 @@ def main():
     # dominant kernel: the verify op (plan + rows kernels), timed by captured events
     vlaunches = rec["decode_steps"]
     v_avg_ms = rec["verify_ms"] / max(1, vlaunches)
-    alg_bytes = st["rows_needed"] * row_bytes / max(1, vlaunches)      # per launch
-    moved_bytes = st["rows_verified"] * row_bytes / max(1, vlaunches)
+    alg_bytes = rec["verify_rows_needed"] * row_bytes / max(1, vlaunches)   # per launch
+    moved_bytes = rec["verify_rows_verified"] * row_bytes / max(1, vlaunches)
     achieved = alg_bytes / (v_avg_ms * 1e-3) / 1e9
     steady_alg = r["sst"]["rows_needed"] * row_bytes / (r["steady_ms"] * 1e-3) / 1e9
     steady_moved = r["sst"]["rows_verified"] * row_bytes / (r["steady_ms"] * 1e-3) / 1e9
@@ -476,7 +498,8 @@ def main():
                     "steady_algorithmic": steady_alg, "steady_moved": steady_moved},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": "bs_verify_step (verify_plan + verify_rows), avg over the timed region",
+                     "kernel": "bs_verify_step (plan + rows/split kernels), avg over an "
+                               "instrumented replay of the timed RL steps",
                      "peak_source": peak_src,
                      "steady_frac": steady_alg / hbm},
         "clocks": r["clocks"],

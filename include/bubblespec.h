@@ -208,6 +208,16 @@ bs_status bs_verify_step(bs_ctx* ctx, int32_t n, const int32_t* slots, const voi
 bs_status bs_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* out_tokens,
                     const int32_t* out_len, int32_t k, int32_t* finished, void* stream);
 
+/* ---------------------------------------------------------------- tuning */
+/* Select the kernel bs_verify_step uses for rows without top-p (all compute identical
+ * results): 0 auto (= 3 when ceil(V/8) <= 53248, else 1; env BS_VERIFY_KERNEL
+ * overrides auto), 1 one CTA per row (rows streamed twice through a TMA ring), 2 each row
+ * split over an 8-CTA cluster (one row at a time), 3 pipelined 8-CTA cluster (row slices
+ * resident in shared memory, max and mass passes overlapped across rows).  Takes effect for
+ * calls enqueued (or graphs captured) after it.  Errors: BS_ERR_INVALID on a NULL ctx or an
+ * unknown kind. */
+bs_status bsx_set_verify_kernel(bs_ctx* ctx, int32_t kind);
+
 /* ---------------------------------------------------------------- synthetic workload */
 /* Not part of the method: device twins of workloads/synth.py so a
  * multi-GB logit bank need not be generated on the host.  Bit-identical to numpy. */

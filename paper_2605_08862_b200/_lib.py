@@ -55,6 +55,7 @@ SIGNATURES = {
     "bs_commit": (C.c_int, [_V, _I32, _V, _V, _V, _I32, _V, _V]),
     "bs_stats_read": (C.c_int, [_V, _V, _I32, _I32, _V]),
     "bs_rollout_bind_output": (C.c_int, [_V, _V, _I64]),
+    "bsx_set_verify_kernel": (C.c_int, [_V, _I32]),
     "bsx_synth_bank": (C.c_int, [_V, _I64, _I32, _U32, C.c_float, _V]),
     "bsx_target_rows": (C.c_int, [_V, _I32, _V, _V, _V, _I32, _U32, _I32, _I64, _V, _V]),
 }

@@ -136,6 +136,12 @@ class Context:
                                                  stride if responses is not None else 0),
              "bs_rollout_bind_output")
 
+    VERIFY_KERNELS = {"auto": 0, "rows": 1, "split": 2, "cluster": 3}
+
+    def bsx_set_verify_kernel(self, kind):
+        kind = self.VERIFY_KERNELS[kind] if isinstance(kind, str) else int(kind)
+        _chk(self, load().bsx_set_verify_kernel(self.handle, kind), "bsx_set_verify_kernel")
+
     def bsx_target_rows(self, slots, draft_tokens, draft_len, k, target_seed, mode, nbank,
                         row_index, stream=None):
         _chk(self, load().bsx_target_rows(self.handle, slots.numel(), _p(slots), _p(draft_tokens),

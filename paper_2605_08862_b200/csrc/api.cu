@@ -38,6 +38,12 @@ static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
 extern "C" {
 
+bs_status bsx_set_verify_kernel(bs_ctx* c, int32_t kind) {
+    if (!c || kind < 0 || kind > 3) return BS_ERR_INVALID;
+    c->verify_kind = kind;
+    return BS_OK;
+}
+
 const char* bs_version(void) { return "bubblespec-b200 0.1 (sm_100a)"; }
 
 const char* bs_last_error(const bs_ctx* ctx) {
@@ -78,12 +84,11 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
                c->pos.ensure(R) == cudaSuccess && c->max_len.ensure(R) == cudaSuccess &&
                c->prompt.ensure(R) == cudaSuccess && c->finished.ensure(R) == cudaSuccess &&
                c->uid.ensure(R) == cudaSuccess && c->dev_err.ensure(1) == cudaSuccess &&
-               c->rb_q.ensure(R) == cudaSuccess && c->vqueue.ensure(rows + R + 64) == cudaSuccess &&
+               c->rb_q.ensure(R) == cudaSuccess && c->vqueue.ensure(rows * 12 + 64) == cudaSuccess &&
                c->vctl.ensure(VCTL_WORDS) == cudaSuccess &&
                c->vrow_status.ensure(rows) == cudaSuccess && c->vrow_cand.ensure(rows) == cudaSuccess &&
                c->vrow_z.ensure(rows) == cudaSuccess && c->vrow_norm.ensure(rows) == cudaSuccess &&
-               c->vroll_first.ensure(R) == cudaSuccess && c->vroll_fin.ensure(R) == cudaSuccess &&
-               c->vroll_mask.ensure(R) == cudaSuccess &&
+               c->vroll_first.ensure(R) == cudaSuccess && c->vroll_state.ensure(R) == cudaSuccess &&
                c->staging.tokens.ensure((size_t)cfg->pool_capacity_tokens) == cudaSuccess &&
                c->staging.seq_off.ensure((size_t)cfg->pool_capacity_seqs + 1) == cudaSuccess &&
                c->staging.seq_prompt.ensure((size_t)cfg->pool_capacity_seqs) == cudaSuccess &&
@@ -130,7 +135,7 @@ void bs_destroy(bs_ctx* c) {
     c->seq_start_of.release(); c->seq_end_of.release(); c->prompt_of.release();
     c->table.release(); c->rb_q.release(); c->vqueue.release(); c->vctl.release();
     c->vrow_status.release(); c->vrow_cand.release(); c->vrow_z.release(); c->vrow_norm.release();
-    c->vroll_first.release(); c->vroll_fin.release(); c->vroll_mask.release();
+    c->vroll_first.release(); c->vroll_state.release();
     c->stats.release();
     delete c;
 }
@@ -251,8 +256,6 @@ bs_status bs_verify_step(bs_ctx* c, int32_t n, const int32_t* slots, const void*
     if (!(sp.top_p > 0.f && sp.top_p <= 1.f)) return fail(c, BS_ERR_INVALID, "top_p must be in (0, 1]");
     if (sp.temperature > 0.f && !((float)(1.4426950408889634 / (double)sp.temperature) < INFINITY))
         return fail(c, BS_ERR_INVALID, "temperature too small");
-    if (sp.top_p < 1.f && sp.temperature > 0.f)
-        return fail(c, BS_ERR_INVALID, "top_p < 1 is not implemented yet");
     if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
               (k && !draft_tokens)))
         return fail(c, BS_ERR_INVALID, "null array");

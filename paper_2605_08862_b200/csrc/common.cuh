@@ -7,6 +7,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 namespace bs {
 
 // ------------------------------------------------------------------ error word
@@ -152,6 +154,30 @@ __host__ __device__ inline uint32_t h32(uint32_t x) {
     x *= 0x846CA68Bu;
     x ^= x >> 16;
     return x;
+}
+
+// ---- programmatic dependent launch (decode-loop kernels).  Every kernel of the decode loop
+// is launched with programmatic stream serialization: its CTAs may be scheduled while the
+// previous kernel still runs, and pdl_wait() (griddepcontrol.wait) blocks until that kernel
+// has completed and its memory is visible.  pdl_trigger() lets the next kernel launch early.
+// Kernels call pdl_wait() before touching any global memory.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace bs

@@ -26,7 +26,7 @@ enum : int {
 };
 
 // Control words of the verify kernel: next rollout to claim, number of live rollouts.
-enum : int { VCTL_NEXT = 0, VCTL_NACTIVE = 1, VCTL_WORDS = 4 };
+enum : int { VCTL_NEXT = 0, VCTL_NACTIVE = 1, VCTL_MODE = 2, VCTL_ROWS = 3, VCTL_WORDS = 4 };
 
 template <typename T>
 struct DevBuf {
@@ -67,6 +67,7 @@ struct bs_ctx {
     int M = 0;  // match_max
     std::string err;
     int num_sms = 148;
+    int verify_kind = 0;  // bsx_set_verify_kernel (0: auto)
     // rollout slots
     bs::DevBuf<int32_t> tail;  // [R, M] right-aligned context tail
     bs::DevBuf<int32_t> ctx_len, pos, max_len, prompt, finished;
@@ -77,17 +78,18 @@ struct bs_ctx {
     bs::DevBuf<int32_t> seq_start_of, seq_end_of, prompt_of;  // per sealed pool token
     bs::DevBuf<bs::IndexEntry> table;
     uint64_t table_mask = 0;
-    // verify scratch: clamped q per rollout, the row work queue and its control words
+    // verify scratch: clamped q per rollout, the step's row table (RowDesc, 48 B per row)
+    // and its control words
     bs::DevBuf<int32_t> rb_q, vqueue;
     bs::DevBuf<unsigned int> vctl;
     // per verified row (b*(k_max+1)+j): status, candidate token, Z, fp32 normaliser
     bs::DevBuf<int32_t> vrow_status, vrow_cand;
     bs::DevBuf<unsigned long long> vrow_z;
     bs::DevBuf<float> vrow_norm;
-    // per rollout: first row that decides (reject / bonus / accepted EOS), rows-done mask,
-    // finalized flag
-    bs::DevBuf<int32_t> vroll_first, vroll_fin;
-    bs::DevBuf<unsigned int> vroll_mask;
+    // per rollout: lowest deciding row seen (claim hint) and the state word (rows done |
+    // rows deciding << 32)
+    bs::DevBuf<int32_t> vroll_first;
+    bs::DevBuf<unsigned long long> vroll_state;
     bs::DevBuf<unsigned long long> stats;  // STAT_COUNT counters
     int32_t* responses = nullptr;           // optional [max_rollouts, resp_stride] output
     int64_t resp_stride = 0;

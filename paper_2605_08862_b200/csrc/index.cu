@@ -397,6 +397,8 @@ __device__ __forceinline__ bool probe(const IndexEntry* table, uint64_t mask, ui
 }
 
 __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (b >= a.n) return;
@@ -514,7 +516,8 @@ cudaError_t launch_lookup(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t 
     a.draft_len = draft_len;
     a.match_len = match_len;
     const int blocks = (n * 32 + 255) / 256;
-    lookup_kernel<<<blocks, 256, 0, st>>>(a);
+    cudaError_t le = launch_pdl(lookup_kernel, dim3(blocks), dim3(256), 0, st, a);
+    if (le != cudaSuccess) return le;
     return cudaGetLastError();
 }
 

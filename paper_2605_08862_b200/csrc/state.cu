@@ -26,37 +26,46 @@ __global__ void begin_kernel(int n, int M, const int32_t* slots, const unsigned 
     uid[s] = uids[b];
 }
 
+// One warp per rollout (Alg. 1 lines 15/22): lane i owns tail slot i (M <= 32) and emitted
+// token i (out_len <= k+1 <= 32); the shift of the tail is two shuffles.
 __global__ void commit_kernel(int n, int M, int k, int eos, const int32_t* slots,
                               const int32_t* out_tokens, const int32_t* out_len, int32_t* tail,
                               int32_t* ctx_len, int32_t* pos, const int32_t* max_len,
                               int32_t* finished, int32_t* fin_out, int32_t* resp,
                               int64_t resp_stride) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const int b = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (b >= n) return;
     const int s = slots[b];
     const int no = out_len[b];
+    const int fin = finished[s];
+    const int p = pos[s], L = max_len[s];
     const int32_t* out = out_tokens + (int64_t)b * (k + 1);
     int32_t* tl = tail + (int64_t)s * M;
-    if (no > 0 && !finished[s]) {
-        int32_t old[32];
-        for (int i = 0; i < M; ++i) old[i] = tl[i];
-        for (int i = 0; i < M; ++i) {
-            const int src = i + no;  // index into old ++ out
-            tl[i] = (src < M) ? old[src] : out[src - M];
+    int f = fin;
+    if (no > 0 && !fin) {
+        const int32_t old = (lane < M) ? tl[lane] : -1;
+        const int32_t ot = (lane < no) ? out[lane] : -1;
+        // new tail[i] = (old ++ out)[i + no]
+        const int src = lane + no;
+        const int32_t from_old = __shfl_sync(0xFFFFFFFFu, old, src & 31);
+        const int32_t from_out = __shfl_sync(0xFFFFFFFFu, ot, (src - M) & 31);
+        if (lane < M) tl[lane] = (src < M) ? from_old : from_out;
+        if (resp && lane < no && p + lane < resp_stride) resp[(int64_t)s * resp_stride + p + lane] = ot;
+        const int32_t last = __shfl_sync(0xFFFFFFFFu, ot, no - 1);
+        f = ((eos >= 0 && last == eos) || p + no >= L) ? 1 : 0;
+        if (lane == 0) {
+            ctx_len[s] = min(M, ctx_len[s] + no);
+            pos[s] = p + no;
+            if (f) finished[s] = 1;
         }
-        ctx_len[s] = min(M, ctx_len[s] + no);
-        if (resp) {
-            int32_t* rr = resp + (int64_t)s * resp_stride;
-            for (int i = 0; i < no; ++i)
-                if (pos[s] + i < resp_stride) rr[pos[s] + i] = out[i];
-        }
-        const int p = pos[s] + no;
-        pos[s] = p;
-        if ((eos >= 0 && out[no - 1] == eos) || p >= max_len[s]) finished[s] = 1;
-    } else if (pos[s] >= max_len[s]) {
-        finished[s] = 1;
+    } else if (p >= L) {
+        f = 1;
+        if (lane == 0) finished[s] = 1;
     }
-    if (fin_out) fin_out[b] = finished[s];
+    if (fin_out && lane == 0) fin_out[b] = f;
 }
 
 __global__ void state_kernel(int n, const int32_t* slots, const int32_t* pos,
@@ -96,11 +105,10 @@ cudaError_t launch_begin(bs_ctx* ctx, int32_t n, const int32_t* slots,
 cudaError_t launch_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* out_tokens,
                           const int32_t* out_len, int32_t k, int32_t* finished, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    commit_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, ctx->M, k, ctx->cfg.eos_id, slots, out_tokens,
-                                                   out_len, ctx->tail.p, ctx->ctx_len.p, ctx->pos.p,
-                                                   ctx->max_len.p, ctx->finished.p, finished,
-                                                   ctx->responses, ctx->resp_stride);
-    return cudaGetLastError();
+    return launch_pdl(commit_kernel, dim3((n + 3) / 4), dim3(128), 0, st, n, ctx->M, k,
+                      ctx->cfg.eos_id, slots, out_tokens, out_len, ctx->tail.p, ctx->ctx_len.p,
+                      ctx->pos.p, (const int32_t*)ctx->max_len.p, ctx->finished.p, finished,
+                      ctx->responses, ctx->resp_stride);
 }
 
 cudaError_t launch_state(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* pos,

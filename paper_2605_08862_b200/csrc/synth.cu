@@ -34,6 +34,8 @@ __global__ void target_rows_kernel(int n, int k, int M, const int32_t* slots, co
                                    const int32_t* draft_len, const int32_t* tail, const int32_t* pos,
                                    const int32_t* prompt, uint32_t tseed, int mode, int64_t nbank,
                                    int64_t* row_index) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= n) return;
     const int s = slots[b];
@@ -64,10 +66,10 @@ cudaError_t launch_target_rows(bs_ctx* ctx, int32_t n, const int32_t* slots, con
                                const int32_t* draft_len, int32_t k, uint32_t tseed, int32_t mode,
                                int64_t nbank, int64_t* row_index, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    target_rows_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, k, ctx->M, slots, draft, draft_len,
-                                                        ctx->tail.p, ctx->pos.p, ctx->prompt.p, tseed,
-                                                        mode, nbank, row_index);
-    return cudaGetLastError();
+    return launch_pdl(target_rows_kernel, dim3((n + 127) / 128), dim3(128), 0, st, n, k, ctx->M,
+                      slots, draft, draft_len, (const int32_t*)ctx->tail.p,
+                      (const int32_t*)ctx->pos.p, (const int32_t*)ctx->prompt.p, tseed, mode, nbank,
+                      row_index);
 }
 
 }  // namespace bs

@@ -20,8 +20,9 @@
 // when they were claimed speculatively before that rejection was known.  Rows
 // complete out of order; per rollout, atomicMin keeps the first deciding row and atomicOr
 // the set of completed rows, and the row that completes the prefix finalizes (CAS).
+#include <algorithm>
 #include <cstdlib>
-#include <cub/block/block_scan.cuh>
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -64,6 +65,8 @@ __device__ unsigned long long g_phase[16];
     } while (0)
 #endif
 
+struct RowDesc;
+
 struct VerifyArgs {
     const int32_t* slots;
     const uint16_t* logits;
@@ -76,16 +79,15 @@ struct VerifyArgs {
     const int32_t* pos;
     const unsigned long long* uid;
     const int32_t* rb_q;
-    const int32_t* active;  // compacted live rollouts (plan kernel)
-    unsigned int* ctl;      // VCTL_* words
+    const RowDesc* items;  // the step's rows, j-major (plan kernel)
+    unsigned int* ctl;            // VCTL_* words
     uint32_t* dev_err;
     int32_t* row_status;
     int32_t* row_cand;
     unsigned long long* row_z;
     float* row_norm;
-    int32_t* roll_first;
-    int32_t* roll_fin;
-    unsigned int* roll_mask;
+    int32_t* roll_first;                 // lowest deciding row seen so far (claim hint)
+    unsigned long long* roll_state;      // rows completed (bits 0-31) | rows deciding (32-63)
     int32_t* out_tokens;
     int32_t* out_len;
     int32_t* out_acc;
@@ -96,11 +98,18 @@ struct VerifyArgs {
 
 struct RowDesc {
     int32_t b, j, q, d;  // rollout, row, clamped draft length, d_{j+1} (-1 if j == q); b < 0: end
-    int64_t rowno;
+    int64_t rowno;       // logits row
+    unsigned long long uid;  // rollout uid (Philox counter words 2-3, R6)
+    int32_t position;    // generated-token index of the row's sample (Philox counter word 0)
     int32_t aligned;     // bulk copies usable (16-byte aligned row)
-    int32_t pad;
-    uint32_t rng[8];     // Philox draws: ACCEPT (0-3), SAMPLE (4-7)
+    int32_t pad[2];
 };
+static_assert(sizeof(RowDesc) == 48, "RowDesc layout");
+
+// Philox draw for row dsc and purpose (R6): key = seed, counter = (position, purpose, uid).
+__device__ __forceinline__ U128 row_draw(const VerifyArgs& a, const RowDesc& dsc, uint32_t purpose) {
+    return draw(a.seed, dsc.uid, (uint32_t)dsc.position, purpose);
+}
 
 // Consumer -> epilogue handoff of one row (double-buffered).
 struct EpiBuf {
@@ -127,7 +136,7 @@ struct __align__(16) VShared {
 };
 
 // Alg. 1 lines 10-31 for rollout b, decided at row F (rows < F accepted).
-__device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int F, int q) {
+__device__ void finalize_rollout(const VerifyArgs& a, unsigned long long* s, int b, int F, int q) {
     const int kp1 = a.k + 1;
     int32_t* out = a.out_tokens + (int64_t)b * kp1;
     const int32_t* d = a.draft + (int64_t)b * a.k;
@@ -149,7 +158,6 @@ __device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int F,
         if (a.out_norm) a.out_norm[base + i] = __ldcg(a.row_norm + base + i);
         if (a.out_z) a.out_z[base + i] = __ldcg(a.row_z + base + i);
     }
-    unsigned long long* s = sh.stat;
     if (q > 0) {
         s[STAT_STEPS_SPEC] += 1ull;
         s[STAT_EMIT_SPEC] += (unsigned long long)n;
@@ -163,28 +171,54 @@ __device__ void finalize_rollout(const VerifyArgs& a, VShared& sh, int b, int F,
     s[STAT_ROWS_NEEDED] += (unsigned long long)(F + 1);
 }
 
+// Rollout state word: bit j = row j completed, bit 32+j = row j decides (reject / bonus /
+// accepted EOS).  Alg. 1 is decided once the lowest deciding row F and every row below it
+// are complete; that predicate only turns true once under OR, so the single atomic that
+// makes it true finalizes (no CAS, no store-buffering hazard).
+__device__ __forceinline__ bool prefix_decided(unsigned long long st, int& F) {
+    const uint32_t dec = (uint32_t)(st >> 32);
+    if (!dec) return false;
+    F = __ffs(dec) - 1;
+    const uint32_t need = (F >= 31) ? 0xFFFFFFFFu : ((2u << F) - 1u);
+    return ((uint32_t)st & need) == need;
+}
+
+__device__ __forceinline__ unsigned long long atom_or_acq_rel(unsigned long long* p, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.or.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+
 // Record a completed row and finalize its rollout if this completes the decided prefix.
-__device__ void complete_row(const VerifyArgs& a, VShared& sh, int b, int j, int q, int status,
+__device__ void complete_row(const VerifyArgs& a, unsigned long long* stat, int b, int j, int q, int status,
                              int cand, unsigned long long z, float norm) {
     const int64_t r = (int64_t)b * (a.k + 1) + j;
     a.row_status[r] = status;
     a.row_cand[r] = cand;
     a.row_z[r] = z;
     a.row_norm[r] = norm;
-    __threadfence();
-    // Store-buffering pattern between rows of one rollout: (min first; OR mask) here vs
-    // (OR mask; read first) there.  The fences make at least one of any two finishing
-    // rows see both updates, so exactly one of them finalizes.
-    if (status != ST_CONT) atomicMin(a.roll_first + b, j);
-    __threadfence();
-    const unsigned mask = atomicOr(a.roll_mask + b, 1u << j) | (1u << j);
-    __threadfence();
-    const int F = atomicAdd(a.roll_first + b, 0);
-    const unsigned need = (F >= 31) ? 0xFFFFFFFFu : ((2u << F) - 1u);
-    if ((mask & need) == need && atomicCAS(a.roll_fin + b, 0, 1) == 0) {
-        __threadfence();
-        finalize_rollout(a, sh, b, F, q);
+    const bool decides = status != ST_CONT;
+    if (decides) atomicMin(a.roll_first + b, j);  // claim hint only (relaxed)
+    const unsigned long long mine = (1ull << j) | (decides ? (1ull << (32 + j)) : 0ull);
+    // release: this row's record; acquire: every earlier row's record of the rollout
+    const unsigned long long old = atom_or_acq_rel(a.roll_state + b, mine);
+    int F0, F1;
+    if (!prefix_decided(old, F0) && prefix_decided(old | mine, F1)) finalize_rollout(a, stat, b, F1, q);
+}
+
+// Claim the next needed row of the plan's j-major table (Alg. 1's order across the batch),
+// skipping rows at or above an already-decided row of their rollout.  b < 0: none left.
+__device__ RowDesc claim_row(const VerifyArgs& a, int rows) {
+    for (;;) {
+        const int r = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
+        if (r >= rows) break;
+        const RowDesc it = a.items[r];
+        if (it.j > ld_volatile_i32(a.roll_first + it.b)) continue;  // decided below
+        return it;
     }
+    RowDesc none;
+    none.b = -1;
+    return none;
 }
 
 // ================================================================ epilogue warp
@@ -223,18 +257,14 @@ __device__ void epilogue_row(const VerifyArgs& a, VShared& sh, const EpiBuf& E, 
         const uint64_t Z = shfl_u64(incl, 31);
         const uint64_t md = (d >= 0) ? mass_of(__uint_as_float((uint32_t)row[d] << 16), mp) : 0ull;
         bool acc = false;
-        if (j < q) {
-            const U128 r1{dsc.rng[0], dsc.rng[1], dsc.rng[2], dsc.rng[3]};
-            acc = uniform_floor(r1, Z) < md;
-        }
+        if (j < q) acc = uniform_floor(row_draw(a, dsc, PURPOSE_ACCEPT), Z) < md;
         status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
         Zo = Z;
         norm = (float)ldexp((double)Z, -a.S);
         if (status == ST_DECIDED) {
             // residual (d excluded) or bonus sample (R8) by inverse CDF in ascending id
             const int excl = (j < q) ? d : -1;
-            const U128 r2{dsc.rng[4], dsc.rng[5], dsc.rng[6], dsc.rng[7]};
-            const uint64_t U = uniform_floor(r2, Z - ((j < q) ? md : 0ull));
+            const uint64_t U = uniform_floor(row_draw(a, dsc, PURPOSE_SAMPLE), Z - ((j < q) ? md : 0ull));
             // the excluded token's mass comes off the block holding it
             const int ex_blk = (excl >= 0) ? ((excl / (2 * CHE)) * NCW + ((excl % (2 * CHE)) / CHE) * (NCW / 2) +
                                               ((excl % CHE) / BLK))
@@ -306,7 +336,7 @@ __device__ void epilogue_row(const VerifyArgs& a, VShared& sh, const EpiBuf& E, 
     }
     if (lane == 0) {
         sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-        complete_row(a, sh, b, j, q, ok ? status : ST_DECIDED, ok ? cand : -1, Zo, norm);
+        complete_row(a, sh.stat, b, j, q, ok ? status : ST_DECIDED, ok ? cand : -1, Zo, norm);
     }
     __syncwarp();
 }
@@ -315,10 +345,11 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw);
     VShared& sh = *reinterpret_cast<VShared*>(smem_raw + (size_t)NSTAGE * CHE * 2);
+    pdl_wait();
+    pdl_trigger();
+    if (a.ctl[VCTL_MODE] != 0) return;  // few rows: the split (cluster) kernel runs instead
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nact = (int)a.ctl[VCTL_NACTIVE];
-    const int kp1 = a.k + 1;
-    const int total = kp1 * nact;  // claimable items (j-major), j > q_b are holes
+    const int rows = (int)a.ctl[VCTL_ROWS];
 
     if (tid == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
@@ -345,40 +376,7 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
         const uint64_t pol_first = policy_evict_first();
         uint32_t rph = 0;    // row-empty phase bits, one per FIFO slot
         uint32_t P = 0;      // chunks issued so far: stage P % NSTAGE, use P / NSTAGE
-        // claim the next needed row (j-major over the live rollouts) and fill its descriptor
-        auto claim = [&]() {
-            RowDesc dsc;
-            dsc.b = -1;
-            int b = -1, j = 0, q = 0;
-            for (;;) {
-                const int r = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
-                if (r >= total) break;
-                j = r / nact;
-                const int bb = a.active[r - j * nact];
-                q = a.rb_q[bb];
-                if (j > q) continue;                                   // beyond the draft
-                if (j > ld_volatile_i32(a.roll_first + bb)) continue;  // decided below
-                b = bb;
-                break;
-            }
-            if (b >= 0) {
-                dsc.b = b;
-                dsc.j = j;
-                dsc.q = q;
-                dsc.d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;
-                dsc.rowno = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
-                const uint16_t* row = a.logits + dsc.rowno * a.stride;
-                dsc.aligned = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0) ? 1 : 0;
-                const int slot = a.slots[b];
-                const uint64_t uidv = a.uid[slot];
-                const uint32_t position = (uint32_t)(a.pos[slot] + j);
-                const U128 r1 = draw(a.seed, uidv, position, PURPOSE_ACCEPT);
-                const U128 r2 = draw(a.seed, uidv, position, PURPOSE_SAMPLE);
-                dsc.rng[0] = r1.x0; dsc.rng[1] = r1.x1; dsc.rng[2] = r1.x2; dsc.rng[3] = r1.x3;
-                dsc.rng[4] = r2.x0; dsc.rng[5] = r2.x1; dsc.rng[6] = r2.x2; dsc.rng[7] = r2.x3;
-            }
-            return dsc;
-        };
+        auto claim = [&]() { return claim_row(a, rows); };
         RowDesc nxt = claim();
         for (int seq = 0;; ++seq) {
             const RowDesc cur = nxt;
@@ -603,21 +601,33 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
     }
 }
 
-// ---- plan: clamp q per rollout, compact the live rollouts, reset per-rollout state
+#include "verify_cluster.cuh"
+#include "verify_split.cuh"
+#include "verify_topp.cuh"
+
+// ---- plan: clamp q per rollout, reset per-rollout state, and lay out the step's rows as a
+// j-major table (rows (b, 0) of every live rollout, then (b, 1), ...: Alg. 1's order across
+// the batch) with everything a row needs (no dependent loads when a CTA claims it).
 constexpr int PLAN_NT = 1024;
 __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     int n, int k, int V, const int32_t* slots, const int32_t* draft, const int32_t* draft_len,
-    const int32_t* pos, const int32_t* max_len, const int32_t* finished, int32_t* rb_q,
-    int32_t* active, unsigned int* ctl, int32_t* roll_first, int32_t* roll_fin,
-    unsigned int* roll_mask, int32_t* out_len, int32_t* out_acc, int32_t* out_tokens,
-    float* out_norm, unsigned long long* out_z, uint32_t* dev_err) {
-    using Scan = cub::BlockScan<int, PLAN_NT>;
-    __shared__ typename Scan::TempStorage tmp;
+    const int32_t* pos, const int32_t* max_len, const int32_t* finished,
+    const unsigned long long* uid, const uint16_t* logits, const int64_t* row_index,
+    int64_t stride, int32_t* rb_q, RowDesc* items, unsigned int* ctl, int32_t* roll_first,
+    unsigned long long* roll_state, int32_t* out_len, int32_t* out_acc, int32_t* out_tokens,
+    float* out_norm, unsigned long long* out_z, uint32_t* dev_err, int mode) {
+    __shared__ int hist[33], lvl_off[33], lvl_ctr[33], s_rows, s_nact;
+    pdl_wait();
+    pdl_trigger();
     const int tid = threadIdx.x;
+    if (tid < 33) {
+        hist[tid] = 0;
+        lvl_ctr[tid] = 0;
+    }
+    __syncthreads();
     const int per = (n + PLAN_NT - 1) / PLAN_NT;
     const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
     const int kp1 = k + 1;
-    int mine = 0;
     for (int b = b0; b < b1; ++b) {
         const int s = slots[b];
         const int p = pos[s], L = max_len[s];
@@ -635,9 +645,8 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
         }
         rb_q[b] = q;
         roll_first[b] = q;  // the bonus row q always decides; earlier rows may lower it
-        roll_fin[b] = 0;
-        roll_mask[b] = 0u;
-        mine += (q >= 0) ? 1 : 0;
+        roll_state[b] = 0ull;
+        if (q >= 0) atomicAdd(&hist[q], 1);
         for (int jj = 0; jj < kp1; ++jj) {
             if (out_norm) out_norm[(int64_t)b * kp1 + jj] = 0.f;
             if (out_z) out_z[(int64_t)b * kp1 + jj] = 0ull;
@@ -648,30 +657,89 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
             for (int jj = 0; jj < kp1; ++jj) out_tokens[(int64_t)b * kp1 + jj] = -1;
         }
     }
-    int excl, total;
-    Scan(tmp).ExclusiveSum(mine, excl, total);
-    for (int b = b0; b < b1; ++b)
-        if (rb_q[b] >= 0) active[excl++] = b;
+    __syncthreads();
+    if (tid == 0) {  // level j holds the rollouts with q >= j
+        int off = 0, nact = 0;
+        for (int j = 0; j <= k; ++j) {
+            int cnt = 0;
+            for (int qq = j; qq <= k; ++qq) cnt += hist[qq];
+            if (j == 0) nact = cnt;
+            lvl_off[j] = off;
+            off += cnt;
+        }
+        s_rows = off;
+        s_nact = nact;
+    }
+    __syncthreads();
+    for (int b = b0; b < b1; ++b) {
+        const int q = rb_q[b];
+        if (q < 0) continue;
+        const int s = slots[b];
+        const unsigned long long u = uid[s];
+        const int p = pos[s];
+        for (int j = 0; j <= q; ++j) {
+            RowDesc it;
+            it.b = b;
+            it.j = j;
+            it.q = q;
+            it.d = (j < q) ? draft[(int64_t)b * k + j] : -1;
+            it.rowno = row_index ? row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+            it.uid = u;
+            it.position = p + j;
+            it.aligned = ((reinterpret_cast<uintptr_t>(logits + it.rowno * stride) & 15u) == 0) ? 1 : 0;
+            it.pad[0] = it.pad[1] = 0;
+            items[lvl_off[j] + atomicAdd(&lvl_ctr[j], 1)] = it;  // order within a level: any
+        }
+    }
     if (tid == 0) {
         ctl[VCTL_NEXT] = 0u;
-        ctl[VCTL_NACTIVE] = (unsigned)total;
+        ctl[VCTL_NACTIVE] = (unsigned)s_nact;
+        ctl[VCTL_ROWS] = (unsigned)s_rows;
+        ctl[VCTL_MODE] = (unsigned)mode;
     }
 }
+
+// Slice of a row per cluster CTA: ceil(V / 8) rounded up to whole 256-element tiles.
+static int split_slice(int V) { return ((V + SP_CL - 1) / SP_CL + 255) / 256 * 256; }
+// Which kernel verifies rows (bsx_set_verify_kernel; env BS_VERIFY_KERNEL for tools).
+enum { VK_AUTO = 0, VK_ROWS = 1, VK_SPLIT = 2, VK_CLUSTER = 3 };
+static int verify_kind(const bs_ctx* ctx, int V) {
+    int k = ctx->verify_kind;
+    if (k == VK_AUTO) {
+        static int env = -1;
+        if (env < 0) {
+            const char* s = getenv("BS_VERIFY_KERNEL");
+            env = s ? atoi(s) : 0;
+        }
+        k = env;
+    }
+    if (k == VK_AUTO) k = VK_CLUSTER;
+    if (k == VK_CLUSTER && (V + CK_CL - 1) / CK_CL > CK_MAXSL) k = VK_ROWS;
+    return k;
+}
+// Slice of a row per cluster CTA: ceil(V / 8) rounded up to whole 512-element tiles.
+static int cluster_slice(int V) { return ((V + CK_CL - 1) / CK_CL + CK_TILE - 1) / CK_TILE * CK_TILE; }
+
+static int ntile_ok(int V) { return (V + 255) / 256 <= TP_MAXT ? 1 : 0; }
 
 cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits,
                           const int64_t* row_index, int64_t stride, const int32_t* draft,
                           const int32_t* draft_len, int32_t k, float T, float top_p,
                           int32_t* out_tokens, int32_t* out_len, int32_t* out_acc,
                           float* out_norm, unsigned long long* out_z, cudaStream_t st) {
-    (void)top_p;
     if (n == 0) return cudaSuccess;
     const int V = ctx->cfg.vocab;
-    verify_plan_kernel<<<1, PLAN_NT, 0, st>>>(n, k, V, slots, draft, draft_len, ctx->pos.p,
-                                              ctx->max_len.p, ctx->finished.p, ctx->rb_q.p,
-                                              ctx->vqueue.p, ctx->vctl.p, ctx->vroll_first.p,
-                                              ctx->vroll_fin.p, ctx->vroll_mask.p, out_len,
-                                              out_acc, out_tokens, out_norm, out_z, ctx->dev_err.p);
-    cudaError_t e = cudaGetLastError();
+    const bool topp = T > 0.f && top_p < 1.f;
+    const int kind = topp ? VK_ROWS : verify_kind(ctx, V);
+    const int plan_mode = (kind == VK_SPLIT) ? 1 : (kind == VK_CLUSTER ? 3 : 0);
+    cudaError_t e = launch_pdl(
+        verify_plan_kernel, dim3(1), dim3(PLAN_NT), 0, st, n, k, V, slots, draft, draft_len,
+        (const int32_t*)ctx->pos.p, (const int32_t*)ctx->max_len.p,
+        (const int32_t*)ctx->finished.p, (const unsigned long long*)ctx->uid.p,
+        static_cast<const uint16_t*>(logits), row_index, stride, ctx->rb_q.p,
+        reinterpret_cast<RowDesc*>(ctx->vqueue.p), ctx->vctl.p, ctx->vroll_first.p,
+        ctx->vroll_state.p, out_len, out_acc, out_tokens, out_norm, out_z, ctx->dev_err.p,
+        plan_mode);
     if (e != cudaSuccess) return e;
     VerifyArgs a = {};
     a.slots = slots;
@@ -686,13 +754,14 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.nchunk = (V + CHE - 1) / CHE;
     a.ngroup = (a.nchunk + 1) / 2;
     if (a.ngroup > MAXG) return cudaErrorInvalidValue;
+    if (kind == VK_SPLIT && split_slice(V) / 256 > SP_MAXT) return cudaErrorInvalidValue;
     a.T = T;
     a.c = (T > 0.f) ? (float)(1.4426950408889634 / (double)T) : 0.f;
     a.seed = ctx->cfg.seed;
     a.pos = ctx->pos.p;
     a.uid = ctx->uid.p;
     a.rb_q = ctx->rb_q.p;
-    a.active = ctx->vqueue.p;
+    a.items = reinterpret_cast<const RowDesc*>(ctx->vqueue.p);
     a.ctl = ctx->vctl.p;
     a.dev_err = ctx->dev_err.p;
     a.row_status = ctx->vrow_status.p;
@@ -700,14 +769,60 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.row_z = ctx->vrow_z.p;
     a.row_norm = ctx->vrow_norm.p;
     a.roll_first = ctx->vroll_first.p;
-    a.roll_fin = ctx->vroll_fin.p;
-    a.roll_mask = ctx->vroll_mask.p;
+    a.roll_state = ctx->vroll_state.p;
     a.out_tokens = out_tokens;
     a.out_len = out_len;
     a.out_acc = out_acc;
     a.out_norm = out_norm;
     a.out_z = out_z;
     a.stats = ctx->stats.p;
+    if (topp) {  // R5: top-p filtered rows (verify_topp.cuh)
+        if (ntile_ok(V) == 0) return cudaErrorInvalidValue;
+        const size_t tsm = sizeof(TopPShared);
+        static int tp_configured = 0;
+        if (!tp_configured) {
+            e = cudaFuncSetAttribute(verify_topp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tsm);
+            if (e != cudaSuccess) return e;
+            tp_configured = 1;
+        }
+        const int tgrid = std::max(1, std::min(ctx->num_sms * 2, n * (k + 1)));
+        return launch_pdl(verify_topp_kernel, dim3(tgrid), dim3(TP_NT), tsm, st, a, top_p);
+    }
+    if (kind == VK_CLUSTER) {
+        const int SL = cluster_slice(V);
+        const size_t csm = ck_smem_bytes(SL);
+        static size_t ck_configured = 0;
+        static int ck_clusters = 0;
+        if (ck_configured != csm) {
+            e = cudaFuncSetAttribute(verify_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)csm);
+            if (e != cudaSuccess) return e;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(CK_CL * ctx->num_sms);
+            cfg.blockDim = dim3(CK_NT);
+            cfg.dynamicSmemBytes = csm;
+            int ncl = 0;
+            e = cudaOccupancyMaxActiveClusters(&ncl, verify_cluster_kernel, &cfg);
+            if (e != cudaSuccess) return e;
+            ck_clusters = std::max(1, ncl);
+            ck_configured = csm;
+        }
+        return launch_pdl(verify_cluster_kernel, dim3(ck_clusters * CK_CL), dim3(CK_NT), csm, st, a, SL);
+    }
+    if (kind == VK_SPLIT) {
+        const int SL = split_slice(V);
+        const size_t ssm = ((sizeof(SplitShared) + 127) & ~size_t(127)) + (size_t)SL * 2;
+        static size_t sp_configured = 0;
+        if (sp_configured < ssm) {
+            e = cudaFuncSetAttribute(verify_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ssm);
+            if (e != cudaSuccess) return e;
+            sp_configured = ssm;
+        }
+        const int nclus = std::max(1, (ctx->num_sms * 2) / SP_CL);
+        return launch_pdl(verify_split_kernel, dim3(nclus * SP_CL), dim3(SP_NT), ssm, st, a, SL);
+    }
     const size_t smem = (size_t)NSTAGE * CHE * 2 + sizeof(VShared);
     static int configured = 0;
     if (!configured) {
@@ -717,8 +832,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
         configured = 1;
     }
     const int grid = std::max(1, std::min(ctx->num_sms * CTAS_PER_SM, n * (k + 1)));
-    verify_rows_kernel<<<grid, NTHR, smem, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(verify_rows_kernel, dim3(grid), dim3(NTHR), smem, st, a);
 }
 
 }  // namespace bs

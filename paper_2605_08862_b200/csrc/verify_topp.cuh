@@ -1,0 +1,322 @@
+// verify_topp.cuh — verify + resample under top-p filtering (reading R5, DESIGN.md §3/§5),
+// included by verify.cu (shares its row queue, descriptors and completion protocol).
+//
+// The tie-closed nucleus keeps {i : mass_i >= tau}, tau = max{t : F(t) >= Theta},
+// F(t) = sum of the masses >= t.  mass is a nondecreasing function of the bf16 logit, so
+// tau is found by a mass-weighted select over the 16-bit order key of the logits instead
+// of a sort:
+//   pass 1  row max (R1, validity R0);
+//   pass 2  masses: Z, and the mass of each of 4096 coarse key bins (key >> 4);
+//   select  the coarse bin B where the descending cumulative mass reaches Theta;
+//   pass 3  the masses of the 16 keys inside B -> the crossing key k*, tau = mass(k*);
+//   pass 4  (only when a sample is drawn, or when keys below k* share its mass) the
+//           filtered masses' 256-element tile sums, which give Z' and the inverse CDF.
+// One persistent CTA per row; the row is read from HBM once and re-read from L2.
+#pragma once
+// (included inside namespace bs)
+
+constexpr int TP_NT = 512;            // threads
+constexpr int TP_NW = TP_NT / 32;     // warps
+constexpr int TP_H1 = 4096;           // coarse key bins
+constexpr int TP_MAXT = 2048;         // 256-element tiles: V <= 524288
+
+struct TopPShared {
+    unsigned long long h1[TP_H1];
+    unsigned long long tsum[TP_MAXT];
+    unsigned long long h2[16];
+    unsigned long long stat[STAT_COUNT];
+    float wmax[TP_NW];
+    uint32_t wbad[TP_NW];
+    RowDesc dsc;
+    unsigned long long bz[3];  // [0] Theta remaining inside the coarse bin, [1] sum above it, [2] Z
+    int32_t bsel;              // coarse bin B
+};
+
+// Order-preserving map of bf16 bit patterns to 16-bit keys (larger value -> larger key).
+__device__ __forceinline__ uint32_t tp_key(uint32_t b) {
+    return (b & 0x8000u) ? (~b & 0xFFFFu) : (b | 0x8000u);
+}
+__device__ __forceinline__ uint32_t tp_unkey(uint32_t k) {
+    return (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu);
+}
+
+// Lane's 8 consecutive logits of tile t (-inf beyond V / scalar path when unaligned).
+__device__ __forceinline__ uint4 tp_load8(const uint16_t* row, int e0, int V, bool aligned) {
+    if (aligned && e0 + 8 <= V) return __ldcg(reinterpret_cast<const uint4*>(row + e0));
+    uint16_t t8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t8[i] = (e0 + i < V) ? row[e0 + i] : (uint16_t)0xFF80u;
+    return make_uint4(t8[0] | ((uint32_t)t8[1] << 16), t8[2] | ((uint32_t)t8[3] << 16),
+                      t8[4] | ((uint32_t)t8[5] << 16), t8[6] | ((uint32_t)t8[7] << 16));
+}
+__device__ __forceinline__ void tp_unpack(const uint4 v, uint32_t b[8]) {
+    b[0] = v.x & 0xFFFFu; b[1] = v.x >> 16; b[2] = v.y & 0xFFFFu; b[3] = v.y >> 16;
+    b[4] = v.z & 0xFFFFu; b[5] = v.z >> 16; b[6] = v.w & 0xFFFFu; b[7] = v.w >> 16;
+}
+
+__global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs a, float top_p) {
+    extern __shared__ __align__(16) uint8_t tp_smem[];
+    TopPShared& sh = *reinterpret_cast<TopPShared*>(tp_smem);
+    pdl_wait();
+    pdl_trigger();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rows = (int)a.ctl[VCTL_ROWS];
+    const int V = a.V;
+    const int ntile = (V + 255) / 256;
+    const uint64_t P = (uint64_t)llround((double)top_p * 4294967296.0);  // R5 (top_p < 1)
+    for (int i = tid; i < STAT_COUNT; i += TP_NT) sh.stat[i] = 0ull;
+
+    for (;;) {
+        if (tid == 0) sh.dsc = claim_row(a, rows);
+        __syncthreads();
+        const RowDesc dsc = sh.dsc;
+        if (dsc.b < 0) break;
+        const uint16_t* row = a.logits + dsc.rowno * a.stride;
+        const bool aligned = dsc.aligned != 0;
+        const int j = dsc.j, q = dsc.q, d = dsc.d;
+
+        // ---------------------------------------------------- pass 1: max
+        uint32_t mx = 0xFF80FF80u;
+        for (int t = warp; t < ntile; t += TP_NW) {
+            const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+            mx = hmax2_nan_u32(mx, v.x);
+            mx = hmax2_nan_u32(mx, v.y);
+            mx = hmax2_nan_u32(mx, v.z);
+            mx = hmax2_nan_u32(mx, v.w);
+        }
+        {
+            const float lo = bf16lo(mx), hi = bf16hi(mx);
+            uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
+            float fm = fmaxf(lo, hi);
+#pragma unroll
+            for (int mm = 16; mm; mm >>= 1) fm = fmaxf(fm, __shfl_xor_sync(0xFFFFFFFFu, fm, mm));
+            bad = __any_sync(0xFFFFFFFFu, bad) ? 1u : 0u;
+            if (lane == 0) {
+                sh.wmax[warp] = fm;
+                sh.wbad[warp] = bad;
+            }
+        }
+        for (int i = tid; i < TP_H1; i += TP_NT) sh.h1[i] = 0ull;
+        if (tid < 16) sh.h2[tid] = 0ull;
+        __syncthreads();
+        float m = -INFINITY;
+        uint32_t bb = 0;
+        for (int w = 0; w < TP_NW; ++w) {
+            m = fmaxf(m, sh.wmax[w]);
+            bb |= sh.wbad[w];
+        }
+        uint32_t err = 0;
+        if (bb) err |= DEV_BAD_LOGIT;
+        else if (m == -INFINITY) err |= DEV_ALL_NEGINF;
+        else if (!(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) err |= DEV_RANGE;
+        if (err) {  // R0: the row is an error; the rollout stops (no token)
+            if (tid == 0) {
+                atomicOr(a.dev_err, err);
+                sh.stat[STAT_ROWS_VERIFIED] += 1ull;
+                complete_row(a, sh.stat, dsc.b, j, q, ST_DECIDED, -1, 0ull, 0.f);
+            }
+            __syncthreads();
+            continue;
+        }
+        MassParams mp;
+        mp.c = a.c;
+        mp.nmc = -__fmul_rn(m, a.c);
+        mp.clampv = -(float)(a.S + 2);
+        mp.magic = 12582912.0f + (float)a.S;
+
+        // ---------------------------------------------------- pass 2: masses, Z, coarse bins
+        for (int t = warp; t < ntile; t += TP_NW) {
+            const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+            uint64_t mm[8];
+            mass_pair(v.x, mp, mm[0], mm[1]);
+            mass_pair(v.y, mp, mm[2], mm[3]);
+            mass_pair(v.z, mp, mm[4], mm[5]);
+            mass_pair(v.w, mp, mm[6], mm[7]);
+            uint32_t bits[8];
+            tp_unpack(v, bits);
+            uint64_t s = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                s += mm[i];
+                if (mm[i]) atomicAdd(&sh.h1[tp_key(bits[i]) >> 4], (unsigned long long)mm[i]);
+            }
+            const uint64_t ws = warp_sum_u51(s);
+            if (lane == 0) sh.tsum[t] = ws;
+        }
+        __syncthreads();
+        // Z and the coarse select (warp 0): lane l owns bins [l*128, l*128+128)
+        if (warp == 0) {
+            uint64_t zl = 0;
+            for (int t = lane; t < ntile; t += 32) zl += sh.tsum[t];
+            const uint64_t Z = warp_sum_u64(zl);
+            unsigned __int128 th = (unsigned __int128)P * Z + (((unsigned __int128)1 << 32) - 1);
+            uint64_t theta = (uint64_t)(th >> 32);
+            theta = theta ? theta : 1ull;  // top_p -> 0 keeps the heaviest level (as R5)
+            const int per = TP_H1 / 32;
+            const int lo = (31 - lane) * per;  // lane 0 owns the heaviest bins
+            uint64_t ls = 0;
+            for (int i = 0; i < per; ++i) ls += sh.h1[lo + i];
+            const uint64_t incl = warp_incl_scan_u64(ls, lane);  // mass of bins >= lane's lowest
+            const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= theta);
+            const int L = hit ? (__ffs(hit) - 1) : 31;
+            if (lane == L) {
+                uint64_t above = incl - ls;
+                int B = lo;
+                for (int i = per - 1; i >= 0; --i) {
+                    const uint64_t h = sh.h1[lo + i];
+                    if (above + h >= theta) {
+                        B = lo + i;
+                        break;
+                    }
+                    above += h;
+                }
+                sh.bsel = B;
+                sh.bz[0] = theta - above;  // mass still needed inside bin B
+                sh.bz[1] = above;
+                sh.bz[2] = Z;
+            }
+        }
+        __syncthreads();
+        const int B = sh.bsel;
+
+        // ---------------------------------------------------- pass 3: keys inside bin B
+        for (int t = warp; t < ntile; t += TP_NW) {
+            const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+            uint32_t bits[8];
+            tp_unpack(v, bits);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t kk = tp_key(bits[i]);
+                if ((int)(kk >> 4) == B) {
+                    const uint64_t mi = mass_of(__uint_as_float(bits[i] << 16), mp);
+                    if (mi) atomicAdd(&sh.h2[kk & 15u], (unsigned long long)mi);
+                }
+            }
+        }
+        __syncthreads();
+        // tau = mass(k*); Z' from the histograms unless lower keys share tau (then pass 4)
+        uint64_t tau = 0, Zp = 0;
+        bool tie_below;
+        {
+            const uint64_t need = sh.bz[0];
+            uint64_t above = 0;
+            int ks = B * 16;
+            for (int i = 15; i >= 0; --i) {
+                if (above + sh.h2[i] >= need) {
+                    ks = B * 16 + i;
+                    break;
+                }
+                above += sh.h2[i];
+            }
+            tau = mass_of(__uint_as_float(tp_unkey((uint32_t)ks) << 16), mp);
+            Zp = sh.bz[1] + above + sh.h2[ks & 15];
+            tie_below = ks > 0 && mass_of(__uint_as_float(tp_unkey((uint32_t)ks - 1u) << 16), mp) == tau;
+        }
+        const uint64_t md_full = (d >= 0) ? mass_of(__uint_as_float((uint32_t)row[d] << 16), mp) : 0ull;
+        const uint64_t md = (md_full >= tau) ? md_full : 0ull;  // mass'(d)
+
+        // pass 4: filtered tile sums
+        auto filtered_tiles = [&]() {
+            for (int t = warp; t < ntile; t += TP_NW) {
+                const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+                uint64_t mm[8];
+                mass_pair(v.x, mp, mm[0], mm[1]);
+                mass_pair(v.y, mp, mm[2], mm[3]);
+                mass_pair(v.z, mp, mm[4], mm[5]);
+                mass_pair(v.w, mp, mm[6], mm[7]);
+                uint64_t s = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s += (mm[i] >= tau) ? mm[i] : 0ull;
+                const uint64_t ws = warp_sum_u51(s);
+                if (lane == 0) sh.tsum[t] = ws;
+            }
+            __syncthreads();
+        };
+        bool have_tiles = false;
+        if (tie_below) {
+            __syncthreads();  // tsum of pass 2 was read by warp 0 above
+            filtered_tiles();
+            have_tiles = true;
+            uint64_t zl = 0;
+            for (int t = lane; t < ntile; t += 32) zl += sh.tsum[t];
+            Zp = warp_sum_u64(zl);
+        }
+        // decision (R7) — every thread computes it identically
+        bool acc = false;
+        if (j < q) acc = uniform_floor(row_draw(a, dsc, PURPOSE_ACCEPT), Zp) < md;
+        const int status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
+        int cand = -1;
+        if (status == ST_DECIDED) {
+            // residual (d excluded) or bonus sample (R8): inverse CDF in ascending id
+            if (!have_tiles) {
+                __syncthreads();
+                filtered_tiles();
+            }
+            const int excl = (j < q) ? d : -1;
+            const uint64_t U = uniform_floor(row_draw(a, dsc, PURPOSE_SAMPLE), Zp - ((j < q) ? md : 0ull));
+            if (warp == 0) {
+                const int per = (ntile + 31) / 32;
+                const int i0 = min(ntile, lane * per), i1 = min(ntile, i0 + per);
+                const int ex_t = (excl >= 0) ? excl / 256 : -1;
+                uint64_t ls = 0;
+                for (int i = i0; i < i1; ++i) ls += sh.tsum[i] - ((i == ex_t) ? md : 0ull);
+                const uint64_t incl = warp_incl_scan_u64(ls, lane);
+                const unsigned hit = __ballot_sync(0xFFFFFFFFu, U < incl);
+                const int L = hit ? (__ffs(hit) - 1) : 31;
+                int xt = 0;
+                uint64_t ut = 0;
+                if (lane == L) {
+                    uint64_t cum = incl - ls;
+                    for (int i = i0; i < i1; ++i) {
+                        const uint64_t ts = sh.tsum[i] - ((i == ex_t) ? md : 0ull);
+                        if (U < cum + ts) {
+                            xt = i;
+                            ut = U - cum;
+                            break;
+                        }
+                        cum += ts;
+                    }
+                }
+                xt = __shfl_sync(0xFFFFFFFFu, xt, L);
+                ut = shfl_u64(ut, L);
+                // rescan tile xt: lane l owns its 8 elements
+                const int e0 = xt * 256 + lane * 8;
+                const uint4 v = tp_load8(row, e0, V, aligned);
+                uint64_t mm[8];
+                mass_pair(v.x, mp, mm[0], mm[1]);
+                mass_pair(v.y, mp, mm[2], mm[3]);
+                mass_pair(v.z, mp, mm[4], mm[5]);
+                mass_pair(v.w, mp, mm[6], mm[7]);
+                uint64_t s = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (mm[i] < tau || e0 + i == excl || e0 + i >= V) mm[i] = 0;
+                    s += mm[i];
+                }
+                const uint64_t inc2 = warp_incl_scan_u64(s, lane);
+                const unsigned hit2 = __ballot_sync(0xFFFFFFFFu, ut < inc2);
+                const int L2 = hit2 ? (__ffs(hit2) - 1) : 31;
+                int tok = -1;
+                if (lane == L2) {
+                    uint64_t cum = inc2 - s;
+                    for (int i = 0; i < 8; ++i) {
+                        cum += mm[i];
+                        if (cum > ut) {
+                            tok = e0 + i;
+                            break;
+                        }
+                    }
+                }
+                cand = __shfl_sync(0xFFFFFFFFu, tok, L2);
+            }
+        }
+        if (tid == 0) {
+            sh.stat[STAT_ROWS_VERIFIED] += 1ull;
+            complete_row(a, sh.stat, dsc.b, j, q, status, cand, Zp, (float)ldexp((double)sh.bz[2], -a.S));
+        }
+        __syncthreads();
+    }
+    if (a.stats && tid == 0)
+        for (int i = 0; i < STAT_COUNT; ++i)
+            if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
+}

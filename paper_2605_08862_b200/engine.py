@@ -101,10 +101,12 @@ class RolloutEngine:
         return g
 
     def run_graph(self):
-        self.graph.replay()
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
 
     def all_finished(self) -> bool:
-        return bool(self.finished.all().item())
+        with torch.cuda.stream(self.stream):
+            return bool(self.finished.all().item())
 
     def run_until_done(self, max_steps: int = 1 << 20, chunk: int = 64, use_graph: bool = True):
         """Decode until every rollout finished (EOS or max_len); host checks once per chunk."""

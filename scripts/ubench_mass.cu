@@ -55,6 +55,19 @@ __device__ __forceinline__ void pair(uint32_t w, float c, float nmc, float clamp
         m1 = __float_as_uint(p.y);
         return;
     }
+    if (MODE == 6) {
+        // FP64 floor: double(e') from the float bits (re-bias +896 folded into the shift of
+        // t's bits: t's low bits are n+S+896 when magic carries +896), then
+        // DADD.RZ(x, 2^52) leaves floor(x) in the low mantissa bits; the bits are summed
+        // raw and count * bits(2^52) is taken off once at the end.
+        const uint32_t hx = (__float_as_uint(p.x) >> 3) + (__float_as_uint(t.x) << 20);
+        const uint32_t hy = (__float_as_uint(p.y) >> 3) + (__float_as_uint(t.y) << 20);
+        const double dx = __hiloint2double((int)hx, (int)(__float_as_uint(p.x) << 29));
+        const double dy = __hiloint2double((int)hy, (int)(__float_as_uint(p.y) << 29));
+        m0 = (unsigned long long)__double_as_longlong(__dadd_rz(dx, 4503599627370496.0));
+        m1 = (unsigned long long)__double_as_longlong(__dadd_rz(dy, 4503599627370496.0));
+        return;
+    }
     if (MODE == 4 || MODE == 5) {
         // conversion-free floor: e' = A*2^23 + B, A = floor(e'/2^23), B = floor(e' - A*2^23)
         const float e0 = __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23));
@@ -141,6 +154,8 @@ __global__ void check(unsigned long long* bad) {
         local += (a0 != b0) + (a1 != b1);
         pair<5>(w, c, -mc, -46.f, 12582912.f + 44.f, b0, b1);
         local += (a0 != b0) + (a1 != b1);
+        pair<6>(w, c, -mc, -46.f, 12582912.f + 44.f + 896.f, b0, b1);
+        local += (a0 != b0 - 0x4330000000000000ull) + (a1 != b1 - 0x4330000000000000ull);
     }
     atomicAdd(&nb, local);
     __syncthreads();
@@ -160,8 +175,8 @@ int main() {
     cudaMemcpy(in, h, sizeof h, cudaMemcpyHostToDevice);
     const float c = 1.4426950f, nmc = -1.4426950f * 8.0f, clampv = -46.f, magic = 12582912.f + 44.f;
     const int iters = 2000;
-    const char* names[6] = {"F2I.U64", "integer shift", "50/50 mix", "poly only", "fp split rz", "fp split rz x2"};
-    for (int mode = 0; mode < 6; ++mode) {
+    const char* names[7] = {"F2I.U64", "integer shift", "50/50 mix", "poly only", "fp split rz", "fp split rz x2", "fp64 dadd.rz"};
+    for (int mode = 0; mode < 7; ++mode) {
         for (int rep = 0; rep < 2; ++rep) {
             cudaEvent_t a, b;
             cudaEventCreate(&a);
@@ -174,6 +189,7 @@ int main() {
             if (mode == 3) k<3><<<g, blk>>>(in, out, iters, c, nmc, clampv, magic);
             if (mode == 4) k<4><<<g, blk>>>(in, out, iters, c, nmc, clampv, magic);
             if (mode == 5) k<5><<<g, blk>>>(in, out, iters, c, nmc, clampv, magic);
+            if (mode == 6) k<6><<<g, blk>>>(in, out, iters, c, nmc, clampv, magic + 896.f);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms = 0;

@@ -64,10 +64,15 @@ def _compare_step(orc, rows, drafts, dlen, k, T, top_p, seed, uids, max_len, eos
             assert int(oz[b, j]) == 0 and float(on[b, j]) == 0.0
 
 
+KERNELS = ["rows", "split", "cluster"]  # bsx_set_verify_kernel: every verify kernel
+
+
+@pytest.mark.parametrize("path", KERNELS)
 @pytest.mark.parametrize("V,T,stride", [(1024, 1.0, None), (1000, 0.7, None), (4096, 1.3, None),
                                         (1001, 1.0, 1003), (1024, 0.0, None), (33, 1.0, None),
-                                        (151936, 1.0, None)])
-def test_verify_step_parity(bs, orc, V, T, stride):
+                                        (151936, 1.0, None), (151936, 0.0, None),
+                                        (200003, 0.9, None)])
+def test_verify_step_parity(bs, orc, V, T, stride, path):
     """Random logits rows (several tiles + ragged tail, odd strides), random drafts mixing
     the argmax (often accepted) with random tokens."""
     rng = np.random.default_rng(V + int(T * 10))
@@ -86,6 +91,7 @@ def test_verify_step_parity(bs, orc, V, T, stride):
     seed = 0xABCDEF
     ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=8, max_rollouts=n,
                      pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    ctx.bsx_set_verify_kernel(path)
     uids = np.arange(n, dtype=np.uint64) * np.uint64(7919) + np.uint64(3)
     _begin(bs, ctx, n, max_len, uids, 8)
     got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, T, 1.0, stride)
@@ -93,7 +99,50 @@ def test_verify_step_parity(bs, orc, V, T, stride):
     _compare_step(orc, rows, drafts, dlen, k, T, 1.0, seed, uids, max_len, -1, got)
 
 
-def test_verify_eos_and_edge_cases(bs, orc):
+def _topp_rows(rng, kind, n, k, V):
+    if kind == "quant":      # logits on a 0.5 grid: large tie groups straddle the threshold
+        vals = np.round(rng.normal(0, 2.0, size=(n, k + 1, V)) * 2) / 2
+    elif kind == "dense0":   # logits near 0, where distinct bf16 keys share one mass
+        vals = rng.uniform(-0.01, 0.01, size=(n, k + 1, V))
+    else:
+        vals = rng.normal(0, 2.0, size=(n, k + 1, V))
+    rows = f32_to_bf16_bits(vals.astype(np.float32))
+    for b in range(n):
+        for j in range(k + 1):
+            if rng.random() < 0.5:
+                rows[b, j, rng.integers(0, V, 3)] = f32_to_bf16_bits(np.float32(3.0))
+    return rows
+
+
+@pytest.mark.parametrize("V,T,top_p,kind,stride", [
+    (1024, 1.0, 0.9, "normal", None), (4099, 0.7, 0.5, "normal", None),
+    (1000, 1.3, 0.999, "quant", None), (4096, 1.0, 0.3, "quant", None),
+    (3000, 1.0, 0.6, "dense0", None), (1001, 1.0, 0.8, "quant", 1003),
+    (513, 1.0, 1e-6, "normal", None), (151936, 1.0, 0.95, "normal", None),
+    (151936, 0.8, 0.7, "dense0", None)])
+def test_verify_top_p_parity(bs, orc, V, T, top_p, kind, stride):
+    """Top-p (reading R5, tie-closed nucleus): the mass-weighted key select on the GPU keeps
+    exactly the oracle's set; accepted lengths, tokens and Z' bit-exact."""
+    rng = np.random.default_rng(V * 7 + int(top_p * 1000))
+    k = 4 if V < 100000 else 6
+    n = 40 if V < 100000 else 8
+    rows = _topp_rows(rng, kind, n, k, V)
+    argm = bf16_bits_to_f32(rows).argmax(axis=2)
+    drafts = np.where(rng.random((n, k)) < 0.7, argm[:, :k], rng.integers(0, V, (n, k)))
+    dlen = rng.integers(0, k + 1, n)
+    max_len = np.full(n, 1000)
+    seed = 0x5EED
+    ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=8, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    uids = np.arange(n, dtype=np.uint64) * np.uint64(104729) + np.uint64(5)
+    _begin(bs, ctx, n, max_len, uids, 8)
+    got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, T, top_p, stride)
+    assert ctx.bs_sync_status() == 0
+    _compare_step(orc, rows, drafts, dlen, k, T, top_p, seed, uids, max_len, -1, got)
+
+
+@pytest.mark.parametrize("path", KERNELS)
+def test_verify_eos_and_edge_cases(bs, orc, path):
     """Accepted EOS ends the block; q=0 is a plain sample; -inf logits; max_len clamp."""
     V, k, n, eos = 64, 4, 32, 5
     rng = np.random.default_rng(1)
@@ -111,6 +160,7 @@ def test_verify_eos_and_edge_cases(bs, orc):
     seed = 99
     ctx = bs.Context(vocab=V, eos_id=eos, k_max=k, match_max=8, max_rollouts=n,
                      pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    ctx.bsx_set_verify_kernel(path)
     uids = np.arange(n, dtype=np.uint64) + np.uint64(11)
     _begin(bs, ctx, n, max_len, uids, 8)
     got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, 1.0, 1.0)
@@ -118,12 +168,14 @@ def test_verify_eos_and_edge_cases(bs, orc):
     _compare_step(orc, rows, drafts, dlen, k, 1.0, 1.0, seed, uids, max_len, eos, got)
 
 
-def test_verify_device_errors(bs):
+@pytest.mark.parametrize("path", KERNELS)
+def test_verify_device_errors(bs, path):
     V, k, n = 64, 2, 4
     rows = np.zeros((n, k + 1, V), dtype=np.uint16)
     rows[1, 0, 3] = 0x7FC0  # NaN
     ctx = bs.Context(vocab=V, k_max=k, match_max=8, max_rollouts=n, pool_capacity_tokens=16,
                      pool_capacity_seqs=4)
+    ctx.bsx_set_verify_kernel(path)
     _begin(bs, ctx, n, [10] * n, np.arange(n, dtype=np.uint64), 8)
     _verify_gpu(bs, ctx, rows, np.zeros((n, k), np.int64), np.full(n, 2), k, 1.0, 1.0)
     assert ctx.bs_sync_status() & 0x1
