@@ -78,6 +78,13 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     c->S = mass_shift(cfg->vocab);
     c->M = cfg->match_max;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    {  // per-RL-step scratch is stream-ordered from the default pool: keep freed memory cached
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cfg->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     const size_t R = (size_t)cfg->max_rollouts;
     const size_t rows = R * (size_t)(cfg->k_max + 1);
     bool okk = c->tail.ensure(R * c->M) == cudaSuccess && c->ctx_len.ensure(R) == cudaSuccess &&

@@ -49,6 +49,25 @@ struct DevBuf {
     }
 };
 
+// Stream-ordered scratch: cudaMallocAsync / cudaFreeAsync from the device's default memory
+// pool (bs_create keeps freed pool memory cached), so per-RL-step builds never hit the
+// synchronising cudaMalloc / cudaFree.  Freed (stream-ordered) when it goes out of scope.
+template <typename T>
+struct AsyncBuf {
+    T* p = nullptr;
+    cudaStream_t st = nullptr;
+    cudaError_t alloc(size_t n, cudaStream_t s) {
+        st = s;
+        return cudaMallocAsync(reinterpret_cast<void**>(&p), (n ? n : 1) * sizeof(T), s);
+    }
+    AsyncBuf() = default;
+    AsyncBuf(const AsyncBuf&) = delete;
+    AsyncBuf& operator=(const AsyncBuf&) = delete;
+    ~AsyncBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
 struct Pool {
     DevBuf<int32_t> tokens;
     DevBuf<int64_t> seq_off;  // absolute offsets into tokens, n_seqs + 1

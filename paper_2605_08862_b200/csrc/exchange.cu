@@ -152,8 +152,8 @@ bs_status bs_draft_exchange(bs_ctx* c, void* comm_v, int32_t rank, int32_t world
         P.n_tokens = 0;
     }
     // 1. counts
-    DevBuf<int64_t> cnt;
-    if (cnt.ensure(2 * (size_t)(world + 1)) != cudaSuccess) return BS_ERR_OOM;
+    AsyncBuf<int64_t> cnt;  // stream-ordered scratch (no synchronising cudaMalloc / cudaFree)
+    if (cnt.alloc(2 * (size_t)(world + 1), st) != cudaSuccess) return BS_ERR_OOM;
     int64_t mine[2] = {P.n_seqs, P.n_tokens};
     cudaMemcpyAsync(cnt.p + 2 * world, mine, sizeof mine, cudaMemcpyHostToDevice, st);
     if (a.AllGather(cnt.p + 2 * world, cnt.p, 2, ncclInt64, comm, st) != ncclSuccess) {
@@ -170,11 +170,13 @@ bs_status bs_draft_exchange(bs_ctx* c, void* comm_v, int32_t rank, int32_t world
         tot_seqs += counts[2 * r];
     }
     // 2. padded payload all-gather (offsets, prompt ids, tokens) in one NCCL group
-    DevBuf<int64_t> soff, roff;
-    DevBuf<int32_t> sprm, rprm, stok, rtok;
-    if (soff.ensure(max_seqs + 1) || roff.ensure((size_t)world * (max_seqs + 1)) ||
-        sprm.ensure(std::max<int64_t>(max_seqs, 1)) || rprm.ensure((size_t)world * std::max<int64_t>(max_seqs, 1)) ||
-        stok.ensure(std::max<int64_t>(max_tok, 1)) || rtok.ensure((size_t)world * std::max<int64_t>(max_tok, 1)))
+    AsyncBuf<int64_t> soff, roff;
+    AsyncBuf<int32_t> sprm, rprm, stok, rtok;
+    if (soff.alloc(max_seqs + 1, st) || roff.alloc((size_t)world * (max_seqs + 1), st) ||
+        sprm.alloc(std::max<int64_t>(max_seqs, 1), st) ||
+        rprm.alloc((size_t)world * std::max<int64_t>(max_seqs, 1), st) ||
+        stok.alloc(std::max<int64_t>(max_tok, 1), st) ||
+        rtok.alloc((size_t)world * std::max<int64_t>(max_tok, 1), st))
         return BS_ERR_OOM;
     cudaMemsetAsync(soff.p, 0, sizeof(int64_t) * (max_seqs + 1), st);
     if (P.n_seqs) {
@@ -211,8 +213,8 @@ bs_status bs_draft_exchange(bs_ctx* c, void* comm_v, int32_t rank, int32_t world
         c->err = "exchange: routed pool exceeds capacity";
         return BS_ERR_CAPACITY;
     }
-    DevBuf<int64_t> dplan;
-    if (dplan.ensure(3 * (size_t)std::max(nkeep, 1))) return BS_ERR_OOM;
+    AsyncBuf<int64_t> dplan;
+    if (dplan.alloc(3 * (size_t)std::max(nkeep, 1), st)) return BS_ERR_OOM;
     cudaMemcpyAsync(dplan.p, src.data(), sizeof(int64_t) * nkeep, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dplan.p + nkeep, dst.data(), sizeof(int64_t) * nkeep, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dplan.p + 2 * nkeep, len.data(), sizeof(int64_t) * nkeep, cudaMemcpyHostToDevice, st);
@@ -226,8 +228,6 @@ bs_status bs_draft_exchange(bs_ctx* c, void* comm_v, int32_t rank, int32_t world
     if (nkeep)
         cudaMemcpyAsync(P.seq_prompt.p, pp.data(), sizeof(int32_t) * nkeep, cudaMemcpyHostToDevice, st);
     cudaError_t e = cudaStreamSynchronize(st);
-    cnt.release(); soff.release(); roff.release(); sprm.release(); rprm.release();
-    stok.release(); rtok.release(); dplan.release();
     if (e != cudaSuccess) return BS_ERR_CUDA;
     P.n_seqs = nkeep;
     P.n_tokens = ntok;

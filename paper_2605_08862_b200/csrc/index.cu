@@ -243,32 +243,43 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         return cudaStreamSynchronize(st);
     }
     const int* T = ctx->sealed.tokens.p;
-    // scratch
-    DevBuf<int32_t> act, act_next, flag, runid, runid_pos, fu, nflag;
-    DevBuf<unsigned long long> keys, keys_sorted;
-    DevBuf<int> d_count;
-    BS_TRY(act.ensure(n));
-    BS_TRY(act_next.ensure(n));
-    BS_TRY(flag.ensure(n));
-    BS_TRY(runid.ensure(n));
-    BS_TRY(runid_pos.ensure(n));
-    BS_TRY(fu.ensure(n));
-    BS_TRY(nflag.ensure(n));
-    BS_TRY(keys.ensure(n));
-    BS_TRY(keys_sorted.ensure(n));
-    BS_TRY(d_count.ensure(1));
+    // scratch (stream-ordered: no synchronising cudaMalloc / cudaFree per seal)
+    AsyncBuf<int32_t> act, act_next, flag, runid, runid_pos, fu, nflag;
+    AsyncBuf<unsigned long long> keys, keys_sorted;
+    AsyncBuf<int> d_count;
+    BS_TRY(act.alloc(n, st));
+    BS_TRY(act_next.alloc(n, st));
+    BS_TRY(flag.alloc(n, st));
+    BS_TRY(runid.alloc(n, st));
+    BS_TRY(runid_pos.alloc(n, st));
+    BS_TRY(fu.alloc(n, st));
+    BS_TRY(nflag.alloc(n, st));
+    BS_TRY(keys.alloc(n, st));
+    BS_TRY(keys_sorted.alloc(n, st));
+    BS_TRY(d_count.alloc(1, st));
     size_t tmp_bytes = 0, t1 = 0, t2 = 0, t3 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t1, keys.p, keys_sorted.p, act.p, act_next.p, n, 0, 64, st);
     cub::DeviceScan::InclusiveSum(nullptr, t2, flag.p, runid.p, n, st);
     cub::DeviceSelect::Flagged(nullptr, t3, act.p, nflag.p, act_next.p, d_count.p, n, st);
     tmp_bytes = std::max(t1, std::max(t2, t3));
-    DevBuf<uint8_t> tmp;
-    BS_TRY(tmp.ensure(tmp_bytes));
+    AsyncBuf<uint8_t> tmp;
+    BS_TRY(tmp.alloc(tmp_bytes, st));
     const int G = std::max(1, std::min(ctx->num_sms * 8, (n + 255) / 256));
     iota_kernel<<<G, 256, 0, st>>>(act.p, n);
     fill_kernel<<<G, 256, 0, st>>>(fu.p, n, 0x7FFFFFFF);
 
     std::vector<Level> levels;
+    struct LevelFree {  // per-level arrays: stream-ordered frees on every exit path
+        std::vector<Level>& lv;
+        cudaStream_t st;
+        ~LevelFree() {
+            for (auto& l : lv) {
+                if (l.pos_sorted) cudaFreeAsync(l.pos_sorted, st);
+                if (l.runstart) cudaFreeAsync(l.runstart, st);
+                if (l.parent) cudaFreeAsync(l.parent, st);
+            }
+        }
+    } level_free{levels, st};
     int A = n;
     uint64_t hi_max = 0;  // max of the high key part (prompt id or previous run count)
     {
@@ -276,9 +287,10 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         hi_max = 0xFFFFFFFFull;
     }
     for (int l = 1; l <= D && A > 0; ++l) {
-        Level lv;
+        levels.push_back(Level{});
+        Level& lv = levels.back();
         lv.A = A;
-        BS_TRY(cudaMalloc(&lv.pos_sorted, sizeof(int32_t) * (size_t)A));
+        BS_TRY(cudaMallocAsync(reinterpret_cast<void**>(&lv.pos_sorted), sizeof(int32_t) * (size_t)A, st));
         const int g = std::max(1, std::min(ctx->num_sms * 8, (A + 255) / 256));
         level_keys_kernel<<<g, 256, 0, st>>>(l, A, VB, act.p, T, ctx->prompt_of.p, runid_pos.p, keys.p);
         const int end_bit = std::min(64, VB + bits_for(hi_max));
@@ -292,8 +304,8 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         BS_TRY(cudaMemcpyAsync(&nr, runid.p + (A - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
         BS_TRY(cudaStreamSynchronize(st));
         lv.nruns = nr;
-        BS_TRY(cudaMalloc(&lv.runstart, sizeof(int32_t) * (size_t)(nr + 1)));
-        BS_TRY(cudaMalloc(&lv.parent, sizeof(int32_t) * (size_t)std::max(nr, 1)));
+        BS_TRY(cudaMallocAsync(reinterpret_cast<void**>(&lv.runstart), sizeof(int32_t) * (size_t)(nr + 1), st));
+        BS_TRY(cudaMallocAsync(reinterpret_cast<void**>(&lv.parent), sizeof(int32_t) * (size_t)std::max(nr, 1), st));
         run_starts_kernel<<<g, 256, 0, st>>>(l, A, VB, keys_sorted.p, flag.p, runid.p, lv.runstart, lv.parent);
         run_members_kernel<<<g, 256, 0, st>>>(l, A, lv.pos_sorted, runid.p, lv.runstart, ctx->seq_end_of.p,
                                               runid_pos.p, fu.p, nflag.p);
@@ -302,7 +314,6 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         int an = 0;
         BS_TRY(cudaMemcpyAsync(&an, d_count.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         BS_TRY(cudaStreamSynchronize(st));
-        levels.push_back(lv);
         A = an;
         hi_max = (uint64_t)nr;
     }
@@ -319,13 +330,13 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
     // descending pass
     int maxr = 1;
     for (auto& lv : levels) maxr = std::max(maxr, lv.nruns);
-    DevBuf<int32_t> pqa, poa, pqb, pob, cbeg, cend;
-    BS_TRY(pqa.ensure(maxr));
-    BS_TRY(poa.ensure(maxr));
-    BS_TRY(pqb.ensure(maxr));
-    BS_TRY(pob.ensure(maxr));
-    BS_TRY(cbeg.ensure(maxr));
-    BS_TRY(cend.ensure(maxr));
+    AsyncBuf<int32_t> pqa, poa, pqb, pob, cbeg, cend;
+    BS_TRY(pqa.alloc(maxr, st));
+    BS_TRY(poa.alloc(maxr, st));
+    BS_TRY(pqb.alloc(maxr, st));
+    BS_TRY(pob.alloc(maxr, st));
+    BS_TRY(cbeg.alloc(maxr, st));
+    BS_TRY(cend.alloc(maxr, st));
     int32_t *pq_child = pqb.p, *po_child = pob.p, *pq = pqa.p, *po = poa.p;
     const int L = (int)levels.size();
     for (int li = L - 1; li >= 0; --li) {
@@ -348,17 +359,7 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         std::swap(pq, pq_child);
         std::swap(po, po_child);
     }
-    cudaError_t e = cudaStreamSynchronize(st);
-    for (auto& lv : levels) {
-        cudaFree(lv.pos_sorted);
-        cudaFree(lv.runstart);
-        cudaFree(lv.parent);
-    }
-    act.release(); act_next.release(); flag.release(); runid.release(); runid_pos.release();
-    fu.release(); nflag.release(); keys.release(); keys_sorted.release(); d_count.release();
-    tmp.release(); pqa.release(); poa.release(); pqb.release(); pob.release(); cbeg.release();
-    cend.release();
-    return e;
+    return cudaStreamSynchronize(st);
 }
 
 // ------------------------------------------------------------------ lookup (K1)

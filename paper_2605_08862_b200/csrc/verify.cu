@@ -208,9 +208,9 @@ __device__ void complete_row(const VerifyArgs& a, unsigned long long* stat, int 
 
 // Claim the next needed row of the plan's j-major table (Alg. 1's order across the batch),
 // skipping rows at or above an already-decided row of their rollout.  b < 0: none left.
-__device__ RowDesc claim_row(const VerifyArgs& a, int rows) {
+__device__ RowDesc claim_row(const VerifyArgs& a, int rows, int base = 0) {
     for (;;) {
-        const int r = (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
+        const int r = base + (int)atomicAdd(a.ctl + VCTL_NEXT, 1u);
         if (r >= rows) break;
         const RowDesc it = a.items[r];
         if (it.j > ld_volatile_i32(a.roll_first + it.b)) continue;  // decided below

@@ -96,27 +96,44 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
 
     if (warp == CK_PROD) {
         // ================================================================ producer
-        if (lane == 0) {
-            for (int i = 0;; ++i) {
-                const int s = i % CK_D, bi = i % CK_NB;
-                // arm the descriptor slot for row i (its use by row i-4 completed: this lane
-                // waited on it)
-                mbar_arrive_expect_tx(&sh.dfull[s], (uint32_t)sizeof(RowDesc));
-                // the slice buffer is free once the compute warps are done with row i-2
-                if (i >= CK_NB) mbar_wait(&sh.empty[bi], ((i / CK_NB) - 1) & 1);
-                if (rank == 0) {
-                    // every CTA's epilogue is done with row i-4 (its descriptor slot)
-                    if (i >= CK_D) mbar_wait_cluster(&sh.dempty[s], ((i / CK_D) - 1) & 1);
-                    RowDesc nd = claim_row(a, rows);  // just in time: limits speculation
-                    const uint4* src = reinterpret_cast<const uint4*>(&nd);
-                    uint4* dst = reinterpret_cast<uint4*>(&sh.dq[s]);
-                    for (int r = 0; r < CK_CL; ++r)
-                        for (int w = 0; w < (int)(sizeof(RowDesc) / 16); ++w)
-                            st_async_v4(dst + w, src[w], &sh.dfull[s], (uint32_t)r);
-                }
-                mbar_wait(&sh.dfull[s], (i / CK_D) & 1);
-                const RowDesc dsc = sh.dq[s];
-                if (dsc.b < 0) break;
+        // The leader claims row i+1 right after issuing row i's copy (one row of lookahead:
+        // the claim's dependent loads stay off the compute warps' critical path) and
+        // broadcasts each descriptor with 24 lanes (8 CTAs x 3 x 16 bytes).
+        const int cid = (int)(blockIdx.x / CK_CL), ncl = (int)(gridDim.x / CK_CL);
+        auto broadcast = [&](int r) {
+            const int s = r % CK_D;
+            // every CTA's epilogue is done with row r-4 (the slot's previous use)
+            if (r >= CK_D) mbar_wait_cluster(&sh.dempty[s], ((r / CK_D) - 1) & 1);
+            RowDesc nd;
+            if (lane == 0) {
+                if (r == 0 && cid < rows) nd = a.items[cid];  // first claim: static
+                else nd = claim_row(a, rows, ncl);
+            }
+            uint32_t w[12];
+            memcpy(w, &nd, sizeof(w));
+#pragma unroll
+            for (int x = 0; x < 12; ++x) w[x] = __shfl_sync(0xFFFFFFFFu, w[x], 0);
+            if (lane < 3 * CK_CL) {
+                const int part = lane % 3;
+                uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
+                if (part == 1) v = make_uint4(w[4], w[5], w[6], w[7]);
+                if (part == 2) v = make_uint4(w[8], w[9], w[10], w[11]);
+                st_async_v4(reinterpret_cast<uint4*>(&sh.dq[s]) + part, v, &sh.dfull[s], (uint32_t)(lane / 3));
+            }
+        };
+        if (lane == 0) mbar_arrive_expect_tx(&sh.dfull[0], (uint32_t)sizeof(RowDesc));
+        if (rank == 0) broadcast(0);
+        for (int i = 0;; ++i) {
+            const int s = i % CK_D, bi = i % CK_NB;
+            // arm the descriptor slot for row i (its use by row i-4 completed: this warp
+            // waited on it); the leader's bytes may already have arrived
+            if (i > 0 && lane == 0) mbar_arrive_expect_tx(&sh.dfull[s], (uint32_t)sizeof(RowDesc));
+            mbar_wait(&sh.dfull[s], (i / CK_D) & 1);
+            const RowDesc dsc = sh.dq[s];
+            if (dsc.b < 0) break;
+            // the slice buffer is free once the mass warps are done with row i-2
+            if (i >= CK_NB) mbar_wait(&sh.empty[bi], ((i / CK_NB) - 1) & 1);
+            if (lane == 0) {
                 uint16_t* buf = bufs + (size_t)bi * SL;
                 const uint16_t* src = a.logits + dsc.rowno * a.stride + e_lo;
                 const int nb = dsc.aligned ? (len & ~7) : 0;  // 16-byte multiple
@@ -129,6 +146,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                     mbar_arrive(&sh.full[bi]);
                 }
             }
+            if (rank == 0) broadcast(i + 1);
         }
     } else if (warp == CK_EPI) {
         // ================================================================ epilogue
@@ -278,7 +296,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
         }
     } else if (warp >= CK_NMW) {
         // ================================================================ max warps
-        const int xw = warp - CK_NMW, xt0 = tid - CK_NMW * 32;  // 0..63
+        const int xw = warp - CK_NMW;
         for (int i = 0;; ++i) {
             const int s = i % CK_D, bi = i % CK_NB;
             mbar_wait(&sh.dfull[s], (i / CK_D) & 1);
@@ -336,12 +354,14 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                 for (int w = 0; w < CK_NXW; ++w) sidx = min(sidx, sh.widx[w]);
                 if (sidx != 0x7FFFFFFF) sidx += e_lo;
             }
-            if (xt0 == 0) {
-                // arm row i's max slot: its row i-4 phase completed (the mass warps waited on
-                // it before freeing the buffer this row now occupies)
-                mbar_arrive_expect_tx(&sh.maxbar[s], (uint32_t)(CK_CL * 16));
-                const uint4 v = make_uint4(__float_as_uint(sm), sb, (uint32_t)sidx, 0u);
-                for (int r = 0; r < CK_CL; ++r) st_async_v4(&sh.cmax[s][rank], v, &sh.maxbar[s], (uint32_t)r);
+            if (xw == 0) {
+                // arm row i's max slot (its row i-4 phase completed: the mass warps waited on
+                // it before freeing the buffer this row now occupies), then one lane per CTA
+                if (lane == 0) mbar_arrive_expect_tx(&sh.maxbar[s], (uint32_t)(CK_CL * 16));
+                __syncwarp();
+                if (lane < CK_CL)
+                    st_async_v4(&sh.cmax[s][rank], make_uint4(__float_as_uint(sm), sb, (uint32_t)sidx, 0u),
+                                &sh.maxbar[s], (uint32_t)lane);
             }
             named_bar(2, CK_NXW * 32);  // wmax / widx reusable
         }
@@ -392,7 +412,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             }
             if (lane == 0) sh.wsum[warp] = wacc;
             named_bar(1, CK_NMW * 32);
-            if (tid == 0) {
+            if (warp == 0) {
                 uint64_t cs = 0;
 #pragma unroll
                 for (int w = 0; w < CK_NMW; ++w) cs += sh.wsum[w];
@@ -400,14 +420,18 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                 const uint64_t mdl = (a.T > 0.f && ok && dsc.d >= 0 && dl >= 0 && dl < len)
                                          ? mass_of(__uint_as_float((uint32_t)buf[dl] << 16), mp)
                                          : 0ull;
-                sh.erec[s] = make_uint4(__float_as_uint(m), bad, (uint32_t)g, 0u);
-                // arm row i's sum slot (its row i-4 phase completed: the max warps' eempty
-                // wait precedes this row's max); the arrive also releases the tile sums and
-                // erec to this CTA's epilogue
-                mbar_arrive_expect_tx(&sh.sumbar[s], (uint32_t)(CK_CL * 16));
-                const uint4 v = make_uint4((uint32_t)cs, (uint32_t)(cs >> 32), (uint32_t)mdl,
-                                           (uint32_t)(mdl >> 32));
-                for (int r = 0; r < CK_CL; ++r) st_async_v4(&sh.csum[s][rank], v, &sh.sumbar[s], (uint32_t)r);
+                if (lane == 0) {
+                    sh.erec[s] = make_uint4(__float_as_uint(m), bad, (uint32_t)g, 0u);
+                    // arm row i's sum slot (its row i-4 phase completed: the max warps' eempty
+                    // wait precedes this row's max); the arrive also releases the tile sums
+                    // and erec to this CTA's epilogue
+                    mbar_arrive_expect_tx(&sh.sumbar[s], (uint32_t)(CK_CL * 16));
+                }
+                __syncwarp();
+                if (lane < CK_CL)
+                    st_async_v4(&sh.csum[s][rank],
+                                make_uint4((uint32_t)cs, (uint32_t)(cs >> 32), (uint32_t)mdl, (uint32_t)(mdl >> 32)),
+                                &sh.sumbar[s], (uint32_t)lane);
             }
             named_bar(1, CK_NMW * 32);  // wsum reusable
             if (lane == 0) mbar_arrive(&sh.empty[bi]);  // slice buffer free

@@ -18,6 +18,7 @@ from paper_2605_08862_b200.engine import RolloutEngine, Target  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--chunk", type=int, default=64)
 ap.add_argument("--config", default="q7")
+ap.add_argument("--no-events", action="store_true", help="time whole chunks only (no event nodes)")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 dev = torch.device("cuda", 0)
@@ -44,29 +45,44 @@ chunk = a.chunk
 # ev[i][0..4]: before lookup, target rows, verify, commit, after commit
 ev = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(5)] for _ in range(chunk)]
 OPS = ["lookup", "target_rows", "verify", "commit"]
+import time as _time  # noqa: E402
+
 for rl in (1, 2):
+    t0 = _time.perf_counter()
     with torch.cuda.stream(stream):
         ctx.bs_draft_pool_put(rl, d(h["seq_prompt"]), d(h["seq_off"]), d(h["tokens"]),
                               len(h["tokens"]), stream=stream)
+        stream.synchronize()
+        t1 = _time.perf_counter()
         eng.seal(rl)
+        stream.synchronize()
+        t2 = _time.perf_counter()
         eng.begin(d(h["uids"].view(np.int64)), d(h["pid"]), d(h["tails"]), d(h["max_len"]))
+    rec = not a.no_events
     with torch.cuda.stream(stream):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             for i in range(chunk):
-                ev[i][0].record(stream)
+                if rec:
+                    ev[i][0].record(stream)
                 ctx.bs_draft_lookup(eng.rl_step, eng.slots, k, eng.draft, eng.draft_len,
                                     eng.match_len, stream=stream)
-                ev[i][1].record(stream)
+                if rec:
+                    ev[i][1].record(stream)
                 ctx.bsx_target_rows(eng.slots, eng.draft, eng.draft_len, k, eng.target.target_seed,
                                     eng.target.mode, eng.target.nbank, eng.row_index, stream=stream)
-                ev[i][2].record(stream)
+                if rec:
+                    ev[i][2].record(stream)
                 ctx.bs_verify_step(eng.slots, bank, eng.row_index, V, eng.draft, eng.draft_len, k,
                                    eng.T, eng.top_p, eng.out_tokens, eng.out_len, eng.out_acc,
                                    stream=stream)
-                ev[i][3].record(stream)
+                if rec:
+                    ev[i][3].record(stream)
                 ctx.bs_commit(eng.slots, eng.out_tokens, eng.out_len, k, eng.finished, stream=stream)
-                ev[i][4].record(stream)
+                if rec:
+                    ev[i][4].record(stream)
+    stream.synchronize()
+    t3 = _time.perf_counter()
     rows = []
     cs, ce = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     while True:
@@ -76,11 +92,15 @@ for rl in (1, 2):
             ce.record(stream)
             live = int((~eng.finished.bool()).sum().item())
         tot = cs.elapsed_time(ce)
-        per = [sum(ev[i][o].elapsed_time(ev[i][o + 1]) for i in range(chunk)) for o in range(4)]
+        per = ([sum(ev[i][o].elapsed_time(ev[i][o + 1]) for i in range(chunk)) for o in range(4)]
+               if rec else [0.0] * 4)
         rows.append([live, tot] + per)
         if live == 0:
             break
+    t4 = _time.perf_counter()
     if rl == 2:
+        print(f"host wall: put {1e3 * (t1 - t0):.1f} ms, seal {1e3 * (t2 - t1):.1f} ms, "
+              f"begin+capture {1e3 * (t3 - t2):.1f} ms, decode loop {1e3 * (t4 - t3):.1f} ms")
         arr = np.array(rows)
         T = arr[:, 1].sum()
         print(f"chunks {len(rows)}, total {T:.1f} ms; " + ", ".join(

@@ -55,6 +55,15 @@ __device__ __forceinline__ void pair(uint32_t w, float c, float nmc, float clamp
         m1 = __float_as_uint(p.y);
         return;
     }
+    if (MODE == 7) {
+        // mixed pipes: lane x by F2I.U64, lane y by the FP64 DADD.RZ floor (t from magic+896:
+        // the x lane's exponent insert subtracts the extra 896 << 23)
+        m0 = f2u(__uint_as_float(__float_as_uint(p.x) + ((__float_as_uint(t.x) - 896u) << 23)));
+        const uint32_t hy = (__float_as_uint(p.y) >> 3) + (__float_as_uint(t.y) << 20);
+        const double dy = __hiloint2double((int)hy, (int)(__float_as_uint(p.y) << 29));
+        m1 = (unsigned long long)__double_as_longlong(__dadd_rz(dy, 4503599627370496.0)) - 0x4330000000000000ull;
+        return;
+    }
     if (MODE == 6) {
         // FP64 floor: double(e') from the float bits (re-bias +896 folded into the shift of
         // t's bits: t's low bits are n+S+896 when magic carries +896), then
@@ -139,7 +148,7 @@ __global__ void check(unsigned long long* bad) {
     __shared__ unsigned long long nb;
     if (threadIdx.x == 0) nb = 0;
     __syncthreads();
-    unsigned long long local = 0;
+    unsigned long long local = 0, local6 = 0, local7 = 0;
     for (int r = 0; r < 64; ++r) {
         const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) * 64 + r;
         // y spans [-46, 1]: logits l = bf16 from hash, c and m chosen per block
@@ -155,9 +164,13 @@ __global__ void check(unsigned long long* bad) {
         pair<5>(w, c, -mc, -46.f, 12582912.f + 44.f, b0, b1);
         local += (a0 != b0) + (a1 != b1);
         pair<6>(w, c, -mc, -46.f, 12582912.f + 44.f + 896.f, b0, b1);
-        local += (a0 != b0 - 0x4330000000000000ull) + (a1 != b1 - 0x4330000000000000ull);
+        local6 += (a0 != b0 - 0x4330000000000000ull) + (a1 != b1 - 0x4330000000000000ull);
+        pair<7>(w, c, -mc, -46.f, 12582912.f + 44.f + 896.f, b0, b1);
+        local7 += (a0 != b0) + (a1 != b1);
     }
     atomicAdd(&nb, local);
+    atomicAdd(&bad[1], local6);
+    atomicAdd(&bad[2], local7);
     __syncthreads();
     if (threadIdx.x == 0) atomicAdd(bad, nb);
 }
@@ -175,8 +188,8 @@ int main() {
     cudaMemcpy(in, h, sizeof h, cudaMemcpyHostToDevice);
     const float c = 1.4426950f, nmc = -1.4426950f * 8.0f, clampv = -46.f, magic = 12582912.f + 44.f;
     const int iters = 2000;
-    const char* names[7] = {"F2I.U64", "integer shift", "50/50 mix", "poly only", "fp split rz", "fp split rz x2", "fp64 dadd.rz"};
-    for (int mode = 0; mode < 7; ++mode) {
+    const char* names[8] = {"F2I.U64", "integer shift", "50/50 mix", "poly only", "fp split rz", "fp split rz x2", "fp64 dadd.rz", "F2I + DADD mix"};
+    for (int mode = 0; mode < 8; ++mode) {
         for (int rep = 0; rep < 2; ++rep) {
             cudaEvent_t a, b;
             cudaEventCreate(&a);
@@ -190,6 +203,7 @@ int main() {
             if (mode == 4) k<4><<<g, blk>>>(in, out, iters, c, nmc, clampv, magic);
             if (mode == 5) k<5><<<g, blk>>>(in, out, iters, c, nmc, clampv, magic);
             if (mode == 6) k<6><<<g, blk>>>(in, out, iters, c, nmc, clampv, magic + 896.f);
+            if (mode == 7) k<7><<<g, blk>>>(in, out, iters, c, nmc, clampv, magic + 896.f);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms = 0;
@@ -200,10 +214,11 @@ int main() {
         }
     }
     // bit-equality of the conversion-free floor against F2I.U64 over a dense y sweep
-    cudaMemset(out, 0, 8);
+    cudaMemset(out, 0, 24);
     check<<<4096, 256>>>(out);
-    unsigned long long bad = 0;
-    cudaMemcpy(&bad, out, 8, cudaMemcpyDeviceToHost);
-    printf("fp-split vs F2I.U64 mismatches: %llu of %d\n", bad, 4096 * 256 * 64);
+    unsigned long long bad[3] = {0, 0, 0};
+    cudaMemcpy(bad, out, 24, cudaMemcpyDeviceToHost);
+    printf("mismatches vs F2I.U64 (of %d): fp split %llu, fp64 dadd %llu, F2I+DADD mix %llu\n",
+           4096 * 256 * 64 * 2, bad[0], bad[1], bad[2]);
     return 0;
 }
