@@ -75,6 +75,9 @@ def load():
         if hasattr(lib, "bsx_phase_times"):  # diagnostics (not part of the C-ABI header)
             lib.bsx_phase_times.restype = C.c_int
             lib.bsx_phase_times.argtypes = [C.c_void_p, C.c_int]
+        if hasattr(lib, "bsx_trace_read"):
+            lib.bsx_trace_read.restype = C.c_int
+            lib.bsx_trace_read.argtypes = [C.c_void_p, C.c_int, C.c_int]
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -48,7 +48,9 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
 
 
 if __name__ == "__main__":
-    if "--timing" in sys.argv:
+    if "--trace" in sys.argv:
+        print(build(force=True, variant="trace", defines=["BS_TRACE"]))
+    elif "--timing" in sys.argv:
         print(build(force=True, variant="timing", defines=["BS_PHASE_TIMING"]))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -96,6 +96,8 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
                c->vrow_status.ensure(rows) == cudaSuccess && c->vrow_cand.ensure(rows) == cudaSuccess &&
                c->vrow_z.ensure(rows) == cudaSuccess && c->vrow_norm.ensure(rows) == cudaSuccess &&
                c->vroll_first.ensure(R) == cudaSuccess && c->vroll_state.ensure(R) == cudaSuccess &&
+               c->vnext_row.ensure(R) == cudaSuccess && c->vrrec.ensure(R) == cudaSuccess &&
+               c->vlive.ensure(R) == cudaSuccess &&
                c->staging.tokens.ensure((size_t)cfg->pool_capacity_tokens) == cudaSuccess &&
                c->staging.seq_off.ensure((size_t)cfg->pool_capacity_seqs + 1) == cudaSuccess &&
                c->staging.seq_prompt.ensure((size_t)cfg->pool_capacity_seqs) == cudaSuccess &&
@@ -118,6 +120,11 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     cudaMemset(c->finished.p, 0, R * sizeof(int32_t));
     cudaMemset(c->dev_err.p, 0, sizeof(uint32_t));
     cudaMemset(c->vctl.p, 0, VCTL_WORDS * sizeof(unsigned int));
+    cudaMemset(c->vnext_row.p, 0, R * sizeof(unsigned long long));
+    {  // scheduler epoch starts at 1: zeroed claim counters (epoch 0) read as unplanned
+        const unsigned int one = 1u;
+        cudaMemcpy(c->vctl.p + SC_EPOCH, &one, sizeof one, cudaMemcpyHostToDevice);
+    }
     cudaMemset(c->stats.p, 0, STAT_COUNT * sizeof(unsigned long long));
     cudaMemset(c->table.p, 0, 2 * sizeof(IndexEntry));
     cudaMemset(c->staging.seq_off.p, 0, sizeof(int64_t));
@@ -143,6 +150,7 @@ void bs_destroy(bs_ctx* c) {
     c->table.release(); c->rb_q.release(); c->vqueue.release(); c->vctl.release();
     c->vrow_status.release(); c->vrow_cand.release(); c->vrow_z.release(); c->vrow_norm.release();
     c->vroll_first.release(); c->vroll_state.release();
+    c->vnext_row.release(); c->vrrec.release(); c->vlive.release();
     c->stats.release();
     delete c;
 }

@@ -26,7 +26,25 @@ enum : int {
 };
 
 // Control words of the verify kernel: next rollout to claim, number of live rollouts.
-enum : int { VCTL_NEXT = 0, VCTL_NACTIVE = 1, VCTL_MODE = 2, VCTL_ROWS = 3, VCTL_WORDS = 4 };
+enum : int { VCTL_NEXT = 0, VCTL_NACTIVE = 1, VCTL_MODE = 2, VCTL_ROWS = 3 };
+// Scheduler words of the cluster verify kernel (verify_cluster.cuh): static cursor,
+// rollouts done, CTAs exited, launch epoch.  All but the epoch are zero between launches
+// (the last CTA out resets them).
+enum : int {
+    SC_STATIC = 8, SC_NLIVE = 9, SC_PLANNED = 10, SC_DONE = 13, SC_EXIT = 14, SC_EPOCH = 15,
+    VCTL_WORDS = 16
+};
+
+// Per-rollout plan of one verify launch (cluster kernel), written by the planning warps at
+// kernel start and published by its epoch tag (written last).
+struct RollRec {
+    int32_t q, slot, pos, tag;   // clamped draft length (-1: no rows), slot, position, epoch
+    unsigned long long uid;
+    long long rowno0;            // logits row of row 0
+    int32_t d0, aligned0;        // d_1 (or -1), row 0 16-byte aligned
+    int32_t pad[2];
+};
+static_assert(sizeof(RollRec) == 48, "RollRec layout");
 
 template <typename T>
 struct DevBuf {
@@ -109,6 +127,11 @@ struct bs_ctx {
     // rows deciding << 32)
     bs::DevBuf<int32_t> vroll_first;
     bs::DevBuf<unsigned long long> vroll_state;
+    // cluster-kernel scheduler: per-rollout claim counter (epoch << 32 | next unclaimed
+    // row) and per-rollout plan records
+    bs::DevBuf<unsigned long long> vnext_row;
+    bs::DevBuf<bs::RollRec> vrrec;
+    bs::DevBuf<int32_t> vlive;  // the launch's live rollouts (compacted by the planners)
     bs::DevBuf<unsigned long long> stats;  // STAT_COUNT counters
     int32_t* responses = nullptr;           // optional [max_rollouts, resp_stride] output
     int64_t resp_stride = 0;

@@ -1,6 +1,7 @@
 // ptx.cuh — thin inline-PTX wrappers for sm_100a: mbarrier, 1-D bulk copy (TMA), cache hints.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace bs {
 
@@ -31,31 +32,38 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// try_wait with a suspend-time hint: a waiting warp sleeps (NANOSLEEP.SYNCS) until the phase
+// completes or the hint expires instead of spinning, so waiting warps do not take issue
+// slots from the working ones.
+constexpr uint32_t MBAR_SUSPEND_NS = 1000000u;
+
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
     uint32_t ok;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, p;\n"
         "}\n"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
+        : "r"(smem_u32(bar)), "r"(phase), "r"(MBAR_SUSPEND_NS)
         : "memory");
     return ok != 0;
 }
 
+// Cluster-scope wait: relaxed polls, one acquire fence once the phase has completed.
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t phase) {
     uint32_t ok;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, p;\n"
         "}\n"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
+        : "r"(smem_u32(bar)), "r"(phase), "r"(MBAR_SUSPEND_NS)
         : "memory");
+    if (ok) asm volatile("fence.acquire.cluster;" ::: "memory");
     return ok != 0;
 }
 
@@ -71,7 +79,11 @@ __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t phase, bool 
     const uint64_t t0 = globaltimer_ns();
     for (uint32_t it = 1;; ++it) {
         if (cluster ? mbar_try_wait_cluster(bar, phase) : mbar_try_wait(bar, phase)) return;
-        if ((it & 255u) == 0 && globaltimer_ns() - t0 > 4000000000ull) __trap();
+        if ((it & 15u) == 0 && globaltimer_ns() - t0 > 3000000000ull) {
+            printf("bs watchdog: block %d thread %d mbarrier smem+0x%x phase %u\n", (int)blockIdx.x,
+                   (int)threadIdx.x, smem_u32(bar), phase);
+            __trap();
+        }
     }
 }
 
@@ -127,6 +139,34 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+
+// GPU-scope acquire / release / relaxed global accesses (the verify scheduler's queues).
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 
 __device__ __forceinline__ uint4 lds128(const void* p) {

@@ -22,6 +22,7 @@
 // the set of completed rows, and the row that completes the prefix finalizes (CAS).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -67,6 +68,35 @@ __device__ unsigned long long g_phase[16];
 
 struct RowDesc;
 
+// Optional event trace (build with -DBS_TRACE; read with bsx_trace_read): globaltimer stamps
+// of each row's stages per CTA, for latency analysis (scripts/trace_verify.py).
+#ifdef BS_TRACE
+// per-CTA slices of 2048 events; the index comes from a shared-memory counter (no global
+// round trip), the store is fire-and-forget, so recording barely perturbs the timing
+constexpr int TRACE_PER_CTA = 2048;
+__device__ uint4 g_trace[1 << 20];
+__device__ unsigned int g_trace_n;
+__shared__ unsigned int s_trace_n;
+__device__ __forceinline__ void trace_ev(int type, int seq, int b, int j) {
+    const unsigned i = atomicAdd(&s_trace_n, 1u);
+    const unsigned slot = blockIdx.x * TRACE_PER_CTA + i;
+    if (i < TRACE_PER_CTA && slot < (1u << 20)) {
+        const uint64_t t = globaltimer_ns();
+        g_trace[slot] = make_uint4((uint32_t)blockIdx.x | ((uint32_t)type << 16) | ((uint32_t)(j & 0xFF) << 24),
+                                   (uint32_t)(seq & 0xFFFF) | ((uint32_t)(b & 0xFFFF) << 16), (uint32_t)t,
+                                   (uint32_t)(t >> 32));
+    }
+}
+#define TRACE(type, seq, b, j) trace_ev(type, seq, b, j)
+#else
+#define TRACE(type, seq, b, j) \
+    do {                       \
+    } while (0)
+#endif
+enum { TR_CLAIM0 = 0, TR_CLAIM1 = 1, TR_TMA = 2, TR_MAX0 = 3, TR_MAX1 = 4, TR_MASS0 = 5, TR_MASS1 = 6,
+       TR_EPI0 = 7, TR_EPI1 = 8, TR_END = 9, TR_FIN = 10, TR_SPINS = 11, TR_SC = 12, TR_SQPOP = 13, TR_ITER = 14 };
+
+
 struct VerifyArgs {
     const int32_t* slots;
     const uint16_t* logits;
@@ -94,6 +124,17 @@ struct VerifyArgs {
     float* out_norm;
     unsigned long long* out_z;
     unsigned long long* stats;
+    // cluster-kernel scheduler (verify_cluster.cuh); sctl == nullptr for the other kernels
+    int n;                        // rollouts of this call
+    const int32_t* draft_len;
+    const int32_t* max_len;
+    const int32_t* finished;
+    unsigned int* sctl;           // vctl words SC_*
+    unsigned long long* next_row; // per rollout: epoch << 32 | next unclaimed row
+    RollRec* rrec;                // per rollout: the launch's plan
+    int32_t* live;                // the launch's live rollouts (compacted by the planners)
+    int ncl;                      // clusters in the grid
+    int eager_ok;                 // small live batches claim every row at once
 };
 
 struct RowDesc {
@@ -169,6 +210,10 @@ __device__ void finalize_rollout(const VerifyArgs& a, unsigned long long* s, int
         s[STAT_EMIT_PLAIN] += (unsigned long long)n;
     }
     s[STAT_ROWS_NEEDED] += (unsigned long long)(F + 1);
+    if (a.sctl) {
+        const unsigned dn = atomicAdd(a.sctl + SC_DONE, 1u);  // scheduler termination count
+        TRACE(TR_FIN, (int)dn, b, F);
+    }
 }
 
 // Rollout state word: bit j = row j completed, bit 32+j = row j decides (reject / bonus /
@@ -731,8 +776,11 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     const int V = ctx->cfg.vocab;
     const bool topp = T > 0.f && top_p < 1.f;
     const int kind = topp ? VK_ROWS : verify_kind(ctx, V);
-    const int plan_mode = (kind == VK_SPLIT) ? 1 : (kind == VK_CLUSTER ? 3 : 0);
-    cudaError_t e = launch_pdl(
+    const int plan_mode = (kind == VK_SPLIT) ? 1 : 0;
+    cudaError_t e = cudaSuccess;
+    // the cluster kernel plans in-kernel (each rollout's row-0 claimer); the others take the
+    // plan kernel's j-major row table
+    if (kind != VK_CLUSTER) e = launch_pdl(
         verify_plan_kernel, dim3(1), dim3(PLAN_NT), 0, st, n, k, V, slots, draft, draft_len,
         (const int32_t*)ctx->pos.p, (const int32_t*)ctx->max_len.p,
         (const int32_t*)ctx->finished.p, (const unsigned long long*)ctx->uid.p,
@@ -776,6 +824,17 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.out_norm = out_norm;
     a.out_z = out_z;
     a.stats = ctx->stats.p;
+    if (kind == VK_CLUSTER && !topp) {
+        a.n = n;
+        a.draft_len = draft_len;
+        a.max_len = ctx->max_len.p;
+        a.finished = ctx->finished.p;
+        a.sctl = ctx->vctl.p;
+        a.next_row = ctx->vnext_row.p;
+        a.rrec = ctx->vrrec.p;
+        a.live = ctx->vlive.p;
+        a.eager_ok = getenv("BS_NO_EAGER") ? 0 : 1;
+    }
     if (topp) {  // R5: top-p filtered rows (verify_topp.cuh)
         if (ntile_ok(V) == 0) return cudaErrorInvalidValue;
         const size_t tsm = sizeof(TopPShared);
@@ -808,6 +867,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             ck_clusters = std::max(1, ncl);
             ck_configured = csm;
         }
+        a.ncl = ck_clusters;
         return launch_pdl(verify_cluster_kernel, dim3(ck_clusters * CK_CL), dim3(CK_NT), csm, st, a, SL);
     }
     if (kind == VK_SPLIT) {
@@ -836,6 +896,30 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
 }
 
 }  // namespace bs
+
+// Event trace of the cluster kernel (BS_TRACE builds): copies up to max_ev uint4 events to
+// host memory out, returns the number recorded (and resets the trace when reset != 0).
+extern "C" int bsx_trace_read(void* out, int max_ev, int reset) {
+#ifdef BS_TRACE
+    // compacts the nonzero events (per-CTA slices) into out
+    static uint4* host = nullptr;
+    if (!host) host = (uint4*)malloc(sizeof(uint4) << 20);
+    cudaMemcpyFromSymbol(host, bs::g_trace, sizeof(uint4) << 20);
+    int m = 0;
+    for (int i = 0; i < (1 << 20) && m < max_ev; ++i)
+        if (host[i].z | host[i].w) static_cast<uint4*>(out)[m++] = host[i];
+    if (reset) {
+        memset(host, 0, sizeof(uint4) << 20);
+        cudaMemcpyToSymbol(bs::g_trace, host, sizeof(uint4) << 20);
+    }
+    return m;
+#else
+    (void)out;
+    (void)max_ev;
+    (void)reset;
+    return -1;
+#endif
+}
 
 extern "C" int bsx_phase_times(unsigned long long* out16, int reset) {
 #ifdef BS_PHASE_TIMING

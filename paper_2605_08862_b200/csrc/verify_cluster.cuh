@@ -22,12 +22,12 @@
 // (included inside namespace bs)
 
 constexpr int CK_CL = 8;                  // CTAs per cluster
-constexpr int CK_NMW = 6;                 // mass warps: 0..5
-constexpr int CK_NXW = 2;                 // max warps: 6..7
+constexpr int CK_NMW = 8;                 // mass warps: 0..7 (two per SM sub-partition)
+constexpr int CK_NXW = 2;                 // max warps: 8..9
 constexpr int CK_NCW = CK_NMW + CK_NXW;
 constexpr int CK_PROD = CK_NCW;           // producer warp
 constexpr int CK_EPI = CK_NCW + 1;        // epilogue warp
-constexpr int CK_NT = (CK_NCW + 2) * 32;  // 320 threads
+constexpr int CK_NT = (CK_NCW + 2) * 32;  // 384 threads
 constexpr int CK_NB = 2;                  // slice buffers
 constexpr int CK_D = 4;                   // descriptor / exchange ring depth
 constexpr int CK_TILE = 512;              // elements per tile (16 per lane)
@@ -41,6 +41,7 @@ struct CkShared {
     uint4 cmax[CK_D][CK_CL];  // per CTA: {slice max bits, bad, greedy index, 0}
     uint4 csum[CK_D][CK_CL];  // per CTA: {slice mass sum lo, hi, mass(d) lo, hi}
     uint4 erec[CK_D];         // mass warps -> epilogue: {m bits, bad, greedy index, 0}
+    int mail;  // leader: (rollout << 8 | row) the epilogue found needed next, or -1
     float wmax[CK_NXW];
     uint32_t wbad[CK_NXW];
     int32_t widx[CK_NXW];
@@ -53,6 +54,326 @@ __host__ __device__ constexpr size_t ck_smem_bytes(int SL) {
     return ((sizeof(CkShared) + 127) & ~size_t(127)) + (size_t)CK_NB * SL * 2;
 }
 
+// ---------------------------------------------------------------- row scheduler
+// PLAN.  At kernel start the mass warps of every CTA plan the call's rollouts in parallel
+// (one warp per rollout): clamp q (reading L6), validate the draft, reset the rollout's
+// completion state, write its record, then publish its claim counter next_row[b] =
+// (epoch << 32 | 0) (release; a counter with another epoch reads as "not planned yet").
+//
+// CLAIM.  Every row claim is atomicAdd(next_row[b]) -> r, kept iff r <= roll_first[b] (the
+// lowest deciding row seen, initially q: P:555, rows after the first rejection are not
+// needed).  The leader CTA's producer warp picks b:
+//   * look-ahead (its buffer still busy): the next rollout of the static cursor (row 0);
+//   * buffer free: a warp scan of every rollout's state, best first:
+//       READY  row nr-1 completed and accepted: row nr is needed (deepest first),
+//       STATIC row 0 not claimed yet,
+//       SPEC   row nr-1 still in flight: an idle cluster shortens the chain (shallowest
+//              first), so small batches verify all rows of a rollout at once and full
+//              batches speculate only while draining;
+//     ties rotate by cluster id so concurrent claimers spread over rollouts.
+// No queues: the scan only reads, so idle clusters do not contend.  Returns b = -1 once
+// every rollout of the call is finalized.
+constexpr int SRC_NONE = 0, SRC_READY = 1, SRC_STATIC = 2, SRC_SPEC = 3;
+
+__device__ void ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
+    const int kp1 = a.k + 1;
+    const int sl = a.slots[b];
+    const int p = a.pos[sl], L = a.max_len[sl];
+    int q = -1;
+    if (!a.finished[sl] && p < L) q = min(max(a.draft_len[b], 0), min(a.k, L - p - 1));
+    const int t = (lane < q) ? a.draft[(int64_t)b * a.k + lane] : 0;
+    if (q > 0 && __any_sync(0xFFFFFFFFu, lane < q && (t < 0 || t >= a.V))) {
+        q = -1;
+        if (lane == 0) atomicOr(a.dev_err, DEV_BAD_DRAFT);
+    }
+    if (lane < kp1) {
+        if (a.out_norm) a.out_norm[(int64_t)b * kp1 + lane] = 0.f;
+        if (a.out_z) a.out_z[(int64_t)b * kp1 + lane] = 0ull;
+        if (q < 0) a.out_tokens[(int64_t)b * kp1 + lane] = -1;
+    }
+    const int d0 = __shfl_sync(0xFFFFFFFFu, t, 0);
+    if (lane == 0) {
+        RollRec rr;
+        rr.q = q;
+        rr.slot = sl;
+        rr.pos = p;
+        rr.tag = (int32_t)epoch;
+        rr.uid = a.uid[sl];
+        rr.rowno0 = a.row_index ? a.row_index[(int64_t)b * kp1] : (int64_t)b * kp1;
+        rr.d0 = q > 0 ? d0 : -1;
+        rr.aligned0 = ((reinterpret_cast<uintptr_t>(a.logits + rr.rowno0 * a.stride) & 15u) == 0) ? 1 : 0;
+        rr.pad[0] = rr.pad[1] = 0;
+        a.rrec[b] = rr;
+        a.roll_first[b] = q;  // the bonus row q always decides; -1: no rows
+        a.roll_state[b] = 0ull;
+        if (q < 0) {  // finished / out of length / bad draft: no rows, nothing emitted
+            a.out_len[b] = 0;
+            a.out_acc[b] = 0;
+            atomicAdd(a.sctl + SC_DONE, 1u);
+        }
+        __threadfence();
+        // publish the plan: claim word = epoch << 32 | (q + 1) << 24 | next row (0)
+        st_release_u64(a.next_row + b, ((unsigned long long)epoch << 32) | ((unsigned long long)(q + 1) << 24));
+        if (q >= 0) a.live[atomicAdd(a.sctl + SC_NLIVE, 1u)] = b;
+        __threadfence();
+        atomicAdd(a.sctl + SC_PLANNED, 1u);
+    }
+}
+
+// Row r of rollout b as a descriptor (lane-uniform inputs; every lane computes it).
+__device__ __forceinline__ RowDesc ck_desc(int b, int j, int q, int d, int pos, unsigned long long uid,
+                                           long long rowno, int aligned, int src) {
+    RowDesc r;
+    r.b = b;
+    r.j = j;
+    r.q = q;
+    r.d = d;
+    r.rowno = rowno;
+    r.uid = uid;
+    r.position = pos + j;
+    r.aligned = aligned;
+    r.pad[0] = src;  // claim source (diagnostics)
+    r.pad[1] = 0;
+    return r;
+}
+
+// Claim the next row of rollout b (lane 0 computes, the warp receives the descriptor).
+// Returns false when the claim is not needed (decided below / beyond q / unplanned).
+__device__ __forceinline__ bool ck_take(const VerifyArgs& a, uint32_t epoch, int b, int src, int lane,
+                                        int rpred, RowDesc& out) {
+    // lane 0 claims; lanes 1-3 fetch, meanwhile, the record, roll_first and the predicted
+    // row's draft token / logits row (prediction: the counter value the scan saw)
+    const int kp1 = a.k + 1;
+    const RollRec* rp = a.rrec + b;
+    unsigned long long old = 0;
+    int rf = -1, q = 0, p = 0, d0 = -1, al0 = 0, dpred = -1;
+    unsigned long long u = 0;
+    long long rn0 = 0, rnpred = 0;
+    if (lane == 0) old = atomicAdd(a.next_row + b, 1ull);
+    if (lane == 1) {  // L2 reads (published by another SM this launch)
+        rf = ld_volatile_i32(a.roll_first + b);
+        q = __ldcg(&rp->q);
+        p = __ldcg(&rp->pos);
+        u = __ldcg(&rp->uid);
+        d0 = __ldcg(&rp->d0);
+        rn0 = __ldcg(&rp->rowno0);
+        al0 = __ldcg(&rp->aligned0);
+    }
+    if (lane == 2 && rpred >= 1 && rpred <= a.k) dpred = a.draft[(int64_t)b * a.k + min(rpred, a.k - 1)];
+    if (lane == 3 && rpred >= 1 && rpred <= a.k)
+        rnpred = a.row_index ? a.row_index[(int64_t)b * kp1 + rpred] : (int64_t)b * kp1 + rpred;
+    old = shfl_u64(old, 0);
+    rf = __shfl_sync(0xFFFFFFFFu, rf, 1);
+    const int r = (int)(uint32_t)(old & 0xFFFFFFu);
+    const bool valid = (uint32_t)(old >> 32) == epoch && r <= rf;
+    if (!valid) return false;
+    q = __shfl_sync(0xFFFFFFFFu, q, 1);
+    p = __shfl_sync(0xFFFFFFFFu, p, 1);
+    u = shfl_u64(u, 1);
+    int d = -1, al = 0;
+    long long rn = 0;
+    if (r == 0) {
+        d = __shfl_sync(0xFFFFFFFFu, d0, 1);
+        rn = (long long)shfl_u64((unsigned long long)rn0, 1);
+        al = __shfl_sync(0xFFFFFFFFu, al0, 1);
+    } else {
+        if (r == rpred) {
+            d = __shfl_sync(0xFFFFFFFFu, dpred, 2);
+            rn = (long long)shfl_u64((unsigned long long)rnpred, 3);
+        } else {
+            if (lane == 0) {
+                d = (r < q) ? a.draft[(int64_t)b * a.k + r] : -1;
+                rn = a.row_index ? a.row_index[(int64_t)b * kp1 + r] : (int64_t)b * kp1 + r;
+            }
+            d = __shfl_sync(0xFFFFFFFFu, d, 0);
+            rn = (long long)shfl_u64((unsigned long long)rn, 0);
+        }
+        if (r >= q) d = -1;
+        al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
+    }
+    out = ck_desc(b, r, q, d, p, u, rn, al, src);
+    return true;
+}
+
+// Eager mode: row j of rollout b from the static cursor (each row enumerated exactly once).
+__device__ __forceinline__ bool ck_take_row(const VerifyArgs& a, int b, int j, int lane, RowDesc& out) {
+    const RollRec* rp = a.rrec + b;
+    int valid = 0, q = 0, p = 0, d = -1, al = 0;
+    unsigned long long u = 0;
+    long long rn = 0;
+    if (lane == 0) {
+        q = __ldcg(&rp->q);
+        valid = (j <= q && j <= ld_volatile_i32(a.roll_first + b)) ? 1 : 0;
+        if (valid) {
+            p = __ldcg(&rp->pos);
+            u = __ldcg(&rp->uid);
+            if (j == 0) {
+                d = __ldcg(&rp->d0);
+                rn = __ldcg(&rp->rowno0);
+                al = __ldcg(&rp->aligned0);
+            } else {
+                const int kp1 = a.k + 1;
+                d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;
+                rn = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+                al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
+            }
+        }
+    }
+    valid = __shfl_sync(0xFFFFFFFFu, valid, 0);
+    if (!valid) return false;
+    q = __shfl_sync(0xFFFFFFFFu, q, 0);
+    d = __shfl_sync(0xFFFFFFFFu, d, 0);
+    p = __shfl_sync(0xFFFFFFFFu, p, 0);
+    al = __shfl_sync(0xFFFFFFFFu, al, 0);
+    u = shfl_u64(u, 0);
+    rn = (long long)shfl_u64((unsigned long long)rn, 0);
+    out = ck_desc(b, j, q, d, p, u, rn, al, j == 0 ? SRC_STATIC : SRC_SPEC);
+    return true;
+}
+
+// Warp scan of every rollout's claim state; returns the best rollout, its class and the
+// counter value seen.  Two independent loads per rollout (claim word, state word): one
+// round trip per CK_SCAN*32 rollouts.  roll_first is derived: min(q, lowest deciding row).
+constexpr int CK_SCAN = 8;
+__device__ int ck_scan(const VerifyArgs& a, uint32_t epoch, int lane, int rot, int& src, int& rpred) {
+    const int n = a.n;
+    unsigned best = 0;
+    for (int base = 0; base < n; base += 32 * CK_SCAN) {
+        unsigned long long w[CK_SCAN], st[CK_SCAN];
+#pragma unroll
+        for (int i = 0; i < CK_SCAN; ++i) {
+            const int b = base + i * 32 + lane;
+            w[i] = (b < n) ? ld_relaxed_u64(a.next_row + b) : 0ull;
+            st[i] = (b < n) ? ld_relaxed_u64(a.roll_state + b) : 0ull;
+        }
+#pragma unroll
+        for (int i = 0; i < CK_SCAN; ++i) {
+            const int b = base + i * 32 + lane;
+            if (b >= n || (uint32_t)(w[i] >> 32) != epoch) continue;  // not planned yet
+            const int q = (int)((w[i] >> 24) & 0xFFu) - 1;
+            const int nr = (int)(w[i] & 0xFFFFFFu);
+            const uint32_t dec = (uint32_t)(st[i] >> 32);
+            const int rf = dec ? min(q, __ffs(dec) - 1) : q;
+            if (nr > rf) continue;  // every needed row claimed (or no rows)
+            unsigned prio, sub;
+            if (nr == 0) {
+                prio = 2;
+                sub = 0;
+            } else if (((st[i] >> (nr - 1)) & 1ull) && !((dec >> (nr - 1)) & 1u)) {
+                prio = 3;
+                sub = (unsigned)nr;  // deepest ready row first
+            } else {
+                prio = 1;
+                sub = 63u - (unsigned)nr;  // shallowest speculation first
+            }
+            const unsigned rk = (unsigned)(n - 1 - (b - rot + n) % n);  // rotation: b == rot first
+            best = max(best, (prio << 30) | (sub << 24) | rk);
+        }
+    }
+    best = __reduce_max_sync(0xFFFFFFFFu, best);
+    if (!best) return -1;
+    const unsigned pr = best >> 30, sb = (best >> 24) & 63u;
+    src = (pr == 3) ? SRC_READY : (pr == 2 ? SRC_STATIC : SRC_SPEC);
+    rpred = (pr == 3) ? (int)sb : (pr == 2 ? 0 : 63 - (int)sb);
+    const int rk = (int)(best & 0xFFFFFFu);
+    return (rot + (n - 1 - rk)) % n;
+}
+
+// queues: the caller's buffer is free (any row may be claimed); otherwise look ahead into
+// the static cursor only.  Returns b = -2 when the look-ahead finds nothing.
+// Producer-side claim state kept across claims (saves round trips once the facts are known).
+struct ClaimState {
+    int nlive = -1;          // live rollouts (after the plan completed)
+    bool eager = false;
+    bool static_done = false;  // the static cursor is exhausted
+};
+
+__device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool queues, int rot,
+                            ClaimState& cs, volatile int* mail) {
+    const int n = a.n;
+    uint64_t t_spin0 = 0;
+    RowDesc out;
+    if (cs.nlive < 0) {
+        // the static list is the live rollouts, compacted by the planners: wait for the plan
+        int nl = 0;
+        if (lane == 0) {
+            while ((int)ld_acquire_u32(a.sctl + SC_PLANNED) < n) __nanosleep(64);
+            nl = (int)ld_relaxed_u32(a.sctl + SC_NLIVE);
+        }
+        cs.nlive = __shfl_sync(0xFFFFFFFFu, nl, 0);
+        // eager when every live row fits in flight at once (two per cluster): the static
+        // list then enumerates every row, j-major, and a cluster leaves once it is exhausted
+        cs.eager = a.eager_ok && (long long)cs.nlive * (a.k + 1) <= 2ll * a.ncl;
+    }
+    const int nlive = cs.nlive;
+    const bool eager = cs.eager;
+    const int nstatic = eager ? nlive * (a.k + 1) : nlive;
+    for (int spin = 0;; ++spin) {
+        // 1. this cluster's own epilogue accepted row j of rollout b: row j+1 is needed and
+        //    the chain stays here (no scan)
+        if (!eager) {
+            int mb = -1;
+            if (lane == 0) {
+                mb = *mail;
+                if (mb >= 0) *mail = -1;
+            }
+            mb = __shfl_sync(0xFFFFFFFFu, mb, 0);
+            if (mb >= 0) {
+                if (ck_take(a, epoch, mb >> 8, SRC_READY, lane, mb & 0xFF, out)) return out;
+                continue;
+            }
+        }
+        int b = -1, j = 0;
+        if (!cs.static_done) {
+            if (lane == 0 && (int)ld_relaxed_u32(a.sctl + SC_STATIC) < nstatic) {
+                const int s = (int)atomicAdd(a.sctl + SC_STATIC, 1u);
+                if (s < nstatic) {
+                    b = __ldcg(a.live + s % nlive);
+                    j = s / nlive;
+                }
+            }
+            b = __shfl_sync(0xFFFFFFFFu, b, 0);
+            if (b < 0) cs.static_done = true;
+        }
+        if (b >= 0) {
+            j = __shfl_sync(0xFFFFFFFFu, j, 0);
+            if (eager ? ck_take_row(a, b, j, lane, out) : ck_take(a, epoch, b, SRC_STATIC, lane, 0, out)) return out;
+            continue;
+        }
+        if (eager) break;  // every row claimed: nothing left for this cluster
+        if (queues) {
+            int src = SRC_NONE, rpred = 0;
+            b = ck_scan(a, epoch, lane, rot, src, rpred);
+            if (lane == 0) TRACE(TR_ITER, spin, b, src);
+            if (b >= 0) {
+                if (ck_take(a, epoch, b, src, lane, rpred, out)) return out;
+                continue;
+            }
+        }
+        // nothing claimable now: done, or wait for rows to complete.  The decision is
+        // lane 0's (a per-lane read of a changing word could split the warp)
+        int done = 0;
+        if (lane == 0) done = ((int)ld_relaxed_u32(a.sctl + SC_DONE) >= n) ? 1 : 0;
+        if (__shfl_sync(0xFFFFFFFFu, done, 0)) {
+            if (lane == 0) TRACE(TR_SPINS, spin, 0, 0);
+            break;
+        }
+        if (!queues) {  // static cursor exhausted: the caller retries once its buffer is free
+            out.b = -2;
+            return out;
+        }
+        __nanosleep(64);
+        if (spin == 0) t_spin0 = globaltimer_ns();
+        if ((spin & 1023) == 1023 && lane == 0 && globaltimer_ns() - t_spin0 > 1500000000ull) {
+            printf("bs sched stall: block %d static %u done %u n %d\n", (int)blockIdx.x, a.sctl[SC_STATIC],
+                   a.sctl[SC_DONE], n);
+            __trap();
+        }
+    }
+    out.b = -1;
+    return out;
+}
+
 // Masses of 16 consecutive logits (two 16-byte vectors), elements >= nvalid or == excl
 // zeroed (indices relative to the first element).
 __device__ __forceinline__ void ck_mass16(const uint4 v0, const uint4 v1, const MassParams& mp,
@@ -63,8 +384,6 @@ __device__ __forceinline__ void ck_mass16(const uint4 v0, const uint4 v1, const 
 
 __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
     verify_cluster_kernel(const VerifyArgs a, int SL) {
-    pdl_wait();
-    pdl_trigger();
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(128) uint8_t ck_smem[];
@@ -72,7 +391,6 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
     uint16_t* bufs = reinterpret_cast<uint16_t*>(ck_smem + ((sizeof(CkShared) + 127) & ~size_t(127)));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rank = (int)cluster.block_rank();
-    const int rows = (int)a.ctl[VCTL_ROWS];
     const int V = a.V;
     const int e_lo = rank * SL;
     const int len = max(0, min(SL, V - e_lo));
@@ -92,27 +410,39 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
         fence_mbar_init();
     }
     for (int i = tid; i < STAT_COUNT; i += CK_NT) sh.stat[i] = 0ull;
+    if (tid == 0) sh.mail = -1;
+#ifdef BS_TRACE
+    if (tid == 0) s_trace_n = 0;
+#endif
     cluster.sync();  // every CTA's barriers exist before any remote operation
+    pdl_wait();      // (the prologue above overlaps the previous kernel's tail)
+    pdl_trigger();
+    const uint32_t epoch = ld_relaxed_u32(a.sctl + SC_EPOCH);
+    if (warp < CK_NMW)  // plan the call's rollouts, one warp each, before any row work
+        for (int b = (int)blockIdx.x * CK_NMW + warp; b < a.n; b += (int)gridDim.x * CK_NMW)
+            ck_plan(a, epoch, b, lane);
 
     if (warp == CK_PROD) {
         // ================================================================ producer
         // The leader claims row i+1 right after issuing row i's copy (one row of lookahead:
         // the claim's dependent loads stay off the compute warps' critical path) and
         // broadcasts each descriptor with 24 lanes (8 CTAs x 3 x 16 bytes).
-        const int cid = (int)(blockIdx.x / CK_CL), ncl = (int)(gridDim.x / CK_CL);
+        const int ncl = (int)(gridDim.x / CK_CL);
+        const int rot = (int)(((long long)(blockIdx.x / CK_CL) * a.n) / max(1, ncl));
+        ClaimState cst;
         auto broadcast = [&](int r) {
             const int s = r % CK_D;
             // every CTA's epilogue is done with row r-4 (the slot's previous use)
             if (r >= CK_D) mbar_wait_cluster(&sh.dempty[s], ((r / CK_D) - 1) & 1);
-            RowDesc nd;
-            if (lane == 0) {
-                if (r == 0 && cid < rows) nd = a.items[cid];  // first claim: static
-                else nd = claim_row(a, rows, ncl);
-            }
+            // look ahead into the static list only; ready / speculative rows are claimed
+            // when this cluster can start them (its buffer for row r is free)
+            if (lane == 0) TRACE(TR_CLAIM0, r, 0, 0);
+            // claimed right after the previous row's copy is issued: the claim's round trips
+            // overlap the rows in flight (the row waits for its buffer afterwards)
+            RowDesc nd = ck_claim(a, epoch, lane, true, rot, cst, &sh.mail);
+            if (lane == 0) TRACE(TR_CLAIM1, r | (nd.b >= 0 ? nd.pad[0] << 12 : 0), nd.b, nd.j);
             uint32_t w[12];
             memcpy(w, &nd, sizeof(w));
-#pragma unroll
-            for (int x = 0; x < 12; ++x) w[x] = __shfl_sync(0xFFFFFFFFu, w[x], 0);
             if (lane < 3 * CK_CL) {
                 const int part = lane % 3;
                 uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
@@ -138,6 +468,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                 const uint16_t* src = a.logits + dsc.rowno * a.stride + e_lo;
                 const int nb = dsc.aligned ? (len & ~7) : 0;  // 16-byte multiple
                 for (int e = nb; e < len; ++e) buf[e] = src[e];  // ragged end / unaligned row
+                TRACE(TR_TMA, i, dsc.b, dsc.j);
                 if (nb) {
                     fence_proxy_async_smem();
                     mbar_arrive_expect_tx(&sh.full[bi], (uint32_t)nb * 2u);
@@ -161,6 +492,19 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             if (dsc.b < 0) break;
             mbar_wait(&sh.sumbar[s], (i / CK_D) & 1);
             const int b = dsc.b, j = dsc.j, q = dsc.q, d = dsc.d;
+            if (lane == 0) TRACE(TR_EPI0, i, b, j);
+            // a row above an already-decided row is not needed: no completion.  Dead
+            // is monotone, so every CTA that skipped work on this row sees it dead here too.
+            const bool dead = __shfl_sync(0xFFFFFFFFu, lane == 0 ? (ld_volatile_i32(a.roll_first + b) < j ? 1 : 0) : 0, 0);
+            if (dead) {
+                __syncwarp();
+                if (lane == 0) {
+                    TRACE(TR_EPI1, i, dsc.b, dsc.j);
+                    mbar_arrive(&sh.eempty[s]);
+                    mbar_arrive_remote(&sh.dempty[s], 0u);
+                }
+                continue;
+            }
             const uint4 er = sh.erec[s];  // the cluster max of row i (local record)
             const float m = __uint_as_float(er.x);
             const uint32_t bad = er.y;
@@ -189,6 +533,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                     const int status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
                     sh.stat[STAT_ROWS_VERIFIED] += 1ull;
                     complete_row(a, sh.stat, b, j, q, status, g, 1ull, 1.f);
+                    if (status == ST_CONT) *reinterpret_cast<volatile int*>(&sh.mail) = (b << 8) | (j + 1);
                 }
             } else {
                 const float norm = (float)ldexp((double)Z, -a.S);
@@ -199,6 +544,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                     if (lead) {
                         sh.stat[STAT_ROWS_VERIFIED] += 1ull;
                         complete_row(a, sh.stat, b, j, q, status, -1, Z, norm);
+                        if (status == ST_CONT) *reinterpret_cast<volatile int*>(&sh.mail) = (b << 8) | (j + 1);
                     }
                 } else {
                     // residual (d excluded) or bonus sample (R8): inverse CDF in ascending id
@@ -290,6 +636,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             }
             __syncwarp();
             if (lane == 0) {
+                TRACE(TR_EPI1, i, dsc.b, dsc.j);
                 mbar_arrive(&sh.eempty[s]);             // tile sums / sum slot of row i free
                 mbar_arrive_remote(&sh.dempty[s], 0u);  // descriptor slot of row i free
             }
@@ -301,23 +648,46 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             const int s = i % CK_D, bi = i % CK_NB;
             mbar_wait(&sh.dfull[s], (i / CK_D) & 1);
             if (sh.dq[s].b < 0) break;
+            // dead row (a lower row of its rollout decided): skip the work; the load is
+            // issued now and used after the data wait
+            const int rfx = ld_volatile_i32(a.roll_first + sh.dq[s].b);
+            const int jx = sh.dq[s].j;
             // this CTA's epilogue is done with row i-4 (sum slot, tile sums): every peer's
             // row-i publish lands on completed phases of this CTA's rings
             if (i >= CK_D) mbar_wait(&sh.eempty[s], ((i / CK_D) - 1) & 1);
             mbar_wait(&sh.full[bi], (i / CK_NB) & 1);
+            const bool xdead = __shfl_sync(0xFFFFFFFFu, rfx < jx ? 1 : 0, 0) != 0;
+            if (xw == 0 && lane == 0) TRACE(TR_MAX0, i, 0, 0);
             const uint16_t* buf = bufs + (size_t)bi * SL;
-            uint32_t mx = 0xFF80FF80u;
-            for (int t = xw; t < ntile; t += CK_NXW) {
+            uint32_t mx = 0xFF80FF80u, mx1 = 0xFF80FF80u;
+            const int nfull = xdead ? 0 : len / CK_TILE;  // whole tiles
+            int t = xdead ? ntile : xw;
+            for (; t + 3 * CK_NXW < nfull; t += 4 * CK_NXW) {  // 4 tiles per step: 8 loads in flight
+                uint4 v[8];
+#pragma unroll
+                for (int u2 = 0; u2 < 4; ++u2) {
+                    v[2 * u2] = lds128(buf + (t + u2 * CK_NXW) * CK_TILE + lane * 16);
+                    v[2 * u2 + 1] = lds128(buf + (t + u2 * CK_NXW) * CK_TILE + lane * 16 + 8);
+                }
+#pragma unroll
+                for (int u2 = 0; u2 < 8; u2 += 2) {
+                    mx = hmax2_nan_u32(mx, hmax2_nan_u32(hmax2_nan_u32(v[u2].x, v[u2].y), hmax2_nan_u32(v[u2].z, v[u2].w)));
+                    mx1 = hmax2_nan_u32(mx1, hmax2_nan_u32(hmax2_nan_u32(v[u2 + 1].x, v[u2 + 1].y),
+                                                           hmax2_nan_u32(v[u2 + 1].z, v[u2 + 1].w)));
+                }
+            }
+            for (; t < ntile; t += CK_NXW) {
                 const int e0 = t * CK_TILE + lane * 16;
-                if (t * CK_TILE + CK_TILE <= len) {
+                if (t < nfull) {
                     const uint4 v0 = lds128(buf + e0), v1 = lds128(buf + e0 + 8);
                     mx = hmax2_nan_u32(mx, hmax2_nan_u32(hmax2_nan_u32(v0.x, v0.y), hmax2_nan_u32(v0.z, v0.w)));
-                    mx = hmax2_nan_u32(mx, hmax2_nan_u32(hmax2_nan_u32(v1.x, v1.y), hmax2_nan_u32(v1.z, v1.w)));
+                    mx1 = hmax2_nan_u32(mx1, hmax2_nan_u32(hmax2_nan_u32(v1.x, v1.y), hmax2_nan_u32(v1.z, v1.w)));
                 } else {
                     for (int x = 0; x < 16; ++x)
                         if (e0 + x < len) mx = hmax2_nan_u32(mx, (uint32_t)buf[e0 + x] | 0xFF800000u);
                 }
             }
+            mx = hmax2_nan_u32(mx, mx1);
             const float lo = bf16lo(mx), hi = bf16hi(mx);
             uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
             float fm = fmaxf(lo, hi);
@@ -362,6 +732,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                 if (lane < CK_CL)
                     st_async_v4(&sh.cmax[s][rank], make_uint4(__float_as_uint(sm), sb, (uint32_t)sidx, 0u),
                                 &sh.maxbar[s], (uint32_t)lane);
+                if (lane == 0) TRACE(TR_MAX1, i, 0, 0);
             }
             named_bar(2, CK_NXW * 32);  // wmax / widx reusable
         }
@@ -377,6 +748,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             const RowDesc dsc = sh.dq[s];
             if (dsc.b < 0) break;
             mbar_wait(&sh.maxbar[s], (i / CK_D) & 1);  // the 8 slice maxima of row i
+            if (warp == 0 && lane == 0) TRACE(TR_MASS0, i, 0, 0);
             float m = -INFINITY;
             uint32_t bad = 0;
             int g = 0x7FFFFFFF;
@@ -395,19 +767,31 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             uint64_t wacc = 0;
             if (a.T > 0.f && ok) {
                 mp.nmc = -__fmul_rn(m, a.c);
+                const bool split = a.S <= 44;  // FMA-pipe conversion for half the elements
                 for (int t = warp; t < ntile; t += CK_NMW) {
                     const int e0 = t * CK_TILE + lane * 16;
                     uint64_t acc;
                     if (t * CK_TILE + CK_TILE <= len) {
-                        acc = mass8(lds128(buf + e0), mp) + mass8(lds128(buf + e0 + 8), mp);
+                        const uint4 v0 = lds128(buf + e0), v1 = lds128(buf + e0 + 8);
+#if defined(BS_EXP_F2I)
+                        acc = mass8(v0, mp) + mass8(v1, mp);
+#elif defined(BS_EXP_SPLIT)
+                        acc = mass16_split(v0, v1, mp);
+#else
+                        acc = split ? mass16_mixed(v0, v1, mp) : mass8(v0, mp) + mass8(v1, mp);
+#endif
                     } else {
                         acc = 0;
                         for (int x = 0; x < 16; ++x)
                             if (e0 + x < len) acc += mass_of(__uint_as_float((uint32_t)buf[e0 + x] << 16), mp);
                     }
+#ifdef BS_EXP_NOREDUX
+                    wacc += acc;
+#else
                     const uint64_t ts = warp_sum_u51(acc);
                     if (lane == 0) sh.tsum[s][t] = ts;
                     wacc += ts;
+#endif
                 }
             }
             if (lane == 0) sh.wsum[warp] = wacc;
@@ -434,11 +818,26 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                                 &sh.sumbar[s], (uint32_t)lane);
             }
             named_bar(1, CK_NMW * 32);  // wsum reusable
+            if (warp == 0 && lane == 0) TRACE(TR_MASS1, i, 0, 0);
             if (lane == 0) mbar_arrive(&sh.empty[bi]);  // slice buffer free
         }
     }
     cluster.sync();  // no CTA exits while a peer may still address its shared memory
-    if (a.stats && tid == 0)
-        for (int i = 0; i < STAT_COUNT; ++i)
-            if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
+    if (tid == 0) TRACE(TR_END, 0, 0, 0);
+    if (tid == 0) {
+        if (a.stats)
+            for (int i = 0; i < STAT_COUNT; ++i)
+                if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
+        // the last CTA out resets the scheduler words for the next launch
+        __threadfence();
+        if (atomicAdd(a.sctl + SC_EXIT, 1u) == gridDim.x - 1) {
+            a.sctl[SC_STATIC] = 0u;
+            a.sctl[SC_NLIVE] = 0u;
+            a.sctl[SC_PLANNED] = 0u;
+            a.sctl[SC_DONE] = 0u;
+            a.sctl[SC_EXIT] = 0u;
+            a.sctl[SC_EPOCH] = (epoch + 1u) ? epoch + 1u : 1u;  // never 0 (zeroed entries)
+            __threadfence();
+        }
+    }
 }

@@ -28,6 +28,23 @@ __device__ __forceinline__ F2 fadd2(F2 a, F2 b) {
     return r;
 }
 
+__device__ __forceinline__ F2 fadd2_rz(F2 a, F2 b) {
+    F2 r;
+    asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+        " add.rz.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+__device__ __forceinline__ F2 ffma2_rz(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+        " mov.b64 rc, {%6, %7};\n fma.rz.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+
 // Masses of the two bf16 logits packed in w (R2-R4), bit-identical to mass_of() per lane:
 // the packed FFMA2 / FADD2 perform the same IEEE single operations.
 __device__ __forceinline__ void mass_pair(uint32_t w, const MassParams& mp, uint64_t& m0,
@@ -55,6 +72,64 @@ __device__ __forceinline__ uint64_t mass8(const uint4 v, const MassParams& mp) {
     mass_pair(v.z, mp, c0, c1);
     mass_pair(v.w, mp, d0, d1);
     return ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
+}
+
+// The same two masses with the conversion on the FMA pipe instead of F2I.U64 (the XU pipe),
+// valid for S <= 44: with the polynomial coefficients scaled by 2^-23 (exact), the exponent
+// insert yields x = e' * 2^-23 < 2^23 bit for bit, and
+//   floor(e') = floor(x) * 2^23 + floor(frac(x) * 2^23)
+// where t1 = RZ(x + 2^23) = 2^23 + floor(x), frac(x) = x - (t1 - 2^23) (exact) and
+// t2 = RZ(frac(x) * 2^23 + 2^23) = 2^23 + floor(frac(x) * 2^23).  The raw bits of t1 / t2 are
+// summed in u32 (hi / lo); the 2^23 offsets are taken off once per block.
+__device__ __forceinline__ void mass_pair_split(uint32_t w, const MassParams& mp, uint32_t& hi, uint32_t& lo) {
+    const F2 l{bf16lo(w), bf16hi(w)};
+    F2 y = ffma2(l, F2{mp.c, mp.c}, F2{mp.nmc, mp.nmc});
+    y.x = fmaxf(y.x, mp.clampv);
+    y.y = fmaxf(y.y, mp.clampv);
+    const F2 t = fadd2(y, F2{mp.magic, mp.magic});
+    const F2 n = fadd2(t, F2{-mp.magic, -mp.magic});
+    const F2 f = fadd2(y, F2{-n.x, -n.y});
+    constexpr float K5 = BS_C5 * 0x1p-23f, K4 = BS_C4 * 0x1p-23f, K3 = BS_C3 * 0x1p-23f;
+    constexpr float K2 = BS_C2 * 0x1p-23f, K1 = BS_C1 * 0x1p-23f, K0 = BS_C0 * 0x1p-23f;
+    F2 p = ffma2(F2{K5, K5}, f, F2{K4, K4});
+    p = ffma2(p, f, F2{K3, K3});
+    p = ffma2(p, f, F2{K2, K2});
+    p = ffma2(p, f, F2{K1, K1});
+    p = ffma2(p, f, F2{K0, K0});
+    const F2 x{__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+               __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23))};
+    const F2 t1 = fadd2_rz(x, F2{0x1p23f, 0x1p23f});
+    const F2 fl = fadd2(t1, F2{-0x1p23f, -0x1p23f});
+    const F2 r = fadd2(x, F2{-fl.x, -fl.y});
+    const F2 t2 = ffma2_rz(r, F2{0x1p23f, 0x1p23f}, F2{0x1p23f, 0x1p23f});
+    hi += __float_as_uint(t1.x) + __float_as_uint(t1.y);
+    lo += __float_as_uint(t2.x) + __float_as_uint(t2.y);
+}
+
+// Sum of 16 masses: v0's eight by F2I.U64, v1's eight by the FMA-pipe split floor (S <= 44):
+// the two conversions run on different pipes.
+__device__ __forceinline__ uint64_t mass16_mixed(const uint4 v0, const uint4 v1, const MassParams& mp) {
+    uint32_t hi = 0, lo = 0;
+    mass_pair_split(v1.x, mp, hi, lo);
+    mass_pair_split(v1.y, mp, hi, lo);
+    mass_pair_split(v1.z, mp, hi, lo);
+    mass_pair_split(v1.w, mp, hi, lo);
+    const uint32_t off8 = 8u * 0x4B000000u;  // eight 2^23 offsets, mod 2^32
+    return mass8(v0, mp) + ((uint64_t)(hi - off8) << 23) + (uint64_t)(lo - off8);
+}
+
+__device__ __forceinline__ uint64_t mass16_split(const uint4 v0, const uint4 v1, const MassParams& mp) {
+    uint32_t hi = 0, lo = 0;
+    mass_pair_split(v0.x, mp, hi, lo);
+    mass_pair_split(v0.y, mp, hi, lo);
+    mass_pair_split(v0.z, mp, hi, lo);
+    mass_pair_split(v0.w, mp, hi, lo);
+    mass_pair_split(v1.x, mp, hi, lo);
+    mass_pair_split(v1.y, mp, hi, lo);
+    mass_pair_split(v1.z, mp, hi, lo);
+    mass_pair_split(v1.w, mp, hi, lo);
+    const uint32_t off16 = 16u * 0x4B000000u;
+    return ((uint64_t)(hi - off16) << 23) + (uint64_t)(lo - off16);
 }
 
 // One lane's 8 masses of a tile, elements >= nvalid or == excl (tile-relative) zeroed.
