@@ -177,7 +177,16 @@ def run_ours(args, cfg, rank, world, dist):
     ev_s = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(chunk)]
     ev_e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(chunk)]
 
+    graphs = {}
+
     def capture(instrument=False):
+        """The decode graph (captured once: the library reads the sealed index through a
+        device-resident descriptor, so the graph stays valid across RL steps)."""
+        if instrument not in graphs:
+            graphs[instrument] = capture_new(instrument)
+        return graphs[instrument]
+
+    def capture_new(instrument=False):
         """One graph of `chunk` decode iterations.  Event-record nodes cost several us each
         inside a graph, so the timed graph has none; the instrumented twin (events around
         every bs_verify_step) is replayed separately on the same deterministic work."""
@@ -201,15 +210,27 @@ def run_ours(args, cfg, rank, world, dist):
                                 stream=stream)
         return g
 
+    phases = os.environ.get("BS_BENCH_PHASES")  # diagnostics: host wall per RL-step phase
+
     def rl_step(s, rec, instrument=False):
         d = dins[s]
+        tp = [time.perf_counter()]
+
+        def mark():
+            if phases:
+                stream.synchronize()
+                tp.append(time.perf_counter())
         with torch.cuda.stream(stream):
             ctx.bs_draft_pool_put(s + 1, d["sp"], d["off"], d["tok"], d["ntok"], stream=stream)
+            mark()
             if comm is not None:
                 ctx.bs_draft_exchange(comm, rank, world, s + 1, stream=stream)
             eng.seal(s + 1)  # synchronises the stream (index build is per RL step)
+            mark()
             eng.begin(d["uids"], d["pid"], d["tails"], d["ml"])
-        g = capture(instrument)  # sealed pool / index pointers change per RL step
+            mark()
+        g = capture(instrument)
+        mark()
         rec["launches"] += 2 + rec["seal_launches"]
         steps, chunks = 0, 0
         while True:
@@ -228,6 +249,10 @@ def run_ours(args, cfg, rank, world, dist):
                 break
         rec["decode_steps"] += steps
         rec["launches"] += steps * RolloutEngine.LAUNCHES_PER_STEP
+        mark()
+        if phases:
+            dt = [1e3 * (b - a) for a, b in zip(tp, tp[1:])]
+            log("[phases ms] put %.1f seal %.1f begin %.1f capture %.1f decode %.1f" % tuple(dt[:5]))
         return steps
 
     # seal launch count: our own kernels + CUB device calls per level

@@ -104,7 +104,8 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
                c->sealed.tokens.ensure((size_t)cfg->pool_capacity_tokens) == cudaSuccess &&
                c->sealed.seq_off.ensure((size_t)cfg->pool_capacity_seqs + 1) == cudaSuccess &&
                c->sealed.seq_prompt.ensure((size_t)cfg->pool_capacity_seqs) == cudaSuccess &&
-               c->table.ensure(2) == cudaSuccess && c->stats.ensure(STAT_COUNT) == cudaSuccess;
+               c->table.ensure(2) == cudaSuccess && c->stats.ensure(STAT_COUNT) == cudaSuccess &&
+               c->idx_desc.ensure(1) == cudaSuccess;
     if (!okk) {
         bs_destroy(c);
         cudaGetLastError();
@@ -130,6 +131,10 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     cudaMemset(c->staging.seq_off.p, 0, sizeof(int64_t));
     cudaMemset(c->sealed.seq_off.p, 0, sizeof(int64_t));
     c->table_mask = 1;
+    {
+        bs::IndexDesc d = {c->table.p, 1, c->sealed.tokens.p, c->seq_start_of.p};
+        cudaMemcpy(c->idx_desc.p, &d, sizeof d, cudaMemcpyHostToDevice);
+    }
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         bs_destroy(c);
@@ -147,7 +152,7 @@ void bs_destroy(bs_ctx* c) {
     c->staging.tokens.release(); c->staging.seq_off.release(); c->staging.seq_prompt.release();
     c->sealed.tokens.release(); c->sealed.seq_off.release(); c->sealed.seq_prompt.release();
     c->seq_start_of.release(); c->seq_end_of.release(); c->prompt_of.release();
-    c->table.release(); c->rb_q.release(); c->vqueue.release(); c->vctl.release();
+    c->table.release(); c->idx_desc.release(); c->rb_q.release(); c->vqueue.release(); c->vctl.release();
     c->vrow_status.release(); c->vrow_cand.release(); c->vrow_z.release(); c->vrow_norm.release();
     c->vroll_first.release(); c->vroll_state.release();
     c->vnext_row.release(); c->vrrec.release(); c->vlive.release();

@@ -86,6 +86,15 @@ struct AsyncBuf {
     }
 };
 
+struct IndexEntry;
+// The sealed index as the lookup kernel sees it (device-resident; bs_draft_pool_seal updates it).
+struct IndexDesc {
+    IndexEntry* table;
+    uint64_t mask;
+    const int32_t* T;
+    const int32_t* seq_start_of;
+};
+
 struct Pool {
     DevBuf<int32_t> tokens;
     DevBuf<int64_t> seq_off;  // absolute offsets into tokens, n_seqs + 1
@@ -115,6 +124,7 @@ struct bs_ctx {
     bs::DevBuf<int32_t> seq_start_of, seq_end_of, prompt_of;  // per sealed pool token
     bs::DevBuf<bs::IndexEntry> table;
     uint64_t table_mask = 0;
+    bs::DevBuf<bs::IndexDesc> idx_desc;
     // verify scratch: clamped q per rollout, the step's row table (RowDesc, 48 B per row)
     // and its control words
     bs::DevBuf<int32_t> rb_q, vqueue;

@@ -219,6 +219,17 @@ static int bits_for(uint64_t v) {
         if (e__ != cudaSuccess) return e__; \
     } while (0)
 
+// The lookup kernel reads the sealed index through a device-resident descriptor, so a
+// captured decode-step graph stays valid when a later seal reallocates the index.
+static cudaError_t publish_index(bs_ctx* ctx, cudaStream_t st) {
+    IndexDesc d;
+    d.table = ctx->table.p;
+    d.mask = ctx->table_mask;
+    d.T = ctx->sealed.tokens.p;
+    d.seq_start_of = ctx->seq_start_of.p;
+    return cudaMemcpyAsync(ctx->idx_desc.p, &d, sizeof d, cudaMemcpyHostToDevice, st);  // pageable: staged now
+}
+
 cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
     const int64_t N = ctx->sealed.n_tokens;
     const int M = ctx->M, K = ctx->cfg.k_max, D = M + K;
@@ -240,6 +251,7 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         BS_TRY(ctx->table.ensure(2));
         BS_TRY(cudaMemsetAsync(ctx->table.p, 0, 2 * sizeof(IndexEntry), st));
         ctx->table_mask = 1;
+        BS_TRY(publish_index(ctx, st));
         return cudaStreamSynchronize(st);
     }
     const int* T = ctx->sealed.tokens.p;
@@ -359,6 +371,7 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         std::swap(pq, pq_child);
         std::swap(po, po_child);
     }
+    BS_TRY(publish_index(ctx, st));
     return cudaStreamSynchronize(st);
 }
 
@@ -372,10 +385,7 @@ struct LookupArgs {
     const int32_t* pos;
     const int32_t* max_len;
     const int32_t* finished;
-    const IndexEntry* table;
-    uint64_t mask;
-    const int32_t* T;
-    const int32_t* seq_start_of;
+    const IndexDesc* desc;  // the sealed index (device-resident: stable across RL steps)
     int32_t* draft;
     int32_t* draft_len;
     int32_t* match_len;
@@ -397,12 +407,19 @@ __device__ __forceinline__ bool probe(const IndexEntry* table, uint64_t mask, ui
     }
 }
 
-__global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
+__global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a0) {
     pdl_wait();
     pdl_trigger();
     const int lane = threadIdx.x & 31;
     const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (b >= a.n) return;
+    if (b >= a0.n) return;
+    struct {
+        const IndexEntry* table;
+        uint64_t mask;
+        const int32_t* T;
+        const int32_t* seq_start_of;
+    } x = {a0.desc->table, a0.desc->mask, a0.desc->T, a0.desc->seq_start_of};
+    const LookupArgs& a = a0;
     const int slot = a.slots[b];
     const int M = a.M;
     const int L = a.ctx_len[slot];
@@ -424,7 +441,7 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
     }
     uint32_t occ = 0, meta = 0;
     bool found = false;
-    if (!fin && lane < mmax) found = probe(a.table, a.mask, window_key(H, P, lane + 1), occ, meta);
+    if (!fin && lane < mmax) found = probe(x.table, x.mask, window_key(H, P, lane + 1), occ, meta);
     unsigned hit = __ballot_sync(0xFFFFFFFFu, found);
     int mstar = 0, q = 0, dstart = 0;
     for (;;) {
@@ -434,21 +451,21 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
         const uint32_t meta0 = __shfl_sync(0xFFFFFFFFu, meta, m0 - 1);
         // verify y[-m0:] == T[occ0 .. occ0+m0) (guards a 64-bit key false positive)
         bool okc = true;
-        if (lane < m0) okc = (a.T[(int64_t)occ0 + m0 - 1 - lane] == tok);
+        if (lane < m0) okc = (x.T[(int64_t)occ0 + m0 - 1 - lane] == tok);
         if (!__all_sync(0xFFFFFFFFu, okc)) {
             hit &= ~(1u << (m0 - 1));
             continue;
         }
         if ((meta0 & META_UNIQUE) && (meta0 & META_CONT)) {
             // unique occurrence: extend the anchor to the left within its sequence
-            const int sstart = a.seq_start_of[occ0];
+            const int sstart = x.seq_start_of[occ0];
             const int jj = lane;  // compare y[-m0-1-jj] with T[occ0-1-jj]
             bool eq = false;
             if (m0 + jj < mmax) {
                 const int64_t pp = (int64_t)occ0 - 1 - jj;
                 if (pp >= sstart) {
                     const int yt = a.tail[(int64_t)slot * M + (M - 1 - (m0 + jj))];
-                    eq = (a.T[pp] == yt);
+                    eq = (x.T[pp] == yt);
                 }
             }
             const unsigned eqm = __ballot_sync(0xFFFFFFFFu, eq);
@@ -467,7 +484,7 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
         const uint32_t occs = __shfl_sync(0xFFFFFFFFu, occ, ms - 1);
         const uint32_t metas = __shfl_sync(0xFFFFFFFFu, meta, ms - 1);
         bool oks = true;
-        if (lane < ms) oks = (a.T[(int64_t)occs + ms - 1 - lane] == tok);
+        if (lane < ms) oks = (x.T[(int64_t)occs + ms - 1 - lane] == tok);
         if (!__all_sync(0xFFFFFFFFu, oks)) {
             hit &= ~(1u << (ms - 1));
             continue;
@@ -487,7 +504,7 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
     }
     q = min(q, a.k);
     q = min(q, max(0, ml - p - 1));
-    if (lane < a.k) a.draft[(int64_t)b * a.k + lane] = (lane < q) ? a.T[(int64_t)dstart + lane] : -1;
+    if (lane < a.k) a.draft[(int64_t)b * a.k + lane] = (lane < q) ? x.T[(int64_t)dstart + lane] : -1;
     if (lane == 0) {
         a.draft_len[b] = q;
         if (a.match_len) a.match_len[b] = mstar;
@@ -509,10 +526,7 @@ cudaError_t launch_lookup(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t 
     a.pos = ctx->pos.p;
     a.max_len = ctx->max_len.p;
     a.finished = ctx->finished.p;
-    a.table = ctx->table.p;
-    a.mask = ctx->table_mask;
-    a.T = ctx->sealed.tokens.p;
-    a.seq_start_of = ctx->seq_start_of.p;
+    a.desc = ctx->idx_desc.p;
     a.draft = draft;
     a.draft_len = draft_len;
     a.match_len = match_len;

@@ -857,6 +857,10 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             e = cudaFuncSetAttribute(verify_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)csm);
             if (e != cudaSuccess) return e;
+            if (CK_CL > 8) {
+                e = cudaFuncSetAttribute(verify_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                if (e != cudaSuccess) return e;
+            }
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(CK_CL * ctx->num_sms);
             cfg.blockDim = dim3(CK_NT);

@@ -21,7 +21,11 @@
 #pragma once
 // (included inside namespace bs)
 
+#ifdef BS_CK_CL
+constexpr int CK_CL = BS_CK_CL;           // CTAs per cluster (experiment)
+#else
 constexpr int CK_CL = 8;                  // CTAs per cluster
+#endif
 constexpr int CK_NMW = 8;                 // mass warps: 0..7 (two per SM sub-partition)
 constexpr int CK_NXW = 2;                 // max warps: 8..9
 constexpr int CK_NCW = CK_NMW + CK_NXW;
@@ -286,6 +290,7 @@ struct ClaimState {
     int nlive = -1;          // live rollouts (after the plan completed)
     bool eager = false;
     bool static_done = false;  // the static cursor is exhausted
+    int spec_b = -1, spec_r = 0;  // chain this cluster just continued: speculate its next row
 };
 
 __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool queues, int rot,
@@ -319,7 +324,11 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
             }
             mb = __shfl_sync(0xFFFFFFFFu, mb, 0);
             if (mb >= 0) {
-                if (ck_take(a, epoch, mb >> 8, SRC_READY, lane, mb & 0xFF, out)) return out;
+                if (ck_take(a, epoch, mb >> 8, SRC_READY, lane, mb & 0xFF, out)) {
+                    cs.spec_b = mb >> 8;  // next claim: the chain's following row, speculatively
+                    cs.spec_r = out.j + 1;
+                    return out;
+                }
                 continue;
             }
         }
@@ -339,6 +348,13 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
             j = __shfl_sync(0xFFFFFFFFu, j, 0);
             if (eager ? ck_take_row(a, b, j, lane, out) : ck_take(a, epoch, b, SRC_STATIC, lane, 0, out)) return out;
             continue;
+        }
+        // no certain work left in the static list: speculate the chain just continued here
+        // (its second buffer would idle otherwise; a dead row stops early)
+        if (cs.spec_b >= 0) {
+            const int sb = cs.spec_b, sr = cs.spec_r;
+            cs.spec_b = -1;
+            if (sr <= a.k && ck_take(a, epoch, sb, SRC_SPEC, lane, sr, out)) return out;
         }
         if (eager) break;  // every row claimed: nothing left for this cluster
         if (queues) {
@@ -443,12 +459,12 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             if (lane == 0) TRACE(TR_CLAIM1, r | (nd.b >= 0 ? nd.pad[0] << 12 : 0), nd.b, nd.j);
             uint32_t w[12];
             memcpy(w, &nd, sizeof(w));
-            if (lane < 3 * CK_CL) {
-                const int part = lane % 3;
+            for (int x = lane; x < 3 * CK_CL; x += 32) {
+                const int part = x % 3;
                 uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
                 if (part == 1) v = make_uint4(w[4], w[5], w[6], w[7]);
                 if (part == 2) v = make_uint4(w[8], w[9], w[10], w[11]);
-                st_async_v4(reinterpret_cast<uint4*>(&sh.dq[s]) + part, v, &sh.dfull[s], (uint32_t)(lane / 3));
+                st_async_v4(reinterpret_cast<uint4*>(&sh.dq[s]) + part, v, &sh.dfull[s], (uint32_t)(x / 3));
             }
         };
         if (lane == 0) mbar_arrive_expect_tx(&sh.dfull[0], (uint32_t)sizeof(RowDesc));
