@@ -33,6 +33,11 @@ constexpr int CK_PROD = CK_NCW;           // producer warp
 constexpr int CK_EPI = CK_NCW + 1;        // epilogue warp
 constexpr int CK_NT = (CK_NCW + 2) * 32;  // 384 threads
 constexpr int CK_NB = 2;                  // slice buffers
+#ifdef BS_CK_MINB
+constexpr int CK_MINB = BS_CK_MINB;       // min CTAs per SM (register budget experiment)
+#else
+constexpr int CK_MINB = 2;
+#endif
 constexpr int CK_D = 4;                   // descriptor / exchange ring depth
 constexpr int CK_TILE = 512;              // elements per tile (16 per lane)
 constexpr int CK_MAXT = 104;              // tiles per slice
@@ -398,7 +403,7 @@ __device__ __forceinline__ void ck_mass16(const uint4 v0, const uint4 v1, const 
     mass8_masked(v1, mp, e0 + 8, nvalid, excl, mm + 8);
 }
 
-__global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
+__global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
     verify_cluster_kernel(const VerifyArgs a, int SL) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -764,7 +769,10 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             const RowDesc dsc = sh.dq[s];
             if (dsc.b < 0) break;
             mbar_wait(&sh.maxbar[s], (i / CK_D) & 1);  // the 8 slice maxima of row i
-            if (warp == 0 && lane == 0) TRACE(TR_MASS0, i, 0, 0);
+            if (lane == 0) TRACE(TR_MASS0, i, warp, 0);
+#ifdef BS_TRACE
+            const long long mc0 = clock64();
+#endif
             float m = -INFINITY;
             uint32_t bad = 0;
             int g = 0x7FFFFFFF;
@@ -783,24 +791,8 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
             uint64_t wacc = 0;
             if (a.T > 0.f && ok) {
                 mp.nmc = -__fmul_rn(m, a.c);
-                const bool split = a.S <= 44;  // FMA-pipe conversion for half the elements
-                for (int t = warp; t < ntile; t += CK_NMW) {
-                    const int e0 = t * CK_TILE + lane * 16;
-                    uint64_t acc;
-                    if (t * CK_TILE + CK_TILE <= len) {
-                        const uint4 v0 = lds128(buf + e0), v1 = lds128(buf + e0 + 8);
-#if defined(BS_EXP_F2I)
-                        acc = mass8(v0, mp) + mass8(v1, mp);
-#elif defined(BS_EXP_SPLIT)
-                        acc = mass16_split(v0, v1, mp);
-#else
-                        acc = split ? mass16_mixed(v0, v1, mp) : mass8(v0, mp) + mass8(v1, mp);
-#endif
-                    } else {
-                        acc = 0;
-                        for (int x = 0; x < 16; ++x)
-                            if (e0 + x < len) acc += mass_of(__uint_as_float((uint32_t)buf[e0 + x] << 16), mp);
-                    }
+                const int nfull = len / CK_TILE;  // whole tiles; the slice's ragged end follows
+                auto tile_done = [&](int t, uint64_t acc) {
 #ifdef BS_EXP_NOREDUX
                     wacc += acc;
 #else
@@ -808,9 +800,30 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, 2)
                     if (lane == 0) sh.tsum[s][t] = ts;
                     wacc += ts;
 #endif
+                };
+                if (a.S <= 44) {  // FMA-pipe conversion for half the elements (mass16_mixed)
+                    for (int t = warp; t < nfull; t += CK_NMW) {
+                        const int e0 = t * CK_TILE + lane * 16;
+                        tile_done(t, mass16_mixed(lds128(buf + e0), lds128(buf + e0 + 8), mp));
+                    }
+                } else {
+                    for (int t = warp; t < nfull; t += CK_NMW) {
+                        const int e0 = t * CK_TILE + lane * 16;
+                        tile_done(t, mass8(lds128(buf + e0), mp) + mass8(lds128(buf + e0 + 8), mp));
+                    }
+                }
+                if (nfull < ntile && warp == nfull % CK_NMW) {  // the ragged last tile
+                    const int e0 = nfull * CK_TILE + lane * 16;
+                    uint64_t acc = 0;
+                    for (int x = 0; x < 16; ++x)
+                        if (e0 + x < len) acc += mass_of(__uint_as_float((uint32_t)buf[e0 + x] << 16), mp);
+                    tile_done(nfull, acc);
                 }
             }
             if (lane == 0) sh.wsum[warp] = wacc;
+#ifdef BS_TRACE
+            if (lane == 0) TRACE(TR_MASSL, i, warp, (int)min(255ll, (clock64() - mc0) >> 6));
+#endif
             named_bar(1, CK_NMW * 32);
             if (warp == 0) {
                 uint64_t cs = 0;

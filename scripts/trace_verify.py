@@ -101,7 +101,7 @@ else:
         m = lib.bsx_trace_read(buf.ctypes.data, 1 << 20, 1)
         res.append((s.elapsed_time(e), m, buf[:m].copy(), int(st1[6] - st0[6]), int(st1[7] - st0[7])))
 
-names = ["claim0", "claim1", "tma", "max0", "max1", "mass0", "mass1", "epi0", "epi1", "end", "fin", "spins", "sc", "sqpop", "iter"]
+names = ["claim0", "claim1", "tma", "max0", "max1", "mass0", "mass1", "epi0", "epi1", "end", "fin", "spins", "sc", "sqpop", "iter", "massl"]
 ms, m, ev, rv, rn = res[-1]
 blk = ev[:, 0] & 0xFFFF
 typ = (ev[:, 0] >> 16) & 0xFF
@@ -214,3 +214,35 @@ if os.environ.get("TRACE_FLIGHT"):
     print(f"  claim iterations of block 40: {len(its)}")
     for p_ in its[:60]:
         print(f"    t={p_[0]:7.2f} spin {p_[2]} b {p_[3]} src {p_[4]}")
+if os.environ.get("TRACE_MASS"):
+    # per (block, row): spread of mass-warp start times and loop end times
+    st_, en_ = {}, {}
+    for tt, ty, sq, b_, bk in zip(t, typ, seq, bb, blk):
+        if ty == 5:
+            st_.setdefault((int(bk), int(sq)), []).append(float(tt))
+        if ty == 15:
+            en_.setdefault((int(bk), int(sq)), []).append(float(tt))
+    sp, ln, lo = [], [], []
+    for key_, v in st_.items():
+        if key_ in en_ and len(v) == 8 and len(en_[key_]) == 8:
+            sp.append(max(v) - min(v))
+            ln.append(max(en_[key_]) - min(v))
+            lo.append(min(en_[key_]) - min(v))
+    print(f"  mass warps: start spread median {np.median(sp):.2f} us; first loop end {np.median(lo):.2f}; "
+          f"last loop end {np.median(ln):.2f} us (from first start), rows {len(sp)}")
+    cyc = [int(j_) * 64 for tt, ty, j_ in zip(t, typ, jj) if ty == 15]
+    print(f"  mass loop cycles per warp: median {np.median(cyc):.0f} p90 {np.percentile(cyc, 90):.0f} (x64 quantized)")
+    # which warps finish their mass loop last (per-warp mean lateness vs the row's first finish)
+    fin_w = collections.defaultdict(list) if False else {}
+    per_row = {}
+    for tt, ty, b_, bk, sq in zip(t, typ, bb, blk, seq):
+        if ty == 15:
+            per_row.setdefault((int(bk), int(sq)), {})[int(b_)] = float(tt)
+    late = np.zeros(8); cnt = np.zeros(8)
+    for key_, d_ in per_row.items():
+        if len(d_) == 8:
+            m0 = min(d_.values())
+            for w_, tt in d_.items():
+                late[w_] += tt - m0
+                cnt[w_] += 1
+    print("  mass loop lateness by warp (us):", " ".join(f"w{w_}:{late[w_] / max(1, cnt[w_]):.2f}" for w_ in range(8)))

@@ -5,6 +5,7 @@
 // and 1 vs 2 CTAs per SM.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2605_08862_b200/csrc -o /tmp/ubml scripts/ubench_massloop.cu
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -124,7 +125,7 @@ int main() {
     cudaMalloc(&o, sizeof(unsigned long long) * 2 * sms * NW);
     cudaMalloc(&c, sizeof(long long) * 2 * sms);
     cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice);
-    const int reps = 50;
+    const int reps = getenv("REPS") ? atoi(getenv("REPS")) : 50;
     const char* names[5] = {"mixed", "f2i", "split", "imm", "splimm"};
     for (int mode = 0; mode < 5; ++mode)
         for (int per = 1; per <= 2; ++per) {

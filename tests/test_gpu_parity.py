@@ -306,3 +306,67 @@ def test_synth_bank_matches_numpy(bs):
     torch.cuda.synchronize()
     want = bank_rows(1234, np.arange(rows), V, 11.5)
     assert np.array_equal(bank.cpu().numpy().view(np.uint16), want)
+
+
+def _random_step(rng, n, k, V, peaked=0.6):
+    rows = f32_to_bf16_bits(rng.normal(0, 2.0, size=(n, k + 1, V)).astype(np.float32))
+    for b in range(n):
+        for j in range(k + 1):
+            if rng.random() < peaked:
+                rows[b, j, rng.integers(0, V)] = f32_to_bf16_bits(np.float32(9.0))
+    argm = bf16_bits_to_f32(rows).argmax(axis=2)
+    drafts = np.where(rng.random((n, k)) < 0.8, argm[:, :k], rng.integers(0, V, (n, k)))
+    dlen = rng.integers(0, k + 1, n)
+    return rows, drafts, dlen
+
+
+@pytest.mark.parametrize("eager", [True, False])
+@pytest.mark.parametrize("n_live,n", [(1, 64), (4, 64), (30, 64), (64, 64)])
+def test_cluster_scheduler_mostly_finished(bs, orc, monkeypatch, eager, n_live, n):
+    """The cluster kernel's scheduler (in-kernel plan, compacted live list, eager all-rows
+    mode for small live batches vs lazy ready/static/speculative claims): most slots
+    finished (max_len = 0) must emit nothing; live ones match the oracle bit for bit, and the
+    result does not depend on the scheduling mode."""
+    if not eager:
+        monkeypatch.setenv("BS_NO_EAGER", "1")
+    rng = np.random.default_rng(7 * n_live + n)
+    V, k = 4099, 6
+    rows, drafts, dlen = _random_step(rng, n, k, V)
+    live = rng.permutation(n)[:n_live]
+    max_len = np.zeros(n, dtype=np.int64)
+    max_len[live] = 1000
+    seed = 0x1234
+    ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=8, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    ctx.bsx_set_verify_kernel("cluster")
+    uids = np.arange(n, dtype=np.uint64) * np.uint64(104729) + np.uint64(11)
+    _begin(bs, ctx, n, max_len, uids, 8)
+    got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, 1.0, 1.0)
+    assert ctx.bs_sync_status() == 0
+    ot, ol, oa, on, oz = got
+    dead = np.setdiff1d(np.arange(n), live)
+    assert (ol[dead] == 0).all() and (ot[dead] == -1).all()
+    sel = np.sort(live)
+    _compare_step(orc, rows[sel], drafts[sel], dlen[sel], k, 1.0, 1.0, seed, uids[sel], max_len[sel], -1,
+                  tuple(x[sel] for x in got))
+
+
+def test_cluster_scheduler_repeated_launches(bs, orc):
+    """Many launches on one context (the scheduler's per-launch epoch, counter resets by the
+    last CTA out, plan records overwritten each launch) with a changing live set."""
+    rng = np.random.default_rng(99)
+    V, k, n = 2048, 4, 40
+    seed = 0x77
+    ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=8, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    ctx.bsx_set_verify_kernel("cluster")
+    uids = np.arange(n, dtype=np.uint64) + np.uint64(5)
+    for it in range(12):
+        max_len = np.where(rng.random(n) < 0.5, 1000, 0)
+        _begin(bs, ctx, n, max_len, uids, 8)
+        rows, drafts, dlen = _random_step(rng, n, k, V)
+        got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, 1.0 if it % 3 else 0.0, 1.0)
+        assert ctx.bs_sync_status() == 0
+        live = np.nonzero(max_len)[0]
+        _compare_step(orc, rows[live], drafts[live], dlen[live], k, 1.0 if it % 3 else 0.0, 1.0, seed,
+                      uids[live], max_len[live], -1, tuple(x[live] for x in got))
