@@ -201,13 +201,11 @@ def run_ours(args, cfg, rank, world, dist):
                                       t.mode, t.nbank, eng.row_index, stream=stream)
                     if instrument:
                         ev_s[i].record(stream)
-                    c.bs_verify_step(eng.slots, t.bank, eng.row_index, V, eng.draft,
-                                     eng.draft_len, k, eng.T, eng.top_p, eng.out_tokens,
-                                     eng.out_len, eng.out_acc, stream=stream)
+                    c.bs_verify_commit(eng.slots, t.bank, eng.row_index, V, eng.draft,
+                                       eng.draft_len, k, eng.T, eng.top_p, eng.out_tokens,
+                                       eng.out_len, eng.out_acc, eng.finished, stream=stream)
                     if instrument:
                         ev_e[i].record(stream)
-                    c.bs_commit(eng.slots, eng.out_tokens, eng.out_len, k, eng.finished,
-                                stream=stream)
         return g
 
     phases = os.environ.get("BS_BENCH_PHASES")  # diagnostics: host wall per RL-step phase
@@ -487,7 +485,7 @@ def main():
     hbm = hbm or 6650.0
     ms_per_step = r["elapsed_ms"] / args.steps
     value = r["tokens"] / (r["elapsed_ms"] / 1e3)
-    # dominant kernel: the verify op (plan + rows kernels), timed by captured events
+    # dominant kernel: the verify op (one cluster-kernel launch), timed by captured events
     vlaunches = rec["decode_steps"]
     v_avg_ms = rec["verify_ms"] / max(1, vlaunches)
     alg_bytes = rec["verify_rows_needed"] * row_bytes / max(1, vlaunches)   # per launch
@@ -523,8 +521,8 @@ def main():
                     "steady_algorithmic": steady_alg, "steady_moved": steady_moved},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": "bs_verify_step (plan + rows/split kernels), avg over an "
-                               "instrumented replay of the timed RL steps",
+                     "kernel": "bs_verify_commit (verify_cluster_kernel: in-kernel plan, rows, "
+                               "fused commit), avg over an instrumented replay of the timed RL steps",
                      "peak_source": peak_src,
                      "steady_frac": steady_alg / hbm},
         "clocks": r["clocks"],

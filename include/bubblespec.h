@@ -201,6 +201,19 @@ bs_status bs_verify_step(bs_ctx* ctx, int32_t n, const int32_t* slots, const voi
                          int32_t* out_accepted, float* out_norm, uint64_t* out_z,
                          void* stream);
 
+/* bs_verify_step followed by bs_commit, fused into one launch where the verify kernel
+ * supports it (the cluster kernel, top_p = 1): the thread that finalizes a rollout's
+ * step (Alg. 1 lines 10-31) also performs that rollout's commit (lines 15/22 "y <- y o a";
+ * same state update as bs_commit), so no separate commit kernel runs.  Arguments are
+ * those of bs_verify_step plus bs_commit's `finished` output [n] (may be NULL).  Results
+ * and rollout state are identical to bs_verify_step + bs_commit (tested). */
+bs_status bs_verify_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits_bf16,
+                           const int64_t* row_index, int64_t row_stride_elems,
+                           const int32_t* draft_tokens, const int32_t* draft_len, int32_t k,
+                           bs_sampling sampling, int32_t* out_tokens, int32_t* out_len,
+                           int32_t* out_accepted, float* out_norm, uint64_t* out_z,
+                           int32_t* finished, void* stream);
+
 /* Commit (Alg. 1 lines 15/22 "y <- y o a"): append out_len[b] tokens of row b of
  * out_tokens [n*(k+1)] to each rollout, advance its position, and mark it
  * finished on an emitted EOS or when pos reaches max_len (Alg. 1 line 2).

@@ -118,6 +118,16 @@ class Context:
                                          _p(out_accepted), _p(out_norm), _p(out_z),
                                          _stream(stream, self.device)), "bs_verify_step")
 
+    def bs_verify_commit(self, slots, logits, row_index, row_stride, draft_tokens, draft_len, k,
+                         temperature, top_p, out_tokens, out_len, out_accepted, finished=None,
+                         out_norm=None, out_z=None, stream=None):
+        sp = bs_sampling(temperature, top_p)
+        _chk(self, load().bs_verify_commit(self.handle, slots.numel(), _p(slots), _p(logits),
+                                           _p(row_index), row_stride, _p(draft_tokens),
+                                           _p(draft_len), k, sp, _p(out_tokens), _p(out_len),
+                                           _p(out_accepted), _p(out_norm), _p(out_z), _p(finished),
+                                           _stream(stream, self.device)), "bs_verify_commit")
+
     def bs_commit(self, slots, out_tokens, out_len, k, finished=None, stream=None):
         _chk(self, load().bs_commit(self.handle, slots.numel(), _p(slots), _p(out_tokens),
                                     _p(out_len), k, _p(finished), _stream(stream, self.device)),

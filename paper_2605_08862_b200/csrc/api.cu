@@ -287,6 +287,34 @@ bs_status bs_verify_step(bs_ctx* c, int32_t n, const int32_t* slots, const void*
     return BS_OK;
 }
 
+bs_status bs_verify_commit(bs_ctx* c, int32_t n, const int32_t* slots, const void* logits,
+                           const int64_t* row_index, int64_t stride, const int32_t* draft_tokens,
+                           const int32_t* draft_len, int32_t k, bs_sampling sp, int32_t* out_tokens,
+                           int32_t* out_len, int32_t* out_accepted, float* out_norm, uint64_t* out_z,
+                           int32_t* finished, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
+    if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
+    if (stride < c->cfg.vocab) return fail(c, BS_ERR_INVALID, "row stride < vocab");
+    if (!(sp.temperature >= 0.f) || sp.temperature == INFINITY)
+        return fail(c, BS_ERR_INVALID, "temperature must be finite and >= 0");
+    if (!(sp.top_p > 0.f && sp.top_p <= 1.f)) return fail(c, BS_ERR_INVALID, "top_p must be in (0, 1]");
+    if (sp.temperature > 0.f && !((float)(1.4426950408889634 / (double)sp.temperature) < INFINITY))
+        return fail(c, BS_ERR_INVALID, "temperature too small");
+    if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
+              (k && !draft_tokens)))
+        return fail(c, BS_ERR_INVALID, "null array");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bool fused = false;
+    CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
+                        sp.temperature, sp.top_p, out_tokens, out_len, out_accepted, out_norm,
+                        reinterpret_cast<unsigned long long*>(out_z), S(stream), finished, &fused),
+       "bs_verify_commit");
+    if (!fused)  // kernels without the fused commit: the commit kernel follows
+        CK(c, launch_commit(c, n, slots, out_tokens, out_len, k, finished, S(stream)), "bs_verify_commit");
+    return BS_OK;
+}
+
 bs_status bs_commit(bs_ctx* c, int32_t n, const int32_t* slots, const int32_t* out_tokens,
                     const int32_t* out_len, int32_t k, int32_t* finished, void* stream) {
     if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");

@@ -133,6 +133,15 @@ struct VerifyArgs {
     unsigned long long* next_row; // per rollout: epoch << 32 | next unclaimed row
     RollRec* rrec;                // per rollout: the launch's plan
     int32_t* live;                // the launch's live rollouts (compacted by the planners)
+    // fused commit (bs_verify_commit): the finalizing thread appends the rollout's tokens
+    int commit, M;
+    int32_t* c_tail;
+    int32_t* c_ctx_len;
+    int32_t* c_pos;
+    int32_t* c_finished;
+    int32_t* c_fin_out;
+    int32_t* c_resp;
+    int64_t c_resp_stride;
     int ncl;                      // clusters in the grid
     int eager_ok;                 // small live batches claim every row at once
 };
@@ -175,6 +184,34 @@ struct __align__(16) VShared {
     EpiBuf epi[2];
     unsigned long long stat[STAT_COUNT];
 };
+
+// Alg. 1 lines 15/22 ("y <- y o a") for one rollout, by the warp whose lane 0 just
+// finalized its step: the same state update as commit_kernel (state.cu), fused into the
+// verify launch.  Lane i owns tail slot i (M <= 32) and emitted token i (<= k+1 <= 32).
+__device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane) {
+    __syncwarp();  // lane 0's outputs (finalize_rollout) are visible to the warp
+    const int s = a.slots[b];
+    const int M = a.M;
+    const int no = a.out_len[b];
+    const int p = a.c_pos[s], L = a.max_len[s];
+    const int32_t* out = a.out_tokens + (int64_t)b * (a.k + 1);
+    int32_t* tl = a.c_tail + (int64_t)s * M;
+    const int32_t old = (lane < M) ? tl[lane] : -1;
+    const int32_t ot = (lane < no) ? out[lane] : -1;
+    const int src = lane + no;  // new tail[i] = (old ++ out)[i + no]
+    const int32_t from_old = __shfl_sync(0xFFFFFFFFu, old, src & 31);
+    const int32_t from_out = __shfl_sync(0xFFFFFFFFu, ot, (src - M) & 31);
+    if (lane < M) tl[lane] = (src < M) ? from_old : from_out;
+    if (a.c_resp && lane < no && p + lane < a.c_resp_stride) a.c_resp[(int64_t)s * a.c_resp_stride + p + lane] = ot;
+    const int32_t last = __shfl_sync(0xFFFFFFFFu, ot, (no - 1) & 31);
+    const int f = ((a.eos >= 0 && last == a.eos) || p + no >= L) ? 1 : 0;
+    if (lane == 0) {
+        a.c_ctx_len[s] = min(M, a.c_ctx_len[s] + no);
+        a.c_pos[s] = p + no;
+        if (f) a.c_finished[s] = 1;
+        if (a.c_fin_out) a.c_fin_out[b] = f;
+    }
+}
 
 // Alg. 1 lines 10-31 for rollout b, decided at row F (rows < F accepted).
 __device__ void finalize_rollout(const VerifyArgs& a, unsigned long long* s, int b, int F, int q) {
@@ -235,7 +272,8 @@ __device__ __forceinline__ unsigned long long atom_or_acq_rel(unsigned long long
 }
 
 // Record a completed row and finalize its rollout if this completes the decided prefix.
-__device__ void complete_row(const VerifyArgs& a, unsigned long long* stat, int b, int j, int q, int status,
+// Returns true when this row's completion finalized the rollout's step.
+__device__ bool complete_row(const VerifyArgs& a, unsigned long long* stat, int b, int j, int q, int status,
                              int cand, unsigned long long z, float norm) {
     const int64_t r = (int64_t)b * (a.k + 1) + j;
     a.row_status[r] = status;
@@ -248,7 +286,11 @@ __device__ void complete_row(const VerifyArgs& a, unsigned long long* stat, int 
     // release: this row's record; acquire: every earlier row's record of the rollout
     const unsigned long long old = atom_or_acq_rel(a.roll_state + b, mine);
     int F0, F1;
-    if (!prefix_decided(old, F0) && prefix_decided(old | mine, F1)) finalize_rollout(a, stat, b, F1, q);
+    if (!prefix_decided(old, F0) && prefix_decided(old | mine, F1)) {
+        finalize_rollout(a, stat, b, F1, q);
+        return true;
+    }
+    return false;
 }
 
 // Claim the next needed row of the plan's j-major table (Alg. 1's order across the batch),
@@ -771,7 +813,9 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
                           const int64_t* row_index, int64_t stride, const int32_t* draft,
                           const int32_t* draft_len, int32_t k, float T, float top_p,
                           int32_t* out_tokens, int32_t* out_len, int32_t* out_acc,
-                          float* out_norm, unsigned long long* out_z, cudaStream_t st) {
+                          float* out_norm, unsigned long long* out_z, cudaStream_t st,
+                          int32_t* commit_finished, bool* committed) {
+    if (committed) *committed = false;
     if (n == 0) return cudaSuccess;
     const int V = ctx->cfg.vocab;
     const bool topp = T > 0.f && top_p < 1.f;
@@ -834,6 +878,18 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
         a.rrec = ctx->vrrec.p;
         a.live = ctx->vlive.p;
         a.eager_ok = getenv("BS_NO_EAGER") ? 0 : 1;
+        if (committed) {  // fused commit (bs_verify_commit)
+            a.commit = 1;
+            a.M = ctx->M;
+            a.c_tail = ctx->tail.p;
+            a.c_ctx_len = ctx->ctx_len.p;
+            a.c_pos = ctx->pos.p;
+            a.c_finished = ctx->finished.p;
+            a.c_fin_out = commit_finished;
+            a.c_resp = ctx->responses;
+            a.c_resp_stride = ctx->resp_stride;
+            *committed = true;
+        }
     }
     if (topp) {  // R5: top-p filtered rows (verify_topp.cuh)
         if (ntile_ok(V) == 0) return cudaErrorInvalidValue;

@@ -118,6 +118,11 @@ __device__ void ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
         if (q < 0) {  // finished / out of length / bad draft: no rows, nothing emitted
             a.out_len[b] = 0;
             a.out_acc[b] = 0;
+            if (a.commit) {  // fused commit of an empty step: only the length check
+                const int f = (a.finished[sl] || p >= L) ? 1 : 0;
+                if (f && !a.finished[sl]) a.c_finished[sl] = 1;
+                if (a.c_fin_out) a.c_fin_out[b] = f;
+            }
             atomicAdd(a.sctl + SC_DONE, 1u);
         }
         __threadfence();
@@ -243,7 +248,7 @@ __device__ __forceinline__ bool ck_take_row(const VerifyArgs& a, int b, int j, i
 // Warp scan of every rollout's claim state; returns the best rollout, its class and the
 // counter value seen.  Two independent loads per rollout (claim word, state word): one
 // round trip per CK_SCAN*32 rollouts.  roll_first is derived: min(q, lowest deciding row).
-constexpr int CK_SCAN = 8;
+constexpr int CK_SCAN = 4;
 __device__ int ck_scan(const VerifyArgs& a, uint32_t epoch, int lane, int rot, int& src, int& rpred) {
     const int n = a.n;
     unsigned best = 0;
@@ -541,11 +546,12 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             else if (m == -INFINITY) err |= DEV_ALL_NEGINF;
             else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) err |= DEV_RANGE;
             const bool lead = rank == 0 && lane == 0;
+            bool fz = false;  // lane 0 finalized the rollout's step (fused commit follows)
             if (err) {
                 if (lead) {
                     atomicOr(a.dev_err, err);
                     sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                    complete_row(a, sh.stat, b, j, q, ST_DECIDED, -1, 0ull, 0.f);
+                    fz = complete_row(a, sh.stat, b, j, q, ST_DECIDED, -1, 0ull, 0.f);
                 }
             } else if (a.T == 0.f) {  // greedy (R1): lowest index attaining m
                 const int g = (int)er.z;
@@ -553,7 +559,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                     const bool acc = j < q && d == g;
                     const int status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
                     sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                    complete_row(a, sh.stat, b, j, q, status, g, 1ull, 1.f);
+                    fz = complete_row(a, sh.stat, b, j, q, status, g, 1ull, 1.f);
                     if (status == ST_CONT) *reinterpret_cast<volatile int*>(&sh.mail) = (b << 8) | (j + 1);
                 }
             } else {
@@ -564,7 +570,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 if (status != ST_DECIDED) {
                     if (lead) {
                         sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                        complete_row(a, sh.stat, b, j, q, status, -1, Z, norm);
+                        fz = complete_row(a, sh.stat, b, j, q, status, -1, Z, norm);
                         if (status == ST_CONT) *reinterpret_cast<volatile int*>(&sh.mail) = (b << 8) | (j + 1);
                     }
                 } else {
@@ -650,11 +656,12 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                         tok = __shfl_sync(0xFFFFFFFFu, tok, L2);
                         if (lane == 0) {
                             sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                            complete_row(a, sh.stat, b, j, q, ST_DECIDED, tok, Z, norm);
+                            fz = complete_row(a, sh.stat, b, j, q, ST_DECIDED, tok, Z, norm);
                         }
                     }
                 }
             }
+            if (a.commit && __shfl_sync(0xFFFFFFFFu, fz ? 1 : 0, 0)) commit_rollout_warp(a, b, lane);
             __syncwarp();
             if (lane == 0) {
                 TRACE(TR_EPI1, i, dsc.b, dsc.j);

@@ -31,8 +31,9 @@ class Target:
 
 class RolloutEngine:
     def __init__(self, ctx: Context, n: int, k: int, temperature: float, top_p: float,
-                 target: Target, stream: torch.cuda.Stream | None = None):
+                 target: Target, stream: torch.cuda.Stream | None = None, fused: bool = True):
         self.ctx, self.n, self.k = ctx, n, k
+        self.fused = fused  # bs_verify_commit (one launch) instead of bs_verify_step + bs_commit
         self.T, self.top_p, self.target = temperature, top_p, target
         dev = torch.device("cuda", ctx.device)
         # a dedicated stream: CUDA graphs cannot be captured on the legacy default stream
@@ -81,12 +82,18 @@ class RolloutEngine:
         t = self.target
         c.bsx_target_rows(self.slots, self.draft, self.draft_len, k, t.target_seed, t.mode,
                           t.nbank, self.row_index, stream=s)
-        c.bs_verify_step(self.slots, t.bank, self.row_index, t.bank.shape[1], self.draft,
-                         self.draft_len, k, self.T, self.top_p, self.out_tokens, self.out_len,
-                         self.out_acc, stream=s)
-        c.bs_commit(self.slots, self.out_tokens, self.out_len, k, self.finished, stream=s)
+        if self.fused:
+            c.bs_verify_commit(self.slots, t.bank, self.row_index, t.bank.shape[1], self.draft,
+                               self.draft_len, k, self.T, self.top_p, self.out_tokens, self.out_len,
+                               self.out_acc, self.finished, stream=s)
+        else:
+            c.bs_verify_step(self.slots, t.bank, self.row_index, t.bank.shape[1], self.draft,
+                             self.draft_len, k, self.T, self.top_p, self.out_tokens, self.out_len,
+                             self.out_acc, stream=s)
+            c.bs_commit(self.slots, self.out_tokens, self.out_len, k, self.finished, stream=s)
 
-    LAUNCHES_PER_STEP = 5  # lookup, target rows, verify plan, verify rows, commit
+    # lookup, target rows, verify (+ fused commit; top-p < 1: plan, rows and commit kernels)
+    LAUNCHES_PER_STEP = 3
 
     def capture(self, steps: int):
         """Capture `steps` decoding steps into one CUDA graph (replayed by run_graph)."""

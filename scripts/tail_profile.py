@@ -73,12 +73,12 @@ for rl in (1, 2):
                                     eng.target.mode, eng.target.nbank, eng.row_index, stream=stream)
                 if rec:
                     ev[i][2].record(stream)
-                ctx.bs_verify_step(eng.slots, bank, eng.row_index, V, eng.draft, eng.draft_len, k,
-                                   eng.T, eng.top_p, eng.out_tokens, eng.out_len, eng.out_acc,
-                                   stream=stream)
+                ctx.bs_verify_commit(eng.slots, bank, eng.row_index, V, eng.draft, eng.draft_len, k,
+                                     eng.T, eng.top_p, eng.out_tokens, eng.out_len, eng.out_acc,
+                                     eng.finished, stream=stream)
                 if rec:
                     ev[i][3].record(stream)
-                ctx.bs_commit(eng.slots, eng.out_tokens, eng.out_len, k, eng.finished, stream=stream)
+                pass
                 if rec:
                     ev[i][4].record(stream)
     stream.synchronize()

@@ -10,7 +10,7 @@ from workloads import TargetSpec  # noqa: E402
 from tests.gpu_util import bank_numpy, pools_for, setup_rollouts, to_dev  # noqa: E402
 
 
-def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs):
+def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fused=True):
     from paper_2605_08862_b200.engine import RolloutEngine, Target
 
     ctx = bs.Context(vocab=spec.V, eos_id=eos, k_max=k, match_max=M, max_rollouts=n,
@@ -18,7 +18,8 @@ def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs):
                      seed=seed)
     bank = to_dev(bank_numpy(spec).view(np.int16))
     mode = {"position": 0, "markov": 1, "mixed": 2}[spec.mode]
-    eng = RolloutEngine(ctx, n, k, T, top_p, Target(bank, spec.nbank, spec.target_seed, mode))
+    eng = RolloutEngine(ctx, n, k, T, top_p, Target(bank, spec.nbank, spec.target_seed, mode),
+                        fused=fused)
     return ctx, eng
 
 
@@ -35,16 +36,18 @@ def _oracle_rollouts(orc, spec, pid, tail_rows, uids, ml, pools_np, k, M, T, top
     return ros
 
 
+@pytest.mark.parametrize("fused", [True, False])  # bs_verify_commit vs bs_verify_step + bs_commit
 @pytest.mark.parametrize("T,mode", [(0.0, "markov"), (1.0, "markov"), (1.0, "mixed"),
                                     (0.7, "position")])
-def test_tiny_rollouts_token_for_token(bs, orc, T, mode):
+def test_tiny_rollouts_token_for_token(bs, orc, T, mode, fused):
     """TINY config: V=1024, 4 rollouts of one prompt, k=4, 64-token responses."""
     spec = TargetSpec(V=1024, nbank=256, mode=mode, beta=6.0)
     M, k, L, seed, eos = 16, 4, 64, 5, 1023
     prompts, tails, pid, tail_rows, uids, ml = setup_rollouts(spec, 1, 4, M, L)
     pools_np = pools_for(spec, prompts, tails, 4, np.full(4, 60), 0.85, prefix=M)
     n = len(pid)
-    ctx, eng = _engine(bs, spec, n, k, M, T, 1.0, seed, eos, len(pools_np[2]), len(pools_np[0]))
+    ctx, eng = _engine(bs, spec, n, k, M, T, 1.0, seed, eos, len(pools_np[2]), len(pools_np[0]),
+                       fused=fused)
     resp = torch.full((n, L), -1, dtype=torch.int32, device="cuda")
     ctx.bs_rollout_bind_output(resp, L)
     eng.put_pools(1, to_dev(pools_np[0]), to_dev(pools_np[1]), to_dev(pools_np[2]))
