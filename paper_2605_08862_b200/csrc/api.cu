@@ -122,6 +122,7 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     cudaMemset(c->dev_err.p, 0, sizeof(uint32_t));
     cudaMemset(c->vctl.p, 0, VCTL_WORDS * sizeof(unsigned int));
     cudaMemset(c->vnext_row.p, 0, R * sizeof(unsigned long long));
+    cudaMemset(c->vlive.p, 0, R * sizeof(unsigned long long));
     {  // scheduler epoch starts at 1: zeroed claim counters (epoch 0) read as unplanned
         const unsigned int one = 1u;
         cudaMemcpy(c->vctl.p + SC_EPOCH, &one, sizeof one, cudaMemcpyHostToDevice);

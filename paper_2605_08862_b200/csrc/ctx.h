@@ -30,8 +30,9 @@ enum : int { VCTL_NEXT = 0, VCTL_NACTIVE = 1, VCTL_MODE = 2, VCTL_ROWS = 3 };
 // Scheduler words of the cluster verify kernel (verify_cluster.cuh): static cursor,
 // rollouts done, CTAs exited, launch epoch.  All but the epoch are zero between launches
 // (the last CTA out resets them).
+// SC_NLIVE / SC_PLANNED form one 64-bit word (live count low, planned count high).
 enum : int {
-    SC_STATIC = 8, SC_NLIVE = 9, SC_PLANNED = 10, SC_DONE = 13, SC_EXIT = 14, SC_EPOCH = 15,
+    SC_STATIC = 8, SC_NLIVE = 10, SC_PLANNED = 11, SC_DONE = 13, SC_EXIT = 14, SC_EPOCH = 15,
     VCTL_WORDS = 16
 };
 
@@ -141,7 +142,7 @@ struct bs_ctx {
     // row) and per-rollout plan records
     bs::DevBuf<unsigned long long> vnext_row;
     bs::DevBuf<bs::RollRec> vrrec;
-    bs::DevBuf<int32_t> vlive;  // the launch's live rollouts (compacted by the planners)
+    bs::DevBuf<unsigned long long> vlive;  // live rollouts (epoch << 32 | b), compacted by the planners
     bs::DevBuf<unsigned long long> stats;  // STAT_COUNT counters
     int32_t* responses = nullptr;           // optional [max_rollouts, resp_stride] output
     int64_t resp_stride = 0;

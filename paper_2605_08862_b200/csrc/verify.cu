@@ -94,7 +94,7 @@ __device__ __forceinline__ void trace_ev(int type, int seq, int b, int j) {
     } while (0)
 #endif
 enum { TR_CLAIM0 = 0, TR_CLAIM1 = 1, TR_TMA = 2, TR_MAX0 = 3, TR_MAX1 = 4, TR_MASS0 = 5, TR_MASS1 = 6,
-       TR_EPI0 = 7, TR_EPI1 = 8, TR_END = 9, TR_FIN = 10, TR_SPINS = 11, TR_SC = 12, TR_SQPOP = 13, TR_ITER = 14, TR_MASSL = 15 };
+       TR_EPI0 = 7, TR_EPI1 = 8, TR_END = 9, TR_FIN = 10, TR_SPINS = 11, TR_SC = 12, TR_SQPOP = 13, TR_ITER = 14, TR_MASSL = 15, TR_START = 16, TR_GO = 17, TR_PLANNED = 18 };
 
 
 struct VerifyArgs {
@@ -132,7 +132,7 @@ struct VerifyArgs {
     unsigned int* sctl;           // vctl words SC_*
     unsigned long long* next_row; // per rollout: epoch << 32 | next unclaimed row
     RollRec* rrec;                // per rollout: the launch's plan
-    int32_t* live;                // the launch's live rollouts (compacted by the planners)
+    unsigned long long* live;     // live rollouts (epoch << 32 | b), compacted by the planners
     // fused commit (bs_verify_commit): the finalizing thread appends the rollout's tokens
     int commit, M;
     int32_t* c_tail;

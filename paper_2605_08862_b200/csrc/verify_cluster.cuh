@@ -125,12 +125,15 @@ __device__ void ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
             }
             atomicAdd(a.sctl + SC_DONE, 1u);
         }
-        __threadfence();
-        // publish the plan: claim word = epoch << 32 | (q + 1) << 24 | next row (0)
+        // publish the plan (release: the record and resets above first): claim word =
+        // epoch << 32 | (q + 1) << 24 | next row (0)
         st_release_u64(a.next_row + b, ((unsigned long long)epoch << 32) | ((unsigned long long)(q + 1) << 24));
-        if (q >= 0) a.live[atomicAdd(a.sctl + SC_NLIVE, 1u)] = b;
-        __threadfence();
-        atomicAdd(a.sctl + SC_PLANNED, 1u);
+        // one atomic counts the planned rollout (high half) and, if live, takes its live-list
+        // slot (low half); the tagged entry is published after it
+        const unsigned long long cnt = atomicAdd(reinterpret_cast<unsigned long long*>(a.sctl + SC_NLIVE),
+                                                 (1ull << 32) | (q >= 0 ? 1ull : 0ull));
+        if (q >= 0) st_release_u64(a.live + (uint32_t)cnt, ((unsigned long long)epoch << 32) | (uint32_t)b);
+        TRACE(TR_PLANNED, 0, b, 0);
     }
 }
 
@@ -312,8 +315,13 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
         // the static list is the live rollouts, compacted by the planners: wait for the plan
         int nl = 0;
         if (lane == 0) {
-            while ((int)ld_acquire_u32(a.sctl + SC_PLANNED) < n) __nanosleep(64);
-            nl = (int)ld_relaxed_u32(a.sctl + SC_NLIVE);
+            const unsigned long long* w = reinterpret_cast<const unsigned long long*>(a.sctl + SC_NLIVE);
+            unsigned long long v = ld_acquire_u64(w);
+            while ((int)(v >> 32) < n) {
+                __nanosleep(32);
+                v = ld_acquire_u64(w);
+            }
+            nl = (int)(uint32_t)v;
         }
         cs.nlive = __shfl_sync(0xFFFFFFFFu, nl, 0);
         // eager when every live row fits in flight at once (two per cluster): the static
@@ -347,7 +355,12 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
             if (lane == 0 && (int)ld_relaxed_u32(a.sctl + SC_STATIC) < nstatic) {
                 const int s = (int)atomicAdd(a.sctl + SC_STATIC, 1u);
                 if (s < nstatic) {
-                    b = __ldcg(a.live + s % nlive);
+                    unsigned long long e = ld_acquire_u64(a.live + s % nlive);
+                    while ((uint32_t)(e >> 32) != epoch) {  // slot taken, entry not yet published
+                        __nanosleep(32);
+                        e = ld_acquire_u64(a.live + s % nlive);
+                    }
+                    b = (int)(uint32_t)e;
                     j = s / nlive;
                 }
             }
@@ -438,12 +451,18 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
     for (int i = tid; i < STAT_COUNT; i += CK_NT) sh.stat[i] = 0ull;
     if (tid == 0) sh.mail = -1;
 #ifdef BS_TRACE
-    if (tid == 0) s_trace_n = 0;
+    if (tid == 0) {
+        s_trace_n = 0;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        TRACE(TR_START, 0, (int)smid, 0);
+    }
 #endif
     cluster.sync();  // every CTA's barriers exist before any remote operation
     pdl_wait();      // (the prologue above overlaps the previous kernel's tail)
     pdl_trigger();
     const uint32_t epoch = ld_relaxed_u32(a.sctl + SC_EPOCH);
+    if (tid == 0) TRACE(TR_GO, 0, 0, 0);
     if (warp < CK_NMW)  // plan the call's rollouts, one warp each, before any row work
         for (int b = (int)blockIdx.x * CK_NMW + warp; b < a.n; b += (int)gridDim.x * CK_NMW)
             ck_plan(a, epoch, b, lane);

@@ -25,6 +25,7 @@ ap.add_argument("--k", type=int, default=8)
 ap.add_argument("--iters", type=int, default=6)
 ap.add_argument("--nbank", type=int, default=8192)
 ap.add_argument("--bench", type=int, default=0, help="trace the bench q7 loop after this many decode steps")
+ap.add_argument("--live", type=int, default=0, help="synthetic: only this many live rollouts (rest finished)")
 a = ap.parse_args()
 V, n, k = a.V, a.n, a.k
 lib = bs.load()
@@ -76,10 +77,12 @@ else:
     ctx = bs.Context(vocab=V, k_max=k, match_max=32, max_rollouts=n, pool_capacity_tokens=16,
                      pool_capacity_seqs=4, seed=1)
     slots = torch.arange(n, dtype=torch.int32, device="cuda")
+    mlen = torch.full((n,), 1 << 30, dtype=torch.int32, device="cuda")
+    if a.live:
+        mlen[a.live:] = 0
     ctx.bs_rollout_begin(slots, torch.arange(n, dtype=torch.int64, device="cuda"),
                          torch.zeros(n, dtype=torch.int32, device="cuda"),
-                         torch.zeros((n, 32), dtype=torch.int32, device="cuda"),
-                         torch.full((n,), 1 << 30, dtype=torch.int32, device="cuda"))
+                         torch.zeros((n, 32), dtype=torch.int32, device="cuda"), mlen)
     rng = np.random.default_rng(0)
     rows = rng.integers(0, a.nbank, (a.iters, n, k + 1))
     peaks = bank_peak(1, rows.reshape(-1), V).reshape(rows.shape)
@@ -101,7 +104,8 @@ else:
         m = lib.bsx_trace_read(buf.ctypes.data, 1 << 20, 1)
         res.append((s.elapsed_time(e), m, buf[:m].copy(), int(st1[6] - st0[6]), int(st1[7] - st0[7])))
 
-names = ["claim0", "claim1", "tma", "max0", "max1", "mass0", "mass1", "epi0", "epi1", "end", "fin", "spins", "sc", "sqpop", "iter", "massl"]
+names = ["claim0", "claim1", "tma", "max0", "max1", "mass0", "mass1", "epi0", "epi1", "end", "fin", "spins", "sc",
+         "sqpop", "iter", "massl", "start", "go", "planned"]
 ms, m, ev, rv, rn = res[-1]
 blk = ev[:, 0] & 0xFFFF
 typ = (ev[:, 0] >> 16) & 0xFF
@@ -246,3 +250,22 @@ if os.environ.get("TRACE_MASS"):
                 late[w_] += tt - m0
                 cnt[w_] += 1
     print("  mass loop lateness by warp (us):", " ".join(f"w{w_}:{late[w_] / max(1, cnt[w_]):.2f}" for w_ in range(8)))
+
+if os.environ.get("TRACE_PHASES"):
+    def tmin(ty):
+        v = t[typ == ty]
+        return (v.min(), v.max()) if len(v) else (float("nan"), float("nan"))
+    for ty, nm in [(16, "CTA start"), (17, "past pdl_wait"), (18, "rollout planned"), (1, "claim end"),
+                   (2, "TMA issue"), (8, "epilogue end"), (10, "finalize"), (9, "CTA exit")]:
+        lo, hi = tmin(ty)
+        print(f"  {nm:16s} first {lo:7.2f}  last {hi:7.2f} us")
+if os.environ.get("TRACE_SM"):
+    sm = {int(bk): int(b_) for ty, bk, b_ in zip(typ, blk, bb) if ty == 16}
+    from collections import Counter
+    occ = Counter(sm.values())
+    ncl = max(sm) // 8 + 1
+    print(f"  CTAs {len(sm)}, SMs used {len(occ)}, doubly occupied {sum(1 for v in occ.values() if v > 1)}")
+    for c in range(min(ncl, 12)):
+        sms = [sm.get(8 * c + r, -1) for r in range(8)]
+        partners = sorted({bk // 8 for bk, s_ in sm.items() if s_ in sms and bk // 8 != c})
+        print(f"  cluster {c:2d}: SMs {sms} shares with clusters {partners}")
