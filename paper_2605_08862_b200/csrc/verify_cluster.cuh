@@ -51,6 +51,7 @@ struct CkShared {
     uint4 csum[CK_D][CK_CL];  // per CTA: {slice mass sum lo, hi, mass(d) lo, hi}
     uint4 erec[CK_D];         // mass warps -> epilogue: {m bits, bad, greedy index, 0}
     int mail;  // leader: (rollout << 8 | row) the epilogue found needed next, or -1
+    int plan_b[CK_NMW];  // planning round: rollout per mass warp (-1 dead, -2 none)
     float wmax[CK_NXW];
     uint32_t wbad[CK_NXW];
     int32_t widx[CK_NXW];
@@ -84,13 +85,18 @@ __host__ __device__ constexpr size_t ck_smem_bytes(int SL) {
 // every rollout of the call is finalized.
 constexpr int SRC_NONE = 0, SRC_READY = 1, SRC_STATIC = 2, SRC_SPEC = 3;
 
-__device__ void ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
+// Returns whether rollout b is live (has rows); the caller counts and lists it per CTA.
+__device__ bool ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
     const int kp1 = a.k + 1;
+    // loads that depend on b only go out with the slot lookup (one round trip)
     const int sl = a.slots[b];
+    const int dlen = a.draft_len[b];
+    const int tk = (lane < a.k) ? a.draft[(int64_t)b * a.k + lane] : 0;
+    const long long rowno0 = (lane == 0) ? (a.row_index ? a.row_index[(int64_t)b * kp1] : (int64_t)b * kp1) : 0;
     const int p = a.pos[sl], L = a.max_len[sl];
     int q = -1;
-    if (!a.finished[sl] && p < L) q = min(max(a.draft_len[b], 0), min(a.k, L - p - 1));
-    const int t = (lane < q) ? a.draft[(int64_t)b * a.k + lane] : 0;
+    if (!a.finished[sl] && p < L) q = min(max(dlen, 0), min(a.k, L - p - 1));
+    const int t = (lane < q) ? tk : 0;
     if (q > 0 && __any_sync(0xFFFFFFFFu, lane < q && (t < 0 || t >= a.V))) {
         q = -1;
         if (lane == 0) atomicOr(a.dev_err, DEV_BAD_DRAFT);
@@ -108,7 +114,7 @@ __device__ void ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
         rr.pos = p;
         rr.tag = (int32_t)epoch;
         rr.uid = a.uid[sl];
-        rr.rowno0 = a.row_index ? a.row_index[(int64_t)b * kp1] : (int64_t)b * kp1;
+        rr.rowno0 = rowno0;
         rr.d0 = q > 0 ? d0 : -1;
         rr.aligned0 = ((reinterpret_cast<uintptr_t>(a.logits + rr.rowno0 * a.stride) & 15u) == 0) ? 1 : 0;
         rr.pad[0] = rr.pad[1] = 0;
@@ -128,13 +134,9 @@ __device__ void ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
         // publish the plan (release: the record and resets above first): claim word =
         // epoch << 32 | (q + 1) << 24 | next row (0)
         st_release_u64(a.next_row + b, ((unsigned long long)epoch << 32) | ((unsigned long long)(q + 1) << 24));
-        // one atomic counts the planned rollout (high half) and, if live, takes its live-list
-        // slot (low half); the tagged entry is published after it
-        const unsigned long long cnt = atomicAdd(reinterpret_cast<unsigned long long*>(a.sctl + SC_NLIVE),
-                                                 (1ull << 32) | (q >= 0 ? 1ull : 0ull));
-        if (q >= 0) st_release_u64(a.live + (uint32_t)cnt, ((unsigned long long)epoch << 32) | (uint32_t)b);
         TRACE(TR_PLANNED, 0, b, 0);
     }
+    return q >= 0;
 }
 
 // Row r of rollout b as a descriptor (lane-uniform inputs; every lane computes it).
@@ -214,36 +216,40 @@ __device__ __forceinline__ bool ck_take(const VerifyArgs& a, uint32_t epoch, int
 
 // Eager mode: row j of rollout b from the static cursor (each row enumerated exactly once).
 __device__ __forceinline__ bool ck_take_row(const VerifyArgs& a, int b, int j, int lane, RowDesc& out) {
+    // every load is independent: lanes 0-3 fetch roll_first, the record, the draft token and
+    // the logits row in one round trip
     const RollRec* rp = a.rrec + b;
-    int valid = 0, q = 0, p = 0, d = -1, al = 0;
+    const int kp1 = a.k + 1;
+    int rf = -1, q = 0, p = 0, d0 = -1, al0 = 0, dj = -1;
     unsigned long long u = 0;
-    long long rn = 0;
-    if (lane == 0) {
+    long long rn0 = 0, rnj = 0;
+    if (lane == 0) rf = ld_volatile_i32(a.roll_first + b);
+    if (lane == 1) {
         q = __ldcg(&rp->q);
-        valid = (j <= q && j <= ld_volatile_i32(a.roll_first + b)) ? 1 : 0;
-        if (valid) {
-            p = __ldcg(&rp->pos);
-            u = __ldcg(&rp->uid);
-            if (j == 0) {
-                d = __ldcg(&rp->d0);
-                rn = __ldcg(&rp->rowno0);
-                al = __ldcg(&rp->aligned0);
-            } else {
-                const int kp1 = a.k + 1;
-                d = (j < q) ? a.draft[(int64_t)b * a.k + j] : -1;
-                rn = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
-                al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
-            }
-        }
+        p = __ldcg(&rp->pos);
+        u = __ldcg(&rp->uid);
+        d0 = __ldcg(&rp->d0);
+        rn0 = __ldcg(&rp->rowno0);
+        al0 = __ldcg(&rp->aligned0);
     }
-    valid = __shfl_sync(0xFFFFFFFFu, valid, 0);
-    if (!valid) return false;
-    q = __shfl_sync(0xFFFFFFFFu, q, 0);
-    d = __shfl_sync(0xFFFFFFFFu, d, 0);
-    p = __shfl_sync(0xFFFFFFFFu, p, 0);
-    al = __shfl_sync(0xFFFFFFFFu, al, 0);
-    u = shfl_u64(u, 0);
-    rn = (long long)shfl_u64((unsigned long long)rn, 0);
+    if (lane == 2 && j >= 1 && j < a.k) dj = a.draft[(int64_t)b * a.k + j];
+    if (lane == 3 && j >= 1) rnj = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+    rf = __shfl_sync(0xFFFFFFFFu, rf, 0);
+    q = __shfl_sync(0xFFFFFFFFu, q, 1);
+    if (!(j <= q && j <= rf)) return false;
+    p = __shfl_sync(0xFFFFFFFFu, p, 1);
+    u = shfl_u64(u, 1);
+    int d, al;
+    long long rn;
+    if (j == 0) {
+        d = __shfl_sync(0xFFFFFFFFu, d0, 1);
+        rn = (long long)shfl_u64((unsigned long long)rn0, 1);
+        al = __shfl_sync(0xFFFFFFFFu, al0, 1);
+    } else {
+        d = (j < q) ? __shfl_sync(0xFFFFFFFFu, dj, 2) : -1;
+        rn = (long long)shfl_u64((unsigned long long)rnj, 3);
+        al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
+    }
     out = ck_desc(b, j, q, d, p, u, rn, al, j == 0 ? SRC_STATIC : SRC_SPEC);
     return true;
 }
@@ -304,6 +310,7 @@ struct ClaimState {
     bool eager = false;
     bool static_done = false;  // the static cursor is exhausted
     int spec_b = -1, spec_r = 0;  // chain this cluster just continued: speculate its next row
+    bool placed = false;
 };
 
 __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool queues, int rot,
@@ -311,10 +318,12 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
     const int n = a.n;
     uint64_t t_spin0 = 0;
     RowDesc out;
+    int early = -1;  // first static ticket, taken while the plan is still being built
     if (cs.nlive < 0) {
         // the static list is the live rollouts, compacted by the planners: wait for the plan
         int nl = 0;
         if (lane == 0) {
+            early = (int)atomicAdd(a.sctl + SC_STATIC, 1u);
             const unsigned long long* w = reinterpret_cast<const unsigned long long*>(a.sctl + SC_NLIVE);
             unsigned long long v = ld_acquire_u64(w);
             while ((int)(v >> 32) < n) {
@@ -330,6 +339,13 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
     }
     const int nlive = cs.nlive;
     const bool eager = cs.eager;
+    if (eager && !cs.placed) {
+        // clusters are placed in layers (the first half of the cluster ids on distinct SMs,
+        // the second half sharing those SMs): small batches let the first layer claim first so
+        // rows in flight do not share SMs
+        cs.placed = true;
+        if ((int)(blockIdx.x / CK_CL) >= a.ncl / 2) __nanosleep(1000);
+    }
     const int nstatic = eager ? nlive * (a.k + 1) : nlive;
     for (int spin = 0;; ++spin) {
         // 1. this cluster's own epilogue accepted row j of rollout b: row j+1 is needed and
@@ -352,8 +368,9 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
         }
         int b = -1, j = 0;
         if (!cs.static_done) {
-            if (lane == 0 && (int)ld_relaxed_u32(a.sctl + SC_STATIC) < nstatic) {
-                const int s = (int)atomicAdd(a.sctl + SC_STATIC, 1u);
+            if (lane == 0 && (early >= 0 || (int)ld_relaxed_u32(a.sctl + SC_STATIC) < nstatic)) {
+                const int s = (early >= 0) ? early : (int)atomicAdd(a.sctl + SC_STATIC, 1u);
+                early = -1;
                 if (s < nstatic) {
                     unsigned long long e = ld_acquire_u64(a.live + s % nlive);
                     while ((uint32_t)(e >> 32) != epoch) {  // slot taken, entry not yet published
@@ -463,9 +480,31 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
     pdl_trigger();
     const uint32_t epoch = ld_relaxed_u32(a.sctl + SC_EPOCH);
     if (tid == 0) TRACE(TR_GO, 0, 0, 0);
-    if (warp < CK_NMW)  // plan the call's rollouts, one warp each, before any row work
-        for (int b = (int)blockIdx.x * CK_NMW + warp; b < a.n; b += (int)gridDim.x * CK_NMW)
-            ck_plan(a, epoch, b, lane);
+    if (warp < CK_NMW) {
+        // plan the call's rollouts, one warp each, in rounds over the grid; per round one atomic
+        // per CTA counts its planned rollouts (high half of the packed word) and reserves its
+        // live-list slots (low half), so the plan's completion count is not one hot word
+        for (int base = (int)blockIdx.x * CK_NMW; base < a.n; base += (int)gridDim.x * CK_NMW) {
+            const int b = base + warp;
+            const bool live = (b < a.n) ? ck_plan(a, epoch, b, lane) : false;
+            if (lane == 0) sh.plan_b[warp] = (b < a.n) ? (live ? b : -1) : -2;
+            named_bar(3, CK_NMW * 32);
+            if (warp == 0 && lane == 0) {
+                int np = 0, nl = 0;
+                for (int w = 0; w < CK_NMW; ++w) {
+                    np += sh.plan_b[w] != -2;
+                    nl += sh.plan_b[w] >= 0;
+                }
+                const unsigned long long cnt = atomicAdd(reinterpret_cast<unsigned long long*>(a.sctl + SC_NLIVE),
+                                                         ((unsigned long long)np << 32) | (unsigned long long)nl);
+                unsigned slot = (uint32_t)cnt;
+                for (int w = 0; w < CK_NMW; ++w)
+                    if (sh.plan_b[w] >= 0)
+                        st_release_u64(a.live + slot++, ((unsigned long long)epoch << 32) | (uint32_t)sh.plan_b[w]);
+            }
+            named_bar(3, CK_NMW * 32);  // plan_b reusable
+        }
+    }
 
     if (warp == CK_PROD) {
         // ================================================================ producer

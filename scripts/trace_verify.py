@@ -269,3 +269,11 @@ if os.environ.get("TRACE_SM"):
         sms = [sm.get(8 * c + r, -1) for r in range(8)]
         partners = sorted({bk // 8 for bk, s_ in sm.items() if s_ in sms and bk // 8 != c})
         print(f"  cluster {c:2d}: SMs {sms} shares with clusters {partners}")
+if os.environ.get("TRACE_ROWS"):
+    # per working cluster (leader): stage times of its row(s)
+    for bl in sorted(set(int(x) for x in blk[(typ == 2)])):
+        if bl % 8:
+            continue
+        ev_ = sorted((float(tt), names[int(ty)], int(sq) & 0xFFF, int(b_), int(j_)) for tt, ty, sq, b_, j_, bk in
+                     zip(t, typ, seq, bb, jj, blk) if bk // 8 == bl // 8 and ty in (2, 3, 4, 5, 6, 7, 8, 10))
+        print(f"  cluster {bl // 8}:", " ".join(f"{e[1]}@{e[0]:.1f}" for e in ev_ if e[1] in ('tma', 'epi1', 'fin') or True)[:600])
