@@ -407,6 +407,21 @@ __device__ __forceinline__ bool probe(const IndexEntry* table, uint64_t mask, ui
     }
 }
 
+// HASH_B^i for the lookup's per-lane suffix hash (a warp scan of y[-1-i] * B^i).
+struct HashPow {
+    uint64_t v[32];
+};
+constexpr HashPow make_hash_pow() {
+    HashPow t{};
+    uint64_t x = 1;
+    for (int i = 0; i < 32; ++i) {
+        t.v[i] = x;
+        x *= HASH_B;
+    }
+    return t;
+}
+__constant__ HashPow c_hash_pow = make_hash_pow();
+
 __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a0) {
     pdl_wait();
     pdl_trigger();
@@ -422,17 +437,15 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a0) {
     const LookupArgs& a = a0;
     const int slot = a.slots[b];
     const int M = a.M;
+    // the slot's state and its whole tail go out together (one round trip)
     const int L = a.ctx_len[slot];
     const int P = a.prompt[slot];
     const int p = a.pos[slot], ml = a.max_len[slot];
+    const int tok_raw = (lane < M) ? a.tail[(int64_t)slot * M + (M - 1 - lane)] : -1;  // y[-1-lane]
     const bool fin = a.finished[slot] || p >= ml;
     const int mmax = min(M, L);
-    // y[-1-lane]
-    const int tok = (lane < mmax) ? a.tail[(int64_t)slot * M + (M - 1 - lane)] : -1;
-    // B^lane
-    uint64_t bp = 1;
-    for (int t = 0; t < lane; ++t) bp *= HASH_B;
-    uint64_t H = (lane < mmax) ? (uint64_t)(uint32_t)(tok + 1) * bp : 0ull;
+    const int tok = (lane < mmax) ? tok_raw : -1;
+    uint64_t H = (lane < mmax) ? (uint64_t)(uint32_t)(tok + 1) * c_hash_pow.v[lane] : 0ull;
 #pragma unroll
     for (int dd = 1; dd < 32; dd <<= 1) {
         const uint32_t lo = __shfl_up_sync(0xFFFFFFFFu, (uint32_t)H, dd);
@@ -444,35 +457,41 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a0) {
     if (!fin && lane < mmax) found = probe(x.table, x.mask, window_key(H, P, lane + 1), occ, meta);
     unsigned hit = __ballot_sync(0xFFFFFFFFu, found);
     int mstar = 0, q = 0, dstart = 0;
+    int dpre = -1;        // T[dstart + lane], prefetched when the draft is the m0 window's
+    bool dpre_ok = false;
     for (;;) {
         if (hit == 0) break;
         const int m0 = 32 - __clz(hit);  // largest stored suffix length
         const uint32_t occ0 = __shfl_sync(0xFFFFFFFFu, occ, m0 - 1);
         const uint32_t meta0 = __shfl_sync(0xFFFFFFFFu, meta, m0 - 1);
-        // verify y[-m0:] == T[occ0 .. occ0+m0) (guards a 64-bit key false positive)
-        bool okc = true;
-        if (lane < m0) okc = (x.T[(int64_t)occ0 + m0 - 1 - lane] == tok);
+        const bool uniq = (meta0 & META_UNIQUE) && (meta0 & META_CONT);
+        // one round trip: the anchor check y[-m0:] == T[occ0 .. occ0+m0) (guards a 64-bit
+        // key false positive), the continuation T[occ0+m0 ..] (the draft if this anchor wins;
+        // meta's q tokens exist) and, for a unique window, its left extension T[occ0-1-lane]
+        // and its sequence start
+        const int qm = (int)(meta0 & 0xFFu);
+        const int tchk = (lane < m0) ? x.T[(int64_t)occ0 + m0 - 1 - lane] : 0;
+        const int tcont = (lane < qm) ? x.T[(int64_t)occ0 + m0 + lane] : -1;
+        const int text = (uniq && (int64_t)occ0 - 1 - lane >= 0) ? x.T[(int64_t)occ0 - 1 - lane] : -2;
+        const int sstart = uniq ? x.seq_start_of[occ0] : 0;
+        const bool okc = (lane >= m0) || (tchk == tok);
         if (!__all_sync(0xFFFFFFFFu, okc)) {
             hit &= ~(1u << (m0 - 1));
             continue;
         }
-        if ((meta0 & META_UNIQUE) && (meta0 & META_CONT)) {
+        if (uniq) {
             // unique occurrence: extend the anchor to the left within its sequence
-            const int sstart = x.seq_start_of[occ0];
             const int jj = lane;  // compare y[-m0-1-jj] with T[occ0-1-jj]
+            const int yt = __shfl_sync(0xFFFFFFFFu, tok_raw, (m0 + jj) & 31);
             bool eq = false;
-            if (m0 + jj < mmax) {
-                const int64_t pp = (int64_t)occ0 - 1 - jj;
-                if (pp >= sstart) {
-                    const int yt = a.tail[(int64_t)slot * M + (M - 1 - (m0 + jj))];
-                    eq = (x.T[pp] == yt);
-                }
-            }
+            if (m0 + jj < mmax && (int64_t)occ0 - 1 - jj >= sstart) eq = (text == yt);
             const unsigned eqm = __ballot_sync(0xFFFFFFFFu, eq);
             const int ext = (~eqm == 0u) ? 32 : (__ffs(~eqm) - 1);
             mstar = m0 + ext;
-            q = (int)(meta0 & 0xFFu);
+            q = qm;
             dstart = (int)occ0 + m0;
+            dpre = tcont;
+            dpre_ok = true;
             break;
         }
         // longest stored suffix with a continuation (non-unique entries, <= m0)
@@ -504,7 +523,7 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a0) {
     }
     q = min(q, a.k);
     q = min(q, max(0, ml - p - 1));
-    if (lane < a.k) a.draft[(int64_t)b * a.k + lane] = (lane < q) ? x.T[(int64_t)dstart + lane] : -1;
+    if (lane < a.k) a.draft[(int64_t)b * a.k + lane] = (lane < q) ? (dpre_ok ? dpre : x.T[(int64_t)dstart + lane]) : -1;
     if (lane == 0) {
         a.draft_len[b] = q;
         if (a.match_len) a.match_len[b] = mstar;
