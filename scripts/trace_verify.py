@@ -277,3 +277,50 @@ if os.environ.get("TRACE_ROWS"):
         ev_ = sorted((float(tt), names[int(ty)], int(sq) & 0xFFF, int(b_), int(j_)) for tt, ty, sq, b_, j_, bk in
                      zip(t, typ, seq, bb, jj, blk) if bk // 8 == bl // 8 and ty in (2, 3, 4, 5, 6, 7, 8, 10))
         print(f"  cluster {bl // 8}:", " ".join(f"{e[1]}@{e[0]:.1f}" for e in ev_ if e[1] in ('tma', 'epi1', 'fin') or True)[:600])
+if os.environ.get("TRACE_BUSY"):
+    # mass-warp busy fraction per CTA over time windows (warp 0's MASS0 -> MASSL)
+    m0 = {}
+    busy = []
+    for tt, ty, sq, b_, bk in zip(t, typ, seq, bb, blk):
+        if ty == 5 and int(b_) == 0:
+            m0[(int(bk), int(sq))] = float(tt)
+        if ty == 15 and int(b_) == 0 and (int(bk), int(sq)) in m0:
+            busy.append((m0[(int(bk), int(sq))], float(tt)))
+    span = t[typ == 9].max()
+    ncta = len(set(int(x) for x in blk))
+    for x in np.arange(0, span, 10.0):
+        occ = sum(max(0.0, min(e_, x + 10) - max(s_, x)) for s_, e_ in busy)
+        print(f"  t={x:6.1f}: mass warps busy {100 * occ / (10.0 * ncta):5.1f}% of CTA time")
+if os.environ.get("TRACE_GAPS"):
+    # per leader CTA: consecutive rows i, i+1 -> mass idle gap and what row i+1 waited for
+    ev = {}
+    for tt, ty, sq, b_, bk in zip(t, typ, seq, bb, blk):
+        if int(bk) % 8:
+            continue
+        k_ = (int(ty), int(bk), int(sq) & 0xFFF)
+        if int(ty) in (5, 15) and int(b_) != 0:
+            continue  # warp 0 only for mass events
+        ev.setdefault(k_, float(tt))
+    gaps, wmax, wtma, wclaim = [], [], [], []
+    for (ty, bk, sq), tt in ev.items():
+        if ty != 6:  # mass1 of row sq
+            continue
+        nxt = ev.get((5, bk, sq + 1))
+        if nxt is None:
+            continue
+        gaps.append(nxt - tt)
+        mx1 = ev.get((4, bk, sq + 1))
+        tma1 = ev.get((2, bk, sq + 1))
+        prev_end = ev.get((6, bk, sq - 1))
+        cl = ev.get((1, bk, sq + 1))
+        if mx1 is not None:
+            wmax.append(mx1 - tt)
+        if tma1 is not None and prev_end is not None:
+            wtma.append(tma1 - prev_end)
+        if cl is not None and prev_end is not None:
+            wclaim.append(cl - prev_end)
+    q = lambda v: f"median {np.median(v):6.2f} p75 {np.percentile(v, 75):6.2f} p90 {np.percentile(v, 90):6.2f}" if v else "-"
+    print("  mass idle gap (next mass0 - mass1):", q(gaps))
+    print("  next max1 - mass1 (>0: waiting for max):", q(wmax))
+    print("  next TMA issue - previous-row mass1 (buffer free):", q(wtma))
+    print("  next claim end - previous-row mass1:", q(wclaim))
