@@ -80,8 +80,10 @@ __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t phase, bool 
     for (uint32_t it = 1;; ++it) {
         if (cluster ? mbar_try_wait_cluster(bar, phase) : mbar_try_wait(bar, phase)) return;
         if ((it & 15u) == 0 && globaltimer_ns() - t0 > 3000000000ull) {
+#ifdef BS_TRACE
             printf("bs watchdog: block %d thread %d mbarrier smem+0x%x phase %u\n", (int)blockIdx.x,
                    (int)threadIdx.x, smem_u32(bar), phase);
+#endif
             __trap();
         }
     }

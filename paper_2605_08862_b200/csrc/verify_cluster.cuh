@@ -158,47 +158,60 @@ __device__ __forceinline__ RowDesc ck_desc(int b, int j, int q, int d, int pos, 
 
 // Claim the next row of rollout b (lane 0 computes, the warp receives the descriptor).
 // Returns false when the claim is not needed (decided below / beyond q / unplanned).
-__device__ __forceinline__ bool ck_take(const VerifyArgs& a, uint32_t epoch, int b, int src, int lane,
-                                        int rpred, RowDesc& out) {
-    // lane 0 claims; lanes 1-3 fetch, meanwhile, the record, roll_first and the predicted
-    // row's draft token / logits row (prediction: the counter value the scan saw)
-    const int kp1 = a.k + 1;
-    const RollRec* rp = a.rrec + b;
+// A row claim in flight: lane 0 holds the claim counter's old value, lane 1 the record and
+// roll_first, lanes 2-3 the predicted row's draft token / logits row.  Issued early (the
+// loads complete asynchronously), finished when the row is needed.
+struct TakeIssue {
+    int b = -1, rpred = 0;
     unsigned long long old = 0;
     int rf = -1, q = 0, p = 0, d0 = -1, al0 = 0, dpred = -1;
     unsigned long long u = 0;
     long long rn0 = 0, rnpred = 0;
-    if (lane == 0) old = atomicAdd(a.next_row + b, 1ull);
+};
+
+__device__ __forceinline__ TakeIssue ck_take_issue(const VerifyArgs& a, int b, int lane, int rpred) {
+    TakeIssue t;
+    t.b = b;
+    t.rpred = rpred;
+    const int kp1 = a.k + 1;
+    const RollRec* rp = a.rrec + b;
+    if (lane == 0) t.old = atomicAdd(a.next_row + b, 1ull);
     if (lane == 1) {  // L2 reads (published by another SM this launch)
-        rf = ld_volatile_i32(a.roll_first + b);
-        q = __ldcg(&rp->q);
-        p = __ldcg(&rp->pos);
-        u = __ldcg(&rp->uid);
-        d0 = __ldcg(&rp->d0);
-        rn0 = __ldcg(&rp->rowno0);
-        al0 = __ldcg(&rp->aligned0);
+        t.rf = ld_volatile_i32(a.roll_first + b);
+        t.q = __ldcg(&rp->q);
+        t.p = __ldcg(&rp->pos);
+        t.u = __ldcg(&rp->uid);
+        t.d0 = __ldcg(&rp->d0);
+        t.rn0 = __ldcg(&rp->rowno0);
+        t.al0 = __ldcg(&rp->aligned0);
     }
-    if (lane == 2 && rpred >= 1 && rpred <= a.k) dpred = a.draft[(int64_t)b * a.k + min(rpred, a.k - 1)];
+    if (lane == 2 && rpred >= 1 && rpred <= a.k) t.dpred = a.draft[(int64_t)b * a.k + min(rpred, a.k - 1)];
     if (lane == 3 && rpred >= 1 && rpred <= a.k)
-        rnpred = a.row_index ? a.row_index[(int64_t)b * kp1 + rpred] : (int64_t)b * kp1 + rpred;
-    old = shfl_u64(old, 0);
-    rf = __shfl_sync(0xFFFFFFFFu, rf, 1);
+        t.rnpred = a.row_index ? a.row_index[(int64_t)b * kp1 + rpred] : (int64_t)b * kp1 + rpred;
+    return t;
+}
+
+__device__ __forceinline__ bool ck_take_finish(const VerifyArgs& a, uint32_t epoch, const TakeIssue& t, int src,
+                                               int lane, RowDesc& out) {
+    const int kp1 = a.k + 1, b = t.b;
+    const unsigned long long old = shfl_u64(t.old, 0);
+    const int rf = __shfl_sync(0xFFFFFFFFu, t.rf, 1);
     const int r = (int)(uint32_t)(old & 0xFFFFFFu);
     const bool valid = (uint32_t)(old >> 32) == epoch && r <= rf;
     if (!valid) return false;
-    q = __shfl_sync(0xFFFFFFFFu, q, 1);
-    p = __shfl_sync(0xFFFFFFFFu, p, 1);
-    u = shfl_u64(u, 1);
+    const int q = __shfl_sync(0xFFFFFFFFu, t.q, 1);
+    const int p = __shfl_sync(0xFFFFFFFFu, t.p, 1);
+    const unsigned long long u = shfl_u64(t.u, 1);
     int d = -1, al = 0;
     long long rn = 0;
     if (r == 0) {
-        d = __shfl_sync(0xFFFFFFFFu, d0, 1);
-        rn = (long long)shfl_u64((unsigned long long)rn0, 1);
-        al = __shfl_sync(0xFFFFFFFFu, al0, 1);
+        d = __shfl_sync(0xFFFFFFFFu, t.d0, 1);
+        rn = (long long)shfl_u64((unsigned long long)t.rn0, 1);
+        al = __shfl_sync(0xFFFFFFFFu, t.al0, 1);
     } else {
-        if (r == rpred) {
-            d = __shfl_sync(0xFFFFFFFFu, dpred, 2);
-            rn = (long long)shfl_u64((unsigned long long)rnpred, 3);
+        if (r == t.rpred) {
+            d = __shfl_sync(0xFFFFFFFFu, t.dpred, 2);
+            rn = (long long)shfl_u64((unsigned long long)t.rnpred, 3);
         } else {
             if (lane == 0) {
                 d = (r < q) ? a.draft[(int64_t)b * a.k + r] : -1;
@@ -212,6 +225,11 @@ __device__ __forceinline__ bool ck_take(const VerifyArgs& a, uint32_t epoch, int
     }
     out = ck_desc(b, r, q, d, p, u, rn, al, src);
     return true;
+}
+
+__device__ __forceinline__ bool ck_take(const VerifyArgs& a, uint32_t epoch, int b, int src, int lane,
+                                        int rpred, RowDesc& out) {
+    return ck_take_finish(a, epoch, ck_take_issue(a, b, lane, rpred), src, lane, out);
 }
 
 // Eager mode: row j of rollout b from the static cursor (each row enumerated exactly once).
@@ -310,20 +328,39 @@ struct ClaimState {
     bool eager = false;
     bool static_done = false;  // the static cursor is exhausted
     int spec_b = -1, spec_r = 0;  // chain this cluster just continued: speculate its next row
-    bool placed = false;
+    int sidx = 0;              // next entry of this cluster's share of the static list
+    int pre_idx = -1;          // prefetched entry (index, value)
+    unsigned long long pre_e = 0;
+    TakeIssue pc;              // pre-issued claim of the next static row (pc.b < 0: none)
 };
 
-__device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool queues, int rot,
+// Pre-issue the claim of this cluster's next static row if its live-list entry (prefetched)
+// is already published: the atomic and loads complete while the current row is processed.
+__device__ __forceinline__ void ck_preissue(const VerifyArgs& a, uint32_t epoch, int lane, ClaimState& cs,
+                                            int nlive, int nstatic) {
+    int b = -1;
+    if (lane == 0 && cs.sidx < nstatic && cs.pre_idx == cs.sidx && (uint32_t)(cs.pre_e >> 32) == epoch) {
+        b = (int)(uint32_t)cs.pre_e;
+        cs.sidx += a.ncl;
+        if (cs.sidx < nstatic) {
+            cs.pre_idx = cs.sidx;
+            cs.pre_e = ld_acquire_u64(a.live + cs.sidx % nlive);
+        }
+    }
+    b = __shfl_sync(0xFFFFFFFFu, b, 0);
+    if (b >= 0) cs.pc = ck_take_issue(a, b, lane, 0);
+}
+
+__device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool queues, int rot,
                             ClaimState& cs, volatile int* mail) {
     const int n = a.n;
     uint64_t t_spin0 = 0;
     RowDesc out;
-    int early = -1;  // first static ticket, taken while the plan is still being built
+    const int cid = (int)(blockIdx.x / CK_CL);
     if (cs.nlive < 0) {
         // the static list is the live rollouts, compacted by the planners: wait for the plan
         int nl = 0;
         if (lane == 0) {
-            early = (int)atomicAdd(a.sctl + SC_STATIC, 1u);
             const unsigned long long* w = reinterpret_cast<const unsigned long long*>(a.sctl + SC_NLIVE);
             unsigned long long v = ld_acquire_u64(w);
             while ((int)(v >> 32) < n) {
@@ -336,16 +373,11 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
         // eager when every live row fits in flight at once (two per cluster): the static
         // list then enumerates every row, j-major, and a cluster leaves once it is exhausted
         cs.eager = a.eager_ok && (long long)cs.nlive * (a.k + 1) <= 2ll * a.ncl;
+        cs.sidx = cid;
+        cs.pre_idx = -1;
     }
     const int nlive = cs.nlive;
     const bool eager = cs.eager;
-    if (eager && !cs.placed) {
-        // clusters are placed in layers (the first half of the cluster ids on distinct SMs,
-        // the second half sharing those SMs): small batches let the first layer claim first so
-        // rows in flight do not share SMs
-        cs.placed = true;
-        if ((int)(blockIdx.x / CK_CL) >= a.ncl / 2) __nanosleep(1000);
-    }
     const int nstatic = eager ? nlive * (a.k + 1) : nlive;
     for (int spin = 0;; ++spin) {
         // 1. this cluster's own epilogue accepted row j of rollout b: row j+1 is needed and
@@ -366,19 +398,34 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
                 continue;
             }
         }
+        // 2. this cluster's share of the static list (entries cid, cid + ncl, ...: no shared
+        //    cursor); the next entry is prefetched so a static claim costs one round trip.
+        //    Other clusters' unclaimed rows 0 are stolen by the scan once a share is done.
+        // 2a. the static row whose claim was pre-issued by the previous static claim
+        if (!eager && cs.pc.b >= 0) {
+            const TakeIssue t = cs.pc;
+            cs.pc.b = -1;
+            const bool ok = ck_take_finish(a, epoch, t, SRC_STATIC, lane, out);
+            ck_preissue(a, epoch, lane, cs, nlive, nstatic);
+            if (ok) return out;
+            continue;
+        }
         int b = -1, j = 0;
         if (!cs.static_done) {
-            if (lane == 0 && (early >= 0 || (int)ld_relaxed_u32(a.sctl + SC_STATIC) < nstatic)) {
-                const int s = (early >= 0) ? early : (int)atomicAdd(a.sctl + SC_STATIC, 1u);
-                early = -1;
-                if (s < nstatic) {
-                    unsigned long long e = ld_acquire_u64(a.live + s % nlive);
-                    while ((uint32_t)(e >> 32) != epoch) {  // slot taken, entry not yet published
-                        __nanosleep(32);
-                        e = ld_acquire_u64(a.live + s % nlive);
-                    }
-                    b = (int)(uint32_t)e;
-                    j = s / nlive;
+            if (lane == 0 && cs.sidx < nstatic) {
+                const int s = cs.sidx;
+                const unsigned long long* lp = a.live + s % nlive;
+                unsigned long long e = (cs.pre_idx == s) ? cs.pre_e : ld_acquire_u64(lp);
+                while ((uint32_t)(e >> 32) != epoch) {  // entry not yet published
+                    __nanosleep(32);
+                    e = ld_acquire_u64(lp);
+                }
+                b = (int)(uint32_t)e;
+                j = s / nlive;
+                cs.sidx = s + a.ncl;
+                if (cs.sidx < nstatic) {  // prefetch the next entry of the share
+                    cs.pre_idx = cs.sidx;
+                    cs.pre_e = ld_acquire_u64(a.live + cs.sidx % nlive);
                 }
             }
             b = __shfl_sync(0xFFFFFFFFu, b, 0);
@@ -386,7 +433,13 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
         }
         if (b >= 0) {
             j = __shfl_sync(0xFFFFFFFFu, j, 0);
-            if (eager ? ck_take_row(a, b, j, lane, out) : ck_take(a, epoch, b, SRC_STATIC, lane, 0, out)) return out;
+            if (eager) {
+                if (ck_take_row(a, b, j, lane, out)) return out;
+                continue;
+            }
+            const bool ok = ck_take(a, epoch, b, SRC_STATIC, lane, 0, out);
+            ck_preissue(a, epoch, lane, cs, nlive, nstatic);
+            if (ok) return out;
             continue;
         }
         // no certain work left in the static list: speculate the chain just continued here
@@ -421,8 +474,10 @@ __device__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool 
         __nanosleep(64);
         if (spin == 0) t_spin0 = globaltimer_ns();
         if ((spin & 1023) == 1023 && lane == 0 && globaltimer_ns() - t_spin0 > 1500000000ull) {
-            printf("bs sched stall: block %d static %u done %u n %d\n", (int)blockIdx.x, a.sctl[SC_STATIC],
-                   a.sctl[SC_DONE], n);
+            // 1.5 s without claimable work: protocol bug
+#ifdef BS_TRACE
+            printf("bs sched stall: block %d done %u n %d\n", (int)blockIdx.x, a.sctl[SC_DONE], n);
+#endif
             __trap();
         }
     }
