@@ -209,6 +209,28 @@ def run_ours(args, cfg, rank, world, dist):
         return g
 
     phases = os.environ.get("BS_BENCH_PHASES")  # diagnostics: host wall per RL-step phase
+    flags = [torch.zeros(1, dtype=torch.bool).pin_memory() for _ in range(2)]
+    flag_ev = [torch.cuda.Event() for _ in range(2)]
+
+    def replay_until_done(g):
+        """Replay the decode graph until every rollout finished.  The all-finished flag of
+        chunk c is copied to pinned memory and checked while chunk c+1 already runs, so the
+        GPU does not idle on the host round trip (one extra, all-finished chunk at the end)."""
+        steps = 0
+        with torch.cuda.stream(stream):
+            g.replay()
+            steps += chunk
+            c = 0
+            while True:
+                flags[c % 2].copy_(eng.finished.all().view(1), non_blocking=True)
+                flag_ev[c % 2].record(stream)
+                g.replay()
+                steps += chunk
+                flag_ev[c % 2].synchronize()
+                if bool(flags[c % 2][0]):
+                    break
+                c += 1
+        return steps
 
     def rl_step(s, rec, instrument=False):
         d = dins[s]
@@ -231,23 +253,25 @@ def run_ours(args, cfg, rank, world, dist):
         mark()
         rec["launches"] += 2 + rec["seal_launches"]
         steps, chunks = 0, 0
-        while True:
-            with torch.cuda.stream(stream):
-                g.replay()
-                done = bool(eng.finished.all().item())  # one host sync per chunk
-            steps += chunk
-            if instrument:
+        if instrument:  # events are re-recorded by every replay: one chunk at a time
+            while True:
+                with torch.cuda.stream(stream):
+                    g.replay()
+                    done = bool(eng.finished.all().item())  # one host sync per chunk
+                steps += chunk
                 vt = sum(ev_s[i].elapsed_time(ev_e[i]) for i in range(chunk))
                 rec["verify_ms"] += vt
                 if chunks == 0:
                     rec["verify_ms_steady"] += vt
                     rec["steady_steps"] += chunk
-            chunks += 1
-            if done:
-                break
+                chunks += 1
+                if done:
+                    break
+        else:  # the finished check of chunk c overlaps the replay of chunk c+1
+            steps += replay_until_done(g)
+        mark()
         rec["decode_steps"] += steps
         rec["launches"] += steps * RolloutEngine.LAUNCHES_PER_STEP
-        mark()
         if phases:
             dt = [1e3 * (b - a) for a, b in zip(tp, tp[1:])]
             log("[phases ms] put %.1f seal %.1f begin %.1f capture %.1f decode %.1f" % tuple(dt[:5]))
@@ -310,7 +334,7 @@ def run_ours(args, cfg, rank, world, dist):
     steady_ms = sum(ev_s[i].elapsed_time(ev_e[i]) for i in range(chunk))
     sst = eng.stats(reset=True)
     # ---- e2e: the same RL steps through the public API from pinned HOST buffers
-    e2e = run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, dist)
+    e2e = run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, dist, replay_until_done)
     # ---- gather over ranks
     import torch as _t
 
@@ -332,7 +356,7 @@ def run_ours(args, cfg, rank, world, dist):
                 steady_ms=steady_ms, sst=sst, e2e=e2e, e2e_ms=e2e_ms_all, e2e_tokens=e2e_tok_all)
 
 
-def run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, dist):
+def run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, dist, replay_until_done):
     """End-to-end through the public API: every RL step copies its inputs host->device from
     pinned memory (pools, prompt tails, uids, lengths) and reads the generated responses
     back device->host, inside the timed region."""
@@ -368,11 +392,7 @@ def run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, 
             eng.seal(s)
             eng.begin(d["uids"], d["pid"], d["tails"], d["max_len"])
         g = capture()
-        while True:
-            with torch.cuda.stream(stream):
-                g.replay()
-                if bool(eng.finished.all().item()):
-                    break
+        replay_until_done(g)
         with torch.cuda.stream(stream):
             resp_host.copy_(resp, non_blocking=True)
     end.record(stream)
