@@ -188,15 +188,28 @@ struct __align__(16) VShared {
 // Alg. 1 lines 15/22 ("y <- y o a") for one rollout, by the warp whose lane 0 just
 // finalized its step: the same state update as commit_kernel (state.cu), fused into the
 // verify launch.  Lane i owns tail slot i (M <= 32) and emitted token i (<= k+1 <= 32).
-__device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane) {
+struct CommitPre {
+    int s, p, L, cl, old;  // slot, pos, max_len, ctx_len; lane i: tail slot i
+};
+__device__ __forceinline__ CommitPre commit_prefetch(const VerifyArgs& a, int slot, int lane) {
+    CommitPre c;
+    c.s = slot;
+    c.p = a.c_pos[slot];
+    c.L = a.max_len[slot];
+    c.cl = a.c_ctx_len[slot];
+    c.old = (lane < a.M) ? a.c_tail[(int64_t)slot * a.M + lane] : -1;
+    return c;
+}
+
+__device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane, const CommitPre& c) {
     __syncwarp();  // lane 0's outputs (finalize_rollout) are visible to the warp
-    const int s = a.slots[b];
+    const int s = c.s;
     const int M = a.M;
-    const int no = a.out_len[b];
-    const int p = a.c_pos[s], L = a.max_len[s];
+    const int no = __shfl_sync(0xFFFFFFFFu, lane == 0 ? a.out_len[b] : 0, 0);
+    const int p = c.p, L = c.L;
     const int32_t* out = a.out_tokens + (int64_t)b * (a.k + 1);
     int32_t* tl = a.c_tail + (int64_t)s * M;
-    const int32_t old = (lane < M) ? tl[lane] : -1;
+    const int32_t old = c.old;
     const int32_t ot = (lane < no) ? out[lane] : -1;
     const int src = lane + no;  // new tail[i] = (old ++ out)[i + no]
     const int32_t from_old = __shfl_sync(0xFFFFFFFFu, old, src & 31);
@@ -206,7 +219,7 @@ __device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane) {
     const int32_t last = __shfl_sync(0xFFFFFFFFu, ot, (no - 1) & 31);
     const int f = ((a.eos >= 0 && last == a.eos) || p + no >= L) ? 1 : 0;
     if (lane == 0) {
-        a.c_ctx_len[s] = min(M, a.c_ctx_len[s] + no);
+        a.c_ctx_len[s] = min(M, c.cl + no);
         a.c_pos[s] = p + no;
         if (f) a.c_finished[s] = 1;
         if (a.c_fin_out) a.c_fin_out[b] = f;

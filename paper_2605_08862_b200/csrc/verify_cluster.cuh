@@ -141,7 +141,7 @@ __device__ bool ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
 
 // Row r of rollout b as a descriptor (lane-uniform inputs; every lane computes it).
 __device__ __forceinline__ RowDesc ck_desc(int b, int j, int q, int d, int pos, unsigned long long uid,
-                                           long long rowno, int aligned, int src) {
+                                           long long rowno, int aligned, int src, int slot) {
     RowDesc r;
     r.b = b;
     r.j = j;
@@ -151,8 +151,8 @@ __device__ __forceinline__ RowDesc ck_desc(int b, int j, int q, int d, int pos, 
     r.uid = uid;
     r.position = pos + j;
     r.aligned = aligned;
-    r.pad[0] = src;  // claim source (diagnostics)
-    r.pad[1] = 0;
+    r.pad[0] = src;   // claim source (diagnostics)
+    r.pad[1] = slot;  // rollout slot (fused commit)
     return r;
 }
 
@@ -164,7 +164,7 @@ __device__ __forceinline__ RowDesc ck_desc(int b, int j, int q, int d, int pos, 
 struct TakeIssue {
     int b = -1, rpred = 0;
     unsigned long long old = 0;
-    int rf = -1, q = 0, p = 0, d0 = -1, al0 = 0, dpred = -1;
+    int rf = -1, q = 0, p = 0, d0 = -1, al0 = 0, dpred = -1, slot = 0;
     unsigned long long u = 0;
     long long rn0 = 0, rnpred = 0;
 };
@@ -179,6 +179,7 @@ __device__ __forceinline__ TakeIssue ck_take_issue(const VerifyArgs& a, int b, i
     if (lane == 1) {  // L2 reads (published by another SM this launch)
         t.rf = ld_volatile_i32(a.roll_first + b);
         t.q = __ldcg(&rp->q);
+        t.slot = __ldcg(&rp->slot);
         t.p = __ldcg(&rp->pos);
         t.u = __ldcg(&rp->uid);
         t.d0 = __ldcg(&rp->d0);
@@ -200,6 +201,7 @@ __device__ __forceinline__ bool ck_take_finish(const VerifyArgs& a, uint32_t epo
     const bool valid = (uint32_t)(old >> 32) == epoch && r <= rf;
     if (!valid) return false;
     const int q = __shfl_sync(0xFFFFFFFFu, t.q, 1);
+    const int sl = __shfl_sync(0xFFFFFFFFu, t.slot, 1);
     const int p = __shfl_sync(0xFFFFFFFFu, t.p, 1);
     const unsigned long long u = shfl_u64(t.u, 1);
     int d = -1, al = 0;
@@ -223,7 +225,7 @@ __device__ __forceinline__ bool ck_take_finish(const VerifyArgs& a, uint32_t epo
         if (r >= q) d = -1;
         al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
     }
-    out = ck_desc(b, r, q, d, p, u, rn, al, src);
+    out = ck_desc(b, r, q, d, p, u, rn, al, src, sl);
     return true;
 }
 
@@ -238,12 +240,13 @@ __device__ __forceinline__ bool ck_take_row(const VerifyArgs& a, int b, int j, i
     // the logits row in one round trip
     const RollRec* rp = a.rrec + b;
     const int kp1 = a.k + 1;
-    int rf = -1, q = 0, p = 0, d0 = -1, al0 = 0, dj = -1;
+    int rf = -1, q = 0, p = 0, d0 = -1, al0 = 0, dj = -1, sl = 0;
     unsigned long long u = 0;
     long long rn0 = 0, rnj = 0;
     if (lane == 0) rf = ld_volatile_i32(a.roll_first + b);
     if (lane == 1) {
         q = __ldcg(&rp->q);
+        sl = __ldcg(&rp->slot);
         p = __ldcg(&rp->pos);
         u = __ldcg(&rp->uid);
         d0 = __ldcg(&rp->d0);
@@ -268,7 +271,8 @@ __device__ __forceinline__ bool ck_take_row(const VerifyArgs& a, int b, int j, i
         rn = (long long)shfl_u64((unsigned long long)rnj, 3);
         al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
     }
-    out = ck_desc(b, j, q, d, p, u, rn, al, j == 0 ? SRC_STATIC : SRC_SPEC);
+    sl = __shfl_sync(0xFFFFFFFFu, sl, 1);
+    out = ck_desc(b, j, q, d, p, u, rn, al, j == 0 ? SRC_STATIC : SRC_SPEC, sl);
     return true;
 }
 
@@ -629,6 +633,10 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             mbar_wait(&sh.dfull[s], (i / CK_D) & 1);
             const RowDesc dsc = sh.dq[s];
             if (dsc.b < 0) break;
+            // fused commit: the rollout's state, fetched while this row's sums arrive (only the
+            // finalizing row uses it; nothing else writes it during the launch)
+            CommitPre cp;
+            if (a.commit) cp = commit_prefetch(a, dsc.pad[1], lane);
             mbar_wait(&sh.sumbar[s], (i / CK_D) & 1);
             const int b = dsc.b, j = dsc.j, q = dsc.q, d = dsc.d;
             if (lane == 0) TRACE(TR_EPI0, i, b, j);
@@ -774,7 +782,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                     }
                 }
             }
-            if (a.commit && __shfl_sync(0xFFFFFFFFu, fz ? 1 : 0, 0)) commit_rollout_warp(a, b, lane);
+            if (a.commit && __shfl_sync(0xFFFFFFFFu, fz ? 1 : 0, 0)) commit_rollout_warp(a, b, lane, cp);
             __syncwarp();
             if (lane == 0) {
                 TRACE(TR_EPI1, i, dsc.b, dsc.j);
