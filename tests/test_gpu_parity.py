@@ -370,3 +370,40 @@ def test_cluster_scheduler_repeated_launches(bs, orc):
         live = np.nonzero(max_len)[0]
         _compare_step(orc, rows[live], drafts[live], dlen[live], k, 1.0 if it % 3 else 0.0, 1.0, seed,
                       uids[live], max_len[live], -1, tuple(x[live] for x in got))
+
+
+@pytest.mark.parametrize("k", [2, 4, 8, 16])
+def test_acceptance_sweep_k_qwen_vocab(bs, orc, k):
+    """SWEEP config shapes (BASELINE.json configs[4]): k in {2, 4, 8, 16} at V = 151936 through
+    the default (cluster) kernel, drafts mixing the argmax with random tokens."""
+    rng = np.random.default_rng(1000 + k)
+    V, n = 151936, 6
+    rows, drafts, dlen = _random_step(rng, n, k, V, peaked=0.7)
+    dlen[:] = k
+    max_len = np.full(n, 100000)
+    seed = 0xC0FFEE
+    ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=32, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    uids = np.arange(n, dtype=np.uint64) + np.uint64(1 << 33)
+    _begin(bs, ctx, n, max_len, uids, 32)
+    got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, 1.0, 1.0)
+    assert ctx.bs_sync_status() == 0
+    _compare_step(orc, rows, drafts, dlen, k, 1.0, 1.0, seed, uids, max_len, -1, got)
+
+
+def test_long_context_config_topp(bs, orc):
+    """LC config shapes (BASELINE.json configs[2]): V = 151936, k = 16, top-p 0.95, T = 1
+    (the top-p kernel), with max_len clamping two of the drafts (reading L6)."""
+    rng = np.random.default_rng(4242)
+    V, n, k = 151936, 4, 16
+    rows, drafts, dlen = _random_step(rng, n, k, V, peaked=0.7)
+    dlen[:] = k
+    max_len = np.array([32768, 32768, 9, 3])  # the last two clamp q (reading L6)
+    seed = 0xFEED
+    ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=32, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    uids = np.arange(n, dtype=np.uint64) + np.uint64(77)
+    _begin(bs, ctx, n, max_len, uids, 32)
+    got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, 1.0, 0.95)
+    assert ctx.bs_sync_status() == 0
+    _compare_step(orc, rows, drafts, dlen, k, 1.0, 0.95, seed, uids, max_len, -1, got)
