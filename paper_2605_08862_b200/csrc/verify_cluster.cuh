@@ -31,7 +31,8 @@ constexpr int CK_NXW = 2;                 // max warps: 8..9
 constexpr int CK_NCW = CK_NMW + CK_NXW;
 constexpr int CK_PROD = CK_NCW;           // producer warp
 constexpr int CK_EPI = CK_NCW + 1;        // epilogue warp
-constexpr int CK_NT = (CK_NCW + 2) * 32;  // 384 threads
+constexpr int CK_CLM = CK_NCW + 2;        // claimer warp (leader CTA)
+constexpr int CK_NT = (CK_NCW + 3) * 32;  // 416 threads
 constexpr int CK_NB = 2;                  // slice buffers
 #ifdef BS_CK_MINB
 constexpr int CK_MINB = BS_CK_MINB;       // min CTAs per SM (register budget experiment)
@@ -51,6 +52,7 @@ struct CkShared {
     uint4 csum[CK_D][CK_CL];  // per CTA: {slice mass sum lo, hi, mass(d) lo, hi}
     uint4 erec[CK_D];         // mass warps -> epilogue: {m bits, bad, greedy index, 0}
     int mail;  // leader: (rollout << 8 | row) the epilogue found needed next, or -1
+    int tma_issued;  // leader: rows whose copy the producer has issued (claimer look-ahead)
     int plan_b[CK_NMW];  // planning round: rollout per mass warp (-1 dead, -2 none)
     float wmax[CK_NXW];
     uint32_t wbad[CK_NXW];
@@ -454,7 +456,7 @@ __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch,
             if (sr <= a.k && ck_take(a, epoch, sb, SRC_SPEC, lane, sr, out)) return out;
         }
         if (eager) break;  // every row claimed: nothing left for this cluster
-        if (queues) {
+        {
             int src = SRC_NONE, rpred = 0;
             b = ck_scan(a, epoch, lane, rot, src, rpred);
             if (lane == 0) TRACE(TR_ITER, spin, b, src);
@@ -525,7 +527,10 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
         fence_mbar_init();
     }
     for (int i = tid; i < STAT_COUNT; i += CK_NT) sh.stat[i] = 0ull;
-    if (tid == 0) sh.mail = -1;
+    if (tid == 0) {
+        sh.mail = -1;
+        sh.tma_issued = 0;
+    }
 #ifdef BS_TRACE
     if (tid == 0) {
         s_trace_n = 0;
@@ -565,37 +570,53 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
         }
     }
 
-    if (warp == CK_PROD) {
-        // ================================================================ producer
-        // The leader claims row i+1 right after issuing row i's copy (one row of lookahead:
-        // the claim's dependent loads stay off the compute warps' critical path) and
-        // broadcasts each descriptor with 24 lanes (8 CTAs x 3 x 16 bytes).
-        const int ncl = (int)(gridDim.x / CK_CL);
-        const int rot = (int)(((long long)(blockIdx.x / CK_CL) * a.n) / max(1, ncl));
-        ClaimState cst;
-        auto broadcast = [&](int r) {
-            const int s = r % CK_D;
-            // every CTA's epilogue is done with row r-4 (the slot's previous use)
-            if (r >= CK_D) mbar_wait_cluster(&sh.dempty[s], ((r / CK_D) - 1) & 1);
-            // look ahead into the static list only; ready / speculative rows are claimed
-            // when this cluster can start them (its buffer for row r is free)
-            if (lane == 0) TRACE(TR_CLAIM0, r, 0, 0);
-            // claimed right after the previous row's copy is issued: the claim's round trips
-            // overlap the rows in flight (the row waits for its buffer afterwards)
-            RowDesc nd = ck_claim(a, epoch, lane, true, rot, cst, &sh.mail);
-            if (lane == 0) TRACE(TR_CLAIM1, r | (nd.b >= 0 ? nd.pad[0] << 12 : 0), nd.b, nd.j);
-            uint32_t w[12];
-            memcpy(w, &nd, sizeof(w));
-            for (int x = lane; x < 3 * CK_CL; x += 32) {
-                const int part = x % 3;
-                uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
-                if (part == 1) v = make_uint4(w[4], w[5], w[6], w[7]);
-                if (part == 2) v = make_uint4(w[8], w[9], w[10], w[11]);
-                st_async_v4(reinterpret_cast<uint4*>(&sh.dq[s]) + part, v, &sh.dfull[s], (uint32_t)(x / 3));
+    if (warp == CK_CLM) {
+        // ================================================================ claimer (leader)
+        // Claims rows up to two ahead of the producer's copy issue and broadcasts each
+        // descriptor to the 8 CTAs with 24 lanes (8 CTAs x 3 x 16 bytes).  A claim is a few
+        // dependent round trips (~1.5 us each under full HBM load); in its own warp it never
+        // delays a copy.  It blocks (spins for work) only when every row it claimed has had
+        // its copy issued: a row waiting for a copy may be the one whose completion creates
+        // the work.
+        if (rank == 0) {
+            const int ncl = (int)(gridDim.x / CK_CL);
+            const int rot = (int)(((long long)(blockIdx.x / CK_CL) * a.n) / max(1, ncl));
+            ClaimState cst;
+            for (int r = 0;;) {
+                int issued = 0;
+                if (lane == 0) issued = *reinterpret_cast<volatile int*>(&sh.tma_issued);
+                issued = __shfl_sync(0xFFFFFFFFu, issued, 0);
+                if (r > issued + 2) {  // far enough ahead
+                    __nanosleep(128);
+                    continue;
+                }
+                const int s = r % CK_D;
+                // every CTA's epilogue is done with row r-4 (the slot's previous use)
+                if (r >= CK_D) mbar_wait_cluster(&sh.dempty[s], ((r / CK_D) - 1) & 1);
+                if (lane == 0) TRACE(TR_CLAIM0, r, 0, 0);
+                const RowDesc nd = ck_claim(a, epoch, lane, r <= issued, rot, cst, &sh.mail);
+                if (nd.b == -2) {  // nothing claimable now, and rows are still being copied
+                    __nanosleep(128);
+                    continue;
+                }
+                if (lane == 0) TRACE(TR_CLAIM1, r | (nd.b >= 0 ? nd.pad[0] << 12 : 0), nd.b, nd.j);
+                uint32_t w[12];
+                memcpy(w, &nd, sizeof(w));
+                for (int x = lane; x < 3 * CK_CL; x += 32) {
+                    const int part = x % 3;
+                    uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
+                    if (part == 1) v = make_uint4(w[4], w[5], w[6], w[7]);
+                    if (part == 2) v = make_uint4(w[8], w[9], w[10], w[11]);
+                    st_async_v4(reinterpret_cast<uint4*>(&sh.dq[s]) + part, v, &sh.dfull[s], (uint32_t)(x / 3));
+                }
+                ++r;
+                if (nd.b < 0) break;  // END broadcast: nothing more is claimed
             }
-        };
+        }
+    } else if (warp == CK_PROD) {
+        // ================================================================ producer
+        // Every CTA: bulk-copies (TMA) its slice of each row into one of two buffers.
         if (lane == 0) mbar_arrive_expect_tx(&sh.dfull[0], (uint32_t)sizeof(RowDesc));
-        if (rank == 0) broadcast(0);
         for (int i = 0;; ++i) {
             const int s = i % CK_D, bi = i % CK_NB;
             // arm the descriptor slot for row i (its use by row i-4 completed: this warp
@@ -619,8 +640,8 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 } else {
                     mbar_arrive(&sh.full[bi]);
                 }
+                if (rank == 0) *reinterpret_cast<volatile int*>(&sh.tma_issued) = i + 1;
             }
-            if (rank == 0) broadcast(i + 1);
         }
     } else if (warp == CK_EPI) {
         // ================================================================ epilogue
