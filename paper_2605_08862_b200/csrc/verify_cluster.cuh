@@ -33,7 +33,11 @@ constexpr int CK_PROD = CK_NCW;           // producer warp
 constexpr int CK_EPI = CK_NCW + 1;        // epilogue warp
 constexpr int CK_CLM = CK_NCW + 2;        // claimer warp (leader CTA)
 constexpr int CK_NT = (CK_NCW + 3) * 32;  // 416 threads
+#ifdef BS_CK_NB
+constexpr int CK_NB = BS_CK_NB;           // slice buffers (experiment)
+#else
 constexpr int CK_NB = 2;                  // slice buffers
+#endif
 #ifdef BS_CK_MINB
 constexpr int CK_MINB = BS_CK_MINB;       // min CTAs per SM (register budget experiment)
 #else
