@@ -160,7 +160,12 @@ __host__ __device__ inline uint32_t h32(uint32_t x) {
 // is launched with programmatic stream serialization: its CTAs may be scheduled while the
 // previous kernel still runs, and pdl_wait() (griddepcontrol.wait) blocks until that kernel
 // has completed and its memory is visible.  pdl_trigger() lets the next kernel launch early.
-// Kernels call pdl_wait() before touching any global memory.
+// Kernels call pdl_wait() before touching global memory, with one exception: the cluster
+// verify kernel plans (reads slots, drafts, positions, lengths; writes its scheduler state)
+// before its wait, which is safe because every kernel of ours that writes those inputs or
+// that state (lookup, commit, every verify kernel) triggers its dependents only at exit
+// (lookup: after its stores), and the kernel in between (the model / target rows) waits for
+// them; user kernels launched without PDL complete before the next launch starts anyway.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 

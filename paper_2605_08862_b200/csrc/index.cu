@@ -424,7 +424,8 @@ __constant__ HashPow c_hash_pow = make_hash_pow();
 
 __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a0) {
     pdl_wait();
-    pdl_trigger();
+    // dependents are triggered only after the drafts are stored (end of the kernel): the
+    // verify kernel plans from them before its own griddepcontrol.wait
     const int lane = threadIdx.x & 31;
     const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (b >= a0.n) return;
@@ -528,6 +529,8 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a0) {
         a.draft_len[b] = q;
         if (a.match_len) a.match_len[b] = mstar;
     }
+    __threadfence();
+    pdl_trigger();
 }
 
 cudaError_t launch_lookup(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k, int32_t* draft,

@@ -33,8 +33,7 @@ __global__ void commit_kernel(int n, int M, int k, int eos, const int32_t* slots
                               int32_t* ctx_len, int32_t* pos, const int32_t* max_len,
                               int32_t* finished, int32_t* fin_out, int32_t* resp,
                               int64_t resp_stride) {
-    pdl_wait();
-    pdl_trigger();
+    pdl_wait();  // dependents launch at exit: a verify launch plans from this state early
     const int lane = threadIdx.x & 31;
     const int b = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (b >= n) return;

@@ -445,8 +445,7 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw);
     VShared& sh = *reinterpret_cast<VShared*>(smem_raw + (size_t)NSTAGE * CHE * 2);
-    pdl_wait();
-    pdl_trigger();
+    pdl_wait();  // dependents launch at exit (the cluster kernel plans before its wait)
     if (a.ctl[VCTL_MODE] != 0) return;  // few rows: the split (cluster) kernel runs instead
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rows = (int)a.ctl[VCTL_ROWS];
@@ -717,8 +716,7 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     unsigned long long* roll_state, int32_t* out_len, int32_t* out_acc, int32_t* out_tokens,
     float* out_norm, unsigned long long* out_z, uint32_t* dev_err, int mode) {
     __shared__ int hist[33], lvl_off[33], lvl_ctr[33], s_rows, s_nact;
-    pdl_wait();
-    pdl_trigger();
+    pdl_wait();  // dependents launch at exit (the cluster kernel plans before its wait)
     const int tid = threadIdx.x;
     if (tid < 33) {
         hist[tid] = 0;

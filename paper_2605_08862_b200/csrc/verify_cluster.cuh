@@ -98,7 +98,6 @@ __device__ bool ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
     const int sl = a.slots[b];
     const int dlen = a.draft_len[b];
     const int tk = (lane < a.k) ? a.draft[(int64_t)b * a.k + lane] : 0;
-    const long long rowno0 = (lane == 0) ? (a.row_index ? a.row_index[(int64_t)b * kp1] : (int64_t)b * kp1) : 0;
     const int p = a.pos[sl], L = a.max_len[sl];
     int q = -1;
     if (!a.finished[sl] && p < L) q = min(max(dlen, 0), min(a.k, L - p - 1));
@@ -120,9 +119,9 @@ __device__ bool ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
         rr.pos = p;
         rr.tag = (int32_t)epoch;
         rr.uid = a.uid[sl];
-        rr.rowno0 = rowno0;
+        rr.rowno0 = -1;  // row_index is read at claim time (after griddepcontrol.wait)
         rr.d0 = q > 0 ? d0 : -1;
-        rr.aligned0 = ((reinterpret_cast<uintptr_t>(a.logits + rr.rowno0 * a.stride) & 15u) == 0) ? 1 : 0;
+        rr.aligned0 = 0;
         rr.pad[0] = rr.pad[1] = 0;
         a.rrec[b] = rr;
         a.roll_first[b] = q;  // the bonus row q always decides; -1: no rows
@@ -189,11 +188,9 @@ __device__ __forceinline__ TakeIssue ck_take_issue(const VerifyArgs& a, int b, i
         t.p = __ldcg(&rp->pos);
         t.u = __ldcg(&rp->uid);
         t.d0 = __ldcg(&rp->d0);
-        t.rn0 = __ldcg(&rp->rowno0);
-        t.al0 = __ldcg(&rp->aligned0);
     }
     if (lane == 2 && rpred >= 1 && rpred <= a.k) t.dpred = a.draft[(int64_t)b * a.k + min(rpred, a.k - 1)];
-    if (lane == 3 && rpred >= 1 && rpred <= a.k)
+    if (lane == 3 && rpred >= 0 && rpred <= a.k)
         t.rnpred = a.row_index ? a.row_index[(int64_t)b * kp1 + rpred] : (int64_t)b * kp1 + rpred;
     return t;
 }
@@ -214,8 +211,13 @@ __device__ __forceinline__ bool ck_take_finish(const VerifyArgs& a, uint32_t epo
     long long rn = 0;
     if (r == 0) {
         d = __shfl_sync(0xFFFFFFFFu, t.d0, 1);
-        rn = (long long)shfl_u64((unsigned long long)t.rn0, 1);
-        al = __shfl_sync(0xFFFFFFFFu, t.al0, 1);
+        if (t.rpred == 0) {
+            rn = (long long)shfl_u64((unsigned long long)t.rnpred, 3);
+        } else {
+            if (lane == 0) rn = a.row_index ? a.row_index[(int64_t)b * kp1] : (int64_t)b * kp1;
+            rn = (long long)shfl_u64((unsigned long long)rn, 0);
+        }
+        al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
     } else {
         if (r == t.rpred) {
             d = __shfl_sync(0xFFFFFFFFu, t.dpred, 2);
@@ -256,11 +258,9 @@ __device__ __forceinline__ bool ck_take_row(const VerifyArgs& a, int b, int j, i
         p = __ldcg(&rp->pos);
         u = __ldcg(&rp->uid);
         d0 = __ldcg(&rp->d0);
-        rn0 = __ldcg(&rp->rowno0);
-        al0 = __ldcg(&rp->aligned0);
     }
     if (lane == 2 && j >= 1 && j < a.k) dj = a.draft[(int64_t)b * a.k + j];
-    if (lane == 3 && j >= 1) rnj = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+    if (lane == 3) rnj = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
     rf = __shfl_sync(0xFFFFFFFFu, rf, 0);
     q = __shfl_sync(0xFFFFFFFFu, q, 1);
     if (!(j <= q && j <= rf)) return false;
@@ -268,15 +268,10 @@ __device__ __forceinline__ bool ck_take_row(const VerifyArgs& a, int b, int j, i
     u = shfl_u64(u, 1);
     int d, al;
     long long rn;
-    if (j == 0) {
-        d = __shfl_sync(0xFFFFFFFFu, d0, 1);
-        rn = (long long)shfl_u64((unsigned long long)rn0, 1);
-        al = __shfl_sync(0xFFFFFFFFu, al0, 1);
-    } else {
-        d = (j < q) ? __shfl_sync(0xFFFFFFFFu, dj, 2) : -1;
-        rn = (long long)shfl_u64((unsigned long long)rnj, 3);
-        al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
-    }
+    if (j == 0) d = __shfl_sync(0xFFFFFFFFu, d0, 1);
+    else d = (j < q) ? __shfl_sync(0xFFFFFFFFu, dj, 2) : -1;
+    rn = (long long)shfl_u64((unsigned long long)rnj, 3);
+    al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
     sl = __shfl_sync(0xFFFFFFFFu, sl, 1);
     out = ck_desc(b, j, q, d, p, u, rn, al, j == 0 ? SRC_STATIC : SRC_SPEC, sl);
     return true;
@@ -544,9 +539,16 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
     }
 #endif
     cluster.sync();  // every CTA's barriers exist before any remote operation
-    pdl_wait();      // (the prologue above overlaps the previous kernel's tail)
-    pdl_trigger();
+    // The plan runs before griddepcontrol.wait, overlapping the kernel launched just before
+    // this one (the model forward / target rows): its inputs (slots, drafts, positions,
+    // lengths, uids) come from launches at least two back (the lookup triggers its dependents
+    // only after its stores), and it reads no logits and no row_index.  The previous verify
+    // launch is complete (the lookup waited for it), so the scheduler words are reset.
     const uint32_t epoch = ld_relaxed_u32(a.sctl + SC_EPOCH);
+    // No early launch_dependents: the next launch may plan before its own wait, so it must
+    // not start before this one's scheduler state, plan records and fused commit are final
+    // (the implicit trigger at exit).
+    if (warp >= CK_NMW) pdl_wait();
     if (tid == 0) TRACE(TR_GO, 0, 0, 0);
     if (warp < CK_NMW) {
         // plan the call's rollouts, one warp each, in rounds over the grid; per round one atomic
@@ -572,6 +574,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             }
             named_bar(3, CK_NMW * 32);  // plan_b reusable
         }
+        pdl_wait();
     }
 
     if (warp == CK_CLM) {

@@ -43,8 +43,7 @@ struct SplitShared {
 
 __global__ void __cluster_dims__(SP_CL, 1, 1) __launch_bounds__(SP_NT, 2)
     verify_split_kernel(const VerifyArgs a, int SL) {
-    pdl_wait();
-    pdl_trigger();
+    pdl_wait();  // dependents launch at exit (the cluster kernel plans before its wait)
     if (a.ctl[VCTL_MODE] != 1) return;  // the plan kernel chose the one-CTA-per-row path
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();

@@ -57,8 +57,7 @@ __device__ __forceinline__ void tp_unpack(const uint4 v, uint32_t b[8]) {
 __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs a, float top_p) {
     extern __shared__ __align__(16) uint8_t tp_smem[];
     TopPShared& sh = *reinterpret_cast<TopPShared*>(tp_smem);
-    pdl_wait();
-    pdl_trigger();
+    pdl_wait();  // dependents launch at exit (the cluster kernel plans before its wait)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rows = (int)a.ctl[VCTL_ROWS];
     const int V = a.V;

@@ -407,3 +407,43 @@ def test_long_context_config_topp(bs, orc):
     got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, 1.0, 0.95)
     assert ctx.bs_sync_status() == 0
     _compare_step(orc, rows, drafts, dlen, k, 1.0, 0.95, seed, uids, max_len, -1, got)
+
+
+def test_back_to_back_verify_calls(bs, orc):
+    """Several bs_verify_step calls enqueued back to back on one stream (no synchronisation,
+    no kernel in between): the cluster kernel plans before griddepcontrol.wait, which is only
+    safe because every verify launch releases its dependents at exit.  Each call has its own
+    inputs and outputs; each must match the oracle."""
+    rng = np.random.default_rng(31337)
+    V, k, n, calls = 4096, 6, 24, 6
+    seed = 0x51DE
+    ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=8, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    uids = np.arange(n, dtype=np.uint64) + np.uint64(900)
+    max_len = np.full(n, 1000)
+    _begin(bs, ctx, n, max_len, uids, 8)
+    torch.cuda.synchronize()
+    slots = to_dev(np.arange(n, dtype=np.int32))
+    ins, outs = [], []
+    for c in range(calls):
+        rows, drafts, dlen = _random_step(rng, n, k, V)
+        lg = to_dev(rows.view(np.int16).reshape(-1))
+        dr, dl = to_dev(drafts.astype(np.int32)), to_dev(dlen.astype(np.int32))
+        o = (torch.full((n, k + 1), -7, dtype=torch.int32, device="cuda"),
+             torch.zeros(n, dtype=torch.int32, device="cuda"), torch.zeros(n, dtype=torch.int32, device="cuda"),
+             torch.zeros((n, k + 1), dtype=torch.float32, device="cuda"),
+             torch.zeros((n, k + 1), dtype=torch.int64, device="cuda"))
+        ins.append((rows, drafts, dlen, lg, dr, dl))
+        outs.append(o)
+    torch.cuda.synchronize()
+    for c in range(calls):  # enqueue all, then synchronise once
+        rows, drafts, dlen, lg, dr, dl = ins[c]
+        ot, ol, oa, on, oz = outs[c]
+        ctx.bs_verify_step(slots, lg, None, V, dr, dl, k, 1.0 if c % 2 else 0.8, 1.0, ot, ol, oa, on, oz)
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() == 0
+    for c in range(calls):
+        rows, drafts, dlen = ins[c][:3]
+        got = (outs[c][0].cpu().numpy(), outs[c][1].cpu().numpy(), outs[c][2].cpu().numpy(),
+               outs[c][3].cpu().numpy(), outs[c][4].cpu().numpy().view(np.uint64))
+        _compare_step(orc, rows, drafts, dlen, k, 1.0 if c % 2 else 0.8, 1.0, seed, uids, max_len, -1, got)
