@@ -95,10 +95,13 @@ class ClockSampler:
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        if os.environ.get("BS_NO_CLOCKS"):  # diagnostics only: no sampler
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("BS_CLOCK_MS", "200")], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
@@ -107,7 +110,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append([time.time()] + parts)
+
+    def window(self, t0, t1):
+        """Keep only the samples taken inside [t0, t1] (host time): the sampler is started
+        before the warm-up so its start-up does not overlap the timed region."""
+        self.t0, self.t1 = t0, t1
 
     def stop(self):
         if self.proc:
@@ -117,6 +125,9 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        t0, t1 = getattr(self, "t0", -1e30), getattr(self, "t1", 1e30)
+        rows = [r[1:] for r in self.rows if t0 <= r[0] <= t1] or [r[1:] for r in self.rows]
+        self.rows = rows
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
@@ -281,6 +292,10 @@ def run_ours(args, cfg, rank, world, dist):
     D = cfg["M"] + k
     rec0 = dict(launches=0, verify_ms=0.0, verify_ms_steady=0.0, steady_steps=0, decode_steps=0,
                 seal_launches=4 + 9 * D)
+    # nvidia-smi is started before the warm-up (its start-up stays outside the timed region);
+    # only its samples inside the timed window are kept
+    clocks = ClockSampler(dev.index)
+    clocks.start()
     # ---- warmup
     for s in range(args.warmup):
         rl_step(s, dict(rec0))
@@ -290,34 +305,14 @@ def run_ours(args, cfg, rank, world, dist):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clocks = ClockSampler(dev.index)
-    clocks.start()
-    rec = dict(rec0)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record(stream)
-    for s in range(args.warmup, total_steps):
-        rl_step(s, rec)
-    end.record(stream)
-    torch.cuda.synchronize(dev)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    clk = clocks.stop()
-    elapsed_ms = start.elapsed_time(end)
-    st = eng.stats(reset=True)
-    # ---- the verify op's device time on the same work: instrumented replay of the timed
-    # RL steps (deterministic: same pools, uids and Philox stream -> identical rows)
+    # ---- (untimed, before the timed region: it also settles the device) the verify op's
+    # device time on the same work: instrumented replay of the RL steps that are timed next
+    # (deterministic: same pools, uids and Philox stream -> identical rows)
     reci = dict(rec0)
     for s in range(args.warmup, total_steps):
         rl_step(s, reci, instrument=True)
     torch.cuda.synchronize(dev)
     sti = eng.stats(reset=True)
-    if sti["tokens"] != st["tokens"] or sti["rows_verified"] != st["rows_verified"]:
-        log(f"note: instrumented replay differs ({sti['tokens']} vs {st['tokens']} tokens, "
-            f"{sti['rows_verified']} vs {st['rows_verified']} rows)")
-    rec["verify_ms"] = reci["verify_ms"]
-    rec["verify_rows_verified"] = sti["rows_verified"]
-    rec["verify_rows_needed"] = sti["rows_needed"]
     # ---- steady-state kernel phase: full live batch, first chunk of a fresh RL step
     s_last = total_steps - 1
     d = dins[s_last]
@@ -333,6 +328,28 @@ def run_ours(args, cfg, rank, world, dist):
     torch.cuda.synchronize(dev)
     steady_ms = sum(ev_s[i].elapsed_time(ev_e[i]) for i in range(chunk))
     sst = eng.stats(reset=True)
+    rec = dict(rec0)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_host0 = time.time()
+    start.record(stream)
+    for s in range(args.warmup, total_steps):
+        rl_step(s, rec)
+    end.record(stream)
+    torch.cuda.synchronize(dev)
+    t_host1 = time.time()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.window(t_host0, t_host1)
+    clk = clocks.stop()
+    elapsed_ms = start.elapsed_time(end)
+    st = eng.stats(reset=True)
+    if sti["tokens"] != st["tokens"] or sti["rows_verified"] != st["rows_verified"]:
+        log(f"note: instrumented replay differs ({sti['tokens']} vs {st['tokens']} tokens, "
+            f"{sti['rows_verified']} vs {st['rows_verified']} rows)")
+    rec["verify_ms"] = reci["verify_ms"]
+    rec["verify_rows_verified"] = sti["rows_verified"]
+    rec["verify_rows_needed"] = sti["rows_needed"]
     # ---- e2e: the same RL steps through the public API from pinned HOST buffers
     e2e = run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, dist, replay_until_done)
     # ---- gather over ranks

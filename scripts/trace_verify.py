@@ -324,3 +324,19 @@ if os.environ.get("TRACE_GAPS"):
     print("  next max1 - mass1 (>0: waiting for max):", q(wmax))
     print("  next TMA issue - previous-row mass1 (buffer free):", q(wtma))
     print("  next claim end - previous-row mass1:", q(wclaim))
+if os.environ.get("TRACE_CLAIMS"):
+    c0, c1 = {}, {}
+    for tt, ty, sq, b_, bk in zip(t, typ, seq, bb, blk):
+        if int(bk) % 8:
+            continue
+        key_ = (int(bk), int(sq) & 0xFFF)
+        if ty == 0:
+            c0.setdefault(key_, float(tt))
+        if ty == 1:
+            c1[key_] = (float(tt), int(sq) >> 12, int(b_))
+    bysrc = {}
+    for key_, (tt, src, b_) in c1.items():
+        if key_ in c0 and b_ != 0xFFFF:
+            bysrc.setdefault(src, []).append(tt - c0[key_])
+    for src, v in sorted(bysrc.items()):
+        print(f"  claim duration src {src}: n={len(v)} median {np.median(v):.2f} p75 {np.percentile(v, 75):.2f} p90 {np.percentile(v, 90):.2f} us")
