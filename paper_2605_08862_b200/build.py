@@ -52,5 +52,9 @@ if __name__ == "__main__":
         print(build(force=True, variant="trace", defines=["BS_TRACE"]))
     elif "--timing" in sys.argv:
         print(build(force=True, variant="timing", defines=["BS_PHASE_TIMING"]))
+    elif "--variant" in sys.argv:  # --variant NAME DEF [DEF ...]: experiment builds
+        i = sys.argv.index("--variant")
+        print(build(force=True, verbose="-v" in sys.argv, variant=sys.argv[i + 1],
+                    defines=[d for d in sys.argv[i + 2:] if d != "-v"]))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -201,16 +201,14 @@ __device__ __forceinline__ CommitPre commit_prefetch(const VerifyArgs& a, int sl
     return c;
 }
 
-__device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane, const CommitPre& c) {
-    __syncwarp();  // lane 0's outputs (finalize_rollout) are visible to the warp
+// The emitted block comes in registers from the warp's finalize: no (all lanes), lane i: token i.
+__device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane, const CommitPre& c, int no, int32_t ot) {
     const int s = c.s;
     const int M = a.M;
-    const int no = __shfl_sync(0xFFFFFFFFu, lane == 0 ? a.out_len[b] : 0, 0);
     const int p = c.p, L = c.L;
-    const int32_t* out = a.out_tokens + (int64_t)b * (a.k + 1);
     int32_t* tl = a.c_tail + (int64_t)s * M;
     const int32_t old = c.old;
-    const int32_t ot = (lane < no) ? out[lane] : -1;
+    if (lane >= no) ot = -1;
     const int src = lane + no;  // new tail[i] = (old ++ out)[i + no]
     const int32_t from_old = __shfl_sync(0xFFFFFFFFu, old, src & 31);
     const int32_t from_out = __shfl_sync(0xFFFFFFFFu, ot, (src - M) & 31);
@@ -304,6 +302,79 @@ __device__ bool complete_row(const VerifyArgs& a, unsigned long long* stat, int 
         return true;
     }
     return false;
+}
+
+// complete_row for a whole warp (lane 0 records and ORs; on finalization the warp reads the
+// decided prefix in one parallel round trip: lane i < F the draft token d_{i+1}, lane i <= F
+// row i's normaliser / Z, the deciding row F's status and candidate; row j's own values come
+// from registers).  Returns (all lanes) whether this row finalized the rollout's step; then
+// no = emitted tokens and lane i holds emitted token i (inputs of the fused commit).
+__device__ bool complete_row_warp(const VerifyArgs& a, unsigned long long* stat, int b, int j, int q, int status,
+                                  int cand, unsigned long long z, float norm, int lane, int& no, int32_t& tok) {
+    const int kp1 = a.k + 1;
+    const int64_t base = (int64_t)b * kp1;
+    int F = -1;
+    if (lane == 0) {
+        const int64_t r = base + j;
+        a.row_status[r] = status;
+        a.row_cand[r] = cand;
+        a.row_z[r] = z;
+        a.row_norm[r] = norm;
+        const bool decides = status != ST_CONT;
+        if (decides) atomicMin(a.roll_first + b, j);  // claim hint only (relaxed)
+        const unsigned long long mine = (1ull << j) | (decides ? (1ull << (32 + j)) : 0ull);
+        // release: this row's record; acquire: every earlier row's record of the rollout
+        const unsigned long long old = atom_or_acq_rel(a.roll_state + b, mine);
+        int F0, F1;
+        if (!prefix_decided(old, F0) && prefix_decided(old | mine, F1)) F = F1;
+    }
+    F = __shfl_sync(0xFFFFFFFFu, F, 0);
+    if (F < 0) return false;
+    __syncwarp();  // lane 0's acquire orders the other lanes' reads below
+    const int32_t* d = a.draft + (int64_t)b * a.k;
+    int32_t dl = -1, stF = status, cF = cand;
+    float nl = 0.f;
+    unsigned long long zl = 0ull;
+    // d_{F+1} is needed only for an accepted EOS at row F (this row's status is known)
+    if (lane < F || (lane == F && lane < q && (F != j || status == ST_EOS))) dl = d[lane];
+    if (lane <= F) {
+        nl = (lane == j) ? norm : __ldcg(a.row_norm + base + lane);
+        zl = (lane == j) ? z : __ldcg(a.row_z + base + lane);
+    }
+    if (lane == F && F != j) {
+        stF = __ldcg(a.row_status + base + F);
+        cF = __ldcg(a.row_cand + base + F);
+    }
+    stF = __shfl_sync(0xFFFFFFFFu, stF, F);
+    // Alg. 1 lines 10-31: d_1..d_F accepted, then the sample of row F (or its accepted EOS)
+    tok = (lane < F) ? dl : ((lane == F) ? (stF == ST_EOS ? dl : cF) : -1);
+    no = F + 1;
+    const int acc = (stF == ST_EOS) ? F + 1 : F;
+    if (lane < kp1) a.out_tokens[base + lane] = tok;
+    if (lane <= F) {
+        if (a.out_norm) a.out_norm[base + lane] = nl;
+        if (a.out_z) a.out_z[base + lane] = zl;
+    }
+    if (lane == 0) {
+        a.out_len[b] = no;
+        a.out_acc[b] = acc;
+        if (q > 0) {
+            stat[STAT_STEPS_SPEC] += 1ull;
+            stat[STAT_EMIT_SPEC] += (unsigned long long)no;
+            stat[STAT_ACCEPTED] += (unsigned long long)acc;
+            stat[STAT_PROPOSED] += (unsigned long long)q;
+            stat[STAT_HIST + min(no, STAT_HIST_BINS - 1)] += 1ull;
+        } else {
+            stat[STAT_STEPS_PLAIN] += 1ull;
+            stat[STAT_EMIT_PLAIN] += (unsigned long long)no;
+        }
+        stat[STAT_ROWS_NEEDED] += (unsigned long long)(F + 1);
+        if (a.sctl) {
+            const unsigned dn = atomicAdd(a.sctl + SC_DONE, 1u);  // scheduler termination count
+            TRACE(TR_FIN, (int)dn, b, F);
+        }
+    }
+    return true;
 }
 
 // Claim the next needed row of the plan's j-major table (Alg. 1's order across the batch),

@@ -26,8 +26,13 @@ constexpr int CK_CL = BS_CK_CL;           // CTAs per cluster (experiment)
 #else
 constexpr int CK_CL = 8;                  // CTAs per cluster
 #endif
+#ifdef BS_CK_NMW
+constexpr int CK_NMW = BS_CK_NMW;         // mass warps (experiment)
+constexpr int CK_NXW = BS_CK_NXW;         // max warps (experiment)
+#else
 constexpr int CK_NMW = 8;                 // mass warps: 0..7 (two per SM sub-partition)
 constexpr int CK_NXW = 2;                 // max warps: 8..9
+#endif
 constexpr int CK_NCW = CK_NMW + CK_NXW;
 constexpr int CK_PROD = CK_NCW;           // producer warp
 constexpr int CK_EPI = CK_NCW + 1;        // epilogue warp
@@ -43,7 +48,19 @@ constexpr int CK_MINB = BS_CK_MINB;       // min CTAs per SM (register budget ex
 #else
 constexpr int CK_MINB = 2;
 #endif
+#ifdef BS_CK_LA
+constexpr int CK_LA = BS_CK_LA;           // claimer look-ahead past the issued copies (experiment)
+#else
+constexpr int CK_LA = 2;                  // claimer look-ahead past the issued copies
+#endif
+#ifdef BS_CK_D
+constexpr int CK_D = BS_CK_D;             // descriptor / exchange ring depth (experiment)
+#else
 constexpr int CK_D = 4;                   // descriptor / exchange ring depth
+#endif
+// ring reuse (see the waits): a peer publishes row i+D only after this CTA's mass warps read
+// row i's maxima, which needs D >= 2 x buffers
+static_assert(CK_D >= 2 * CK_NB, "exchange ring shallower than twice the slice buffers");
 constexpr int CK_TILE = 512;              // elements per tile (16 per lane)
 constexpr int CK_MAXT = 104;              // tiles per slice
 constexpr int CK_MAXSL = CK_MAXT * CK_TILE;  // 53248 elements: V <= 425984
@@ -190,8 +207,10 @@ __device__ __forceinline__ TakeIssue ck_take_issue(const VerifyArgs& a, int b, i
         t.d0 = __ldcg(&rp->d0);
     }
     if (lane == 2 && rpred >= 1 && rpred <= a.k) t.dpred = a.draft[(int64_t)b * a.k + min(rpred, a.k - 1)];
-    if (lane == 3 && rpred >= 0 && rpred <= a.k)
+    if (lane == 3 && rpred >= 0 && rpred <= a.k) {
+        pdl_wait();  // row_index comes from the previous launch (the claimer starts before it ends)
         t.rnpred = a.row_index ? a.row_index[(int64_t)b * kp1 + rpred] : (int64_t)b * kp1 + rpred;
+    }
     return t;
 }
 
@@ -214,7 +233,10 @@ __device__ __forceinline__ bool ck_take_finish(const VerifyArgs& a, uint32_t epo
         if (t.rpred == 0) {
             rn = (long long)shfl_u64((unsigned long long)t.rnpred, 3);
         } else {
-            if (lane == 0) rn = a.row_index ? a.row_index[(int64_t)b * kp1] : (int64_t)b * kp1;
+            if (lane == 0) {
+                pdl_wait();
+                rn = a.row_index ? a.row_index[(int64_t)b * kp1] : (int64_t)b * kp1;
+            }
             rn = (long long)shfl_u64((unsigned long long)rn, 0);
         }
         al = ((reinterpret_cast<uintptr_t>(a.logits + rn * a.stride) & 15u) == 0) ? 1 : 0;
@@ -225,6 +247,7 @@ __device__ __forceinline__ bool ck_take_finish(const VerifyArgs& a, uint32_t epo
         } else {
             if (lane == 0) {
                 d = (r < q) ? a.draft[(int64_t)b * a.k + r] : -1;
+                pdl_wait();
                 rn = a.row_index ? a.row_index[(int64_t)b * kp1 + r] : (int64_t)b * kp1 + r;
             }
             d = __shfl_sync(0xFFFFFFFFu, d, 0);
@@ -260,7 +283,10 @@ __device__ __forceinline__ bool ck_take_row(const VerifyArgs& a, int b, int j, i
         d0 = __ldcg(&rp->d0);
     }
     if (lane == 2 && j >= 1 && j < a.k) dj = a.draft[(int64_t)b * a.k + j];
-    if (lane == 3) rnj = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+    if (lane == 3) {
+        pdl_wait();  // row_index comes from the previous launch
+        rnj = a.row_index ? a.row_index[(int64_t)b * kp1 + j] : (int64_t)b * kp1 + j;
+    }
     rf = __shfl_sync(0xFFFFFFFFu, rf, 0);
     q = __shfl_sync(0xFFFFFFFFu, q, 1);
     if (!(j <= q && j <= rf)) return false;
@@ -377,7 +403,7 @@ __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch,
         cs.nlive = __shfl_sync(0xFFFFFFFFu, nl, 0);
         // eager when every live row fits in flight at once (two per cluster): the static
         // list then enumerates every row, j-major, and a cluster leaves once it is exhausted
-        cs.eager = a.eager_ok && (long long)cs.nlive * (a.k + 1) <= 2ll * a.ncl;
+        cs.eager = a.eager_ok && (long long)cs.nlive * (a.k + 1) <= (long long)CK_NB * a.ncl;
         cs.sidx = cid;
         cs.pre_idx = -1;
     }
@@ -548,7 +574,9 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
     // No early launch_dependents: the next launch may plan before its own wait, so it must
     // not start before this one's scheduler state, plan records and fused commit are final
     // (the implicit trigger at exit).
-    if (warp >= CK_NMW) pdl_wait();
+    // The claimer waits only before its row_index loads (ck_take_*): its claims' other
+    // inputs are this launch's plan.
+    if (warp >= CK_NMW && warp != CK_CLM) pdl_wait();
     if (tid == 0) TRACE(TR_GO, 0, 0, 0);
     if (warp < CK_NMW) {
         // plan the call's rollouts, one warp each, in rounds over the grid; per round one atomic
@@ -593,7 +621,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 int issued = 0;
                 if (lane == 0) issued = *reinterpret_cast<volatile int*>(&sh.tma_issued);
                 issued = __shfl_sync(0xFFFFFFFFu, issued, 0);
-                if (r > issued + 2) {  // far enough ahead
+                if (r > issued + CK_LA) {  // far enough ahead
                     __nanosleep(128);
                     continue;
                 }
@@ -694,34 +722,33 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             if (bad) err |= DEV_BAD_LOGIT;
             else if (m == -INFINITY) err |= DEV_ALL_NEGINF;
             else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) err |= DEV_RANGE;
-            const bool lead = rank == 0 && lane == 0;
-            bool fz = false;  // lane 0 finalized the rollout's step (fused commit follows)
+            // the row's result (recorded by one CTA's epilogue warp: rank 0, or the CTA that
+            // owns the sampled token)
+            bool rec = false;
+            int c_status = ST_DECIDED, c_cand = -1;
+            unsigned long long c_z = 0ull;
+            float c_norm = 0.f;
             if (err) {
-                if (lead) {
-                    atomicOr(a.dev_err, err);
-                    sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                    fz = complete_row(a, sh.stat, b, j, q, ST_DECIDED, -1, 0ull, 0.f);
-                }
+                rec = rank == 0;
+                if (rec && lane == 0) atomicOr(a.dev_err, err);
             } else if (a.T == 0.f) {  // greedy (R1): lowest index attaining m
                 const int g = (int)er.z;
-                if (lead) {
-                    const bool acc = j < q && d == g;
-                    const int status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
-                    sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                    fz = complete_row(a, sh.stat, b, j, q, status, g, 1ull, 1.f);
-                    if (status == ST_CONT) *reinterpret_cast<volatile int*>(&sh.mail) = (b << 8) | (j + 1);
-                }
+                const bool acc = j < q && d == g;
+                rec = rank == 0;
+                c_status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
+                c_cand = g;
+                c_z = 1ull;
+                c_norm = 1.f;
             } else {
                 const float norm = (float)ldexp((double)Z, -a.S);
                 bool acc = false;
                 if (j < q) acc = uniform_floor(row_draw(a, dsc, PURPOSE_ACCEPT), Z) < md;
                 const int status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
                 if (status != ST_DECIDED) {
-                    if (lead) {
-                        sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                        fz = complete_row(a, sh.stat, b, j, q, status, -1, Z, norm);
-                        if (status == ST_CONT) *reinterpret_cast<volatile int*>(&sh.mail) = (b << 8) | (j + 1);
-                    }
+                    rec = rank == 0;
+                    c_status = status;
+                    c_z = Z;
+                    c_norm = norm;
                 } else {
                     // residual (d excluded) or bonus sample (R8): inverse CDF in ascending id
                     const int excl = (j < q) ? d : -1;
@@ -803,14 +830,21 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                             }
                         }
                         tok = __shfl_sync(0xFFFFFFFFu, tok, L2);
-                        if (lane == 0) {
-                            sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                            fz = complete_row(a, sh.stat, b, j, q, ST_DECIDED, tok, Z, norm);
-                        }
+                        rec = true;
+                        c_cand = tok;
+                        c_z = Z;
+                        c_norm = norm;
                     }
                 }
             }
-            if (a.commit && __shfl_sync(0xFFFFFFFFu, fz ? 1 : 0, 0)) commit_rollout_warp(a, b, lane, cp);
+            if (rec) {  // warp-uniform
+                if (lane == 0) sh.stat[STAT_ROWS_VERIFIED] += 1ull;
+                int no = 0;
+                int32_t ot = -1;
+                const bool fz = complete_row_warp(a, sh.stat, b, j, q, c_status, c_cand, c_z, c_norm, lane, no, ot);
+                if (lane == 0 && c_status == ST_CONT) *reinterpret_cast<volatile int*>(&sh.mail) = (b << 8) | (j + 1);
+                if (a.commit && fz) commit_rollout_warp(a, b, lane, cp, no, ot);
+            }
             __syncwarp();
             if (lane == 0) {
                 TRACE(TR_EPI1, i, dsc.b, dsc.j);
@@ -843,8 +877,9 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 uint4 v[8];
 #pragma unroll
                 for (int u2 = 0; u2 < 4; ++u2) {
-                    v[2 * u2] = lds128(buf + (t + u2 * CK_NXW) * CK_TILE + lane * 16);
-                    v[2 * u2 + 1] = lds128(buf + (t + u2 * CK_NXW) * CK_TILE + lane * 16 + 8);
+                    // lane l: elements 8l.. and 256+8l.. of the tile (conflict-free 16-byte loads)
+                    v[2 * u2] = lds128(buf + (t + u2 * CK_NXW) * CK_TILE + lane * 8);
+                    v[2 * u2 + 1] = lds128(buf + (t + u2 * CK_NXW) * CK_TILE + CK_TILE / 2 + lane * 8);
                 }
 #pragma unroll
                 for (int u2 = 0; u2 < 8; u2 += 2) {
@@ -856,7 +891,8 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             for (; t < ntile; t += CK_NXW) {
                 const int e0 = t * CK_TILE + lane * 16;
                 if (t < nfull) {
-                    const uint4 v0 = lds128(buf + e0), v1 = lds128(buf + e0 + 8);
+                    const uint4 v0 = lds128(buf + t * CK_TILE + lane * 8);
+                    const uint4 v1 = lds128(buf + t * CK_TILE + CK_TILE / 2 + lane * 8);
                     mx = hmax2_nan_u32(mx, hmax2_nan_u32(hmax2_nan_u32(v0.x, v0.y), hmax2_nan_u32(v0.z, v0.w)));
                     mx1 = hmax2_nan_u32(mx1, hmax2_nan_u32(hmax2_nan_u32(v1.x, v1.y), hmax2_nan_u32(v1.z, v1.w)));
                 } else {
@@ -958,14 +994,16 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
 #endif
                 };
                 if (a.S <= 44) {  // FMA-pipe conversion for half the elements (mass16_mixed)
+                    // lane l: elements 8l.. and 256+8l.. of tile t (conflict-free 16-byte loads;
+                    // the tile sum does not depend on which lane holds which element)
                     for (int t = warp; t < nfull; t += CK_NMW) {
-                        const int e0 = t * CK_TILE + lane * 16;
-                        tile_done(t, mass16_mixed(lds128(buf + e0), lds128(buf + e0 + 8), mp));
+                        const int e0 = t * CK_TILE + lane * 8;
+                        tile_done(t, mass16_mixed(lds128(buf + e0), lds128(buf + e0 + CK_TILE / 2), mp));
                     }
                 } else {
                     for (int t = warp; t < nfull; t += CK_NMW) {
-                        const int e0 = t * CK_TILE + lane * 16;
-                        tile_done(t, mass8(lds128(buf + e0), mp) + mass8(lds128(buf + e0 + 8), mp));
+                        const int e0 = t * CK_TILE + lane * 8;
+                        tile_done(t, mass8(lds128(buf + e0), mp) + mass8(lds128(buf + e0 + CK_TILE / 2), mp));
                     }
                 }
                 if (nfull < ntile && warp == nfull % CK_NMW) {  // the ragged last tile

@@ -340,3 +340,25 @@ if os.environ.get("TRACE_CLAIMS"):
             bysrc.setdefault(src, []).append(tt - c0[key_])
     for src, v in sorted(bysrc.items()):
         print(f"  claim duration src {src}: n={len(v)} median {np.median(v):.2f} p75 {np.percentile(v, 75):.2f} p90 {np.percentile(v, 90):.2f} us")
+if os.environ.get("TRACE_CHAIN"):
+    # the rollouts finalized last: per row, claim end / TMA issue / epilogue end (leader) and source
+    fin = sorted(((float(tt), int(b_), int(j_)) for tt, ty, b_, j_ in zip(t, typ, bb, jj) if ty == 10), reverse=True)
+    rows = {}
+    for tt, ty, sq, b_, j_, bk in zip(t, typ, seq, bb, jj, blk):
+        if int(bk) % 8:
+            continue
+        if ty == 1 and int(b_) != 0xFFFF:
+            rows.setdefault((int(b_), int(j_)), {})["claim"] = (float(tt), int(sq) >> 12, int(bk) // 8)
+        if ty == 2:
+            rows.setdefault((int(b_), int(j_)), {}).setdefault("tma", float(tt))
+        if ty == 8:
+            rows.setdefault((int(b_), int(j_)), {})["epi"] = float(tt)
+    for ft, fb, fF in fin[:int(os.environ["TRACE_CHAIN"])]:
+        print(f"  rollout {fb}: finalized at {ft:.1f} us, F={fF}")
+        for j in range(k + 1):
+            r_ = rows.get((fb, j))
+            if not r_:
+                continue
+            c_ = r_.get("claim", (float("nan"), -1, -1))
+            print(f"     row {j}: claim {c_[0]:6.1f} src {c_[1]} cl {c_[2]:2d}  tma {r_.get('tma', float('nan')):6.1f}  "
+                  f"epi end {r_.get('epi', float('nan')):6.1f}")
