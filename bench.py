@@ -206,15 +206,16 @@ def run_ours(args, cfg, rank, world, dist):
             with torch.cuda.graph(g, stream=stream):
                 for i in range(chunk):
                     c, t = ctx, eng.target
-                    c.bs_draft_lookup(eng.rl_step, eng.slots, k, eng.draft, eng.draft_len,
-                                      eng.match_len, stream=stream)
+                    # the drafts of this step: from the previous verify launch (fused lookup;
+                    # the first step's from eng.begin)
                     c.bsx_target_rows(eng.slots, eng.draft, eng.draft_len, k, t.target_seed,
                                       t.mode, t.nbank, eng.row_index, stream=stream)
                     if instrument:
                         ev_s[i].record(stream)
-                    c.bs_verify_commit(eng.slots, t.bank, eng.row_index, V, eng.draft,
-                                       eng.draft_len, k, eng.T, eng.top_p, eng.out_tokens,
-                                       eng.out_len, eng.out_acc, eng.finished, stream=stream)
+                    c.bs_verify_commit_lookup(eng.rl_step, eng.slots, t.bank, eng.row_index, V, eng.draft,
+                                              eng.draft_len, k, eng.T, eng.top_p, eng.out_tokens,
+                                              eng.out_len, eng.out_acc, eng.finished, eng.match_len,
+                                              stream=stream)
                     if instrument:
                         ev_e[i].record(stream)
         return g
@@ -262,7 +263,7 @@ def run_ours(args, cfg, rank, world, dist):
             mark()
         g = capture(instrument)
         mark()
-        rec["launches"] += 2 + rec["seal_launches"]
+        rec["launches"] += 2 + int(eng.fuse_lookup) + rec["seal_launches"]  # put, begin, first lookup
         steps, chunks = 0, 0
         if instrument:  # events are re-recorded by every replay: one chunk at a time
             while True:
@@ -282,7 +283,7 @@ def run_ours(args, cfg, rank, world, dist):
             steps += replay_until_done(g)
         mark()
         rec["decode_steps"] += steps
-        rec["launches"] += steps * RolloutEngine.LAUNCHES_PER_STEP
+        rec["launches"] += steps * eng.launches_per_step
         if phases:
             dt = [1e3 * (b - a) for a, b in zip(tp, tp[1:])]
             log("[phases ms] put %.1f seal %.1f begin %.1f capture %.1f decode %.1f" % tuple(dt[:5]))

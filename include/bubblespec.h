@@ -214,6 +214,25 @@ bs_status bs_verify_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const v
                            int32_t* out_accepted, float* out_norm, uint64_t* out_z,
                            int32_t* finished, void* stream);
 
+/* bs_verify_commit followed by bs_draft_lookup for the NEXT decoding step (Alg. 1's loop:
+ * the draft of step t+1 is the pool lookup from the context committed at step t),
+ * fused into the same launch where bs_verify_commit is fused: the warp that commits a
+ * rollout then looks up its next draft from the just-committed state (held in registers).
+ *   draft_tokens / draft_len  IN: this step's drafts (as bs_verify_commit);
+ *                             OUT: the next step's drafts for the same slots and k
+ *                             (bs_draft_lookup's outputs), written in place
+ *   match_len    [n] next-step anchored match length (may be NULL)
+ *   rl_step      the index must be sealed for it (as bs_draft_lookup: BS_ERR_STALE)
+ * Other arguments as bs_verify_commit.  Results, rollout state and next drafts are identical
+ * to bs_verify_commit + bs_draft_lookup (tested); where the launch cannot fuse (top_p < 1, V
+ * above the cluster kernel's limit) the separate kernels run. */
+bs_status bs_verify_commit_lookup(bs_ctx* ctx, uint64_t rl_step, int32_t n, const int32_t* slots,
+                                  const void* logits_bf16, const int64_t* row_index,
+                                  int64_t row_stride_elems, int32_t* draft_tokens, int32_t* draft_len,
+                                  int32_t k, bs_sampling sampling, int32_t* out_tokens, int32_t* out_len,
+                                  int32_t* out_accepted, float* out_norm, uint64_t* out_z,
+                                  int32_t* finished, int32_t* match_len, void* stream);
+
 /* Commit (Alg. 1 lines 15/22 "y <- y o a"): append out_len[b] tokens of row b of
  * out_tokens [n*(k+1)] to each rollout, advance its position, and mark it
  * finished on an emitted EOS or when pos reaches max_len (Alg. 1 line 2).

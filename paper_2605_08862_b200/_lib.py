@@ -54,6 +54,8 @@ SIGNATURES = {
                                  _V, _V, _V, _V]),
     "bs_verify_commit": (C.c_int, [_V, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V, _V,
                                    _V, _V, _V, _V, _V]),
+    "bs_verify_commit_lookup": (C.c_int, [_V, _U64, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V,
+                                          _V, _V, _V, _V, _V, _V, _V]),
     "bs_commit": (C.c_int, [_V, _I32, _V, _V, _V, _I32, _V, _V]),
     "bs_stats_read": (C.c_int, [_V, _V, _I32, _I32, _V]),
     "bs_rollout_bind_output": (C.c_int, [_V, _V, _I64]),

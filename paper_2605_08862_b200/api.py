@@ -128,6 +128,19 @@ class Context:
                                            _p(out_accepted), _p(out_norm), _p(out_z), _p(finished),
                                            _stream(stream, self.device)), "bs_verify_commit")
 
+    def bs_verify_commit_lookup(self, rl_step, slots, logits, row_index, row_stride, draft_tokens,
+                                draft_len, k, temperature, top_p, out_tokens, out_len, out_accepted,
+                                finished=None, match_len=None, out_norm=None, out_z=None, stream=None):
+        """bs_verify_commit, then this step's commit feeds the next step's draft lookup in the
+        same launch: draft_tokens / draft_len are overwritten with the next step's drafts."""
+        sp = bs_sampling(temperature, top_p)
+        _chk(self, load().bs_verify_commit_lookup(self.handle, rl_step, slots.numel(), _p(slots), _p(logits),
+                                                  _p(row_index), row_stride, _p(draft_tokens),
+                                                  _p(draft_len), k, sp, _p(out_tokens), _p(out_len),
+                                                  _p(out_accepted), _p(out_norm), _p(out_z), _p(finished),
+                                                  _p(match_len), _stream(stream, self.device)),
+             "bs_verify_commit_lookup")
+
     def bs_commit(self, slots, out_tokens, out_len, k, finished=None, stream=None):
         _chk(self, load().bs_commit(self.handle, slots.numel(), _p(slots), _p(out_tokens),
                                     _p(out_len), k, _p(finished), _stream(stream, self.device)),

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "ctx.h"
+#include "lookup.cuh"
 
 using namespace bs;
 
@@ -313,6 +314,42 @@ bs_status bs_verify_commit(bs_ctx* c, int32_t n, const int32_t* slots, const voi
        "bs_verify_commit");
     if (!fused)  // kernels without the fused commit: the commit kernel follows
         CK(c, launch_commit(c, n, slots, out_tokens, out_len, k, finished, S(stream)), "bs_verify_commit");
+    return BS_OK;
+}
+
+bs_status bs_verify_commit_lookup(bs_ctx* c, uint64_t rl_step, int32_t n, const int32_t* slots,
+                                  const void* logits, const int64_t* row_index, int64_t stride,
+                                  int32_t* draft_tokens, int32_t* draft_len, int32_t k, bs_sampling sp,
+                                  int32_t* out_tokens, int32_t* out_len, int32_t* out_accepted,
+                                  float* out_norm, uint64_t* out_z, int32_t* finished, int32_t* match_len,
+                                  void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (!c->sealed.valid || c->sealed.step != rl_step)
+        return fail(c, BS_ERR_STALE, "index not sealed for rl_step %llu", (unsigned long long)rl_step);
+    if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
+    if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
+    if (stride < c->cfg.vocab) return fail(c, BS_ERR_INVALID, "row stride < vocab");
+    if (!(sp.temperature >= 0.f) || sp.temperature == INFINITY)
+        return fail(c, BS_ERR_INVALID, "temperature must be finite and >= 0");
+    if (!(sp.top_p > 0.f && sp.top_p <= 1.f)) return fail(c, BS_ERR_INVALID, "top_p must be in (0, 1]");
+    if (sp.temperature > 0.f && !((float)(1.4426950408889634 / (double)sp.temperature) < INFINITY))
+        return fail(c, BS_ERR_INVALID, "temperature too small");
+    if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
+              (k && !draft_tokens)))
+        return fail(c, BS_ERR_INVALID, "null array");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bool fused = false, looked = false;
+    const LookupArgs lk = lookup_args(c, n, slots, k, draft_tokens, draft_len, match_len);
+    CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
+                        sp.temperature, sp.top_p, out_tokens, out_len, out_accepted, out_norm,
+                        reinterpret_cast<unsigned long long*>(out_z), S(stream), finished, &fused, &lk,
+                        &looked),
+       "bs_verify_commit_lookup");
+    if (!fused)
+        CK(c, launch_commit(c, n, slots, out_tokens, out_len, k, finished, S(stream)), "bs_verify_commit_lookup");
+    if (!looked)
+        CK(c, launch_lookup(c, n, slots, k, draft_tokens, draft_len, match_len, S(stream)),
+           "bs_verify_commit_lookup");
     return BS_OK;
 }
 

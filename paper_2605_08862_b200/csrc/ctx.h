@@ -150,12 +150,18 @@ struct bs_ctx {
 
 namespace bs {
 // launchers implemented in the .cu files
+struct LookupArgs;
+LookupArgs lookup_args(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k, int32_t* draft,
+                       int32_t* draft_len, int32_t* match_len);
+// committed / looked_up (optional): set when the launch also committed (bs_verify_commit) /
+// also looked up the next step's drafts described by `lookup` (bs_verify_commit_lookup)
 cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits,
                           const int64_t* row_index, int64_t stride, const int32_t* draft,
                           const int32_t* draft_len, int32_t k, float T, float top_p,
                           int32_t* out_tokens, int32_t* out_len, int32_t* out_acc,
                           float* out_norm, unsigned long long* out_z, cudaStream_t st,
-                          int32_t* commit_finished = nullptr, bool* committed = nullptr);
+                          int32_t* commit_finished = nullptr, bool* committed = nullptr,
+                          const LookupArgs* lookup = nullptr, bool* looked_up = nullptr);
 cudaError_t launch_lookup(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k,
                           int32_t* draft, int32_t* draft_len, int32_t* match_len,
                           cudaStream_t st);

@@ -29,6 +29,7 @@
 #include "ctx.h"
 #include "ptx.cuh"
 #include "verify_math.cuh"
+#include "lookup.cuh"
 
 namespace bs {
 
@@ -144,6 +145,10 @@ struct VerifyArgs {
     int64_t c_resp_stride;
     int ncl;                      // clusters in the grid
     int eager_ok;                 // small live batches claim every row at once
+    // fused lookup (bs_verify_commit_lookup): after its commit, the finalizing warp looks up
+    // the rollout's next draft from the committed state (lk.draft / draft_len: the next step's)
+    int lookup;
+    LookupArgs lk;
 };
 
 struct RowDesc {
@@ -190,6 +195,8 @@ struct __align__(16) VShared {
 // verify launch.  Lane i owns tail slot i (M <= 32) and emitted token i (<= k+1 <= 32).
 struct CommitPre {
     int s, p, L, cl, old;  // slot, pos, max_len, ctx_len; lane i: tail slot i
+    int P;                 // prompt (fused lookup)
+    IndexDesc x;           // the sealed index (fused lookup)
 };
 __device__ __forceinline__ CommitPre commit_prefetch(const VerifyArgs& a, int slot, int lane) {
     CommitPre c;
@@ -198,6 +205,10 @@ __device__ __forceinline__ CommitPre commit_prefetch(const VerifyArgs& a, int sl
     c.L = a.max_len[slot];
     c.cl = a.c_ctx_len[slot];
     c.old = (lane < a.M) ? a.c_tail[(int64_t)slot * a.M + lane] : -1;
+    if (a.lookup) {
+        c.P = a.lk.prompt[slot];
+        c.x = *a.lk.desc;
+    }
     return c;
 }
 
@@ -212,7 +223,8 @@ __device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane, const 
     const int src = lane + no;  // new tail[i] = (old ++ out)[i + no]
     const int32_t from_old = __shfl_sync(0xFFFFFFFFu, old, src & 31);
     const int32_t from_out = __shfl_sync(0xFFFFFFFFu, ot, (src - M) & 31);
-    if (lane < M) tl[lane] = (src < M) ? from_old : from_out;
+    const int32_t nt = (src < M) ? from_old : from_out;  // new tail[lane]
+    if (lane < M) tl[lane] = nt;
     if (a.c_resp && lane < no && p + lane < a.c_resp_stride) a.c_resp[(int64_t)s * a.c_resp_stride + p + lane] = ot;
     const int32_t last = __shfl_sync(0xFFFFFFFFu, ot, (no - 1) & 31);
     const int f = ((a.eos >= 0 && last == a.eos) || p + no >= L) ? 1 : 0;
@@ -221,6 +233,10 @@ __device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane, const 
         a.c_pos[s] = p + no;
         if (f) a.c_finished[s] = 1;
         if (a.c_fin_out) a.c_fin_out[b] = f;
+    }
+    if (a.lookup) {  // the next step's draft from the committed state: y[-1-lane] = tail[M-1-lane]
+        const int32_t y = __shfl_sync(0xFFFFFFFFu, nt, (M - 1 - lane) & 31);
+        lookup_rollout(a.lk, c.x, b, min(M, c.cl + no), c.P, p + no, L, f != 0, lane < M ? y : -1, lane);
     }
 }
 
@@ -896,8 +912,10 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
                           const int32_t* draft_len, int32_t k, float T, float top_p,
                           int32_t* out_tokens, int32_t* out_len, int32_t* out_acc,
                           float* out_norm, unsigned long long* out_z, cudaStream_t st,
-                          int32_t* commit_finished, bool* committed) {
+                          int32_t* commit_finished, bool* committed, const LookupArgs* lookup,
+                          bool* looked_up) {
     if (committed) *committed = false;
+    if (looked_up) *looked_up = false;
     if (n == 0) return cudaSuccess;
     const int V = ctx->cfg.vocab;
     const bool topp = T > 0.f && top_p < 1.f;
@@ -971,6 +989,11 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             a.c_resp = ctx->responses;
             a.c_resp_stride = ctx->resp_stride;
             *committed = true;
+            if (lookup && looked_up) {  // fused lookup (bs_verify_commit_lookup)
+                a.lookup = 1;
+                a.lk = *lookup;
+                *looked_up = true;
+            }
         }
     }
     if (topp) {  // R5: top-p filtered rows (verify_topp.cuh)

@@ -603,6 +603,24 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             named_bar(3, CK_NMW * 32);  // plan_b reusable
         }
         pdl_wait();
+        if (a.lookup) {
+            // fused lookup for the rollouts without rows (finished, out of length, bad draft):
+            // their (empty) commit was the plan's; the finalizing epilogue warps look up the
+            // others.  After the wait: the launch before this one (the target) reads the drafts.
+            __syncwarp();
+            for (int base = (int)blockIdx.x * CK_NMW; base < a.n; base += (int)gridDim.x * CK_NMW) {
+                const int b = base + warp;
+                if (b >= a.n) break;
+                const int q = __shfl_sync(0xFFFFFFFFu, lane == 0 ? a.rrec[b].q : 0, 0);  // own store
+                if (q >= 0) continue;
+                const LookupArgs& lk = a.lk;
+                const int sl = a.slots[b];
+                const int M = lk.M;
+                const int tr = (lane < M) ? lk.tail[(int64_t)sl * M + (M - 1 - lane)] : -1;
+                lookup_rollout(lk, *lk.desc, b, lk.ctx_len[sl], lk.prompt[sl], lk.pos[sl], lk.max_len[sl],
+                               lk.finished[sl] != 0, tr, lane);
+            }
+        }
     }
 
     if (warp == CK_CLM) {

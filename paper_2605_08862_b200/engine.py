@@ -31,9 +31,14 @@ class Target:
 
 class RolloutEngine:
     def __init__(self, ctx: Context, n: int, k: int, temperature: float, top_p: float,
-                 target: Target, stream: torch.cuda.Stream | None = None, fused: bool = True):
+                 target: Target, stream: torch.cuda.Stream | None = None, fused: bool = True,
+                 fuse_lookup: bool = True):
         self.ctx, self.n, self.k = ctx, n, k
         self.fused = fused  # bs_verify_commit (one launch) instead of bs_verify_step + bs_commit
+        # bs_verify_commit_lookup: each launch also looks up the next step's drafts (the first
+        # step's lookup runs in begin()), so a decoding step is target rows + one launch
+        self.fuse_lookup = fused and fuse_lookup
+        self.launches_per_step = 2 if self.fuse_lookup else 3
         self.T, self.top_p, self.target = temperature, top_p, target
         dev = torch.device("cuda", ctx.device)
         # a dedicated stream: CUDA graphs cannot be captured on the legacy default stream
@@ -73,16 +78,24 @@ class RolloutEngine:
         self._sync_inputs()
         self.ctx.bs_rollout_begin(self.slots, uids, prompt_ids, prompt_tail, max_len,
                                   stream=self.stream)
+        if self.fuse_lookup:  # the first step's drafts (later ones come from the verify launch)
+            self.ctx.bs_draft_lookup(self.rl_step, self.slots, self.k, self.draft, self.draft_len,
+                                     self.match_len, stream=self.stream)
 
     # ------------------------------------------------------------------ decoding
     def step(self):
         c, k, s = self.ctx, self.k, self.stream
-        c.bs_draft_lookup(self.rl_step, self.slots, k, self.draft, self.draft_len, self.match_len,
-                          stream=s)
+        if not self.fuse_lookup:
+            c.bs_draft_lookup(self.rl_step, self.slots, k, self.draft, self.draft_len, self.match_len,
+                              stream=s)
         t = self.target
         c.bsx_target_rows(self.slots, self.draft, self.draft_len, k, t.target_seed, t.mode,
                           t.nbank, self.row_index, stream=s)
-        if self.fused:
+        if self.fuse_lookup:
+            c.bs_verify_commit_lookup(self.rl_step, self.slots, t.bank, self.row_index, t.bank.shape[1],
+                                      self.draft, self.draft_len, k, self.T, self.top_p, self.out_tokens,
+                                      self.out_len, self.out_acc, self.finished, self.match_len, stream=s)
+        elif self.fused:
             c.bs_verify_commit(self.slots, t.bank, self.row_index, t.bank.shape[1], self.draft,
                                self.draft_len, k, self.T, self.top_p, self.out_tokens, self.out_len,
                                self.out_acc, self.finished, stream=s)
@@ -92,8 +105,8 @@ class RolloutEngine:
                              self.out_acc, stream=s)
             c.bs_commit(self.slots, self.out_tokens, self.out_len, k, self.finished, stream=s)
 
-    # lookup, target rows, verify (+ fused commit; top-p < 1: plan, rows and commit kernels)
-    LAUNCHES_PER_STEP = 3
+    # target rows + verify (fused commit and next lookup), or lookup + target rows + verify;
+    # top-p < 1 adds the plan / commit / lookup kernels
 
     def capture(self, steps: int):
         """Capture `steps` decoding steps into one CUDA graph (replayed by run_graph)."""

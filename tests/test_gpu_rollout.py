@@ -10,7 +10,7 @@ from workloads import TargetSpec  # noqa: E402
 from tests.gpu_util import bank_numpy, pools_for, setup_rollouts, to_dev  # noqa: E402
 
 
-def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fused=True):
+def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fused="lookup"):
     from paper_2605_08862_b200.engine import RolloutEngine, Target
 
     ctx = bs.Context(vocab=spec.V, eos_id=eos, k_max=k, match_max=M, max_rollouts=n,
@@ -18,8 +18,10 @@ def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fuse
                      seed=seed)
     bank = to_dev(bank_numpy(spec).view(np.int16))
     mode = {"position": 0, "markov": 1, "mixed": 2}[spec.mode]
+    # "lookup": bs_verify_commit_lookup; "commit": lookup + bs_verify_commit; "none": lookup +
+    # bs_verify_step + bs_commit
     eng = RolloutEngine(ctx, n, k, T, top_p, Target(bank, spec.nbank, spec.target_seed, mode),
-                        fused=fused)
+                        fused=fused != "none", fuse_lookup=fused == "lookup")
     return ctx, eng
 
 
@@ -36,7 +38,7 @@ def _oracle_rollouts(orc, spec, pid, tail_rows, uids, ml, pools_np, k, M, T, top
     return ros
 
 
-@pytest.mark.parametrize("fused", [True, False])  # bs_verify_commit vs bs_verify_step + bs_commit
+@pytest.mark.parametrize("fused", ["lookup", "commit", "none"])
 @pytest.mark.parametrize("T,mode", [(0.0, "markov"), (1.0, "markov"), (1.0, "mixed"),
                                     (0.7, "position")])
 def test_tiny_rollouts_token_for_token(bs, orc, T, mode, fused):
@@ -118,3 +120,66 @@ def test_qwen_shaped_sampled_parity(bs, orc):
         assert [int(x) for x in got[b, : len(ro.generated)]] == ro.generated, b
     st = eng.stats()
     assert st["verify_steps"] > 0 and st["accepted"] > 0
+
+
+def _run_engine(bs, spec, pid, tail_rows, uids, ml, pools_np, k, M, T, top_p, seed, fused, steps, chunk):
+    n = len(pid)
+    ctx, eng = _engine(bs, spec, n, k, M, T, top_p, seed, -1, len(pools_np[2]), len(pools_np[0]),
+                       fused=fused)
+    L = int(ml.max())
+    resp = torch.full((n, L), -1, dtype=torch.int32, device="cuda")
+    ctx.bs_rollout_bind_output(resp, L)
+    eng.put_pools(1, to_dev(pools_np[0]), to_dev(pools_np[1]), to_dev(pools_np[2]))
+    eng.seal(1)
+    eng.begin(to_dev(uids.view(np.int64)), to_dev(pid), to_dev(tail_rows), to_dev(ml))
+    if chunk:
+        eng.capture(chunk)  # (runs one eager step first)
+        for _ in range(steps // chunk):
+            eng.run_graph()
+    else:
+        for _ in range(steps):
+            eng.step()
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() == 0
+    if fused != "lookup":  # the next step's drafts, as the fused launch leaves them
+        ctx.bs_draft_lookup(eng.rl_step, eng.slots, k, eng.draft, eng.draft_len, eng.match_len,
+                            stream=eng.stream)
+        torch.cuda.synchronize()
+    st = eng.stats()
+    return dict(resp=resp.cpu().numpy(), draft=eng.draft.cpu().numpy(), dlen=eng.draft_len.cpu().numpy(),
+                mlen=eng.match_len.cpu().numpy(), fin=eng.finished.cpu().numpy(), st=st)
+
+
+@pytest.mark.parametrize("top_p", [1.0, 0.9])  # 0.9: the unfused fallback (verify, commit, lookup kernels)
+def test_fused_lookup_matches_separate_lookup_tiny(bs, top_p):
+    """bs_verify_commit_lookup leaves exactly the state, responses and next drafts of
+    bs_verify_commit + bs_draft_lookup (short rollouts: most finish inside the run)."""
+    spec = TargetSpec(V=1024, nbank=256, mode="position", beta=12.0)  # p_peak ~0.9: long accepts
+    M, k, seed = 16, 4, 21
+    ml_ = np.random.default_rng(3).integers(8, 60, 16)
+    prompts, tails, pid, tail_rows, uids, ml = setup_rollouts(spec, 2, 8, M, ml_)
+    pools_np = pools_for(spec, prompts, tails, 8, np.full(16, 60), 0.85, prefix=M)
+    a = _run_engine(bs, spec, pid, tail_rows, uids, ml, pools_np, k, M, 1.0, top_p, seed, "commit", 40, 0)
+    b = _run_engine(bs, spec, pid, tail_rows, uids, ml, pools_np, k, M, 1.0, top_p, seed, "lookup", 40, 0)
+    for key in ("resp", "draft", "dlen", "mlen", "fin"):
+        assert np.array_equal(a[key], b[key]), key
+    drop = lambda d: {x: v for x, v in d.items() if x != "rows_verified"}  # noqa: E731 (speculation)
+    assert drop(a["st"]) == drop(b["st"])
+    assert a["fin"].sum() > 0 and a["st"]["accepted"] > 0
+
+
+def test_fused_lookup_matches_separate_lookup_q7(bs):
+    """Q7 shape (V=151936, 256 rollouts, k=8), the bench's launch path (CUDA graph chunks):
+    fused and separate lookups give identical responses, drafts and statistics."""
+    spec = TargetSpec(V=151936, nbank=512, mode="position", beta=12.0)
+    M, k, seed = 32, 8, 23
+    prompts, tails, pid, tail_rows, uids, ml = setup_rollouts(spec, 16, 16, M, 160)
+    rng = np.random.default_rng(1)
+    pools_np = pools_for(spec, prompts, tails, 16, rng.integers(60, 200, 256), 0.9, prefix=M)
+    a = _run_engine(bs, spec, pid, tail_rows, uids, ml, pools_np, k, M, 1.0, 1.0, seed, "commit", 64, 16)
+    b = _run_engine(bs, spec, pid, tail_rows, uids, ml, pools_np, k, M, 1.0, 1.0, seed, "lookup", 64, 16)
+    for key in ("resp", "draft", "dlen", "mlen", "fin"):
+        assert np.array_equal(a[key], b[key]), key
+    drop = lambda d: {x: v for x, v in d.items() if x != "rows_verified"}  # noqa: E731 (speculation)
+    assert drop(a["st"]) == drop(b["st"])
+    assert a["st"]["accepted"] > 0 and (a["mlen"] > 0).any()
