@@ -559,8 +559,9 @@ def main():
                     "steady_algorithmic": steady_alg, "steady_moved": steady_moved},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": "bs_verify_commit (verify_cluster_kernel: in-kernel plan, rows, "
-                               "fused commit), avg over an instrumented replay of the timed RL steps",
+                     "kernel": "bs_verify_commit_lookup (verify_cluster_kernel: in-kernel plan, rows, "
+                               "fused commit and next-draft lookup), avg over an instrumented replay "
+                               "of the timed RL steps",
                      "peak_source": peak_src,
                      "steady_frac": steady_alg / hbm},
         "clocks": r["clocks"],

@@ -80,7 +80,7 @@ def full(path, tag):
     st = sum(x for x, _ in stalls) or 1
     out = [f"# verify kernel — one full ncu capture ({tag})", "",
            f"Source: `{os.path.basename(path)}` (`ncu --set full --clock-control none "
-           "--import-source on -k regex:verify_cluster -s 100 -c 1` inside `bench.py --steps 1`: a full-batch launch early in the RL step).", "",
+           "--import-source on -k regex:verify_cluster -s 200 -c 1` inside `bench.py --steps 1`: a full-batch launch early in the RL step).", "",
            "| metric | value |", "|---|---|"]
     for k in keys:
         v, u = g(k)

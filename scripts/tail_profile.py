@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--chunk", type=int, default=64)
 ap.add_argument("--config", default="q7")
 ap.add_argument("--no-events", action="store_true", help="time whole chunks only (no event nodes)")
+ap.add_argument("--separate", action="store_true", help="lookup kernel + bs_verify_commit (default: fused lookup)")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 dev = torch.device("cuda", 0)
@@ -44,7 +45,7 @@ def d(x):
 chunk = a.chunk
 # ev[i][0..4]: before lookup, target rows, verify, commit, after commit
 ev = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(5)] for _ in range(chunk)]
-OPS = ["lookup", "target_rows", "verify", "commit"]
+OPS = ["lookup", "target_rows", "verify", "commit"]  # (fused: lookup inside verify)
 import time as _time  # noqa: E402
 
 for rl in (1, 2):
@@ -65,17 +66,24 @@ for rl in (1, 2):
             for i in range(chunk):
                 if rec:
                     ev[i][0].record(stream)
-                ctx.bs_draft_lookup(eng.rl_step, eng.slots, k, eng.draft, eng.draft_len,
-                                    eng.match_len, stream=stream)
+                if a.separate:  # the lookup kernel (else: fused into the previous verify launch)
+                    ctx.bs_draft_lookup(eng.rl_step, eng.slots, k, eng.draft, eng.draft_len,
+                                        eng.match_len, stream=stream)
                 if rec:
                     ev[i][1].record(stream)
                 ctx.bsx_target_rows(eng.slots, eng.draft, eng.draft_len, k, eng.target.target_seed,
                                     eng.target.mode, eng.target.nbank, eng.row_index, stream=stream)
                 if rec:
                     ev[i][2].record(stream)
-                ctx.bs_verify_commit(eng.slots, bank, eng.row_index, V, eng.draft, eng.draft_len, k,
-                                     eng.T, eng.top_p, eng.out_tokens, eng.out_len, eng.out_acc,
-                                     eng.finished, stream=stream)
+                if a.separate:
+                    ctx.bs_verify_commit(eng.slots, bank, eng.row_index, V, eng.draft, eng.draft_len, k,
+                                         eng.T, eng.top_p, eng.out_tokens, eng.out_len, eng.out_acc,
+                                         eng.finished, stream=stream)
+                else:
+                    ctx.bs_verify_commit_lookup(eng.rl_step, eng.slots, bank, eng.row_index, V, eng.draft,
+                                                eng.draft_len, k, eng.T, eng.top_p, eng.out_tokens,
+                                                eng.out_len, eng.out_acc, eng.finished, eng.match_len,
+                                                stream=stream)
                 if rec:
                     ev[i][3].record(stream)
                 pass
