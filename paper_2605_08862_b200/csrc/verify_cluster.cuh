@@ -151,7 +151,6 @@ __device__ bool ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
                 if (f && !a.finished[sl]) a.c_finished[sl] = 1;
                 if (a.c_fin_out) a.c_fin_out[b] = f;
             }
-            atomicAdd(a.sctl + SC_DONE, 1u);
         }
         // publish the plan (release: the record and resets above first): claim word =
         // epoch << 32 | (q + 1) << 24 | next row (0)
@@ -593,6 +592,8 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                     np += sh.plan_b[w] != -2;
                     nl += sh.plan_b[w] >= 0;
                 }
+                // rollouts without rows are done (one termination-count atomic per CTA round)
+                if (np > nl) atomicAdd(a.sctl + SC_DONE, (unsigned)(np - nl));
                 const unsigned long long cnt = atomicAdd(reinterpret_cast<unsigned long long*>(a.sctl + SC_NLIVE),
                                                          ((unsigned long long)np << 32) | (unsigned long long)nl);
                 unsigned slot = (uint32_t)cnt;
@@ -1069,9 +1070,12 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
         if (a.stats)
             for (int i = 0; i < STAT_COUNT; ++i)
                 if (sh.stat[i]) atomicAdd(a.stats + i, sh.stat[i]);
-        // the last CTA out resets the scheduler words for the next launch
+    }
+    // the last cluster out resets the scheduler words for the next launch (one exit atomic per
+    // cluster: the cluster barrier above means its 8 CTAs are past every scheduler access)
+    if (tid == 0 && rank == 0) {
         __threadfence();
-        if (atomicAdd(a.sctl + SC_EXIT, 1u) == gridDim.x - 1) {
+        if (atomicAdd(a.sctl + SC_EXIT, 1u) == gridDim.x / CK_CL - 1) {
             a.sctl[SC_STATIC] = 0u;
             a.sctl[SC_NLIVE] = 0u;
             a.sctl[SC_PLANNED] = 0u;
