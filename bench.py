@@ -3,8 +3,9 @@ verified tokens/s/GPU at V=151936, k=8; mean accepted length; HBM GB/s).
 
 One bench STEP = one RL step of the whole hot path on one synthetic
 batch: pool put (a8) -> cross-rank exchange (a9, N > 1) -> index build (a8) -> rollout begin
--> decoding until every rollout finished (EOS / max_len), each decoding step being lookup
-(a1) -> synthetic target rows -> verify (a2-a6) -> commit (a7).  Inputs (pools, prompt
+-> first lookup (a1) -> decoding until every rollout finished (EOS / max_len), each decoding
+step being synthetic target rows -> one bs_verify_commit_lookup launch: verify (a2-a6),
+commit (a7) and the next step's lookup (a1).  Inputs (pools, prompt
 tails, lengths, the 2.5 GB logit bank) are resident in HBM before the timed region.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config q7]
