@@ -35,6 +35,11 @@ CONFIGS = {
     "q7": dict(V=151936, prompts=16, G=16, k=8, M=32, T=1.0, top_p=1.0, mean_len=4096,
                sigma=0.6, cap=32768, nbank=8192, beta=15.75, match_rate=0.8, noise=0.02,
                G_pre=16, pool_frac=2.0 / 3.0),
+    # configs[2]: "long-context: V=151936, 64 rollouts, 32k-token responses, k=16, draft pool
+    # 8 drafts/prompt, top-p 0.95"
+    "lc": dict(V=151936, prompts=8, G=8, k=16, M=32, T=1.0, top_p=0.95, mean_len=8192,
+               sigma=0.6, cap=32768, nbank=8192, beta=15.75, match_rate=0.8, noise=0.02,
+               G_pre=8, pool_frac=2.0 / 3.0),
     # configs[0]: the small case the oracle finishes in seconds
     "tiny": dict(V=1024, prompts=1, G=4, k=4, M=16, T=1.0, top_p=1.0, mean_len=64, sigma=0.0,
                  cap=64, nbank=256, beta=6.0, match_rate=0.9, noise=0.02, G_pre=4,

@@ -60,7 +60,8 @@ __global__ void commit_kernel(int n, int M, int k, int eos, const int32_t* slots
             pos[s] = p + no;
             if (f) finished[s] = 1;
         }
-    } else if (p >= L) {
+    } else if (!fin) {  // out of length, or an empty block of a live rollout: an error stop
+        // (a needed row or the draft was invalid, reading R0; the error word says which)
         f = 1;
         if (lane == 0) finished[s] = 1;
     }

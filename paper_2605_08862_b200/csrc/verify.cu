@@ -46,7 +46,10 @@ constexpr int MAXG = 32;            // max super-chunks (2 chunks each): V <= 52
 constexpr int BLK = CHE * 2 / NCW;  // elements per warp per super-chunk (2048: 8 tiles)
 constexpr int TPW = BLK / 256;      // 256-element tiles per warp per chunk
 constexpr int EPL = BLK / 32;       // elements per lane when the epilogue rescans a block
-constexpr int ST_CONT = 0, ST_DECIDED = 1, ST_EOS = 2;  // row status
+// row status; ST_ERR: the row is invalid (reading R0), its candidate holds the error bits.  An
+// error row decides like a rejection (Alg. 1 reads nothing above it) and is reported only if
+// it is the rollout's deciding row, i.e. only if Alg. 1 needs it (the oracle stops there).
+constexpr int ST_CONT = 0, ST_DECIDED = 1, ST_EOS = 2, ST_ERR = 3;
 constexpr bool c_claim_early = false;  // producer claims row r+1 under row r's pass 1
 
 // Optional per-stage cycle accounting (build with -DBS_PHASE_TIMING; read with
@@ -171,7 +174,8 @@ struct EpiBuf {
     RowDesc dsc;
     float m;
     int32_t ok;
-    int32_t pad[2];
+    uint32_t err;  // R0 error bits of the row (ok == 0)
+    int32_t pad[1];
     unsigned long long csum[MAXG][NCW];  // exact sums of the 1024-element blocks (greedy:
                                          // csum[0][w] = first argmax index of warp w)
 };
@@ -227,7 +231,8 @@ __device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane, const 
     if (lane < M) tl[lane] = nt;
     if (a.c_resp && lane < no && p + lane < a.c_resp_stride) a.c_resp[(int64_t)s * a.c_resp_stride + p + lane] = ot;
     const int32_t last = __shfl_sync(0xFFFFFFFFu, ot, (no - 1) & 31);
-    const int f = ((a.eos >= 0 && last == a.eos) || p + no >= L) ? 1 : 0;
+    // an empty block of a live rollout is an error stop (reading R0; as commit_kernel)
+    const int f = (no == 0 || (a.eos >= 0 && last == a.eos) || p + no >= L) ? 1 : 0;
     if (lane == 0) {
         a.c_ctx_len[s] = min(M, c.cl + no);
         a.c_pos[s] = p + no;
@@ -247,6 +252,14 @@ __device__ void finalize_rollout(const VerifyArgs& a, unsigned long long* s, int
     const int32_t* d = a.draft + (int64_t)b * a.k;
     const int64_t base = (int64_t)b * kp1;
     const int st = __ldcg(a.row_status + base + F);
+    if (st == ST_ERR) {  // a needed row is invalid (R0): the step emits nothing, the error is reported
+        atomicOr(a.dev_err, (uint32_t)__ldcg(a.row_cand + base + F));
+        for (int i = 0; i < kp1; ++i) out[i] = -1;
+        a.out_len[b] = 0;
+        a.out_acc[b] = 0;
+        if (a.sctl) atomicAdd(a.sctl + SC_DONE, 1u);
+        return;
+    }
     int n = 0;
     for (int i = 0; i < F; ++i) out[n++] = d[i];
     int acc = F;
@@ -362,6 +375,19 @@ __device__ bool complete_row_warp(const VerifyArgs& a, unsigned long long* stat,
         cF = __ldcg(a.row_cand + base + F);
     }
     stF = __shfl_sync(0xFFFFFFFFu, stF, F);
+    if (stF == ST_ERR) {  // a needed row is invalid (R0): the step emits nothing (the commit stops it)
+        cF = __shfl_sync(0xFFFFFFFFu, cF, F);
+        if (lane < kp1) a.out_tokens[base + lane] = -1;
+        tok = -1;
+        no = 0;
+        if (lane == 0) {
+            atomicOr(a.dev_err, (uint32_t)cF);
+            a.out_len[b] = 0;
+            a.out_acc[b] = 0;
+            if (a.sctl) atomicAdd(a.sctl + SC_DONE, 1u);
+        }
+        return true;
+    }
     // Alg. 1 lines 10-31: d_1..d_F accepted, then the sample of row F (or its accepted EOS)
     tok = (lane < F) ? dl : ((lane == F) ? (stF == ST_EOS ? dl : cF) : -1);
     no = F + 1;
@@ -523,7 +549,7 @@ __device__ void epilogue_row(const VerifyArgs& a, VShared& sh, const EpiBuf& E, 
     }
     if (lane == 0) {
         sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-        complete_row(a, sh.stat, b, j, q, ok ? status : ST_DECIDED, ok ? cand : -1, Zo, norm);
+        complete_row(a, sh.stat, b, j, q, ok ? status : ST_ERR, ok ? cand : (int)E.err, Zo, norm);
     }
     __syncwarp();
 }
@@ -707,11 +733,11 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
         else if (m == -INFINITY) { ok = false; err |= DEV_ALL_NEGINF; }
         else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) { ok = false; err |= DEV_RANGE; }
         if (tid == 0) {
-            if (err) atomicOr(a.dev_err, err);
-            mbar_arrive(&sh.rempty[f]);  // the descriptor slot is free (register copy kept)
+            mbar_arrive(&sh.rempty[f]);  // (error bits reported at finalize if the row is needed)  // the descriptor slot is free (register copy kept)
             E.dsc = dsc;
             E.m = m;
             E.ok = ok ? 1 : 0;
+            E.err = err;
         }
         mp.nmc = -__fmul_rn(m, a.c);
 
@@ -977,7 +1003,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
         a.next_row = ctx->vnext_row.p;
         a.rrec = ctx->vrrec.p;
         a.live = ctx->vlive.p;
-        a.eager_ok = getenv("BS_NO_EAGER") ? 0 : 1;
+        a.eager_ok = getenv("BS_NO_EAGER") ? 0 : (getenv("BS_FORCE_EAGER") ? 2 : 1);
         if (committed) {  // fused commit (bs_verify_commit)
             a.commit = 1;
             a.M = ctx->M;

@@ -146,8 +146,9 @@ __device__ bool ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
         if (q < 0) {  // finished / out of length / bad draft: no rows, nothing emitted
             a.out_len[b] = 0;
             a.out_acc[b] = 0;
-            if (a.commit) {  // fused commit of an empty step: only the length check
-                const int f = (a.finished[sl] || p >= L) ? 1 : 0;
+            if (a.commit) {  // fused commit of an empty step (as commit_kernel): finished,
+                // out of length, or a bad draft (an error stop of a live rollout)
+                const int f = 1;
                 if (f && !a.finished[sl]) a.c_finished[sl] = 1;
                 if (a.c_fin_out) a.c_fin_out[b] = f;
             }
@@ -402,7 +403,7 @@ __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch,
         cs.nlive = __shfl_sync(0xFFFFFFFFu, nl, 0);
         // eager when every live row fits in flight at once (two per cluster): the static
         // list then enumerates every row, j-major, and a cluster leaves once it is exhausted
-        cs.eager = a.eager_ok && (long long)cs.nlive * (a.k + 1) <= (long long)CK_NB * a.ncl;
+        cs.eager = a.eager_ok == 2 || (a.eager_ok && (long long)cs.nlive * (a.k + 1) <= (long long)CK_NB * a.ncl);
         cs.sidx = cid;
         cs.pre_idx = -1;
     }
@@ -747,9 +748,10 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             int c_status = ST_DECIDED, c_cand = -1;
             unsigned long long c_z = 0ull;
             float c_norm = 0.f;
-            if (err) {
+            if (err) {  // R0: reported at finalize only if Alg. 1 needs this row
                 rec = rank == 0;
-                if (rec && lane == 0) atomicOr(a.dev_err, err);
+                c_status = ST_ERR;
+                c_cand = (int)err;
             } else if (a.T == 0.f) {  // greedy (R1): lowest index attaining m
                 const int g = (int)er.z;
                 const bool acc = j < q && d == g;
@@ -1012,12 +1014,14 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                     wacc += ts;
 #endif
                 };
-                if (a.S <= 44) {  // FMA-pipe conversion for half the elements (mass16_mixed)
+                const uint32_t L02 = row_clamp_l0(mp.c, mp.nmc, a.S);
+                if (L02) {  // the fast mass loop (bf16 pre-clamp, ALU unpack, F2I conversion)
                     // lane l: elements 8l.. and 256+8l.. of tile t (conflict-free 16-byte loads;
                     // the tile sum does not depend on which lane holds which element)
                     for (int t = warp; t < nfull; t += CK_NMW) {
                         const int e0 = t * CK_TILE + lane * 8;
-                        tile_done(t, mass16_mixed(lds128(buf + e0), lds128(buf + e0 + CK_TILE / 2), mp));
+                        tile_done(t, mass16_fast(lds128(buf + e0), lds128(buf + e0 + CK_TILE / 2), mp.c, mp.nmc,
+                                                 mp.magic, L02));
                     }
                 } else {
                     for (int t = warp; t < nfull; t += CK_NMW) {

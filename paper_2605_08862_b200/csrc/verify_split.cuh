@@ -180,10 +180,9 @@ __global__ void __cluster_dims__(SP_CL, 1, 1) __launch_bounds__(SP_NT, 2)
         else if (m == -INFINITY) err |= DEV_ALL_NEGINF;
         else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) err |= DEV_RANGE;
         if (err) {
-            if (rank == 0 && tid == 0) {
-                atomicOr(a.dev_err, err);
+            if (rank == 0 && tid == 0) {  // reported at finalize only if Alg. 1 needs this row
                 sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                complete_row(a, sh.stat, dsc.b, j, q, ST_DECIDED, -1, 0ull, 0.f);
+                complete_row(a, sh.stat, dsc.b, j, q, ST_ERR, (int)err, 0ull, 0.f);
             }
             continue;
         }

@@ -109,10 +109,9 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
         else if (m == -INFINITY) err |= DEV_ALL_NEGINF;
         else if (!(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) err |= DEV_RANGE;
         if (err) {  // R0: the row is an error; the rollout stops (no token)
-            if (tid == 0) {
-                atomicOr(a.dev_err, err);
+            if (tid == 0) {  // reported at finalize only if Alg. 1 needs this row
                 sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                complete_row(a, sh.stat, dsc.b, j, q, ST_DECIDED, -1, 0ull, 0.f);
+                complete_row(a, sh.stat, dsc.b, j, q, ST_ERR, (int)err, 0ull, 0.f);
             }
             __syncthreads();
             continue;

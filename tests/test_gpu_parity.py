@@ -187,6 +187,63 @@ def test_verify_device_errors(bs, path):
     assert ctx.bs_sync_status() & 0x2
 
 
+def _error_rows(V, k, seed=5):
+    """Four rollouts (k = 2) around invalid rows (reading R0): 0 rejects d_1 for certain
+    (mass(d_1) = 0, R7) so its NaN row 1 is never needed; 1 has a NaN in row 0 (needed);
+    2 accepts d_1 for certain (p(d_1) = 1) and has a NaN in row 1 (needed); 3 is ordinary."""
+    n = 4
+    rows = bank_rows(seed, np.arange(n * (k + 1)), V, 6.0).reshape(n, k + 1, V).copy()
+    drafts = np.tile(np.arange(1, k + 1), (n, 1)).astype(np.int64)
+    rows[0, 0, drafts[0, 0]] = 0xFF80  # -inf: p(d_1) = 0
+    rows[0, 1, 7] = 0x7FC0             # NaN in a row Alg. 1 never reads
+    rows[1, 0, 9] = 0x7FC0             # NaN in row 0: needed
+    rows[2, 0, :] = 0xFF80
+    rows[2, 0, drafts[2, 0]] = 0x3F80  # only d_1 finite: p(d_1) = 1
+    rows[2, 1, 11] = 0x7F80            # +inf in row 1: needed
+    return rows, drafts, np.full(n, k)
+
+
+@pytest.mark.parametrize("path", KERNELS)
+@pytest.mark.parametrize("V", [64, 4099])
+def test_verify_error_only_if_needed(bs, orc, path, V):
+    """The error word reports an invalid row only if Alg. 1 reads it (the oracle stops there,
+    P:538-561 read in order); a rollout whose needed row is invalid emits nothing and the
+    commit stops it; the other rollouts match the oracle token for token."""
+    k, n, seed = 2, 4, 3
+    rows, drafts, dlen = _error_rows(V, k)
+    uids = np.arange(n, dtype=np.uint64) + np.uint64(5)
+    ml = np.full(n, 50)
+    for case in ("unneeded_only", "needed"):
+        r = rows.copy()
+        if case == "unneeded_only":  # rollouts 1 and 2 made valid again
+            r[1, 0, 9] = 0
+            r[2, 1, 11] = 0
+        ctx = bs.Context(vocab=V, k_max=k, match_max=8, max_rollouts=n, pool_capacity_tokens=16,
+                         pool_capacity_seqs=4, seed=seed)
+        ctx.bsx_set_verify_kernel(path)
+        _begin(bs, ctx, n, ml, uids, 8)
+        ot, ol, oa, _, _ = _verify_gpu(bs, ctx, r, drafts, dlen, k, 1.0, 1.0)
+        word = ctx.bs_sync_status()
+        bad = {1, 2} if case == "needed" else set()
+        assert (word & 0x1 != 0) == bool(bad), (case, word)
+        for b in range(n):
+            if b in bad:
+                with pytest.raises(orc.OracleError):
+                    orc.verify_one([r[b, j] for j in range(k + 1)], 1.0, 1.0, seed, int(uids[b]), 0,
+                                   int(ml[b]), -1, False, [int(x) for x in drafts[b]], k)
+                assert ol[b] == 0 and oa[b] == 0 and (ot[b] == -1).all()
+                continue
+            o = orc.verify_one([r[b, j] for j in range(k + 1)], 1.0, 1.0, seed, int(uids[b]), 0,
+                               int(ml[b]), -1, False, [int(x) for x in drafts[b]], k)
+            assert [int(x) for x in ot[b, : ol[b]]] == o.tokens, (case, b)
+        # the commit stops a rollout whose step emitted nothing (an error stop)
+        slots = to_dev(np.arange(n, dtype=np.int32))
+        fin = torch.zeros(n, dtype=torch.int32, device="cuda")
+        ctx.bs_commit(slots, to_dev(ot.astype(np.int32)), to_dev(ol.astype(np.int32)), k, fin)
+        torch.cuda.synchronize()
+        assert [int(x) for x in fin.cpu()] == [1 if b in bad else 0 for b in range(n)]
+
+
 # ------------------------------------------------------------------ lookup
 def _gpu_lookup(bs, ctx, seq_prompt, seq_off, tokens, ctxs, prompt_of, k, M, max_len=1 << 20,
                 rl_step=1):
