@@ -59,9 +59,12 @@ typedef enum {
 #define BS_DEV_RANGE       0x4u  /* |fl(m * log2e/T)| >= 2^24 (reading R0)              */
 #define BS_DEV_BAD_DRAFT   0x8u  /* draft token outside [0, V)                          */
 #define BS_DEV_INDEX_KEY   0x10u /* 64-bit key collision between two index windows      */
+#define BS_DEV_STALE       0x20u /* a lookup ran while the index was stale: pools were put  */
+                                 /* for a newer rl_step than the one sealed;  */
+                                 /* its drafts are empty; bs_sync_status -> BS_ERR_STALE   */
 
 typedef struct {
-    int32_t vocab;                /* V >= 1: logits row length                          */
+    int32_t vocab;                /* V in [1, 524288]: logits row length                */
     int32_t eos_id;               /* EOS token id, or -1 for none (Alg. 1) */
     int32_t k_max;                /* max draft block length K, 1..31 (P:299 uses 4)    */
     int32_t match_max;            /* M, max anchor length, 1..32 (reading L1)          */
@@ -249,6 +252,21 @@ bs_status bs_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t*
  * calls enqueued (or graphs captured) after it.  Errors: BS_ERR_INVALID on a NULL ctx or an
  * unknown kind. */
 bs_status bsx_set_verify_kernel(bs_ctx* ctx, int32_t kind);
+
+/* Programmatic dependent launch (PDL) contract of the verify launches.  With on = 1 the
+ * caller promises that the kernel enqueued immediately before a bs_verify_* call on its
+ * stream writes none of the verify's plan inputs (slots, draft_tokens, draft_len) nor any
+ * rollout state (it may write the logits and row_index: those are read only after the
+ * launch's griddepcontrol.wait); the launch then plans its rollouts before that wait,
+ * overlapping the preceding kernel (the model forward).  RolloutEngine's decode step (target
+ * rows -> verify) keeps that contract.  Default 0: every read follows the wait.  Errors:
+ * BS_ERR_INVALID on a NULL ctx or on not in {0, 1}. */
+bs_status bsx_set_early_plan(bs_ctx* ctx, int32_t on);
+
+/* Diagnostics (host memory out[n]): 0 resident clusters of the cluster verify kernel (0 until
+ * its first launch), 1 cooperative launch in use (-1 untested, 0 no, 1 yes), 2 SM count,
+ * 3 early plan.  Returns the number of values written. */
+int32_t bsx_launch_info(const bs_ctx* ctx, int64_t* out, int32_t n);
 
 /* ---------------------------------------------------------------- synthetic workload */
 /* Not part of the method: device twins of workloads/synth.py so a

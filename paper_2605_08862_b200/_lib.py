@@ -60,6 +60,8 @@ SIGNATURES = {
     "bs_stats_read": (C.c_int, [_V, _V, _I32, _I32, _V]),
     "bs_rollout_bind_output": (C.c_int, [_V, _V, _I64]),
     "bsx_set_verify_kernel": (C.c_int, [_V, _I32]),
+    "bsx_set_early_plan": (C.c_int, [_V, _I32]),
+    "bsx_launch_info": (C.c_int, [_V, C.POINTER(C.c_int64), _I32]),
     "bsx_synth_bank": (C.c_int, [_V, _I64, _I32, _U32, C.c_float, _V]),
     "bsx_target_rows": (C.c_int, [_V, _I32, _V, _V, _V, _I32, _U32, _I32, _I64, _V, _V]),
 }

@@ -72,7 +72,7 @@ class Context:
     def bs_sync_status(self, stream=None) -> int:
         w = C.c_uint32(0)
         st = load().bs_sync_status(self.handle, _stream(stream, self.device), C.byref(w))
-        if st not in (0, 7):
+        if st not in (0, 4, 7):  # OK, STALE (BS_DEV_STALE), DEVICE: the word says which
             _chk(self, st, "bs_sync_status")
         return int(w.value)
 
@@ -164,6 +164,15 @@ class Context:
     def bsx_set_verify_kernel(self, kind):
         kind = self.VERIFY_KERNELS[kind] if isinstance(kind, str) else int(kind)
         _chk(self, load().bsx_set_verify_kernel(self.handle, kind), "bsx_set_verify_kernel")
+
+    def bsx_launch_info(self) -> dict:
+        out = (C.c_int64 * 4)()
+        load().bsx_launch_info(self.handle, out, 4)
+        return {"clusters": int(out[0]), "cooperative": int(out[1]), "sms": int(out[2]),
+                "early_plan": int(out[3])}
+
+    def bsx_set_early_plan(self, on: bool):
+        _chk(self, load().bsx_set_early_plan(self.handle, int(bool(on))), "bsx_set_early_plan")
 
     def bsx_target_rows(self, slots, draft_tokens, draft_len, k, target_seed, mode, nbank,
                         row_index, stream=None):

@@ -45,6 +45,20 @@ bs_status bsx_set_verify_kernel(bs_ctx* c, int32_t kind) {
     return BS_OK;
 }
 
+bs_status bsx_set_early_plan(bs_ctx* c, int32_t on) {
+    if (!c || on < 0 || on > 1) return BS_ERR_INVALID;
+    c->early_plan = on;
+    return BS_OK;
+}
+
+int32_t bsx_launch_info(const bs_ctx* c, int64_t* out, int32_t n) {
+    if (!c || !out || n < 1) return 0;
+    const int64_t v[4] = {c->kcfg_clusters, c->kcfg_coop, c->num_sms, c->early_plan};
+    const int m = n < 4 ? n : 4;
+    for (int i = 0; i < m; ++i) out[i] = v[i];
+    return m;
+}
+
 const char* bs_version(void) { return "bubblespec-b200 0.1 (sm_100a)"; }
 
 const char* bs_last_error(const bs_ctx* ctx) {
@@ -63,8 +77,9 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     if (cfg->pool_capacity_tokens < 0 || cfg->pool_capacity_seqs < 0)
         return fail(nullptr, BS_ERR_INVALID, "negative pool capacity");
     if (cfg->eos_id >= cfg->vocab) return fail(nullptr, BS_ERR_INVALID, "eos_id >= vocab");
-    if ((int64_t)((cfg->vocab + 7) / 8) * 2 * 8 > (int64_t)8 * 76 * 1024 * 2)
-        return fail(nullptr, BS_ERR_INVALID, "vocab too large for an 8-CTA cluster row");
+    // the largest vocabulary every verify kernel supports: the rows kernel's 32 super-chunks
+    // of 16384 elements and the top-p kernel's 2048 coarse bins of 256 (V <= 524288)
+    if (cfg->vocab > 524288) return fail(nullptr, BS_ERR_INVALID, "vocab > 524288 is not supported");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0) {
@@ -79,6 +94,11 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     c->S = mass_shift(cfg->vocab);
     c->M = cfg->match_max;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    {  // tool / experiment overrides, read once per context (not per launch)
+        const char* s = getenv("BS_VERIFY_KERNEL");
+        c->env_kind = s ? atoi(s) : 0;
+        c->env_eager = getenv("BS_NO_EAGER") ? 0 : (getenv("BS_FORCE_EAGER") ? 2 : 1);
+    }
     {  // per-RL-step scratch is stream-ordered from the default pool: keep freed memory cached
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, cfg->device) == cudaSuccess) {
@@ -106,7 +126,7 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
                c->sealed.seq_off.ensure((size_t)cfg->pool_capacity_seqs + 1) == cudaSuccess &&
                c->sealed.seq_prompt.ensure((size_t)cfg->pool_capacity_seqs) == cudaSuccess &&
                c->table.ensure(2) == cudaSuccess && c->stats.ensure(STAT_COUNT) == cudaSuccess &&
-               c->idx_desc.ensure(1) == cudaSuccess;
+               c->idx_desc.ensure(1) == cudaSuccess && c->cur_step.ensure(1) == cudaSuccess;
     if (!okk) {
         bs_destroy(c);
         cudaGetLastError();
@@ -134,8 +154,10 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     cudaMemset(c->sealed.seq_off.p, 0, sizeof(int64_t));
     c->table_mask = 1;
     {
-        bs::IndexDesc d = {c->table.p, 1, c->sealed.tokens.p, c->seq_start_of.p};
+        bs::IndexDesc d = {c->table.p, 1, c->sealed.tokens.p, c->seq_start_of.p, ~0ull};
         cudaMemcpy(c->idx_desc.p, &d, sizeof d, cudaMemcpyHostToDevice);
+        const unsigned long long none = ~0ull;  // no pool put / sealed yet
+        cudaMemcpy(c->cur_step.p, &none, sizeof none, cudaMemcpyHostToDevice);
     }
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -154,7 +176,7 @@ void bs_destroy(bs_ctx* c) {
     c->staging.tokens.release(); c->staging.seq_off.release(); c->staging.seq_prompt.release();
     c->sealed.tokens.release(); c->sealed.seq_off.release(); c->sealed.seq_prompt.release();
     c->seq_start_of.release(); c->seq_end_of.release(); c->prompt_of.release();
-    c->table.release(); c->idx_desc.release(); c->rb_q.release(); c->vqueue.release(); c->vctl.release();
+    c->table.release(); c->idx_desc.release(); c->cur_step.release(); c->rb_q.release(); c->vqueue.release(); c->vctl.release();
     c->vrow_status.release(); c->vrow_cand.release(); c->vrow_z.release(); c->vrow_norm.release();
     c->vroll_first.release(); c->vroll_state.release();
     c->vnext_row.release(); c->vrrec.release(); c->vlive.release();
@@ -170,6 +192,7 @@ bs_status bs_sync_status(bs_ctx* c, void* stream, uint32_t* word) {
     CK(c, cudaMemsetAsync(c->dev_err.p, 0, sizeof(uint32_t), S(stream)), "clear error word");
     CK(c, cudaStreamSynchronize(S(stream)), "bs_sync_status");
     if (word) *word = w;
+    if (w & BS_DEV_STALE) return fail(c, BS_ERR_STALE, "device error word 0x%x: lookup against a stale index", w);
     if (w) return fail(c, BS_ERR_DEVICE, "device error word 0x%x", w);
     return BS_OK;
 }
@@ -210,6 +233,9 @@ bs_status bs_draft_pool_put(bs_ctx* c, uint64_t rl_step, int32_t n_seqs, const i
         P.step = rl_step;
         P.n_tokens = 0;
         P.n_seqs = 0;
+        CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+        // from here until the seal of rl_step, lookups of the older index are stale
+        CK(c, bs::set_cur_step(c, rl_step, S(stream)), "bs_draft_pool_put");
     }
     if (P.n_tokens + n_tokens > c->cfg.pool_capacity_tokens ||
         (int64_t)P.n_seqs + n_seqs > c->cfg.pool_capacity_seqs)
@@ -228,24 +254,34 @@ bs_status bs_draft_pool_seal(bs_ctx* c, uint64_t rl_step, void* stream) {
     if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
     CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
     Pool& P = c->staging;
-    if (!P.valid || P.step != rl_step) {  // nothing put for this step: an empty pool
+    if (!P.valid || P.step != rl_step) {
+        // a repeated seal of the step already sealed is a no-op (it must not seal an empty pool)
+        if (c->sealed.valid && c->sealed.step == rl_step) return BS_OK;
+        // nothing put for this step: an empty pool
         P.valid = true;
         P.step = rl_step;
         P.n_tokens = 0;
         P.n_seqs = 0;
         CK(c, cudaMemsetAsync(P.seq_off.p, 0, sizeof(int64_t), S(stream)), "seal");
     }
+    // the index is built from the assembled pool; on failure the pools are swapped back, so the
+    // assembled pool stays staged for a retry, and the index is published as invalid (its
+    // lookups are stale) instead of leaving a half-built table in use
     std::swap(c->staging, c->sealed);
-    c->staging.valid = false;
-    c->sealed.valid = false;
+    c->sealed.step = rl_step;
     std::string why;
     cudaError_t e = seal_index(c, S(stream), why);
+    if (e == cudaSuccess) e = bs::set_cur_step(c, rl_step, S(stream));
     if (e != cudaSuccess) {
+        std::swap(c->staging, c->sealed);
+        c->staging.valid = true;
+        c->sealed.valid = false;
+        bs::invalidate_index(c, S(stream));
         if (!why.empty()) return fail(c, BS_ERR_CAPACITY, "seal: %s", why.c_str());
         return cuda_fail(c, e, "bs_draft_pool_seal");
     }
     c->sealed.valid = true;
-    c->sealed.step = rl_step;
+    c->staging.valid = false;
     return BS_OK;
 }
 

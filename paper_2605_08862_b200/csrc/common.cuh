@@ -13,7 +13,8 @@ namespace bs {
 
 // ------------------------------------------------------------------ error word
 constexpr uint32_t DEV_BAD_LOGIT = 0x1u, DEV_ALL_NEGINF = 0x2u, DEV_RANGE = 0x4u,
-                   DEV_BAD_DRAFT = 0x8u, DEV_INDEX_KEY = 0x10u;
+                   DEV_BAD_DRAFT = 0x8u, DEV_INDEX_KEY = 0x10u,
+                   DEV_STALE = 0x20u;
 
 // ------------------------------------------------------------------ Philox4x32-10 (R6)
 struct U128 {
@@ -170,19 +171,29 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args&&... args) {
+cudaError_t launch_pdl_ex(bool cooperative, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t st, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    // cooperative: the launch fails instead of running when the grid cannot be co-resident
+    // (the persistent verify scheduler spins on work of CTAs that would otherwise never run)
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cooperative ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    return launch_pdl_ex(false, kernel, grid, block, smem, st, std::forward<Args>(args)...);
 }
 
 }  // namespace bs

@@ -94,6 +94,7 @@ struct IndexDesc {
     uint64_t mask;
     const int32_t* T;
     const int32_t* seq_start_of;
+    unsigned long long step;  // the rl_step this index was sealed for (~0: none / failed seal)
 };
 
 struct Pool {
@@ -115,6 +116,13 @@ struct bs_ctx {
     std::string err;
     int num_sms = 148;
     int verify_kind = 0;  // bsx_set_verify_kernel (0: auto)
+    int early_plan = 0;   // bsx_set_early_plan: the verify launch may plan before its PDL wait
+    // per-context (hence per-device) kernel launch setup, done once on this ctx's device:
+    // dynamic shared memory attributes set, and the cluster kernel's resident cluster count
+    size_t kcfg_cluster_smem = 0, kcfg_split_smem = 0;
+    int kcfg_clusters = 0, kcfg_topp = 0, kcfg_rows = 0;
+    int kcfg_coop = -1;  // cooperative cluster launches: -1 untested, 0 unsupported, 1 used
+    int env_kind = 0, env_eager = 1;  // BS_VERIFY_KERNEL / BS_NO_EAGER, BS_FORCE_EAGER (tools), read at create
     // rollout slots
     bs::DevBuf<int32_t> tail;  // [R, M] right-aligned context tail
     bs::DevBuf<int32_t> ctx_len, pos, max_len, prompt, finished;
@@ -126,6 +134,10 @@ struct bs_ctx {
     bs::DevBuf<bs::IndexEntry> table;
     uint64_t table_mask = 0;
     bs::DevBuf<bs::IndexDesc> idx_desc;
+    // the rl_step of the latest put / exchange / seal (device word): a lookup whose index was
+    // sealed for another step is stale, checked on the device so that replayed
+    // CUDA graphs are covered too
+    bs::DevBuf<unsigned long long> cur_step;
     // verify scratch: clamped q per rollout, the step's row table (RowDesc, 48 B per row)
     // and its control words
     bs::DevBuf<int32_t> rb_q, vqueue;
@@ -166,6 +178,10 @@ cudaError_t launch_lookup(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t 
                           int32_t* draft, int32_t* draft_len, int32_t* match_len,
                           cudaStream_t st);
 cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why);
+// device word cur_step <- step (the latest put / exchange / seal; staleness)
+cudaError_t set_cur_step(bs_ctx* ctx, uint64_t step, cudaStream_t st);
+// publish the index descriptor with no sealed step (every lookup is stale until a seal)
+void invalidate_index(bs_ctx* ctx, cudaStream_t st);
 cudaError_t launch_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* out_tokens,
                           const int32_t* out_len, int32_t k, int32_t* finished, cudaStream_t st);
 cudaError_t launch_begin(bs_ctx* ctx, int32_t n, const int32_t* slots,

@@ -150,6 +150,7 @@ bs_status bs_draft_exchange(bs_ctx* c, void* comm_v, int32_t rank, int32_t world
         P.step = rl_step;
         P.n_seqs = 0;
         P.n_tokens = 0;
+        if (bs::set_cur_step(c, rl_step, st) != cudaSuccess) return BS_ERR_CUDA;
     }
     // 1. counts
     AsyncBuf<int64_t> cnt;  // stream-ordered scratch (no synchronising cudaMalloc / cudaFree)

@@ -222,13 +222,24 @@ static int bits_for(uint64_t v) {
 
 // The lookup kernel reads the sealed index through a device-resident descriptor, so a
 // captured decode-step graph stays valid when a later seal reallocates the index.
-static cudaError_t publish_index(bs_ctx* ctx, cudaStream_t st) {
+static cudaError_t publish_index(bs_ctx* ctx, cudaStream_t st, unsigned long long step) {
     IndexDesc d;
+    d.step = step;
     d.table = ctx->table.p;
     d.mask = ctx->table_mask;
     d.T = ctx->sealed.tokens.p;
     d.seq_start_of = ctx->seq_start_of.p;
     return cudaMemcpyAsync(ctx->idx_desc.p, &d, sizeof d, cudaMemcpyHostToDevice, st);  // pageable: staged now
+}
+
+cudaError_t set_cur_step(bs_ctx* ctx, uint64_t step, cudaStream_t st) {
+    const unsigned long long v = step;
+    return cudaMemcpyAsync(ctx->cur_step.p, &v, sizeof v, cudaMemcpyHostToDevice, st);  // pageable: staged now
+}
+
+void invalidate_index(bs_ctx* ctx, cudaStream_t st) {
+    publish_index(ctx, st, ~0ull);
+    cudaStreamSynchronize(st);
 }
 
 cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
@@ -252,7 +263,7 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         BS_TRY(ctx->table.ensure(2));
         BS_TRY(cudaMemsetAsync(ctx->table.p, 0, 2 * sizeof(IndexEntry), st));
         ctx->table_mask = 1;
-        BS_TRY(publish_index(ctx, st));
+        BS_TRY(publish_index(ctx, st, ctx->sealed.step));
         return cudaStreamSynchronize(st);
     }
     const int* T = ctx->sealed.tokens.p;
@@ -372,7 +383,7 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         std::swap(pq, pq_child);
         std::swap(po, po_child);
     }
-    BS_TRY(publish_index(ctx, st));
+    BS_TRY(publish_index(ctx, st, ctx->sealed.step));
     return cudaStreamSynchronize(st);
 }
 
@@ -385,6 +396,7 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
     const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (b >= a.n) return;
     const IndexDesc x = *a.desc;
+    const unsigned long long cur = *a.cur_step;
     const int slot = a.slots[b];
     const int M = a.M;
     // the slot's state and its whole tail go out together (one round trip)
@@ -393,7 +405,7 @@ __global__ void __launch_bounds__(256) lookup_kernel(const LookupArgs a) {
     const int p = a.pos[slot], ml = a.max_len[slot];
     const int tok_raw = (lane < M) ? a.tail[(int64_t)slot * M + (M - 1 - lane)] : -1;  // y[-1-lane]
     const bool fin = a.finished[slot] != 0;
-    lookup_rollout(a, x, b, L, P, p, ml, fin, tok_raw, lane);
+    lookup_rollout(a, x, b, L, P, p, ml, fin, tok_raw, lane, x.step != cur);
     __threadfence();
     pdl_trigger();
 }
@@ -413,6 +425,8 @@ LookupArgs lookup_args(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k, 
     a.max_len = ctx->max_len.p;
     a.finished = ctx->finished.p;
     a.desc = ctx->idx_desc.p;
+    a.cur_step = ctx->cur_step.p;
+    a.dev_err = ctx->dev_err.p;
     a.draft = draft;
     a.draft_len = draft_len;
     a.match_len = match_len;

@@ -18,6 +18,8 @@ struct LookupArgs {
     const int32_t* max_len;
     const int32_t* finished;
     const IndexDesc* desc;  // the sealed index (device-resident: stable across RL steps)
+    const unsigned long long* cur_step;  // rl_step of the latest put / seal (staleness)
+    uint32_t* dev_err;
     int32_t* draft;
     int32_t* draft_len;
     int32_t* match_len;
@@ -57,10 +59,13 @@ __constant__ HashPow c_hash_pow = make_hash_pow();
 // Rollout b's draft for its next step from its state: context length L, prompt P, position p,
 // max length ml, finished flag fin, and lane i's context token y[-1-i] (tok_raw, lane < M).
 // Writes draft[b, 0..k), draft_len[b], match_len[b].  Whole warp.
+// stale: the index was sealed for another rl_step than the latest put (a hard
+// error): the draft is empty and the error word says so.
 __device__ __forceinline__ void lookup_rollout(const LookupArgs& a, const IndexDesc& x, int b, int L, int P, int p,
-                                               int ml, bool fin, int tok_raw, int lane) {
+                                               int ml, bool fin, int tok_raw, int lane, bool stale) {
     const int M = a.M;
-    fin = fin || p >= ml;
+    if (stale && lane == 0) atomicOr(a.dev_err, DEV_STALE);
+    fin = fin || p >= ml || stale;
     const int mmax = min(M, L);
     const int tok = (lane < mmax) ? tok_raw : -1;
     uint64_t H = (lane < mmax) ? (uint64_t)(uint32_t)(tok + 1) * c_hash_pow.v[lane] : 0ull;

@@ -24,6 +24,7 @@ __global__ void begin_kernel(int n, int M, const int32_t* slots, const unsigned 
     prompt[s] = prompt_ids[b];
     finished[s] = 0;
     uid[s] = uids[b];
+    __threadfence();  // visible before a later launch's early plan reads it
 }
 
 // One warp per rollout (Alg. 1 lines 15/22): lane i owns tail slot i (M <= 32) and emitted
@@ -66,6 +67,7 @@ __global__ void commit_kernel(int n, int M, int k, int eos, const int32_t* slots
         if (lane == 0) finished[s] = 1;
     }
     if (fin_out && lane == 0) fin_out[b] = f;
+    __threadfence();  // visible before a later launch's early plan reads it
 }
 
 __global__ void state_kernel(int n, const int32_t* slots, const int32_t* pos,

@@ -148,6 +148,7 @@ struct VerifyArgs {
     int64_t c_resp_stride;
     int ncl;                      // clusters in the grid
     int eager_ok;                 // small live batches claim every row at once
+    int early_plan;               // plan before griddepcontrol.wait (bsx_set_early_plan)
     // fused lookup (bs_verify_commit_lookup): after its commit, the finalizing warp looks up
     // the rollout's next draft from the committed state (lk.draft / draft_len: the next step's)
     int lookup;
@@ -201,6 +202,7 @@ struct CommitPre {
     int s, p, L, cl, old;  // slot, pos, max_len, ctx_len; lane i: tail slot i
     int P;                 // prompt (fused lookup)
     IndexDesc x;           // the sealed index (fused lookup)
+    unsigned long long cur;  // rl_step of the latest put / seal (staleness)
 };
 __device__ __forceinline__ CommitPre commit_prefetch(const VerifyArgs& a, int slot, int lane) {
     CommitPre c;
@@ -212,6 +214,7 @@ __device__ __forceinline__ CommitPre commit_prefetch(const VerifyArgs& a, int sl
     if (a.lookup) {
         c.P = a.lk.prompt[slot];
         c.x = *a.lk.desc;
+        c.cur = *a.lk.cur_step;
     }
     return c;
 }
@@ -241,7 +244,8 @@ __device__ void commit_rollout_warp(const VerifyArgs& a, int b, int lane, const 
     }
     if (a.lookup) {  // the next step's draft from the committed state: y[-1-lane] = tail[M-1-lane]
         const int32_t y = __shfl_sync(0xFFFFFFFFu, nt, (M - 1 - lane) & 31);
-        lookup_rollout(a.lk, c.x, b, min(M, c.cl + no), c.P, p + no, L, f != 0, lane < M ? y : -1, lane);
+        lookup_rollout(a.lk, c.x, b, min(M, c.cl + no), c.P, p + no, L, f != 0, lane < M ? y : -1, lane,
+                       c.x.step != c.cur);
     }
 }
 
@@ -916,14 +920,7 @@ static int split_slice(int V) { return ((V + SP_CL - 1) / SP_CL + 255) / 256 * 2
 enum { VK_AUTO = 0, VK_ROWS = 1, VK_SPLIT = 2, VK_CLUSTER = 3 };
 static int verify_kind(const bs_ctx* ctx, int V) {
     int k = ctx->verify_kind;
-    if (k == VK_AUTO) {
-        static int env = -1;
-        if (env < 0) {
-            const char* s = getenv("BS_VERIFY_KERNEL");
-            env = s ? atoi(s) : 0;
-        }
-        k = env;
-    }
+    if (k == VK_AUTO) k = ctx->env_kind;
     if (k == VK_AUTO) k = VK_CLUSTER;
     if (k == VK_CLUSTER && (V + CK_CL - 1) / CK_CL > CK_MAXSL) k = VK_ROWS;
     return k;
@@ -1003,7 +1000,8 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
         a.next_row = ctx->vnext_row.p;
         a.rrec = ctx->vrrec.p;
         a.live = ctx->vlive.p;
-        a.eager_ok = getenv("BS_NO_EAGER") ? 0 : (getenv("BS_FORCE_EAGER") ? 2 : 1);
+        a.eager_ok = ctx->env_eager;
+        a.early_plan = ctx->early_plan;
         if (committed) {  // fused commit (bs_verify_commit)
             a.commit = 1;
             a.M = ctx->M;
@@ -1025,12 +1023,11 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     if (topp) {  // R5: top-p filtered rows (verify_topp.cuh)
         if (ntile_ok(V) == 0) return cudaErrorInvalidValue;
         const size_t tsm = sizeof(TopPShared);
-        static int tp_configured = 0;
-        if (!tp_configured) {
+        if (!ctx->kcfg_topp) {
             e = cudaFuncSetAttribute(verify_topp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)tsm);
             if (e != cudaSuccess) return e;
-            tp_configured = 1;
+            ctx->kcfg_topp = 1;
         }
         const int tgrid = std::max(1, std::min(ctx->num_sms * 2, n * (k + 1)));
         return launch_pdl(verify_topp_kernel, dim3(tgrid), dim3(TP_NT), tsm, st, a, top_p);
@@ -1038,9 +1035,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     if (kind == VK_CLUSTER) {
         const int SL = cluster_slice(V);
         const size_t csm = ck_smem_bytes(SL);
-        static size_t ck_configured = 0;
-        static int ck_clusters = 0;
-        if (ck_configured != csm) {
+        if (ctx->kcfg_cluster_smem != csm) {
             e = cudaFuncSetAttribute(verify_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)csm);
             if (e != cudaSuccess) return e;
@@ -1055,32 +1050,44 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             int ncl = 0;
             e = cudaOccupancyMaxActiveClusters(&ncl, verify_cluster_kernel, &cfg);
             if (e != cudaSuccess) return e;
-            ck_clusters = std::max(1, ncl);
-            ck_configured = csm;
+            ctx->kcfg_clusters = std::max(1, ncl);
+            ctx->kcfg_cluster_smem = csm;
         }
-        a.ncl = ck_clusters;
-        return launch_pdl(verify_cluster_kernel, dim3(ck_clusters * CK_CL), dim3(CK_NT), csm, st, a, SL);
+        a.ncl = ctx->kcfg_clusters;
+        const dim3 grid(ctx->kcfg_clusters * CK_CL);
+        if (ctx->kcfg_coop < 0) {  // probe once, outside stream capture (a failed launch would end it)
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(st, &cs);
+            if (cs == cudaStreamCaptureStatusNone) {
+                e = launch_pdl_ex(true, verify_cluster_kernel, grid, dim3(CK_NT), csm, st, a, SL);
+                if (e == cudaSuccess) {
+                    ctx->kcfg_coop = 1;
+                    return e;
+                }
+                cudaGetLastError();
+                ctx->kcfg_coop = 0;
+            }
+        }
+        return launch_pdl_ex(ctx->kcfg_coop == 1, verify_cluster_kernel, grid, dim3(CK_NT), csm, st, a, SL);
     }
     if (kind == VK_SPLIT) {
         const int SL = split_slice(V);
         const size_t ssm = ((sizeof(SplitShared) + 127) & ~size_t(127)) + (size_t)SL * 2;
-        static size_t sp_configured = 0;
-        if (sp_configured < ssm) {
+        if (ctx->kcfg_split_smem < ssm) {
             e = cudaFuncSetAttribute(verify_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)ssm);
             if (e != cudaSuccess) return e;
-            sp_configured = ssm;
+            ctx->kcfg_split_smem = ssm;
         }
         const int nclus = std::max(1, (ctx->num_sms * 2) / SP_CL);
         return launch_pdl(verify_split_kernel, dim3(nclus * SP_CL), dim3(SP_NT), ssm, st, a, SL);
     }
     const size_t smem = (size_t)NSTAGE * CHE * 2 + sizeof(VShared);
-    static int configured = 0;
-    if (!configured) {
+    if (!ctx->kcfg_rows) {
         e = cudaFuncSetAttribute(verify_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
         if (e != cudaSuccess) return e;
-        configured = 1;
+        ctx->kcfg_rows = 1;
     }
     const int grid = std::max(1, std::min(ctx->num_sms * CTAS_PER_SM, n * (k + 1)));
     return launch_pdl(verify_rows_kernel, dim3(grid), dim3(NTHR), smem, st, a);

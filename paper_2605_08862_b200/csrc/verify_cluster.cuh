@@ -565,7 +565,10 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
     }
 #endif
     cluster.sync();  // every CTA's barriers exist before any remote operation
-    // The plan runs before griddepcontrol.wait, overlapping the kernel launched just before
+    // Without the caller's early-plan promise (bsx_set_early_plan) everything waits for the
+    // previous kernel first: only griddepcontrol.wait makes its writes visible.
+    if (!a.early_plan) pdl_wait();
+    // With it, the plan runs before griddepcontrol.wait, overlapping the kernel launched just before
     // this one (the model forward / target rows): its inputs (slots, drafts, positions,
     // lengths, uids) come from launches at least two back (the lookup triggers its dependents
     // only after its stores), and it reads no logits and no row_index.  The previous verify
@@ -619,8 +622,9 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 const int sl = a.slots[b];
                 const int M = lk.M;
                 const int tr = (lane < M) ? lk.tail[(int64_t)sl * M + (M - 1 - lane)] : -1;
-                lookup_rollout(lk, *lk.desc, b, lk.ctx_len[sl], lk.prompt[sl], lk.pos[sl], lk.max_len[sl],
-                               lk.finished[sl] != 0, tr, lane);
+                const IndexDesc x = *lk.desc;
+                lookup_rollout(lk, x, b, lk.ctx_len[sl], lk.prompt[sl], lk.pos[sl], lk.max_len[sl],
+                               lk.finished[sl] != 0, tr, lane, x.step != *lk.cur_step);
             }
         }
     }

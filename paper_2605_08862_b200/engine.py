@@ -40,6 +40,9 @@ class RolloutEngine:
         self.fuse_lookup = fused and fuse_lookup
         self.launches_per_step = 2 if self.fuse_lookup else 3
         self.T, self.top_p, self.target = temperature, top_p, target
+        # the kernel right before each verify launch is bsx_target_rows (the synthetic model),
+        # which writes only row_index: the verify may plan before its PDL wait
+        ctx.bsx_set_early_plan(True)
         dev = torch.device("cuda", ctx.device)
         # a dedicated stream: CUDA graphs cannot be captured on the legacy default stream
         self.stream = stream or torch.cuda.Stream(dev)

@@ -183,3 +183,42 @@ def test_fused_lookup_matches_separate_lookup_q7(bs):
     drop = lambda d: {x: v for x, v in d.items() if x != "rows_verified"}  # noqa: E731 (speculation)
     assert drop(a["st"]) == drop(b["st"])
     assert a["st"]["accepted"] > 0 and (a["mlen"] > 0).any()
+
+
+@pytest.mark.parametrize("fused", ["lookup", "none"])
+def test_graph_replay_staleness_on_device(bs, fused):
+    """SPEC S:340 (a lookup against a pool sealed for another RL step is a hard error) under
+    CUDA-graph replay, where the host-side rl_step check cannot run: a put for a new step
+    without its seal makes every replayed lookup stale on the device (empty drafts,
+    BS_DEV_STALE -> BS_ERR_STALE); after the seal the same graph replays cleanly; a repeated
+    seal of the sealed step is a no-op."""
+    spec = TargetSpec(V=1024, nbank=64, mode="mixed", beta=6.0)
+    M, k, L = 16, 4, 4000
+    prompts, tails, pid, tail_rows, uids, ml = setup_rollouts(spec, 2, 4, M, L)
+    pools_np = pools_for(spec, prompts, tails, 4, np.full(8, 300), 0.9, prefix=M)
+    n = len(pid)
+    ctx, eng = _engine(bs, spec, n, k, M, 1.0, 1.0, 7, -1, 2 * len(pools_np[2]), 2 * len(pools_np[0]),
+                       fused=fused)
+    put = lambda s: eng.put_pools(s, to_dev(pools_np[0]), to_dev(pools_np[1]), to_dev(pools_np[2]))  # noqa: E731
+    put(1)
+    eng.seal(1)
+    eng.begin(to_dev(uids.view(np.int64)), to_dev(pid), to_dev(tail_rows), to_dev(ml))
+    eng.capture(4)
+    eng.run_graph()
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() == 0
+    assert eng.stats(reset=True)["proposed"] > 0  # the sealed index serves drafts
+    put(2)  # a new RL step's pools: the step-1 index is stale until the step-2 seal
+    eng.run_graph()
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() & 0x20  # BS_DEV_STALE
+    st = eng.stats(reset=True)
+    # empty drafts: plain decoding only (fused lookup: the replay's first step still uses the
+    # drafts looked up before the put)
+    assert st["proposed"] <= (n * k if fused == "lookup" else 0) and st["tokens"] > 0
+    eng.seal(2)
+    eng.seal(2)  # repeated seal of the sealed step: a no-op, the index keeps its pools
+    eng.run_graph()
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() == 0
+    assert eng.stats(reset=True)["proposed"] > 0
