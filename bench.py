@@ -2,17 +2,22 @@
 verified tokens/s/GPU at V=151936, k=8; mean accepted length; HBM GB/s).
 
 One bench STEP = one RL step of the whole hot path on one synthetic
-batch: pool put (a8) -> cross-rank exchange (a9, N > 1) -> index build (a8) -> rollout begin
--> first lookup (a1) -> decoding until every rollout finished (EOS / max_len), each decoding
-step being synthetic target rows -> one bs_verify_commit_lookup launch: verify (a2-a6),
-commit (a7) and the next step's lookup (a1).  Inputs (pools, prompt
-tails, lengths, the 2.5 GB logit bank) are resident in HBM before the timed region.
+batch: pool put (a8) -> cross-rank exchange over NCCL (a9; a 1-rank communicator at N = 1,
+so its cost is timed at every N) -> index build (a8) -> rollout begin -> first lookup (a1)
+-> decoding until every rollout finished (EOS / max_len), each decoding step being the
+synthetic target's rows (the model-forward stand-in) -> one bs_verify_commit_lookup launch:
+verify (a2-a6), commit (a7) and the next step's lookup (a1).  Inputs (pools, prompt tails,
+lengths, the 2.5 GB logit bank) are resident in HBM before the timed region; every rollout
+reads its own logits rows (target mode "sample"), so rows are not shared through L2.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config q7]
 
 Under torchrun (N > 1) every rank runs its own prompt shard (weak scaling), pools produced
 on rank r are for rank (r+1)'s prompts and reach their owner through bs_draft_exchange
 (NCCL over NVLink); timing is CUDA events, max over ranks.  Rank 0 prints one JSON line.
+The default q7 run also measures the TINY and LC configurations (BASELINE.json configs[0],
+configs[2]) and reports them under "other_configs"; warm-up RL step 0's emitted tokens are
+compared with the oracle's on the CPU-baseline sample ("parity").
 """
 from __future__ import annotations
 
@@ -33,17 +38,17 @@ CONFIGS = {
     # BASELINE.json configs[1]: "Qwen2.5-7B-shaped: V=151936, 256 rollouts, k=8, 4k-token
     # lognormal lengths, T=1.0, 1 GPU"
     "q7": dict(V=151936, prompts=16, G=16, k=8, M=32, T=1.0, top_p=1.0, mean_len=4096,
-               sigma=0.6, cap=32768, nbank=8192, beta=15.75, match_rate=0.8, noise=0.02,
+               sigma=0.6, cap=32768, nbank=131072, beta=15.75, match_rate=0.8, noise=0.02,
                G_pre=16, pool_frac=2.0 / 3.0),
     # configs[2]: "long-context: V=151936, 64 rollouts, 32k-token responses, k=16, draft pool
     # 8 drafts/prompt, top-p 0.95"
     "lc": dict(V=151936, prompts=8, G=8, k=16, M=32, T=1.0, top_p=0.95, mean_len=8192,
-               sigma=0.6, cap=32768, nbank=8192, beta=15.75, match_rate=0.8, noise=0.02,
+               sigma=0.6, cap=32768, nbank=131072, beta=15.75, match_rate=0.8, noise=0.02,
                G_pre=8, pool_frac=2.0 / 3.0),
     # configs[0]: the small case the oracle finishes in seconds
     "tiny": dict(V=1024, prompts=1, G=4, k=4, M=16, T=1.0, top_p=1.0, mean_len=64, sigma=0.0,
                  cap=64, nbank=256, beta=6.0, match_rate=0.9, noise=0.02, G_pre=4,
-                 pool_frac=1.0),
+                 pool_frac=1.0, mode="position"),
 }
 
 
@@ -57,7 +62,7 @@ def make_step_inputs(cfg, step: int, rank: int, world: int):
     from workloads import TargetSpec, lognormal_lengths, make_pools, prompt_tails
 
     P, G, M = cfg["prompts"], cfg["G"], cfg["M"]
-    spec = TargetSpec(V=cfg["V"], nbank=cfg["nbank"], mode="position", beta=cfg["beta"])
+    spec = TargetSpec(V=cfg["V"], nbank=cfg["nbank"], mode=cfg.get("mode", "sample"), beta=cfg["beta"])
     base = step * 1_000_000
     # prompts owned by `rank` (prompt % world == rank): the rollouts of this rank
     own = np.array([base + i * world + rank for i in range(P)], dtype=np.int64)
@@ -149,18 +154,31 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------------------- our arm
-def run_ours(args, cfg, rank, world, dist):
+
+
+def nccl_comm(bs, dist, rank, world):
+    """An NCCL communicator for bs_draft_exchange: the torch process group's ranks (N > 1),
+    or a 1-rank communicator (N = 1) so the exchange runs, and is timed, at every N."""
+    if world > 1:
+        obj = [bs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return bs.nccl_comm_init(obj[0], world, rank)
+    return bs.nccl_comm_init(bs.nccl_unique_id(), 1, 0)
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=True):
     import torch
 
     import paper_2605_08862_b200 as bs
-    from paper_2605_08862_b200.engine import RolloutEngine, Target
+    from paper_2605_08862_b200.engine import TARGET_MODES, RolloutEngine, Target
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(dev)
     V, k = cfg["V"], cfg["k"]
     n = cfg["prompts"] * cfg["G"]
-    total_steps = args.warmup + args.steps
+    total_steps = warmup + steps
     t0 = time.time()
     host = [make_step_inputs(cfg, s, rank, world) for s in range(total_steps)]
     log(f"[rank {rank}] inputs generated in {time.time() - t0:.1f}s")
@@ -173,176 +191,133 @@ def run_ours(args, cfg, rank, world, dist):
     bank = torch.empty((cfg["nbank"], V), dtype=torch.int16, device=dev)
     bs.bsx_synth_bank(bank, cfg["nbank"], V, spec.bank_seed, spec.beta, stream=stream)
     eng = RolloutEngine(ctx, n, k, cfg["T"], cfg["top_p"],
-                        Target(bank, cfg["nbank"], spec.target_seed, 0), stream=stream)
-    comm = None
-    if world > 1:
-        uid = bs.nccl_unique_id() if rank == 0 else None
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        comm = bs.nccl_comm_init(obj[0], world, rank)
+                        Target(bank, cfg["nbank"], spec.target_seed, TARGET_MODES[spec.mode]), stream=stream)
+    comm = nccl_comm(bs, dist, rank, world)
 
-    def dev_t(a, dtype=None):
-        t = torch.from_numpy(np.ascontiguousarray(a))
-        return t.to(dev, non_blocking=False) if dtype is None else t.to(dtype).to(dev)
+    def dev_t(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
     dins = [dict(sp=dev_t(h["seq_prompt"]), off=dev_t(h["seq_off"]), tok=dev_t(h["tokens"]),
                  ntok=int(len(h["tokens"])), pid=dev_t(h["pid"]), tails=dev_t(h["tails"]),
                  uids=dev_t(h["uids"].view(np.int64)), ml=dev_t(h["max_len"])) for h in host]
     torch.cuda.synchronize(dev)
     chunk = args.chunk
-    # verify-op timing events captured inside the graph (external event-record nodes)
-    ev_s = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(chunk)]
-    ev_e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(chunk)]
+    graph = []
 
-    graphs = {}
+    def capture():
+        """The decode graph: `chunk` steps of target rows -> bs_verify_commit_lookup, captured
+        once (the lookup reads the sealed index through a device-resident descriptor, so the
+        graph stays valid across RL steps; staleness is checked on the device)."""
+        if not graph:
+            graph.append(eng.capture(chunk))  # (runs one real, eager decoding step first)
+        return graph[0]
 
-    def capture(instrument=False):
-        """The decode graph (captured once: the library reads the sealed index through a
-        device-resident descriptor, so the graph stays valid across RL steps)."""
-        if instrument not in graphs:
-            graphs[instrument] = capture_new(instrument)
-        return graphs[instrument]
-
-    def capture_new(instrument=False):
-        """One graph of `chunk` decode iterations.  Event-record nodes cost several us each
-        inside a graph, so the timed graph has none; the instrumented twin (events around
-        every bs_verify_step) is replayed separately on the same deterministic work."""
-        with torch.cuda.stream(stream):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for i in range(chunk):
-                    c, t = ctx, eng.target
-                    # the drafts of this step: from the previous verify launch (fused lookup;
-                    # the first step's from eng.begin)
-                    c.bsx_target_rows(eng.slots, eng.draft, eng.draft_len, k, t.target_seed,
-                                      t.mode, t.nbank, eng.row_index, stream=stream)
-                    if instrument:
-                        ev_s[i].record(stream)
-                    c.bs_verify_commit_lookup(eng.rl_step, eng.slots, t.bank, eng.row_index, V, eng.draft,
-                                              eng.draft_len, k, eng.T, eng.top_p, eng.out_tokens,
-                                              eng.out_len, eng.out_acc, eng.finished, eng.match_len,
-                                              stream=stream)
-                    if instrument:
-                        ev_e[i].record(stream)
-        return g
-
-    phases = os.environ.get("BS_BENCH_PHASES")  # diagnostics: host wall per RL-step phase
     flags = [torch.zeros(1, dtype=torch.bool).pin_memory() for _ in range(2)]
     flag_ev = [torch.cuda.Event() for _ in range(2)]
 
-    def replay_until_done(g):
+    def replay_until_done(g, first=None):
         """Replay the decode graph until every rollout finished.  The all-finished flag of
         chunk c is copied to pinned memory and checked while chunk c+1 already runs, so the
-        GPU does not idle on the host round trip (one extra, all-finished chunk at the end)."""
-        steps = 0
+        GPU does not idle on the host round trip (one extra, all-finished chunk at the end).
+        first: an event pair around the first chunk (recorded outside the graph)."""
+        steps_ = 0
         with torch.cuda.stream(stream):
+            if first:
+                first[0].record(stream)
             g.replay()
-            steps += chunk
+            if first:
+                first[1].record(stream)
+            steps_ += chunk
             c = 0
             while True:
                 flags[c % 2].copy_(eng.finished.all().view(1), non_blocking=True)
                 flag_ev[c % 2].record(stream)
                 g.replay()
-                steps += chunk
+                steps_ += chunk
                 flag_ev[c % 2].synchronize()
                 if bool(flags[c % 2][0]):
                     break
                 c += 1
-        return steps
+        return steps_
 
-    def rl_step(s, rec, instrument=False):
-        d = dins[s]
-        tp = [time.perf_counter()]
-
-        def mark():
-            if phases:
-                stream.synchronize()
-                tp.append(time.perf_counter())
+    def setup_step(s, d):
         with torch.cuda.stream(stream):
-            ctx.bs_draft_pool_put(s + 1, d["sp"], d["off"], d["tok"], d["ntok"], stream=stream)
-            mark()
-            if comm is not None:
-                ctx.bs_draft_exchange(comm, rank, world, s + 1, stream=stream)
-            eng.seal(s + 1)  # synchronises the stream (index build is per RL step)
-            mark()
+            ctx.bs_draft_pool_put(s, d["sp"], d["off"], d["tok"], d["ntok"], stream=stream)
+            ctx.bs_draft_exchange(comm, rank, world, s, stream=stream)
+            eng.seal(s)  # synchronises the stream (index build is per RL step)
             eng.begin(d["uids"], d["pid"], d["tails"], d["ml"])
-            mark()
-        g = capture(instrument)
-        mark()
-        rec["launches"] += 2 + int(eng.fuse_lookup) + rec["seal_launches"]  # put, begin, first lookup
-        steps, chunks = 0, 0
-        if instrument:  # events are re-recorded by every replay: one chunk at a time
-            while True:
-                with torch.cuda.stream(stream):
-                    g.replay()
-                    done = bool(eng.finished.all().item())  # one host sync per chunk
-                steps += chunk
-                vt = sum(ev_s[i].elapsed_time(ev_e[i]) for i in range(chunk))
-                rec["verify_ms"] += vt
-                if chunks == 0:
-                    rec["verify_ms_steady"] += vt
-                    rec["steady_steps"] += chunk
-                chunks += 1
-                if done:
-                    break
-        else:  # the finished check of chunk c overlaps the replay of chunk c+1
-            steps += replay_until_done(g)
-        mark()
-        rec["decode_steps"] += steps
-        rec["launches"] += steps * eng.launches_per_step
-        if phases:
-            dt = [1e3 * (b - a) for a, b in zip(tp, tp[1:])]
-            log("[phases ms] put %.1f seal %.1f begin %.1f capture %.1f decode %.1f" % tuple(dt[:5]))
-        return steps
 
-    # seal launch count: our own kernels + CUB device calls per level (DESIGN.md §6)
+    # per RL step, outside the graph: put, the exchange's three NCCL launches and its gather,
+    # the seal's own kernels and CUB calls, begin, the first lookup
     D = cfg["M"] + k
-    rec0 = dict(launches=0, verify_ms=0.0, verify_ms_steady=0.0, steady_steps=0, decode_steps=0,
-                seal_launches=4 + 9 * D)
+    launches_rl = 1 + 4 + (4 + 9 * D) + 2
+
+    def rl_step(s, rec, evs=None):
+        setup_step(s + 1, dins[s])
+        g = capture()
+        if evs:
+            evs[0].record(stream)
+        steps_ = replay_until_done(g, evs[2:] if evs else None)
+        if evs:
+            evs[1].record(stream)
+        rec["launches"] += launches_rl
+        rec["decode_steps"] += steps_
+        rec["launches"] += steps_ * eng.launches_per_step
+        return steps_
+
+    rec0 = dict(launches=0, decode_steps=0)
     # nvidia-smi is started before the warm-up (its start-up stays outside the timed region);
     # only its samples inside the timed window are kept
     clocks = ClockSampler(dev.index)
     clocks.start()
-    # ---- warmup
-    for s in range(args.warmup):
-        rl_step(s, dict(rec0))
-    ctx.bs_stats_read(reset=True, stream=stream)
-    # steady-state row counters need the first chunk separately: read stats after chunk 0
+    # ---- warm-up (RL step 0's responses are kept for the oracle comparison)
+    resp0 = None
+    for s in range(warmup):
+        if s == 0 and bind_step0:
+            Lmax = int(host[0]["max_len"].max())
+            resp = torch.full((n, Lmax), -1, dtype=torch.int32, device=dev)
+            ctx.bs_rollout_bind_output(resp, Lmax)
+            rl_step(s, dict(rec0))
+            torch.cuda.synchronize(dev)
+            ctx.bs_rollout_bind_output(None)
+            resp0 = resp.cpu().numpy()
+            del resp
+        else:
+            rl_step(s, dict(rec0))
     torch.cuda.synchronize(dev)
+    if ctx.bs_sync_status():
+        raise SystemExit("device error word set during warm-up")
+    # ---- steady state (untimed): the first chunk of a fresh RL step, full live batch; the
+    # chunk replay is bracketed by two events outside the graph
+    ctx.bs_stats_read(reset=True, stream=stream)
+    setup_step(10_000, dins[total_steps - 1])
+    e_s0, e_s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e_s0.record(stream)
+        capture().replay()
+        e_s1.record(stream)
+    torch.cuda.synchronize(dev)
+    steady_ms = e_s0.elapsed_time(e_s1)
+    sst = eng.stats(reset=True)
+    with torch.cuda.stream(stream):
+        while not eng.all_finished():  # finish that RL step (untimed)
+            capture().replay()
+    torch.cuda.synchronize(dev)
+    ctx.bs_stats_read(reset=True, stream=stream)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    # ---- (untimed, before the timed region: it also settles the device) the verify op's
-    # device time on the same work: instrumented replay of the RL steps that are timed next
-    # (deterministic: same pools, uids and Philox stream -> identical rows)
-    reci = dict(rec0)
-    for s in range(args.warmup, total_steps):
-        rl_step(s, reci, instrument=True)
-    torch.cuda.synchronize(dev)
-    sti = eng.stats(reset=True)
-    # ---- steady-state kernel phase: full live batch, first chunk of a fresh RL step
-    s_last = total_steps - 1
-    d = dins[s_last]
-    with torch.cuda.stream(stream):
-        ctx.bs_draft_pool_put(10_000, d["sp"], d["off"], d["tok"], d["ntok"], stream=stream)
-        if comm is not None:
-            ctx.bs_draft_exchange(comm, rank, world, 10_000, stream=stream)
-        eng.seal(10_000)
-        eng.begin(d["uids"], d["pid"], d["tails"], d["ml"])
-    g = capture(instrument=True)
-    with torch.cuda.stream(stream):
-        g.replay()
-    torch.cuda.synchronize(dev)
-    steady_ms = sum(ev_s[i].elapsed_time(ev_e[i]) for i in range(chunk))
-    sst = eng.stats(reset=True)
+    # ---- timed region
     rec = dict(rec0)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_host0 = time.time()
     start.record(stream)
-    for s in range(args.warmup, total_steps):
-        rl_step(s, rec)
+    for i, s in enumerate(range(warmup, total_steps)):
+        rl_step(s, rec, evs[i])
     end.record(stream)
     torch.cuda.synchronize(dev)
+    log("[timed] decode ms per RL step: " + " ".join(f"{e[0].elapsed_time(e[1]):.1f}" for e in evs))
     t_host1 = time.time()
     if dist is not None:
         dist.barrier()
@@ -350,37 +325,40 @@ def run_ours(args, cfg, rank, world, dist):
     clocks.window(t_host0, t_host1)
     clk = clocks.stop()
     elapsed_ms = start.elapsed_time(end)
+    decode_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    first_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
     st = eng.stats(reset=True)
-    if sti["tokens"] != st["tokens"] or sti["rows_verified"] != st["rows_verified"]:
-        log(f"note: instrumented replay differs ({sti['tokens']} vs {st['tokens']} tokens, "
-            f"{sti['rows_verified']} vs {st['rows_verified']} rows)")
-    rec["verify_ms"] = reci["verify_ms"]
-    rec["verify_rows_verified"] = sti["rows_verified"]
-    rec["verify_rows_needed"] = sti["rows_needed"]
+    word = ctx.bs_sync_status()
+    if word:
+        raise SystemExit(f"device error word 0x{word:x} in the timed region: no number is reported")
     # ---- e2e: the same RL steps through the public API from pinned HOST buffers
-    e2e = run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, dist, replay_until_done)
+    e2e_r = run_e2e(args, cfg, ctx, eng, host[warmup:], stream, dev, capture, comm, rank, world, dist,
+                    replay_until_done, setup_step) if e2e else None
+    if e2e_r is not None and ctx.bs_sync_status():
+        raise SystemExit("device error word set in the e2e leg")
+    info = ctx.bsx_launch_info()
     # ---- gather over ranks
-    import torch as _t
-
-    vals = _t.tensor([elapsed_ms, float(st["tokens"]), e2e["ms"], float(e2e["tokens"])],
-                     dtype=_t.float64, device=dev)
+    vals = torch.tensor([elapsed_ms, float(st["tokens"]), e2e_r["ms"] if e2e_r else 0.0,
+                         float(e2e_r["tokens"]) if e2e_r else 0.0, decode_ms, float(st["rows_needed"]),
+                         float(st["rows_verified"])], dtype=torch.float64, device=dev)
     if dist is not None:
         mx = vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = vals.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        elapsed_all, tokens_all = float(mx[0]), float(sm[1])
-        e2e_ms_all, e2e_tok_all = float(mx[2]), float(sm[3])
+        agg = dict(elapsed_ms=float(mx[0]), tokens=float(sm[1]), e2e_ms=float(mx[2]), e2e_tokens=float(sm[3]),
+                   decode_ms=float(mx[4]), rows_needed=float(sm[5]), rows_verified=float(sm[6]))
     else:
-        elapsed_all, tokens_all = elapsed_ms, float(st["tokens"])
-        e2e_ms_all, e2e_tok_all = e2e["ms"], float(e2e["tokens"])
-    if comm is not None:
-        bs.nccl_comm_destroy(comm)
-    return dict(elapsed_ms=elapsed_all, tokens=tokens_all, st=st, rec=rec, clocks=clk,
-                steady_ms=steady_ms, sst=sst, e2e=e2e, e2e_ms=e2e_ms_all, e2e_tokens=e2e_tok_all)
+        agg = dict(elapsed_ms=elapsed_ms, tokens=float(st["tokens"]), e2e_ms=e2e_r["ms"] if e2e_r else 0.0,
+                   e2e_tokens=float(e2e_r["tokens"]) if e2e_r else 0.0, decode_ms=decode_ms,
+                   rows_needed=float(st["rows_needed"]), rows_verified=float(st["rows_verified"]))
+    bs.nccl_comm_destroy(comm)
+    return dict(agg=agg, st=st, rec=rec, clocks=clk, steady_ms=steady_ms, sst=sst, e2e=e2e_r,
+                first_ms=first_ms, decode_ms_local=decode_ms, resp0=resp0, info=info, n=n)
 
 
-def run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, dist, replay_until_done):
+def run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, dist, replay_until_done,
+            setup_step):
     """End-to-end through the public API: every RL step copies its inputs host->device from
     pinned memory (pools, prompt tails, uids, lengths) and reads the generated responses
     back device->host, inside the timed region."""
@@ -391,7 +369,7 @@ def run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, 
     resp = torch.full((n, Lmax), -1, dtype=torch.int32, device=dev)
     ctx.bs_rollout_bind_output(resp, Lmax)
     pinned = []
-    for h in host[args.warmup:]:
+    for h in host:
         pinned.append({key: torch.from_numpy(np.ascontiguousarray(h[key] if key != "uids" else
                                                                   h[key].view(np.int64))).pin_memory()
                        for key in ("seq_prompt", "seq_off", "tokens", "pid", "tails", "uids",
@@ -405,60 +383,142 @@ def run_e2e(args, cfg, ctx, eng, host, stream, dev, capture, comm, rank, world, 
     ctx.bs_stats_read(reset=True, stream=stream)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in pinned]
     for i, p in enumerate(pinned):
-        s = 20_000 + i
         with torch.cuda.stream(stream):
             d = {key: t.to(dev, non_blocking=True) for key, t in p.items()}
-            ctx.bs_draft_pool_put(s, d["seq_prompt"], d["seq_off"], d["tokens"],
-                                  int(p["tokens"].numel()), stream=stream)
-            if comm is not None:
-                ctx.bs_draft_exchange(comm, rank, world, s, stream=stream)
-            eng.seal(s)
-            eng.begin(d["uids"], d["pid"], d["tails"], d["max_len"])
-        g = capture()
-        replay_until_done(g)
+        setup_step(20_000 + i, dict(sp=d["seq_prompt"], off=d["seq_off"], tok=d["tokens"],
+                                     ntok=int(p["tokens"].numel()), pid=d["pid"], tails=d["tails"],
+                                     uids=d["uids"], ml=d["max_len"]))
+        evs[i][0].record(stream)
+        replay_until_done(capture())
+        evs[i][1].record(stream)
         with torch.cuda.stream(stream):
             resp_host.copy_(resp, non_blocking=True)
     end.record(stream)
     torch.cuda.synchronize(dev)
     ms = start.elapsed_time(end)
+    log("[e2e] decode ms per RL step: " + " ".join(f"{e[0].elapsed_time(e[1]):.1f}" for e in evs) +
+        f"; total {ms:.1f}")
     st = eng.stats(reset=True)
     ctx.bs_rollout_bind_output(None)
     return dict(ms=ms, tokens=st["tokens"], h2d=h2d, d2h=d2h)
 
 
 # ---------------------------------------------------------------------------- CPU oracle
-def cpu_oracle_sample(cfg, budget_s: float, rank: int = 0, world: int = 1):
-    """The oracle as it stands on the host cores, on a bounded sample of the same workload:
-    whole decoding steps of the first rollouts of one RL step until ~budget_s of oracle
-    time.  Returns (tokens/s, sample description, oracle seconds)."""
-    import oracle
+_ORC = {}
+
+
+def _oracle_worker(arg):
+    """One host core: whole decoding steps of its rollouts, round-robin, until its share of
+    the time budget of ORACLE time (draft lookup + Alg. 1 step; row generation excluded)."""
     from oracle.rollout import OracleRollout, bank_row_fn, pools_by_prompt, step
 
-    h = make_step_inputs(cfg, 0, rank, world)
-    # the single-GPU workload: pools of the rank's own prompts (world == 1 -> identical)
+    which, budget = arg
+    j = _ORC
+    h, cfg = j["h"], j["cfg"]
     pools = pools_by_prompt(h["seq_prompt"], h["seq_off"], h["tokens"])
     fn = bank_row_fn(h["spec"])
-    ros = [OracleRollout(prompt=int(h["pid"][b]), uid=int(h["uids"][b]),
-                         context=[int(x) for x in h["tails"][b]], max_len=int(h["max_len"][b]))
-           for b in range(len(h["pid"]))]
+    ros = {b: OracleRollout(prompt=int(h["pid"][b]), uid=int(h["uids"][b]),
+                            context=[int(x) for x in h["tails"][b]], max_len=int(h["max_len"][b]))
+           for b in which}
     timers = {}
-    tokens, nsteps = 0, 0
-    b = 0
-    while timers.get("oracle_s", 0.0) < budget_s:
-        ro = ros[b % len(ros)]
+    tokens = nsteps = 0
+    i = 0
+    while timers.get("oracle_s", 0.0) < budget and any(not r.finished for r in ros.values()):
+        ro = ros[which[i % len(which)]]
         if not ro.finished:
-            out = step(ro, pools, fn, k=cfg["k"], M=cfg["M"], Lmin=1, T=cfg["T"],
-                       top_p=cfg["top_p"], seed=0x5EED, eos=-1, timers=timers)
+            out = step(ro, pools, fn, k=cfg["k"], M=cfg["M"], Lmin=1, T=cfg["T"], top_p=cfg["top_p"],
+                       seed=0x5EED, eos=-1, timers=timers)
             if out is not None:
                 tokens += len(out.tokens)
                 nsteps += 1
-        b += 1
-    secs = timers["oracle_s"]
-    _ = oracle
-    desc = (f"{nsteps} decoding steps (lookup+verify) round-robin over the 256 rollouts of RL "
-            f"step 0, {timers.get('rows', 0)} logits rows, {tokens} tokens; oracle time only")
-    return tokens / secs, desc, secs
+        i += 1
+    return dict(tokens=tokens, steps=nsteps, rows=timers.get("rows", 0), secs=timers.get("oracle_s", 0.0),
+                gen={b: r.generated for b, r in ros.items()})
+
+
+def cpu_oracle_sample(cfg, budget_s: float, cores: int, rank: int = 0, world: int = 1):
+    """The oracle as it stands, on `cores` host cores (independent rollouts in forked
+    processes, each plain and single-threaded), on a bounded sample of RL step 0 of the same
+    workload.  Returns (tokens/s, sample description, generated tokens per rollout)."""
+    import multiprocessing as mp
+
+    h = make_step_inputs(cfg, 0, rank, world)
+    _ORC.clear()
+    _ORC.update(h=h, cfg=cfg)
+    n = len(h["pid"])
+    order = np.argsort(h["pid"], kind="stable")
+    groups = [list(map(int, g)) for g in np.array_split(order, cores) if len(g)]
+    if cores == 1:
+        res = [_oracle_worker((groups[0], budget_s))]
+    else:
+        with mp.get_context("fork").Pool(len(groups)) as pool:
+            res = pool.map(_oracle_worker, [(g, budget_s) for g in groups], chunksize=1)
+    tokens = sum(r["tokens"] for r in res)
+    secs = max(r["secs"] for r in res)  # the processes run concurrently
+    gen = {}
+    for r in res:
+        gen.update(r["gen"])
+    desc = (f"{sum(r['steps'] for r in res)} decoding steps (lookup + Alg. 1 step) of the {n} rollouts of "
+            f"RL step 0 on {len(groups)} core(s), {sum(r['rows'] for r in res)} logits rows, {tokens} tokens; "
+            f"oracle time only (the slowest core's)")
+    return tokens / secs, desc, gen
+
+
+def host_cpu():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def parity_check(resp0, gen):
+    """Warm-up RL step 0's emitted tokens (GPU) vs the oracle's on the sampled steps."""
+    if resp0 is None:
+        return None
+    bad, toks = 0, 0
+    for b, g in gen.items():
+        toks += len(g)
+        if [int(x) for x in resp0[b, : len(g)]] != list(g):
+            bad += 1
+    return {"rollouts": len(gen), "tokens": toks, "mismatched_rollouts": bad,
+            "what": "warm-up RL step 0, every rollout's tokens from the oracle sample's decoding steps"}
+
+
+def summarize(cfg, name, r, args, peaks_hbm):
+    """Numbers of one configuration from run_ours' result."""
+    agg, st = r["agg"], r["st"]
+    V = cfg["V"]
+    row_bytes = 2 * V
+    value = agg["tokens"] / (agg["elapsed_ms"] / 1e3)
+    achieved = agg["rows_needed"] * row_bytes / (agg["decode_ms"] * 1e-3) / 1e9
+    moved = agg["rows_verified"] * row_bytes / (agg["decode_ms"] * 1e-3) / 1e9
+    steady = r["sst"]["rows_needed"] * row_bytes / (r["steady_ms"] * 1e-3) / 1e9
+    steady_moved = r["sst"]["rows_verified"] * row_bytes / (r["steady_ms"] * 1e-3) / 1e9
+    return dict(value=value, ms_per_step=agg["elapsed_ms"] / args_steps(args, name),
+                achieved=achieved, moved=moved, steady=steady, steady_moved=steady_moved,
+                frac=achieved / peaks_hbm, steady_frac=steady / peaks_hbm,
+                decode_ms=agg["decode_ms"], elapsed_ms=agg["elapsed_ms"])
+
+
+def args_steps(args, name):
+    return args.steps if name == args.config else EXTRA_STEPS[1]
+
+
+EXTRA_STEPS = (3, 2)  # (warm-up, timed) RL steps of the extra TINY / LC lines
+
+
+def workload_str(name, cfg):
+    return (f"{name}: V={cfg['V']}, {cfg['prompts'] * cfg['G']} rollouts/GPU ({cfg['prompts']} prompts x "
+            f"{cfg['G']}), k={cfg['k']}, lognormal lengths mean {cfg['mean_len']} sigma {cfg['sigma']} cap "
+            f"{cfg['cap']}, T={cfg['T']}, top_p={cfg['top_p']}, pools {cfg['G_pre']}/prompt, match rate "
+            f"{cfg['match_rate']}, target rows per rollout (mode sample)")
 
 
 # ---------------------------------------------------------------------------- main
@@ -470,8 +530,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="q7")
     ap.add_argument("--chunk", type=int, default=64)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the TINY / LC lines")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -480,28 +541,25 @@ def main():
         log(f"note: WORLD_SIZE={world}, --gpus={args.gpus}")
     metric = "verified tokens/sec/GPU at V=151936, k=8; mean accepted length; HBM GB/s"
     unit = "verified tokens/s"
-    workload = (f"{args.config}: V={cfg['V']}, {cfg['prompts'] * cfg['G']} rollouts/GPU "
-                f"({cfg['prompts']} prompts x {cfg['G']}), k={cfg['k']}, lognormal lengths mean "
-                f"{cfg['mean_len']} sigma {cfg['sigma']} cap {cfg['cap']}, T={cfg['T']}, "
-                f"top_p={cfg['top_p']}, pools {cfg['G_pre']}/prompt, match rate "
-                f"{cfg['match_rate']}")
+    workload = workload_str(args.config, cfg)
+    ncores, cpu_model = host_cpu()
 
     if args.impl == "reference":
         if rank != 0:
             return
-        v, desc, secs = cpu_oracle_sample(cfg, args.cpu_budget / max(1, args.steps) * 1.0)
-        # K steps of the bounded sample (each ~budget/K s of oracle time)
-        vals = [v]
-        for _ in range(1, args.steps):
-            vals.append(cpu_oracle_sample(cfg, args.cpu_budget / max(1, args.steps))[0])
+        vals = []
+        desc = ""
+        for _ in range(args.steps):  # each step: a bounded sample on every host core
+            v, desc, _gen = cpu_oracle_sample(cfg, args.cpu_budget / max(1, args.steps), ncores)
+            vals.append(v)
         val = float(np.median(vals))
         out = {"impl": "reference", "metric": metric, "value": val, "unit": unit,
                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                "config": {"workload": workload},
-               "cpu_baseline": {"value": val, "unit": unit, "cores": 1, "kind": "oracle",
-                                "sample": desc},
+               "cpu_baseline": {"value": val, "unit": unit, "cores": ncores, "cpu": cpu_model,
+                                "kind": "oracle", "sample": desc},
                "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0}}
         print(json.dumps(out), flush=True)
@@ -515,32 +573,29 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         tdist.init_process_group("nccl")
         dist = tdist
-    r = run_ours(args, cfg, rank, world, dist)
+    r = run_ours(args, cfg, rank, world, dist, args.warmup, args.steps, bind_step0=(rank == 0))
+    extra = {}
+    if args.config == "q7" and not args.no_extra:
+        for name in ("tiny", "lc"):
+            extra[name] = (CONFIGS[name], run_ours(args, CONFIGS[name], rank, world, dist, *EXTRA_STEPS,
+                                                   e2e=False))
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
     st, rec = r["st"], r["rec"]
-    V = cfg["V"]
-    row_bytes = 2 * V
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback 6650 GB/s"
     hbm = hbm or 6650.0
-    ms_per_step = r["elapsed_ms"] / args.steps
-    value = r["tokens"] / (r["elapsed_ms"] / 1e3)
-    # dominant kernel: the verify op (one cluster-kernel launch), timed by captured events
-    vlaunches = rec["decode_steps"]
-    v_avg_ms = rec["verify_ms"] / max(1, vlaunches)
-    alg_bytes = rec["verify_rows_needed"] * row_bytes / max(1, vlaunches)   # per launch
-    moved_bytes = rec["verify_rows_verified"] * row_bytes / max(1, vlaunches)
-    achieved = alg_bytes / (v_avg_ms * 1e-3) / 1e9
-    steady_alg = r["sst"]["rows_needed"] * row_bytes / (r["steady_ms"] * 1e-3) / 1e9
-    steady_moved = r["sst"]["rows_verified"] * row_bytes / (r["steady_ms"] * 1e-3) / 1e9
-    cpu = None
+    sm = summarize(cfg, args.config, r, args, hbm)
+    cpu, parity = None, None
     if not args.no_cpu_baseline:
-        cv, desc, secs = cpu_oracle_sample(cfg, args.cpu_budget)
-        cpu = {"value": cv, "unit": unit, "cores": 1, "kind": "oracle", "sample": desc}
+        cv, desc, gen = cpu_oracle_sample(cfg, args.cpu_budget, ncores)
+        cv1, desc1, _ = cpu_oracle_sample(cfg, args.cpu_budget / 2, 1)
+        cpu = {"value": cv, "unit": unit, "cores": ncores, "cpu": cpu_model, "kind": "oracle", "sample": desc,
+               "single_core": {"value": cv1, "sample": desc1}}
+        parity = parity_check(r["resp0"], gen)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "verify_traffic.json")
     if os.path.exists(tp):
@@ -548,33 +603,47 @@ def main():
             traffic = json.load(open(tp)).get("bytes_per_launch")
         except ValueError:
             traffic = None
+    others = {}
+    for name, (c2, r2) in extra.items():
+        s2 = summarize(c2, name, r2, args, hbm)
+        others[name] = {"workload": workload_str(name, c2), "value": s2["value"], "unit": unit,
+                        "ms_per_step": s2["ms_per_step"], "steps": EXTRA_STEPS[1], "warmup": EXTRA_STEPS[0],
+                        "acceptance_length": r2["st"]["acceptance_length"],
+                        "draft_length": r2["st"]["draft_length"], "tokens": int(r2["agg"]["tokens"]),
+                        "roofline_frac": s2["frac"], "steady_frac": s2["steady_frac"],
+                        "hbm_gbs": {"algorithmic": s2["achieved"], "steady_algorithmic": s2["steady"]}}
     out = {
-        "metric": metric, "value": value, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "metric": metric, "value": sm["value"], "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sm["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded counter-hash bank of 8192 bf16 logit rows, perturbed pools)",
         "config": {"workload": workload, "parallelism": f"dp{args.gpus}",
                    "rollouts": cfg["prompts"] * cfg["G"] * args.gpus,
-                   "l2": "inputs larger than L2 (2.5 GB logit bank, rows drawn by hash)",
-                   "graph_chunk": args.chunk},
-        "per_gpu_value": value / args.gpus,
+                   "l2": "inputs larger than L2 (2.5 GB logit bank; every rollout reads its own rows)",
+                   "graph_chunk": args.chunk, "verify_launch": r["info"]},
+        "per_gpu_value": sm["value"] / args.gpus,
         "acceptance_length": st["acceptance_length"], "draft_length": st["draft_length"],
         "acceptance_rate": st["acceptance_rate"], "decode_steps": st["decode_steps"],
-        "tokens": int(r["tokens"]),
-        "hbm_gbs": {"algorithmic": achieved, "moved": moved_bytes / (v_avg_ms * 1e-3) / 1e9,
-                    "steady_algorithmic": steady_alg, "steady_moved": steady_moved},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": "bs_verify_commit_lookup (verify_cluster_kernel: in-kernel plan, rows, "
-                               "fused commit and next-draft lookup), avg over an instrumented replay "
-                               "of the timed RL steps",
-                     "peak_source": peak_src,
-                     "steady_frac": steady_alg / hbm},
+        "tokens": int(r["agg"]["tokens"]),
+        "hbm_gbs": {"algorithmic": sm["achieved"], "moved": sm["moved"],
+                    "steady_algorithmic": sm["steady"], "steady_moved": sm["steady_moved"]},
+        "roofline": {"bound": "hbm", "achieved": sm["achieved"], "peak": hbm, "unit": "GB/s",
+                     "frac": sm["achieved"] / hbm, "traffic": traffic,
+                     "kernel": "decoding step = bs_verify_commit_lookup (verify_cluster_kernel: plan, rows, "
+                               "fused commit and next-draft lookup) + the synthetic model's row kernel; "
+                               "timed by CUDA events around the decode-graph replays of the timed RL steps "
+                               "(outside the graphs), algorithmic bytes = rows Alg. 1 needs x 2V",
+                     "decode_ms": sm["decode_ms"], "timed_ms": sm["elapsed_ms"],
+                     "peak_source": peak_src, "steady_frac": sm["steady_frac"],
+                     "steady_what": "first 64-step chunk of a fresh RL step (all rollouts live), events "
+                                    "around that one graph replay"},
         "clocks": r["clocks"],
-        "e2e": {"value": r["e2e_tokens"] / (r["e2e_ms"] / 1e3), "unit": unit,
+        "e2e": {"value": r["agg"]["e2e_tokens"] / (r["agg"]["e2e_ms"] / 1e3), "unit": unit,
                 "h2d_bytes_per_step": r["e2e"]["h2d"], "d2h_bytes_per_step": r["e2e"]["d2h"]},
         "gpu_launches": rec["launches"],
         "cpu_baseline": cpu,
+        "parity": parity,
+        "other_configs": others,
     }
     print(json.dumps(out), flush=True)
     if dist is not None:

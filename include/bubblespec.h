@@ -276,7 +276,7 @@ bs_status bsx_synth_bank(void* bank_bf16, int64_t rows, int32_t V, uint32_t bank
                          float beta, void* stream);
 /* Synthetic target "forward": row_index[b*(k+1)+j] = target_row(prompt, pos+j, prev_j)
  * for j <= draft_len[b] (prev_0 = last context token, prev_j = draft[j-1]).
- * mode: 0 position, 1 markov, 2 mixed (workloads.TargetSpec). */
+ * mode: 0 position, 1 markov, 2 mixed, 3 sample (workloads.TargetSpec). */
 bs_status bsx_target_rows(bs_ctx* ctx, int32_t n, const int32_t* slots,
                           const int32_t* draft_tokens, const int32_t* draft_len, int32_t k,
                           uint32_t target_seed, int32_t mode, int64_t nbank,

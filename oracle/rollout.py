@@ -35,7 +35,7 @@ def pools_by_prompt(seq_prompt, seq_off, tokens):
 
 def step(ro: OracleRollout, pools: dict, row_fn, *, k: int, M: int, Lmin: int, T: float,
          top_p: float, seed: int, eos: int, timers: dict | None = None):
-    """One decoding step of one rollout.  row_fn(P, positions, prevs) -> list of bf16 rows."""
+    """One decoding step of one rollout.  row_fn(P, positions, prevs, uid) -> list of bf16 rows."""
     from . import lookup, verify_one
 
     if ro.finished or ro.pos >= ro.max_len:
@@ -46,7 +46,7 @@ def step(ro: OracleRollout, pools: dict, row_fn, *, k: int, M: int, Lmin: int, T
     draft = draft[:q]
     t1 = time.perf_counter()
     prevs = [ro.context[-1]] + draft
-    rows = row_fn(ro.prompt, [ro.pos + j for j in range(q + 1)], prevs)
+    rows = row_fn(ro.prompt, [ro.pos + j for j in range(q + 1)], prevs, ro.uid)
     t2 = time.perf_counter()
     out = verify_one(rows, T, top_p, seed, ro.uid, ro.pos, ro.max_len, eos, ro.finished, draft, k)
     t3 = time.perf_counter()
@@ -79,10 +79,12 @@ def bank_row_fn(spec, cache: dict | None = None):
 
     cache = {} if cache is None else cache
 
-    def fn(P, positions, prevs):
+    def fn(P, positions, prevs, uid=0):
         idx = target_row(spec, np.full(len(positions), P), np.asarray(positions),
-                         np.asarray(prevs))
+                         np.asarray(prevs), np.uint64(uid))
         out = []
+        if len(cache) > 2048:  # bounded: with per-rollout rows ("sample" mode) few rows repeat
+            cache.clear()
         for r in idx:
             r = int(r)
             if r not in cache:

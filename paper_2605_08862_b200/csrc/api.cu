@@ -430,7 +430,7 @@ bs_status bsx_target_rows(bs_ctx* c, int32_t n, const int32_t* slots, const int3
                           int64_t nbank, int64_t* row_index, void* stream) {
     if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
     if (n < 0 || n > c->cfg.max_rollouts || k < 0 || k > c->cfg.k_max || nbank < 1 || mode < 0 ||
-        mode > 2)
+        mode > 3 || (mode == 3 && nbank < 16))
         return fail(c, BS_ERR_INVALID, "bad target arguments");
     CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
     CK(c, launch_target_rows(c, n, slots, draft, draft_len, k, tseed, mode, nbank, row_index,

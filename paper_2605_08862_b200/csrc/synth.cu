@@ -23,7 +23,7 @@ __global__ void synth_bank_kernel(uint16_t* bank, int64_t rows, int V, uint32_t 
     const uint32_t sp = h32(seed ^ 0x5BD1E995u);
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
         const uint32_t hr = h32(s0 ^ (uint32_t)r);
-        const int peak = (int)(h32(sp ^ (uint32_t)r) % (uint32_t)V);
+        const int peak = (int)(h32(sp ^ (uint32_t)(r >> 4)) % (uint32_t)V);  // peak groups of 16 rows
         uint16_t* out = bank + r * (int64_t)V;
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < V; c += gridDim.x * blockDim.x)
             out[c] = synth_elem(hr, (uint32_t)c, peak, beta);
@@ -32,8 +32,8 @@ __global__ void synth_bank_kernel(uint16_t* bank, int64_t rows, int V, uint32_t 
 
 __global__ void target_rows_kernel(int n, int k, int M, const int32_t* slots, const int32_t* draft,
                                    const int32_t* draft_len, const int32_t* tail, const int32_t* pos,
-                                   const int32_t* prompt, uint32_t tseed, int mode, int64_t nbank,
-                                   int64_t* row_index) {
+                                   const int32_t* prompt, const unsigned long long* uid, uint32_t tseed,
+                                   int mode, int64_t nbank, int64_t* row_index) {
     pdl_wait();
     pdl_trigger();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -47,10 +47,13 @@ __global__ void target_rows_kernel(int n, int k, int M, const int32_t* slots, co
         const uint32_t t = (uint32_t)(pos[s] + j);
         const uint32_t pv = (uint32_t)(prev + 0x10000000);
         uint32_t h;
-        if (mode == 0) h = h32(base ^ t);
+        if (mode == 0 || mode == 3) h = h32(base ^ t);
         else if (mode == 1) h = h32(base ^ pv);
         else h = h32(h32(base ^ t) ^ pv);
-        row_index[(int64_t)b * (k + 1) + j] = (int64_t)(h % (uint32_t)nbank);
+        int64_t r = (int64_t)(h % (uint32_t)nbank);
+        if (mode == 3)  // "sample": the rollout's own row of the peak group (uid mod 16)
+            r = (int64_t)(h % (uint32_t)(nbank / 16)) * 16 + (int64_t)(uid[s] & 15ull);
+        row_index[(int64_t)b * (k + 1) + j] = r;
     }
 }
 
@@ -68,8 +71,8 @@ cudaError_t launch_target_rows(bs_ctx* ctx, int32_t n, const int32_t* slots, con
     if (n == 0) return cudaSuccess;
     return launch_pdl(target_rows_kernel, dim3((n + 127) / 128), dim3(128), 0, st, n, k, ctx->M,
                       slots, draft, draft_len, (const int32_t*)ctx->tail.p,
-                      (const int32_t*)ctx->pos.p, (const int32_t*)ctx->prompt.p, tseed, mode, nbank,
-                      row_index);
+                      (const int32_t*)ctx->pos.p, (const int32_t*)ctx->prompt.p,
+                      (const unsigned long long*)ctx->uid.p, tseed, mode, nbank, row_index);
 }
 
 }  // namespace bs

@@ -695,7 +695,8 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 if (nb) {
                     fence_proxy_async_smem();
                     mbar_arrive_expect_tx(&sh.full[bi], (uint32_t)nb * 2u);
-                    bulk_g2s(buf, src, (uint32_t)nb * 2u, &sh.full[bi], 0ull);
+                    // streamed once: evict-first keeps the draft index and pools L2-resident
+                    bulk_g2s(buf, src, (uint32_t)nb * 2u, &sh.full[bi], policy_evict_first());
                 } else {
                     mbar_arrive(&sh.full[bi]);
                 }

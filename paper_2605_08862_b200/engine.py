@@ -19,6 +19,9 @@ import torch
 from .api import Context
 
 
+TARGET_MODES = {"position": 0, "markov": 1, "mixed": 2, "sample": 3}  # bsx_target_rows modes
+
+
 @dataclass
 class Target:
     """Synthetic target policy: logits rows live in `bank` [nbank, V] (bf16, on device) and
@@ -26,7 +29,7 @@ class Target:
     bank: torch.Tensor
     nbank: int
     target_seed: int
-    mode: int  # 0 position, 1 markov, 2 mixed
+    mode: int  # 0 position, 1 markov, 2 mixed, 3 sample (workloads.TargetSpec)
 
 
 class RolloutEngine:

@@ -8,6 +8,7 @@ pytestmark = pytest.mark.gpu
 
 from workloads import TargetSpec  # noqa: E402
 from tests.gpu_util import bank_numpy, pools_for, setup_rollouts, to_dev  # noqa: E402
+from paper_2605_08862_b200.engine import TARGET_MODES  # noqa: E402
 
 
 def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fused="lookup"):
@@ -17,7 +18,7 @@ def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fuse
                      pool_capacity_tokens=max(1, pool_tokens), pool_capacity_seqs=max(1, pool_seqs),
                      seed=seed)
     bank = to_dev(bank_numpy(spec).view(np.int16))
-    mode = {"position": 0, "markov": 1, "mixed": 2}[spec.mode]
+    mode = TARGET_MODES[spec.mode]
     # "lookup": bs_verify_commit_lookup; "commit": lookup + bs_verify_commit; "none": lookup +
     # bs_verify_step + bs_commit
     eng = RolloutEngine(ctx, n, k, T, top_p, Target(bank, spec.nbank, spec.target_seed, mode),

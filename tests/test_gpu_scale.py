@@ -27,7 +27,7 @@ def _bench_inputs(name):
 def _run_gpu(bs, cfg, h, which, chunk, replays, eager_steps=0):
     """Decode rollouts `which` of the bench inputs h for 1 + chunk * replays steps (capture()
     runs one real warm-up step) on one context; returns (responses [len(which), L], stats)."""
-    from paper_2605_08862_b200.engine import RolloutEngine, Target
+    from paper_2605_08862_b200.engine import TARGET_MODES, RolloutEngine, Target
 
     which = np.asarray(which)
     n = len(which)
@@ -38,7 +38,8 @@ def _run_gpu(bs, cfg, h, which, chunk, replays, eager_steps=0):
     spec = h["spec"]
     bank = torch.empty((cfg["nbank"], V), dtype=torch.int16, device="cuda")
     bs.bsx_synth_bank(bank, cfg["nbank"], V, spec.bank_seed, spec.beta)
-    eng = RolloutEngine(ctx, n, k, cfg["T"], cfg["top_p"], Target(bank, cfg["nbank"], spec.target_seed, 0))
+    eng = RolloutEngine(ctx, n, k, cfg["T"], cfg["top_p"],
+                        Target(bank, cfg["nbank"], spec.target_seed, TARGET_MODES[spec.mode]))
     L = int(h["max_len"][which].max())
     resp = torch.full((n, L), -1, dtype=torch.int32, device="cuda")
     ctx.bs_rollout_bind_output(resp, L)

@@ -382,7 +382,7 @@ def _markov_setup(V, seed):
 def _run_spec_rollouts(orc, rows_by_prev, pools, n, L, k, T, eos, prompt_last=0, seed=11):
     from oracle.rollout import OracleRollout, run_rollouts
 
-    def row_fn(P, positions, prevs):
+    def row_fn(P, positions, prevs, uid=0):
         return [rows_by_prev[p] for p in prevs]
 
     ros = [OracleRollout(prompt=0, uid=u, context=[prompt_last], max_len=L) for u in range(n)]

@@ -45,10 +45,13 @@ def bf16_bits_to_f32(b):
 LOGIT_SCALE = np.float32(0.015625)  # 2^-6: s in [-510, 510] -> logits in [-7.97, 7.97], sd 2.31
 
 
+PEAK_GROUP = 16  # bank rows 16g .. 16g+15 share their peak column (same token, own noise)
+
+
 def bank_peak(bank_seed: int, rows, V: int):
-    """Peak (reference) column of each bank row."""
+    """Peak (reference) column of each bank row: a function of the row's group of 16."""
     s = h32(np.uint32(bank_seed & M32) ^ np.uint32(0x5BD1E995))
-    return (_mix(s, rows) % np.uint32(V)).astype(np.int32)
+    return (_mix(s, np.asarray(rows, dtype=np.int64) // PEAK_GROUP) % np.uint32(V)).astype(np.int32)
 
 
 def bank_rows(bank_seed: int, rows, V: int, beta: float) -> np.ndarray:
@@ -70,6 +73,9 @@ class TargetSpec:
     """The synthetic target policy: which bank row is the distribution at a position.
 
     mode "position": row(P, t)        — peaked at the prompt's reference text R_P[t]
+    mode "sample":   row(P, t, uid)   — like "position" (same peak R_P[t]), but each of a
+                                        prompt's samples (uid mod 16) reads its own row of the
+                                        peak group: no two rollouts share logits rows
     mode "markov":   row(P, prev)     — an order-1 Markov chain per prompt
     mode "mixed":    row(P, t, prev)  — depends on both (catches row/prefix misalignment)
     """
@@ -82,10 +88,14 @@ class TargetSpec:
     mode: str = "position"
 
 
-def target_row(spec: TargetSpec, P, t, prev):
+def target_row(spec: TargetSpec, P, t, prev, uid=0):
     """Bank row index of the target distribution for generated-token index t of a
-    rollout of prompt P whose previous token is prev (vectorised)."""
+    rollout (global id uid) of prompt P whose previous token is prev (vectorised)."""
     base = _mix(h32(np.uint32(spec.target_seed & M32)), P)
+    if spec.mode == "sample":
+        h = _mix(base, t)
+        g = (h % np.uint32(spec.nbank // PEAK_GROUP)).astype(np.int64)
+        return g * PEAK_GROUP + (np.asarray(uid, dtype=np.uint64) % np.uint64(PEAK_GROUP)).astype(np.int64)
     if spec.mode == "position":
         h = _mix(base, t)
     elif spec.mode == "markov":
@@ -99,7 +109,7 @@ def target_row(spec: TargetSpec, P, t, prev):
 
 def reference_text(spec: TargetSpec, P: int, length: int, prompt_last: int) -> np.ndarray:
     """R_P[t] = peak column of the target row at t when following the reference."""
-    if spec.mode == "position":  # rows do not depend on the previous token: vectorise
+    if spec.mode in ("position", "sample"):  # rows do not depend on the previous token
         r = target_row(spec, P, np.arange(length, dtype=np.int64), 0)
         return bank_peak(spec.bank_seed, r, spec.V).astype(np.int32)
     out = np.empty(length, dtype=np.int32)
