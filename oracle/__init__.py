@@ -65,15 +65,32 @@ def lib():
         L.orc_top_p_filter.restype = C.c_uint64
         L.orc_row_dist.argtypes = [P(C.c_uint16), C.c_int, C.c_float, C.c_float, P(C.c_uint64),
                                    P(_RowStats)]
+        L.orc_row_dist_k.argtypes = [P(C.c_uint16), C.c_int, C.c_float, C.c_float, C.c_int,
+                                     P(C.c_uint64), P(_RowStats)]
+        L.orc_top_k_filter.argtypes = [P(C.c_uint64), C.c_int, C.c_int]
+        L.orc_top_k_filter.restype = C.c_uint64
+        L.orc_verify_one_k.argtypes = [
+            P(P(C.c_uint16)), C.c_int, C.c_float, C.c_float, C.c_int32, C.c_uint64, C.c_uint64,
+            C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), C.c_int32, C.c_int32,
+            P(C.c_int32), P(C.c_int32), P(C.c_int32), P(C.c_float), P(C.c_double), P(C.c_uint64),
+            P(C.c_int32)]
         L.orc_sample_index.argtypes = [P(C.c_uint64), C.c_int, C.c_int32, C.c_uint64]
         L.orc_sample_index.restype = C.c_int32
         L.orc_verify_one.argtypes = [
             P(P(C.c_uint16)), C.c_int, C.c_float, C.c_float, C.c_uint64, C.c_uint64, C.c_int32,
             C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), C.c_int32, C.c_int32, P(C.c_int32),
             P(C.c_int32), P(C.c_int32), P(C.c_float), P(C.c_double), P(C.c_uint64), P(C.c_int32)]
+        L.orc_verify_one_r.argtypes = [
+            P(P(C.c_uint16)), C.c_int, C.c_float, C.c_float, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+            C.c_int32, P(C.c_int32), C.c_int32, C.c_int32, P(C.c_uint32), P(C.c_uint32),
+            P(C.c_int32), P(C.c_int32), P(C.c_int32), P(C.c_float), P(C.c_double), P(C.c_uint64),
+            P(C.c_int32)]
         L.orc_lookup.argtypes = [P(C.c_int32), P(C.c_int64), C.c_int32, P(C.c_int32), C.c_int32,
                                  C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32),
                                  P(C.c_int32)]
+        L.orc_lookup_ngram.argtypes = [P(C.c_int32), P(C.c_int64), C.c_int32, P(C.c_int32),
+                                       C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_int32),
+                                       P(C.c_int32), P(C.c_int32)]
         _lib = L
     return _lib
 
@@ -118,6 +135,12 @@ def temp_scale(T: float) -> float:
     return float(lib().orc_temp_scale(T))
 
 
+def top_k_filter(masses, top_k: int):
+    m = np.ascontiguousarray(masses, dtype=np.uint64).copy()
+    z = lib().orc_top_k_filter(_ptr(m, C.c_uint64), len(m), top_k)
+    return m, int(z)
+
+
 def top_p_filter(masses, top_p: float):
     m = np.ascontiguousarray(masses, dtype=np.uint64).copy()
     z = lib().orc_top_p_filter(_ptr(m, C.c_uint64), len(m), top_p)
@@ -135,12 +158,12 @@ class RowDist:
     norm_r: float
 
 
-def row_dist(row_bits: np.ndarray, T: float, top_p: float = 1.0) -> RowDist:
+def row_dist(row_bits: np.ndarray, T: float, top_p: float = 1.0, top_k: int = 0) -> RowDist:
     row = np.ascontiguousarray(row_bits, dtype=np.uint16)
     mass = np.zeros(len(row), dtype=np.uint64)
     st = _RowStats()
-    rc = lib().orc_row_dist(_ptr(row, C.c_uint16), len(row), T, top_p, _ptr(mass, C.c_uint64),
-                            C.byref(st))
+    rc = lib().orc_row_dist_k(_ptr(row, C.c_uint16), len(row), T, top_p, top_k, _ptr(mass, C.c_uint64),
+                              C.byref(st))
     if rc != OK:
         raise OracleError(rc)
     return RowDist(mass, int(st.z), int(st.z_full), float(st.m), int(st.greedy),
@@ -170,7 +193,7 @@ class StepOut:
 
 
 def verify_one(rows, T: float, top_p: float, seed: int, uid: int, pos: int, max_len: int,
-               eos: int, finished: bool, draft, k: int) -> StepOut:
+               eos: int, finished: bool, draft, k: int, top_k: int = 0) -> StepOut:
     """Alg. 1 step for one rollout.  rows: list of q+1 bf16 rows (uint16 arrays)."""
     V = len(rows[0])
     nr = len(rows)
@@ -182,7 +205,7 @@ def verify_one(rows, T: float, top_p: float, seed: int, uid: int, pos: int, max_
     nrm = np.zeros(k + 1, dtype=np.float32)
     n64 = np.zeros(k + 1, dtype=np.float64)
     zz = np.zeros(k + 1, dtype=np.uint64)
-    rc = lib().orc_verify_one(arr, V, T, top_p, seed, uid, pos, max_len, eos, int(finished),
+    rc = lib().orc_verify_one_k(arr, V, T, top_p, top_k, seed, uid, pos, max_len, eos, int(finished),
                               _ptr(d, C.c_int32), len(draft), k, _ptr(out, C.c_int32),
                               C.byref(ol), C.byref(oa), _ptr(nrm, C.c_float),
                               _ptr(n64, C.c_double), _ptr(zz, C.c_uint64), C.byref(ru))
@@ -191,6 +214,30 @@ def verify_one(rows, T: float, top_p: float, seed: int, uid: int, pos: int, max_
     n = ru.value
     return StepOut([int(x) for x in out[: ol.value]], oa.value, n, [float(x) for x in nrm[:n]],
                    [float(x) for x in n64[:n]], [int(x) for x in zz[:n]])
+
+
+def _r128_words(r: int):
+    return [(r >> 96) & 0xFFFFFFFF, (r >> 64) & 0xFFFFFFFF, (r >> 32) & 0xFFFFFFFF, r & 0xFFFFFFFF]
+
+
+def verify_one_r(rows, T: float, top_p: float, pos: int, max_len: int, eos: int, draft, k: int,
+                 r_acc, r_smp, top_k: int = 0) -> StepOut:
+    """Alg. 1 step with caller-chosen uniforms: r_acc[j] / r_smp[j] are the 128-bit integers
+    r128 of the accept test on row j and of a sample from row j (j = 0..k)."""
+    V = len(rows[0])
+    keep = [np.ascontiguousarray(r, dtype=np.uint16) for r in rows]
+    arr = (C.POINTER(C.c_uint16) * len(keep))(*[_ptr(r, C.c_uint16) for r in keep])
+    d = np.ascontiguousarray(np.asarray(list(draft) + [0], dtype=np.int32))
+    ra = np.asarray([w for r in r_acc for w in _r128_words(int(r))], dtype=np.uint32)
+    rs = np.asarray([w for r in r_smp for w in _r128_words(int(r))], dtype=np.uint32)
+    out = np.zeros(k + 1, dtype=np.int32)
+    ol, oa, ru = C.c_int32(), C.c_int32(), C.c_int32()
+    rc = lib().orc_verify_one_r(arr, V, T, top_p, top_k, pos, max_len, eos, 0, _ptr(d, C.c_int32), len(draft), k,
+                                _ptr(ra, C.c_uint32), _ptr(rs, C.c_uint32), _ptr(out, C.c_int32),
+                                C.byref(ol), C.byref(oa), None, None, None, C.byref(ru))
+    if rc != OK:
+        raise OracleError(rc)
+    return StepOut([int(x) for x in out[: ol.value]], oa.value, ru.value, [], [], [])
 
 
 # ---------------------------------------------------------------- lookup
@@ -211,6 +258,24 @@ def lookup(pool_seqs, ctx, M: int, Lmin: int, K: int):
     if rc != OK:
         raise OracleError(rc)
     return [int(x) for x in draft[: q.value]], ms.value
+
+
+def lookup_ngram(pool_seqs, ctx, n_min: int, n_max: int, K: int):
+    """n-gram linear-scan drafter (reading N1) over one prompt's pool.  Returns (draft, n)."""
+    lens = [len(s) for s in pool_seqs]
+    off = np.zeros(len(pool_seqs) + 1, dtype=np.int64)
+    off[1:] = np.cumsum(lens)
+    toks = (np.concatenate([np.asarray(s, dtype=np.int32) for s in pool_seqs])
+            if pool_seqs and off[-1] > 0 else np.zeros(1, dtype=np.int32))
+    c = np.ascontiguousarray(np.asarray(list(ctx) if len(ctx) else [0], dtype=np.int32))
+    draft = np.zeros(max(K, 1), dtype=np.int32)
+    q, nn = C.c_int32(), C.c_int32()
+    rc = lib().orc_lookup_ngram(_ptr(toks, C.c_int32), _ptr(off, C.c_int64), len(pool_seqs),
+                                _ptr(c, C.c_int32), len(ctx), n_min, n_max, K, _ptr(draft, C.c_int32),
+                                C.byref(q), C.byref(nn))
+    if rc != OK:
+        raise OracleError(rc)
+    return [int(x) for x in draft[: q.value]], nn.value
 
 
 from .rollout import OracleRollout, run_rollouts  # noqa: E402,F401

@@ -190,8 +190,39 @@ uint64_t orc_top_p_filter(uint64_t* mass, int V, float top_p) {
     return zk;
 }
 
+/* R5k top-k ("any top-p/top-k filtering"; SPEC S:74 applies top-k, then top-p): keep i
+ * <=> fewer than top_k tokens have a strictly larger mass, i.e. mass_i >= the top_k-th largest
+ * mass (tie-closed like R5: a tie group straddling the k-th place is kept whole).  top_k <= 0
+ * or >= V keeps every token.  Zeroes the dropped masses, returns the kept sum.               */
+uint64_t orc_top_k_filter(uint64_t* mass, int V, int top_k) {
+    uint64_t Z = 0;
+    if (top_k <= 0 || top_k >= V) {
+        for (int i = 0; i < V; ++i) Z += mass[i];
+        return Z;
+    }
+    uint64_t* sorted = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)V);
+    memcpy(sorted, mass, sizeof(uint64_t) * (size_t)V);
+    qsort(sorted, (size_t)V, sizeof(uint64_t), cmp_u64_desc);
+    uint64_t tau = sorted[top_k - 1];
+    free(sorted);
+    for (int i = 0; i < V; ++i) {
+        if (mass[i] >= tau) Z += mass[i];
+        else mass[i] = 0;
+    }
+    return Z;
+}
+
+/* Row distribution with top-k then top-p (R5k, R5); orc_row_dist is top_k = 0. */
+int orc_row_dist_k(const uint16_t* row, int V, float T, float top_p, int top_k, uint64_t* mass,
+                   orc_row_stats* st);
+
 int orc_row_dist(const uint16_t* row, int V, float T, float top_p, uint64_t* mass,
                  orc_row_stats* st) {
+    return orc_row_dist_k(row, V, T, top_p, 0, mass, st);
+}
+
+int orc_row_dist_k(const uint16_t* row, int V, float T, float top_p, int top_k, uint64_t* mass,
+                   orc_row_stats* st) {
     if (V < 1 || !(T >= 0.0f) || !(top_p > 0.0f) || !(top_p <= 1.0f)) return ORC_ERR_INVALID;
     /* R0 + R1 */
     float m = -INFINITY;
@@ -234,7 +265,8 @@ int orc_row_dist(const uint16_t* row, int V, float T, float top_p, uint64_t* mas
     st->z_full = Z;
     st->norm_fp64 = nf;
     st->norm_r = (float)ldexp((double)Z, -S);
-    st->z = orc_top_p_filter(mass, V, top_p);
+    orc_top_k_filter(mass, V, top_k);           /* R5k first ...                 */
+    st->z = orc_top_p_filter(mass, V, top_p);   /* ... then R5 on the top-k masses     */
     return ORC_OK;
 }
 
@@ -260,11 +292,16 @@ int32_t orc_sample_index(const uint64_t* mass, int V, int32_t excl, uint64_t U) 
 /*   (pos+j-1, ACCEPT=0).  Residual / bonus: counter (pos+s, SAMPLE=1).        */
 /* Reading L6: q is clamped to max_len - pos - 1 (the last token is sampled).   */
 /* ------------------------------------------------------------------------- */
-int orc_verify_one(const uint16_t* const* rows, int V, float T, float top_p, uint64_t seed,
-                   uint64_t uid, int32_t pos, int32_t max_len, int32_t eos, int32_t finished,
-                   const int32_t* draft, int32_t q_in, int32_t k, int32_t* out_tokens,
-                   int32_t* out_len, int32_t* out_acc, float* out_norm_r, double* out_norm64,
-                   uint64_t* out_z, int32_t* rows_used) {
+/* orc_verify_one_r: the step with the uniforms supplied by the caller.  r_acc + 4*j is the
+ * r128 of the accept test of d_{j+1} on row j (counter (pos+j, ACCEPT)), r_smp + 4*j the r128
+ * of a sample from row j (counter (pos+j, SAMPLE)), j = 0..k.  orc_verify_one fills them from
+ * Philox (R6); tests drive every branch of a step with chosen uniforms through this entry
+ * (the exact losslessness enumeration of SURVEY c.6 / S:591).                              */
+int orc_verify_one_r(const uint16_t* const* rows, int V, float T, float top_p, int32_t top_k, int32_t pos,
+                     int32_t max_len, int32_t eos, int32_t finished, const int32_t* draft,
+                     int32_t q_in, int32_t k, const uint32_t* r_acc, const uint32_t* r_smp,
+                     int32_t* out_tokens, int32_t* out_len, int32_t* out_acc, float* out_norm_r,
+                     double* out_norm64, uint64_t* out_z, int32_t* rows_used) {
     *out_len = 0;
     *out_acc = 0;
     *rows_used = 0;
@@ -280,17 +317,15 @@ int orc_verify_one(const uint16_t* const* rows, int V, float T, float top_p, uin
     int status = ORC_OK;
     for (int j = 0; j <= q; ++j) {
         orc_row_stats st;
-        status = orc_row_dist(rows[j], V, T, top_p, mass, &st);
+        status = orc_row_dist_k(rows[j], V, T, top_p, top_k, mass, &st);
         if (status != ORC_OK) break;
         *rows_used = j + 1;
         if (out_norm_r) out_norm_r[j] = st.norm_r;
         if (out_norm64) out_norm64[j] = st.norm_fp64;
         if (out_z) out_z[j] = st.z;
-        uint32_t r[4];
         if (j < q) {
             int32_t d = draft[j];
-            orc_draw_r128(seed, uid, (uint32_t)(pos + j), 0u, r);
-            uint64_t U = orc_uniform_floor(r, st.z);
+            uint64_t U = orc_uniform_floor(r_acc + 4 * j, st.z);
             if (U < mass[d]) { /* accepted (Eq. 2) */
                 out_tokens[n_out++] = d;
                 *out_acc += 1;
@@ -298,19 +333,43 @@ int orc_verify_one(const uint16_t* const* rows, int V, float T, float top_p, uin
                 continue;
             }
             /* rejected: one recovered token from the residual (Eq. 3) */
-            orc_draw_r128(seed, uid, (uint32_t)(pos + j), 1u, r);
-            uint64_t Ux = orc_uniform_floor(r, st.z - mass[d]);
+            uint64_t Ux = orc_uniform_floor(r_smp + 4 * j, st.z - mass[d]);
             out_tokens[n_out++] = orc_sample_index(mass, V, d, Ux);
             break;
         }
         /* j == q: all q drafts accepted (or q == 0): bonus / plain sample */
-        orc_draw_r128(seed, uid, (uint32_t)(pos + q), 1u, r);
-        uint64_t Ub = orc_uniform_floor(r, st.z);
+        uint64_t Ub = orc_uniform_floor(r_smp + 4 * q, st.z);
         out_tokens[n_out++] = orc_sample_index(mass, V, -1, Ub);
     }
     free(mass);
     *out_len = n_out;
     return status;
+}
+
+int orc_verify_one_k(const uint16_t* const* rows, int V, float T, float top_p, int32_t top_k,
+                     uint64_t seed, uint64_t uid, int32_t pos, int32_t max_len, int32_t eos,
+                     int32_t finished, const int32_t* draft, int32_t q_in, int32_t k,
+                     int32_t* out_tokens, int32_t* out_len, int32_t* out_acc, float* out_norm_r,
+                     double* out_norm64, uint64_t* out_z, int32_t* rows_used) {
+    if (k < 0 || k > 64) return ORC_ERR_INVALID;
+    uint32_t r_acc[4 * 65], r_smp[4 * 65];
+    for (int j = 0; j <= k; ++j) {
+        orc_draw_r128(seed, uid, (uint32_t)(pos + j), 0u, r_acc + 4 * j);
+        orc_draw_r128(seed, uid, (uint32_t)(pos + j), 1u, r_smp + 4 * j);
+    }
+    return orc_verify_one_r(rows, V, T, top_p, top_k, pos, max_len, eos, finished, draft, q_in, k,
+                            r_acc, r_smp, out_tokens, out_len, out_acc, out_norm_r, out_norm64,
+                            out_z, rows_used);
+}
+
+int orc_verify_one(const uint16_t* const* rows, int V, float T, float top_p, uint64_t seed,
+                   uint64_t uid, int32_t pos, int32_t max_len, int32_t eos, int32_t finished,
+                   const int32_t* draft, int32_t q_in, int32_t k, int32_t* out_tokens,
+                   int32_t* out_len, int32_t* out_acc, float* out_norm_r, double* out_norm64,
+                   uint64_t* out_z, int32_t* rows_used) {
+    return orc_verify_one_k(rows, V, T, top_p, 0, seed, uid, pos, max_len, eos, finished, draft,
+                            q_in, k, out_tokens, out_len, out_acc, out_norm_r, out_norm64, out_z,
+                            rows_used);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -396,5 +455,41 @@ int orc_lookup(const int32_t* tokens, const int64_t* seq_off, int32_t n_seqs, co
     free(occ_e);
     free(kids);
     *q_out = q;
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Draft-source variant: the n-gram linear-scan drafter ("an n-gram-style */
+/* scheme that performs pattern matching directly over raw token sequences",    */
+/* P:405 "merely performs a linear match of repeated token sequences to return  */
+/* the candidate with the longest common prefix"; the paper's Table 7 ablation, */
+/* P:389-406).  Reading N1: the anchor is the longest suffix     */
+/* y[-n:], n in [n_min, min(n_max, |y|)], that occurs in the prompt's pool       */
+/* followed by at least one token; among its occurrences the FIRST in pool order */
+/* (sequence index, then position) wins, and the draft is the up to K tokens    */
+/* that follow it in its own sequence.  No counting, no index: the scan is      */
+/* linear in the pool (the cost the paper attributes to it).            */
+/* ------------------------------------------------------------------------- */
+int orc_lookup_ngram(const int32_t* tokens, const int64_t* seq_off, int32_t n_seqs,
+                     const int32_t* ctx, int32_t ctx_len, int32_t n_min, int32_t n_max, int32_t K,
+                     int32_t* draft, int32_t* q_out, int32_t* n_out) {
+    *q_out = 0;
+    *n_out = 0;
+    if (n_min < 1 || n_max < n_min || K < 0) return ORC_ERR_INVALID;
+    int32_t top = ctx_len < n_max ? ctx_len : n_max;
+    for (int32_t m = top; m >= n_min; --m) {
+        const int32_t* w = ctx + ctx_len - m;
+        for (int32_t s = 0; s < n_seqs; ++s) {
+            int64_t a = seq_off[s], b = seq_off[s + 1];
+            for (int64_t st = a; st + m < b; ++st) { /* st+m < b: followed by a token */
+                if (!window_at(tokens, st, b, w, m)) continue;
+                int32_t q = 0;
+                for (int64_t p = st + m; p < b && q < K; ++p) draft[q++] = tokens[p];
+                *q_out = q;
+                *n_out = m;
+                return ORC_OK;
+            }
+        }
+    }
     return ORC_OK;
 }

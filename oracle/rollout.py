@@ -34,21 +34,28 @@ def pools_by_prompt(seq_prompt, seq_off, tokens):
 
 
 def step(ro: OracleRollout, pools: dict, row_fn, *, k: int, M: int, Lmin: int, T: float,
-         top_p: float, seed: int, eos: int, timers: dict | None = None):
-    """One decoding step of one rollout.  row_fn(P, positions, prevs, uid) -> list of bf16 rows."""
-    from . import lookup, verify_one
+         top_p: float, seed: int, eos: int, timers: dict | None = None, top_k: int = 0,
+         ngram: tuple | None = None):
+    """One decoding step of one rollout.  row_fn(P, positions, prevs, uid) -> list of bf16 rows.
+    ngram = (n_min, n_max): draft with the n-gram linear-scan drafter (reading N1) instead of
+    the suffix lookup."""
+    from . import lookup, lookup_ngram, verify_one
 
     if ro.finished or ro.pos >= ro.max_len:
         return None
     t0 = time.perf_counter()
-    draft, mstar = lookup(pools.get(ro.prompt, []), ro.context[-M:], M, Lmin, k)
+    if ngram is None:
+        draft, mstar = lookup(pools.get(ro.prompt, []), ro.context[-M:], M, Lmin, k)
+    else:
+        draft, mstar = lookup_ngram(pools.get(ro.prompt, []), ro.context[-M:], ngram[0], ngram[1], k)
     q = min(len(draft), k, max(0, ro.max_len - ro.pos - 1))
     draft = draft[:q]
     t1 = time.perf_counter()
     prevs = [ro.context[-1]] + draft
     rows = row_fn(ro.prompt, [ro.pos + j for j in range(q + 1)], prevs, ro.uid)
     t2 = time.perf_counter()
-    out = verify_one(rows, T, top_p, seed, ro.uid, ro.pos, ro.max_len, eos, ro.finished, draft, k)
+    out = verify_one(rows, T, top_p, seed, ro.uid, ro.pos, ro.max_len, eos, ro.finished, draft, k,
+                     top_k=top_k)
     t3 = time.perf_counter()
     if timers is not None:
         timers["oracle_s"] = timers.get("oracle_s", 0.0) + (t1 - t0) + (t3 - t2)
@@ -63,12 +70,12 @@ def step(ro: OracleRollout, pools: dict, row_fn, *, k: int, M: int, Lmin: int, T
 
 
 def run_rollouts(rollouts, pools, row_fn, *, k, M, Lmin, T, top_p, seed, eos, max_steps=None,
-                 timers=None):
+                 timers=None, top_k=0, ngram=None):
     for ro in rollouts:
         n = 0
         while not ro.finished and (max_steps is None or n < max_steps):
             step(ro, pools, row_fn, k=k, M=M, Lmin=Lmin, T=T, top_p=top_p, seed=seed, eos=eos,
-                 timers=timers)
+                 timers=timers, top_k=top_k, ngram=ngram)
             n += 1
     return rollouts
 

@@ -95,3 +95,59 @@ def test_route_plan_host_logic():
     src, dst, ln, pr, nt = bs_route_plan(world, 0, counts, offs.ravel(), prm.ravel(), max_seqs,
                                          max_tok)
     assert list(pr) == [3, 6, 9] and list(ln) == [2, 4, 5] and list(src) == [0, 20, 24]
+
+
+def _golden(tag):
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.txt")):
+        if line.startswith("# " + tag):
+            return line
+    raise KeyError(tag)
+
+
+def test_metrics_from_counters_spec_hand_trace():
+    """SPEC S:494-496 hand trace (tests/golden/spec_examples.txt 'metrics'): three verification
+    steps emitting (2, 3, 1) tokens for (4, 4, 2) proposed drafts -> AL 2.0, DL 10/3, AR 0.3,
+    through the engine's counter -> metric conversion (summarize_stats)."""
+    import re
+
+    from paper_2605_08862_b200.engine import summarize_stats
+
+    line = _golden("metrics")
+    emitted = [int(x) for x in re.search(r"emitted \(([\d,]+)\)", line).group(1).split(",")]
+    proposed = [int(x) for x in re.search(r"proposed \(([\d,]+)\)", line).group(1).split(",")]
+    al, num, den, ar = re.search(r"AL ([\d.]+), DL (\d+)/(\d+), AR ([\d.]+)", line).groups()
+    st = np.zeros(41, dtype=np.uint64)
+    st[0] = len(emitted)                          # verification steps
+    st[2] = sum(emitted)                          # tokens they emitted
+    st[4] = sum(e - 1 for e in emitted)           # accepted drafts (each step ends in a sample)
+    st[5] = sum(proposed)
+    for e in emitted:
+        st[8 + e] += 1
+    m = summarize_stats(st)
+    assert m["acceptance_length"] == float(al)
+    assert m["draft_length"] == int(num) / int(den)
+    assert abs(m["acceptance_rate"] - float(ar)) < 1e-12
+    assert m["streak_hist"][1:4] == [1, 1, 1]
+
+
+def test_metric_identity_table1():
+    """AR = (AL - 1) / DL (SURVEY c.6 metrics pin) on the paper's Table 1 rows (P:269, P:273,
+    P:277, golden 'table1'): summarize_stats on counters built from each row's AL and DL
+    reproduces the printed AR to the table's rounding."""
+    import re
+
+    from paper_2605_08862_b200.engine import summarize_stats
+
+    line = _golden("table1")
+    rows = re.findall(r"\(AL ([\d.]+), DL ([\d.]+), AR ([\d.]+)%\)|\(([\d.]+), ([\d.]+), ([\d.]+)%\)", line)
+    assert len(rows) == 3
+    for r in rows:
+        al, dl, ar = [float(x) for x in (r[:3] if r[0] else r[3:])]
+        steps = 10_000
+        st = np.zeros(41, dtype=np.uint64)
+        st[0] = steps
+        st[2] = round(al * steps)
+        st[4] = round((al - 1) * steps)
+        st[5] = round(dl * steps)
+        m = summarize_stats(st)
+        assert abs(100 * m["acceptance_rate"] - ar) < 0.06, (al, dl, ar, m["acceptance_rate"])

@@ -219,6 +219,62 @@ def test_top_p_nucleus_properties(orc):
 
 
 # ------------------------------------------------------------------ sampling (R8), Eq. 3
+def test_top_k_hand_examples(orc):
+    """Reading R5k (P:202 'any top-p/top-k filtering'): keep the top_k heaviest masses,
+    tie-closed.  (5,3,2), top_k 2 -> (0.625, 0.375, 0) after renormalisation; ties (4,4,4,1):
+    top_k 1 or 2 keeps the whole tie group; top_k 0 or >= V is the identity."""
+    for scale in (1, 1 << 20, 1 << 40):
+        m, z = orc.top_k_filter(np.array([5, 3, 2], dtype=np.uint64) * np.uint64(scale), 2)
+        assert [Fraction(int(x), z) for x in m] == [Fraction(5, 8), Fraction(3, 8), 0]
+    for kk in (1, 2, 3):
+        m, z = orc.top_k_filter(np.array([4, 4, 1, 4], dtype=np.uint64), kk)
+        assert list(m) == [4, 4, 0, 4] and z == 12
+    m, z = orc.top_k_filter(np.array([4, 4, 1, 4], dtype=np.uint64), 4)
+    assert list(m) == [4, 4, 1, 4] and z == 13
+    m, z = orc.top_k_filter(np.array([7, 0, 2], dtype=np.uint64), 0)
+    assert list(m) == [7, 0, 2] and z == 9
+
+
+def test_top_k_properties_random(orc):
+    """Tie-closed top-k on random masses (many ties): every mass is kept or zeroed; the kept
+    set is a top set of the mass order (each kept mass > each dropped one); if anything was
+    dropped it has >= top_k members and is minimal (fewer than top_k masses exceed its
+    lightest level); filtering twice changes nothing (SPEC S:96's idempotence holds for
+    top-k)."""
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        V = int(rng.integers(1, 40))
+        mass = rng.integers(0, 6, V).astype(np.uint64) * np.uint64(1 << int(rng.integers(0, 40)))
+        kk = int(rng.integers(0, V + 3))
+        m, z = orc.top_k_filter(mass, kk)
+        assert ((m == mass) | (m == 0)).all() and z == int(m.sum())
+        kept, dropped = mass[m > 0], mass[(m == 0) & (mass > 0)]
+        if kk <= 0 or kk >= V:
+            assert len(dropped) == 0
+        if len(dropped):
+            assert len(kept) >= kk and dropped.max() < kept.min()
+            assert int((mass > kept.min()).sum()) < kk
+        m2, z2 = orc.top_k_filter(m, kk)
+        assert (m2 == m).all() and z2 == z
+
+
+def test_top_k_then_top_p_order(orc):
+    """SPEC S:74 / S:99 filter order, top-k THEN top-p, on a row whose masses are ~(4,3,2,1)
+    (logits ln 4, ln 3, ln 2, 0): top_k 2 renormalises to ~(4/7, 3/7) and top_p 0.5 then keeps
+    only token 0 (4/7 >= 0.5); the opposite order would keep {0, 1} (0.4 < 0.5).  top_k 1
+    equals greedy's support (argmax), top_k = V equals no filter."""
+    row = bf16_row([math.log(4), math.log(3), math.log(2), 0.0])
+    d = orc.row_dist(row, 1.0, 0.5, 2)
+    assert [int(x) > 0 for x in d.mass] == [True, False, False, False] and d.z == int(d.mass[0])
+    d = orc.row_dist(row, 1.0, 1.0, 2)
+    assert [int(x) > 0 for x in d.mass] == [True, True, False, False]
+    d = orc.row_dist(row, 1.0, 0.5, 0)
+    assert [int(x) > 0 for x in d.mass] == [True, True, False, False]
+    full = orc.row_dist(row, 1.0)
+    assert (orc.row_dist(row, 1.0, 1.0, 4).mass == full.mass).all()
+    assert int(np.argmax(orc.row_dist(row, 1.0, 1.0, 1).mass)) == orc.row_dist(row, 0.0).greedy
+
+
 def test_inverse_cdf_spec_example(orc):
     """(0.5,0.5): u = 0.25 -> 0, u = 0.75 -> 1; S:85 degenerate (0,1,0) -> 1."""
     mass = [1, 1]
@@ -427,6 +483,91 @@ def test_lossless_sequence_distribution_chi_square(orc):
     assert chisquare(obs, ex).pvalue > 1e-3
 
 
+@pytest.mark.parametrize("T,top_p", [(1.0, 1.0), (0.7, 1.0), (1.0, 0.8), (0.0, 1.0)])
+def test_lossless_exact_enumeration(orc, T, top_p):
+    """S:591 / SURVEY c.6 'losslessness, exact' (P:211 'exactly preserves the target rollout
+    distribution'): V=4 order-1 Markov target, L=5, K=2, EOS=3, a 6-sequence pool.  Every
+    branch of every speculative step is enumerated with the ideal uniform (accept d with
+    mass'(d)/Z', residual x with mass'_x/(Z'-mass'(d)), bonus x with mass'_x/Z'), and each branch
+    is confirmed by driving the oracle's step (orc_verify_one_r) with a uniform inside that
+    branch's interval.  The distribution over whole rollouts EQUALS the autoregressive product
+    of the same rows (Fractions: TV = 0), so a dropped, misplaced or mis-indexed term anywhere in
+    the step (row j vs j-1, the excluded token, the bonus row, the EOS stop, the length clamp)
+    fails it."""
+    TWO128 = 1 << 128
+    V, L, k, eos, M = 4, 5, 2, 3, 8
+    rows = _markov_setup(V, 12)
+    pool = [[0, 1, 2, 1, 0], [1, 2, 1, 2], [2, 2, 0, 1], [0, 0, 1, 2, 3], [1, 1, 1], [2, 0]]
+    dists = [orc.row_dist(r, T, top_p) for r in rows]
+    mass_of = [[int(x) for x in d.mass] for d in dists]
+
+    def r_inside(C, Z):  # the smallest r128 with floor(r * Z / 2^128) == C (C < Z)
+        return -(-C * TWO128 // Z)
+
+    def branches(draft, prevs):
+        pr = Fraction(1)
+        acc_r, smp_r = [0] * (k + 1), [0] * (k + 1)
+        q = len(draft)
+        for j in range(q + 1):
+            mass, Z = mass_of[prevs[j]], dists[prevs[j]].z
+            if j < q:
+                d = draft[j]
+                if mass[d] < Z:  # rejection at row j, then the residual sample (Eq. 3)
+                    Zx, C = Z - mass[d], 0
+                    for x in range(V):
+                        if x != d and mass[x]:
+                            ra, rs = list(acc_r), list(smp_r)
+                            ra[j], rs[j] = TWO128 - 1, r_inside(C, Zx)
+                            yield draft[:j] + [x], pr * Fraction(Z - mass[d], Z) * Fraction(mass[x], Zx), ra, rs
+                            C += mass[x]
+                if mass[d] == 0:
+                    return
+                pr *= Fraction(mass[d], Z)  # accepted (Eq. 2): U = 0 < mass(d)
+                if d == eos:
+                    yield draft[:j + 1], pr, list(acc_r), list(smp_r)
+                    return
+            else:  # bonus (or the plain sample when q = 0)
+                C = 0
+                for x in range(V):
+                    if mass[x]:
+                        rs = list(smp_r)
+                        rs[q] = r_inside(C, Z)
+                        yield draft + [x], pr * Fraction(mass[x], Z), list(acc_r), rs
+                        C += mass[x]
+
+    spec, steps_with_drafts = {}, [0]
+
+    def run(gen, pr):
+        if len(gen) == L or (gen and gen[-1] == eos):
+            spec[tuple(gen)] = spec.get(tuple(gen), Fraction(0)) + pr
+            return
+        ctx = [0] + gen
+        draft, _ = orc.lookup(pool, ctx, M, 1, k)
+        draft = draft[:max(0, min(len(draft), L - len(gen) - 1))]
+        steps_with_drafts[0] += bool(draft)
+        prevs = [ctx[-1]] + draft
+        for toks, p, ra, rs in branches(draft, prevs):
+            out = orc.verify_one_r([rows[x] for x in prevs], T, top_p, len(gen), L, eos, draft, k, ra, rs)
+            assert out.tokens == toks, (gen, draft, toks, out.tokens)
+            run(gen + toks, pr * p)
+
+    run([], Fraction(1))
+    ar = {}
+
+    def expand(prefix, prev, p):
+        if len(prefix) == L or (prefix and prefix[-1] == eos):
+            ar[tuple(prefix)] = p
+            return
+        for x in range(V):
+            if mass_of[prev][x]:
+                expand(prefix + [x], x, p * Fraction(mass_of[prev][x], dists[prev].z))
+
+    expand([], 0, Fraction(1))
+    assert steps_with_drafts[0] >= 2  # the pool drafted (on many branches at T > 0, top_p = 1)
+    assert sum(spec.values()) == 1
+    assert spec == ar  # total variation 0
+
+
 def test_empty_pool_is_plain_decoding(orc):
     """north_star (3) / S:252: with an empty pool every step is one plain sample drawn
     with counter (t, SAMPLE); under T = 0 this is the argmax chain (numpy argmax)."""
@@ -540,3 +681,44 @@ def test_lookup_invariants(orc):
             w = ctx[-(m + 1):]
             assert not any(seq[i:i + len(w)] == w and i + len(w) < len(seq)
                            for seq in pool for i in range(len(seq)))
+
+
+# ------------------------------------------------------------------ n-gram drafter (f4)
+def test_ngram_hand_examples(orc):
+    """Reading N1 ('a linear match of repeated token sequences ... the candidate with
+    the longest common prefix'): the longest suffix wins; among its occurrences the first in
+    pool order; the draft is cut at its sequence's end; a terminal-only match does not anchor;
+    n is bounded by n_max and n_min."""
+    pool = [[1, 2, 3, 4], [9, 1, 2, 5], [7, 7, 1, 2]]
+    assert orc.lookup_ngram(pool, [8, 1, 2], 1, 4, 3) == ([3, 4], 2)      # first occurrence
+    assert orc.lookup_ngram(pool, [9, 1, 2], 1, 4, 3) == ([5], 3)         # longest wins
+    assert orc.lookup_ngram(pool, [9, 1, 2], 1, 2, 3) == ([3, 4], 2)      # n_max caps n
+    assert orc.lookup_ngram(pool, [6, 4], 1, 4, 3) == ([], 0)             # 4 only ends a sequence
+    assert orc.lookup_ngram(pool, [7, 7], 1, 4, 5) == ([1, 2], 2)
+    assert orc.lookup_ngram(pool, [5, 7], 2, 4, 3) == ([], 0)             # n_min 2: no match
+    assert orc.lookup_ngram(pool, [5, 7], 1, 4, 3) == ([7, 1, 2], 1)      # K = 3 tokens
+    assert orc.lookup_ngram([], [1], 1, 4, 3) == ([], 0)
+
+
+def test_ngram_vs_backward_match_scan(orc):
+    """Independent route: for every pool position e (followed by a token) the backward match
+    length against the context, then the best (length desc, position asc); 300 random pools."""
+    rng = np.random.default_rng(17)
+    for _ in range(300):
+        vocab = int(rng.integers(2, 6))
+        pool = [list(rng.integers(0, vocab, int(rng.integers(0, 12)))) for _ in range(int(rng.integers(0, 5)))]
+        ctx = list(rng.integers(0, vocab, int(rng.integers(1, 10))))
+        n_min, n_max, K = int(rng.integers(1, 3)), int(rng.integers(3, 8)), int(rng.integers(1, 6))
+        best = (0, 0, None)
+        flat = [(s, i) for s, seq in enumerate(pool) for i in range(len(seq))]
+        for pos, (s, e) in enumerate(flat):
+            seq = pool[s]
+            if e + 1 >= len(seq):
+                continue
+            n = 0
+            while n < min(n_max, len(ctx)) and e - n >= 0 and seq[e - n] == ctx[-1 - n]:
+                n += 1
+            if n >= n_min and n > best[0]:
+                best = (n, pos, seq[e + 1:e + 1 + K])
+        want = (best[2], best[0]) if best[2] is not None else ([], 0)
+        assert orc.lookup_ngram(pool, ctx, n_min, n_max, K) == ([int(x) for x in want[0]], want[1])
