@@ -79,6 +79,9 @@ typedef struct {
 typedef struct {
     float temperature; /* T >= 0; T == 0 is greedy (argmax, lowest id)          */
     float top_p;       /* (0, 1]; nucleus over integer masses (reading R5)     */
+    int32_t top_k;     /* >= 0; 0 = off.  Keep the top_k heaviest masses, tie-closed  */
+                       /* (reading R5k, "any top-p/top-k filtering"), applied   */
+                       /* before top-p.  Ignored when T == 0 (greedy).     */
 } bs_sampling;
 
 /* ---------------------------------------------------------------- lifetime */
@@ -181,6 +184,20 @@ bs_status bs_draft_lookup(bs_ctx* ctx, uint64_t rl_step, int32_t n, const int32_
                           int32_t k, int32_t* draft_tokens, int32_t* draft_len,
                           int32_t* match_len, void* stream);
 
+/* Draft-source variant: the n-gram linear-scan drafter ("pattern
+ * matching directly over raw token sequences", "a linear match of repeated token
+ * sequences to return the candidate with the longest common prefix"; the paper's Table 7
+ * ablation).  Reading N1: anchor on the longest suffix y[-n:] of the rollout's
+ * context, n in [n_min, min(n_max, |y|)], that occurs in its prompt's sealed pool followed by a
+ * token; the first such occurrence in pool order (sequence index, then position) gives the
+ * draft: the up to k tokens after it in its sequence.  No index is used: the cost is linear in
+ * the prompt's pool (one CTA per rollout).  Outputs as bs_draft_lookup (match_len = n, 0 if none;
+ * draft_len clamped to max_len - pos - 1, 0 if finished).  Errors: BS_ERR_STALE as
+ * bs_draft_lookup; BS_ERR_INVALID unless 1 <= n_min <= n_max <= match_max and 0 <= k <= k_max. */
+bs_status bs_draft_lookup_ngram(bs_ctx* ctx, uint64_t rl_step, int32_t n, const int32_t* slots,
+                                int32_t k, int32_t n_min, int32_t n_max, int32_t* draft_tokens,
+                                int32_t* draft_len, int32_t* match_len, void* stream);
+
 /* Lossless verification of one draft block per rollout (Eq. 2 P:203-205,
  * Eq. 3, Alg. 1, bonus P:308).  Pure: reads rollout state,
  * writes only its outputs.
@@ -246,11 +263,11 @@ bs_status bs_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t*
 /* ---------------------------------------------------------------- tuning */
 /* Select the kernel bs_verify_step uses for rows without top-p (all compute identical
  * results): 0 auto (= 3 when ceil(V/8) <= 53248, else 1; env BS_VERIFY_KERNEL
- * overrides auto), 1 one CTA per row (rows streamed twice through a TMA ring), 2 each row
- * split over an 8-CTA cluster (one row at a time), 3 pipelined 8-CTA cluster (row slices
- * resident in shared memory, max and mass passes overlapped across rows).  Takes effect for
- * calls enqueued (or graphs captured) after it.  Errors: BS_ERR_INVALID on a NULL ctx or an
- * unknown kind. */
+ * overrides auto), 1 one CTA per row (rows streamed twice through a TMA ring), 3 pipelined
+ * 8-CTA cluster (row slices resident in shared memory, max and mass passes overlapped across
+ * rows).  Takes effect for calls enqueued (or graphs captured) after it.  Errors:
+ * BS_ERR_INVALID on a NULL ctx or an unknown kind (2, the former unpipelined split kernel, is
+ * no longer accepted). */
 bs_status bsx_set_verify_kernel(bs_ctx* ctx, int32_t kind);
 
 /* Programmatic dependent launch (PDL) contract of the verify launches.  With on = 1 the
@@ -262,6 +279,12 @@ bs_status bsx_set_verify_kernel(bs_ctx* ctx, int32_t kind);
  * rows -> verify) keeps that contract.  Default 0: every read follows the wait.  Errors:
  * BS_ERR_INVALID on a NULL ctx or on not in {0, 1}. */
 bs_status bsx_set_early_plan(bs_ctx* ctx, int32_t on);
+
+/* Cap the cluster verify kernel's grid at max_clusters 8-CTA clusters (0 = every cluster that
+ * can be resident, the default).  Lets several contexts (e.g. rollout groups on separate
+ * streams) run their verify launches concurrently on one GPU.  Takes effect for calls enqueued
+ * (or graphs captured) after it.  Errors: BS_ERR_INVALID on a NULL ctx or max_clusters < 0. */
+bs_status bsx_set_max_clusters(bs_ctx* ctx, int32_t max_clusters);
 
 /* Diagnostics (host memory out[n]): 0 resident clusters of the cluster verify kernel (0 until
  * its first launch), 1 cooperative launch in use (-1 untested, 0 no, 1 yes), 2 SM count,

@@ -27,7 +27,7 @@ class bs_config(C.Structure):
 
 
 class bs_sampling(C.Structure):
-    _fields_ = [("temperature", C.c_float), ("top_p", C.c_float)]
+    _fields_ = [("temperature", C.c_float), ("top_p", C.c_float), ("top_k", C.c_int32)]
 
 
 _V = C.c_void_p
@@ -52,6 +52,7 @@ SIGNATURES = {
     "bs_draft_lookup": (C.c_int, [_V, _U64, _I32, _V, _I32, _V, _V, _V, _V]),
     "bs_verify_step": (C.c_int, [_V, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V, _V,
                                  _V, _V, _V, _V]),
+    "bs_draft_lookup_ngram": (C.c_int, [_V, _U64, _I32, _V, _I32, _I32, _I32, _V, _V, _V, _V]),
     "bs_verify_commit": (C.c_int, [_V, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V, _V,
                                    _V, _V, _V, _V, _V]),
     "bs_verify_commit_lookup": (C.c_int, [_V, _U64, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V,
@@ -61,6 +62,7 @@ SIGNATURES = {
     "bs_rollout_bind_output": (C.c_int, [_V, _V, _I64]),
     "bsx_set_verify_kernel": (C.c_int, [_V, _I32]),
     "bsx_set_early_plan": (C.c_int, [_V, _I32]),
+    "bsx_set_max_clusters": (C.c_int, [_V, _I32]),
     "bsx_launch_info": (C.c_int, [_V, C.POINTER(C.c_int64), _I32]),
     "bsx_synth_bank": (C.c_int, [_V, _I64, _I32, _U32, C.c_float, _V]),
     "bsx_target_rows": (C.c_int, [_V, _I32, _V, _V, _V, _I32, _U32, _I32, _I64, _V, _V]),

@@ -108,10 +108,16 @@ class Context:
                                           _p(draft_tokens), _p(draft_len), _p(match_len),
                                           _stream(stream, self.device)), "bs_draft_lookup")
 
+    def bs_draft_lookup_ngram(self, rl_step, slots, k, n_min, n_max, draft_tokens, draft_len,
+                              match_len=None, stream=None):
+        _chk(self, load().bs_draft_lookup_ngram(self.handle, rl_step, slots.numel(), _p(slots), k, n_min,
+                                                n_max, _p(draft_tokens), _p(draft_len), _p(match_len),
+                                                _stream(stream, self.device)), "bs_draft_lookup_ngram")
+
     def bs_verify_step(self, slots, logits, row_index, row_stride, draft_tokens, draft_len, k,
                        temperature, top_p, out_tokens, out_len, out_accepted, out_norm=None,
-                       out_z=None, stream=None):
-        sp = bs_sampling(temperature, top_p)
+                       out_z=None, stream=None, top_k=0):
+        sp = bs_sampling(temperature, top_p, top_k)
         _chk(self, load().bs_verify_step(self.handle, slots.numel(), _p(slots), _p(logits),
                                          _p(row_index), row_stride, _p(draft_tokens),
                                          _p(draft_len), k, sp, _p(out_tokens), _p(out_len),
@@ -120,8 +126,8 @@ class Context:
 
     def bs_verify_commit(self, slots, logits, row_index, row_stride, draft_tokens, draft_len, k,
                          temperature, top_p, out_tokens, out_len, out_accepted, finished=None,
-                         out_norm=None, out_z=None, stream=None):
-        sp = bs_sampling(temperature, top_p)
+                         out_norm=None, out_z=None, stream=None, top_k=0):
+        sp = bs_sampling(temperature, top_p, top_k)
         _chk(self, load().bs_verify_commit(self.handle, slots.numel(), _p(slots), _p(logits),
                                            _p(row_index), row_stride, _p(draft_tokens),
                                            _p(draft_len), k, sp, _p(out_tokens), _p(out_len),
@@ -130,10 +136,11 @@ class Context:
 
     def bs_verify_commit_lookup(self, rl_step, slots, logits, row_index, row_stride, draft_tokens,
                                 draft_len, k, temperature, top_p, out_tokens, out_len, out_accepted,
-                                finished=None, match_len=None, out_norm=None, out_z=None, stream=None):
+                                finished=None, match_len=None, out_norm=None, out_z=None, stream=None,
+                                top_k=0):
         """bs_verify_commit, then this step's commit feeds the next step's draft lookup in the
         same launch: draft_tokens / draft_len are overwritten with the next step's drafts."""
-        sp = bs_sampling(temperature, top_p)
+        sp = bs_sampling(temperature, top_p, top_k)
         _chk(self, load().bs_verify_commit_lookup(self.handle, rl_step, slots.numel(), _p(slots), _p(logits),
                                                   _p(row_index), row_stride, _p(draft_tokens),
                                                   _p(draft_len), k, sp, _p(out_tokens), _p(out_len),
@@ -159,7 +166,7 @@ class Context:
                                                  stride if responses is not None else 0),
              "bs_rollout_bind_output")
 
-    VERIFY_KERNELS = {"auto": 0, "rows": 1, "split": 2, "cluster": 3}
+    VERIFY_KERNELS = {"auto": 0, "rows": 1, "cluster": 3}
 
     def bsx_set_verify_kernel(self, kind):
         kind = self.VERIFY_KERNELS[kind] if isinstance(kind, str) else int(kind)
@@ -173,6 +180,9 @@ class Context:
 
     def bsx_set_early_plan(self, on: bool):
         _chk(self, load().bsx_set_early_plan(self.handle, int(bool(on))), "bsx_set_early_plan")
+
+    def bsx_set_max_clusters(self, max_clusters: int):
+        _chk(self, load().bsx_set_max_clusters(self.handle, int(max_clusters)), "bsx_set_max_clusters")
 
     def bsx_target_rows(self, slots, draft_tokens, draft_len, k, target_seed, mode, nbank,
                         row_index, stream=None):

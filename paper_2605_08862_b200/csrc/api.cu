@@ -40,7 +40,7 @@ static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 extern "C" {
 
 bs_status bsx_set_verify_kernel(bs_ctx* c, int32_t kind) {
-    if (!c || kind < 0 || kind > 3) return BS_ERR_INVALID;
+    if (!c || kind < 0 || kind > 3 || kind == 2) return BS_ERR_INVALID;
     c->verify_kind = kind;
     return BS_OK;
 }
@@ -48,6 +48,12 @@ bs_status bsx_set_verify_kernel(bs_ctx* c, int32_t kind) {
 bs_status bsx_set_early_plan(bs_ctx* c, int32_t on) {
     if (!c || on < 0 || on > 1) return BS_ERR_INVALID;
     c->early_plan = on;
+    return BS_OK;
+}
+
+bs_status bsx_set_max_clusters(bs_ctx* c, int32_t max_clusters) {
+    if (!c || max_clusters < 0) return BS_ERR_INVALID;
+    c->max_clusters = max_clusters;
     return BS_OK;
 }
 
@@ -300,6 +306,33 @@ bs_status bs_draft_lookup(bs_ctx* c, uint64_t rl_step, int32_t n, const int32_t*
     return BS_OK;
 }
 
+bs_status bs_draft_lookup_ngram(bs_ctx* c, uint64_t rl_step, int32_t n, const int32_t* slots, int32_t k,
+                                int32_t n_min, int32_t n_max, int32_t* draft_tokens, int32_t* draft_len,
+                                int32_t* match_len, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (!c->sealed.valid || c->sealed.step != rl_step)
+        return fail(c, BS_ERR_STALE, "index not sealed for rl_step %llu", (unsigned long long)rl_step);
+    if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
+    if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
+    if (n_min < 1 || n_max < n_min || n_max > c->M)
+        return fail(c, BS_ERR_INVALID, "need 1 <= n_min <= n_max <= match_max");
+    if (n && (!slots || !draft_len || (k && !draft_tokens))) return fail(c, BS_ERR_INVALID, "null array");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_lookup_ngram(c, n, slots, k, n_min, n_max, draft_tokens, draft_len, match_len, S(stream)),
+       "bs_draft_lookup_ngram");
+    return BS_OK;
+}
+
+// Host-side check of bs_sampling (returns the reason, or nullptr if valid).
+static const char* sampling_invalid(const bs_sampling& sp) {
+    if (!(sp.temperature >= 0.f) || sp.temperature == INFINITY) return "temperature must be finite and >= 0";
+    if (!(sp.top_p > 0.f && sp.top_p <= 1.f)) return "top_p must be in (0, 1]";
+    if (sp.top_k < 0) return "top_k must be >= 0";
+    if (sp.temperature > 0.f && !((float)(1.4426950408889634 / (double)sp.temperature) < INFINITY))
+        return "temperature too small";
+    return nullptr;
+}
+
 bs_status bs_verify_step(bs_ctx* c, int32_t n, const int32_t* slots, const void* logits,
                          const int64_t* row_index, int64_t stride, const int32_t* draft_tokens,
                          const int32_t* draft_len, int32_t k, bs_sampling sp,
@@ -309,17 +342,13 @@ bs_status bs_verify_step(bs_ctx* c, int32_t n, const int32_t* slots, const void*
     if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
     if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
     if (stride < c->cfg.vocab) return fail(c, BS_ERR_INVALID, "row stride < vocab");
-    if (!(sp.temperature >= 0.f) || sp.temperature == INFINITY)
-        return fail(c, BS_ERR_INVALID, "temperature must be finite and >= 0");
-    if (!(sp.top_p > 0.f && sp.top_p <= 1.f)) return fail(c, BS_ERR_INVALID, "top_p must be in (0, 1]");
-    if (sp.temperature > 0.f && !((float)(1.4426950408889634 / (double)sp.temperature) < INFINITY))
-        return fail(c, BS_ERR_INVALID, "temperature too small");
+    if (const char* why = sampling_invalid(sp)) return fail(c, BS_ERR_INVALID, "%s", why);
     if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
               (k && !draft_tokens)))
         return fail(c, BS_ERR_INVALID, "null array");
     CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
     CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
-                        sp.temperature, sp.top_p, out_tokens, out_len, out_accepted, out_norm,
+                        sp.temperature, sp.top_p, sp.top_k, out_tokens, out_len, out_accepted, out_norm,
                         reinterpret_cast<unsigned long long*>(out_z), S(stream)),
        "bs_verify_step");
     return BS_OK;
@@ -334,18 +363,14 @@ bs_status bs_verify_commit(bs_ctx* c, int32_t n, const int32_t* slots, const voi
     if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
     if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
     if (stride < c->cfg.vocab) return fail(c, BS_ERR_INVALID, "row stride < vocab");
-    if (!(sp.temperature >= 0.f) || sp.temperature == INFINITY)
-        return fail(c, BS_ERR_INVALID, "temperature must be finite and >= 0");
-    if (!(sp.top_p > 0.f && sp.top_p <= 1.f)) return fail(c, BS_ERR_INVALID, "top_p must be in (0, 1]");
-    if (sp.temperature > 0.f && !((float)(1.4426950408889634 / (double)sp.temperature) < INFINITY))
-        return fail(c, BS_ERR_INVALID, "temperature too small");
+    if (const char* why = sampling_invalid(sp)) return fail(c, BS_ERR_INVALID, "%s", why);
     if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
               (k && !draft_tokens)))
         return fail(c, BS_ERR_INVALID, "null array");
     CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
     bool fused = false;
     CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
-                        sp.temperature, sp.top_p, out_tokens, out_len, out_accepted, out_norm,
+                        sp.temperature, sp.top_p, sp.top_k, out_tokens, out_len, out_accepted, out_norm,
                         reinterpret_cast<unsigned long long*>(out_z), S(stream), finished, &fused),
        "bs_verify_commit");
     if (!fused)  // kernels without the fused commit: the commit kernel follows
@@ -365,11 +390,7 @@ bs_status bs_verify_commit_lookup(bs_ctx* c, uint64_t rl_step, int32_t n, const 
     if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
     if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
     if (stride < c->cfg.vocab) return fail(c, BS_ERR_INVALID, "row stride < vocab");
-    if (!(sp.temperature >= 0.f) || sp.temperature == INFINITY)
-        return fail(c, BS_ERR_INVALID, "temperature must be finite and >= 0");
-    if (!(sp.top_p > 0.f && sp.top_p <= 1.f)) return fail(c, BS_ERR_INVALID, "top_p must be in (0, 1]");
-    if (sp.temperature > 0.f && !((float)(1.4426950408889634 / (double)sp.temperature) < INFINITY))
-        return fail(c, BS_ERR_INVALID, "temperature too small");
+    if (const char* why = sampling_invalid(sp)) return fail(c, BS_ERR_INVALID, "%s", why);
     if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
               (k && !draft_tokens)))
         return fail(c, BS_ERR_INVALID, "null array");
@@ -377,7 +398,7 @@ bs_status bs_verify_commit_lookup(bs_ctx* c, uint64_t rl_step, int32_t n, const 
     bool fused = false, looked = false;
     const LookupArgs lk = lookup_args(c, n, slots, k, draft_tokens, draft_len, match_len);
     CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
-                        sp.temperature, sp.top_p, out_tokens, out_len, out_accepted, out_norm,
+                        sp.temperature, sp.top_p, sp.top_k, out_tokens, out_len, out_accepted, out_norm,
                         reinterpret_cast<unsigned long long*>(out_z), S(stream), finished, &fused, &lk,
                         &looked),
        "bs_verify_commit_lookup");

@@ -95,6 +95,10 @@ struct IndexDesc {
     const int32_t* T;
     const int32_t* seq_start_of;
     unsigned long long step;  // the rl_step this index was sealed for (~0: none / failed seal)
+    // the sealed pool as the n-gram drafter scans it (bs_draft_lookup_ngram)
+    const int64_t* seq_off;     // [n_seqs + 1] offsets into T
+    const int32_t* seq_prompt;  // [n_seqs]
+    int32_t n_seqs;
 };
 
 struct Pool {
@@ -117,6 +121,7 @@ struct bs_ctx {
     int num_sms = 148;
     int verify_kind = 0;  // bsx_set_verify_kernel (0: auto)
     int early_plan = 0;   // bsx_set_early_plan: the verify launch may plan before its PDL wait
+    int max_clusters = 0; // bsx_set_max_clusters: cap on the cluster verify grid (0: all resident)
     // per-context (hence per-device) kernel launch setup, done once on this ctx's device:
     // dynamic shared memory attributes set, and the cluster kernel's resident cluster count
     size_t kcfg_cluster_smem = 0, kcfg_split_smem = 0;
@@ -169,7 +174,7 @@ LookupArgs lookup_args(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k, 
 // also looked up the next step's drafts described by `lookup` (bs_verify_commit_lookup)
 cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits,
                           const int64_t* row_index, int64_t stride, const int32_t* draft,
-                          const int32_t* draft_len, int32_t k, float T, float top_p,
+                          const int32_t* draft_len, int32_t k, float T, float top_p, int32_t top_k,
                           int32_t* out_tokens, int32_t* out_len, int32_t* out_acc,
                           float* out_norm, unsigned long long* out_z, cudaStream_t st,
                           int32_t* commit_finished = nullptr, bool* committed = nullptr,
@@ -177,6 +182,9 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
 cudaError_t launch_lookup(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k,
                           int32_t* draft, int32_t* draft_len, int32_t* match_len,
                           cudaStream_t st);
+cudaError_t launch_lookup_ngram(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t k, int32_t n_min,
+                                int32_t n_max, int32_t* draft, int32_t* draft_len, int32_t* match_len,
+                                cudaStream_t st);
 cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why);
 // device word cur_step <- step (the latest put / exchange / seal; staleness)
 cudaError_t set_cur_step(bs_ctx* ctx, uint64_t step, cudaStream_t st);

@@ -229,6 +229,9 @@ static cudaError_t publish_index(bs_ctx* ctx, cudaStream_t st, unsigned long lon
     d.mask = ctx->table_mask;
     d.T = ctx->sealed.tokens.p;
     d.seq_start_of = ctx->seq_start_of.p;
+    d.seq_off = ctx->sealed.seq_off.p;
+    d.seq_prompt = ctx->sealed.seq_prompt.p;
+    d.n_seqs = ctx->sealed.n_seqs;
     return cudaMemcpyAsync(ctx->idx_desc.p, &d, sizeof d, cudaMemcpyHostToDevice, st);  // pageable: staged now
 }
 

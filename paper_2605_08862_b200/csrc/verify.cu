@@ -563,7 +563,6 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
     uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw);
     VShared& sh = *reinterpret_cast<VShared*>(smem_raw + (size_t)NSTAGE * CHE * 2);
     pdl_wait();  // dependents launch at exit (the cluster kernel plans before its wait)
-    if (a.ctl[VCTL_MODE] != 0) return;  // few rows: the split (cluster) kernel runs instead
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rows = (int)a.ctl[VCTL_ROWS];
 
@@ -818,7 +817,6 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) verify_rows_kernel(const Ve
 }
 
 #include "verify_cluster.cuh"
-#include "verify_split.cuh"
 #include "verify_topp.cuh"
 
 // ---- plan: clamp q per rollout, reset per-rollout state, and lay out the step's rows as a
@@ -914,10 +912,8 @@ __global__ void __launch_bounds__(PLAN_NT) verify_plan_kernel(
     }
 }
 
-// Slice of a row per cluster CTA: ceil(V / 8) rounded up to whole 256-element tiles.
-static int split_slice(int V) { return ((V + SP_CL - 1) / SP_CL + 255) / 256 * 256; }
 // Which kernel verifies rows (bsx_set_verify_kernel; env BS_VERIFY_KERNEL for tools).
-enum { VK_AUTO = 0, VK_ROWS = 1, VK_SPLIT = 2, VK_CLUSTER = 3 };
+enum { VK_AUTO = 0, VK_ROWS = 1, VK_CLUSTER = 3 };  // (2: the unpipelined split kernel, removed)
 static int verify_kind(const bs_ctx* ctx, int V) {
     int k = ctx->verify_kind;
     if (k == VK_AUTO) k = ctx->env_kind;
@@ -932,7 +928,7 @@ static int ntile_ok(int V) { return (V + 255) / 256 <= TP_MAXT ? 1 : 0; }
 
 cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits,
                           const int64_t* row_index, int64_t stride, const int32_t* draft,
-                          const int32_t* draft_len, int32_t k, float T, float top_p,
+                          const int32_t* draft_len, int32_t k, float T, float top_p, int32_t top_k,
                           int32_t* out_tokens, int32_t* out_len, int32_t* out_acc,
                           float* out_norm, unsigned long long* out_z, cudaStream_t st,
                           int32_t* commit_finished, bool* committed, const LookupArgs* lookup,
@@ -941,9 +937,9 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     if (looked_up) *looked_up = false;
     if (n == 0) return cudaSuccess;
     const int V = ctx->cfg.vocab;
-    const bool topp = T > 0.f && top_p < 1.f;
+    if (top_k >= V) top_k = 0;  // keeps every token
+    const bool topp = T > 0.f && (top_p < 1.f || top_k > 0);  // filtered rows (R5k, R5)
     const int kind = topp ? VK_ROWS : verify_kind(ctx, V);
-    const int plan_mode = (kind == VK_SPLIT) ? 1 : 0;
     cudaError_t e = cudaSuccess;
     // the cluster kernel plans in-kernel (each rollout's row-0 claimer); the others take the
     // plan kernel's j-major row table
@@ -953,8 +949,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
         (const int32_t*)ctx->finished.p, (const unsigned long long*)ctx->uid.p,
         static_cast<const uint16_t*>(logits), row_index, stride, ctx->rb_q.p,
         reinterpret_cast<RowDesc*>(ctx->vqueue.p), ctx->vctl.p, ctx->vroll_first.p,
-        ctx->vroll_state.p, out_len, out_acc, out_tokens, out_norm, out_z, ctx->dev_err.p,
-        plan_mode);
+        ctx->vroll_state.p, out_len, out_acc, out_tokens, out_norm, out_z, ctx->dev_err.p, 0);
     if (e != cudaSuccess) return e;
     VerifyArgs a = {};
     a.slots = slots;
@@ -969,7 +964,6 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     a.nchunk = (V + CHE - 1) / CHE;
     a.ngroup = (a.nchunk + 1) / 2;
     if (a.ngroup > MAXG) return cudaErrorInvalidValue;
-    if (kind == VK_SPLIT && split_slice(V) / 256 > SP_MAXT) return cudaErrorInvalidValue;
     a.T = T;
     a.c = (T > 0.f) ? (float)(1.4426950408889634 / (double)T) : 0.f;
     a.seed = ctx->cfg.seed;
@@ -1020,7 +1014,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             }
         }
     }
-    if (topp) {  // R5: top-p filtered rows (verify_topp.cuh)
+    if (topp) {  // R5k / R5: top-k / top-p filtered rows (verify_topp.cuh)
         if (ntile_ok(V) == 0) return cudaErrorInvalidValue;
         const size_t tsm = sizeof(TopPShared);
         if (!ctx->kcfg_topp) {
@@ -1030,7 +1024,7 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             ctx->kcfg_topp = 1;
         }
         const int tgrid = std::max(1, std::min(ctx->num_sms * 2, n * (k + 1)));
-        return launch_pdl(verify_topp_kernel, dim3(tgrid), dim3(TP_NT), tsm, st, a, top_p);
+        return launch_pdl(verify_topp_kernel, dim3(tgrid), dim3(TP_NT), tsm, st, a, top_p, top_k);
     }
     if (kind == VK_CLUSTER) {
         const int SL = cluster_slice(V);
@@ -1053,8 +1047,10 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             ctx->kcfg_clusters = std::max(1, ncl);
             ctx->kcfg_cluster_smem = csm;
         }
-        a.ncl = ctx->kcfg_clusters;
-        const dim3 grid(ctx->kcfg_clusters * CK_CL);
+        const int ncl_use = ctx->max_clusters > 0 ? std::min(ctx->max_clusters, ctx->kcfg_clusters)
+                                                  : ctx->kcfg_clusters;
+        a.ncl = ncl_use;
+        const dim3 grid(ncl_use * CK_CL);
         if (ctx->kcfg_coop < 0) {  // probe once, outside stream capture (a failed launch would end it)
             cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
             cudaStreamIsCapturing(st, &cs);
@@ -1069,18 +1065,6 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             }
         }
         return launch_pdl_ex(ctx->kcfg_coop == 1, verify_cluster_kernel, grid, dim3(CK_NT), csm, st, a, SL);
-    }
-    if (kind == VK_SPLIT) {
-        const int SL = split_slice(V);
-        const size_t ssm = ((sizeof(SplitShared) + 127) & ~size_t(127)) + (size_t)SL * 2;
-        if (ctx->kcfg_split_smem < ssm) {
-            e = cudaFuncSetAttribute(verify_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)ssm);
-            if (e != cudaSuccess) return e;
-            ctx->kcfg_split_smem = ssm;
-        }
-        const int nclus = std::max(1, (ctx->num_sms * 2) / SP_CL);
-        return launch_pdl(verify_split_kernel, dim3(nclus * SP_CL), dim3(SP_NT), ssm, st, a, SL);
     }
     const size_t smem = (size_t)NSTAGE * CHE * 2 + sizeof(VShared);
     if (!ctx->kcfg_rows) {

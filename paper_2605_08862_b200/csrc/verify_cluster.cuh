@@ -383,7 +383,7 @@ __device__ __forceinline__ void ck_preissue(const VerifyArgs& a, uint32_t epoch,
 }
 
 __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool queues, int rot,
-                            ClaimState& cs, volatile int* mail) {
+                            ClaimState& cs, int* mail) {
     const int n = a.n;
     uint64_t t_spin0 = 0;
     RowDesc out;
@@ -415,10 +415,7 @@ __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch,
         //    the chain stays here (no scan)
         if (!eager) {
             int mb = -1;
-            if (lane == 0) {
-                mb = *mail;
-                if (mb >= 0) *mail = -1;
-            }
+            if (lane == 0) mb = atomicExch(mail, -1);  // read and clear in one shared atomic
             mb = __shfl_sync(0xFFFFFFFFu, mb, 0);
             if (mb >= 0) {
                 if (ck_take(a, epoch, mb >> 8, SRC_READY, lane, mb & 0xFF, out)) {
@@ -643,7 +640,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             ClaimState cst;
             for (int r = 0;;) {
                 int issued = 0;
-                if (lane == 0) issued = *reinterpret_cast<volatile int*>(&sh.tma_issued);
+                if (lane == 0) issued = atomicOr(&sh.tma_issued, 0);  // (an atomic: no shared-memory race)
                 issued = __shfl_sync(0xFFFFFFFFu, issued, 0);
                 if (r > issued + CK_LA) {  // far enough ahead
                     __nanosleep(128);
@@ -700,7 +697,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 } else {
                     mbar_arrive(&sh.full[bi]);
                 }
-                if (rank == 0) *reinterpret_cast<volatile int*>(&sh.tma_issued) = i + 1;
+                if (rank == 0) atomicExch(&sh.tma_issued, i + 1);
             }
         }
     } else if (warp == CK_EPI) {
@@ -868,7 +865,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 int no = 0;
                 int32_t ot = -1;
                 const bool fz = complete_row_warp(a, sh.stat, b, j, q, c_status, c_cand, c_z, c_norm, lane, no, ot);
-                if (lane == 0 && c_status == ST_CONT) *reinterpret_cast<volatile int*>(&sh.mail) = (b << 8) | (j + 1);
+                if (lane == 0 && c_status == ST_CONT) atomicExch(&sh.mail, (b << 8) | (j + 1));
                 if (a.commit && fz) commit_rollout_warp(a, b, lane, cp, no, ot);
             }
             __syncwarp();

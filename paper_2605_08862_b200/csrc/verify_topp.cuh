@@ -1,5 +1,14 @@
-// verify_topp.cuh — verify + resample under top-p filtering (reading R5, DESIGN.md §3/§5),
-// included by verify.cu (shares its row queue, descriptors and completion protocol).
+// verify_topp.cuh — verify + resample under top-k / top-p filtering (readings R5k, R5,
+// DESIGN.md §2/§4), included by verify.cu (shares its row queue, descriptors and completion
+// protocol).
+//
+// Top-k (R5k, applied first) keeps {i : mass_i >= tau_k}, tau_k the top_k-th largest
+// mass: mass is nondecreasing in the logit, so tau_k = mass(kappa), kappa the top_k-th largest
+// 16-bit order key among the positive-mass tokens, found by a COUNT-weighted select over the
+// same coarse bins (pass 2 also counts tokens per bin; pass 3k counts the 16 keys of the
+// crossing bin); the kept sum Z_k comes from one filtered tile pass.  Top-p then runs on the
+// top-k masses (Theta from Z_k); its crossing key lies among keys with mass >= tau_k because
+// Theta <= Z_k, so the unfiltered mass histograms still locate it.
 //
 // The tie-closed nucleus keeps {i : mass_i >= tau}, tau = max{t : F(t) >= Theta},
 // F(t) = sum of the masses >= t.  mass is a nondecreasing function of the bf16 logit, so
@@ -22,6 +31,8 @@ constexpr int TP_MAXT = 2048;         // 256-element tiles: V <= 524288
 
 struct TopPShared {
     unsigned long long h1[TP_H1];
+    uint32_t hc[TP_H1];       // top-k: positive-mass tokens per coarse bin
+    uint32_t h2c[16];         // top-k: positive-mass tokens per key of the crossing bin
     unsigned long long tsum[TP_MAXT];
     unsigned long long h2[16];
     unsigned long long stat[STAT_COUNT];
@@ -30,6 +41,7 @@ struct TopPShared {
     RowDesc dsc;
     unsigned long long bz[3];  // [0] Theta remaining inside the coarse bin, [1] sum above it, [2] Z
     int32_t bsel;              // coarse bin B
+    int32_t bselk, needk;      // top-k: coarse bin of kappa, tokens still needed inside it
 };
 
 // Order-preserving map of bf16 bit patterns to 16-bit keys (larger value -> larger key).
@@ -54,7 +66,7 @@ __device__ __forceinline__ void tp_unpack(const uint4 v, uint32_t b[8]) {
     b[4] = v.z & 0xFFFFu; b[5] = v.z >> 16; b[6] = v.w & 0xFFFFu; b[7] = v.w >> 16;
 }
 
-__global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs a, float top_p) {
+__global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs a, float top_p, int top_k) {
     extern __shared__ __align__(16) uint8_t tp_smem[];
     TopPShared& sh = *reinterpret_cast<TopPShared*>(tp_smem);
     pdl_wait();  // dependents launch at exit (the cluster kernel plans before its wait)
@@ -63,6 +75,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
     const int V = a.V;
     const int ntile = (V + 255) / 256;
     const uint64_t P = (uint64_t)llround((double)top_p * 4294967296.0);  // R5 (top_p < 1)
+    const bool use_p = top_p < 1.f, use_k = top_k > 0;
     for (int i = tid; i < STAT_COUNT; i += TP_NT) sh.stat[i] = 0ull;
 
     for (;;) {
@@ -96,7 +109,12 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
             }
         }
         for (int i = tid; i < TP_H1; i += TP_NT) sh.h1[i] = 0ull;
-        if (tid < 16) sh.h2[tid] = 0ull;
+        if (use_k)
+            for (int i = tid; i < TP_H1; i += TP_NT) sh.hc[i] = 0u;
+        if (tid < 16) {
+            sh.h2[tid] = 0ull;
+            sh.h2c[tid] = 0u;
+        }
         __syncthreads();
         float m = -INFINITY;
         uint32_t bb = 0;
@@ -136,66 +154,154 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 s += mm[i];
-                if (mm[i]) atomicAdd(&sh.h1[tp_key(bits[i]) >> 4], (unsigned long long)mm[i]);
+                if (mm[i]) {
+                    const uint32_t kb = tp_key(bits[i]) >> 4;
+                    if (use_p) atomicAdd(&sh.h1[kb], (unsigned long long)mm[i]);
+                    if (use_k) atomicAdd(&sh.hc[kb], 1u);
+                }
             }
             const uint64_t ws = warp_sum_u51(s);
             if (lane == 0) sh.tsum[t] = ws;
         }
         __syncthreads();
-        // Z and the coarse select (warp 0): lane l owns bins [l*128, l*128+128)
-        if (warp == 0) {
+        // pass 4: filtered tile sums (masses >= t); tiles_tau = the t sh.tsum reflects
+        uint64_t tiles_tau = 0;  // pass 2's sums keep every mass
+        auto filtered_tiles = [&](uint64_t t) {
+            __syncthreads();  // earlier readers of sh.tsum are done
+            for (int tt = warp; tt < ntile; tt += TP_NW) {
+                const uint4 v = tp_load8(row, tt * 256 + lane * 8, V, aligned);
+                uint64_t mm[8];
+                mass_pair(v.x, mp, mm[0], mm[1]);
+                mass_pair(v.y, mp, mm[2], mm[3]);
+                mass_pair(v.z, mp, mm[4], mm[5]);
+                mass_pair(v.w, mp, mm[6], mm[7]);
+                uint64_t s = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s += (mm[i] >= t) ? mm[i] : 0ull;
+                const uint64_t ws = warp_sum_u51(s);
+                if (lane == 0) sh.tsum[tt] = ws;
+            }
+            __syncthreads();
+            tiles_tau = t;
+        };
+        auto tiles_total = [&]() {  // every thread: the sum of sh.tsum
             uint64_t zl = 0;
             for (int t = lane; t < ntile; t += 32) zl += sh.tsum[t];
-            const uint64_t Z = warp_sum_u64(zl);
-            unsigned __int128 th = (unsigned __int128)P * Z + (((unsigned __int128)1 << 32) - 1);
-            uint64_t theta = (uint64_t)(th >> 32);
-            theta = theta ? theta : 1ull;  // top_p -> 0 keeps the heaviest level (as R5)
-            const int per = TP_H1 / 32;
-            const int lo = (31 - lane) * per;  // lane 0 owns the heaviest bins
-            uint64_t ls = 0;
-            for (int i = 0; i < per; ++i) ls += sh.h1[lo + i];
-            const uint64_t incl = warp_incl_scan_u64(ls, lane);  // mass of bins >= lane's lowest
-            const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= theta);
-            const int L = hit ? (__ffs(hit) - 1) : 31;
-            if (lane == L) {
-                uint64_t above = incl - ls;
-                int B = lo;
-                for (int i = per - 1; i >= 0; --i) {
-                    const uint64_t h = sh.h1[lo + i];
-                    if (above + h >= theta) {
-                        B = lo + i;
+            return warp_sum_u64(zl);
+        };
+        const uint64_t Z = tiles_total();  // R4: the unfiltered normaliser
+        // ---------------------------------------------------- top-k (R5k): tau_k, Z_k
+        uint64_t tau = 0, Zk = Z;
+        if (use_k) {
+            if (warp == 0) {  // count select over the coarse bins, heaviest first
+                const int per = TP_H1 / 32;
+                const int lo = (31 - lane) * per;
+                uint32_t ls = 0;
+                for (int i = 0; i < per; ++i) ls += sh.hc[lo + i];
+                uint32_t incl = ls;
+#pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, dd);
+                    if (lane >= dd) incl += o;
+                }
+                const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= (uint32_t)top_k);
+                if (lane == 0 && !hit) sh.bselk = -1;  // fewer than top_k positive masses: keep all
+                const int L = hit ? (__ffs(hit) - 1) : 32;
+                if (lane == L) {
+                    uint32_t above = incl - ls;
+                    int Bk = lo;
+                    for (int i = per - 1; i >= 0; --i) {
+                        const uint32_t h = sh.hc[lo + i];
+                        if (above + h >= (uint32_t)top_k) {
+                            Bk = lo + i;
+                            break;
+                        }
+                        above += h;
+                    }
+                    sh.bselk = Bk;
+                    sh.needk = top_k - (int)above;
+                }
+            }
+            __syncthreads();
+            const int Bk = sh.bselk;
+            if (Bk >= 0) {
+                // pass 3k: counts of the 16 keys inside bin Bk
+                for (int t = warp; t < ntile; t += TP_NW) {
+                    const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+                    uint32_t bits[8];
+                    tp_unpack(v, bits);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint32_t kk = tp_key(bits[i]);
+                        if ((int)(kk >> 4) == Bk && mass_of(__uint_as_float(bits[i] << 16), mp))
+                            atomicAdd(&sh.h2c[kk & 15u], 1u);
+                    }
+                }
+                __syncthreads();
+                int ks = Bk * 16, cnt = 0;
+                for (int i = 15; i >= 0; --i) {
+                    cnt += (int)sh.h2c[i];
+                    if (cnt >= sh.needk) {
+                        ks = Bk * 16 + i;
                         break;
                     }
-                    above += h;
                 }
-                sh.bsel = B;
-                sh.bz[0] = theta - above;  // mass still needed inside bin B
-                sh.bz[1] = above;
-                sh.bz[2] = Z;
+                tau = mass_of(__uint_as_float(tp_unkey((uint32_t)ks) << 16), mp);  // tau_k
+                filtered_tiles(tau);
+                Zk = tiles_total();
             }
         }
-        __syncthreads();
-        const int B = sh.bsel;
-
-        // ---------------------------------------------------- pass 3: keys inside bin B
-        for (int t = warp; t < ntile; t += TP_NW) {
-            const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
-            uint32_t bits[8];
-            tp_unpack(v, bits);
+        // ---------------------------------------------------- top-p (R5) on the top-k masses
+        uint64_t Zp = Zk;
+        bool tie_below = false;
+        if (use_p) {
+            // coarse select (warp 0): lane l owns bins [l*128, l*128+128), heaviest first
+            if (warp == 0) {
+                unsigned __int128 th = (unsigned __int128)P * Zk + (((unsigned __int128)1 << 32) - 1);
+                uint64_t theta = (uint64_t)(th >> 32);
+                theta = theta ? theta : 1ull;  // top_p -> 0 keeps the heaviest level (as R5)
+                const int per = TP_H1 / 32;
+                const int lo = (31 - lane) * per;  // lane 0 owns the heaviest bins
+                uint64_t ls = 0;
+                for (int i = 0; i < per; ++i) ls += sh.h1[lo + i];
+                const uint64_t incl = warp_incl_scan_u64(ls, lane);  // mass of bins >= lane's lowest
+                const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= theta);
+                const int L = hit ? (__ffs(hit) - 1) : 31;
+                if (lane == L) {
+                    uint64_t above = incl - ls;
+                    int B = lo;
+                    for (int i = per - 1; i >= 0; --i) {
+                        const uint64_t h = sh.h1[lo + i];
+                        if (above + h >= theta) {
+                            B = lo + i;
+                            break;
+                        }
+                        above += h;
+                    }
+                    sh.bsel = B;
+                    sh.bz[0] = theta - above;  // mass still needed inside bin B
+                    sh.bz[1] = above;
+                }
+            }
+            __syncthreads();
+            const int B = sh.bsel;
+            // pass 3: keys inside bin B
+            for (int t = warp; t < ntile; t += TP_NW) {
+                const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+                uint32_t bits[8];
+                tp_unpack(v, bits);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const uint32_t kk = tp_key(bits[i]);
-                if ((int)(kk >> 4) == B) {
-                    const uint64_t mi = mass_of(__uint_as_float(bits[i] << 16), mp);
-                    if (mi) atomicAdd(&sh.h2[kk & 15u], (unsigned long long)mi);
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t kk = tp_key(bits[i]);
+                    if ((int)(kk >> 4) == B) {
+                        const uint64_t mi = mass_of(__uint_as_float(bits[i] << 16), mp);
+                        if (mi) atomicAdd(&sh.h2[kk & 15u], (unsigned long long)mi);
+                    }
                 }
             }
-        }
-        __syncthreads();
-        // tau = mass(k*); Z' from the histograms unless lower keys share tau (then pass 4)
-        uint64_t tau = 0, Zp = 0;
-        bool tie_below;
-        {
+            __syncthreads();
+            // tau = mass(k*) (>= tau_k: Theta <= Z_k); Z' from the histograms unless lower keys
+            // share tau (then a filtered pass)
             const uint64_t need = sh.bz[0];
             uint64_t above = 0;
             int ks = B * 16;
@@ -209,36 +315,14 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
             tau = mass_of(__uint_as_float(tp_unkey((uint32_t)ks) << 16), mp);
             Zp = sh.bz[1] + above + sh.h2[ks & 15];
             tie_below = ks > 0 && mass_of(__uint_as_float(tp_unkey((uint32_t)ks - 1u) << 16), mp) == tau;
+            if (tie_below) {
+                filtered_tiles(tau);
+                Zp = tiles_total();
+            }
         }
         const uint64_t md_full = (d >= 0) ? mass_of(__uint_as_float((uint32_t)row[d] << 16), mp) : 0ull;
         const uint64_t md = (md_full >= tau) ? md_full : 0ull;  // mass'(d)
 
-        // pass 4: filtered tile sums
-        auto filtered_tiles = [&]() {
-            for (int t = warp; t < ntile; t += TP_NW) {
-                const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
-                uint64_t mm[8];
-                mass_pair(v.x, mp, mm[0], mm[1]);
-                mass_pair(v.y, mp, mm[2], mm[3]);
-                mass_pair(v.z, mp, mm[4], mm[5]);
-                mass_pair(v.w, mp, mm[6], mm[7]);
-                uint64_t s = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) s += (mm[i] >= tau) ? mm[i] : 0ull;
-                const uint64_t ws = warp_sum_u51(s);
-                if (lane == 0) sh.tsum[t] = ws;
-            }
-            __syncthreads();
-        };
-        bool have_tiles = false;
-        if (tie_below) {
-            __syncthreads();  // tsum of pass 2 was read by warp 0 above
-            filtered_tiles();
-            have_tiles = true;
-            uint64_t zl = 0;
-            for (int t = lane; t < ntile; t += 32) zl += sh.tsum[t];
-            Zp = warp_sum_u64(zl);
-        }
         // decision (R7) — every thread computes it identically
         bool acc = false;
         if (j < q) acc = uniform_floor(row_draw(a, dsc, PURPOSE_ACCEPT), Zp) < md;
@@ -246,10 +330,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
         int cand = -1;
         if (status == ST_DECIDED) {
             // residual (d excluded) or bonus sample (R8): inverse CDF in ascending id
-            if (!have_tiles) {
-                __syncthreads();
-                filtered_tiles();
-            }
+            if (tiles_tau != tau) filtered_tiles(tau);
             const int excl = (j < q) ? d : -1;
             const uint64_t U = uniform_floor(row_draw(a, dsc, PURPOSE_SAMPLE), Zp - ((j < q) ? md : 0ull));
             if (warp == 0) {
@@ -310,7 +391,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
         }
         if (tid == 0) {
             sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-            complete_row(a, sh.stat, dsc.b, j, q, status, cand, Zp, (float)ldexp((double)sh.bz[2], -a.S));
+            complete_row(a, sh.stat, dsc.b, j, q, status, cand, Zp, (float)ldexp((double)Z, -a.S));
         }
         __syncthreads();
     }

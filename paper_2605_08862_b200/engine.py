@@ -35,14 +35,17 @@ class Target:
 class RolloutEngine:
     def __init__(self, ctx: Context, n: int, k: int, temperature: float, top_p: float,
                  target: Target, stream: torch.cuda.Stream | None = None, fused: bool = True,
-                 fuse_lookup: bool = True):
+                 fuse_lookup: bool = True, top_k: int = 0, ngram: tuple | None = None):
         self.ctx, self.n, self.k = ctx, n, k
         self.fused = fused  # bs_verify_commit (one launch) instead of bs_verify_step + bs_commit
         # bs_verify_commit_lookup: each launch also looks up the next step's drafts (the first
         # step's lookup runs in begin()), so a decoding step is target rows + one launch
-        self.fuse_lookup = fused and fuse_lookup
+        # ngram = (n_min, n_max): drafts from the n-gram linear-scan drafter (bs_draft_lookup_ngram,
+        # its own launch) instead of the suffix index
+        self.ngram = ngram
+        self.fuse_lookup = fused and fuse_lookup and ngram is None
         self.launches_per_step = 2 if self.fuse_lookup else 3
-        self.T, self.top_p, self.target = temperature, top_p, target
+        self.T, self.top_p, self.top_k, self.target = temperature, top_p, top_k, target
         # the kernel right before each verify launch is bsx_target_rows (the synthetic model),
         # which writes only row_index: the verify may plan before its PDL wait
         ctx.bsx_set_early_plan(True)
@@ -89,26 +92,35 @@ class RolloutEngine:
                                      self.match_len, stream=self.stream)
 
     # ------------------------------------------------------------------ decoding
+    def _lookup(self):
+        c, k, s = self.ctx, self.k, self.stream
+        if self.ngram is not None:
+            c.bs_draft_lookup_ngram(self.rl_step, self.slots, k, self.ngram[0], self.ngram[1], self.draft,
+                                    self.draft_len, self.match_len, stream=s)
+        else:
+            c.bs_draft_lookup(self.rl_step, self.slots, k, self.draft, self.draft_len, self.match_len,
+                              stream=s)
+
     def step(self):
         c, k, s = self.ctx, self.k, self.stream
         if not self.fuse_lookup:
-            c.bs_draft_lookup(self.rl_step, self.slots, k, self.draft, self.draft_len, self.match_len,
-                              stream=s)
+            self._lookup()
         t = self.target
         c.bsx_target_rows(self.slots, self.draft, self.draft_len, k, t.target_seed, t.mode,
                           t.nbank, self.row_index, stream=s)
         if self.fuse_lookup:
             c.bs_verify_commit_lookup(self.rl_step, self.slots, t.bank, self.row_index, t.bank.shape[1],
                                       self.draft, self.draft_len, k, self.T, self.top_p, self.out_tokens,
-                                      self.out_len, self.out_acc, self.finished, self.match_len, stream=s)
+                                      self.out_len, self.out_acc, self.finished, self.match_len, stream=s,
+                                      top_k=self.top_k)
         elif self.fused:
             c.bs_verify_commit(self.slots, t.bank, self.row_index, t.bank.shape[1], self.draft,
                                self.draft_len, k, self.T, self.top_p, self.out_tokens, self.out_len,
-                               self.out_acc, self.finished, stream=s)
+                               self.out_acc, self.finished, stream=s, top_k=self.top_k)
         else:
             c.bs_verify_step(self.slots, t.bank, self.row_index, t.bank.shape[1], self.draft,
                              self.draft_len, k, self.T, self.top_p, self.out_tokens, self.out_len,
-                             self.out_acc, stream=s)
+                             self.out_acc, stream=s, top_k=self.top_k)
             c.bs_commit(self.slots, self.out_tokens, self.out_len, k, self.finished, stream=s)
 
     # target rows + verify (fused commit and next lookup), or lookup + target rows + verify;

@@ -95,7 +95,7 @@ for live in (0, 1, 8, 256):
     res = {nm: time_graph(op(nm)) for nm in ("torch_noop", "lookup", "target_rows", "verify", "commit")}
     print(f"live {live:3d}: " + "  ".join(f"{k_} {v:6.2f} us" for k_, v in res.items()))
 for live in (1, 8, 32, 256):
-    for kind in ("rows", "split", "cluster"):
+    for kind in ("rows", "cluster"):
         ctx.bsx_set_verify_kernel(kind)
         begin(live)
         print(f"live {live:3d} {kind:8s}: verify {time_graph(op('verify')):7.2f} us")

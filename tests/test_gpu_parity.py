@@ -13,7 +13,7 @@ from workloads import TargetSpec, bank_rows, bf16_bits_to_f32, f32_to_bf16_bits 
 from tests.gpu_util import bank_numpy, pools_for, setup_rollouts, to_dev  # noqa: E402
 
 
-def _verify_gpu(bs, ctx, rows_dense, drafts, dlen, k, T, top_p, stride=None):
+def _verify_gpu(bs, ctx, rows_dense, drafts, dlen, k, T, top_p, stride=None, top_k=0):
     """Run bs_verify_step on dense rows [n, k+1, V] (uint16) with rollouts already begun."""
     n = drafts.shape[0]
     V = rows_dense.shape[2]
@@ -31,7 +31,8 @@ def _verify_gpu(bs, ctx, rows_dense, drafts, dlen, k, T, top_p, stride=None):
     out_n = torch.zeros((n, k + 1), dtype=torch.float32, device="cuda")
     out_z = torch.zeros((n, k + 1), dtype=torch.int64, device="cuda")
     ctx.bs_verify_step(slots, lg, None, stride, to_dev(drafts.astype(np.int32)),
-                       to_dev(dlen.astype(np.int32)), k, T, top_p, out_t, out_l, out_a, out_n, out_z)
+                       to_dev(dlen.astype(np.int32)), k, T, top_p, out_t, out_l, out_a, out_n, out_z,
+                       top_k=top_k)
     torch.cuda.synchronize()
     return (out_t.cpu().numpy(), out_l.cpu().numpy(), out_a.cpu().numpy(), out_n.cpu().numpy(),
             out_z.cpu().numpy().view(np.uint64))
@@ -47,12 +48,12 @@ def _begin(bs, ctx, n, pos_max_len, uids, M):
 
 
 def _compare_step(orc, rows, drafts, dlen, k, T, top_p, seed, uids, max_len, eos, got,
-                  pos=0):
+                  pos=0, top_k=0):
     ot, ol, oa, on, oz = got
     for b in range(drafts.shape[0]):
         q = int(dlen[b])
         o = orc.verify_one([rows[b, j] for j in range(k + 1)], T, top_p, seed, int(uids[b]), pos,
-                           int(max_len[b]), eos, False, [int(x) for x in drafts[b, :q]], k)
+                           int(max_len[b]), eos, False, [int(x) for x in drafts[b, :q]], k, top_k=top_k)
         assert int(ol[b]) == len(o.tokens), (b, ol[b], o.tokens)
         assert [int(x) for x in ot[b, : ol[b]]] == o.tokens, (b, ot[b], o.tokens)
         assert int(oa[b]) == o.accepted
@@ -64,7 +65,7 @@ def _compare_step(orc, rows, drafts, dlen, k, T, top_p, seed, uids, max_len, eos
             assert int(oz[b, j]) == 0 and float(on[b, j]) == 0.0
 
 
-KERNELS = ["rows", "split", "cluster"]  # bsx_set_verify_kernel: every verify kernel
+KERNELS = ["rows", "cluster"]  # bsx_set_verify_kernel: every verify kernel
 
 
 @pytest.mark.parametrize("path", KERNELS)
@@ -139,6 +140,33 @@ def test_verify_top_p_parity(bs, orc, V, T, top_p, kind, stride):
     got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, T, top_p, stride)
     assert ctx.bs_sync_status() == 0
     _compare_step(orc, rows, drafts, dlen, k, T, top_p, seed, uids, max_len, -1, got)
+
+
+@pytest.mark.parametrize("V,T,top_p,top_k,kind", [
+    (1024, 1.0, 1.0, 1, "normal"), (1024, 1.0, 1.0, 50, "normal"), (4099, 0.7, 1.0, 7, "quant"),
+    (1000, 1.0, 1.0, 3, "dense0"), (3000, 1.3, 0.9, 20, "normal"), (4096, 1.0, 0.5, 200, "quant"),
+    (1001, 1.0, 0.8, 2, "quant"), (2048, 1.0, 1.0, 2047, "normal"), (2048, 1.0, 1.0, 4096, "normal"),
+    (151936, 1.0, 1.0, 50, "normal"), (151936, 1.0, 0.95, 40, "dense0")])
+def test_verify_top_k_parity(bs, orc, V, T, top_p, top_k, kind):
+    """Top-k then top-p (readings R5k, R5; SPEC S:74 order): the count-weighted key select on
+    the GPU keeps exactly the oracle's tie-closed top-k set, top-p then runs on it; accepted
+    lengths, tokens and Z' bit-exact ("quant" rows have many tied logits at the k-th place)."""
+    rng = np.random.default_rng(V * 11 + top_k)
+    k = 4 if V < 100000 else 6
+    n = 40 if V < 100000 else 8
+    rows = _topp_rows(rng, kind, n, k, V)
+    argm = bf16_bits_to_f32(rows).argmax(axis=2)
+    drafts = np.where(rng.random((n, k)) < 0.7, argm[:, :k], rng.integers(0, V, (n, k)))
+    dlen = rng.integers(0, k + 1, n)
+    max_len = np.full(n, 1000)
+    seed = 0x5EED
+    ctx = bs.Context(vocab=V, eos_id=-1, k_max=k, match_max=8, max_rollouts=n,
+                     pool_capacity_tokens=16, pool_capacity_seqs=4, seed=seed)
+    uids = np.arange(n, dtype=np.uint64) * np.uint64(7919) + np.uint64(3)
+    _begin(bs, ctx, n, max_len, uids, 8)
+    got = _verify_gpu(bs, ctx, rows, drafts, dlen, k, T, top_p, top_k=top_k)
+    assert ctx.bs_sync_status() == 0
+    _compare_step(orc, rows, drafts, dlen, k, T, top_p, seed, uids, max_len, -1, got, top_k=top_k)
 
 
 @pytest.mark.parametrize("path", KERNELS)
@@ -246,7 +274,7 @@ def test_verify_error_only_if_needed(bs, orc, path, V):
 
 # ------------------------------------------------------------------ lookup
 def _gpu_lookup(bs, ctx, seq_prompt, seq_off, tokens, ctxs, prompt_of, k, M, max_len=1 << 20,
-                rl_step=1):
+                rl_step=1, ngram=None):
     n = len(ctxs)
     ctx.bs_draft_pool_put(rl_step, to_dev(seq_prompt.astype(np.int32)), to_dev(seq_off),
                           to_dev(tokens.astype(np.int32)) if len(tokens) else
@@ -263,10 +291,57 @@ def _gpu_lookup(bs, ctx, seq_prompt, seq_off, tokens, ctxs, prompt_of, k, M, max
     d = torch.zeros((n, k), dtype=torch.int32, device="cuda")
     dl = torch.zeros(n, dtype=torch.int32, device="cuda")
     ml = torch.zeros(n, dtype=torch.int32, device="cuda")
-    ctx.bs_draft_lookup(rl_step, slots, k, d, dl, ml)
+    if ngram is None:
+        ctx.bs_draft_lookup(rl_step, slots, k, d, dl, ml)
+    else:
+        ctx.bs_draft_lookup_ngram(rl_step, slots, k, ngram[0], ngram[1], d, dl, ml)
     torch.cuda.synchronize()
     assert ctx.bs_sync_status() == 0
     return d.cpu().numpy(), dl.cpu().numpy(), ml.cpu().numpy()
+
+
+@pytest.mark.parametrize("vocab,n_min,n_max,M,k", [(3, 1, 8, 8, 4), (5, 2, 6, 8, 3), (2, 1, 32, 32, 16),
+                                                   (50, 1, 4, 16, 8), (4, 3, 3, 8, 5)])
+def test_ngram_lookup_parity_random_pools(bs, orc, vocab, n_min, n_max, M, k):
+    """Draft-source variant f4 (reading N1): the GPU n-gram linear scan == the oracle's
+    (drafts and match length n), random pools of several prompts, ragged and empty sequences,
+    contexts copied from pool sequences (long matches), max_len clamps."""
+    rng = np.random.default_rng(vocab * 31 + n_max)
+    n_prompts = 5
+    seqs, sp = [], []
+    for P in range(n_prompts):
+        for _ in range(int(rng.integers(0, 6))):
+            seqs.append(rng.integers(0, vocab, int(rng.integers(0, 300))).astype(np.int32))
+            sp.append(P)
+    off = np.zeros(len(seqs) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(s) for s in seqs])
+    tokens = np.concatenate(seqs) if seqs and off[-1] else np.zeros(0, np.int32)
+    ctxs, pof = [], []
+    for _ in range(150):
+        P = int(rng.integers(0, n_prompts))
+        own = [s for s, p in zip(seqs, sp) if p == P and len(s) > 3]
+        if own and rng.random() < 0.6:
+            s = own[int(rng.integers(0, len(own)))]
+            e = int(rng.integers(1, len(s) + 1))
+            c = list(rng.integers(0, vocab, int(rng.integers(0, 5)))) + list(s[:e])
+        else:
+            c = list(rng.integers(0, vocab, int(rng.integers(1, 40))))
+        ctxs.append([int(x) for x in c] or [0])
+        pof.append(P)
+    ctx = bs.Context(vocab=vocab, k_max=k, match_max=M, max_rollouts=len(ctxs),
+                     pool_capacity_tokens=max(1, len(tokens)), pool_capacity_seqs=max(1, len(seqs)))
+    max_len = 3 if vocab == 4 else 1 << 20
+    d, dl, ml = _gpu_lookup(bs, ctx, np.asarray(sp), off, tokens, ctxs, pof, k, M, max_len=max_len,
+                            ngram=(n_min, n_max))
+    pools = {}
+    for s_, p_ in zip(seqs, sp):
+        pools.setdefault(p_, []).append([int(x) for x in s_])
+    for b, (c, P) in enumerate(zip(ctxs, pof)):
+        want, n = orc.lookup_ngram(pools.get(P, []), c[-M:], n_min, n_max, k)
+        want = want[:max(0, max_len - 1)]  # L6 clamp at pos 0
+        assert int(dl[b]) == len(want), (b, c, want, d[b], dl[b])
+        assert [int(x) for x in d[b, :dl[b]]] == want, b
+        assert int(ml[b]) == n, b
 
 
 @pytest.mark.parametrize("vocab,Lmin,M,k", [(3, 1, 8, 4), (5, 1, 6, 3), (4, 2, 8, 5),

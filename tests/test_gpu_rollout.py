@@ -11,7 +11,7 @@ from tests.gpu_util import bank_numpy, pools_for, setup_rollouts, to_dev  # noqa
 from paper_2605_08862_b200.engine import TARGET_MODES  # noqa: E402
 
 
-def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fused="lookup"):
+def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fused="lookup", top_k=0):
     from paper_2605_08862_b200.engine import RolloutEngine, Target
 
     ctx = bs.Context(vocab=spec.V, eos_id=eos, k_max=k, match_max=M, max_rollouts=n,
@@ -22,12 +22,12 @@ def _engine(bs, spec, n, k, M, T, top_p, seed, eos, pool_tokens, pool_seqs, fuse
     # "lookup": bs_verify_commit_lookup; "commit": lookup + bs_verify_commit; "none": lookup +
     # bs_verify_step + bs_commit
     eng = RolloutEngine(ctx, n, k, T, top_p, Target(bank, spec.nbank, spec.target_seed, mode),
-                        fused=fused != "none", fuse_lookup=fused == "lookup")
+                        fused=fused != "none", fuse_lookup=fused == "lookup", top_k=top_k)
     return ctx, eng
 
 
 def _oracle_rollouts(orc, spec, pid, tail_rows, uids, ml, pools_np, k, M, T, top_p, seed, eos,
-                     which, max_steps=None):
+                     which, max_steps=None, top_k=0):
     from oracle.rollout import OracleRollout, bank_row_fn, pools_by_prompt, run_rollouts
 
     pools = pools_by_prompt(*pools_np)
@@ -35,7 +35,7 @@ def _oracle_rollouts(orc, spec, pid, tail_rows, uids, ml, pools_np, k, M, T, top
                          context=[int(x) for x in tail_rows[b] if x >= 0], max_len=int(ml[b]))
            for b in which]
     run_rollouts(ros, pools, bank_row_fn(spec), k=k, M=M, Lmin=1, T=T, top_p=top_p, seed=seed,
-                 eos=eos, max_steps=max_steps)
+                 eos=eos, max_steps=max_steps, top_k=top_k)
     return ros
 
 
@@ -71,6 +71,81 @@ def test_tiny_rollouts_token_for_token(bs, orc, T, mode, fused):
     assert st["verify_steps"] == n_spec
     assert st["tokens"] == sum(len(r.generated) for r in ros)
     assert n_spec > 0
+    # every device counter behind AL / DL / AR equals the oracle's own
+    # accounting of the same steps: (q, m*, draft, emitted, accepted, StepOut)
+    steps_ = [s_ for ro in ros for s_ in ro.steps]
+    vs = [s_ for s_ in steps_ if s_[0] > 0]
+    assert st["plain_steps"] == len(steps_) - len(vs)
+    assert st["accepted"] == sum(s_[4] for s_ in vs)
+    assert st["proposed"] == sum(s_[0] for s_ in vs)
+    assert st["rows_needed"] == sum(s_[5].rows_used for s_ in steps_)
+    hist = [0] * len(st["streak_hist"])
+    for s_ in vs:
+        hist[min(len(s_[3]), len(hist) - 1)] += 1
+    assert st["streak_hist"] == hist
+    if st["verify_steps"]:
+        assert st["acceptance_length"] == sum(len(s_[3]) for s_ in vs) / len(vs)
+
+
+@pytest.mark.parametrize("top_k,top_p", [(5, 1.0), (40, 0.9)])
+def test_tiny_rollouts_top_k(bs, orc, top_k, top_p):
+    """TINY rollouts under top-k (then top-p) filtering (readings R5k, R5): the filtered verify
+    kernel with its separate commit / lookup launches, token-for-token vs the oracle's loop."""
+    spec = TargetSpec(V=1024, nbank=256, mode="mixed", beta=6.0)
+    M, k, L, seed, eos = 16, 4, 48, 9, 1023
+    prompts, tails, pid, tail_rows, uids, ml = setup_rollouts(spec, 1, 4, M, L)
+    pools_np = pools_for(spec, prompts, tails, 4, np.full(4, 44), 0.85, prefix=M)
+    n = len(pid)
+    ctx, eng = _engine(bs, spec, n, k, M, 1.0, top_p, seed, eos, len(pools_np[2]), len(pools_np[0]),
+                       top_k=top_k)
+    resp = torch.full((n, L), -1, dtype=torch.int32, device="cuda")
+    ctx.bs_rollout_bind_output(resp, L)
+    eng.put_pools(1, to_dev(pools_np[0]), to_dev(pools_np[1]), to_dev(pools_np[2]))
+    eng.seal(1)
+    eng.begin(to_dev(uids.view(np.int64)), to_dev(pid), to_dev(tail_rows), to_dev(ml))
+    eng.run_until_done(chunk=8, use_graph=True)
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() == 0
+    got = resp.cpu().numpy()
+    ros = _oracle_rollouts(orc, spec, pid, tail_rows, uids, ml, pools_np, k, M, 1.0, top_p, seed, eos,
+                           range(n), top_k=top_k)
+    for b, ro in enumerate(ros):
+        assert [int(x) for x in got[b, : len(ro.generated)]] == ro.generated, b
+    assert eng.stats()["proposed"] > 0
+
+
+@pytest.mark.parametrize("ngram", [(1, 4), (2, 8)])
+def test_tiny_rollouts_ngram_drafts(bs, orc, ngram):
+    """TINY rollouts drafted by the n-gram linear-scan drafter (f4, reading N1) under graph
+    replay: token-for-token vs the oracle's loop with the same drafter; drafts accepted."""
+    spec = TargetSpec(V=1024, nbank=256, mode="position", beta=12.0)
+    M, k, L, seed, eos = 16, 4, 48, 21, -1
+    prompts, tails, pid, tail_rows, uids, ml = setup_rollouts(spec, 2, 3, M, L)
+    pools_np = pools_for(spec, prompts, tails, 4, np.full(8, 44), 0.85, prefix=M)
+    n = len(pid)
+    ctx, eng = _engine(bs, spec, n, k, M, 1.0, 1.0, seed, eos, len(pools_np[2]), len(pools_np[0]))
+    eng.ngram = ngram
+    eng.fuse_lookup = False
+    resp = torch.full((n, L), -1, dtype=torch.int32, device="cuda")
+    ctx.bs_rollout_bind_output(resp, L)
+    eng.put_pools(1, to_dev(pools_np[0]), to_dev(pools_np[1]), to_dev(pools_np[2]))
+    eng.seal(1)
+    eng.begin(to_dev(uids.view(np.int64)), to_dev(pid), to_dev(tail_rows), to_dev(ml))
+    eng.run_until_done(chunk=8, use_graph=True)
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() == 0
+    got = resp.cpu().numpy()
+    from oracle.rollout import OracleRollout, bank_row_fn, pools_by_prompt, run_rollouts
+
+    ros = [OracleRollout(prompt=int(pid[b]), uid=int(uids[b]), context=[int(x) for x in tail_rows[b] if x >= 0],
+                         max_len=int(ml[b])) for b in range(n)]
+    run_rollouts(ros, pools_by_prompt(*pools_np), bank_row_fn(spec), k=k, M=M, Lmin=1, T=1.0, top_p=1.0,
+                 seed=seed, eos=eos, ngram=ngram)
+    for b, ro in enumerate(ros):
+        assert [int(x) for x in got[b, : len(ro.generated)]] == ro.generated, b
+    st = eng.stats()
+    assert st["accepted"] > 0
+    assert st["accepted"] == sum(s_[4] for ro in ros for s_ in ro.steps)
 
 
 def test_tiny_rollouts_graph_replay_matches_eager(bs, orc):
