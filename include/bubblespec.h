@@ -171,6 +171,37 @@ bs_status bs_nccl_unique_id(void* id128);
 bs_status bs_nccl_comm_init(void** comm_out, const void* id128, int32_t world, int32_t rank);
 bs_status bs_nccl_comm_destroy(void* comm);
 
+/* ---------------------------------------------------------------- bubble pre-generation */
+/* Polling synchronizer of rollout pre-generation ("during the
+ * pre-generation of B_{t+1}, each rank queries a central synchronizer every T decoding steps.
+ * If the synchronizer reports that all ranks have completed B_t, pre-generation is halted";
+ * T = 50).  It is an array of BS_BUBBLE_MAX_RANKS 64-bit words in the owner rank's
+ * device memory (one per DP rank: the latest rl_step that rank finished, ~0 before any),
+ * mapped into the other ranks' address spaces over NVLink by CUDA IPC.  Arrive and poll are
+ * single-kernel, stream-ordered calls (capturable in a CUDA graph with the pre-generation
+ * steps): no collective, so a rank still decoding its batch never waits on the pollers.
+ * Pre-generation itself is plain decoding (bs_verify_* with draft_len = 0) of the next RL
+ * step's prompts in spare rollout slots; its responses become the next step's pools
+ * (bs_draft_pool_put, then bs_draft_exchange routes them to their owner ranks). */
+#define BS_BUBBLE_MAX_RANKS 64
+typedef struct bs_bubble_sync bs_bubble_sync;
+/* Owner side: allocate the words on `device` (all ~0). */
+bs_status bs_bubble_sync_create(int32_t device, bs_bubble_sync** out);
+/* Owner side: the 64-byte CUDA IPC handle of the words (host memory handle64[64]), to be sent to
+ * the other ranks (e.g. over the torch process group). */
+bs_status bs_bubble_sync_export(const bs_bubble_sync* sync, void* handle64);
+/* Peer side: map the owner's words on this rank's `device` (NVLink peer access).  A process
+ * cannot open its own handle: the owner uses the object bs_bubble_sync_create returned. */
+bs_status bs_bubble_sync_open(int32_t device, const void* handle64, bs_bubble_sync** out);
+void bs_bubble_sync_destroy(bs_bubble_sync* sync);
+/* Stream-ordered: after the work already on `stream` (the rank's last decoding step of B_t),
+ * store rl_step into word `rank` (a system-scope release store).  rl_step != ~0. */
+bs_status bs_bubble_sync_arrive(bs_bubble_sync* sync, int32_t rank, uint64_t rl_step, void* stream);
+/* Stream-ordered: *halt (a device int32) = 1 if every word 0..world-1 holds >= rl_step (all
+ * ranks completed B_t: stop pre-generating), else 0 (system-scope acquire loads). */
+bs_status bs_bubble_sync_poll(bs_bubble_sync* sync, int32_t world, uint64_t rl_step, int32_t* halt,
+                              void* stream);
+
 /* ---------------------------------------------------------------- per decoding step */
 /* Draft lookup (Alg. 1 line 3: "Retrieve a draft block from T using prefix y"):
  * anchor on the longest suffix (<= M) of each rollout's context that occurs in

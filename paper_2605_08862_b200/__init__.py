@@ -5,6 +5,7 @@ The CUDA library (libbubblespec.so, sm_100a) is required; there is no CPU fallba
 """
 from ._lib import LIB_PATH, BubbleSpecError, load  # noqa: F401
 from .api import (  # noqa: F401
+    BubbleSync,
     Context,
     bs_route_plan,
     bsx_synth_bank,
@@ -13,3 +14,4 @@ from .api import (  # noqa: F401
     nccl_unique_id,
 )
 from .engine import RolloutEngine  # noqa: F401
+from .pregen import Pregenerator, pool_sequences  # noqa: F401

@@ -52,6 +52,12 @@ SIGNATURES = {
     "bs_draft_lookup": (C.c_int, [_V, _U64, _I32, _V, _I32, _V, _V, _V, _V]),
     "bs_verify_step": (C.c_int, [_V, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V, _V,
                                  _V, _V, _V, _V]),
+    "bs_bubble_sync_create": (C.c_int, [_I32, C.POINTER(_V)]),
+    "bs_bubble_sync_export": (C.c_int, [_V, _V]),
+    "bs_bubble_sync_open": (C.c_int, [_I32, _V, C.POINTER(_V)]),
+    "bs_bubble_sync_destroy": (None, [_V]),
+    "bs_bubble_sync_arrive": (C.c_int, [_V, _I32, _U64, _V]),
+    "bs_bubble_sync_poll": (C.c_int, [_V, _I32, _U64, _V, _V]),
     "bs_draft_lookup_ngram": (C.c_int, [_V, _U64, _I32, _V, _I32, _I32, _I32, _V, _V, _V, _V]),
     "bs_verify_commit": (C.c_int, [_V, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V, _V,
                                    _V, _V, _V, _V, _V]),

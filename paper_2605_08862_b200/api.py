@@ -234,3 +234,49 @@ def nccl_comm_init(uid: bytes, world: int, rank: int):
 
 def nccl_comm_destroy(comm):
     _chk(None, load().bs_nccl_comm_destroy(comm), "bs_nccl_comm_destroy")
+
+
+class BubbleSync:
+    """The polling synchronizer of pre-generation (bs_bubble_sync_*).  The owner
+    rank creates it (handle=None) and sends export() to the others, which open it."""
+
+    def __init__(self, device: int, handle: bytes | None = None):
+        lib = load()
+        h = _V()
+        self.device = device
+        if handle is None:
+            st = lib.bs_bubble_sync_create(device, C.byref(h))
+        else:
+            buf = C.create_string_buffer(bytes(handle), 64)
+            st = lib.bs_bubble_sync_open(device, buf, C.byref(h))
+        if st != 0:
+            raise BubbleSpecError(st, "bs_bubble_sync_create/open", "")
+        self.handle = h
+
+    def export(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        st = load().bs_bubble_sync_export(self.handle, buf)
+        if st != 0:
+            raise BubbleSpecError(st, "bs_bubble_sync_export", "")
+        return buf.raw
+
+    def arrive(self, rank: int, rl_step: int, stream=None):
+        st = load().bs_bubble_sync_arrive(self.handle, rank, rl_step, _stream(stream, self.device))
+        if st != 0:
+            raise BubbleSpecError(st, "bs_bubble_sync_arrive", "")
+
+    def poll(self, world: int, rl_step: int, halt, stream=None):
+        st = load().bs_bubble_sync_poll(self.handle, world, rl_step, _p(halt), _stream(stream, self.device))
+        if st != 0:
+            raise BubbleSpecError(st, "bs_bubble_sync_poll", "")
+
+    def close(self):
+        if self.handle:
+            load().bs_bubble_sync_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -35,7 +35,8 @@ class Target:
 class RolloutEngine:
     def __init__(self, ctx: Context, n: int, k: int, temperature: float, top_p: float,
                  target: Target, stream: torch.cuda.Stream | None = None, fused: bool = True,
-                 fuse_lookup: bool = True, top_k: int = 0, ngram: tuple | None = None):
+                 fuse_lookup: bool = True, top_k: int = 0, ngram: tuple | None = None,
+                 slot0: int = 0, plain: bool = False):
         self.ctx, self.n, self.k = ctx, n, k
         self.fused = fused  # bs_verify_commit (one launch) instead of bs_verify_step + bs_commit
         # bs_verify_commit_lookup: each launch also looks up the next step's drafts (the first
@@ -43,8 +44,11 @@ class RolloutEngine:
         # ngram = (n_min, n_max): drafts from the n-gram linear-scan drafter (bs_draft_lookup_ngram,
         # its own launch) instead of the suffix index
         self.ngram = ngram
-        self.fuse_lookup = fused and fuse_lookup and ngram is None
-        self.launches_per_step = 2 if self.fuse_lookup else 3
+        # plain = True: no drafts at all (draft_len stays 0): plain decoding, one sample per step
+        # (Alg. 1 lines 4-7) -- the pre-generation of the next RL step's responses
+        self.plain = plain
+        self.fuse_lookup = fused and fuse_lookup and ngram is None and not plain
+        self.launches_per_step = 2 if (self.fuse_lookup or plain) else 3
         self.T, self.top_p, self.top_k, self.target = temperature, top_p, top_k, target
         # the kernel right before each verify launch is bsx_target_rows (the synthetic model),
         # which writes only row_index: the verify may plan before its PDL wait
@@ -53,7 +57,7 @@ class RolloutEngine:
         # a dedicated stream: CUDA graphs cannot be captured on the legacy default stream
         self.stream = stream or torch.cuda.Stream(dev)
         i32 = dict(dtype=torch.int32, device=dev)
-        self.slots = torch.arange(n, **i32)
+        self.slots = torch.arange(slot0, slot0 + n, **i32)  # this engine's rollout slots
         self.draft = torch.full((n, max(k, 1)), -1, **i32)
         self.draft_len = torch.zeros(n, **i32)
         self.match_len = torch.zeros(n, **i32)
@@ -103,7 +107,7 @@ class RolloutEngine:
 
     def step(self):
         c, k, s = self.ctx, self.k, self.stream
-        if not self.fuse_lookup:
+        if not self.fuse_lookup and not self.plain:
             self._lookup()
         t = self.target
         c.bsx_target_rows(self.slots, self.draft, self.draft_len, k, t.target_seed, t.mode,

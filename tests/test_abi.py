@@ -151,3 +151,16 @@ def test_metric_identity_table1():
         st[5] = round(dl * steps)
         m = summarize_stats(st)
         assert abs(100 * m["acceptance_rate"] - ar) < 0.06, (al, dl, ar, m["acceptance_rate"])
+
+
+def test_pool_sequences_from_pregen():
+    """Pre-generated responses -> pool sequences (reading L4: [last M prompt tokens] +
+    response, padding dropped, empty responses skipped), host logic of f1."""
+    from paper_2605_08862_b200.pregen import pool_sequences
+
+    tails = np.array([[-1, -1, 5, 6], [1, 2, 3, 4], [-1, 9, 9, 9]], dtype=np.int32)
+    resp = np.array([[10, 11, 12, -1], [20, -1, -1, -1], [30, 31, 32, 33]], dtype=np.int32)
+    sp, off, tok = pool_sequences([7, 8, 9], tails, resp, [3, 0, 4], M=3)
+    assert list(sp) == [7, 9]
+    assert list(off) == [0, 5, 12]
+    assert list(tok) == [5, 6, 10, 11, 12, 9, 9, 9, 30, 31, 32, 33]
