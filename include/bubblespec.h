@@ -291,6 +291,31 @@ bs_status bs_verify_commit_lookup(bs_ctx* ctx, uint64_t rl_step, int32_t n, cons
 bs_status bs_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* out_tokens,
                     const int32_t* out_len, int32_t k, int32_t* finished, void* stream);
 
+/* ---------------------------------------------------------------- unified attention (f2) */
+/* Unified variable-query-length decode attention (Table 2 at
+ * P:220-232): one launch over a batch mixing plain decode requests (q_len = 1) and speculative
+ * requests (q_len = 1 + drafts), causal grouped-query attention over a paged bf16 KV cache,
+ * the short-query matmuls on the tensor cores (tcgen05, TMEM accumulators, TMA-loaded KV).
+ *   q            [T, H_q, head_dim] bf16, T = sum_b q_len[b]; request b's rows follow request
+ *                b-1's (b = 0 first); its q_len[b] tokens are the LAST of its context
+ *   k_cache/v_cache [num_pages, H_kv, page_size, head_dim] bf16 (device)
+ *   page_table   [B, max_pages] int32 (device): page of tokens [i*page_size, (i+1)*page_size)
+ *   ctx_len_dev  [B] int32 (device) and ctx_len / q_len [B] (HOST copies: the launch plan)
+ *   scale        softmax scale (<= 0: 1/sqrt(head_dim))
+ *   out          [T, H_q, head_dim] bf16: softmax(q k^T * scale, causal) v, token i of request b
+ *                attending keys 0 .. ctx_len[b] - q_len[b] + i, query head h using KV head
+ *                h / (H_q / H_kv)
+ *   workspace    device scratch of bs_unified_attention_workspace() bytes
+ * Supported: head_dim = 128, page_size = 64, q_len[b] * H_q / H_kv <= 128.  Errors:
+ * BS_ERR_INVALID (shapes), BS_ERR_CAPACITY (workspace too small), BS_ERR_CUDA. */
+bs_status bs_unified_attention_workspace(int32_t B, const int32_t* ctx_len, const int32_t* q_len, int32_t H_q,
+                                         int32_t H_kv, int64_t* bytes);
+bs_status bs_unified_attention(const void* q, const void* k_cache, const void* v_cache, int64_t num_pages,
+                               const int32_t* page_table, int32_t max_pages, const int32_t* ctx_len_dev,
+                               const int32_t* ctx_len, const int32_t* q_len, int32_t B, int32_t H_q, int32_t H_kv,
+                               int32_t head_dim, int32_t page_size, float scale, void* out, void* workspace,
+                               int64_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------- tuning */
 /* Select the kernel bs_verify_step uses for rows without top-p (all compute identical
  * results): 0 auto (= 3 when ceil(V/8) <= 53248, else 1; env BS_VERIFY_KERNEL
@@ -328,6 +353,9 @@ int32_t bsx_launch_info(const bs_ctx* ctx, int64_t* out, int32_t n);
 /* bank[rows, V] bf16: Irwin-Hall(4 hashed bytes) * 2^-6; the peak column holds beta. */
 bs_status bsx_synth_bank(void* bank_bf16, int64_t rows, int32_t V, uint32_t bank_seed,
                          float beta, void* stream);
+/* out[i] (bf16), i < n: (sum of the 4 bytes of h32(i * 0x9E3779B1 + base) - 510) * mult, the
+ * values of workloads/attn.py (bit-identical). */
+bs_status bsx_synth_attn_values(void* out_bf16, int64_t n, uint32_t base, float mult, void* stream);
 /* Synthetic target "forward": row_index[b*(k+1)+j] = target_row(prompt, pos+j, prev_j)
  * for j <= draft_len[b] (prev_0 = last context token, prev_j = draft[j-1]).
  * mode: 0 position, 1 markov, 2 mixed, 3 sample (workloads.TargetSpec). */

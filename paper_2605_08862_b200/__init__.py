@@ -8,6 +8,8 @@ from .api import (  # noqa: F401
     BubbleSync,
     Context,
     bs_route_plan,
+    bs_unified_attention,
+    bsx_synth_attn_values,
     bsx_synth_bank,
     nccl_comm_destroy,
     nccl_comm_init,

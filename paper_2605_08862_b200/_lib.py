@@ -58,6 +58,10 @@ SIGNATURES = {
     "bs_bubble_sync_destroy": (None, [_V]),
     "bs_bubble_sync_arrive": (C.c_int, [_V, _I32, _U64, _V]),
     "bs_bubble_sync_poll": (C.c_int, [_V, _I32, _U64, _V, _V]),
+    "bs_unified_attention_workspace": (C.c_int, [_I32, _V, _V, _I32, _I32, C.POINTER(_I64)]),
+    "bs_unified_attention": (C.c_int, [_V, _V, _V, _I64, _V, _I32, _V, _V, _V, _I32, _I32, _I32, _I32, _I32,
+                                       C.c_float, _V, _V, _I64, _V]),
+    "bsx_synth_attn_values": (C.c_int, [_V, _I64, _U32, C.c_float, _V]),
     "bs_draft_lookup_ngram": (C.c_int, [_V, _U64, _I32, _V, _I32, _I32, _I32, _V, _V, _V, _V]),
     "bs_verify_commit": (C.c_int, [_V, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V, _V,
                                    _V, _V, _V, _V, _V]),
