@@ -282,34 +282,43 @@ class BubbleSync:
             pass
 
 
-def bs_unified_attention(q, k_cache, v_cache, page_table, ctx_len, q_len, H_kv: int, out=None, scale: float = 0.0,
-                         workspace=None, stream=None):
+def unified_attention_workspace_bytes(ctx_len, q_len, H_q: int, H_kv: int) -> int:
+    """bs_unified_attention_workspace for host lists ctx_len / q_len."""
+    import numpy as np
+
+    ql = np.ascontiguousarray(np.asarray(q_len, dtype=np.int32))
+    cl = np.ascontiguousarray(np.asarray(ctx_len, dtype=np.int32))
+    ip = C.POINTER(C.c_int32)
+    nbytes = C.c_int64()
+    st = load().bs_unified_attention_workspace(len(ql), cl.ctypes.data_as(ip), ql.ctypes.data_as(ip), H_q, H_kv,
+                                               C.byref(nbytes))
+    if st != 0:
+        raise BubbleSpecError(st, "bs_unified_attention_workspace", "")
+    return int(nbytes.value)
+
+
+def bs_unified_attention(q, k_cache, v_cache, page_table, ctx_len_dev, ctx_len, q_len, H_kv: int, out=None,
+                         scale: float = 0.0, workspace=None, stream=None):
     """Unified variable-query-length decode attention (bs_unified_attention).  q [T, H_q, 128],
     k_cache / v_cache [num_pages, H_kv, 64, 128] (bf16 tensors, or int16 holding bf16 bits),
-    page_table [B, max_pages] int32 and ctx_len [B] int32 on the device; q_len / ctx_len also
-    host lists (the launch plan).  Returns out [T, H_q, 128] (same dtype as q)."""
+    page_table [B, max_pages] int32 and ctx_len_dev [B] int32 on the device; ctx_len / q_len the
+    host copies (the launch plan).  Returns out [T, H_q, 128] (same dtype as q)."""
     import numpy as np
 
     lib = load()
     ql = np.ascontiguousarray(np.asarray(q_len, dtype=np.int32))
-    cl = np.ascontiguousarray(ctx_len.cpu().numpy().astype(np.int32) if torch.is_tensor(ctx_len)
-                              else np.asarray(ctx_len, dtype=np.int32))
+    cl = np.ascontiguousarray(np.asarray(ctx_len, dtype=np.int32))
     B = len(ql)
     H_q = q.shape[1]
     ip = C.POINTER(C.c_int32)
-    nbytes = C.c_int64()
-    st = lib.bs_unified_attention_workspace(B, cl.ctypes.data_as(ip), ql.ctypes.data_as(ip), H_q, H_kv,
-                                            C.byref(nbytes))
-    if st != 0:
-        raise BubbleSpecError(st, "bs_unified_attention_workspace", "")
-    if workspace is None or workspace.numel() < nbytes.value:
-        workspace = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device=q.device)
+    if workspace is None:
+        workspace = torch.empty(max(1, unified_attention_workspace_bytes(cl, ql, H_q, H_kv)), dtype=torch.uint8,
+                                device=q.device)
     if out is None:
         out = torch.empty_like(q)
-    cl_dev = torch.from_numpy(cl).to(q.device)
     st = lib.bs_unified_attention(_p(q), _p(k_cache), _p(v_cache), k_cache.shape[0], _p(page_table),
-                                  page_table.shape[1], _p(cl_dev), cl.ctypes.data_as(ip), ql.ctypes.data_as(ip), B,
-                                  H_q, H_kv, q.shape[2], k_cache.shape[2], scale, _p(out), _p(workspace),
+                                  page_table.shape[1], _p(ctx_len_dev), cl.ctypes.data_as(ip), ql.ctypes.data_as(ip),
+                                  B, H_q, H_kv, q.shape[2], k_cache.shape[2], scale, _p(out), _p(workspace),
                                   workspace.numel(), _stream(stream, q.device.index))
     if st != 0:
         raise BubbleSpecError(st, "bs_unified_attention", "")

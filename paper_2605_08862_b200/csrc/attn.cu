@@ -43,12 +43,12 @@ constexpr int AT_TILE = 128;     // keys per tile (two pages)
 constexpr int AT_ROWS = 128;     // MMA M
 constexpr int AT_NT = 320;       // warps 0-7 softmax (two column groups), 8 TMA, 9 MMA
 constexpr int AT_NSM = 256;      // softmax threads
-constexpr int AT_STAGES = 2;
+constexpr int AT_KST = 2;  // K ring (a K tile is free once S = Q K^T completed)
+constexpr int AT_VST = 3;  // V ring (a V tile is free once O += P V completed: later)
 constexpr int AT_SPLIT_TILES = 16;  // tiles per work unit (2048 keys)
 constexpr uint32_t AT_HALF = AT_ROWS * 128;          // one [128 rows][64 bf16] swizzled block: 16 KB
 constexpr uint32_t AT_OP = 2 * AT_HALF;              // a 128 x 128 bf16 operand: 32 KB
-constexpr uint32_t AT_STAGE_BYTES = 2 * AT_OP;       // K + V tile
-constexpr size_t AT_SMEM = 1024 /*align*/ + 2 * AT_OP /*Q, P*/ + AT_STAGES * AT_STAGE_BYTES + 256;
+constexpr size_t AT_SMEM = 1024 /*align*/ + (2 /*Q, P*/ + AT_KST + AT_VST) * (size_t)AT_OP + 256;
 
 struct AttnUnit {
     int32_t b, h, t0, t1;
@@ -138,6 +138,23 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, float* v) {
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+        ::"r"(taddr), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+          "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]),
+          "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]),
+          "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ex2(float x) {  // MUFU.EX2 (P is rounded to bf16 afterwards)
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Shared-memory matrix descriptor (tcgen05), 128-byte swizzle: start, leading / stride byte
 // offsets (16-byte units), version 1, layout type 2 (SWIZZLE_128B).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -165,30 +182,38 @@ unified_attn_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
     uint8_t* smem = at_smem_raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-byte aligned (swizzle atoms)
     uint8_t* Qs = smem;
     uint8_t* Ps = smem + AT_OP;
-    uint8_t* KV = smem + 2 * AT_OP;  // stage s: K at s * STAGE, V at s * STAGE + OP
-    uint64_t* bars = reinterpret_cast<uint64_t*>(KV + AT_STAGES * AT_STAGE_BYTES);
-    uint64_t* kv_full = bars;             // [2]
-    uint64_t* kv_empty = bars + 2;        // [2]
-    uint64_t* s_full = bars + 4;
-    uint64_t* p_full = bars + 5;
-    uint64_t* o_full = bars + 6;
-    uint64_t* q_full = bars + 7;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    uint8_t* Ks = smem + 2 * AT_OP;           // K stage s at s * OP
+    uint8_t* Vs = Ks + AT_KST * AT_OP;        // V stage s at s * OP
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Vs + AT_VST * AT_OP);
+    uint64_t* k_full = bars;                  // [AT_KST]
+    uint64_t* k_empty = bars + AT_KST;        // [AT_KST]
+    uint64_t* v_full = bars + 2 * AT_KST;     // [AT_VST]
+    uint64_t* v_empty = v_full + AT_VST;      // [AT_VST]
+    uint64_t* s_full = v_empty + AT_VST;      // [2]: S double-buffered in TMEM
+    uint64_t* p_full = s_full + 2;
+    uint64_t* o_full = s_full + 3;
+    uint64_t* q_full = s_full + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < AT_STAGES; ++s) {
-            at_mbar_init(kv_full + s, 1);
-            at_mbar_init(kv_empty + s, 1);
+        for (int s = 0; s < AT_KST; ++s) {
+            at_mbar_init(k_full + s, 1);
+            at_mbar_init(k_empty + s, 1);
+        }
+        for (int s = 0; s < AT_VST; ++s) {
+            at_mbar_init(v_full + s, 1);
+            at_mbar_init(v_empty + s, 1);
         }
         at_mbar_init(s_full, 1);
+        at_mbar_init(s_full + 1, 1);
         at_mbar_init(p_full, AT_NSM);
         at_mbar_init(o_full, 1);
         at_mbar_init(q_full, AT_NSM);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 9) {  // TMEM: S in columns [0, 128), O_t in [128, 256)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;"
+    if (warp == 9) {  // TMEM: S in columns [0, 128) and [128, 256) (alternating tiles), O in [256, 384)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
                      ::"r"(smem_u32(tmem_slot)) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -207,24 +232,32 @@ unified_attn_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
                 const int ctx = a.ctx_len[un.b];
                 const int npg = (ctx + AT_PAGE - 1) / AT_PAGE;
                 for (int t = un.t0; t < un.t1; ++t, ++it) {
-                    const int s = it % AT_STAGES;
-                    if (it >= AT_STAGES) at_wait(kv_empty + s, ((it / AT_STAGES) - 1) & 1);
-                    at_arrive_tx(kv_full + s, AT_STAGE_BYTES);
-                    uint8_t* Kt = KV + s * AT_STAGE_BYTES;
-                    uint8_t* Vt = Kt + AT_OP;
+                    const int ks = it % AT_KST, vs = it % AT_VST;
+                    long long row[2];
 #pragma unroll
                     for (int pg = 0; pg < 2; ++pg) {
                         const int pi = 2 * t + pg;
                         // a page past the context: rows beyond the tensor map -> TMA zero fill
-                        const long long row = (pi < npg)
+                        row[pg] = (pi < npg)
                             ? ((long long)a.page_table[(long long)un.b * a.max_pages + pi] * a.H_kv + un.h) * AT_PAGE
                             : a.kv_rows;
-#pragma unroll
-                        for (int hf = 0; hf < 2; ++hf) {
-                            tma_load_2d(Kt + hf * AT_HALF + pg * (AT_PAGE * 128), &kmap, hf * 64, (int)row, kv_full + s);
-                            tma_load_2d(Vt + hf * AT_HALF + pg * (AT_PAGE * 128), &vmap, hf * 64, (int)row, kv_full + s);
-                        }
                     }
+                    if (it >= AT_KST) at_wait(k_empty + ks, ((it / AT_KST) - 1) & 1);
+                    at_arrive_tx(k_full + ks, AT_OP);
+#pragma unroll
+                    for (int pg = 0; pg < 2; ++pg)
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf)
+                            tma_load_2d(Ks + ks * AT_OP + hf * AT_HALF + pg * (AT_PAGE * 128), &kmap, hf * 64,
+                                        (int)row[pg], k_full + ks);
+                    if (it >= AT_VST) at_wait(v_empty + vs, ((it / AT_VST) - 1) & 1);
+                    at_arrive_tx(v_full + vs, AT_OP);
+#pragma unroll
+                    for (int pg = 0; pg < 2; ++pg)
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf)
+                            tma_load_2d(Vs + vs * AT_OP + hf * AT_HALF + pg * (AT_PAGE * 128), &vmap, hf * 64,
+                                        (int)row[pg], v_full + vs);
                 }
             }
         }
@@ -232,50 +265,66 @@ unified_attn_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
         // ================================================================ MMA issuer
         const uint32_t id1 = f16_idesc(AT_TILE, false), id2 = f16_idesc(AT_D, true);
         const uint32_t qa = smem_u32(Qs), pa = smem_u32(Ps);
+        // O_t = P V for tile j (its P is in smem once p_full completes), then release the stage
+        auto mma2 = [&](int j, bool acc_prev) {
+            at_wait(v_full + j % AT_VST, (j / AT_VST) & 1);
+            at_wait(p_full, j & 1);
+            tc_fence_after();
+            const uint32_t va = smem_u32(Vs + (j % AT_VST) * AT_OP);
+            if (lane == 0) {
+#pragma unroll
+                for (int kk = 0; kk < AT_TILE / 16; ++kk) {  // K dimension = keys
+                    const uint32_t aoff = (uint32_t)(kk >> 2) * AT_HALF + (uint32_t)(kk & 3) * 32u;
+                    // V: MN-major (d contiguous), 16 keys = 2048 bytes; d-halves 16 KB apart
+                    tc_mma(tmem + 256, sw128_desc(pa + aoff, 16, 1024), sw128_desc(va + kk * 2048u, AT_HALF, 1024),
+                           id2, (acc_prev || kk > 0) ? 1u : 0u);  // O accumulates in TMEM over the unit
+                }
+                tc_commit(o_full);
+                tc_commit(v_empty + j % AT_VST);
+            }
+            __syncwarp();
+        };
         int it = 0, uq = 0;
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uq) {
             const AttnUnit un = a.units[u];
             at_wait(q_full, uq & 1);  // this unit's Q rows are in smem
             tc_fence_after();
             for (int t = un.t0; t < un.t1; ++t, ++it) {
-                const int s = it % AT_STAGES;
-                at_wait(kv_full + s, (it / AT_STAGES) & 1);
+                // S(t) = Q K^T into the S buffer of tile parity: issued before the previous tile's
+                // P V, so it runs while the softmax warps still work on the previous tile
+                const int ks = it % AT_KST;
+                at_wait(k_full + ks, (it / AT_KST) & 1);
                 tc_fence_after();
-                const uint32_t ka = smem_u32(KV + s * AT_STAGE_BYTES), va = ka + AT_OP;
+                const uint32_t ka = smem_u32(Ks + ks * AT_OP);
                 if (lane == 0) {
 #pragma unroll
-                    for (int kk = 0; kk < AT_D / 16; ++kk) {  // S = Q K^T: K dimension = d
+                    for (int kk = 0; kk < AT_D / 16; ++kk) {  // K dimension = d
                         const uint32_t off = (uint32_t)(kk >> 2) * AT_HALF + (uint32_t)(kk & 3) * 32u;
-                        tc_mma(tmem, sw128_desc(qa + off, 16, 1024), sw128_desc(ka + off, 16, 1024), id1, kk > 0);
+                        tc_mma(tmem + (it & 1) * 128, sw128_desc(qa + off, 16, 1024), sw128_desc(ka + off, 16, 1024),
+                               id1, kk > 0);
                     }
-                    tc_commit(s_full);
+                    tc_commit(s_full + (it & 1));
+                    tc_commit(k_empty + ks);
                 }
                 __syncwarp();
-                at_wait(p_full, it & 1);  // P (bf16) written by the softmax warps
-                tc_fence_after();
-                if (lane == 0) {
-#pragma unroll
-                    for (int kk = 0; kk < AT_TILE / 16; ++kk) {  // O_t = P V: K dimension = keys
-                        const uint32_t aoff = (uint32_t)(kk >> 2) * AT_HALF + (uint32_t)(kk & 3) * 32u;
-                        // V: MN-major (d contiguous), 16 keys = 2048 bytes; d-halves 16 KB apart
-                        tc_mma(tmem + 128, sw128_desc(pa + aoff, 16, 1024), sw128_desc(va + kk * 2048u, AT_HALF, 1024),
-                               id2, kk > 0);
-                    }
-                    tc_commit(o_full);
-                    tc_commit(kv_empty + s);
-                }
-                __syncwarp();
+                if (t > un.t0) mma2(it - 1, t - 1 > un.t0);
             }
+            mma2(it - 1, un.t1 - 1 > un.t0);
         }
     } else {
         // ================================================================ softmax / correction
         // Two column groups share each row (warps w and w + 4 see the same TMEM lanes): group
-        // grp writes P for keys [64 grp, 64 grp + 64) and keeps O columns [64 grp, 64 grp + 64)
-        // in registers; both compute the row max over all 128 keys (same m, same alpha).
+        // grp reads S columns / writes P for keys [64 grp, 64 grp + 64) and owns O columns
+        // [64 grp, 64 grp + 64); the two halves of the row max meet in shared memory.  O
+        // accumulates in TMEM across the unit's tiles (MMA accumulate); the running max used for
+        // the exponent is raised only when the true max exceeds it by more than 2^8 (then O and
+        // l are rescaled in place), so most tiles touch O not at all.
         __shared__ float l_other[AT_ROWS];
+        __shared__ float pmax[2][AT_ROWS];
         const int grp = warp >> 2;
         const int r = (warp & 3) * 32 + lane;  // row = TMEM lane
         const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        constexpr float RESCALE = 8.f;  // log2 headroom of the stale max
         int it = 0, uq = 0;
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uq) {
             const AttnUnit un = a.units[u];
@@ -284,6 +333,7 @@ unified_attn_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
             const int nrows = ql * a.G;
             const int qi = r / a.G, g = r - qi * a.G;
             const int pos = ctx - ql + qi;  // absolute position of this row's query token
+            const int full_below = ctx - ql;  // keys < = this are visible to every row
             // this group's half of the Q row -> swizzled smem (zero padding rows); the previous
             // unit's MMAs are complete
             {
@@ -297,89 +347,108 @@ unified_attn_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             at_arrive(q_full);
-            float o[AT_D / 2];
-#pragma unroll
-            for (int j = 0; j < AT_D / 2; ++j) o[j] = 0.f;
             float m = -INFINITY, l = 0.f;
             for (int t = un.t0; t < un.t1; ++t, ++it) {
-                at_wait(s_full, it & 1);
+                at_wait(s_full + (it & 1), (it >> 1) & 1);
                 tc_fence_after();
-                // logits of this tile in the exp2 domain, causal + context mask; two passes over
-                // the TMEM row (max, then exp / P / sum) keep 32 logits in registers at a time
-                const int key0 = t * AT_TILE;
-                float mt = -INFINITY;
+                const uint32_t srow = trow + (it & 1) * 128;
+                const int key0 = t * AT_TILE + grp * 64;
+                const bool edge = t * AT_TILE + AT_TILE - 1 > full_below;  // uniform over the CTA
+                float sv[64];
+                tc_ld32(srow + grp * 64, sv);
+                tc_ld32(srow + grp * 64 + 32, sv + 32);
+                float mx = -INFINITY;
+                if (edge) {
 #pragma unroll
-                for (int c4 = 0; c4 < AT_TILE / 32; ++c4) {
-                    float sv[32];
-                    tc_ld32(trow + c4 * 32, sv);
+                    for (int j = 0; j < 64; ++j) {
+                        if (key0 + j > pos || key0 + j >= ctx) sv[j] = -INFINITY;
+                        mx = fmaxf(mx, sv[j]);
+                    }
+                } else {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int key = key0 + c4 * 32 + j;
-                        if (key <= pos && key < ctx) mt = fmaxf(mt, sv[j] * a.c);
+                    for (int j = 0; j < 64; ++j) mx = fmaxf(mx, sv[j]);
+                }
+                pmax[grp][r] = mx;
+                asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");  // the row's two warps
+                mx = fmaxf(mx, pmax[grp ^ 1][r]) * a.c;  // (c > 0)
+                bool rescale = false;
+                float alpha = 1.f;
+                if (m == -INFINITY) {
+                    m = mx;  // first visible keys of this row in the unit (O holds only zeros)
+                } else if (mx > m + RESCALE) {
+                    alpha = ex2(m - mx);
+                    rescale = true;
+                    m = mx;
+                    l *= alpha;
+                }
+                // the previous tile's P V has landed in O (and no longer reads P): rescale O if
+                // needed, then overwrite P
+                if (t > un.t0) {  // the previous tile's P V has landed in O: rescale it if needed
+                    at_wait(o_full, (it - 1) & 1);
+                    tc_fence_after();
+                    if (__any_sync(0xFFFFFFFFu, rescale)) {  // (tcgen05.ld/st are warp-collective)
+#pragma unroll
+                        for (int c2 = 0; c2 < 2; ++c2) {
+                            float ov[32];
+                            tc_ld32(trow + 256 + grp * 64 + c2 * 32, ov);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) ov[j] *= alpha;
+                            tc_st32(trow + 256 + grp * 64 + c2 * 32, ov);
+                        }
                     }
                 }
-                const float mn = fmaxf(m, mt);
-                const float alpha = (mn == -INFINITY) ? 1.f : exp2f(m - mn);
+                const float mneg = -m;
+                const bool live = m != -INFINITY;
                 float lt = 0.f;
 #pragma unroll
-                for (int c2 = 0; c2 < 2; ++c2) {
-                    const int c4 = grp * 2 + c2;
-                    float sv[32];
-                    tc_ld32(trow + c4 * 32, sv);
+                for (int j = 0; j < 64; j += 8) {  // P -> bf16, 16-byte swizzled stores
+                    uint32_t w[4];
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {  // P -> bf16, 16-byte swizzled stores
-                        uint32_t w[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int key = key0 + c4 * 32 + j + 2 * e;
-                            const bool ok0 = key <= pos && key < ctx, ok1 = key + 1 <= pos && key + 1 < ctx;
-                            const float p0 = ok0 ? exp2f(fmaf(sv[j + 2 * e], a.c, -mn)) : 0.f;
-                            const float p1 = ok1 ? exp2f(fmaf(sv[j + 2 * e + 1], a.c, -mn)) : 0.f;
-                            const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
-                            // the sum uses the bf16 values the MMA multiplies (P and l consistent)
-                            lt += __low2float(pb) + __high2float(pb);
-                            w[e] = *reinterpret_cast<const uint32_t*>(&pb);
-                        }
-                        *reinterpret_cast<uint4*>(Ps + sw_off(r, c4 * 32 + j)) = make_uint4(w[0], w[1], w[2], w[3]);
+                    for (int e = 0; e < 4; ++e) {
+                        const float p0 = live ? ex2(fmaf(sv[j + 2 * e], a.c, mneg)) : 0.f;
+                        const float p1 = live ? ex2(fmaf(sv[j + 2 * e + 1], a.c, mneg)) : 0.f;
+                        const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+                        // the sum uses the bf16 values the MMA multiplies (P and l consistent)
+                        const float2 pf = __bfloat1622float2(pb);
+                        lt += pf.x + pf.y;
+                        w[e] = *reinterpret_cast<const uint32_t*>(&pb);
                     }
+                    *reinterpret_cast<uint4*>(Ps + sw_off(r, grp * 64 + j)) = make_uint4(w[0], w[1], w[2], w[3]);
                 }
+                l += lt;
                 // keys past the context in this tile: zero their V rows (the cache may hold
-                // anything there; 0 * NaN would poison O).  Row r of the tile = key key0 + r;
-                // group grp zeroes d-half grp.
-                if (key0 + AT_TILE > ctx && key0 + r >= ctx) {
-                    at_wait(kv_full + it % AT_STAGES, (it / AT_STAGES) & 1);  // (landed: MMA1 waited on it)
-                    uint8_t* Vt = KV + (it % AT_STAGES) * AT_STAGE_BYTES + AT_OP + grp * AT_HALF;
+                // anything there; 0 * NaN would poison O).  Row r of the tile = key
+                // t * 128 + r; group grp zeroes d-half grp.
+                if (t * AT_TILE + AT_TILE > ctx && t * AT_TILE + r >= ctx) {
+                    at_wait(v_full + it % AT_VST, (it / AT_VST) & 1);  // V(t) has landed
+                    uint8_t* Vt = Vs + (it % AT_VST) * AT_OP + grp * AT_HALF;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(Vt + r * 128 + c * 16) = make_uint4(0, 0, 0, 0);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 tc_fence_before();
                 at_arrive(p_full);
-                l = l * alpha + lt;
-                m = mn;
-                at_wait(o_full, it & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int c2 = 0; c2 < 2; ++c2) {
-                    float ov[32];
-                    tc_ld32(trow + 128 + grp * 64 + c2 * 32, ov);
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) o[c2 * 32 + j] = fmaf(o[c2 * 32 + j], alpha, ov[j]);
-                }
-                tc_fence_before();
             }
+            at_wait(o_full, (it - 1) & 1);  // the unit's last P V
+            tc_fence_after();
             // the row sum is split over the two groups' keys
             if (grp == 1) l_other[r] = l;
             asm volatile("bar.sync 1, %0;" ::"n"(AT_NSM) : "memory");
-            if (r < nrows) {
-                float4* dst = reinterpret_cast<float4*>(a.part_o + ((long long)u * AT_ROWS + r) * AT_D + grp * 64);
+            {
+                float ov[64];  // (warp-collective loads, then the row's own stores)
+                tc_ld32(trow + 256 + grp * 64, ov);
+                tc_ld32(trow + 256 + grp * 64 + 32, ov + 32);
+                if (r < nrows) {
+                    float4* dst = reinterpret_cast<float4*>(a.part_o + ((long long)u * AT_ROWS + r) * AT_D + grp * 64);
 #pragma unroll
-                for (int j = 0; j < AT_D / 8; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-                if (grp == 0) {
-                    a.part_ml[((long long)u * AT_ROWS + r) * 2] = m;
-                    a.part_ml[((long long)u * AT_ROWS + r) * 2 + 1] = l + l_other[r];
+                    for (int j = 0; j < 16; ++j) dst[j] = make_float4(ov[4 * j], ov[4 * j + 1], ov[4 * j + 2], ov[4 * j + 3]);
+                    if (grp == 0) {
+                        a.part_ml[((long long)u * AT_ROWS + r) * 2] = m;
+                        a.part_ml[((long long)u * AT_ROWS + r) * 2 + 1] = l + l_other[r];
+                    }
                 }
             }
+            tc_fence_before();
             asm volatile("bar.sync 1, %0;" ::"n"(AT_NSM) : "memory");  // l_other reused next unit
         }
     }
@@ -387,7 +456,7 @@ unified_attn_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
     __syncthreads();
     if (warp == 9) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
     __threadfence();
     pdl_trigger();

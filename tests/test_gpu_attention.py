@@ -35,7 +35,7 @@ def _run(bs, b, poison_tail=False):
         vc[~used] = 0x7FC0
     q = to_dev(b.q.view(np.int16))
     out = bs.bs_unified_attention(q, to_dev(kc.view(np.int16)), to_dev(vc.view(np.int16)), to_dev(b.page_table),
-                                  to_dev(b.ctx_len), list(np.diff(b.q_off)), b.H_kv)
+                                  to_dev(b.ctx_len), b.ctx_len, list(np.diff(b.q_off)), b.H_kv)
     torch.cuda.synchronize()
     return bf16_bits_to_f32(out.cpu().numpy().view(np.uint16)).astype(np.float64)
 
