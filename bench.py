@@ -191,7 +191,8 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
     bank = torch.empty((cfg["nbank"], V), dtype=torch.int16, device=dev)
     bs.bsx_synth_bank(bank, cfg["nbank"], V, spec.bank_seed, spec.beta, stream=stream)
     eng = RolloutEngine(ctx, n, k, cfg["T"], cfg["top_p"],
-                        Target(bank, cfg["nbank"], spec.target_seed, TARGET_MODES[spec.mode]), stream=stream)
+                        Target(bank, cfg["nbank"], spec.target_seed, TARGET_MODES[spec.mode]), stream=stream,
+                        plain=cfg.get("plain", False))
     comm = nccl_comm(bs, dist, rank, world)
 
     def dev_t(a):
@@ -212,7 +213,7 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
             graph.append(eng.capture(chunk))  # (runs one real, eager decoding step first)
         return graph[0]
 
-    flags = [torch.zeros(1, dtype=torch.bool).pin_memory() for _ in range(2)]
+    flags = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2)]
     flag_ev = [torch.cuda.Event() for _ in range(2)]
 
     def replay_until_done(g, first=None):
@@ -230,12 +231,13 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
             steps_ += chunk
             c = 0
             while True:
-                flags[c % 2].copy_(eng.finished.all().view(1), non_blocking=True)
+                # live rollouts after chunk c (0: all finished), read while chunk c+1 runs
+                flags[c % 2].copy_((eng.finished == 0).sum().view(1).to(torch.int32), non_blocking=True)
                 flag_ev[c % 2].record(stream)
                 g.replay()
                 steps_ += chunk
                 flag_ev[c % 2].synchronize()
-                if bool(flags[c % 2][0]):
+                if int(flags[c % 2][0]) == 0:
                     break
                 c += 1
         return steps_
@@ -512,6 +514,19 @@ def args_steps(args, name):
 
 
 EXTRA_STEPS = (3, 2)  # (warm-up, timed) RL steps of the extra TINY / LC lines
+SWEEP_STEPS = (1, 1)  # (warm-up, timed) RL steps of each acceptance-sweep point
+
+
+def sweep_configs():
+    """BASELINE.json configs[4] ("acceptance sweep: draft match rate 0-90%, k in {2,4,8,16} ...
+    vs plain decoding"), at one GPU on a shortened Q7 workload (mean length 1024): k in
+    {2, 4, 8, 16} at match rate 0.8, match rate in {0, 0.5, 0.95} at k = 8, and plain decoding
+    (no drafts: one sample per decoding step)."""
+    base = dict(CONFIGS["q7"], mean_len=1024, cap=8192)
+    pts = [("k%d_r0.8" % k, dict(base, k=k)) for k in (2, 4, 8, 16)]
+    pts += [("k8_r%g" % r, dict(base, match_rate=r)) for r in (0.0, 0.5, 0.95)]
+    pts.append(("plain", dict(base, k=8, plain=True)))
+    return pts
 
 
 def workload_str(name, cfg):
@@ -533,6 +548,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the TINY / LC lines")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the acceptance sweep (configs[4])")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -579,6 +595,23 @@ def main():
         for name in ("tiny", "lc"):
             extra[name] = (CONFIGS[name], run_ours(args, CONFIGS[name], rank, world, dist, *EXTRA_STEPS,
                                                    e2e=False))
+    f_rows = {}
+    if args.config == "q7" and not args.no_extra and rank == 0:
+        # the NEXT rows of SURVEY §8(f) on this GPU: f2 unified attention (the paper's Table 2
+        # setting) and f1 bubble pre-generation (virtual DP ranks); scripts/ hold the drivers
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import attn_bench
+        import bubble_pregen
+
+        f_rows["unified_attention"] = attn_bench.main(["--iters", "10"], quiet=True)
+        summ, rep = bubble_pregen.main(["--steps", "3"], quiet=True)
+        f_rows["bubble_pregen"] = dict(summ, steps=[{k2: v for k2, v in r_.items() if k2 in (
+            "rl_step", "step_ms", "bubble_frac", "acceptance_length", "mean_decode_steps_per_rollout",
+            "slowest_rank_decode_steps", "pregen_tokens")} for r_ in rep])
+    sweep = []
+    if args.config == "q7" and not args.no_sweep and not args.no_extra:
+        for name, c in sweep_configs():
+            sweep.append((name, c, run_ours(args, c, rank, world, dist, *SWEEP_STEPS, e2e=False)))
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -612,6 +645,22 @@ def main():
                         "draft_length": r2["st"]["draft_length"], "tokens": int(r2["agg"]["tokens"]),
                         "roofline_frac": s2["frac"], "steady_frac": s2["steady_frac"],
                         "hbm_gbs": {"algorithmic": s2["achieved"], "steady_algorithmic": s2["steady"]}}
+    sweep_out = []
+    plain_steps = None
+    for name, c2, r2 in sweep:
+        s2 = summarize(c2, name, r2, args, hbm)
+        s2["ms_per_step"] = r2["agg"]["elapsed_ms"] / SWEEP_STEPS[1]
+        rec2 = {"point": name, "k": c2["k"], "match_rate": c2["match_rate"], "plain": c2.get("plain", False),
+                "value": s2["value"], "unit": unit, "ms_per_rl_step": s2["ms_per_step"],
+                "acceptance_length": r2["st"]["acceptance_length"],
+                "decode_steps_per_rollout": r2["st"]["decode_steps"] / r2["n"],
+                "roofline_frac": s2["frac"], "steady_frac": s2["steady_frac"]}
+        if c2.get("plain"):
+            plain_steps = rec2["decode_steps_per_rollout"]
+        sweep_out.append(rec2)
+    for rec2 in sweep_out:
+        if plain_steps:
+            rec2["decode_step_reduction_vs_plain"] = 1 - rec2["decode_steps_per_rollout"] / plain_steps
     out = {
         "metric": metric, "value": sm["value"], "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sm["ms_per_step"], "higher_is_better": True,
@@ -644,6 +693,10 @@ def main():
         "cpu_baseline": cpu,
         "parity": parity,
         "other_configs": others,
+        "next_rows": f_rows or None,
+        "sweep": {"workload": "BASELINE.json configs[4] at 1 GPU: q7 shape with mean length 1024 (cap 8192), "
+                              "1 warm-up + 1 timed RL step per point; plain = no drafts",
+                  "points": sweep_out} if sweep_out else None,
     }
     print(json.dumps(out), flush=True)
     if dist is not None:

@@ -28,7 +28,7 @@ import paper_2605_08862_b200 as bs  # noqa: E402
 PAGE, D = 64, 128
 
 
-def main():
+def main(argv=None, quiet=False):
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--spec", type=int, default=32, help="speculative requests")
@@ -37,7 +37,7 @@ def main():
     ap.add_argument("--heads", default="28,4", help="H_q,H_kv (Qwen2.5-7B 28,4; Qwen3-8B 32,8)")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    a = ap.parse_args()
+    a = ap.parse_args(argv)
     H_q, H_kv = (int(x) for x in a.heads.split(","))
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -123,7 +123,9 @@ def main():
     res["paper"] = {"normal_ms": 0.372, "split_prefill_ms": 0.753, "split_decode_ms": 0.226, "unified_ms": 0.380,
                     "note": "P:229-231, unstated GPU/model: context only"}
     res["peak_gbs"] = hbm
-    print(json.dumps(res), flush=True)
+    if not quiet:
+        print(json.dumps(res), flush=True)
+    return res
 
 
 if __name__ == "__main__":

@@ -34,7 +34,7 @@ from paper_2605_08862_b200.engine import TARGET_MODES, RolloutEngine, Target  # 
 from workloads import TargetSpec, lognormal_lengths, prompt_tails  # noqa: E402
 
 
-def main():
+def main(argv=None, quiet=False):
     ap = argparse.ArgumentParser()
     ap.add_argument("--ranks", type=int, default=4)
     ap.add_argument("--prompts", type=int, default=4, help="prompts per rank")
@@ -46,7 +46,7 @@ def main():
     ap.add_argument("--poll", type=int, default=50)
     ap.add_argument("--chunk", type=int, default=64)
     ap.add_argument("--beta", type=float, default=15.75)
-    a = ap.parse_args()
+    a = ap.parse_args(argv)
     R, P, G, V, k, M = a.ranks, a.prompts, a.G, a.V, a.k, 32
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -171,18 +171,22 @@ def main():
                "verify_steps": vsteps, "plain_steps": sum(s_["plain_steps"] for s_ in stats),
                "pregen_tokens": pre_tokens, "tokens_per_s": tokens / (step_ms / 1e3)}
         report.append(rec)
-        print(json.dumps(rec), flush=True)
+        if not quiet:
+            print(json.dumps(rec), flush=True)
         for r in range(R):
             assert ctxs[r].bs_sync_status() == 0
     first, last = report[0], report[-1]
-    print(json.dumps({"summary": True, "ranks": R, "rollouts_per_rank": n, "mean_len": a.mean_len,
+    summary = {"summary": True, "ranks": R, "rollouts_per_rank": n, "mean_len": a.mean_len,
                       "decode_step_reduction_slowest_rank": 1 - last["slowest_rank_decode_steps"]
                       / first["slowest_rank_decode_steps"],
                       "decode_step_reduction_per_rollout": 1 - last["mean_decode_steps_per_rollout"]
                       / first["mean_decode_steps_per_rollout"],
                       "speedup_step_time": first["step_ms"] / last["step_ms"],
-                      "bubble_frac_step0": first["bubble_frac"]}), flush=True)
+                      "bubble_frac_step0": first["bubble_frac"]}
+    if not quiet:
+        print(json.dumps(summary), flush=True)
     sync.close()
+    return summary, report
 
 
 if __name__ == "__main__":
