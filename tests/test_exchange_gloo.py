@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _rank_pools(rank, world):
+def _rank_pools(rank, world, source="perturbed"):
     from workloads import TargetSpec, make_pools, prompt_tails
 
     spec = TargetSpec(V=1000, nbank=64)
@@ -29,10 +29,19 @@ def _rank_pools(rank, world):
     prompts = np.array([i * world + prod_for for i in range(3)], dtype=np.int64)
     tails = prompt_tails(5, prompts, 8, spec.V)
     lens = np.random.default_rng(rank).integers(0, 30, (3, 4))
+    if source == "pregen":
+        # f1: the responses this rank pre-generated in its bubble for the next prompts (4 per
+        # prompt, some empty: the synchronizer halted them early), as pool sequences
+        from paper_2605_08862_b200.pregen import pool_sequences
+
+        pid = np.repeat(prompts, 4).astype(np.int32)
+        trows = np.repeat(tails, 4, axis=0)
+        resp = np.random.default_rng(100 + rank).integers(0, spec.V, (12, 30)).astype(np.int32)
+        return pool_sequences(pid, trows, resp, lens.ravel(), M=8)
     return make_pools(spec, prompts, tails, 4, lens, 0.8, prefix=8)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, source="perturbed"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -41,7 +50,7 @@ def _worker(rank, world, port, q):
     try:
         from paper_2605_08862_b200 import bs_route_plan
 
-        sp, off, tok = _rank_pools(rank, world)
+        sp, off, tok = _rank_pools(rank, world, source)
         cnt = torch.tensor([len(sp), len(tok)], dtype=torch.int64)
         allc = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(allc, cnt)
@@ -70,14 +79,16 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_exchange_routing_world2():
+@pytest.mark.parametrize("source", ["perturbed", "pregen"])
+def test_exchange_routing_world2(source):
+    """source "pregen": the pools are f1's pre-generated responses (pregen.pool_sequences)."""
     import torch.multiprocessing as mp
 
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, source)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -89,7 +100,7 @@ def test_exchange_routing_world2():
         assert p.exitcode == 0
     produced = []
     for r in range(world):
-        sp, off, tok = _rank_pools(r, world)
+        sp, off, tok = _rank_pools(r, world, source)
         produced += [(int(P), tok[off[s]:off[s + 1]].tolist()) for s, P in enumerate(sp)]
     union = []
     for r in range(world):
