@@ -85,3 +85,37 @@ def test_paged_batch_gathers_each_requests_pages():
         assert np.array_equal(k, kk) and np.array_equal(v, vv)
         r0, r1 = int(b.q_off[r]), int(b.q_off[r + 1])
         np.testing.assert_array_equal(o[r0:r1], attention_request(b.q[r0:r1], k, v, 2))
+
+
+# ------------------------------------------------------------------ f3 LM-head logits oracle
+def test_lm_head_one_hot_weights_copy_the_hidden_state():
+    """W[v] = s_v * e_{v mod d}: logits[r, v] = bf16(s_v * h[r, v mod d]) exactly (one product,
+    no sum), including the round-to-nearest-even of the product."""
+    from oracle.lm_head import lm_head_logits
+
+    rng = np.random.default_rng(7)
+    rows, d, V = 5, 16, 48
+    h = _bits(rng.normal(size=(rows, d)))
+    scale = np.array([1.0, 3.0, -0.375, 2.0 ** -7] * (V // 4))
+    w = np.zeros((V, d))
+    w[np.arange(V), np.arange(V) % d] = scale
+    out = lm_head_logits(h, _bits(w))
+    want = f32_to_bf16_bits((bf16_bits_to_f32(h)[:, np.arange(V) % d].astype(np.float64) * scale).astype(np.float32))
+    np.testing.assert_array_equal(out, want)
+
+
+def test_lm_head_rne_tie_and_row_stats():
+    """A dot product landing exactly half-way between two bf16 values rounds to the even one;
+    row statistics: max, the lowest index attaining it, -inf is not an error, NaN / +inf are."""
+    from oracle.lm_head import lm_head_logits, row_stats
+
+    # 1 + 2^-8 is half-way between 1 and 1 + 2^-7: ties to even (1.0); 1 + 3*2^-8 -> 1 + 2^-6
+    h = _bits([[1.0, 2.0 ** -8]])
+    w = _bits([[1.0, 1.0], [1.0, 3.0]])
+    out = bf16_bits_to_f32(lm_head_logits(h, w))
+    assert out[0, 0] == 1.0 and out[0, 1] == 1.0 + 2.0 ** -6
+    m, am, bad = row_stats(_bits([[1.0, 5.0, 5.0, -np.inf], [-np.inf, -2.0, -np.inf, -3.0]]))
+    assert list(m) == [5.0, -2.0] and list(am) == [1, 1] and not bad.any()
+    nan_row = np.array([[0x3F80, 0x7FC0, 0x3F80]], dtype=np.uint16)
+    inf_row = np.array([[0x3F80, 0x7F80, 0x3F80]], dtype=np.uint16)
+    assert row_stats(nan_row)[2][0] and row_stats(inf_row)[2][0]
