@@ -602,8 +602,10 @@ def main():
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         import attn_bench
         import bubble_pregen
+        import lmhead_bench
 
         f_rows["unified_attention"] = attn_bench.main(["--iters", "10"], quiet=True)
+        f_rows["lm_head_fused_stats"] = lmhead_bench.main(["--rows", "256,2304", "--iters", "5"], quiet=True)
         summ, rep = bubble_pregen.main(["--steps", "3"], quiet=True)
         f_rows["bubble_pregen"] = dict(summ, steps=[{k2: v for k2, v in r_.items() if k2 in (
             "rl_step", "step_ms", "bubble_frac", "acceptance_length", "mean_decode_steps_per_rollout",

@@ -316,6 +316,23 @@ bs_status bs_unified_attention(const void* q, const void* k_cache, const void* v
                                int32_t head_dim, int32_t page_size, float scale, void* out, void* workspace,
                                int64_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------- LM head + fused row statistics (f3) */
+/* The target policy's logits from the last hidden states, on the tensor cores, with the
+ * verify's first pass fused into the GEMM epilogue:
+ *   logits[r, v] = bf16(sum_k h[r, k] * W[v, k])  (fp32 accumulation, round to nearest even)
+ *   row_key[r]   = (order key of max_v logits[r, v]) << 32 | (0xFFFFFFFF - lowest argmax)
+ *                  (order key of bf16 bits b: b | 0x8000 if b >= 0 else ~b & 0xFFFF; NaN excluded)
+ *   row_bad[r]   = 1 if a NaN or +inf logit occurred (reading R0)
+ * h [rows, d] and W [V, d] bf16 row-major (16-byte aligned), d a multiple of 64; logits row stride
+ * ld_logits >= V elements.  Errors: BS_ERR_INVALID, BS_ERR_CUDA. */
+bs_status bs_lm_head_logits(const void* h, const void* w, int32_t rows, int32_t d, int32_t V, void* logits,
+                            int64_t ld_logits, uint64_t* row_key, uint32_t* row_bad, void* stream);
+/* Give the verify launches of this ctx the row statistics of bs_lm_head_logits (indexed like the
+ * logits rows the verify reads); the cluster verify kernel then skips its max pass.  Results are
+ * identical (tested).  NULL, NULL clears.  The arrays must describe the logits of every verify call
+ * made while set. */
+bs_status bsx_set_row_stats(bs_ctx* ctx, const uint64_t* row_key, const uint32_t* row_bad);
+
 /* ---------------------------------------------------------------- tuning */
 /* Select the kernel bs_verify_step uses for rows without top-p (all compute identical
  * results): 0 auto (= 3 when ceil(V/8) <= 53248, else 1; env BS_VERIFY_KERNEL

@@ -7,6 +7,7 @@ from ._lib import LIB_PATH, BubbleSpecError, load  # noqa: F401
 from .api import (  # noqa: F401
     BubbleSync,
     Context,
+    bs_lm_head_logits,
     bs_route_plan,
     bs_unified_attention,
     bsx_synth_attn_values,

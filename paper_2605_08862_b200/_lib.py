@@ -62,6 +62,8 @@ SIGNATURES = {
     "bs_unified_attention": (C.c_int, [_V, _V, _V, _I64, _V, _I32, _V, _V, _V, _I32, _I32, _I32, _I32, _I32,
                                        C.c_float, _V, _V, _I64, _V]),
     "bsx_synth_attn_values": (C.c_int, [_V, _I64, _U32, C.c_float, _V]),
+    "bs_lm_head_logits": (C.c_int, [_V, _V, _I32, _I32, _I32, _V, _I64, _V, _V, _V]),
+    "bsx_set_row_stats": (C.c_int, [_V, _V, _V]),
     "bs_draft_lookup_ngram": (C.c_int, [_V, _U64, _I32, _V, _I32, _I32, _I32, _V, _V, _V, _V]),
     "bs_verify_commit": (C.c_int, [_V, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V, _V,
                                    _V, _V, _V, _V, _V]),

@@ -181,6 +181,9 @@ class Context:
     def bsx_set_early_plan(self, on: bool):
         _chk(self, load().bsx_set_early_plan(self.handle, int(bool(on))), "bsx_set_early_plan")
 
+    def bsx_set_row_stats(self, row_key=None, row_bad=None):
+        _chk(self, load().bsx_set_row_stats(self.handle, _p(row_key), _p(row_bad)), "bsx_set_row_stats")
+
     def bsx_set_max_clusters(self, max_clusters: int):
         _chk(self, load().bsx_set_max_clusters(self.handle, int(max_clusters)), "bsx_set_max_clusters")
 
@@ -329,3 +332,21 @@ def bsx_synth_attn_values(out, base: int, mult: float, stream=None):
     st = load().bsx_synth_attn_values(_p(out), out.numel(), base & 0xFFFFFFFF, mult,
                                       _stream(stream, out.device.index))
     _chk(None, st, "bsx_synth_attn_values")
+
+
+def bs_lm_head_logits(h, w, logits=None, row_key=None, row_bad=None, stream=None):
+    """LM-head logits with fused row statistics (bs_lm_head_logits).  h [rows, d], w [V, d]
+    (bf16, or int16 bf16 bits).  Returns (logits [rows, V] like h's dtype, row_key int64 [rows],
+    row_bad int32 [rows])."""
+    rows, d = h.shape
+    V = w.shape[0]
+    if logits is None:
+        logits = torch.empty((rows, V), dtype=h.dtype, device=h.device)
+    if row_key is None:
+        row_key = torch.empty(rows, dtype=torch.int64, device=h.device)
+    if row_bad is None:
+        row_bad = torch.empty(rows, dtype=torch.int32, device=h.device)
+    st = load().bs_lm_head_logits(_p(h), _p(w), rows, d, V, _p(logits), logits.stride(0), _p(row_key), _p(row_bad),
+                                  _stream(stream, h.device.index))
+    _chk(None, st, "bs_lm_head_logits")
+    return logits, row_key, row_bad

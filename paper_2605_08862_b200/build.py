@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbubblespec.so")
-SOURCES = ["api.cu", "verify.cu", "index.cu", "state.cu", "synth.cu", "exchange.cu", "ngram.cu", "bubble.cu", "attn.cu"]
+SOURCES = ["api.cu", "verify.cu", "index.cu", "state.cu", "synth.cu", "exchange.cu", "ngram.cu", "bubble.cu", "attn.cu", "lmhead.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -57,6 +57,13 @@ bs_status bsx_set_max_clusters(bs_ctx* c, int32_t max_clusters) {
     return BS_OK;
 }
 
+bs_status bsx_set_row_stats(bs_ctx* c, const uint64_t* row_key, const uint32_t* row_bad) {
+    if (!c || (!row_key) != (!row_bad)) return BS_ERR_INVALID;
+    c->rs_key = reinterpret_cast<const unsigned long long*>(row_key);
+    c->rs_bad = row_bad;
+    return BS_OK;
+}
+
 int32_t bsx_launch_info(const bs_ctx* c, int64_t* out, int32_t n) {
     if (!c || !out || n < 1) return 0;
     const int64_t v[4] = {c->kcfg_clusters, c->kcfg_coop, c->num_sms, c->early_plan};

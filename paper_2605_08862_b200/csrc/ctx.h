@@ -122,6 +122,8 @@ struct bs_ctx {
     int verify_kind = 0;  // bsx_set_verify_kernel (0: auto)
     int early_plan = 0;   // bsx_set_early_plan: the verify launch may plan before its PDL wait
     int max_clusters = 0; // bsx_set_max_clusters: cap on the cluster verify grid (0: all resident)
+    const unsigned long long* rs_key = nullptr;  // bsx_set_row_stats (LM-head epilogue row statistics)
+    const uint32_t* rs_bad = nullptr;
     // per-context (hence per-device) kernel launch setup, done once on this ctx's device:
     // dynamic shared memory attributes set, and the cluster kernel's resident cluster count
     size_t kcfg_cluster_smem = 0, kcfg_split_smem = 0;

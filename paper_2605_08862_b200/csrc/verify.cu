@@ -153,6 +153,10 @@ struct VerifyArgs {
     // the rollout's next draft from the committed state (lk.draft / draft_len: the next step's)
     int lookup;
     LookupArgs lk;
+    // row statistics precomputed by the LM-head epilogue (bsx_set_row_stats; cluster kernel):
+    // per logits row, (order key of the max << 32 | ~argmax) and a NaN / +inf flag
+    const unsigned long long* rs_key;
+    const uint32_t* rs_bad;
 };
 
 struct RowDesc {
@@ -996,6 +1000,8 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
         a.live = ctx->vlive.p;
         a.eager_ok = ctx->env_eager;
         a.early_plan = ctx->early_plan;
+        a.rs_key = ctx->rs_key;
+        a.rs_bad = ctx->rs_bad;
         if (committed) {  // fused commit (bs_verify_commit)
             a.commit = 1;
             a.M = ctx->M;

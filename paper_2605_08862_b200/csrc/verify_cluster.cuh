@@ -889,6 +889,25 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             // this CTA's epilogue is done with row i-4 (sum slot, tile sums): every peer's
             // row-i publish lands on completed phases of this CTA's rings
             if (i >= CK_D) mbar_wait(&sh.eempty[s], ((i / CK_D) - 1) & 1);
+            if (a.rs_key) {
+                // the LM-head epilogue already reduced this row (R0 / R1): publish its maximum,
+                // lowest argmax and NaN / +inf flag without reading the slice
+                if (xw == 0) {
+                    const long long rn = sh.dq[s].rowno;
+                    const unsigned long long kv = __ldg(a.rs_key + rn);
+                    const uint32_t kb = (uint32_t)(kv >> 32);
+                    const uint32_t bits = (kb & 0x8000u) ? (kb & 0x7FFFu) : (~kb & 0xFFFFu);
+                    const float sm = __uint_as_float(bits << 16);
+                    const uint32_t sb = (__ldg(a.rs_bad + rn) != 0u || kv == 0ull) ? 1u : 0u;
+                    const uint32_t sidx = (a.T == 0.f) ? (uint32_t)(0xFFFFFFFFull - (kv & 0xFFFFFFFFull)) : 0x7FFFFFFFu;
+                    if (lane == 0) mbar_arrive_expect_tx(&sh.maxbar[s], (uint32_t)(CK_CL * 16));
+                    __syncwarp();
+                    if (lane < CK_CL)
+                        st_async_v4(&sh.cmax[s][rank], make_uint4(__float_as_uint(sm), sb, sidx, 0u), &sh.maxbar[s],
+                                    (uint32_t)lane);
+                }
+                continue;
+            }
             mbar_wait(&sh.full[bi], (i / CK_NB) & 1);
             const bool xdead = __shfl_sync(0xFFFFFFFFu, rfx < jx ? 1 : 0, 0) != 0;
             if (xw == 0 && lane == 0) TRACE(TR_MAX0, i, 0, 0);
