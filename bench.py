@@ -254,8 +254,12 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
     D = cfg["M"] + k
     launches_rl = 1 + 4 + (4 + 9 * D) + 2
 
+    setup_ms = []
+
     def rl_step(s, rec, evs=None):
-        setup_step(s + 1, dins[s])
+        t_set = time.perf_counter()
+        setup_step(s + 1, dins[s])  # (the seal synchronises: host time covers the device work)
+        setup_ms.append((time.perf_counter() - t_set) * 1e3)
         g = capture()
         if evs:
             evs[0].record(stream)
@@ -320,6 +324,8 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
     end.record(stream)
     torch.cuda.synchronize(dev)
     log("[timed] decode ms per RL step: " + " ".join(f"{e[0].elapsed_time(e[1]):.1f}" for e in evs))
+    log("[timed] setup (put, exchange, seal, begin) host ms per RL step: "
+        + " ".join(f"{x:.1f}" for x in setup_ms[-len(evs):]))
     t_host1 = time.time()
     if dist is not None:
         dist.barrier()
