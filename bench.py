@@ -232,7 +232,7 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
             c = 0
             while True:
                 # live rollouts after chunk c (0: all finished), read while chunk c+1 runs
-                flags[c % 2].copy_((eng.finished == 0).sum().view(1).to(torch.int32), non_blocking=True)
+                flags[c % 2].copy_(eng.live_count(), non_blocking=True)
                 flag_ev[c % 2].record(stream)
                 g.replay()
                 steps_ += chunk

@@ -114,6 +114,10 @@ bs_status bs_rollout_begin(bs_ctx* ctx, int32_t n, const int32_t* slots, const u
 bs_status bs_rollout_state(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* pos,
                            int32_t* finished, void* stream);
 
+/* live[0] (device int32) = how many of slots[0..n) are not finished (one kernel; stream-ordered,
+ * graph-capturable): the caller's "all rollouts done?" check without a host-side reduction. */
+bs_status bs_rollout_live(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* live, void* stream);
+
 /* Bind (or unbind with NULL) a caller-owned device buffer [max_rollouts, stride]:
  * bs_commit then also writes every emitted token of slot s at responses[s*stride + t]
  * (t = generated-token index, t < stride), i.e. the rollout y of Alg. 1. */

@@ -42,6 +42,7 @@ SIGNATURES = {
     "bs_version": (C.c_char_p, []),
     "bs_rollout_begin": (C.c_int, [_V, _I32, _V, _V, _V, _V, _V, _V]),
     "bs_rollout_state": (C.c_int, [_V, _I32, _V, _V, _V, _V]),
+    "bs_rollout_live": (C.c_int, [_V, _I32, _V, _V, _V]),
     "bs_draft_pool_put": (C.c_int, [_V, _U64, _I32, _V, _V, _V, _I64, _V]),
     "bs_draft_pool_seal": (C.c_int, [_V, _U64, _V]),
     "bs_draft_exchange": (C.c_int, [_V, _V, _I32, _I32, _U64, _V]),

@@ -82,6 +82,10 @@ class Context:
                                            _p(prompt_tail), _p(max_len),
                                            _stream(stream, self.device)), "bs_rollout_begin")
 
+    def bs_rollout_live(self, slots, live, stream=None):
+        _chk(self, load().bs_rollout_live(self.handle, slots.numel(), _p(slots), _p(live),
+                                          _stream(stream, self.device)), "bs_rollout_live")
+
     def bs_rollout_state(self, slots, pos=None, finished=None, stream=None):
         _chk(self, load().bs_rollout_state(self.handle, slots.numel(), _p(slots), _p(pos),
                                            _p(finished), _stream(stream, self.device)),

@@ -233,6 +233,14 @@ bs_status bs_rollout_state(bs_ctx* c, int32_t n, const int32_t* slots, int32_t* 
     return BS_OK;
 }
 
+bs_status bs_rollout_live(bs_ctx* c, int32_t n, const int32_t* slots, int32_t* live, void* stream) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (n < 0 || n > c->cfg.max_rollouts || !live || (n && !slots)) return fail(c, BS_ERR_INVALID, "bad arguments");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    CK(c, launch_live_count(c, n, slots, live, S(stream)), "bs_rollout_live");
+    return BS_OK;
+}
+
 bs_status bs_draft_pool_put(bs_ctx* c, uint64_t rl_step, int32_t n_seqs, const int32_t* prompt_ids,
                             const int64_t* seq_offsets, const int32_t* tokens, int64_t n_tokens,
                             void* stream) {

@@ -197,6 +197,7 @@ cudaError_t launch_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const in
 cudaError_t launch_begin(bs_ctx* ctx, int32_t n, const int32_t* slots,
                          const unsigned long long* uids, const int32_t* prompt_ids,
                          const int32_t* tail, const int32_t* max_len, cudaStream_t st);
+cudaError_t launch_live_count(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* out, cudaStream_t st);
 cudaError_t launch_state(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* pos,
                          int32_t* finished, cudaStream_t st);
 cudaError_t launch_pool_append(bs_ctx* ctx, int32_t n_seqs, const int32_t* prompt_ids,

@@ -25,9 +25,15 @@
 
 namespace bs {
 
-constexpr int LM_BM = 128, LM_BN = 256, LM_BK = 64, LM_ST = 4, LM_NT = 192;
+#ifndef BS_LM_BN
+#define BS_LM_BN 256
+#endif
+#ifndef BS_LM_ST
+#define BS_LM_ST 4
+#endif
+constexpr int LM_BM = 128, LM_BN = BS_LM_BN, LM_BK = 64, LM_ST = BS_LM_ST, LM_NT = 192;
 constexpr uint32_t LM_ABYTES = LM_BM * LM_BK * 2;  // 16 KB
-constexpr uint32_t LM_BBYTES = LM_BN * LM_BK * 2;  // 32 KB
+constexpr uint32_t LM_BBYTES = LM_BN * LM_BK * 2;  // 32 KB at N = 256
 constexpr size_t LM_SMEM = 1024 + (size_t)LM_ST * (LM_ABYTES + LM_BBYTES) + 256;
 
 struct LmArgs {

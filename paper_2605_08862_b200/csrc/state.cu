@@ -79,6 +79,21 @@ __global__ void state_kernel(int n, const int32_t* slots, const int32_t* pos,
     if (fin_out) fin_out[b] = finished[s];
 }
 
+// Number of unfinished rollouts among slots[0..n) (one CTA; the host's per-chunk done check).
+__global__ void live_count_kernel(int n, const int32_t* slots, const int32_t* finished, int32_t* out) {
+    __shared__ int wsum[32];
+    int c = 0;
+    for (int b = threadIdx.x; b < n; b += blockDim.x) c += finished[slots[b]] == 0;
+    c = __reduce_add_sync(0xFFFFFFFFu, c);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int t = (threadIdx.x < (int)(blockDim.x >> 5)) ? wsum[threadIdx.x] : 0;
+        t = __reduce_add_sync(0xFFFFFFFFu, t);
+        if (threadIdx.x == 0) *out = t;
+    }
+}
+
 __global__ void pool_append_kernel(int n_seqs, int64_t n_tokens, const int32_t* prompt_ids,
                                    const int64_t* seq_off, const int32_t* tokens, int64_t base_tok,
                                    int base_seq, int32_t* dst_tokens, int64_t* dst_off,
@@ -117,6 +132,11 @@ cudaError_t launch_state(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* 
                          int32_t* finished, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     state_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, slots, ctx->pos.p, ctx->finished.p, pos, finished);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_live_count(bs_ctx* ctx, int32_t n, const int32_t* slots, int32_t* out, cudaStream_t st) {
+    live_count_kernel<<<1, 256, 0, st>>>(n, slots, ctx->finished.p, out);
     return cudaGetLastError();
 }
 

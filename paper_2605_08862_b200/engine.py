@@ -66,6 +66,7 @@ class RolloutEngine:
         self.out_len = torch.zeros(n, **i32)
         self.out_acc = torch.zeros(n, **i32)
         self.finished = torch.zeros(n, **i32)
+        self.live = torch.zeros(1, **i32)  # bs_rollout_live output
         self.rl_step = 0
         self.graph = None
         self.graph_steps = 0
@@ -146,9 +147,17 @@ class RolloutEngine:
         with torch.cuda.stream(self.stream):
             self.graph.replay()
 
+    def live_count(self):
+        """Enqueue bs_rollout_live on the engine stream; returns the device int32 [1] holding the
+        number of this engine's rollouts not yet finished."""
+        self.ctx.bs_rollout_live(self.slots, self.live, stream=self.stream)
+        return self.live
+
     def all_finished(self) -> bool:
         with torch.cuda.stream(self.stream):
-            return bool(self.finished.all().item())
+            live = self.live_count()
+            self.stream.synchronize()
+            return int(live.item()) == 0
 
     def run_until_done(self, max_steps: int = 1 << 20, chunk: int = 64, use_graph: bool = True):
         """Decode until every rollout finished (EOS or max_len); host checks once per chunk."""

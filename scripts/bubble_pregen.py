@@ -117,7 +117,7 @@ def main(argv=None, quiet=False):
                     with torch.cuda.stream(eng.stream):
                         eng.graph.replay()
                         main_steps[r] += a.chunk
-                        flags[r].copy_(eng.finished.all().view(1).int(), non_blocking=True)
+                        flags[r].copy_(eng.live_count(), non_blocking=True)  # live rollouts
                 elif state[r] == "pregen":
                     with torch.cuda.stream(pre.stream):
                         pre.graph.replay()
@@ -128,7 +128,7 @@ def main(argv=None, quiet=False):
                     continue
                 s = mains[r].stream
                 s.synchronize()
-                if state[r] == "main" and int(flags[r][0]):
+                if state[r] == "main" and int(flags[r][0]) == 0:  # the batch is done
                     t_done[r].record(s)
                     sync.arrive(r, step, stream=s)
                     pid, trows, ml = next_b[r]
