@@ -320,9 +320,8 @@ unified_attn_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
         // the exponent is raised only when the true max exceeds it by more than 2^8 (then O and
         // l are rescaled in place), so most tiles touch O not at all.
         __shared__ float l_other[AT_ROWS];
-        __shared__ float pmax[2][2][AT_ROWS];  // [tile parity][group][row]: a partner reads tile t's
-                                               // value before it reaches tile t+1's barrier, the
-                                               // writer reuses the slot only at tile t+2
+        __shared__ float pmax[2][AT_ROWS];  // [group][row]; a pair barrier before each write keeps
+                                            // the partner's read of the previous tile's value first
         const int grp = warp >> 2;
         const int r = (warp & 3) * 32 + lane;  // row = TMEM lane
         const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
@@ -370,9 +369,10 @@ unified_attn_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
 #pragma unroll
                     for (int j = 0; j < 64; ++j) mx = fmaxf(mx, sv[j]);
                 }
-                pmax[it & 1][grp][r] = mx;
+                asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");  // partner read the last one
+                pmax[grp][r] = mx;
                 asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");  // the row's two warps
-                mx = fmaxf(mx, pmax[it & 1][grp ^ 1][r]) * a.c;  // (c > 0)
+                mx = fmaxf(mx, pmax[grp ^ 1][r]) * a.c;  // (c > 0)
                 bool rescale = false;
                 float alpha = 1.f;
                 if (m == -INFINITY) {
