@@ -30,11 +30,11 @@ constexpr int TP_H1 = 4096;           // coarse key bins
 constexpr int TP_MAXT = 2048;         // 256-element tiles: V <= 524288
 
 struct TopPShared {
-    unsigned long long h1[TP_H1];
+    uint32_t h1lo[TP_H1], h1hi[TP_H1];  // coarse-bin masses (Hist64)
     uint32_t hc[TP_H1];       // top-k: positive-mass tokens per coarse bin
     uint32_t h2c[16];         // top-k: positive-mass tokens per key of the crossing bin
     unsigned long long tsum[TP_MAXT];
-    unsigned long long h2[16];
+    uint32_t h2lo[16], h2hi[16];        // masses of the 16 keys of the crossing bin (Hist64)
     unsigned long long stat[STAT_COUNT];
     float wmax[TP_NW];
     uint32_t wbad[TP_NW];
@@ -52,6 +52,25 @@ __device__ __forceinline__ uint32_t tp_unkey(uint32_t k) {
     return (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu);
 }
 
+// Shared-memory 64-bit histogram bins kept as two 32-bit words: an add is one native 32-bit
+// shared atomic on the low word plus, only when it carries or the value has high bits, one on the
+// high word (a 64-bit shared atomic add is far slower under contention).
+struct Hist64 {
+    uint32_t* lo;
+    uint32_t* hi;
+    __device__ __forceinline__ void add(uint32_t bin, uint64_t v) const {
+        const uint32_t vl = (uint32_t)v;
+        const uint32_t old = atomicAdd(lo + bin, vl);
+        const uint32_t h = (uint32_t)(v >> 32) + ((old + vl < old) ? 1u : 0u);
+        if (h) atomicAdd(hi + bin, h);
+    }
+    __device__ __forceinline__ uint64_t get(int bin) const { return ((uint64_t)hi[bin] << 32) | lo[bin]; }
+    __device__ __forceinline__ void clear(int bin) const {
+        lo[bin] = 0u;
+        hi[bin] = 0u;
+    }
+};
+
 // Lane's 8 consecutive logits of tile t (-inf beyond V / scalar path when unaligned).
 __device__ __forceinline__ uint4 tp_load8(const uint16_t* row, int e0, int V, bool aligned) {
     if (aligned && e0 + 8 <= V) return __ldcg(reinterpret_cast<const uint4*>(row + e0));
@@ -64,6 +83,32 @@ __device__ __forceinline__ uint4 tp_load8(const uint16_t* row, int e0, int V, bo
 __device__ __forceinline__ void tp_unpack(const uint4 v, uint32_t b[8]) {
     b[0] = v.x & 0xFFFFu; b[1] = v.x >> 16; b[2] = v.y & 0xFFFFu; b[3] = v.y >> 16;
     b[4] = v.z & 0xFFFFu; b[5] = v.z >> 16; b[6] = v.w & 0xFFFFu; b[7] = v.w >> 16;
+}
+
+// Stream the row tile by tile (warp w: tiles w, w + TP_NW, ...), TP_U tiles' loads issued
+// before any is consumed: one CTA per row, so the passes are bound by how many bytes each warp
+// keeps in flight (one 16-byte load per lane at a time was ~1 KB per warp: latency-bound).
+#ifndef BS_TP_U
+#define BS_TP_U 2
+#endif
+constexpr int TP_U = BS_TP_U;
+template <class F>
+__device__ __forceinline__ void tp_stream(const uint16_t* row, int ntile, int V, bool aligned, int warp, int lane,
+                                          F&& f) {
+    for (int t0 = warp; t0 < ntile; t0 += TP_NW * TP_U) {
+        uint4 v[TP_U];
+#pragma unroll
+        for (int u = 0; u < TP_U; ++u) {
+            const int t = t0 + u * TP_NW;
+            v[u] = (t < ntile) ? tp_load8(row, t * 256 + lane * 8, V, aligned)
+                               : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+        }
+#pragma unroll
+        for (int u = 0; u < TP_U; ++u) {
+            const int t = t0 + u * TP_NW;
+            if (t < ntile) f(t, v[u]);  // (warp-uniform)
+        }
+    }
 }
 
 __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs a, float top_p, int top_k) {
@@ -89,13 +134,12 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
 
         // ---------------------------------------------------- pass 1: max
         uint32_t mx = 0xFF80FF80u;
-        for (int t = warp; t < ntile; t += TP_NW) {
-            const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+        tp_stream(row, ntile, V, aligned, warp, lane, [&](int, const uint4 v) {
             mx = hmax2_nan_u32(mx, v.x);
             mx = hmax2_nan_u32(mx, v.y);
             mx = hmax2_nan_u32(mx, v.z);
             mx = hmax2_nan_u32(mx, v.w);
-        }
+        });
         {
             const float lo = bf16lo(mx), hi = bf16hi(mx);
             uint32_t bad = (isnan(lo) || isnan(hi) || lo == INFINITY || hi == INFINITY) ? 1u : 0u;
@@ -108,11 +152,12 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 sh.wbad[warp] = bad;
             }
         }
-        for (int i = tid; i < TP_H1; i += TP_NT) sh.h1[i] = 0ull;
+        const Hist64 H1{sh.h1lo, sh.h1hi}, H2{sh.h2lo, sh.h2hi};
+        for (int i = tid; i < TP_H1; i += TP_NT) H1.clear(i);
         if (use_k)
             for (int i = tid; i < TP_H1; i += TP_NT) sh.hc[i] = 0u;
         if (tid < 16) {
-            sh.h2[tid] = 0ull;
+            H2.clear(tid);
             sh.h2c[tid] = 0u;
         }
         __syncthreads();
@@ -141,8 +186,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
         mp.magic = 12582912.0f + (float)a.S;
 
         // ---------------------------------------------------- pass 2: masses, Z, coarse bins
-        for (int t = warp; t < ntile; t += TP_NW) {
-            const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+        tp_stream(row, ntile, V, aligned, warp, lane, [&](int t, const uint4 v) {
             uint64_t mm[8];
             mass_pair(v.x, mp, mm[0], mm[1]);
             mass_pair(v.y, mp, mm[2], mm[3]);
@@ -156,20 +200,19 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 s += mm[i];
                 if (mm[i]) {
                     const uint32_t kb = tp_key(bits[i]) >> 4;
-                    if (use_p) atomicAdd(&sh.h1[kb], (unsigned long long)mm[i]);
+                    if (use_p) H1.add(kb, mm[i]);
                     if (use_k) atomicAdd(&sh.hc[kb], 1u);
                 }
             }
             const uint64_t ws = warp_sum_u51(s);
             if (lane == 0) sh.tsum[t] = ws;
-        }
+        });
         __syncthreads();
         // pass 4: filtered tile sums (masses >= t); tiles_tau = the t sh.tsum reflects
         uint64_t tiles_tau = 0;  // pass 2's sums keep every mass
         auto filtered_tiles = [&](uint64_t t) {
             __syncthreads();  // earlier readers of sh.tsum are done
-            for (int tt = warp; tt < ntile; tt += TP_NW) {
-                const uint4 v = tp_load8(row, tt * 256 + lane * 8, V, aligned);
+            tp_stream(row, ntile, V, aligned, warp, lane, [&](int tt, const uint4 v) {
                 uint64_t mm[8];
                 mass_pair(v.x, mp, mm[0], mm[1]);
                 mass_pair(v.y, mp, mm[2], mm[3]);
@@ -180,7 +223,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 for (int i = 0; i < 8; ++i) s += (mm[i] >= t) ? mm[i] : 0ull;
                 const uint64_t ws = warp_sum_u51(s);
                 if (lane == 0) sh.tsum[tt] = ws;
-            }
+            });
             __syncthreads();
             tiles_tau = t;
         };
@@ -226,8 +269,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
             const int Bk = sh.bselk;
             if (Bk >= 0) {
                 // pass 3k: counts of the 16 keys inside bin Bk
-                for (int t = warp; t < ntile; t += TP_NW) {
-                    const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+                tp_stream(row, ntile, V, aligned, warp, lane, [&](int, const uint4 v) {
                     uint32_t bits[8];
                     tp_unpack(v, bits);
 #pragma unroll
@@ -236,7 +278,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                         if ((int)(kk >> 4) == Bk && mass_of(__uint_as_float(bits[i] << 16), mp))
                             atomicAdd(&sh.h2c[kk & 15u], 1u);
                     }
-                }
+                });
                 __syncthreads();
                 int ks = Bk * 16, cnt = 0;
                 for (int i = 15; i >= 0; --i) {
@@ -263,7 +305,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 const int per = TP_H1 / 32;
                 const int lo = (31 - lane) * per;  // lane 0 owns the heaviest bins
                 uint64_t ls = 0;
-                for (int i = 0; i < per; ++i) ls += sh.h1[lo + i];
+                for (int i = 0; i < per; ++i) ls += H1.get(lo + i);
                 const uint64_t incl = warp_incl_scan_u64(ls, lane);  // mass of bins >= lane's lowest
                 const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= theta);
                 const int L = hit ? (__ffs(hit) - 1) : 31;
@@ -271,7 +313,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                     uint64_t above = incl - ls;
                     int B = lo;
                     for (int i = per - 1; i >= 0; --i) {
-                        const uint64_t h = sh.h1[lo + i];
+                        const uint64_t h = H1.get(lo + i);
                         if (above + h >= theta) {
                             B = lo + i;
                             break;
@@ -286,8 +328,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
             __syncthreads();
             const int B = sh.bsel;
             // pass 3: keys inside bin B
-            for (int t = warp; t < ntile; t += TP_NW) {
-                const uint4 v = tp_load8(row, t * 256 + lane * 8, V, aligned);
+            tp_stream(row, ntile, V, aligned, warp, lane, [&](int, const uint4 v) {
                 uint32_t bits[8];
                 tp_unpack(v, bits);
 #pragma unroll
@@ -295,10 +336,10 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                     const uint32_t kk = tp_key(bits[i]);
                     if ((int)(kk >> 4) == B) {
                         const uint64_t mi = mass_of(__uint_as_float(bits[i] << 16), mp);
-                        if (mi) atomicAdd(&sh.h2[kk & 15u], (unsigned long long)mi);
+                        if (mi) H2.add(kk & 15u, mi);
                     }
                 }
-            }
+            });
             __syncthreads();
             // tau = mass(k*) (>= tau_k: Theta <= Z_k); Z' from the histograms unless lower keys
             // share tau (then a filtered pass)
@@ -306,14 +347,14 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
             uint64_t above = 0;
             int ks = B * 16;
             for (int i = 15; i >= 0; --i) {
-                if (above + sh.h2[i] >= need) {
+                if (above + H2.get(i) >= need) {
                     ks = B * 16 + i;
                     break;
                 }
-                above += sh.h2[i];
+                above += H2.get(i);
             }
             tau = mass_of(__uint_as_float(tp_unkey((uint32_t)ks) << 16), mp);
-            Zp = sh.bz[1] + above + sh.h2[ks & 15];
+            Zp = sh.bz[1] + above + H2.get(ks & 15);
             tie_below = ks > 0 && mass_of(__uint_as_float(tp_unkey((uint32_t)ks - 1u) << 16), mp) == tau;
             if (tie_below) {
                 filtered_tiles(tau);
