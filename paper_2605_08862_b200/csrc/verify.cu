@@ -928,7 +928,9 @@ static int verify_kind(const bs_ctx* ctx, int V) {
 // Slice of a row per cluster CTA: ceil(V / 8) rounded up to whole 512-element tiles.
 static int cluster_slice(int V) { return ((V + CK_CL - 1) / CK_CL + CK_TILE - 1) / CK_TILE * CK_TILE; }
 
-static int ntile_ok(int V) { return (V + 255) / 256 <= TP_MAXT ? 1 : 0; }
+// Slice of a filtered row per cluster CTA: ceil(V / 8) rounded up to whole 256-element tiles.
+static int topp_slice(int V) { return ((V + TP_CL - 1) / TP_CL + 255) / 256 * 256; }
+static int ntile_ok(int V) { return topp_slice(V) / 256 <= TP_MAXLT ? 1 : 0; }
 
 cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const void* logits,
                           const int64_t* row_index, int64_t stride, const int32_t* draft,
@@ -1029,8 +1031,10 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
             if (e != cudaSuccess) return e;
             ctx->kcfg_topp = 1;
         }
-        const int tgrid = std::max(1, std::min(ctx->num_sms * 2, n * (k + 1)));
-        return launch_pdl(verify_topp_kernel, dim3(tgrid), dim3(TP_NT), tsm, st, a, top_p, top_k);
+        // one 8-CTA cluster per row in flight (two CTAs per SM)
+        const int tcl = std::max(1, std::min((ctx->num_sms * 2) / TP_CL, n * (k + 1)));
+        return launch_pdl(verify_topp_kernel, dim3(tcl * TP_CL), dim3(TP_NT), tsm, st, a, top_p, top_k,
+                          topp_slice(V));
     }
     if (kind == VK_CLUSTER) {
         const int SL = cluster_slice(V);

@@ -20,26 +20,40 @@
 //   pass 3  the masses of the 16 keys inside B -> the crossing key k*, tau = mass(k*);
 //   pass 4  (only when a sample is drawn, or when keys below k* share its mass) the
 //           filtered masses' 256-element tile sums, which give Z' and the inverse CDF.
-// One persistent CTA per row; the row is read from HBM once and re-read from L2.
+// Each row is split over an 8-CTA thread-block cluster (CTA r: elements [r SL, r SL + SL)):
+// every pass runs on the slices in parallel, the per-slice histograms and sums are added into
+// the leader CTA's shared memory over DSMEM (remote shared atomics) at cluster barriers, and
+// every CTA then reads the cluster totals from the leader, so all of them take the same
+// decisions; the sample's crossing slice rescans its crossing tile.  (One CTA per row, the
+// round-1 layout, made a tail step of the long-context config cost ~150 us per row.)
 #pragma once
 // (included inside namespace bs)
 
+constexpr int TP_CL = 8;              // CTAs per row (cluster)
 constexpr int TP_NT = 512;            // threads
 constexpr int TP_NW = TP_NT / 32;     // warps
 constexpr int TP_H1 = 4096;           // coarse key bins
-constexpr int TP_MAXT = 2048;         // 256-element tiles: V <= 524288
+constexpr int TP_MAXLT = 256;         // 256-element tiles per slice: V <= 8 * 65536 = 524288
+constexpr int TP_MAXT = TP_CL * TP_MAXLT;
 
 struct TopPShared {
-    uint32_t h1lo[TP_H1], h1hi[TP_H1];  // coarse-bin masses (Hist64)
-    uint32_t hc[TP_H1];       // top-k: positive-mass tokens per coarse bin
-    uint32_t h2c[16];         // top-k: positive-mass tokens per key of the crossing bin
-    unsigned long long tsum[TP_MAXT];
+    uint32_t h1lo[TP_H1], h1hi[TP_H1];  // coarse-bin masses (Hist64); the leader's: cluster sums
+    uint32_t hc[TP_H1];                 // top-k: positive-mass tokens per coarse bin
+    uint32_t h2c[16];                   // top-k: positive-mass tokens per key of the crossing bin
     uint32_t h2lo[16], h2hi[16];        // masses of the 16 keys of the crossing bin (Hist64)
+    unsigned long long tsum[TP_MAXLT];  // this slice's 256-element tile sums
     unsigned long long stat[STAT_COUNT];
     float wmax[TP_NW];
     uint32_t wbad[TP_NW];
+    // written into the LEADER's copy by every CTA (DSMEM), read by all after a cluster barrier
+    float cmax[TP_CL];
+    uint32_t cbad[TP_CL];
+    unsigned long long zsum[TP_CL];     // slice sums: unfiltered
+    unsigned long long fsum[3][TP_CL];  // slice sums of filtered passes (rotating)
+    int32_t cand;                       // the sampled token (from the crossing slice)
+    // the leader's broadcasts
     RowDesc dsc;
-    unsigned long long bz[3];  // [0] Theta remaining inside the coarse bin, [1] sum above it, [2] Z
+    unsigned long long bz[2];  // [0] Theta remaining inside the coarse bin, [1] sum above it
     int32_t bsel;              // coarse bin B
     int32_t bselk, needk;      // top-k: coarse bin of kappa, tokens still needed inside it
 };
@@ -111,30 +125,51 @@ __device__ __forceinline__ void tp_stream(const uint16_t* row, int ntile, int V,
     }
 }
 
-__global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs a, float top_p, int top_k) {
+__global__ void __cluster_dims__(TP_CL, 1, 1) __launch_bounds__(TP_NT, 2)
+verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
+    namespace cg = cooperative_groups;
     extern __shared__ __align__(16) uint8_t tp_smem[];
     TopPShared& sh = *reinterpret_cast<TopPShared*>(tp_smem);
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    TopPShared* L = cl.map_shared_rank(&sh, 0);  // the leader's copy
     pdl_wait();  // dependents launch at exit (the cluster kernel plans before its wait)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rows = (int)a.ctl[VCTL_ROWS];
     const int V = a.V;
-    const int ntile = (V + 255) / 256;
+    const int e_lo = rank * SL, len = max(0, min(SL, V - e_lo));
+    const int nlt = (len + 255) / 256;  // this slice's tiles
     const uint64_t P = (uint64_t)llround((double)top_p * 4294967296.0);  // R5 (top_p < 1)
     const bool use_p = top_p < 1.f, use_k = top_k > 0;
     for (int i = tid; i < STAT_COUNT; i += TP_NT) sh.stat[i] = 0ull;
+    const Hist64 H1{sh.h1lo, sh.h1hi}, H2{sh.h2lo, sh.h2hi};
+    const Hist64 H1L{L->h1lo, L->h1hi}, H2L{L->h2lo, L->h2hi};
 
     for (;;) {
-        if (tid == 0) sh.dsc = claim_row(a, rows);
-        __syncthreads();
-        const RowDesc dsc = sh.dsc;
-        if (dsc.b < 0) break;
+        if (rank == 0 && tid == 0) sh.dsc = claim_row(a, rows);
+        // clear this CTA's accumulators (the leader's are the cluster totals)
+        for (int i = tid; i < TP_H1; i += TP_NT) {
+            H1.clear(i);
+            sh.hc[i] = 0u;
+        }
+        if (tid < 16) {
+            H2.clear(tid);
+            sh.h2c[tid] = 0u;
+        }
+        cl.sync();  // S1: the claim is published; every accumulator is clear; the last row is done
+        const RowDesc dsc = L->dsc;
+        if (dsc.b < 0) {
+            cl.sync();  // no CTA may exit while another still reads the leader's shared memory
+            break;
+        }
         const uint16_t* row = a.logits + dsc.rowno * a.stride;
+        const uint16_t* srow = row + e_lo;
         const bool aligned = dsc.aligned != 0;
         const int j = dsc.j, q = dsc.q, d = dsc.d;
 
-        // ---------------------------------------------------- pass 1: max
+        // ---------------------------------------------------- pass 1: max (slice, then cluster)
         uint32_t mx = 0xFF80FF80u;
-        tp_stream(row, ntile, V, aligned, warp, lane, [&](int, const uint4 v) {
+        tp_stream(srow, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
             mx = hmax2_nan_u32(mx, v.x);
             mx = hmax2_nan_u32(mx, v.y);
             mx = hmax2_nan_u32(mx, v.z);
@@ -152,31 +187,34 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 sh.wbad[warp] = bad;
             }
         }
-        const Hist64 H1{sh.h1lo, sh.h1hi}, H2{sh.h2lo, sh.h2hi};
-        for (int i = tid; i < TP_H1; i += TP_NT) H1.clear(i);
-        if (use_k)
-            for (int i = tid; i < TP_H1; i += TP_NT) sh.hc[i] = 0u;
-        if (tid < 16) {
-            H2.clear(tid);
-            sh.h2c[tid] = 0u;
-        }
         __syncthreads();
+        if (tid == 0) {
+            float cm = -INFINITY;
+            uint32_t cb = 0;
+            for (int w = 0; w < TP_NW; ++w) {
+                cm = fmaxf(cm, sh.wmax[w]);
+                cb |= sh.wbad[w];
+            }
+            L->cmax[rank] = cm;
+            L->cbad[rank] = cb;
+        }
+        cl.sync();  // S2: every slice's max in the leader
         float m = -INFINITY;
         uint32_t bb = 0;
-        for (int w = 0; w < TP_NW; ++w) {
-            m = fmaxf(m, sh.wmax[w]);
-            bb |= sh.wbad[w];
+        for (int r = 0; r < TP_CL; ++r) {
+            m = fmaxf(m, L->cmax[r]);
+            bb |= L->cbad[r];
         }
         uint32_t err = 0;
         if (bb) err |= DEV_BAD_LOGIT;
         else if (m == -INFINITY) err |= DEV_ALL_NEGINF;
         else if (!(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) err |= DEV_RANGE;
         if (err) {  // R0: the row is an error; the rollout stops (no token)
-            if (tid == 0) {  // reported at finalize only if Alg. 1 needs this row
+            if (rank == 0 && tid == 0) {  // reported at finalize only if Alg. 1 needs this row
                 sh.stat[STAT_ROWS_VERIFIED] += 1ull;
                 complete_row(a, sh.stat, dsc.b, j, q, ST_ERR, (int)err, 0ull, 0.f);
             }
-            __syncthreads();
+            cl.sync();  // S_end: every CTA is done reading the leader's row state
             continue;
         }
         MassParams mp;
@@ -186,7 +224,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
         mp.magic = 12582912.0f + (float)a.S;
 
         // ---------------------------------------------------- pass 2: masses, Z, coarse bins
-        tp_stream(row, ntile, V, aligned, warp, lane, [&](int t, const uint4 v) {
+        tp_stream(srow, nlt, len, aligned, warp, lane, [&](int t, const uint4 v) {
             uint64_t mm[8];
             mass_pair(v.x, mp, mm[0], mm[1]);
             mass_pair(v.y, mp, mm[2], mm[3]);
@@ -208,11 +246,35 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
             if (lane == 0) sh.tsum[t] = ws;
         });
         __syncthreads();
-        // pass 4: filtered tile sums (masses >= t); tiles_tau = the t sh.tsum reflects
-        uint64_t tiles_tau = 0;  // pass 2's sums keep every mass
+        // this slice's tile sums -> its sum in the leader (every thread computes it, tid 0 stores)
+        auto slice_total = [&]() {
+            uint64_t zl = 0;
+            for (int t = lane; t < nlt; t += 32) zl += sh.tsum[t];
+            return warp_sum_u64(zl);
+        };
+        {
+            const uint64_t zs = slice_total();
+            if (tid == 0) L->zsum[rank] = zs;
+        }
+        if (rank != 0) {  // this slice's histograms into the leader's (remote shared atomics)
+            for (int i = tid; i < TP_H1; i += TP_NT) {
+                if (use_p) {
+                    const uint64_t h = H1.get(i);
+                    if (h) H1L.add((uint32_t)i, h);
+                }
+                if (use_k && sh.hc[i]) atomicAdd(&L->hc[i], sh.hc[i]);
+            }
+        }
+        cl.sync();  // S3: cluster histograms and slice sums in the leader
+        uint64_t Z = 0;
+        for (int r = 0; r < TP_CL; ++r) Z += L->zsum[r];  // R4: the unfiltered normaliser
+        // filtered slice tile sums (masses >= t) and their slice total into fsum[slot]
+        uint64_t tiles_tau = 0;  // pass 2's tile sums keep every mass
+        const unsigned long long* tiles_sums = L->zsum;
+        int fslot = 0;
         auto filtered_tiles = [&](uint64_t t) {
             __syncthreads();  // earlier readers of sh.tsum are done
-            tp_stream(row, ntile, V, aligned, warp, lane, [&](int tt, const uint4 v) {
+            tp_stream(srow, nlt, len, aligned, warp, lane, [&](int tt, const uint4 v) {
                 uint64_t mm[8];
                 mass_pair(v.x, mp, mm[0], mm[1]);
                 mass_pair(v.y, mp, mm[2], mm[3]);
@@ -225,18 +287,20 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 if (lane == 0) sh.tsum[tt] = ws;
             });
             __syncthreads();
+            const uint64_t fs = slice_total();
+            if (tid == 0) L->fsum[fslot][rank] = fs;
+            cl.sync();  // every slice's filtered sum in the leader
             tiles_tau = t;
+            tiles_sums = L->fsum[fslot];
+            fslot = (fslot + 1) % 3;
+            uint64_t tot = 0;
+            for (int r = 0; r < TP_CL; ++r) tot += tiles_sums[r];
+            return tot;
         };
-        auto tiles_total = [&]() {  // every thread: the sum of sh.tsum
-            uint64_t zl = 0;
-            for (int t = lane; t < ntile; t += 32) zl += sh.tsum[t];
-            return warp_sum_u64(zl);
-        };
-        const uint64_t Z = tiles_total();  // R4: the unfiltered normaliser
         // ---------------------------------------------------- top-k (R5k): tau_k, Z_k
         uint64_t tau = 0, Zk = Z;
         if (use_k) {
-            if (warp == 0) {  // count select over the coarse bins, heaviest first
+            if (rank == 0 && warp == 0) {  // count select over the coarse bins, heaviest first
                 const int per = TP_H1 / 32;
                 const int lo = (31 - lane) * per;
                 uint32_t ls = 0;
@@ -249,8 +313,8 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 }
                 const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= (uint32_t)top_k);
                 if (lane == 0 && !hit) sh.bselk = -1;  // fewer than top_k positive masses: keep all
-                const int L = hit ? (__ffs(hit) - 1) : 32;
-                if (lane == L) {
+                const int Lh = hit ? (__ffs(hit) - 1) : 32;
+                if (lane == Lh) {
                     uint32_t above = incl - ls;
                     int Bk = lo;
                     for (int i = per - 1; i >= 0; --i) {
@@ -265,11 +329,11 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                     sh.needk = top_k - (int)above;
                 }
             }
-            __syncthreads();
-            const int Bk = sh.bselk;
+            cl.sync();  // S4: the leader's select
+            const int Bk = L->bselk;
             if (Bk >= 0) {
-                // pass 3k: counts of the 16 keys inside bin Bk
-                tp_stream(row, ntile, V, aligned, warp, lane, [&](int, const uint4 v) {
+                // pass 3k: counts of the 16 keys inside bin Bk (slice -> leader)
+                tp_stream(srow, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
                     uint32_t bits[8];
                     tp_unpack(v, bits);
 #pragma unroll
@@ -280,25 +344,26 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                     }
                 });
                 __syncthreads();
+                if (rank != 0 && tid < 16 && sh.h2c[tid]) atomicAdd(&L->h2c[tid], sh.h2c[tid]);
+                cl.sync();  // S5: the 16 key counts in the leader
+                const int needk = L->needk;
                 int ks = Bk * 16, cnt = 0;
                 for (int i = 15; i >= 0; --i) {
-                    cnt += (int)sh.h2c[i];
-                    if (cnt >= sh.needk) {
+                    cnt += (int)L->h2c[i];
+                    if (cnt >= needk) {
                         ks = Bk * 16 + i;
                         break;
                     }
                 }
                 tau = mass_of(__uint_as_float(tp_unkey((uint32_t)ks) << 16), mp);  // tau_k
-                filtered_tiles(tau);
-                Zk = tiles_total();
+                Zk = filtered_tiles(tau);
             }
         }
         // ---------------------------------------------------- top-p (R5) on the top-k masses
         uint64_t Zp = Zk;
-        bool tie_below = false;
         if (use_p) {
-            // coarse select (warp 0): lane l owns bins [l*128, l*128+128), heaviest first
-            if (warp == 0) {
+            // coarse select (leader, warp 0): lane l owns bins [l*128, l*128+128), heaviest first
+            if (rank == 0 && warp == 0) {
                 unsigned __int128 th = (unsigned __int128)P * Zk + (((unsigned __int128)1 << 32) - 1);
                 uint64_t theta = (uint64_t)(th >> 32);
                 theta = theta ? theta : 1ull;  // top_p -> 0 keeps the heaviest level (as R5)
@@ -308,8 +373,8 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 for (int i = 0; i < per; ++i) ls += H1.get(lo + i);
                 const uint64_t incl = warp_incl_scan_u64(ls, lane);  // mass of bins >= lane's lowest
                 const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= theta);
-                const int L = hit ? (__ffs(hit) - 1) : 31;
-                if (lane == L) {
+                const int Lh = hit ? (__ffs(hit) - 1) : 31;
+                if (lane == Lh) {
                     uint64_t above = incl - ls;
                     int B = lo;
                     for (int i = per - 1; i >= 0; --i) {
@@ -325,10 +390,10 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                     sh.bz[1] = above;
                 }
             }
-            __syncthreads();
-            const int B = sh.bsel;
-            // pass 3: keys inside bin B
-            tp_stream(row, ntile, V, aligned, warp, lane, [&](int, const uint4 v) {
+            cl.sync();  // S6: the leader's coarse select
+            const int B = L->bsel;
+            // pass 3: masses of the keys inside bin B (slice -> leader)
+            tp_stream(srow, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
                 uint32_t bits[8];
                 tp_unpack(v, bits);
 #pragma unroll
@@ -341,67 +406,82 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 }
             });
             __syncthreads();
+            if (rank != 0 && tid < 16) {
+                const uint64_t h = H2.get(tid);
+                if (h) H2L.add((uint32_t)tid, h);
+            }
+            cl.sync();  // S7: the 16 key masses in the leader
             // tau = mass(k*) (>= tau_k: Theta <= Z_k); Z' from the histograms unless lower keys
-            // share tau (then a filtered pass)
-            const uint64_t need = sh.bz[0];
+            // share tau (then a filtered pass) — every CTA computes the same values
+            const uint64_t need = L->bz[0];
             uint64_t above = 0;
             int ks = B * 16;
             for (int i = 15; i >= 0; --i) {
-                if (above + H2.get(i) >= need) {
+                const uint64_t h = H2L.get(i);
+                if (above + h >= need) {
                     ks = B * 16 + i;
                     break;
                 }
-                above += H2.get(i);
+                above += h;
             }
             tau = mass_of(__uint_as_float(tp_unkey((uint32_t)ks) << 16), mp);
-            Zp = sh.bz[1] + above + H2.get(ks & 15);
-            tie_below = ks > 0 && mass_of(__uint_as_float(tp_unkey((uint32_t)ks - 1u) << 16), mp) == tau;
-            if (tie_below) {
-                filtered_tiles(tau);
-                Zp = tiles_total();
-            }
+            Zp = L->bz[1] + above + H2L.get(ks & 15);
+            const bool tie_below = ks > 0 && mass_of(__uint_as_float(tp_unkey((uint32_t)ks - 1u) << 16), mp) == tau;
+            if (tie_below) Zp = filtered_tiles(tau);
         }
         const uint64_t md_full = (d >= 0) ? mass_of(__uint_as_float((uint32_t)row[d] << 16), mp) : 0ull;
         const uint64_t md = (md_full >= tau) ? md_full : 0ull;  // mass'(d)
 
-        // decision (R7) — every thread computes it identically
+        // decision (R7) — every thread of every CTA computes it identically
         bool acc = false;
         if (j < q) acc = uniform_floor(row_draw(a, dsc, PURPOSE_ACCEPT), Zp) < md;
         const int status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
-        int cand = -1;
         if (status == ST_DECIDED) {
-            // residual (d excluded) or bonus sample (R8): inverse CDF in ascending id
+            // residual (d excluded) or bonus sample (R8): inverse CDF in ascending id over the
+            // slices, then the crossing slice's tiles, then one tile's elements
             if (tiles_tau != tau) filtered_tiles(tau);
             const int excl = (j < q) ? d : -1;
             const uint64_t U = uniform_floor(row_draw(a, dsc, PURPOSE_SAMPLE), Zp - ((j < q) ? md : 0ull));
-            if (warp == 0) {
-                const int per = (ntile + 31) / 32;
-                const int i0 = min(ntile, lane * per), i1 = min(ntile, i0 + per);
-                const int ex_t = (excl >= 0) ? excl / 256 : -1;
+            const int ex_s = (excl >= 0) ? excl / SL : -1;
+            int xs = TP_CL - 1;
+            uint64_t us = 0, cum = 0;
+            for (int r = 0; r < TP_CL; ++r) {
+                const uint64_t ss = tiles_sums[r] - ((r == ex_s) ? md : 0ull);
+                if (U < cum + ss) {
+                    xs = r;
+                    us = U - cum;
+                    break;
+                }
+                cum += ss;
+            }
+            if (rank == xs && warp == 0) {
+                const int per = (nlt + 31) / 32;
+                const int i0 = min(nlt, lane * per), i1 = min(nlt, i0 + per);
+                const int ex_t = (excl >= 0 && ex_s == rank) ? (excl - e_lo) / 256 : -1;
                 uint64_t ls = 0;
                 for (int i = i0; i < i1; ++i) ls += sh.tsum[i] - ((i == ex_t) ? md : 0ull);
                 const uint64_t incl = warp_incl_scan_u64(ls, lane);
-                const unsigned hit = __ballot_sync(0xFFFFFFFFu, U < incl);
-                const int L = hit ? (__ffs(hit) - 1) : 31;
+                const unsigned hit = __ballot_sync(0xFFFFFFFFu, us < incl);
+                const int Lh = hit ? (__ffs(hit) - 1) : 31;
                 int xt = 0;
                 uint64_t ut = 0;
-                if (lane == L) {
-                    uint64_t cum = incl - ls;
+                if (lane == Lh) {
+                    uint64_t c2 = incl - ls;
                     for (int i = i0; i < i1; ++i) {
                         const uint64_t ts = sh.tsum[i] - ((i == ex_t) ? md : 0ull);
-                        if (U < cum + ts) {
+                        if (us < c2 + ts) {
                             xt = i;
-                            ut = U - cum;
+                            ut = us - c2;
                             break;
                         }
-                        cum += ts;
+                        c2 += ts;
                     }
                 }
-                xt = __shfl_sync(0xFFFFFFFFu, xt, L);
-                ut = shfl_u64(ut, L);
-                // rescan tile xt: lane l owns its 8 elements
-                const int e0 = xt * 256 + lane * 8;
-                const uint4 v = tp_load8(row, e0, V, aligned);
+                xt = __shfl_sync(0xFFFFFFFFu, xt, Lh);
+                ut = shfl_u64(ut, Lh);
+                // rescan tile xt of the slice: lane l owns its 8 elements
+                const int e0 = e_lo + xt * 256 + lane * 8;
+                const uint4 v = tp_load8(row, e0, min(V, e_lo + len), aligned);
                 uint64_t mm[8];
                 mass_pair(v.x, mp, mm[0], mm[1]);
                 mass_pair(v.y, mp, mm[2], mm[3]);
@@ -410,7 +490,7 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 uint64_t s = 0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    if (mm[i] < tau || e0 + i == excl || e0 + i >= V) mm[i] = 0;
+                    if (mm[i] < tau || e0 + i == excl || e0 + i >= e_lo + len) mm[i] = 0;
                     s += mm[i];
                 }
                 const uint64_t inc2 = warp_incl_scan_u64(s, lane);
@@ -418,23 +498,26 @@ __global__ void __launch_bounds__(TP_NT, 2) verify_topp_kernel(const VerifyArgs 
                 const int L2 = hit2 ? (__ffs(hit2) - 1) : 31;
                 int tok = -1;
                 if (lane == L2) {
-                    uint64_t cum = inc2 - s;
+                    uint64_t c3 = inc2 - s;
                     for (int i = 0; i < 8; ++i) {
-                        cum += mm[i];
-                        if (cum > ut) {
+                        c3 += mm[i];
+                        if (c3 > ut) {
                             tok = e0 + i;
                             break;
                         }
                     }
                 }
-                cand = __shfl_sync(0xFFFFFFFFu, tok, L2);
+                tok = __shfl_sync(0xFFFFFFFFu, tok, L2);
+                if (lane == 0) L->cand = tok;
             }
+            cl.sync();  // S8: the sampled token in the leader
         }
-        if (tid == 0) {
+        if (rank == 0 && tid == 0) {
             sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-            complete_row(a, sh.stat, dsc.b, j, q, status, cand, Zp, (float)ldexp((double)Z, -a.S));
+            complete_row(a, sh.stat, dsc.b, j, q, status, status == ST_DECIDED ? sh.cand : -1, Zp,
+                         (float)ldexp((double)Z, -a.S));
         }
-        __syncthreads();
+        cl.sync();  // S_end: every CTA is done reading the leader's row state before it is reset
     }
     if (a.stats && tid == 0)
         for (int i = 0; i < STAT_COUNT; ++i)
