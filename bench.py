@@ -269,6 +269,7 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
         rec["launches"] += launches_rl
         rec["decode_steps"] += steps_
         rec["launches"] += steps_ * eng.launches_per_step
+        rec["launches"] += steps_ // chunk - 1  # bs_rollout_live per checked chunk (the done flag)
         return steps_
 
     rec0 = dict(launches=0, decode_steps=0)
