@@ -242,12 +242,19 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
                 c += 1
         return steps_
 
+    setup_parts = []
+
     def setup_step(s, d):
         with torch.cuda.stream(stream):
+            t0 = time.perf_counter()
             ctx.bs_draft_pool_put(s, d["sp"], d["off"], d["tok"], d["ntok"], stream=stream)
-            ctx.bs_draft_exchange(comm, rank, world, s, stream=stream)
+            t1 = time.perf_counter()
+            ctx.bs_draft_exchange(comm, rank, world, s, stream=stream)  # synchronises the stream
+            t2 = time.perf_counter()
             eng.seal(s)  # synchronises the stream (index build is per RL step)
+            t3 = time.perf_counter()
             eng.begin(d["uids"], d["pid"], d["tails"], d["ml"])
+            setup_parts.append(((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t3 - t2) * 1e3))
 
     # per RL step, outside the graph: put, the exchange's three NCCL launches and its gather,
     # the seal's own kernels and CUB calls, begin, the first lookup
@@ -326,7 +333,8 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
     torch.cuda.synchronize(dev)
     log("[timed] decode ms per RL step: " + " ".join(f"{e[0].elapsed_time(e[1]):.1f}" for e in evs))
     log("[timed] setup (put, exchange, seal, begin) host ms per RL step: "
-        + " ".join(f"{x:.1f}" for x in setup_ms[-len(evs):]))
+        + " ".join(f"{x:.1f}" for x in setup_ms[-len(evs):]) + "  (put / exchange / seal: "
+        + " ".join(f"{a_:.1f}/{b_:.1f}/{c_:.1f}" for a_, b_, c_ in setup_parts[-len(evs):]) + ")")
     t_host1 = time.time()
     if dist is not None:
         dist.barrier()

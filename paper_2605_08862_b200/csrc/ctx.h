@@ -61,6 +61,20 @@ struct DevBuf {
         if (e == cudaSuccess) n = alloc;
         return e;
     }
+    // Stream-ordered growth (cudaMallocAsync / cudaFreeAsync from the device's memory pool, which
+    // bs_create keeps cached): no device-synchronising cudaMalloc / cudaFree on a per-RL-step path
+    // (a synchronous re-allocation of the index table once stalled a seal for over a second).
+    // Buffers grown this way must be released with release_async.
+    cudaError_t ensure_async(size_t want, cudaStream_t st) {
+        if (want <= n && p) return cudaSuccess;
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+        n = 0;
+        const size_t alloc = want ? want + want / 4 : 1;  // 25 % headroom: fewer regrowths
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), alloc * sizeof(T), st);
+        if (e == cudaSuccess) n = alloc;
+        return e;
+    }
     void release() {
         if (p) cudaFree(p);
         p = nullptr;

@@ -255,15 +255,15 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
         return cudaErrorInvalidValue;
     }
     const int n = (int)N;
-    BS_TRY(ctx->seq_start_of.ensure(n));
-    BS_TRY(ctx->seq_end_of.ensure(n));
-    BS_TRY(ctx->prompt_of.ensure(n));
+    BS_TRY(ctx->seq_start_of.ensure_async(n, st));
+    BS_TRY(ctx->seq_end_of.ensure_async(n, st));
+    BS_TRY(ctx->prompt_of.ensure_async(n, st));
     if (ctx->sealed.n_seqs > 0 && n > 0)
         seq_meta_kernel<<<std::min(ctx->sealed.n_seqs, 4096), 256, 0, st>>>(
             ctx->sealed.seq_off.p, ctx->sealed.seq_prompt.p, ctx->sealed.n_seqs, ctx->seq_start_of.p,
             ctx->seq_end_of.p, ctx->prompt_of.p);
     if (n == 0) {
-        BS_TRY(ctx->table.ensure(2));
+        BS_TRY(ctx->table.ensure_async(2, st));
         BS_TRY(cudaMemsetAsync(ctx->table.p, 0, 2 * sizeof(IndexEntry), st));
         ctx->table_mask = 1;
         BS_TRY(publish_index(ctx, st, ctx->sealed.step));
@@ -349,7 +349,7 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
     for (size_t li = 0; li < levels.size() && (int)li < M; ++li) cap_need += levels[li].nruns;
     uint64_t cap = 2;
     while (cap < (uint64_t)(2 * cap_need + 2)) cap <<= 1;
-    BS_TRY(ctx->table.ensure(cap));
+    BS_TRY(ctx->table.ensure_async(cap, st));
     BS_TRY(cudaMemsetAsync(ctx->table.p, 0, cap * sizeof(IndexEntry), st));
     ctx->table_mask = cap - 1;
     first_unique_kernel<<<G, 256, 0, st>>>(n, M, K, T, fu.p, ctx->seq_end_of.p, ctx->prompt_of.p,

@@ -561,7 +561,11 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
         TRACE(TR_START, 0, (int)smid, 0);
     }
 #endif
-    cluster.sync();  // every CTA's barriers exist before any remote operation
+    // every CTA's barriers exist before any remote operation: the mbarrier inits are published by
+    // fence.mbarrier_init.release.cluster above, so a relaxed cluster arrive suffices (no full
+    // fence); the CTA's own shared-memory initialisation is ordered by the CTA barrier
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
     // Without the caller's early-plan promise (bsx_set_early_plan) everything waits for the
     // previous kernel first: only griddepcontrol.wait makes its writes visible.
     if (!a.early_plan) pdl_wait();
