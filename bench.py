@@ -192,7 +192,7 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
     bs.bsx_synth_bank(bank, cfg["nbank"], V, spec.bank_seed, spec.beta, stream=stream)
     eng = RolloutEngine(ctx, n, k, cfg["T"], cfg["top_p"],
                         Target(bank, cfg["nbank"], spec.target_seed, TARGET_MODES[spec.mode]), stream=stream,
-                        plain=cfg.get("plain", False))
+                        plain=cfg.get("plain", False), ngram=cfg.get("ngram"))
     comm = nccl_comm(bs, dist, rank, world)
 
     def dev_t(a):
@@ -541,6 +541,9 @@ def sweep_configs():
     pts = [("k%d_r0.8" % k, dict(base, k=k)) for k in (2, 4, 8, 16)]
     pts += [("k8_r%g" % r, dict(base, match_rate=r)) for r in (0.0, 0.5, 0.95)]
     pts.append(("plain", dict(base, k=8, plain=True)))
+    # f4 draft-source ablation (the paper's Table 7): the n-gram linear-scan drafter
+    # on the same workload as k8_r0.8 (suffix index)
+    pts.append(("ngram_k8_r0.8", dict(base, ngram=(1, 32))))
     return pts
 
 
@@ -668,6 +671,7 @@ def main():
         s2 = summarize(c2, name, r2, args, hbm)
         s2["ms_per_step"] = r2["agg"]["elapsed_ms"] / SWEEP_STEPS[1]
         rec2 = {"point": name, "k": c2["k"], "match_rate": c2["match_rate"], "plain": c2.get("plain", False),
+                "drafter": "none" if c2.get("plain") else ("ngram" if c2.get("ngram") else "suffix index"),
                 "value": s2["value"], "unit": unit, "ms_per_rl_step": s2["ms_per_step"],
                 "acceptance_length": r2["st"]["acceptance_length"],
                 "decode_steps_per_rollout": r2["st"]["decode_steps"] / r2["n"],

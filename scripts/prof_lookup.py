@@ -63,17 +63,28 @@ if a.decode:
     assert ctx.bs_sync_status() == 0
     print("decode mode: ran", a.iters, "steps with standalone lookups")
     sys.exit(0)
-ts = []
-for _ in range(a.iters):
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(eng.stream):
-        s.record(eng.stream)
-        ctx.bs_draft_lookup(1, eng.slots, k, eng.draft, eng.draft_len, eng.match_len, stream=eng.stream)
-        e.record(eng.stream)
-    torch.cuda.synchronize()
-    ts.append(s.elapsed_time(e) * 1e3)
+def timed_calls(fn):
+    out = []
+    for _ in range(a.iters):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(eng.stream):
+            s.record(eng.stream)
+            fn()
+            e.record(eng.stream)
+        torch.cuda.synchronize()
+        out.append(s.elapsed_time(e) * 1e3)
+    return out
+
+
+# the n-gram linear-scan drafter (f4) on the same state, for the per-call comparison
+tn = timed_calls(lambda: ctx.bs_draft_lookup_ngram(1, eng.slots, k, 1, 32, eng.draft, eng.draft_len, eng.match_len,
+                                                    stream=eng.stream))
+dl_ng = eng.draft_len.cpu().numpy().copy()
+ts = timed_calls(lambda: ctx.bs_draft_lookup(1, eng.slots, k, eng.draft, eng.draft_len, eng.match_len,
+                                             stream=eng.stream))
 assert ctx.bs_sync_status() == 0
 ml = eng.match_len.cpu().numpy()
 dl = eng.draft_len.cpu().numpy()
 print(f"lookup: {n} rollouts, pool {len(h['tokens'])} tokens, median {np.median(ts[2:]):.1f} us/call, "
       f"mean anchor {ml.mean():.1f}, mean draft {dl.mean():.2f}")
+print(f"ngram drafter: median {np.median(tn[2:]):.1f} us/call, mean draft {dl_ng.mean():.2f}")
