@@ -60,6 +60,7 @@ def _check(b, got):
     ([9, 3, 1, 5, 2], [9, 300, 2100, 4097, 65], 32, 8),  # Qwen3-8B heads; 2+ KV splits
     ([4, 1], [5000, 4100], 16, 8),                       # G = 2
     ([32], [200], 4, 1),                                 # G = 4, 128 rows
+    ([17, 1, 9], [300, 5000, 2049], 28, 4),              # k = 16 drafts (LC): 17 x 7 = 119 rows
 ])
 def test_unified_attention_parity(bs, q_len, ctx, H_q, H_kv):
     b = make_attn_batch(len(ctx) * 7 + H_q, q_len, ctx, H_q=H_q, H_kv=H_kv)
