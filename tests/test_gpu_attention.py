@@ -105,3 +105,42 @@ def test_synth_attn_values_match_numpy(bs):
     from workloads import f32_to_bf16_bits
 
     assert np.array_equal(t.cpu().numpy().view(np.uint16), f32_to_bf16_bits(_vals(9, 2, n, 1.0)))
+
+
+def test_unified_attention_table2_full_size_sampled(bs):
+    """At the size the bench times (the paper's Table 2 setting: 128 requests x 8192 keys, 32 of
+    them with 4 drafts, Qwen2.5-7B heads, values from the device twin of the generator, shuffled
+    pages): sampled requests (speculative and plain, first / last) against the oracle."""
+    from oracle.attention import attention_request
+    from workloads.attn import PAGE as PG
+
+    H_q, H_kv, D, B, ctx_len = 28, 4, 128, 128, 8192
+    rng = np.random.default_rng(0)
+    q_len = np.ones(B, dtype=np.int32)
+    spec = rng.choice(B, 32, replace=False)
+    q_len[spec] = 5
+    ctx = np.full(B, ctx_len, dtype=np.int32)
+    npg = ctx_len // PG
+    perm = np.random.default_rng(1).permutation(B * npg).astype(np.int32)
+    pt = perm.reshape(B, npg)
+    mult = float(np.float32(1.0 / 147.8))
+    kc = torch.empty((B * npg, H_kv, PG, D), dtype=torch.int16, device="cuda")
+    vc = torch.empty_like(kc)
+    bs.bsx_synth_attn_values(kc, 11, mult)
+    bs.bsx_synth_attn_values(vc, 12, mult)
+    q = torch.empty((int(q_len.sum()), H_q, D), dtype=torch.int16, device="cuda")
+    bs.bsx_synth_attn_values(q, 13, mult)
+    out = bs.bs_unified_attention(q, kc, vc, to_dev(pt), to_dev(ctx), ctx, q_len, H_kv)
+    torch.cuda.synchronize()
+    q_off = np.concatenate([[0], np.cumsum(q_len)])
+    sample = sorted({0, B - 1, int(spec[0]), int(spec[1]), int(np.setdiff1d(np.arange(B), spec)[3])})
+    for b in sample:
+        pages = torch.from_numpy(pt[b].astype(np.int64)).cuda()
+        k = kc[pages].permute(0, 2, 1, 3).reshape(ctx_len, H_kv, D).cpu().numpy().view(np.uint16)
+        v = vc[pages].permute(0, 2, 1, 3).reshape(ctx_len, H_kv, D).cpu().numpy().view(np.uint16)
+        qb = q[q_off[b]:q_off[b + 1]].cpu().numpy().view(np.uint16)
+        ref = attention_request(qb, k, v, H_kv)
+        got = bf16_bits_to_f32(out[q_off[b]:q_off[b + 1]].cpu().numpy().view(np.uint16)).astype(np.float64)
+        vmax = float(np.abs(bf16_bits_to_f32(v)).max())
+        bound = 2.0 ** -8 * vmax + 2.0 ** -8 * np.abs(ref)
+        assert (np.abs(got - ref) <= bound).all(), b

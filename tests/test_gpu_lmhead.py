@@ -116,3 +116,34 @@ def test_verify_with_fused_stats_is_identical(bs, orc, T):
         o = orc.verify_one([lg[b, j] for j in range(k + 1)], T, 1.0, 77, int(uids[b]), 0, 1000, -1, False,
                            [int(x) for x in drafts[b, :q]], k)
         assert [int(x) for x in ot[b, :ol[b]]] == o.tokens, b
+
+
+def test_lm_head_full_size_sampled_rows(bs):
+    """At the size the bench times (Qwen2.5-7B head, d 3584, V 151936, 2304 rows = 256 rollouts x
+    9): the fused statistics of EVERY row equal the GPU logits' own, and sampled rows' logits are
+    within the fp32-summation bound of the fp64 oracle."""
+    rows, d, V = 2304, 3584, 151936
+    mult_w = float(np.float32(3.0 / np.sqrt(d) / 147.8))
+    w = torch.empty((V, d), dtype=torch.int16, device="cuda")
+    bs.bsx_synth_attn_values(w, 22, mult_w)
+    h = torch.empty((rows, d), dtype=torch.int16, device="cuda")
+    bs.bsx_synth_attn_values(h, 21, float(np.float32(1.0 / 147.8)))
+    lg, key, bad = bs.bs_lm_head_logits(h, w)
+    torch.cuda.synchronize()
+    f = lg.view(torch.bfloat16).float()
+    m_dev = f.max(dim=1).values
+    am_dev = (f == m_dev[:, None]).int().argmax(dim=1)
+    m, am = _decode_key(key.cpu().numpy())
+    np.testing.assert_array_equal(m, m_dev.cpu().numpy())
+    np.testing.assert_array_equal(am, am_dev.cpu().numpy())
+    assert not bad.cpu().numpy().any()
+    sample = [0, 1, 777, 1500, rows - 1]
+    hs = h[sample].cpu().numpy().view(np.uint16)
+    wn = w.cpu().numpy().view(np.uint16)
+    ref = lm_head_logits(hs, wn)
+    g = bf16_bits_to_f32(lg[sample].cpu().numpy().view(np.uint16)).astype(np.float64)
+    r = bf16_bits_to_f32(ref).astype(np.float64)
+    hf, wf = np.abs(bf16_bits_to_f32(hs).astype(np.float64)), np.abs(bf16_bits_to_f32(wn).astype(np.float64))
+    bound = np.abs(r) * 2.0 ** -7 + d * 2.0 ** -24 * (hf @ wf.T)
+    assert (np.abs(g - r) <= bound).all()
+    assert (lg[sample].cpu().numpy().view(np.uint16) == ref).mean() > 0.99
