@@ -198,6 +198,30 @@ __device__ __forceinline__ uint64_t mass_pair_f2i(uint32_t w, float c, float nmc
     return m0 + m1;
 }
 
+#ifdef BS_UB_MUFU
+// MEASUREMENT BUILD ONLY (libbubblespec_ubmufu.so; decisions are NOT R's): the mass loop with
+// MUFU ex2.approx and fp32 sums instead of R's polynomial and integer masses: the upper bound
+// on what a certified fast path could gain in this kernel.
+__device__ __forceinline__ float ex2_mufu(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float mass_pair_mufu(uint32_t w, float c, float nmcs) {
+    const F2 l{bf16lo_alu(w), bf16hi_alu(w)};
+    const F2 y = ffma2(l, F2{c, c}, F2{nmcs, nmcs});
+    return ex2_mufu(y.x) + ex2_mufu(y.y);
+}
+__device__ __forceinline__ uint64_t mass16_fast(uint4 v0, uint4 v1, float c, float nmc, float magic, uint32_t L02) {
+    const float nmcs = nmc + (magic - 12582912.0f);
+    const float s = ((mass_pair_mufu(v0.x, c, nmcs) + mass_pair_mufu(v0.y, c, nmcs)) +
+                     (mass_pair_mufu(v0.z, c, nmcs) + mass_pair_mufu(v0.w, c, nmcs))) +
+                    ((mass_pair_mufu(v1.x, c, nmcs) + mass_pair_mufu(v1.y, c, nmcs)) +
+                     (mass_pair_mufu(v1.z, c, nmcs) + mass_pair_mufu(v1.w, c, nmcs)));
+    (void)L02;
+    return f2u64_rz(s);
+}
+#else
 // Sum of the 16 masses of two 16-byte bf16 vectors; L02 from row_clamp_l0 (nonzero).
 __device__ __forceinline__ uint64_t mass16_fast(uint4 v0, uint4 v1, float c, float nmc, float magic, uint32_t L02) {
     v0.x = hmax2_nan_u32(v0.x, L02);
@@ -213,6 +237,7 @@ __device__ __forceinline__ uint64_t mass16_fast(uint4 v0, uint4 v1, float c, flo
            ((mass_pair_f2i(v1.x, c, nmc, magic) + mass_pair_f2i(v1.y, c, nmc, magic)) +
             (mass_pair_f2i(v1.z, c, nmc, magic) + mass_pair_f2i(v1.w, c, nmc, magic)));
 }
+#endif
 
 // Exact warp sum of u64 lane values < 2^51 with three 32-bit REDUX sums.
 __device__ __forceinline__ uint64_t warp_sum_u51(uint64_t v) {
