@@ -18,6 +18,10 @@
  *  - Every call is stream-ordered and asynchronous on `stream` (a cudaStream_t
  *    passed as void*; NULL = legacy default stream).  One bs_ctx must be driven
  *    from one stream at a time; a bs_ctx is not thread-safe (one per GPU / rank).
+ *  - Device: a call on a bs_ctx (or a bs_bubble_sync) runs on that object's device
+ *    and restores the caller's current device before it returns; the context-free
+ *    calls (bs_unified_attention, bs_lm_head_logits) run on the caller's current
+ *    device, which must hold their pointers and `stream`.
  *  - Host-side argument validation returns a bs_status synchronously and never
  *    throws; bs_last_error() gives the text.  Device-side anomalies (NaN / +inf
  *    logits, an all -inf row, |max logit / T| too large, draft id outside [0, V),

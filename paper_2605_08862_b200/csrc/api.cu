@@ -100,8 +100,8 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
         return fail(nullptr, BS_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
     }
     if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, BS_ERR_INVALID, "bad device ordinal");
-    e = cudaSetDevice(cfg->device);
-    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+    bs::DeviceScope dev_scope_(cfg->device);
+    if (dev_scope_.err != cudaSuccess) return cuda_fail(nullptr, dev_scope_.err, "cudaSetDevice");
     bs_ctx* c = new bs_ctx();
     c->cfg = *cfg;
     c->S = mass_shift(cfg->vocab);
@@ -183,7 +183,7 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
 
 void bs_destroy(bs_ctx* c) {
     if (!c) return;
-    cudaSetDevice(c->cfg.device);
+    bs::DeviceScope dev_scope_(c->cfg.device);
     c->tail.release(); c->ctx_len.release(); c->pos.release(); c->max_len.release();
     c->prompt.release(); c->finished.release(); c->uid.release(); c->dev_err.release();
     c->staging.tokens.release(); c->staging.seq_off.release(); c->staging.seq_prompt.release();
@@ -199,7 +199,8 @@ void bs_destroy(bs_ctx* c) {
 
 bs_status bs_sync_status(bs_ctx* c, void* stream, uint32_t* word) {
     if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     uint32_t w = 0;
     CK(c, cudaMemcpyAsync(&w, c->dev_err.p, sizeof w, cudaMemcpyDeviceToHost, S(stream)), "read error word");
     CK(c, cudaMemsetAsync(c->dev_err.p, 0, sizeof(uint32_t), S(stream)), "clear error word");
@@ -217,7 +218,8 @@ bs_status bs_rollout_begin(bs_ctx* c, int32_t n, const int32_t* slots, const uin
     if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
     if (n && (!slots || !uids || !prompt_ids || !prompt_tail || !max_len))
         return fail(c, BS_ERR_INVALID, "null array");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_begin(c, n, slots, reinterpret_cast<const unsigned long long*>(uids), prompt_ids,
                        prompt_tail, max_len, S(stream)),
        "bs_rollout_begin");
@@ -228,7 +230,8 @@ bs_status bs_rollout_state(bs_ctx* c, int32_t n, const int32_t* slots, int32_t* 
                            int32_t* finished, void* stream) {
     if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
     if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_state(c, n, slots, pos, finished, S(stream)), "bs_rollout_state");
     return BS_OK;
 }
@@ -236,7 +239,8 @@ bs_status bs_rollout_state(bs_ctx* c, int32_t n, const int32_t* slots, int32_t* 
 bs_status bs_rollout_live(bs_ctx* c, int32_t n, const int32_t* slots, int32_t* live, void* stream) {
     if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
     if (n < 0 || n > c->cfg.max_rollouts || !live || (n && !slots)) return fail(c, BS_ERR_INVALID, "bad arguments");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_live_count(c, n, slots, live, S(stream)), "bs_rollout_live");
     return BS_OK;
 }
@@ -254,7 +258,8 @@ bs_status bs_draft_pool_put(bs_ctx* c, uint64_t rl_step, int32_t n_seqs, const i
         P.step = rl_step;
         P.n_tokens = 0;
         P.n_seqs = 0;
-        CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+        bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
         // from here until the seal of rl_step, lookups of the older index are stale
         CK(c, bs::set_cur_step(c, rl_step, S(stream)), "bs_draft_pool_put");
     }
@@ -263,7 +268,8 @@ bs_status bs_draft_pool_put(bs_ctx* c, uint64_t rl_step, int32_t n_seqs, const i
         return fail(c, BS_ERR_CAPACITY, "pool capacity exceeded (%lld tokens, %d seqs)",
                     (long long)(P.n_tokens + n_tokens), P.n_seqs + n_seqs);
     if (n_seqs == 0) return BS_OK;
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_pool_append(c, n_seqs, prompt_ids, seq_offsets, tokens, n_tokens, S(stream)),
        "bs_draft_pool_put");
     P.n_tokens += n_tokens;
@@ -273,7 +279,8 @@ bs_status bs_draft_pool_put(bs_ctx* c, uint64_t rl_step, int32_t n_seqs, const i
 
 bs_status bs_draft_pool_seal(bs_ctx* c, uint64_t rl_step, void* stream) {
     if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     Pool& P = c->staging;
     if (!P.valid || P.step != rl_step) {
         // a repeated seal of the step already sealed is a no-op (it must not seal an empty pool)
@@ -315,7 +322,8 @@ bs_status bs_draft_lookup(bs_ctx* c, uint64_t rl_step, int32_t n, const int32_t*
     if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
     if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
     if (n && (!slots || !draft_len || (k && !draft_tokens))) return fail(c, BS_ERR_INVALID, "null array");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_lookup(c, n, slots, k, draft_tokens, draft_len, match_len, S(stream)),
        "bs_draft_lookup");
     return BS_OK;
@@ -332,7 +340,8 @@ bs_status bs_draft_lookup_ngram(bs_ctx* c, uint64_t rl_step, int32_t n, const in
     if (n_min < 1 || n_max < n_min || n_max > c->M)
         return fail(c, BS_ERR_INVALID, "need 1 <= n_min <= n_max <= match_max");
     if (n && (!slots || !draft_len || (k && !draft_tokens))) return fail(c, BS_ERR_INVALID, "null array");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_lookup_ngram(c, n, slots, k, n_min, n_max, draft_tokens, draft_len, match_len, S(stream)),
        "bs_draft_lookup_ngram");
     return BS_OK;
@@ -361,7 +370,8 @@ bs_status bs_verify_step(bs_ctx* c, int32_t n, const int32_t* slots, const void*
     if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
               (k && !draft_tokens)))
         return fail(c, BS_ERR_INVALID, "null array");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
                         sp.temperature, sp.top_p, sp.top_k, out_tokens, out_len, out_accepted, out_norm,
                         reinterpret_cast<unsigned long long*>(out_z), S(stream)),
@@ -382,7 +392,8 @@ bs_status bs_verify_commit(bs_ctx* c, int32_t n, const int32_t* slots, const voi
     if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
               (k && !draft_tokens)))
         return fail(c, BS_ERR_INVALID, "null array");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     bool fused = false;
     CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
                         sp.temperature, sp.top_p, sp.top_k, out_tokens, out_len, out_accepted, out_norm,
@@ -409,7 +420,8 @@ bs_status bs_verify_commit_lookup(bs_ctx* c, uint64_t rl_step, int32_t n, const 
     if (n && (!slots || !logits || !draft_len || !out_tokens || !out_len || !out_accepted ||
               (k && !draft_tokens)))
         return fail(c, BS_ERR_INVALID, "null array");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     bool fused = false, looked = false;
     const LookupArgs lk = lookup_args(c, n, slots, k, draft_tokens, draft_len, match_len);
     CK(c, launch_verify(c, n, slots, logits, row_index, stride, draft_tokens, draft_len, k,
@@ -431,14 +443,16 @@ bs_status bs_commit(bs_ctx* c, int32_t n, const int32_t* slots, const int32_t* o
     if (n < 0 || n > c->cfg.max_rollouts) return fail(c, BS_ERR_INVALID, "n out of range");
     if (k < 0 || k > c->cfg.k_max) return fail(c, BS_ERR_INVALID, "k out of range");
     if (n && (!slots || !out_tokens || !out_len)) return fail(c, BS_ERR_INVALID, "null array");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_commit(c, n, slots, out_tokens, out_len, k, finished, S(stream)), "bs_commit");
     return BS_OK;
 }
 
 bs_status bs_stats_read(bs_ctx* c, uint64_t* out, int32_t n, int32_t reset, void* stream) {
     if (!c || (n && !out) || n < 0) return fail(c, BS_ERR_INVALID, "bad arguments");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     const int m = n < (int)STAT_COUNT ? n : (int)STAT_COUNT;
     if (m) CK(c, cudaMemcpyAsync(out, c->stats.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, S(stream)), "stats");
     if (reset) CK(c, cudaMemsetAsync(c->stats.p, 0, STAT_COUNT * sizeof(uint64_t), S(stream)), "stats");
@@ -468,7 +482,8 @@ bs_status bsx_target_rows(bs_ctx* c, int32_t n, const int32_t* slots, const int3
     if (n < 0 || n > c->cfg.max_rollouts || k < 0 || k > c->cfg.k_max || nbank < 1 || mode < 0 ||
         mode > 3 || (mode == 3 && nbank < 16))
         return fail(c, BS_ERR_INVALID, "bad target arguments");
-    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    CK(c, dev_scope_.err, "cudaSetDevice");
     CK(c, launch_target_rows(c, n, slots, draft, draft_len, k, tseed, mode, nbank, row_index,
                              S(stream)),
        "bsx_target_rows");

@@ -28,6 +28,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -654,7 +655,7 @@ bs_status bs_unified_attention(const void* q, const void* k_cache, const void* v
     int dev = 0;
     cudaGetDevice(&dev);
     // per-device launch attribute (setting it twice from racing threads is harmless)
-    static int configured[64] = {0};
+    static std::atomic<int> configured[64] = {};
     if (dev < 0 || dev >= 64 || !configured[dev]) {
         if (cudaFuncSetAttribute(unified_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AT_SMEM) !=
             cudaSuccess)

@@ -61,7 +61,8 @@ extern "C" {
 bs_status bs_bubble_sync_create(int32_t device, bs_bubble_sync** out) {
     if (!out) return BS_ERR_INVALID;
     *out = nullptr;
-    if (cudaSetDevice(device) != cudaSuccess) return BS_ERR_CUDA;
+    bs::DeviceScope dev_scope_(device);
+    if (dev_scope_.err != cudaSuccess) return BS_ERR_CUDA;
     auto* s = new (std::nothrow) bs_bubble_sync();
     if (!s) return BS_ERR_OOM;
     s->device = device;
@@ -83,7 +84,8 @@ bs_status bs_bubble_sync_create(int32_t device, bs_bubble_sync** out) {
 
 bs_status bs_bubble_sync_export(const bs_bubble_sync* s, void* handle64) {
     if (!s || !handle64 || !s->owner) return BS_ERR_INVALID;
-    if (cudaSetDevice(s->device) != cudaSuccess) return BS_ERR_CUDA;
+    bs::DeviceScope dev_scope_(s->device);
+    if (dev_scope_.err != cudaSuccess) return BS_ERR_CUDA;
     cudaIpcMemHandle_t h;
     if (cudaIpcGetMemHandle(&h, s->words) != cudaSuccess) return BS_ERR_CUDA;
     static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
@@ -94,7 +96,8 @@ bs_status bs_bubble_sync_export(const bs_bubble_sync* s, void* handle64) {
 bs_status bs_bubble_sync_open(int32_t device, const void* handle64, bs_bubble_sync** out) {
     if (!out || !handle64) return BS_ERR_INVALID;
     *out = nullptr;
-    if (cudaSetDevice(device) != cudaSuccess) return BS_ERR_CUDA;
+    bs::DeviceScope dev_scope_(device);
+    if (dev_scope_.err != cudaSuccess) return BS_ERR_CUDA;
     auto* s = new (std::nothrow) bs_bubble_sync();
     if (!s) return BS_ERR_OOM;
     s->device = device;
@@ -114,7 +117,7 @@ bs_status bs_bubble_sync_open(int32_t device, const void* handle64, bs_bubble_sy
 
 void bs_bubble_sync_destroy(bs_bubble_sync* s) {
     if (!s) return;
-    cudaSetDevice(s->device);
+    bs::DeviceScope dev_scope_(s->device);
     if (s->owner) cudaFree(s->words);
     else cudaIpcCloseMemHandle(s->words);
     delete s;
@@ -122,7 +125,8 @@ void bs_bubble_sync_destroy(bs_bubble_sync* s) {
 
 bs_status bs_bubble_sync_arrive(bs_bubble_sync* s, int32_t rank, uint64_t rl_step, void* stream) {
     if (!s || rank < 0 || rank >= BS_BUBBLE_MAX_RANKS || rl_step == ~0ull) return BS_ERR_INVALID;
-    if (cudaSetDevice(s->device) != cudaSuccess) return BS_ERR_CUDA;
+    bs::DeviceScope dev_scope_(s->device);
+    if (dev_scope_.err != cudaSuccess) return BS_ERR_CUDA;
     // a plain (fully stream-ordered) launch: the rank's last decoding step has completed
     bs::bubble_arrive_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(s->words, (int)rank,
                                                                               (unsigned long long)rl_step);
@@ -133,7 +137,8 @@ bs_status bs_bubble_sync_arrive(bs_bubble_sync* s, int32_t rank, uint64_t rl_ste
 bs_status bs_bubble_sync_poll(bs_bubble_sync* s, int32_t world, uint64_t rl_step, int32_t* halt,
                               void* stream) {
     if (!s || !halt || world < 1 || world > BS_BUBBLE_MAX_RANKS) return BS_ERR_INVALID;
-    if (cudaSetDevice(s->device) != cudaSuccess) return BS_ERR_CUDA;
+    bs::DeviceScope dev_scope_(s->device);
+    if (dev_scope_.err != cudaSuccess) return BS_ERR_CUDA;
     bs::bubble_poll_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
         (const unsigned long long*)s->words, (int)world, (unsigned long long)rl_step, halt);
     const cudaError_t e = cudaGetLastError();

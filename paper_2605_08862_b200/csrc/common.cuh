@@ -11,6 +11,25 @@
 
 namespace bs {
 
+// ------------------------------------------------------------------ host: device scope
+// Every C-ABI call runs on its context's device and leaves the caller's current device as it
+// found it (one process may drive several GPUs, and the caller's framework keeps its own).
+struct DeviceScope {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceScope(int dev) {
+        err = cudaGetDevice(&prev);
+        if (err != cudaSuccess) prev = -1;
+        else if (prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
 // ------------------------------------------------------------------ error word
 constexpr uint32_t DEV_BAD_LOGIT = 0x1u, DEV_ALL_NEGINF = 0x2u, DEV_RANGE = 0x4u,
                    DEV_BAD_DRAFT = 0x8u, DEV_INDEX_KEY = 0x10u,

@@ -143,7 +143,8 @@ bs_status bs_draft_exchange(bs_ctx* c, void* comm_v, int32_t rank, int32_t world
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ncclComm_t comm = (ncclComm_t)comm_v;
-    if (cudaSetDevice(c->cfg.device) != cudaSuccess) return BS_ERR_CUDA;
+    bs::DeviceScope dev_scope_(c->cfg.device);
+    if (dev_scope_.err != cudaSuccess) return BS_ERR_CUDA;
     Pool& P = c->staging;
     if (!P.valid || P.step != rl_step) {
         P.valid = true;

@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 
 #include "../../include/bubblespec.h"
@@ -273,7 +274,7 @@ extern "C" bs_status bs_lm_head_logits(const void* h, const void* w, int32_t row
     if (!lm_map(&hm, h, rows, d, LM_BM) || !lm_map(&wm, w, V, d, LM_BN)) return BS_ERR_CUDA;
     int dev = 0;
     cudaGetDevice(&dev);
-    static int configured[64] = {0};  // per-device attribute (a racing second set is harmless)
+    static std::atomic<int> configured[64] = {};  // per-device attribute (a racing second set is harmless)
     if (dev < 0 || dev >= 64 || !configured[dev]) {
         if (cudaFuncSetAttribute(lm_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM) != cudaSuccess)
             return BS_ERR_CUDA;
