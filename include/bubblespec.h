@@ -313,7 +313,10 @@ bs_status bs_commit(bs_ctx* ctx, int32_t n, const int32_t* slots, const int32_t*
  *   out          [T, H_q, head_dim] bf16: softmax(q k^T * scale, causal) v, token i of request b
  *                attending keys 0 .. ctx_len[b] - q_len[b] + i, query head h using KV head
  *                h / (H_q / H_kv)
- *   workspace    device scratch of bs_unified_attention_workspace() bytes
+ *   workspace    device scratch of bs_unified_attention_workspace() bytes; the call builds
+ *                its work units (request, KV head, key-tile range) on the host from ctx_len /
+ *                q_len and copies them into the workspace on `stream` from pageable memory, so
+ *                it is not CUDA-graph capturable (capture the decode loop around it instead)
  * Supported: head_dim = 128, page_size = 64, q_len[b] * H_q / H_kv <= 128.  Errors:
  * BS_ERR_INVALID (shapes), BS_ERR_CAPACITY (workspace too small), BS_ERR_CUDA. */
 bs_status bs_unified_attention_workspace(int32_t B, const int32_t* ctx_len, const int32_t* q_len, int32_t H_q,

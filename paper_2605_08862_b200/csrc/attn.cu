@@ -625,10 +625,12 @@ bs_status bs_unified_attention(const void* q, const void* k_cache, const void* v
     if ((int64_t)ws_bytes(p) > workspace_bytes) return BS_ERR_CAPACITY;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint8_t* w = static_cast<uint8_t*>(workspace);
+    cudaError_t put_err = cudaSuccess;
     auto put = [&](const void* src, size_t bytes) {
         uint8_t* d = w;
         w += align256(bytes);
-        if (bytes) cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);  // pageable: staged now
+        // pageable source: the runtime stages it before returning, so the host plan may go
+        if (bytes && put_err == cudaSuccess) put_err = cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
         return d;
     };
     AttnArgs a = {};
@@ -637,6 +639,7 @@ bs_status bs_unified_attention(const void* q, const void* k_cache, const void* v
     const int32_t* row_b = reinterpret_cast<const int32_t*>(put(p.row_b.data(), p.row_b.size() * 4));
     const int32_t* u0 = reinterpret_cast<const int32_t*>(put(p.bh_unit0.data(), p.bh_unit0.size() * 4));
     const int32_t* un = reinterpret_cast<const int32_t*>(put(p.bh_units.data(), p.bh_units.size() * 4));
+    if (put_err != cudaSuccess) return BS_ERR_CUDA;
     a.part_ml = reinterpret_cast<float*>(w);
     w += align256(p.units.size() * AT_ROWS * 2 * 4);
     a.part_o = reinterpret_cast<float*>(w);
