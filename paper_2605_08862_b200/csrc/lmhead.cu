@@ -243,15 +243,16 @@ lm_head_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_constant__
 }
 
 static bool lm_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
+    // resolved once per process (a function-local static: thread-safe initialisation)
+    static const PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult qr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
-            qr != cudaDriverEntryPointSuccess)
-            return false;
-        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
+        return (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+                qr == cudaDriverEntryPointSuccess)
+                   ? reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p)
+                   : nullptr;
+    }();
+    if (!enc) return false;
     const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
     const cuuint32_t box[2] = {(cuuint32_t)LM_BK, (cuuint32_t)box_rows};
