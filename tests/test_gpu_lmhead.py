@@ -147,3 +147,26 @@ def test_lm_head_full_size_sampled_rows(bs):
     bound = np.abs(r) * 2.0 ** -7 + d * 2.0 ** -24 * (hf @ wf.T)
     assert (np.abs(g - r) <= bound).all()
     assert (lg[sample].cpu().numpy().view(np.uint16) == ref).mean() > 0.99
+
+
+@pytest.mark.parametrize("zero_max", [False, True])
+def test_lm_head_stats_ties_and_zero_maxima(bs, zero_max):
+    """R1's ties: logits = s_r * w[v, 0] exactly (h one-hot), w[:, 0] drawn from a few values so
+    the row maximum repeats within and across 32-column chunks and tiles; with zero_max the
+    maximum is +-0 (the epilogue's per-element path).  The fused statistics must equal the GPU
+    logits' own (lowest column of the maximum, order-key ties as R1)."""
+    rows, d, V = 6, 64, 1000  # V not a multiple of 32: the last chunk straddles V
+    rng = np.random.default_rng(7 + zero_max)
+    h = np.zeros((rows, d), np.uint16)
+    h[:, 0] = np.where(np.arange(rows) % 2 == 0, 0x3F80, 0xBF80)  # +1 / -1
+    vals = np.array([-2.0, -1.0, 0.0] if zero_max else [-2.0, -1.0, 0.0, 1.0, 2.0], np.float32)
+    w = f32_to_bf16_bits(_vals(5, 22, V * d, 0.5)).reshape(V, d)
+    w[:, 0] = f32_to_bf16_bits(rng.choice(vals, V).astype(np.float32))
+    if zero_max:
+        h[1::2, 0] = 0x3F80  # every row +1: maximum 0
+    lg, key, bad = _gpu(bs, h, w)
+    m_ref, am_ref, bad_ref = row_stats(lg)
+    m, am = _decode_key(key)
+    np.testing.assert_array_equal(m, m_ref)
+    np.testing.assert_array_equal(am, am_ref)
+    assert not bad.any() and not bad_ref.any()
