@@ -88,6 +88,9 @@ def lib():
         L.orc_lookup.argtypes = [P(C.c_int32), P(C.c_int64), C.c_int32, P(C.c_int32), C.c_int32,
                                  C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32),
                                  P(C.c_int32)]
+        L.orc_lookup_conf.argtypes = [P(C.c_int32), P(C.c_int64), C.c_int32, P(C.c_int32), C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_int32, C.c_uint64, P(C.c_int32),
+                                      P(C.c_int32), P(C.c_int32)]
         L.orc_lookup_ngram.argtypes = [P(C.c_int32), P(C.c_int64), C.c_int32, P(C.c_int32),
                                        C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_int32),
                                        P(C.c_int32), P(C.c_int32)]
@@ -241,9 +244,14 @@ def verify_one_r(rows, T: float, top_p: float, pos: int, max_len: int, eos: int,
 
 
 # ---------------------------------------------------------------- lookup
-def lookup(pool_seqs, ctx, M: int, Lmin: int, K: int):
+def tau_fixed(min_token_prob: float) -> int:
+    """Reading C1: the confidence threshold as the integer round(tau * 2^32) in [0, 2^32]."""
+    return min(1 << 32, max(0, int(round(float(min_token_prob) * 4294967296.0))))
+
+
+def lookup(pool_seqs, ctx, M: int, Lmin: int, K: int, min_token_prob: float = 0.0):
     """Brute-force draft lookup over one prompt's pool (list of token sequences).
-    Returns (draft list, m_star)."""
+    min_token_prob > 0: confidence-scored drafts (reading C1).  Returns (draft list, m_star)."""
     lens = [len(s) for s in pool_seqs]
     off = np.zeros(len(pool_seqs) + 1, dtype=np.int64)
     off[1:] = np.cumsum(lens)
@@ -252,9 +260,9 @@ def lookup(pool_seqs, ctx, M: int, Lmin: int, K: int):
     c = np.ascontiguousarray(np.asarray(list(ctx) if len(ctx) else [0], dtype=np.int32))
     draft = np.zeros(max(K, 1), dtype=np.int32)
     q, ms = C.c_int32(), C.c_int32()
-    rc = lib().orc_lookup(_ptr(toks, C.c_int32), _ptr(off, C.c_int64), len(pool_seqs),
-                          _ptr(c, C.c_int32), len(ctx), M, Lmin, K, _ptr(draft, C.c_int32),
-                          C.byref(q), C.byref(ms))
+    rc = lib().orc_lookup_conf(_ptr(toks, C.c_int32), _ptr(off, C.c_int64), len(pool_seqs),
+                               _ptr(c, C.c_int32), len(ctx), M, Lmin, K, tau_fixed(min_token_prob),
+                               _ptr(draft, C.c_int32), C.byref(q), C.byref(ms))
     if rc != OK:
         raise OracleError(rc)
     return [int(x) for x in draft[: q.value]], ms.value

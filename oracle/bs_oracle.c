@@ -395,12 +395,28 @@ static int cmp_i32(const void* a, const void* b) {
     return x < y ? -1 : (x > y ? 1 : 0);
 }
 
+/* Confidence-scored drafts (draft-source variant; reading C1;    */
+/* P:405 "selects candidate tokens with higher confidence based on token node occurrence     */
+/* frequencies"; Arctic-style min_token_prob): the descent above stops before token c_j when   */
+/* its empirical probability cnt(w c_j) / cnt(w) -- cnt(w) = ALL occurrences of the current   */
+/* window w, including those that end a sequence -- is below tau = tau_q / 2^32, compared     */
+/* exactly in integers: cnt(w c_j) * 2^32 < tau_q * cnt(w).  tau_q = 0 is orc_lookup.          */
+int orc_lookup_conf(const int32_t* tokens, const int64_t* seq_off, int32_t n_seqs, const int32_t* ctx,
+                    int32_t ctx_len, int32_t M, int32_t Lmin, int32_t K, uint64_t tau_q, int32_t* draft,
+                    int32_t* q_out, int32_t* mstar_out);
+
 int orc_lookup(const int32_t* tokens, const int64_t* seq_off, int32_t n_seqs, const int32_t* ctx,
                int32_t ctx_len, int32_t M, int32_t Lmin, int32_t K, int32_t* draft,
                int32_t* q_out, int32_t* mstar_out) {
+    return orc_lookup_conf(tokens, seq_off, n_seqs, ctx, ctx_len, M, Lmin, K, 0ull, draft, q_out, mstar_out);
+}
+
+int orc_lookup_conf(const int32_t* tokens, const int64_t* seq_off, int32_t n_seqs, const int32_t* ctx,
+                    int32_t ctx_len, int32_t M, int32_t Lmin, int32_t K, uint64_t tau_q, int32_t* draft,
+                    int32_t* q_out, int32_t* mstar_out) {
     *q_out = 0;
     *mstar_out = 0;
-    if (M < 1 || Lmin < 1 || K < 0) return ORC_ERR_INVALID;
+    if (M < 1 || Lmin < 1 || K < 0 || tau_q > (1ull << 32)) return ORC_ERR_INVALID;
     int32_t mmax = ctx_len < M ? ctx_len : M;
     int32_t mstar = 0;
     /* anchor: longest suffix with a continuation */
@@ -442,6 +458,8 @@ int orc_lookup(const int32_t* tokens, const int64_t* seq_off, int32_t n_seqs, co
             if (b - a > best_n) { best_n = b - a; best = kids[a]; } /* strict >: lowest id on ties */
             a = b;
         }
+        /* reading C1: cnt(w c_j) / cnt(w) below tau stops the draft (n_occ = cnt(w)) */
+        if ((uint64_t)best_n * (1ull << 32) < tau_q * (uint64_t)n_occ) break;
         draft[q++] = best;
         int64_t keep = 0;
         for (int64_t o = 0; o < n_occ; ++o)

@@ -35,17 +35,17 @@ def pools_by_prompt(seq_prompt, seq_off, tokens):
 
 def step(ro: OracleRollout, pools: dict, row_fn, *, k: int, M: int, Lmin: int, T: float,
          top_p: float, seed: int, eos: int, timers: dict | None = None, top_k: int = 0,
-         ngram: tuple | None = None):
+         ngram: tuple | None = None, min_token_prob: float = 0.0):
     """One decoding step of one rollout.  row_fn(P, positions, prevs, uid) -> list of bf16 rows.
     ngram = (n_min, n_max): draft with the n-gram linear-scan drafter (reading N1) instead of
-    the suffix lookup."""
+    the suffix lookup; min_token_prob > 0: confidence-scored suffix drafts (reading C1)."""
     from . import lookup, lookup_ngram, verify_one
 
     if ro.finished or ro.pos >= ro.max_len:
         return None
     t0 = time.perf_counter()
     if ngram is None:
-        draft, mstar = lookup(pools.get(ro.prompt, []), ro.context[-M:], M, Lmin, k)
+        draft, mstar = lookup(pools.get(ro.prompt, []), ro.context[-M:], M, Lmin, k, min_token_prob)
     else:
         draft, mstar = lookup_ngram(pools.get(ro.prompt, []), ro.context[-M:], ngram[0], ngram[1], k)
     q = min(len(draft), k, max(0, ro.max_len - ro.pos - 1))
@@ -70,12 +70,12 @@ def step(ro: OracleRollout, pools: dict, row_fn, *, k: int, M: int, Lmin: int, T
 
 
 def run_rollouts(rollouts, pools, row_fn, *, k, M, Lmin, T, top_p, seed, eos, max_steps=None,
-                 timers=None, top_k=0, ngram=None):
+                 timers=None, top_k=0, ngram=None, min_token_prob=0.0):
     for ro in rollouts:
         n = 0
         while not ro.finished and (max_steps is None or n < max_steps):
             step(ro, pools, row_fn, k=k, M=M, Lmin=Lmin, T=T, top_p=top_p, seed=seed, eos=eos,
-                 timers=timers, top_k=top_k, ngram=ngram)
+                 timers=timers, top_k=top_k, ngram=ngram, min_token_prob=min_token_prob)
             n += 1
     return rollouts
 

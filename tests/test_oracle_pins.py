@@ -592,9 +592,10 @@ def test_empty_pool_is_plain_decoding(orc):
 
 
 # ------------------------------------------------------------------ lookup
-def _trie_lookup(pool, ctx, M, Lmin, K):
+def _trie_lookup(pool, ctx, M, Lmin, K, tau_q=0):
     """Independent route to the lookup definition: count every window of the pool with
-    a Python Counter (a depth-bounded suffix trie), then anchor + greedy descent."""
+    a Python Counter (a depth-bounded suffix trie), then anchor + greedy descent; tau_q > 0:
+    stop before a child whose count is below tau_q / 2^32 of its node's count (reading C1)."""
     from collections import Counter
 
     D = M + K + 1
@@ -620,6 +621,8 @@ def _trie_lookup(pool, ctx, M, Lmin, K):
         if not kids:
             break
         best = min(kids, key=lambda t: (-kids[t], t))
+        if kids[best] * (1 << 32) < tau_q * cnt[tuple(w)]:
+            break
         out.append(best)
         w.append(best)
     return out, mstar
@@ -722,3 +725,45 @@ def test_ngram_vs_backward_match_scan(orc):
                 best = (n, pos, seq[e + 1:e + 1 + K])
         want = (best[2], best[0]) if best[2] is not None else ([], 0)
         assert orc.lookup_ngram(pool, ctx, n_min, n_max, K) == ([int(x) for x in want[0]], want[1])
+
+
+# ------------------------------------------------------------------ confidence-scored drafts (C1)
+def test_lookup_conf_hand_example(orc):
+    """Reading C1 on the S:154 pool: after the anchor "1 2" (3 occurrences) the greedy child 3
+    has probability 2/3, so it is drafted for tau <= 2/3 and not above; tau = 0 is the plain
+    lookup; a unique continuation (probability 1) survives tau = 1."""
+    pool = [[1, 2, 3], [1, 2, 3], [1, 2, 5]]
+    assert orc.lookup(pool, [9, 1, 2], 8, 1, 4, 0.0) == orc.lookup(pool, [9, 1, 2], 8, 1, 4)
+    assert orc.lookup(pool, [9, 1, 2], 8, 1, 4, 0.5) == ([3], 2)
+    assert orc.lookup(pool, [9, 1, 2], 8, 1, 4, 2.0 / 3.0 - 1e-9) == ([3], 2)
+    assert orc.lookup(pool, [9, 1, 2], 8, 1, 4, 0.7) == ([], 2)
+    # "7 8" occurs once and continues: every step has probability 1
+    assert orc.lookup([[7, 8, 9, 10, 11]], [7, 8], 8, 1, 3, 1.0) == ([9, 10, 11], 2)
+    # a window that also ends a sequence: cnt(w) counts that occurrence (2 of 3 continue with 4)
+    assert orc.lookup([[3, 4], [3, 4], [3]], [3], 8, 1, 2, 0.6) == ([4], 1)
+    assert orc.lookup([[3, 4], [3, 4], [3]], [3], 8, 1, 2, 0.7) == ([], 1)
+
+
+def test_lookup_conf_vs_trie_random(orc):
+    """Random pools: the thresholded oracle == the independent trie with the same rule, the
+    drafts are prefixes of the plain drafts and shrink as tau grows, and at tau = 1 every
+    drafted token is the continuation of ALL occurrences of its window."""
+    rng = np.random.default_rng(11)
+    for t in range(150):
+        V = int(rng.integers(2, 5))
+        pool = [[int(x) for x in rng.integers(0, V, int(rng.integers(0, 14)))] for _ in range(int(rng.integers(0, 6)))]
+        for _ in range(4):
+            ctx = [int(x) for x in rng.integers(0, V, int(rng.integers(1, 9)))]
+            M, Lmin, K = int(rng.integers(1, 6)), int(rng.integers(1, 3)), int(rng.integers(1, 6))
+            plain = orc.lookup(pool, ctx, M, Lmin, K)
+            prev = plain[0]
+            for tau in (0.25, 0.5, 0.75, 1.0):
+                got = orc.lookup(pool, ctx, M, Lmin, K, tau)
+                assert got == _trie_lookup(pool, ctx, M, Lmin, K, orc.tau_fixed(tau))
+                assert got[1] == plain[1] and got[0] == prev[:len(got[0])]
+                prev = got[0]
+            w = ctx[len(ctx) - plain[1]:] if plain[1] else []
+            for tok in prev:  # tau = 1: deterministic continuations only
+                occ = [(s, i) for s in pool for i in range(len(s) - len(w) + 1) if s[i:i + len(w)] == w]
+                assert occ and all(i + len(w) < len(s) and s[i + len(w)] == tok for s, i in occ)
+                w = w + [tok]
