@@ -154,6 +154,16 @@ bs_status bs_draft_pool_put(bs_ctx* ctx, uint64_t rl_step, int32_t n_seqs,
  * another rl_step then return BS_ERR_STALE. */
 bs_status bs_draft_pool_seal(bs_ctx* ctx, uint64_t rl_step, void* stream);
 
+/* Confidence-scored drafts (draft-source variant; "candidate tokens with
+ * higher confidence based on token node occurrence frequencies"; reading C1): from
+ * the NEXT bs_draft_pool_seal on, the greedy descent of every draft stops before a token whose
+ * empirical probability cnt(w c) / cnt(w) in the prompt's pool is below min_token_prob (cnt(w)
+ * counts every occurrence of the current window w, also those ending a sequence), compared
+ * exactly as cnt(w c) * 2^32 < round(min_token_prob * 2^32) * cnt(w).  The anchor is chosen as
+ * before; a low-confidence first token gives an empty draft.  0 (the default) is the plain
+ * greedy descent.  Host-only (no stream work).  BS_ERR_INVALID unless 0 <= min_token_prob <= 1. */
+bs_status bs_draft_set_min_token_prob(bs_ctx* ctx, float min_token_prob);
+
 /* Cross-rank draft exchange: all-gather the staging pools of all
  * ranks of `nccl_comm` (an ncclComm_t of world size R, this rank = rank) and keep
  * only sequences whose prompt_id % R == rank.  Replaces the staging pool with the

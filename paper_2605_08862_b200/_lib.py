@@ -66,6 +66,7 @@ SIGNATURES = {
     "bs_lm_head_logits": (C.c_int, [_V, _V, _I32, _I32, _I32, _V, _I64, _V, _V, _V]),
     "bsx_set_row_stats": (C.c_int, [_V, _V, _V]),
     "bs_draft_lookup_ngram": (C.c_int, [_V, _U64, _I32, _V, _I32, _I32, _I32, _V, _V, _V, _V]),
+    "bs_draft_set_min_token_prob": (C.c_int, [_V, C.c_float]),
     "bs_verify_commit": (C.c_int, [_V, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V, _V,
                                    _V, _V, _V, _V, _V]),
     "bs_verify_commit_lookup": (C.c_int, [_V, _U64, _I32, _V, _V, _V, _I64, _V, _V, _I32, bs_sampling, _V,

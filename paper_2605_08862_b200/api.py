@@ -98,6 +98,10 @@ class Context:
                                             n_tokens, _stream(stream, self.device)),
              "bs_draft_pool_put")
 
+    def bs_draft_set_min_token_prob(self, min_token_prob: float):
+        _chk(self, load().bs_draft_set_min_token_prob(self.handle, float(min_token_prob)),
+             "bs_draft_set_min_token_prob")
+
     def bs_draft_pool_seal(self, rl_step, stream=None):
         _chk(self, load().bs_draft_pool_seal(self.handle, rl_step, _stream(stream, self.device)),
              "bs_draft_pool_seal")

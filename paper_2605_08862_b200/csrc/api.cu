@@ -329,6 +329,15 @@ bs_status bs_draft_lookup(bs_ctx* c, uint64_t rl_step, int32_t n, const int32_t*
     return BS_OK;
 }
 
+bs_status bs_draft_set_min_token_prob(bs_ctx* c, float min_token_prob) {
+    if (!c) return fail(nullptr, BS_ERR_INVALID, "null ctx");
+    if (!(min_token_prob >= 0.f && min_token_prob <= 1.f))
+        return fail(c, BS_ERR_INVALID, "min_token_prob must be in [0, 1]");
+    // reading C1: the threshold as round(tau * 2^32) in [0, 2^32], used by the next seal
+    c->tau_q = (uint64_t)llround((double)min_token_prob * 4294967296.0);
+    return BS_OK;
+}
+
 bs_status bs_draft_lookup_ngram(bs_ctx* c, uint64_t rl_step, int32_t n, const int32_t* slots, int32_t k,
                                 int32_t n_min, int32_t n_max, int32_t* draft_tokens, int32_t* draft_len,
                                 int32_t* match_len, void* stream) {

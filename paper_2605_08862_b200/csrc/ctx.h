@@ -131,6 +131,7 @@ struct bs_ctx {
     bs_config cfg;
     int S = 0;  // mass shift (reading R4)
     int M = 0;  // match_max
+    uint64_t tau_q = 0;  // confidence threshold round(min_token_prob * 2^32) for the next seal (C1)
     std::string err;
     int num_sms = 148;
     int verify_kind = 0;  // bsx_set_verify_kernel (0: auto)

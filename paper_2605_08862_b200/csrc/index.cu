@@ -138,7 +138,7 @@ __global__ void child_ranges_kernel(int nruns_child, const int32_t* parent, int3
 
 // Descending pass at level l: greedy path end points for non-unique runs, table inserts
 // for l <= M (non-unique windows, and first-unique windows).
-__global__ void level_paths_kernel(int l, int M, int K, int top, Level lv, Level ch,
+__global__ void level_paths_kernel(int l, int M, int K, uint64_t tau_q, int top, Level lv, Level ch,
                                    const int32_t* cbeg, const int32_t* cend, const int32_t* pq_child,
                                    const int32_t* po_child, int32_t* pq, int32_t* po,
                                    const int32_t* T, const int32_t* seq_end_of,
@@ -150,6 +150,7 @@ __global__ void level_paths_kernel(int l, int M, int K, int top, Level lv, Level
         const int i0 = lv.pos_sorted[rs];
         if (size == 1) continue;  // unique windows: first_unique_kernel
         int q = 0, occ = i0;
+        bool cont = false;  // the window has a continuation (anchor eligibility, L2)
         if (!top) {
             const int c0 = cbeg[R], c1 = cend[R];
             int best = -1, bsz = 0;
@@ -160,7 +161,10 @@ __global__ void level_paths_kernel(int l, int M, int K, int top, Level lv, Level
                     best = C;
                 }
             }
-            if (best >= 0) {
+            cont = best >= 0;
+            // reading C1: the greedy child's empirical probability bsz / size below tau ends the
+            // draft here (q = 0); a child that passes continues with ITS (already gated) draft
+            if (cont && ((uint64_t)bsz << 32) >= tau_q * (uint64_t)size) {
                 const int cpos = ch.pos_sorted[ch.runstart[best]];
                 if (bsz == 1) {
                     occ = cpos;
@@ -174,7 +178,7 @@ __global__ void level_paths_kernel(int l, int M, int K, int top, Level lv, Level
         pq[R] = q;
         po[R] = occ;
         if (l <= M) {
-            const uint32_t meta = (uint32_t)q | (q > 0 ? META_CONT : 0u);
+            const uint32_t meta = (uint32_t)q | (cont ? META_CONT : 0u);
             table_insert(table, mask, window_key(hash_window(T, occ, l), prompt_of[occ], l),
                          (uint32_t)occ, meta, dev_err);
         }
@@ -379,7 +383,7 @@ cudaError_t seal_index(bs_ctx* ctx, cudaStream_t st, std::string& why) {
             if (ch.nruns > 0) child_ranges_kernel<<<gc, 256, 0, st>>>(ch.nruns, ch.parent, cbeg.p, cend.p);
         }
         const int gr = std::max(1, std::min(ctx->num_sms * 8, (lv.nruns + 255) / 256));
-        level_paths_kernel<<<gr, 256, 0, st>>>(l, M, K, top, lv, ch, cbeg.p, cend.p, pq_child, po_child, pq, po,
+        level_paths_kernel<<<gr, 256, 0, st>>>(l, M, K, ctx->tau_q, top, lv, ch, cbeg.p, cend.p, pq_child, po_child, pq, po,
                                                T, ctx->seq_end_of.p, ctx->prompt_of.p, fu.p, ctx->table.p,
                                                ctx->table_mask, ctx->dev_err.p);
         BS_TRY(cudaGetLastError());

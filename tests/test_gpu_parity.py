@@ -274,8 +274,10 @@ def test_verify_error_only_if_needed(bs, orc, path, V):
 
 # ------------------------------------------------------------------ lookup
 def _gpu_lookup(bs, ctx, seq_prompt, seq_off, tokens, ctxs, prompt_of, k, M, max_len=1 << 20,
-                rl_step=1, ngram=None):
+                rl_step=1, ngram=None, min_token_prob=None):
     n = len(ctxs)
+    if min_token_prob is not None:
+        ctx.bs_draft_set_min_token_prob(min_token_prob)  # applies from the seal below (C1)
     ctx.bs_draft_pool_put(rl_step, to_dev(seq_prompt.astype(np.int32)), to_dev(seq_off),
                           to_dev(tokens.astype(np.int32)) if len(tokens) else
                           to_dev(np.zeros(1, np.int32)), int(len(tokens)))
@@ -344,11 +346,14 @@ def test_ngram_lookup_parity_random_pools(bs, orc, vocab, n_min, n_max, M, k):
         assert int(ml[b]) == n, b
 
 
-@pytest.mark.parametrize("vocab,Lmin,M,k", [(3, 1, 8, 4), (5, 1, 6, 3), (4, 2, 8, 5),
-                                            (50, 1, 32, 8), (2, 1, 32, 16)])
-def test_lookup_parity_random_pools(bs, orc, vocab, Lmin, M, k):
+@pytest.mark.parametrize("vocab,Lmin,M,k,tau", [(3, 1, 8, 4, 0.0), (5, 1, 6, 3, 0.0), (4, 2, 8, 5, 0.0),
+                                                (50, 1, 32, 8, 0.0), (2, 1, 32, 16, 0.0),
+                                                (3, 1, 8, 4, 0.3), (4, 2, 8, 5, 0.5), (2, 1, 32, 16, 0.6),
+                                                (5, 1, 6, 3, 1.0), (50, 1, 32, 8, 0.34)])
+def test_lookup_parity_random_pools(bs, orc, vocab, Lmin, M, k, tau):
     """random pools x prefixes, GPU index lookup == brute-force oracle (drafts and
-    anchor length), several prompts per pool."""
+    anchor length), several prompts per pool; tau > 0: confidence-scored drafts (reading C1,
+    the threshold applied by the index build, the oracle's descent stops at the same step)."""
     rng = np.random.default_rng(vocab * 100 + M)
     n_prompts = 6
     seqs, sp = [], []
@@ -375,12 +380,13 @@ def test_lookup_parity_random_pools(bs, orc, vocab, Lmin, M, k):
         pof.append(P)
     ctx = bs.Context(vocab=vocab, k_max=k, match_max=M, match_min=Lmin, max_rollouts=len(ctxs),
                      pool_capacity_tokens=max(1, len(tokens)), pool_capacity_seqs=max(1, len(seqs)))
-    d, dl, ml = _gpu_lookup(bs, ctx, np.asarray(sp, np.int32), off, tokens, ctxs, pof, k, M)
+    d, dl, ml = _gpu_lookup(bs, ctx, np.asarray(sp, np.int32), off, tokens, ctxs, pof, k, M,
+                            min_token_prob=tau if tau else None)
     pools = {}
     for s, P in zip(seqs, sp):
         pools.setdefault(P, []).append([int(x) for x in s])
     for b, c in enumerate(ctxs):
-        want_d, want_m = orc.lookup(pools.get(pof[b], []), c[-M:], M, Lmin, k)
+        want_d, want_m = orc.lookup(pools.get(pof[b], []), c[-M:], M, Lmin, k, tau)
         assert list(d[b, : dl[b]]) == want_d, (b, c, want_d, d[b], dl[b])
         assert int(ml[b]) == want_m, (b, c, ml[b], want_m)
 
@@ -400,9 +406,11 @@ def test_lookup_stale_and_clamp(bs, orc):
         ctx.bs_draft_lookup(2, slots, k, z, z[:, 0].contiguous())
 
 
-def test_lookup_index_on_perturbed_pools(bs, orc):
+@pytest.mark.parametrize("tau", [0.0, 0.9])  # 0.9: shortens 688 -> 534 drafted tokens here
+def test_lookup_index_on_perturbed_pools(bs, orc, tau):
     """Qwen-shaped vocab, pools = 16 perturbed copies of a reference text (the bench's
-    recipe): GPU == oracle on contexts sampled along the reference."""
+    recipe): GPU == oracle on contexts sampled along the reference (tau > 0:
+    confidence-scored drafts, reading C1)."""
     spec = TargetSpec(V=151936, nbank=64, mode="position")
     M, k = 32, 8
     prompts, tails, *_ = setup_rollouts(spec, 3, 1, M, 100)
@@ -421,12 +429,15 @@ def test_lookup_index_on_perturbed_pools(bs, orc):
             pof.append(int(P))
     ctx = bs.Context(vocab=spec.V, k_max=k, match_max=M, max_rollouts=len(ctxs),
                      pool_capacity_tokens=len(tok), pool_capacity_seqs=len(sp))
-    d, dl, ml = _gpu_lookup(bs, ctx, sp, off, tok, ctxs, pof, k, M)
+    d, dl, ml = _gpu_lookup(bs, ctx, sp, off, tok, ctxs, pof, k, M, min_token_prob=tau)
     pools = {}
     for s_i, P in enumerate(sp):
         pools.setdefault(int(P), []).append([int(x) for x in tok[off[s_i]:off[s_i + 1]]])
+    if tau:  # the threshold must actually shorten some drafts on this workload
+        plain = [len(orc.lookup(pools[pof[b]], c[-M:], M, 1, k)[0]) for b, c in enumerate(ctxs)]
+        assert sum(plain) > int(dl.sum())
     for b, c in enumerate(ctxs):
-        want_d, want_m = orc.lookup(pools[pof[b]], c[-M:], M, 1, k)
+        want_d, want_m = orc.lookup(pools[pof[b]], c[-M:], M, 1, k, tau)
         assert list(d[b, : dl[b]]) == want_d and int(ml[b]) == want_m, b
 
 

@@ -114,6 +114,49 @@ def test_tiny_rollouts_top_k(bs, orc, top_k, top_p):
     assert eng.stats()["proposed"] > 0
 
 
+@pytest.mark.parametrize("tau", [0.3, 0.6])
+def test_tiny_rollouts_confidence_scored_drafts(bs, orc, tau):
+    """TINY rollouts with confidence-scored suffix drafts (f4, reading C1: the index build stops
+    each greedy descent at the first child below min_token_prob), fused verify + commit + lookup
+    under graph replay: token-for-token vs the oracle's loop with the same threshold, and fewer
+    drafted tokens than without the threshold."""
+    spec = TargetSpec(V=1024, nbank=256, mode="position", beta=12.0)
+    M, k, L, seed, eos = 16, 4, 48, 21, -1
+    prompts, tails, pid, tail_rows, uids, ml = setup_rollouts(spec, 2, 3, M, L)
+    pools_np = pools_for(spec, prompts, tails, 4, np.full(8, 44), 0.7, prefix=M)
+    n = len(pid)
+    ctx, eng = _engine(bs, spec, n, k, M, 1.0, 1.0, seed, eos, len(pools_np[2]), len(pools_np[0]))
+    ctx.bs_draft_set_min_token_prob(tau)
+    resp = torch.full((n, L), -1, dtype=torch.int32, device="cuda")
+    ctx.bs_rollout_bind_output(resp, L)
+    eng.put_pools(1, to_dev(pools_np[0]), to_dev(pools_np[1]), to_dev(pools_np[2]))
+    eng.seal(1)
+    eng.begin(to_dev(uids.view(np.int64)), to_dev(pid), to_dev(tail_rows), to_dev(ml))
+    eng.run_until_done(chunk=8, use_graph=True)
+    torch.cuda.synchronize()
+    assert ctx.bs_sync_status() == 0
+    got = resp.cpu().numpy()
+    from oracle.rollout import OracleRollout, bank_row_fn, pools_by_prompt, run_rollouts
+
+    def oracle_run(t):
+        ros = [OracleRollout(prompt=int(pid[b]), uid=int(uids[b]),
+                             context=[int(x) for x in tail_rows[b] if x >= 0], max_len=int(ml[b]))
+               for b in range(n)]
+        run_rollouts(ros, pools_by_prompt(*pools_np), bank_row_fn(spec), k=k, M=M, Lmin=1, T=1.0,
+                     top_p=1.0, seed=seed, eos=eos, min_token_prob=t)
+        return ros
+
+    ros = oracle_run(tau)
+    for b, ro in enumerate(ros):
+        assert [int(x) for x in got[b, : len(ro.generated)]] == ro.generated, b
+    st = eng.stats()
+    assert st["accepted"] == sum(s_[4] for ro in ros for s_ in ro.steps)
+    assert st["proposed"] == sum(s_[0] for ro in ros for s_ in ro.steps)
+    plain = oracle_run(0.0)
+    assert st["proposed"] / st["decode_steps"] < (sum(s_[0] for ro in plain for s_ in ro.steps)
+                                                  / sum(len(ro.steps) for ro in plain))
+
+
 @pytest.mark.parametrize("ngram", [(1, 4), (2, 8)])
 def test_tiny_rollouts_ngram_drafts(bs, orc, ngram):
     """TINY rollouts drafted by the n-gram linear-scan drafter (f4, reading N1) under graph
