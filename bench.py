@@ -193,6 +193,8 @@ def run_ours(args, cfg, rank, world, dist, warmup, steps, bind_step0=False, e2e=
     eng = RolloutEngine(ctx, n, k, cfg["T"], cfg["top_p"],
                         Target(bank, cfg["nbank"], spec.target_seed, TARGET_MODES[spec.mode]), stream=stream,
                         plain=cfg.get("plain", False), ngram=cfg.get("ngram"))
+    if cfg.get("min_token_prob"):  # f4: confidence-scored suffix drafts (reading C1), from the first seal
+        ctx.bs_draft_set_min_token_prob(cfg["min_token_prob"])
     comm = nccl_comm(bs, dist, rank, world)
 
     def dev_t(a):
@@ -544,6 +546,8 @@ def sweep_configs():
     # f4 draft-source ablation (the paper's Table 7): the n-gram linear-scan drafter
     # on the same workload as k8_r0.8 (suffix index)
     pts.append(("ngram_k8_r0.8", dict(base, ngram=(1, 32))))
+    # ... and confidence-scored suffix drafts (reading C1, Arctic-style min_token_prob)
+    pts += [("conf%g_k8_r0.8" % t, dict(base, min_token_prob=t)) for t in (0.3, 0.6)]
     return pts
 
 
@@ -671,7 +675,9 @@ def main():
         s2 = summarize(c2, name, r2, args, hbm)
         s2["ms_per_step"] = r2["agg"]["elapsed_ms"] / SWEEP_STEPS[1]
         rec2 = {"point": name, "k": c2["k"], "match_rate": c2["match_rate"], "plain": c2.get("plain", False),
-                "drafter": "none" if c2.get("plain") else ("ngram" if c2.get("ngram") else "suffix index"),
+                "drafter": "none" if c2.get("plain") else ("ngram" if c2.get("ngram") else (
+                    "suffix index, min_token_prob %g" % c2["min_token_prob"] if c2.get("min_token_prob")
+                    else "suffix index")),
                 "value": s2["value"], "unit": unit, "ms_per_rl_step": s2["ms_per_step"],
                 "acceptance_length": r2["st"]["acceptance_length"],
                 "decode_steps_per_rollout": r2["st"]["decode_steps"] / r2["n"],
