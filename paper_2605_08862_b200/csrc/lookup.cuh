@@ -123,6 +123,14 @@ __device__ __forceinline__ void lookup_rollout(const LookupArgs& a, const IndexD
         const unsigned contm = __ballot_sync(0xFFFFFFFFu, found && (meta & META_CONT)) & hit & lim;
         if (contm == 0) break;
         const int ms = 32 - __clz(contm);
+        if (ms == m0) {  // the checked m0 window itself: its continuation is already loaded
+            mstar = m0;
+            q = qm;
+            dstart = (int)occ0 + m0;
+            dpre = tcont;
+            dpre_ok = true;
+            break;
+        }
         const uint32_t occs = __shfl_sync(0xFFFFFFFFu, occ, ms - 1);
         const uint32_t metas = __shfl_sync(0xFFFFFFFFu, meta, ms - 1);
         bool oks = true;

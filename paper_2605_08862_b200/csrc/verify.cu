@@ -98,7 +98,7 @@ __device__ __forceinline__ void trace_ev(int type, int seq, int b, int j) {
     } while (0)
 #endif
 enum { TR_CLAIM0 = 0, TR_CLAIM1 = 1, TR_TMA = 2, TR_MAX0 = 3, TR_MAX1 = 4, TR_MASS0 = 5, TR_MASS1 = 6,
-       TR_EPI0 = 7, TR_EPI1 = 8, TR_END = 9, TR_FIN = 10, TR_SPINS = 11, TR_SC = 12, TR_SQPOP = 13, TR_ITER = 14, TR_MASSL = 15, TR_START = 16, TR_GO = 17, TR_PLANNED = 18 };
+       TR_EPI0 = 7, TR_EPI1 = 8, TR_END = 9, TR_FIN = 10, TR_SPINS = 11, TR_SC = 12, TR_SQPOP = 13, TR_ITER = 14, TR_MASSL = 15, TR_START = 16, TR_GO = 17, TR_PLANNED = 18, TR_PDESC = 19, TR_POST = 20, TR_LOOP = 21, TR_BCAST = 22 };
 
 
 struct VerifyArgs {
@@ -346,8 +346,11 @@ __device__ bool complete_row(const VerifyArgs& a, unsigned long long* stat, int 
 // row i's normaliser / Z, the deciding row F's status and candidate; row j's own values come
 // from registers).  Returns (all lanes) whether this row finalized the rollout's step; then
 // no = emitted tokens and lane i holds emitted token i (inputs of the fused commit).
+// dpf: lane i's draft token d_{i+1} (lane < q) if the caller prefetched it, else DPF_NONE.
+constexpr int32_t DPF_NONE = -0x7FFFFFFF;
 __device__ bool complete_row_warp(const VerifyArgs& a, unsigned long long* stat, int b, int j, int q, int status,
-                                  int cand, unsigned long long z, float norm, int lane, int& no, int32_t& tok) {
+                                  int cand, unsigned long long z, float norm, int lane, int& no, int32_t& tok,
+                                  int32_t dpf = DPF_NONE) {
     const int kp1 = a.k + 1;
     const int64_t base = (int64_t)b * kp1;
     int F = -1;
@@ -373,7 +376,7 @@ __device__ bool complete_row_warp(const VerifyArgs& a, unsigned long long* stat,
     float nl = 0.f;
     unsigned long long zl = 0ull;
     // d_{F+1} is needed only for an accepted EOS at row F (this row's status is known)
-    if (lane < F || (lane == F && lane < q && (F != j || status == ST_EOS))) dl = d[lane];
+    if (lane < F || (lane == F && lane < q && (F != j || status == ST_EOS))) dl = (dpf != DPF_NONE) ? dpf : d[lane];
     if (lane <= F) {
         nl = (lane == j) ? norm : __ldcg(a.row_norm + base + lane);
         zl = (lane == j) ? z : __ldcg(a.row_z + base + lane);

@@ -359,27 +359,60 @@ struct ClaimState {
     bool eager = false;
     bool static_done = false;  // the static cursor is exhausted
     int spec_b = -1, spec_r = 0;  // chain this cluster just continued: speculate its next row
-    int sidx = 0;              // next entry of this cluster's share of the static list
-    int pre_idx = -1;          // prefetched entry (index, value)
-    unsigned long long pre_e = 0;
+    int sidx = 0;              // next entry of this cluster's share of the static list (uniform)
+    int sh_base = -1;          // share position of the window held in registers (-1: none)
+    unsigned long long my_e = 0;  // lane l: live-list entry of share position sh_base + l
     TakeIssue pc;              // pre-issued claim of the next static row (pc.b < 0: none)
+    bool post = false;         // ck_post is due after the broadcast
 };
 
-// Pre-issue the claim of this cluster's next static row if its live-list entry (prefetched)
-// is already published: the atomic and loads complete while the current row is processed.
-__device__ __forceinline__ void ck_preissue(const VerifyArgs& a, uint32_t epoch, int lane, ClaimState& cs,
-                                            int nlive, int nstatic) {
-    int b = -1;
-    if (lane == 0 && cs.sidx < nstatic && cs.pre_idx == cs.sidx && (uint32_t)(cs.pre_e >> 32) == epoch) {
-        b = (int)(uint32_t)cs.pre_e;
-        cs.sidx += a.ncl;
-        if (cs.sidx < nstatic) {
-            cs.pre_idx = cs.sidx;
-            cs.pre_e = ld_acquire_u64(a.live + cs.sidx % nlive);
-        }
+// Load a window of 32 entries of this cluster's share of the static list (share position
+// p = base + lane is static entry cid + p * ncl) in one round of acquire loads, so the claims'
+// record loads are ordered after the planners' publication.  Entries not yet published (the
+// plan count precedes the list stores) are polled again.
+__device__ __forceinline__ void ck_share_load(const VerifyArgs& a, uint32_t epoch, int lane, ClaimState& cs,
+                                              int nstatic, int base) {
+    const int cid = (int)(blockIdx.x / CK_CL);
+    const int s = cid + (base + lane) * a.ncl;
+    bool need = s < nstatic;
+    unsigned long long e = 0;
+    for (;;) {
+        if (need) e = ld_acquire_u64(a.live + s % cs.nlive);
+        need = need && (uint32_t)(e >> 32) != epoch;
+        if (!__any_sync(0xFFFFFFFFu, need)) break;
+        __nanosleep(32);
     }
-    b = __shfl_sync(0xFFFFFFFFu, b, 0);
-    if (b >= 0) cs.pc = ck_take_issue(a, b, lane, 0);
+    cs.sh_base = base;
+    cs.my_e = e;
+}
+
+// The rollout of static entry cs.sidx, from the register window (loading the next window when
+// the share runs past it).
+__device__ __forceinline__ int ck_share_get(const VerifyArgs& a, uint32_t epoch, int lane, ClaimState& cs,
+                                            int nstatic) {
+    const int cid = (int)(blockIdx.x / CK_CL);
+    const int k = (cs.sidx - cid) / a.ncl;
+    if (cs.sh_base < 0 || k - cs.sh_base >= 32) ck_share_load(a, epoch, lane, cs, nstatic, k);
+    return (int)(uint32_t)shfl_u64(cs.my_e, k - cs.sh_base);
+}
+
+// Pre-issue the claim of this cluster's next static row: the atomic and loads complete while
+// the current row is processed (at a window boundary the next static claim loads the window).
+__device__ __forceinline__ void ck_preissue(const VerifyArgs& a, uint32_t epoch, int lane, ClaimState& cs,
+                                            int nstatic) {
+    if (cs.sidx >= nstatic) return;
+    const int cid = (int)(blockIdx.x / CK_CL);
+    const int k = (cs.sidx - cid) / a.ncl;
+    if (cs.sh_base < 0 || k - cs.sh_base >= 32) return;
+    const int b = (int)(uint32_t)shfl_u64(cs.my_e, k - cs.sh_base);
+    cs.sidx += a.ncl;
+    cs.pc = ck_take_issue(a, b, lane, 0);
+}
+
+// Deferred claim bookkeeping, run by the claimer once it has broadcast the row it just claimed
+// (nothing is issued between a claim and its broadcast): pre-issue the next static claim.
+__device__ __forceinline__ void ck_post(const VerifyArgs& a, uint32_t epoch, int lane, ClaimState& cs) {
+    if (!cs.eager && cs.pc.b < 0) ck_preissue(a, epoch, lane, cs, cs.nlive);
 }
 
 __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch, int lane, bool queues, int rot,
@@ -405,7 +438,7 @@ __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch,
         // list then enumerates every row, j-major, and a cluster leaves once it is exhausted
         cs.eager = a.eager_ok == 2 || (a.eager_ok && (long long)cs.nlive * (a.k + 1) <= (long long)CK_NB * a.ncl);
         cs.sidx = cid;
-        cs.pre_idx = -1;
+        cs.sh_base = -1;
     }
     const int nlive = cs.nlive;
     const bool eager = cs.eager;
@@ -427,47 +460,36 @@ __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch,
             }
         }
         // 2. this cluster's share of the static list (entries cid, cid + ncl, ...: no shared
-        //    cursor); the next entry is prefetched so a static claim costs one round trip.
+        //    cursor); the share is held in registers, 32 entries per window, and the next
+        //    static claim is pre-issued, so a static claim costs no dependent round trip.
         //    Other clusters' unclaimed rows 0 are stolen by the scan once a share is done.
         // 2a. the static row whose claim was pre-issued by the previous static claim
         if (!eager && cs.pc.b >= 0) {
             const TakeIssue t = cs.pc;
             cs.pc.b = -1;
-            const bool ok = ck_take_finish(a, epoch, t, SRC_STATIC, lane, out);
-            ck_preissue(a, epoch, lane, cs, nlive, nstatic);
-            if (ok) return out;
+            if (ck_take_finish(a, epoch, t, SRC_STATIC, lane, out)) {
+                cs.post = true;
+                return out;
+            }
+            ck_post(a, epoch, lane, cs);
             continue;
         }
         int b = -1, j = 0;
         if (!cs.static_done) {
-            if (lane == 0 && cs.sidx < nstatic) {
-                const int s = cs.sidx;
-                const unsigned long long* lp = a.live + s % nlive;
-                unsigned long long e = (cs.pre_idx == s) ? cs.pre_e : ld_acquire_u64(lp);
-                while ((uint32_t)(e >> 32) != epoch) {  // entry not yet published
-                    __nanosleep(32);
-                    e = ld_acquire_u64(lp);
-                }
-                b = (int)(uint32_t)e;
-                j = s / nlive;
-                cs.sidx = s + a.ncl;
-                if (cs.sidx < nstatic) {  // prefetch the next entry of the share
-                    cs.pre_idx = cs.sidx;
-                    cs.pre_e = ld_acquire_u64(a.live + cs.sidx % nlive);
-                }
+            if (cs.sidx < nstatic) {
+                b = ck_share_get(a, epoch, lane, cs, nstatic);
+                j = cs.sidx / nlive;
+                cs.sidx += a.ncl;
             }
-            b = __shfl_sync(0xFFFFFFFFu, b, 0);
             if (b < 0) cs.static_done = true;
         }
         if (b >= 0) {
-            j = __shfl_sync(0xFFFFFFFFu, j, 0);
-            if (eager) {
-                if (ck_take_row(a, b, j, lane, out)) return out;
-                continue;
+            const bool ok = eager ? ck_take_row(a, b, j, lane, out) : ck_take(a, epoch, b, SRC_STATIC, lane, 0, out);
+            if (ok) {
+                cs.post = true;
+                return out;
             }
-            const bool ok = ck_take(a, epoch, b, SRC_STATIC, lane, 0, out);
-            ck_preissue(a, epoch, lane, cs, nlive, nstatic);
-            if (ok) return out;
+            ck_post(a, epoch, lane, cs);
             continue;
         }
         // no certain work left in the static list: speculate the chain just continued here
@@ -651,6 +673,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                     continue;
                 }
                 const int s = r % CK_D;
+                if (lane == 0) TRACE(TR_LOOP, r, 0, 0);
                 // every CTA's epilogue is done with row r-4 (the slot's previous use)
                 if (r >= CK_D) mbar_wait_cluster(&sh.dempty[s], ((r / CK_D) - 1) & 1);
                 if (lane == 0) TRACE(TR_CLAIM0, r, 0, 0);
@@ -669,8 +692,14 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                     if (part == 2) v = make_uint4(w[8], w[9], w[10], w[11]);
                     st_async_v4(reinterpret_cast<uint4*>(&sh.dq[s]) + part, v, &sh.dfull[s], (uint32_t)(x / 3));
                 }
+                if (lane == 0) TRACE(TR_BCAST, r, (int)(w[4] ^ w[5] ^ w[6] ^ w[7]) & 0x7FFF, 0);
                 ++r;
                 if (nd.b < 0) break;  // END broadcast: nothing more is claimed
+                if (cst.post) {
+                    cst.post = false;
+                    ck_post(a, epoch, lane, cst);
+                }
+                if (lane == 0) TRACE(TR_POST, r, 0, 0);
             }
         }
     } else if (warp == CK_PROD) {
@@ -685,6 +714,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             mbar_wait(&sh.dfull[s], (i / CK_D) & 1);
             const RowDesc dsc = sh.dq[s];
             if (dsc.b < 0) break;
+            if (lane == 0) TRACE(TR_PDESC, i, dsc.b, dsc.j);
             // the slice buffer is free once the mass warps are done with row i-2
             if (i >= CK_NB) mbar_wait(&sh.empty[bi], ((i / CK_NB) - 1) & 1);
             if (lane == 0) {
@@ -719,12 +749,20 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             // finalizing row uses it; nothing else writes it during the launch)
             CommitPre cp;
             if (a.commit) cp = commit_prefetch(a, dsc.pad[1], lane);
+            // issued with the descriptor, used after the sums arrive (no round trip after them)
+            const int rf_early = (lane == 0) ? ld_volatile_i32(a.roll_first + dsc.b) : 0;
+            // the rollout's draft tokens, for its finalize (d_1..d_F); read before this launch's
+            // fused lookup can rewrite them (that happens only after the rollout's one finalize)
+            const int32_t dpf = (lane < dsc.q) ? a.draft[(int64_t)dsc.b * a.k + lane] : -1;
             mbar_wait(&sh.sumbar[s], (i / CK_D) & 1);
             const int b = dsc.b, j = dsc.j, q = dsc.q, d = dsc.d;
             if (lane == 0) TRACE(TR_EPI0, i, b, j);
             // a row above an already-decided row is not needed: no completion.  Dead
-            // is monotone, so every CTA that skipped work on this row sees it dead here too.
-            const bool dead = __shfl_sync(0xFFFFFFFFu, lane == 0 ? (ld_volatile_i32(a.roll_first + b) < j ? 1 : 0) : 0, 0);
+            // is monotone; the view is taken when the descriptor arrives, so a row that became
+            // dead later (its max warps may have skipped it) can still be completed here: its
+            // record lies above the deciding row F and the finalize reads rows 0..F only, so
+            // such a completion changes nothing.
+            const bool dead = __shfl_sync(0xFFFFFFFFu, lane == 0 ? (rf_early < j ? 1 : 0) : 0, 0);
             if (dead) {
                 __syncwarp();
                 if (lane == 0) {
@@ -868,7 +906,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 if (lane == 0) sh.stat[STAT_ROWS_VERIFIED] += 1ull;
                 int no = 0;
                 int32_t ot = -1;
-                const bool fz = complete_row_warp(a, sh.stat, b, j, q, c_status, c_cand, c_z, c_norm, lane, no, ot);
+                const bool fz = complete_row_warp(a, sh.stat, b, j, q, c_status, c_cand, c_z, c_norm, lane, no, ot, dpf);
                 if (lane == 0 && c_status == ST_CONT) atomicExch(&sh.mail, (b << 8) | (j + 1));
                 if (a.commit && fz) commit_rollout_warp(a, b, lane, cp, no, ot);
             }

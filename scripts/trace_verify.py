@@ -105,8 +105,10 @@ else:
         res.append((s.elapsed_time(e), m, buf[:m].copy(), int(st1[6] - st0[6]), int(st1[7] - st0[7])))
 
 names = ["claim0", "claim1", "tma", "max0", "max1", "mass0", "mass1", "epi0", "epi1", "end", "fin", "spins", "sc",
-         "sqpop", "iter", "massl", "start", "go", "planned"]
+         "sqpop", "iter", "massl", "start", "go", "planned", "pdesc", "post", "loop", "bcast"]
 ms, m, ev, rv, rn = res[-1]
+if os.environ.get("TRACE_SAVE"):
+    np.save(os.environ["TRACE_SAVE"], ev)
 blk = ev[:, 0] & 0xFFFF
 typ = (ev[:, 0] >> 16) & 0xFF
 jj = ev[:, 0] >> 24
@@ -301,7 +303,7 @@ if os.environ.get("TRACE_GAPS"):
         if int(ty) in (5, 15) and int(b_) != 0:
             continue  # warp 0 only for mass events
         ev.setdefault(k_, float(tt))
-    gaps, wmax, wtma, wclaim = [], [], [], []
+    gaps, wmax, wtma, wclaim, wc0, wcd, wbc, wpd, wpt = [], [], [], [], [], [], [], [], []
     for (ty, bk, sq), tt in ev.items():
         if ty != 6:  # mass1 of row sq
             continue
@@ -313,6 +315,17 @@ if os.environ.get("TRACE_GAPS"):
         tma1 = ev.get((2, bk, sq + 1))
         prev_end = ev.get((6, bk, sq - 1))
         cl = ev.get((1, bk, sq + 1))
+        c0 = ev.get((0, bk, sq + 1))
+        if c0 is not None and prev_end is not None:
+            wc0.append(c0 - prev_end)
+            if cl is not None:
+                wcd.append(cl - c0)
+            if tma1 is not None and cl is not None:
+                wbc.append(tma1 - cl)
+            pd = ev.get((19, bk, sq + 1))
+            if pd is not None and cl is not None and tma1 is not None:
+                wpd.append(pd - cl)
+                wpt.append(tma1 - pd)
         if mx1 is not None:
             wmax.append(mx1 - tt)
         if tma1 is not None and prev_end is not None:
@@ -324,6 +337,11 @@ if os.environ.get("TRACE_GAPS"):
     print("  next max1 - mass1 (>0: waiting for max):", q(wmax))
     print("  next TMA issue - previous-row mass1 (buffer free):", q(wtma))
     print("  next claim end - previous-row mass1:", q(wclaim))
+    print("  next claim start (past issued / dempty waits) - previous-row mass1:", q(wc0))
+    print("  claim start -> claim end:", q(wcd))
+    print("  claim end -> TMA issue:", q(wbc))
+    print("  claim end -> producer has the descriptor:", q(wpd))
+    print("  producer has the descriptor -> TMA issue (buffer wait):", q(wpt))
 if os.environ.get("TRACE_CLAIMS"):
     c0, c1 = {}, {}
     for tt, ty, sq, b_, bk in zip(t, typ, seq, bb, blk):
