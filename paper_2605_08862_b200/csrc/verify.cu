@@ -319,6 +319,16 @@ __device__ __forceinline__ unsigned long long atom_or_acq_rel(unsigned long long
     return old;
 }
 
+__device__ __forceinline__ unsigned long long atom_or_acquire(unsigned long long* p, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.acquire.gpu.global.or.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ void red_or_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Record a completed row and finalize its rollout if this completes the decided prefix.
 // Returns true when this row's completion finalized the rollout's step.
 __device__ bool complete_row(const VerifyArgs& a, unsigned long long* stat, int b, int j, int q, int status,
@@ -354,21 +364,42 @@ __device__ bool complete_row_warp(const VerifyArgs& a, unsigned long long* stat,
     const int kp1 = a.k + 1;
     const int64_t base = (int64_t)b * kp1;
     int F = -1;
-    if (lane == 0) {
-        const int64_t r = base + j;
-        a.row_status[r] = status;
-        a.row_cand[r] = cand;
-        a.row_z[r] = z;
-        a.row_norm[r] = norm;
-        const bool decides = status != ST_CONT;
-        if (decides) atomicMin(a.roll_first + b, j);  // claim hint only (relaxed)
-        const unsigned long long mine = (1ull << j) | (decides ? (1ull << (32 + j)) : 0ull);
-        // release: this row's record; acquire: every earlier row's record of the rollout
-        const unsigned long long old = atom_or_acq_rel(a.roll_state + b, mine);
-        int F0, F1;
-        if (!prefix_decided(old, F0) && prefix_decided(old | mine, F1)) F = F1;
+    const bool decides = status != ST_CONT;
+    if (j == 0 && decides) {
+        // Row 0 decides: F = 0 and this completion is the one that finalizes (rows are claimed
+        // once), and no other warp reads row 0's record (only a finalizer reads records, and
+        // it is this warp), so no record, no release and no returned value: the state and the
+        // claim hint are updated fire-and-forget for the scheduler's scans and dead checks.
+        if (lane == 0) {
+            atomicMin(a.roll_first + b, 0);
+            red_or_relaxed(a.roll_state + b, 1ull | (1ull << 32));
+        }
+        F = 0;
+    } else {
+        if (lane == 0) {
+            const int64_t r = base + j;
+            // A finalizer reads the record of the deciding row F (status, candidate) and, only
+            // when the caller asked for them, the normalisers / Z of rows 0..F.  An accepted row
+            // (never F) without those outputs therefore stores nothing and needs no release.
+            const bool outs = a.out_norm != nullptr || a.out_z != nullptr;
+            if (decides) {
+                a.row_status[r] = status;
+                a.row_cand[r] = cand;
+            }
+            if (outs) {
+                a.row_z[r] = z;
+                a.row_norm[r] = norm;
+            }
+            if (decides) atomicMin(a.roll_first + b, j);  // claim hint only (relaxed)
+            const unsigned long long mine = (1ull << j) | (decides ? (1ull << (32 + j)) : 0ull);
+            // release: this row's record; acquire: every earlier row's record of the rollout
+            const unsigned long long old = (decides || outs) ? atom_or_acq_rel(a.roll_state + b, mine)
+                                                             : atom_or_acquire(a.roll_state + b, mine);
+            int F0, F1;
+            if (!prefix_decided(old, F0) && prefix_decided(old | mine, F1)) F = F1;
+        }
+        F = __shfl_sync(0xFFFFFFFFu, F, 0);
     }
-    F = __shfl_sync(0xFFFFFFFFu, F, 0);
     if (F < 0) return false;
     __syncwarp();  // lane 0's acquire orders the other lanes' reads below
     const int32_t* d = a.draft + (int64_t)b * a.k;
@@ -377,7 +408,7 @@ __device__ bool complete_row_warp(const VerifyArgs& a, unsigned long long* stat,
     unsigned long long zl = 0ull;
     // d_{F+1} is needed only for an accepted EOS at row F (this row's status is known)
     if (lane < F || (lane == F && lane < q && (F != j || status == ST_EOS))) dl = (dpf != DPF_NONE) ? dpf : d[lane];
-    if (lane <= F) {
+    if (lane <= F && (a.out_norm || a.out_z)) {
         nl = (lane == j) ? norm : __ldcg(a.row_norm + base + lane);
         zl = (lane == j) ? z : __ldcg(a.row_z + base + lane);
     }

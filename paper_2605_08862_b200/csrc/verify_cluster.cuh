@@ -62,6 +62,7 @@ constexpr int CK_D = 4;                   // descriptor / exchange ring depth
 // row i's maxima, which needs D >= 2 x buffers
 static_assert(CK_D >= 2 * CK_NB, "exchange ring shallower than twice the slice buffers");
 constexpr int CK_TILE = 512;              // elements per tile (16 per lane)
+constexpr int CK_BUF_LOCK = 1 << 30;      // slice buffer held by the epilogue (crossing tile)
 constexpr int CK_MAXT = 104;              // tiles per slice
 constexpr int CK_MAXSL = CK_MAXT * CK_TILE;  // 53248 elements: V <= 425984
 
@@ -74,6 +75,7 @@ struct CkShared {
     uint4 erec[CK_D];         // mass warps -> epilogue: {m bits, bad, greedy index, 0}
     int mail;  // leader: (rollout << 8 | row) the epilogue found needed next, or -1
     int tma_issued;  // leader: rows whose copy the producer has issued (claimer look-ahead)
+    int bufst[CK_NB];  // row (sequence number) a slice buffer holds; | CK_BUF_LOCK while the epilogue reads it
     int plan_b[CK_NMW];  // planning round: rollout per mass warp (-1 dead, -2 none)
     float wmax[CK_NXW];
     uint32_t wbad[CK_NXW];
@@ -574,6 +576,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
     if (tid == 0) {
         sh.mail = -1;
         sh.tma_issued = 0;
+        for (int x = 0; x < CK_NB; ++x) sh.bufst[x] = -1;
     }
 #ifdef BS_TRACE
     if (tid == 0) {
@@ -718,6 +721,10 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             // the slice buffer is free once the mass warps are done with row i-2
             if (i >= CK_NB) mbar_wait(&sh.empty[bi], ((i / CK_NB) - 1) & 1);
             if (lane == 0) {
+                // take the buffer over from row i-2 (wait while that row's epilogue reads its
+                // crossing tile from it)
+                const int prev = (i >= CK_NB) ? i - CK_NB : -1;
+                while (atomicCAS(&sh.bufst[bi], prev, i) != prev) __nanosleep(32);
                 uint16_t* buf = bufs + (size_t)bi * SL;
                 const uint16_t* src = a.logits + dsc.rowno * a.stride + e_lo;
                 const int nb = dsc.aligned ? (len & ~7) : 0;  // 16-byte multiple
@@ -859,11 +866,30 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                         }
                         xt = __shfl_sync(0xFFFFFFFFu, xt, L);
                         ut = shfl_u64(ut, L);
-                        // re-read the tile (L2): lane l owns its 16 consecutive elements
+                        // the crossing tile: lane l owns its 16 consecutive elements; from the
+                        // slice buffer while no later row has taken it over (locked meanwhile),
+                        // else re-read from L2 / HBM
+                        const int bi = i % CK_NB;
+                        int own = 0;
+                        if (lane == 0) own = atomicCAS(&sh.bufst[bi], i, i | CK_BUF_LOCK) == i;
+                        own = __shfl_sync(0xFFFFFFFFu, own, 0);
                         const uint16_t* rowp = a.logits + dsc.rowno * a.stride + e_lo;
                         const int e0 = xt * CK_TILE + lane * 16;
                         uint4 v0, v1;
-                        if (dsc.aligned && e0 + 16 <= len) {
+                        if (own) {
+                            const uint16_t* bp = bufs + (size_t)bi * SL;
+                            if (e0 + 16 <= len) {
+                                v0 = lds128(bp + e0);
+                                v1 = lds128(bp + e0 + 8);
+                            } else {
+                                uint16_t t16[16];
+                                for (int x = 0; x < 16; ++x) t16[x] = (e0 + x < len) ? bp[e0 + x] : (uint16_t)0xFF80u;
+                                v0 = make_uint4(t16[0] | ((uint32_t)t16[1] << 16), t16[2] | ((uint32_t)t16[3] << 16),
+                                                t16[4] | ((uint32_t)t16[5] << 16), t16[6] | ((uint32_t)t16[7] << 16));
+                                v1 = make_uint4(t16[8] | ((uint32_t)t16[9] << 16), t16[10] | ((uint32_t)t16[11] << 16),
+                                                t16[12] | ((uint32_t)t16[13] << 16), t16[14] | ((uint32_t)t16[15] << 16));
+                            }
+                        } else if (dsc.aligned && e0 + 16 <= len) {
                             v0 = __ldcg(reinterpret_cast<const uint4*>(rowp + e0));
                             v1 = __ldcg(reinterpret_cast<const uint4*>(rowp + e0 + 8));
                         } else {
@@ -877,6 +903,10 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                         mp.nmc = -__fmul_rn(m, a.c);
                         uint64_t mm[16];
                         ck_mass16(v0, v1, mp, e0, len, excl_l, mm);
+                        if (own) {  // every lane has consumed its tile registers: hand the buffer back
+                            __syncwarp();
+                            if (lane == 0) atomicExch(&sh.bufst[bi], i);
+                        }
                         uint64_t sl = 0;
 #pragma unroll
                         for (int x = 0; x < 16; ++x) sl += mm[x];
