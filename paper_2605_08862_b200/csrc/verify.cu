@@ -98,7 +98,7 @@ __device__ __forceinline__ void trace_ev(int type, int seq, int b, int j) {
     } while (0)
 #endif
 enum { TR_CLAIM0 = 0, TR_CLAIM1 = 1, TR_TMA = 2, TR_MAX0 = 3, TR_MAX1 = 4, TR_MASS0 = 5, TR_MASS1 = 6,
-       TR_EPI0 = 7, TR_EPI1 = 8, TR_END = 9, TR_FIN = 10, TR_SPINS = 11, TR_SC = 12, TR_SQPOP = 13, TR_ITER = 14, TR_MASSL = 15, TR_START = 16, TR_GO = 17, TR_PLANNED = 18, TR_PDESC = 19, TR_POST = 20, TR_LOOP = 21, TR_BCAST = 22 };
+       TR_EPI0 = 7, TR_EPI1 = 8, TR_END = 9, TR_FIN = 10, TR_SPINS = 11, TR_SC = 12, TR_SQPOP = 13, TR_ITER = 14, TR_MASSL = 15, TR_START = 16, TR_GO = 17, TR_PLANNED = 18, TR_PDESC = 19, TR_POST = 20, TR_LOOP = 21, TR_BCAST = 22, TR_EX1 = 24, TR_EX2 = 25, TR_EX3 = 26 };
 
 
 struct VerifyArgs {

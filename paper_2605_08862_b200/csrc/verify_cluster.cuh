@@ -779,6 +779,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 }
                 continue;
             }
+            if (lane == 0) TRACE(TR_EX1, i, dsc.b, dsc.j);
             const uint4 er = sh.erec[s];  // the cluster max of row i (local record)
             const float m = __uint_as_float(er.x);
             const uint32_t bad = er.y;
@@ -793,20 +794,23 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
             if (bad) err |= DEV_BAD_LOGIT;
             else if (m == -INFINITY) err |= DEV_ALL_NEGINF;
             else if (a.T > 0.f && !(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) err |= DEV_RANGE;
-            // the row's result (recorded by one CTA's epilogue warp: rank 0, or the CTA that
-            // owns the sampled token)
+            // the row's result (recorded by one CTA's epilogue warp: the CTA that owns the
+            // sampled token, else a rank that rotates with (b, j), so the completions of accepted
+            // rows -- a few dependent round trips each -- spread over the cluster's 8 epilogue
+            // warps instead of queueing on one)
+            const int rec_rank = (int)((unsigned)(3 * b + j) % (unsigned)CK_CL);
             bool rec = false;
             int c_status = ST_DECIDED, c_cand = -1;
             unsigned long long c_z = 0ull;
             float c_norm = 0.f;
             if (err) {  // R0: reported at finalize only if Alg. 1 needs this row
-                rec = rank == 0;
+                rec = rank == rec_rank;
                 c_status = ST_ERR;
                 c_cand = (int)err;
             } else if (a.T == 0.f) {  // greedy (R1): lowest index attaining m
                 const int g = (int)er.z;
                 const bool acc = j < q && d == g;
-                rec = rank == 0;
+                rec = rank == rec_rank;
                 c_status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
                 c_cand = g;
                 c_z = 1ull;
@@ -817,7 +821,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                 if (j < q) acc = uniform_floor(row_draw(a, dsc, PURPOSE_ACCEPT), Z) < md;
                 const int status = acc ? ((a.eos >= 0 && d == a.eos) ? ST_EOS : ST_CONT) : ST_DECIDED;
                 if (status != ST_DECIDED) {
-                    rec = rank == 0;
+                    rec = rank == rec_rank;
                     c_status = status;
                     c_z = Z;
                     c_norm = norm;
@@ -839,6 +843,7 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                         }
                         cum += cs;
                     }
+                    if (lane == 0) TRACE(TR_EX2, i, rc, dsc.j);
                     if (rc == rank) {
                         // crossing tile of this slice (the excluded token's mass off its tile)
                         const int excl_l = excl - e_lo;  // slice-relative (may be out of range)
@@ -932,19 +937,25 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
                     }
                 }
             }
+            if (lane == 0) TRACE(TR_EX3, i, dsc.b, dsc.j);
+            // The row's result is in registers: an accepted row posts its successor to this
+            // cluster's mailbox (row j+1 is needed: the chain continues here) and the row's
+            // slot is handed back before the completion protocol's round trips, so neither the
+            // chain nor the claimer (which reuses the slot four rows later) waits for them.
+            __syncwarp();
+            if (lane == 0) {
+                if (rec && c_status == ST_CONT)  // the leader's claimer reads the mailbox
+                    atomicExch(cluster.map_shared_rank(&sh.mail, 0), (b << 8) | (j + 1));
+                TRACE(TR_EPI1, i, dsc.b, dsc.j);
+                mbar_arrive(&sh.eempty[s]);             // tile sums / sum slot of row i free
+                mbar_arrive_remote(&sh.dempty[s], 0u);  // descriptor slot of row i free
+            }
             if (rec) {  // warp-uniform
                 if (lane == 0) sh.stat[STAT_ROWS_VERIFIED] += 1ull;
                 int no = 0;
                 int32_t ot = -1;
                 const bool fz = complete_row_warp(a, sh.stat, b, j, q, c_status, c_cand, c_z, c_norm, lane, no, ot, dpf);
-                if (lane == 0 && c_status == ST_CONT) atomicExch(&sh.mail, (b << 8) | (j + 1));
                 if (a.commit && fz) commit_rollout_warp(a, b, lane, cp, no, ot);
-            }
-            __syncwarp();
-            if (lane == 0) {
-                TRACE(TR_EPI1, i, dsc.b, dsc.j);
-                mbar_arrive(&sh.eempty[s]);             // tile sums / sum slot of row i free
-                mbar_arrive_remote(&sh.dempty[s], 0u);  // descriptor slot of row i free
             }
         }
     } else if (warp >= CK_NMW) {
