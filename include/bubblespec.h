@@ -73,7 +73,7 @@ typedef struct {
     int32_t k_max;                /* max draft block length K, 1..31 (P:299 uses 4)    */
     int32_t match_max;            /* M, max anchor length, 1..32 (reading L1)          */
     int32_t match_min;            /* L_min >= 1, min anchor length              */
-    int32_t max_rollouts;         /* number of rollout slots                            */
+    int32_t max_rollouts;         /* number of rollout slots, in [1, 2097151]           */
     int64_t pool_capacity_tokens; /* pool token capacity per RL step                    */
     int32_t pool_capacity_seqs;   /* pool sequence capacity per RL step                 */
     int32_t device;               /* CUDA device ordinal                                */

@@ -86,7 +86,9 @@ bs_status bs_create(const bs_config* cfg, bs_ctx** out) {
     if (cfg->match_max < 1 || cfg->match_max > 32)
         return fail(nullptr, BS_ERR_INVALID, "match_max must be in [1, 32]");
     if (cfg->match_min < 1) return fail(nullptr, BS_ERR_INVALID, "match_min must be >= 1");
-    if (cfg->max_rollouts < 1) return fail(nullptr, BS_ERR_INVALID, "max_rollouts must be >= 1");
+    // (the verify launch packs planned / live / hot rollout counts into 21-bit fields)
+    if (cfg->max_rollouts < 1 || cfg->max_rollouts > 2097151)
+        return fail(nullptr, BS_ERR_INVALID, "max_rollouts must be in [1, 2097151]");
     if (cfg->pool_capacity_tokens < 0 || cfg->pool_capacity_seqs < 0)
         return fail(nullptr, BS_ERR_INVALID, "negative pool capacity");
     if (cfg->eos_id >= cfg->vocab) return fail(nullptr, BS_ERR_INVALID, "eos_id >= vocab");

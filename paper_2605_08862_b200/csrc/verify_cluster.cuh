@@ -110,12 +110,31 @@ __host__ __device__ constexpr size_t ck_smem_bytes(int SL) {
 // every rollout of the call is finalized.
 constexpr int SRC_NONE = 0, SRC_READY = 1, SRC_STATIC = 2, SRC_SPEC = 3;
 
-// Returns whether rollout b is live (has rows); the caller counts and lists it per CTA.
-__device__ bool ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
+// Static-list order: "hot" rollouts -- a draft and at least CK_HOT_T tokens accepted in the
+// previous step (out_acc of the launch before; acceptance runs in streaks while a rollout
+// follows its prompt's pool) -- come first, so their likely acceptance chains start early and
+// the single-row rollouts fill the end of the launch.  Only the order changes, never a result.
+#ifdef BS_HOT_T
+constexpr int CK_HOT_T = BS_HOT_T;
+#else
+constexpr int CK_HOT_T = 2;
+#endif
+constexpr unsigned long long CK_M21 = (1ull << 21) - 1ull;  // plan word: planned | live | hot, 21 bits each
+
+// Entry idx of the static list: hot rollouts from the front of the live array, the others from
+// its back (reversed).
+__device__ __forceinline__ const unsigned long long* ck_live_at(const VerifyArgs& a, int idx, int nhot) {
+    return a.live + (idx < nhot ? idx : a.n - 1 - (idx - nhot));
+}
+
+// Returns 0 if rollout b has no rows, 1 if it is live, 2 if it is live and hot; the caller counts
+// and lists it per CTA.
+__device__ int ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
     const int kp1 = a.k + 1;
     // loads that depend on b only go out with the slot lookup (one round trip)
     const int sl = a.slots[b];
     const int dlen = a.draft_len[b];
+    const int prev_acc = (lane == 0) ? a.out_acc[b] : 0;  // the previous step's (read before the reset below)
     const int tk = (lane < a.k) ? a.draft[(int64_t)b * a.k + lane] : 0;
     const int p = a.pos[sl], L = a.max_len[sl];
     int q = -1;
@@ -160,7 +179,8 @@ __device__ bool ck_plan(const VerifyArgs& a, uint32_t epoch, int b, int lane) {
         st_release_u64(a.next_row + b, ((unsigned long long)epoch << 32) | ((unsigned long long)(q + 1) << 24));
         TRACE(TR_PLANNED, 0, b, 0);
     }
-    return q >= 0;
+    const bool hot = __shfl_sync(0xFFFFFFFFu, prev_acc >= CK_HOT_T ? 1 : 0, 0) != 0;
+    return q < 0 ? 0 : ((q > 0 && hot) ? 2 : 1);
 }
 
 // Row r of rollout b as a descriptor (lane-uniform inputs; every lane computes it).
@@ -358,6 +378,7 @@ __device__ int ck_scan(const VerifyArgs& a, uint32_t epoch, int lane, int rot, i
 // Producer-side claim state kept across claims (saves round trips once the facts are known).
 struct ClaimState {
     int nlive = -1;          // live rollouts (after the plan completed)
+    int nhot = 0;            // of which hot (listed first)
     bool eager = false;
     bool static_done = false;  // the static cursor is exhausted
     int spec_b = -1, spec_r = 0;  // chain this cluster just continued: speculate its next row
@@ -379,7 +400,7 @@ __device__ __forceinline__ void ck_share_load(const VerifyArgs& a, uint32_t epoc
     bool need = s < nstatic;
     unsigned long long e = 0;
     for (;;) {
-        if (need) e = ld_acquire_u64(a.live + s % cs.nlive);
+        if (need) e = ld_acquire_u64(ck_live_at(a, s % cs.nlive, cs.nhot));
         need = need && (uint32_t)(e >> 32) != epoch;
         if (!__any_sync(0xFFFFFFFFu, need)) break;
         __nanosleep(32);
@@ -425,17 +446,19 @@ __device__ __forceinline__ RowDesc ck_claim(const VerifyArgs& a, uint32_t epoch,
     const int cid = (int)(blockIdx.x / CK_CL);
     if (cs.nlive < 0) {
         // the static list is the live rollouts, compacted by the planners: wait for the plan
-        int nl = 0;
+        int nl = 0, nh = 0;
         if (lane == 0) {
             const unsigned long long* w = reinterpret_cast<const unsigned long long*>(a.sctl + SC_NLIVE);
             unsigned long long v = ld_acquire_u64(w);
-            while ((int)(v >> 32) < n) {
+            while ((int)(v >> 42) < n) {
                 __nanosleep(32);
                 v = ld_acquire_u64(w);
             }
-            nl = (int)(uint32_t)v;
+            nl = (int)((v >> 21) & CK_M21);
+            nh = (int)(v & CK_M21);
         }
         cs.nlive = __shfl_sync(0xFFFFFFFFu, nl, 0);
+        cs.nhot = __shfl_sync(0xFFFFFFFFu, nh, 0);
         // eager when every live row fits in flight at once (two per cluster): the static
         // list then enumerates every row, j-major, and a cluster leaves once it is exhausted
         cs.eager = a.eager_ok == 2 || (a.eager_ok && (long long)cs.nlive * (a.k + 1) <= (long long)CK_NB * a.ncl);
@@ -613,23 +636,31 @@ __global__ void __cluster_dims__(CK_CL, 1, 1) __launch_bounds__(CK_NT, CK_MINB)
         // live-list slots (low half), so the plan's completion count is not one hot word
         for (int base = (int)blockIdx.x * CK_NMW; base < a.n; base += (int)gridDim.x * CK_NMW) {
             const int b = base + warp;
-            const bool live = (b < a.n) ? ck_plan(a, epoch, b, lane) : false;
-            if (lane == 0) sh.plan_b[warp] = (b < a.n) ? (live ? b : -1) : -2;
+            const int live = (b < a.n) ? ck_plan(a, epoch, b, lane) : 0;
+            if (lane == 0) sh.plan_b[warp] = (b < a.n) ? (live ? (b | (live == 2 ? (1 << 30) : 0)) : -1) : -2;
             named_bar(3, CK_NMW * 32);
             if (warp == 0 && lane == 0) {
-                int np = 0, nl = 0;
+                int np = 0, nl = 0, nh = 0;
                 for (int w = 0; w < CK_NMW; ++w) {
                     np += sh.plan_b[w] != -2;
                     nl += sh.plan_b[w] >= 0;
+                    nh += sh.plan_b[w] >= (1 << 30);
                 }
                 // rollouts without rows are done (one termination-count atomic per CTA round)
                 if (np > nl) atomicAdd(a.sctl + SC_DONE, (unsigned)(np - nl));
-                const unsigned long long cnt = atomicAdd(reinterpret_cast<unsigned long long*>(a.sctl + SC_NLIVE),
-                                                         ((unsigned long long)np << 32) | (unsigned long long)nl);
-                unsigned slot = (uint32_t)cnt;
-                for (int w = 0; w < CK_NMW; ++w)
-                    if (sh.plan_b[w] >= 0)
-                        st_release_u64(a.live + slot++, ((unsigned long long)epoch << 32) | (uint32_t)sh.plan_b[w]);
+                // planned << 42 | live << 21 | hot: counts and list slots in one atomic
+                const unsigned long long cnt =
+                    atomicAdd(reinterpret_cast<unsigned long long*>(a.sctl + SC_NLIVE),
+                              ((unsigned long long)np << 42) | ((unsigned long long)nl << 21) | (unsigned long long)nh);
+                unsigned hs = (unsigned)(cnt & CK_M21);
+                unsigned cs = (unsigned)((cnt >> 21) & CK_M21) - hs;
+                for (int w = 0; w < CK_NMW; ++w) {
+                    const int pb = sh.plan_b[w];
+                    if (pb < 0) continue;
+                    const int bb = pb & ((1 << 30) - 1);
+                    unsigned long long* dst = (pb >= (1 << 30)) ? a.live + hs++ : a.live + (a.n - 1 - (int)cs++);
+                    st_release_u64(dst, ((unsigned long long)epoch << 32) | (uint32_t)bb);
+                }
             }
             named_bar(3, CK_NMW * 32);  // plan_b reusable
         }
