@@ -66,6 +66,13 @@ def test_invalid_config_rejected_before_device(lib):
     assert b"vocab" in L.bs_last_error(None)
     cfg = bs_config(1024, -1, 40, 32, 1, 4, 16, 4, 0, 0)
     assert L.bs_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    # the verify launch packs rollout counts into 21-bit fields
+    cfg = bs_config(1024, -1, 4, 32, 1, 1 << 21, 16, 4, 0, 0)
+    assert L.bs_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    assert b"max_rollouts" in L.bs_last_error(None)
+    cfg = bs_config(600000, -1, 4, 32, 1, 4, 16, 4, 0, 0)
+    assert L.bs_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    assert b"vocab" in L.bs_last_error(None)
 
 
 def test_version_string(lib):
