@@ -1058,17 +1058,20 @@ cudaError_t launch_verify(bs_ctx* ctx, int32_t n, const int32_t* slots, const vo
     }
     if (topp) {  // R5k / R5: top-k / top-p filtered rows (verify_topp.cuh)
         if (ntile_ok(V) == 0) return cudaErrorInvalidValue;
-        const size_t tsm = sizeof(TopPShared);
-        if (!ctx->kcfg_topp) {
+        // the slice staged in shared memory when it fits beside TopPShared at two CTAs per SM
+        const size_t staged_sm = tp_shared_bytes() + (size_t)topp_slice(V) * 2;
+        const int staged = staged_sm <= TP_STAGE_MAX ? 1 : 0;
+        const size_t tsm = staged ? staged_sm : tp_shared_bytes();
+        if (ctx->kcfg_topp != (int)tsm) {
             e = cudaFuncSetAttribute(verify_topp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)tsm);
             if (e != cudaSuccess) return e;
-            ctx->kcfg_topp = 1;
+            ctx->kcfg_topp = (int)tsm;
         }
         // one 8-CTA cluster per row in flight (two CTAs per SM)
         const int tcl = std::max(1, std::min((ctx->num_sms * 2) / TP_CL, n * (k + 1)));
         return launch_pdl(verify_topp_kernel, dim3(tcl * TP_CL), dim3(TP_NT), tsm, st, a, top_p, top_k,
-                          topp_slice(V));
+                          topp_slice(V), staged);
     }
     if (kind == VK_CLUSTER) {
         const int SL = cluster_slice(V);

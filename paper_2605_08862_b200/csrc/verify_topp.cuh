@@ -41,6 +41,7 @@ struct TopPShared {
     uint32_t hc[TP_H1];                 // top-k: positive-mass tokens per coarse bin
     uint32_t h2c[16];                   // top-k: positive-mass tokens per key of the crossing bin
     uint32_t h2lo[16], h2hi[16];        // masses of the 16 keys of the crossing bin (Hist64)
+    uint32_t h3c[16];                   // top-p: tokens per key of the crossing bin (this slice)
     unsigned long long tsum[TP_MAXLT];  // this slice's 256-element tile sums
     unsigned long long stat[STAT_COUNT];
     float wmax[TP_NW];
@@ -56,7 +57,14 @@ struct TopPShared {
     unsigned long long bz[2];  // [0] Theta remaining inside the coarse bin, [1] sum above it
     int32_t bsel;              // coarse bin B
     int32_t bselk, needk;      // top-k: coarse bin of kappa, tokens still needed inside it
+    uint64_t sbar;             // the staged slice's bulk copy (mbarrier)
+    unsigned long long wtot[TP_NW];  // coarse select: per-warp mass totals (block scan)
 };
+
+// The slice is staged in shared memory (one bulk copy per row, after the TopPShared block) when
+// both fit two CTAs per SM; the passes then read shared memory instead of re-streaming L2.
+__host__ __device__ constexpr size_t tp_shared_bytes() { return (sizeof(TopPShared) + 127) & ~size_t(127); }
+constexpr size_t TP_STAGE_MAX = 110 * 1024;  // per CTA, two CTAs per SM
 
 // Order-preserving map of bf16 bit patterns to 16-bit keys (larger value -> larger key).
 __device__ __forceinline__ uint32_t tp_key(uint32_t b) {
@@ -106,15 +114,16 @@ __device__ __forceinline__ void tp_unpack(const uint4 v, uint32_t b[8]) {
 #define BS_TP_U 2
 #endif
 constexpr int TP_U = BS_TP_U;
+// sbuf (staged slice, -inf padded to whole tiles) replaces the global loads when non-null.
 template <class F>
-__device__ __forceinline__ void tp_stream(const uint16_t* row, int ntile, int V, bool aligned, int warp, int lane,
-                                          F&& f) {
+__device__ __forceinline__ void tp_stream(const uint16_t* row, const uint16_t* sbuf, int ntile, int V, bool aligned,
+                                          int warp, int lane, F&& f) {
     for (int t0 = warp; t0 < ntile; t0 += TP_NW * TP_U) {
         uint4 v[TP_U];
 #pragma unroll
         for (int u = 0; u < TP_U; ++u) {
             const int t = t0 + u * TP_NW;
-            v[u] = (t < ntile) ? tp_load8(row, t * 256 + lane * 8, V, aligned)
+            v[u] = (t < ntile) ? (sbuf ? lds128(sbuf + t * 256 + lane * 8) : tp_load8(row, t * 256 + lane * 8, V, aligned))
                                : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
         }
 #pragma unroll
@@ -125,16 +134,39 @@ __device__ __forceinline__ void tp_stream(const uint16_t* row, int ntile, int V,
     }
 }
 
+// Counts of the 16 keys of coarse bin B in this thread's elements of the slice, 8 bits per key
+// packed in 4 words (a thread sees at most 128 elements per pass: SL <= 65536 over 512 threads).
+// Every element with a given key has the same mass (mass is a function of the bf16 value), so a
+// key's mass total is its count times that mass: no per-element 64-bit shared atomics, which
+// all landed on the same 16 bins.
+__device__ __forceinline__ void tp_key_count(uint32_t c4[4], uint32_t kk, int B) {
+    if ((int)(kk >> 4) == B) {
+        const uint32_t k4 = kk & 15u, w = k4 >> 2, inc = 1u << ((k4 & 3u) * 8u);
+        c4[0] += (w == 0u) ? inc : 0u;
+        c4[1] += (w == 1u) ? inc : 0u;
+        c4[2] += (w == 2u) ? inc : 0u;
+        c4[3] += (w == 3u) ? inc : 0u;
+    }
+}
+// The warp's count of key kq of the packed per-lane counts.
+__device__ __forceinline__ uint32_t tp_warp_count(const uint32_t c4[4], int kq) {
+    return __reduce_add_sync(0xFFFFFFFFu, (c4[kq >> 2] >> ((kq & 3) * 8)) & 0xFFu);
+}
+
 __global__ void __cluster_dims__(TP_CL, 1, 1) __launch_bounds__(TP_NT, 2)
-verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
+verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int staged) {
     namespace cg = cooperative_groups;
-    extern __shared__ __align__(16) uint8_t tp_smem[];
+    extern __shared__ __align__(128) uint8_t tp_smem[];
     TopPShared& sh = *reinterpret_cast<TopPShared*>(tp_smem);
+    uint16_t* const sbuf_base = reinterpret_cast<uint16_t*>(tp_smem + tp_shared_bytes());
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
     TopPShared* L = cl.map_shared_rank(&sh, 0);  // the leader's copy
     pdl_wait();  // dependents launch at exit (the cluster kernel plans before its wait)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef BS_PHASE_TIMING
+    long long ph_t = clock64();
+#endif
     const int rows = (int)a.ctl[VCTL_ROWS];
     const int V = a.V;
     const int e_lo = rank * SL, len = max(0, min(SL, V - e_lo));
@@ -142,6 +174,9 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
     const uint64_t P = (uint64_t)llround((double)top_p * 4294967296.0);  // R5 (top_p < 1)
     const bool use_p = top_p < 1.f, use_k = top_k > 0;
     for (int i = tid; i < STAT_COUNT; i += TP_NT) sh.stat[i] = 0ull;
+    if (tid == 0) mbar_init(&sh.sbar, 1);
+    __syncthreads();
+    uint32_t sphase = 0;  // the staging barrier's phase
     const Hist64 H1{sh.h1lo, sh.h1hi}, H2{sh.h2lo, sh.h2hi};
     const Hist64 H1L{L->h1lo, L->h1hi}, H2L{L->h2lo, L->h2hi};
 
@@ -155,8 +190,9 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
         if (tid < 16) {
             H2.clear(tid);
             sh.h2c[tid] = 0u;
+            sh.h3c[tid] = 0u;
         }
-        cl.sync();  // S1: the claim is published; every accumulator is clear; the last row is done
+        PH_MARK(0); cl.sync(); PH_MARK(8);  // S1: the claim is published; every accumulator is clear; the last row is done
         const RowDesc dsc = L->dsc;
         if (dsc.b < 0) {
             cl.sync();  // no CTA may exit while another still reads the leader's shared memory
@@ -166,10 +202,28 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
         const uint16_t* srow = row + e_lo;
         const bool aligned = dsc.aligned != 0;
         const int j = dsc.j, q = dsc.q, d = dsc.d;
+        const uint16_t* sbuf = nullptr;
+        if (staged) {  // the slice into shared memory: one bulk copy, -inf padding to whole tiles
+            const int ncopy = aligned ? (len & ~7) : 0;  // a 16-byte multiple
+            if (tid == 0) {
+                if (ncopy) {
+                    fence_proxy_async_smem();  // the previous row's reads of the buffer come first
+                    mbar_arrive_expect_tx(&sh.sbar, (uint32_t)ncopy * 2u);
+                    bulk_g2s(sbuf_base, srow, (uint32_t)ncopy * 2u, &sh.sbar, policy_evict_first());
+                } else {
+                    mbar_arrive(&sh.sbar);
+                }
+            }
+            for (int e = ncopy + tid; e < nlt * 256; e += TP_NT) sbuf_base[e] = (e < len) ? srow[e] : (uint16_t)0xFF80u;
+            mbar_wait(&sh.sbar, sphase);
+            sphase ^= 1u;
+            __syncthreads();  // the generic tail fill
+            sbuf = sbuf_base;
+        }
 
         // ---------------------------------------------------- pass 1: max (slice, then cluster)
         uint32_t mx = 0xFF80FF80u;
-        tp_stream(srow, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
+        tp_stream(srow, sbuf, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
             mx = hmax2_nan_u32(mx, v.x);
             mx = hmax2_nan_u32(mx, v.y);
             mx = hmax2_nan_u32(mx, v.z);
@@ -198,7 +252,7 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
             L->cmax[rank] = cm;
             L->cbad[rank] = cb;
         }
-        cl.sync();  // S2: every slice's max in the leader
+        PH_MARK(1); cl.sync(); PH_MARK(9);  // S2: every slice's max in the leader
         float m = -INFINITY;
         uint32_t bb = 0;
         for (int r = 0; r < TP_CL; ++r) {
@@ -210,9 +264,11 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
         else if (m == -INFINITY) err |= DEV_ALL_NEGINF;
         else if (!(fabsf(__fmul_rn(m, a.c)) < 16777216.0f)) err |= DEV_RANGE;
         if (err) {  // R0: the row is an error; the rollout stops (no token)
-            if (rank == 0 && tid == 0) {  // reported at finalize only if Alg. 1 needs this row
-                sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-                complete_row(a, sh.stat, dsc.b, j, q, ST_ERR, (int)err, 0ull, 0.f);
+            if (rank == 0 && warp == 0) {  // reported at finalize only if Alg. 1 needs this row
+                if (lane == 0) sh.stat[STAT_ROWS_VERIFIED] += 1ull;
+                int no = 0;
+                int32_t tk = -1;
+                complete_row_warp(a, sh.stat, dsc.b, j, q, ST_ERR, (int)err, 0ull, 0.f, lane, no, tk);
             }
             cl.sync();  // S_end: every CTA is done reading the leader's row state
             continue;
@@ -224,7 +280,7 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
         mp.magic = 12582912.0f + (float)a.S;
 
         // ---------------------------------------------------- pass 2: masses, Z, coarse bins
-        tp_stream(srow, nlt, len, aligned, warp, lane, [&](int t, const uint4 v) {
+        tp_stream(srow, sbuf, nlt, len, aligned, warp, lane, [&](int t, const uint4 v) {
             uint64_t mm[8];
             mass_pair(v.x, mp, mm[0], mm[1]);
             mass_pair(v.y, mp, mm[2], mm[3]);
@@ -265,7 +321,7 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
                 if (use_k && sh.hc[i]) atomicAdd(&L->hc[i], sh.hc[i]);
             }
         }
-        cl.sync();  // S3: cluster histograms and slice sums in the leader
+        PH_MARK(2); cl.sync(); PH_MARK(10);  // S3: cluster histograms and slice sums in the leader
         uint64_t Z = 0;
         for (int r = 0; r < TP_CL; ++r) Z += L->zsum[r];  // R4: the unfiltered normaliser
         // filtered slice tile sums (masses >= t) and their slice total into fsum[slot]
@@ -274,7 +330,7 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
         int fslot = 0;
         auto filtered_tiles = [&](uint64_t t) {
             __syncthreads();  // earlier readers of sh.tsum are done
-            tp_stream(srow, nlt, len, aligned, warp, lane, [&](int tt, const uint4 v) {
+            tp_stream(srow, sbuf, nlt, len, aligned, warp, lane, [&](int tt, const uint4 v) {
                 uint64_t mm[8];
                 mass_pair(v.x, mp, mm[0], mm[1]);
                 mass_pair(v.y, mp, mm[2], mm[3]);
@@ -289,7 +345,7 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
             __syncthreads();
             const uint64_t fs = slice_total();
             if (tid == 0) L->fsum[fslot][rank] = fs;
-            cl.sync();  // every slice's filtered sum in the leader
+            PH_MARK(3); cl.sync(); PH_MARK(11);  // every slice's filtered sum in the leader
             tiles_tau = t;
             tiles_sums = L->fsum[fslot];
             fslot = (fslot + 1) % 3;
@@ -333,16 +389,20 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
             const int Bk = L->bselk;
             if (Bk >= 0) {
                 // pass 3k: counts of the 16 keys inside bin Bk (slice -> leader)
-                tp_stream(srow, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
+                uint32_t c4[4] = {0u, 0u, 0u, 0u};
+                tp_stream(srow, sbuf, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
                     uint32_t bits[8];
                     tp_unpack(v, bits);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const uint32_t kk = tp_key(bits[i]);
-                        if ((int)(kk >> 4) == Bk && mass_of(__uint_as_float(bits[i] << 16), mp))
-                            atomicAdd(&sh.h2c[kk & 15u], 1u);
-                    }
+                    for (int i = 0; i < 8; ++i) tp_key_count(c4, tp_key(bits[i]), Bk);
                 });
+#pragma unroll
+                for (int kq = 0; kq < 16; ++kq) {  // positive-mass tokens only (mass is the key's)
+                    const uint32_t cnt = tp_warp_count(c4, kq);
+                    if (lane == 0 && cnt &&
+                        mass_of(__uint_as_float(tp_unkey((uint32_t)(Bk * 16 + kq)) << 16), mp))
+                        atomicAdd(&sh.h2c[kq], cnt);
+                }
                 __syncthreads();
                 if (rank != 0 && tid < 16 && sh.h2c[tid]) atomicAdd(&L->h2c[tid], sh.h2c[tid]);
                 cl.sync();  // S5: the 16 key counts in the leader
@@ -362,25 +422,33 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
         // ---------------------------------------------------- top-p (R5) on the top-k masses
         uint64_t Zp = Zk;
         if (use_p) {
-            // coarse select (leader, warp 0): lane l owns bins [l*128, l*128+128), heaviest first
-            if (rank == 0 && warp == 0) {
+            // coarse select (leader, all threads): thread t owns bins [4088 - 8t, 4095 - 8t],
+            // heaviest first; a block scan of the per-thread masses finds the one thread whose
+            // bins cross Theta, which walks them from the heaviest down
+            if (rank == 0) {
                 unsigned __int128 th = (unsigned __int128)P * Zk + (((unsigned __int128)1 << 32) - 1);
                 uint64_t theta = (uint64_t)(th >> 32);
                 theta = theta ? theta : 1ull;  // top_p -> 0 keeps the heaviest level (as R5)
-                const int per = TP_H1 / 32;
-                const int lo = (31 - lane) * per;  // lane 0 owns the heaviest bins
+                constexpr int PB = TP_H1 / TP_NT;
+                const int hb = TP_H1 - 1 - tid * PB;  // this thread's heaviest bin
                 uint64_t ls = 0;
-                for (int i = 0; i < per; ++i) ls += H1.get(lo + i);
-                const uint64_t incl = warp_incl_scan_u64(ls, lane);  // mass of bins >= lane's lowest
-                const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= theta);
-                const int Lh = hit ? (__ffs(hit) - 1) : 31;
-                if (lane == Lh) {
-                    uint64_t above = incl - ls;
-                    int B = lo;
-                    for (int i = per - 1; i >= 0; --i) {
-                        const uint64_t h = H1.get(lo + i);
+#pragma unroll
+                for (int i = 0; i < PB; ++i) ls += H1.get(hb - i);
+                const uint64_t wincl = warp_incl_scan_u64(ls, lane);
+                if (lane == 31) sh.wtot[warp] = wincl;
+                __syncthreads();
+                uint64_t before = 0;
+                for (int w = 0; w < warp; ++w) before += sh.wtot[w];
+                const uint64_t incl = before + wincl;  // mass of the bins >= this thread's lowest
+                const uint64_t above0 = incl - ls;
+                const bool last = tid == TP_NT - 1;
+                if ((incl >= theta && above0 < theta) || (last && incl < theta)) {
+                    uint64_t above = above0;
+                    int B = hb - (PB - 1);
+                    for (int i = 0; i < PB; ++i) {
+                        const uint64_t h = H1.get(hb - i);
                         if (above + h >= theta) {
-                            B = lo + i;
+                            B = hb - i;
                             break;
                         }
                         above += h;
@@ -390,27 +458,28 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
                     sh.bz[1] = above;
                 }
             }
-            cl.sync();  // S6: the leader's coarse select
+            PH_MARK(4); cl.sync(); PH_MARK(12);  // S6: the leader's coarse select
             const int B = L->bsel;
             // pass 3: masses of the keys inside bin B (slice -> leader)
-            tp_stream(srow, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
+            uint32_t c4[4] = {0u, 0u, 0u, 0u};
+            tp_stream(srow, sbuf, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
                 uint32_t bits[8];
                 tp_unpack(v, bits);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const uint32_t kk = tp_key(bits[i]);
-                    if ((int)(kk >> 4) == B) {
-                        const uint64_t mi = mass_of(__uint_as_float(bits[i] << 16), mp);
-                        if (mi) H2.add(kk & 15u, mi);
-                    }
-                }
+                for (int i = 0; i < 8; ++i) tp_key_count(c4, tp_key(bits[i]), B);
             });
-            __syncthreads();
-            if (rank != 0 && tid < 16) {
-                const uint64_t h = H2.get(tid);
-                if (h) H2L.add((uint32_t)tid, h);
+#pragma unroll
+            for (int kq = 0; kq < 16; ++kq) {
+                const uint32_t cnt = tp_warp_count(c4, kq);
+                if (lane == 0 && cnt) atomicAdd(&sh.h3c[kq], cnt);
             }
-            cl.sync();  // S7: the 16 key masses in the leader
+            __syncthreads();
+            if (tid < 16 && sh.h3c[tid]) {  // the slice's key masses: count x the key's mass
+                const uint64_t h =
+                    (uint64_t)sh.h3c[tid] * mass_of(__uint_as_float(tp_unkey((uint32_t)(B * 16 + tid)) << 16), mp);
+                if (h) (rank != 0 ? H2L : H2).add((uint32_t)tid, h);
+            }
+            PH_MARK(5); cl.sync(); PH_MARK(13);  // S7: the 16 key masses in the leader
             // tau = mass(k*) (>= tau_k: Theta <= Z_k); Z' from the histograms unless lower keys
             // share tau (then a filtered pass) — every CTA computes the same values
             const uint64_t need = L->bz[0];
@@ -510,12 +579,14 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL) {
                 tok = __shfl_sync(0xFFFFFFFFu, tok, L2);
                 if (lane == 0) L->cand = tok;
             }
-            cl.sync();  // S8: the sampled token in the leader
+            PH_MARK(6); cl.sync(); PH_MARK(14);  // S8: the sampled token in the leader
         }
-        if (rank == 0 && tid == 0) {
-            sh.stat[STAT_ROWS_VERIFIED] += 1ull;
-            complete_row(a, sh.stat, dsc.b, j, q, status, status == ST_DECIDED ? sh.cand : -1, Zp,
-                         (float)ldexp((double)Z, -a.S));
+        if (rank == 0 && warp == 0) {  // the completion protocol, its finalize in parallel over the warp
+            if (lane == 0) sh.stat[STAT_ROWS_VERIFIED] += 1ull;
+            int no = 0;
+            int32_t tk = -1;
+            complete_row_warp(a, sh.stat, dsc.b, j, q, status, status == ST_DECIDED ? sh.cand : -1, Zp,
+                              (float)ldexp((double)Z, -a.S), lane, no, tk);
         }
         cl.sync();  // S_end: every CTA is done reading the leader's row state before it is reset
     }

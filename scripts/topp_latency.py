@@ -35,6 +35,9 @@ for n in [int(x) for x in a.ns.split(",")]:
     rows = rng.integers(0, nbank, (a.reps, n, k + 1))
     peaks = bank_peak(1, rows.reshape(-1), V).reshape(rows.shape)
     ts = []
+    lib = bs.load()
+    ph = np.zeros(16, np.uint64)
+    timing = hasattr(lib, "bsx_phase_times") and lib.bsx_phase_times(ph.ctypes.data, 1) == 1
     for i in range(a.reps):
         ri = torch.from_numpy(rows[i]).cuda().contiguous()
         dr = torch.from_numpy(peaks[i, :, :k].astype(np.int32)).cuda().contiguous()
@@ -51,3 +54,10 @@ for n in [int(x) for x in a.ns.split(",")]:
     st = ctx.bs_stats_read()
     print(f"n={n:4d} top_p={a.top_p} top_k={a.top_k}: median {np.median(ts[2:]):8.1f} us/call, rows verified "
           f"{int(st[6]) / a.reps:.1f}, needed {int(st[7]) / a.reps:.1f}")
+    if timing:  # BS_PHASE_TIMING build: thread 0 of every CTA, cycles summed over CTAs and calls
+        lib.bsx_phase_times(ph.ctypes.data, 1)
+        names = ["claim+clear", "pass 1 max", "pass 2 masses+hist+merge", "filtered pass", "coarse select",
+                 "pass 3 keys", "epilogue/sample"]
+        tot = float(ph[:15].sum())
+        for i, nm in enumerate(names):
+            print(f"    {nm:26s} work {100 * float(ph[i]) / tot:5.1f}%  barrier after {100 * float(ph[8 + i]) / tot:5.1f}%")
