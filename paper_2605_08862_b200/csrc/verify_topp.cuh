@@ -294,7 +294,11 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
                 s += mm[i];
                 if (mm[i]) {
                     const uint32_t kb = tp_key(bits[i]) >> 4;
+#ifndef BS_TP_EXP_NOHIST  // measurement only: pass 2 without its histogram atomics
                     if (use_p) H1.add(kb, mm[i]);
+#else
+                    (void)kb;
+#endif
                     if (use_k) atomicAdd(&sh.hc[kb], 1u);
                 }
             }
