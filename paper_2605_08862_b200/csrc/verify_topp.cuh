@@ -292,24 +292,16 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 s += mm[i];
-                if (use_k && mm[i]) atomicAdd(&sh.hc[tp_key(bits[i]) >> 4], 1u);
-            }
+                if (mm[i]) {
+                    const uint32_t kb = tp_key(bits[i]) >> 4;
 #ifndef BS_TP_EXP_NOHIST  // measurement only: pass 2 without its histogram atomics
-            if (use_p) {
-                // Hist64 adds of the 8 masses with the low-word atomics issued back to back (their
-                // returned old values only decide the rare high-word adds afterwards), instead of
-                // one add's round trip after another
-                uint32_t old[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) old[i] = mm[i] ? atomicAdd(sh.h1lo + (tp_key(bits[i]) >> 4), (uint32_t)mm[i]) : 0u;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const uint32_t vl = (uint32_t)mm[i];
-                    const uint32_t h = (uint32_t)(mm[i] >> 32) + ((old[i] + vl < old[i]) ? 1u : 0u);
-                    if (h) atomicAdd(sh.h1hi + (tp_key(bits[i]) >> 4), h);
+                    if (use_p) H1.add(kb, mm[i]);
+#else
+                    (void)kb;
+#endif
+                    if (use_k) atomicAdd(&sh.hc[kb], 1u);
                 }
             }
-#endif
             const uint64_t ws = warp_sum_u51(s);
             if (lane == 0) sh.tsum[t] = ws;
         });
