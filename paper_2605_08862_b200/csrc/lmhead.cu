@@ -491,11 +491,14 @@ extern "C" bs_status bs_lm_head_logits(const void* h, const void* w, int32_t row
         ld_logits < V || (((uintptr_t)h | (uintptr_t)w) & 15u))
         return BS_ERR_INVALID;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // the CTA-pair kernel unless BS_LM_KERNEL=1 (the 1-CTA kernel, kept for measurement)
-    static const bool one_cta = [] {
+    // the 1-CTA kernel (M 128 tiles) up to 128 rows, where the pair kernel's 256-row tiles would
+    // be half padding (measured at d 3,584, V 151,936: 0.200 vs 0.233 ms at 128 rows, 86 vs 74 %
+    // of HBM on W), the CTA-pair kernel above; BS_LM_KERNEL=1 / 2 forces one (measurement)
+    static const int lm_kernel = [] {
         const char* e = getenv("BS_LM_KERNEL");
-        return e && atoi(e) == 1;
+        return e ? atoi(e) : 0;
     }();
+    const bool one_cta = lm_kernel == 1 || (lm_kernel != 2 && rows <= LM_BM);
     CUtensorMap hm, wm;
     if (!lm_map(&hm, h, rows, d, LM_BM) || !lm_map(&wm, w, V, d, one_cta ? LM_BN : LM_BN / 2)) return BS_ERR_CUDA;
     int dev = 0;
