@@ -58,6 +58,15 @@ struct TopPShared {
     int32_t bsel;              // coarse bin B
     int32_t bselk, needk;      // top-k: coarse bin of kappa, tokens still needed inside it
     uint64_t sbar;             // the staged slice's bulk copy (mbarrier)
+    // this CTA's copies of the leader's cluster totals, gathered by a few threads right after the
+    // barrier that completes them (every thread re-reading them over DSMEM, in loops that break
+    // early, cost serial remote round trips under 4,096-fold contention)
+    float xm[TP_CL];
+    uint32_t xb[TP_CL];
+    unsigned long long xz[TP_CL];   // the current slice sums (tiles_sums)
+    unsigned long long xh2[16];     // the crossing bin's key masses
+    unsigned long long xbz[2];
+    uint32_t xc[16];                // top-k: the crossing bin's key counts
     unsigned long long wtot[TP_NW];  // coarse select: per-warp mass totals (block scan)
 };
 
@@ -253,11 +262,16 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
             L->cbad[rank] = cb;
         }
         PH_MARK(1); cl.sync(); PH_MARK(9);  // S2: every slice's max in the leader
+        if (tid < TP_CL) {
+            sh.xm[tid] = L->cmax[tid];
+            sh.xb[tid] = L->cbad[tid];
+        }
+        __syncthreads();
         float m = -INFINITY;
         uint32_t bb = 0;
         for (int r = 0; r < TP_CL; ++r) {
-            m = fmaxf(m, L->cmax[r]);
-            bb |= L->cbad[r];
+            m = fmaxf(m, sh.xm[r]);
+            bb |= sh.xb[r];
         }
         uint32_t err = 0;
         if (bb) err |= DEV_BAD_LOGIT;
@@ -326,11 +340,13 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
             }
         }
         PH_MARK(2); cl.sync(); PH_MARK(10);  // S3: cluster histograms and slice sums in the leader
+        if (tid < TP_CL) sh.xz[tid] = L->zsum[tid];
+        __syncthreads();
         uint64_t Z = 0;
-        for (int r = 0; r < TP_CL; ++r) Z += L->zsum[r];  // R4: the unfiltered normaliser
+        for (int r = 0; r < TP_CL; ++r) Z += sh.xz[r];  // R4: the unfiltered normaliser
         // filtered slice tile sums (masses >= t) and their slice total into fsum[slot]
         uint64_t tiles_tau = 0;  // pass 2's tile sums keep every mass
-        const unsigned long long* tiles_sums = L->zsum;
+        const unsigned long long* tiles_sums = sh.xz;  // (this CTA's copy of the slice sums)
         int fslot = 0;
         auto filtered_tiles = [&](uint64_t t) {
             __syncthreads();  // earlier readers of sh.tsum are done
@@ -350,8 +366,10 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
             const uint64_t fs = slice_total();
             if (tid == 0) L->fsum[fslot][rank] = fs;
             PH_MARK(3); cl.sync(); PH_MARK(11);  // every slice's filtered sum in the leader
+            if (tid < TP_CL) sh.xz[tid] = L->fsum[fslot][tid];  // (readers of the previous copy are
+            __syncthreads();                                      //  past this call's first barrier)
             tiles_tau = t;
-            tiles_sums = L->fsum[fslot];
+            tiles_sums = sh.xz;
             fslot = (fslot + 1) % 3;
             uint64_t tot = 0;
             for (int r = 0; r < TP_CL; ++r) tot += tiles_sums[r];
@@ -410,10 +428,12 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
                 __syncthreads();
                 if (rank != 0 && tid < 16 && sh.h2c[tid]) atomicAdd(&L->h2c[tid], sh.h2c[tid]);
                 cl.sync();  // S5: the 16 key counts in the leader
+                if (tid < 16) sh.xc[tid] = L->h2c[tid];
+                __syncthreads();
                 const int needk = L->needk;
                 int ks = Bk * 16, cnt = 0;
                 for (int i = 15; i >= 0; --i) {
-                    cnt += (int)L->h2c[i];
+                    cnt += (int)sh.xc[i];
                     if (cnt >= needk) {
                         ks = Bk * 16 + i;
                         break;
@@ -484,13 +504,16 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
                 if (h) (rank != 0 ? H2L : H2).add((uint32_t)tid, h);
             }
             PH_MARK(5); cl.sync(); PH_MARK(13);  // S7: the 16 key masses in the leader
+            if (tid < 16) sh.xh2[tid] = H2L.get(tid);
+            if (tid == 16 || tid == 17) sh.xbz[tid - 16] = L->bz[tid - 16];
+            __syncthreads();
             // tau = mass(k*) (>= tau_k: Theta <= Z_k); Z' from the histograms unless lower keys
             // share tau (then a filtered pass) — every CTA computes the same values
-            const uint64_t need = L->bz[0];
+            const uint64_t need = sh.xbz[0];
             uint64_t above = 0;
             int ks = B * 16;
             for (int i = 15; i >= 0; --i) {
-                const uint64_t h = H2L.get(i);
+                const uint64_t h = sh.xh2[i];
                 if (above + h >= need) {
                     ks = B * 16 + i;
                     break;
@@ -498,7 +521,7 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
                 above += h;
             }
             tau = mass_of(__uint_as_float(tp_unkey((uint32_t)ks) << 16), mp);
-            Zp = L->bz[1] + above + H2L.get(ks & 15);
+            Zp = sh.xbz[1] + above + sh.xh2[ks & 15];
             const bool tie_below = ks > 0 && mass_of(__uint_as_float(tp_unkey((uint32_t)ks - 1u) << 16), mp) == tau;
             if (tie_below) Zp = filtered_tiles(tau);
         }
