@@ -67,6 +67,8 @@ struct TopPShared {
     unsigned long long xh2[16];     // the crossing bin's key masses
     unsigned long long xbz[2];
     uint32_t xc[16];                // top-k: the crossing bin's key counts
+    RowDesc xdsc;                   // the row's descriptor
+    int32_t xB;                     // the coarse bin of the top-p crossing
     unsigned long long wtot[TP_NW];  // coarse select: per-warp mass totals (block scan)
 };
 
@@ -202,7 +204,10 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
             sh.h3c[tid] = 0u;
         }
         PH_MARK(0); cl.sync(); PH_MARK(8);  // S1: the claim is published; every accumulator is clear; the last row is done
-        const RowDesc dsc = L->dsc;
+        static_assert(sizeof(RowDesc) == 48, "RowDesc layout");
+        if (tid < 12) reinterpret_cast<uint32_t*>(&sh.xdsc)[tid] = reinterpret_cast<const uint32_t*>(&L->dsc)[tid];
+        __syncthreads();
+        const RowDesc dsc = sh.xdsc;
         if (dsc.b < 0) {
             cl.sync();  // no CTA may exit while another still reads the leader's shared memory
             break;
@@ -483,7 +488,9 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
                 }
             }
             PH_MARK(4); cl.sync(); PH_MARK(12);  // S6: the leader's coarse select
-            const int B = L->bsel;
+            if (tid == 0) sh.xB = L->bsel;
+            __syncthreads();
+            const int B = sh.xB;
             // pass 3: masses of the keys inside bin B (slice -> leader)
             uint32_t c4[4] = {0u, 0u, 0u, 0u};
             tp_stream(srow, sbuf, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
