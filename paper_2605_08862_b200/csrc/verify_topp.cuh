@@ -21,10 +21,12 @@
 //   pass 4  (only when a sample is drawn, or when keys below k* share its mass) the
 //           filtered masses' 256-element tile sums, which give Z' and the inverse CDF.
 // Each row is split over an 8-CTA thread-block cluster (CTA r: elements [r SL, r SL + SL)):
-// every pass runs on the slices in parallel, the per-slice histograms and sums are added into
-// the leader CTA's shared memory over DSMEM (remote shared atomics) at cluster barriers, and
-// every CTA then reads the cluster totals from the leader, so all of them take the same
-// decisions; the sample's crossing slice rescans its crossing tile.  (One CTA per row, the
+// the slice is staged in shared memory by one bulk copy (when it fits beside the histograms at
+// two CTAs per SM; else the passes stream it from L2), every pass runs on the slices in
+// parallel, the per-slice histograms and sums are added into the leader CTA's shared memory
+// over DSMEM (remote shared atomics) at cluster barriers, and every CTA then gathers the
+// cluster totals from the leader into its own shared memory (a few threads), so all of them
+// take the same decisions; the sample's crossing slice rescans its crossing tile.  (One CTA per row, the
 // round-1 layout, made a tail step of the long-context config cost ~150 us per row.)
 #pragma once
 // (included inside namespace bs)
@@ -118,9 +120,9 @@ __device__ __forceinline__ void tp_unpack(const uint4 v, uint32_t b[8]) {
     b[4] = v.z & 0xFFFFu; b[5] = v.z >> 16; b[6] = v.w & 0xFFFFu; b[7] = v.w >> 16;
 }
 
-// Stream the row tile by tile (warp w: tiles w, w + TP_NW, ...), TP_U tiles' loads issued
-// before any is consumed: one CTA per row, so the passes are bound by how many bytes each warp
-// keeps in flight (one 16-byte load per lane at a time was ~1 KB per warp: latency-bound).
+// Stream the slice tile by tile (warp w: tiles w, w + TP_NW, ...), TP_U tiles' loads issued
+// before any is consumed (from the staged copy in shared memory, or from L2 when the slice was
+// too large to stage).
 #ifndef BS_TP_U
 #define BS_TP_U 2
 #endif
