@@ -495,12 +495,14 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
             const int B = sh.xB;
             // pass 3: masses of the keys inside bin B (slice -> leader)
             uint32_t c4[4] = {0u, 0u, 0u, 0u};
+#ifndef BS_TP_EXP_NOP3  // measurement only: no pass 3
             tp_stream(srow, sbuf, nlt, len, aligned, warp, lane, [&](int, const uint4 v) {
                 uint32_t bits[8];
                 tp_unpack(v, bits);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) tp_key_count(c4, tp_key(bits[i]), B);
             });
+#endif
 #pragma unroll
             for (int kq = 0; kq < 16; ++kq) {
                 const uint32_t cnt = tp_warp_count(c4, kq);
