@@ -42,7 +42,8 @@ struct TopPShared {
     uint32_t h1lo[TP_H1], h1hi[TP_H1];  // coarse-bin masses (Hist64); the leader's: cluster sums
     uint32_t hc[TP_H1];                 // top-k: positive-mass tokens per coarse bin
     uint32_t h2c[16];                   // top-k: positive-mass tokens per key of the crossing bin
-    uint32_t h2lo[16], h2hi[16];        // masses of the 16 keys of the crossing bin (Hist64)
+    unsigned long long h2part[TP_CL][16];  // the leader's: each slice's masses of the 16 keys of
+                                           // the crossing bin (plain remote stores, no atomics)
     uint32_t h3c[16];                   // top-p: tokens per key of the crossing bin (this slice)
     unsigned long long tsum[TP_MAXLT];  // this slice's 256-element tile sums
     unsigned long long stat[STAT_COUNT];
@@ -190,8 +191,8 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
     if (tid == 0) mbar_init(&sh.sbar, 1);
     __syncthreads();
     uint32_t sphase = 0;  // the staging barrier's phase
-    const Hist64 H1{sh.h1lo, sh.h1hi}, H2{sh.h2lo, sh.h2hi};
-    const Hist64 H1L{L->h1lo, L->h1hi}, H2L{L->h2lo, L->h2hi};
+    const Hist64 H1{sh.h1lo, sh.h1hi};
+    const Hist64 H1L{L->h1lo, L->h1hi};
 
     for (;;) {
         if (rank == 0 && tid == 0) sh.dsc = claim_row(a, rows);
@@ -201,7 +202,6 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
             sh.hc[i] = 0u;
         }
         if (tid < 16) {
-            H2.clear(tid);
             sh.h2c[tid] = 0u;
             sh.h3c[tid] = 0u;
         }
@@ -509,13 +509,21 @@ verify_topp_kernel(const VerifyArgs a, float top_p, int top_k, int SL, int stage
                 if (lane == 0 && cnt) atomicAdd(&sh.h3c[kq], cnt);
             }
             __syncthreads();
-            if (tid < 16 && sh.h3c[tid]) {  // the slice's key masses: count x the key's mass
-                const uint64_t h =
-                    (uint64_t)sh.h3c[tid] * mass_of(__uint_as_float(tp_unkey((uint32_t)(B * 16 + tid)) << 16), mp);
-                if (h) (rank != 0 ? H2L : H2).add((uint32_t)tid, h);
+            if (tid < 16) {  // the slice's key masses (count x the key's mass) into its part
+                const uint32_t cnt = sh.h3c[tid];
+                L->h2part[rank][tid] =
+                    cnt ? (uint64_t)cnt * mass_of(__uint_as_float(tp_unkey((uint32_t)(B * 16 + tid)) << 16), mp) : 0ull;
             }
-            PH_MARK(5); cl.sync(); PH_MARK(13);  // S7: the 16 key masses in the leader
-            if (tid < 16) sh.xh2[tid] = H2L.get(tid);
+            PH_MARK(5); cl.sync(); PH_MARK(13);  // S7: every slice's key masses in the leader
+            if (tid < 16) {  // the cluster's key masses: the 8 parts, loaded together
+                unsigned long long pv[TP_CL];
+#pragma unroll
+                for (int r = 0; r < TP_CL; ++r) pv[r] = L->h2part[r][tid];
+                unsigned long long tot = 0;
+#pragma unroll
+                for (int r = 0; r < TP_CL; ++r) tot += pv[r];
+                sh.xh2[tid] = tot;
+            }
             if (tid == 16 || tid == 17) sh.xbz[tid - 16] = L->bz[tid - 16];
             __syncthreads();
             // tau = mass(k*) (>= tau_k: Theta <= Z_k); Z' from the histograms unless lower keys
